@@ -1,0 +1,86 @@
+"""Nystrom-Schur preconditioner M_2 = A_G^{-1} + Z Sigma Z^T (PAPER.md:965-989,
+Alg. 2 "Construction of the Nystrom-Schur preconditioner"; eq:left_prec_mat
+PAPER.md:937-943; Alg. 1).
+
+Step by step in the paper's order, with the DESIGN.md readings:
+  1  G = Omega (n_G x (k+p) Gaussian, passed in; reading C7)
+  2-4 Y = A_GI S_I^{-1} A_IG G, computed through the equivalent border system
+     (reading C1, from Woodbury eq:S-1 PAPER.md:807-813):
+        B = K_G G;  solve S_G X = B by BF block CG to tol_inner;  Y = A_G X
+  5  Y = Q R  (Householder QR, sign-normalised so diag(R) >= 0)
+  6  C = G^T Y, symmetrised (C + C^T)/2 (reading C6)
+  7  EVD C = V1 D1 V1^T + V2 D2 V2^T, D1 = eigenvalues >= eps = eps_rel * lambda_max(C)
+  8  T = R V1 D1^{-1} V1^T R^T (symmetrised)
+  9  EVD T = W E W^T, descending
+  10 U~ = Q W(:, 1:k), Sigma = E(1:k)   (reading C5: Q, not "YW"; rank = min(r, k))
+  11 solve A_G Z = U~
+  12 M_2 r = A_G^{-1} r + Z Sigma Z^T r
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .bcg import bf_bcg
+from .schur import SchurOracle
+
+NSP_ERR_RANK_COLLAPSE = -5
+
+
+@dataclass
+class NystromResult:
+    Z: np.ndarray          # n_G x r
+    sigma: np.ndarray      # r, descending
+    U: np.ndarray          # n_G x r (orthonormal)
+    rank: int
+    bcg: dict
+    status: int
+
+
+def nystrom_from_Y(Omega: np.ndarray, Y: np.ndarray, k: int, eps_rel: float = 1e-12):
+    """Alg. 2 steps 5-10 on given (Omega, Y). Returns (U, sigma, r_C)."""
+    Q, R = np.linalg.qr(Y)                               # step 5
+    sgn = np.where(np.diag(R) < 0, -1.0, 1.0)
+    Q, R = Q * sgn, (R.T * sgn).T
+    C = Omega.T @ Y                                      # step 6
+    C = 0.5 * (C + C.T)
+    d, V = np.linalg.eigh(C)                             # step 7
+    if d.size == 0 or not d.max() > 0:
+        return Q[:, :0], np.zeros(0), 0
+    keep = d >= eps_rel * d.max()
+    V1, D1 = V[:, keep], d[keep]
+    T = R @ V1 @ np.diag(1.0 / D1) @ V1.T @ R.T          # step 8
+    T = 0.5 * (T + T.T)
+    e, W = np.linalg.eigh(T)                             # step 9
+    order = np.argsort(-e, kind="stable")
+    e, W = e[order], W[:, order]
+    r = min(int(keep.sum()), k)                          # rank = min(r, k)
+    U = Q @ W[:, :r]                                     # step 10 (reading C5)
+    return U, e[:r], int(keep.sum())
+
+
+def nystrom_schur(S: SchurOracle, Omega: np.ndarray, k: int, tol_inner: float = 0.1,
+                  maxit_inner: int = 1000, precond: str = "none", tau: float = 1e-14,
+                  eps_rel: float = 1e-12, exact_inner: bool = False) -> NystromResult:
+    d = S.d
+    B = S.k_gamma(Omega)                                  # steps 1-2 (reading C1)
+    if exact_inner:
+        X = np.linalg.solve(S.dense(), B)
+        info = {"iters": 0, "status": 0, "widths": []}
+    else:
+        M = S.solve_AG if precond == "AG" else None
+        X, info = bf_bcg(S.apply, B, tol_inner, maxit_inner, M, tau)   # step 3
+    Y = d.A_G @ X                                         # step 4
+    U, sigma, rC = nystrom_from_Y(Omega, Y, k, eps_rel)
+    status = 0 if rC > 0 else NSP_ERR_RANK_COLLAPSE
+    Z = S.solve_AG(U) if U.shape[1] else U               # step 11
+    return NystromResult(Z, sigma, U, U.shape[1], info, status)
+
+
+def apply_M2(S: SchurOracle, Z: np.ndarray, sigma: np.ndarray, r: np.ndarray) -> np.ndarray:
+    """Alg. 2 step 12: M_2 r = A_G^{-1} r + Z (Sigma (Z^T r))."""
+    out = S.solve_AG(r)
+    if Z.shape[1]:
+        out = out + Z @ (sigma * (Z.T @ r)) if r.ndim == 1 else out + Z @ (sigma[:, None] * (Z.T @ r))
+    return out

@@ -1,0 +1,102 @@
+"""Border Schur complement S_G = A_G - A_GI A_I^{-1} A_IG (PAPER.md:387-390,
+§2.3 eq:schur_complement), explicit (dense) and implicit (applied through
+per-block direct solves), plus K_G := A_GI A_I^{-1} A_IG (the border
+contribution; SURVEY.md §0 notation) and A_G^{-1} (the first-level
+preconditioner S~_1^{-1}, PAPER.md:422-428 eq:S1).
+
+A_I is block diagonal (eq:perm_A), so A_I^{-1} acts block by block:
+A_GI A_I^{-1} A_IG X = sum_j A_GI_j A_I_j^{-1} A_I_jG X.  Each A_I_j^{-1} is a
+library sparse direct solve (scipy SuperLU) used as a primitive step.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from .dbbd import DBBD
+
+
+def _lu(M: sp.csr_matrix):
+    return spla.splu(sp.csc_matrix(M), permc_spec="MMD_AT_PLUS_A",
+                     diag_pivot_thresh=0.0, options={"SymmetricMode": True})
+
+
+class SchurOracle:
+    def __init__(self, d: DBBD, blocks_needed=None):
+        self.d = d
+        self._lu = {}
+        self._lu_G = None
+        self._A_GI = None
+        self.blocks_needed = blocks_needed
+
+    # --- A_I_j^{-1} -----------------------------------------------------
+    def lu_block(self, j: int):
+        if j not in self._lu:
+            self._lu[j] = _lu(self.d.A_I[j]) if self.d.A_I[j].shape[0] > 0 else None
+        return self._lu[j]
+
+    def solve_AI_block(self, j: int, R: np.ndarray) -> np.ndarray:
+        lu = self.lu_block(j)
+        if lu is None:
+            return np.zeros_like(R)
+        return lu.solve(np.ascontiguousarray(R))
+
+    def A_GI(self, j: int) -> sp.csr_matrix:
+        if self._A_GI is None:
+            self._A_GI = [None] * self.d.K
+        if self._A_GI[j] is None:
+            self._A_GI[j] = self.d.A_IG[j].T.tocsr()
+        return self._A_GI[j]
+
+    # --- K_G X = A_GI A_I^{-1} A_IG X -------------------------------------
+    def k_gamma(self, X: np.ndarray) -> np.ndarray:
+        X = np.asarray(X, dtype=np.float64)
+        out = np.zeros((self.d.n_gamma,) + X.shape[1:])
+        for j in range(self.d.K):
+            F = self.d.A_IG[j] @ X                 # A_I_jG X   (Alg. 2 step 2)
+            if not np.any(F):
+                continue
+            U = self.solve_AI_block(j, F)          # A_I_j^{-1} F
+            out += self.A_GI(j) @ U                # A_GI_j U   (Alg. 2 step 4)
+        return out
+
+    # --- S_G X (eq:schur_complement) ---------------------------------------
+    def apply(self, X: np.ndarray) -> np.ndarray:
+        return self.d.A_G @ np.asarray(X, dtype=np.float64) - self.k_gamma(X)
+
+    def apply_rows(self, X: np.ndarray, rows: np.ndarray) -> np.ndarray:
+        """(S_G X)[rows, :] computed one output row at a time: only the blocks
+        adjacent to a sampled Gamma row contribute to it."""
+        X = np.asarray(X, dtype=np.float64)
+        rows = np.asarray(rows)
+        out = np.asarray(self.d.A_G[rows] @ X)
+        for j in range(self.d.K):
+            AGIj = self.A_GI(j)[rows]
+            if AGIj.nnz == 0:
+                continue
+            F = self.d.A_IG[j] @ X
+            U = self.solve_AI_block(j, F)
+            out -= AGIj @ U
+        return out
+
+    # --- explicit dense S_G (tiny cases only) ------------------------------
+    def dense(self) -> np.ndarray:
+        S = self.d.A_G.toarray()
+        for j in range(self.d.K):
+            if self.d.A_I[j].shape[0] == 0:
+                continue
+            AIj = self.d.A_I[j].toarray()
+            AIGj = self.d.A_IG[j].toarray()
+            S -= AIGj.T @ np.linalg.solve(AIj, AIGj)
+        return S
+
+    # --- A_G^{-1} (eq:S1) ---------------------------------------------------
+    def solve_AG(self, R: np.ndarray) -> np.ndarray:
+        if self._lu_G is None:
+            self._lu_G = _lu(self.d.A_G)
+        return self._lu_G.solve(np.ascontiguousarray(R, dtype=np.float64))
+
+    # --- A_I^{-1} on a full interior vector (block by block) ---------------
+    def solve_AI(self, r_I: list) -> list:
+        return [self.solve_AI_block(j, r_I[j]) for j in range(self.d.K)]

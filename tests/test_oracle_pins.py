@@ -1,0 +1,384 @@
+"""Pins of the CPU oracle against things other than itself (closed forms,
+brute-force elimination, exact-arithmetic termination, exactness).  CPU only.
+
+Each test names the passage (PAPER.md line / SURVEY.md §8(c) pin table) that
+fixes the expected value.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle as O
+from oracle.bcg import NSP_OK, NSP_ERR_STAGNATION
+from oracle.nystrom import apply_M2, nystrom_from_Y
+from nsp_inputs import philox
+from nsp_inputs import problems as P
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------------------
+# inputs
+# ---------------------------------------------------------------------------
+
+def test_philox_known_answers():
+    """Random123 KAT vectors (tests/golden/philox4x32_10_kat.txt)."""
+    for line in open(os.path.join(GOLDEN, "philox4x32_10_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        w = [int(x, 16) for x in line.split()]
+        out = philox.philox4x32_10(np.array([w[:4]], dtype=np.uint32), (w[4], w[5]))[0]
+        assert [int(x) for x in out] == w[6:10]
+
+
+def test_gaussian_moments_and_determinism():
+    g = philox.gaussian(0, 0, 200_000)
+    assert abs(g.mean()) < 4 / math.sqrt(g.size) * 1.5
+    assert abs(g.var() - 1) < 0.02
+    assert np.array_equal(g[:1000], philox.gaussian(0, 0, 1000))
+    assert not np.array_equal(g[:1000], philox.gaussian(1, 0, 1000))
+
+
+@pytest.mark.parametrize("dims,coef", [((13, 9), None), ((12, 10), [1.0, 1e-3]), ((6, 5, 4), None)])
+def test_laplacian_closed_form_spectrum(dims, coef):
+    """north_star: eigenvalues sum_d c_d 4 sin^2(pi k_d / (2(m_d+1)))."""
+    A = P.laplacian(dims, coef).to_scipy().toarray()
+    assert np.array_equal(A, A.T)
+    coef = coef or [1.0] * len(dims)
+    grids = np.meshgrid(*[c * 4 * np.sin(np.pi * np.arange(1, m + 1) / (2 * (m + 1))) ** 2
+                          for m, c in zip(dims, coef)], indexing="ij")
+    lam = np.sort(sum(grids).ravel())
+    assert np.max(np.abs(np.linalg.eigvalsh(A) - lam)) < 1e-12 * lam.max()
+
+
+def test_cfg1_partition_sizes():
+    """BASELINE.json configs[0] n_G = 127; C11 blocks 1024/992/992/961 (tests/golden/cfg_sizes.txt)."""
+    for line in open(os.path.join(GOLDEN, "cfg_sizes.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, n, nnz, ng, K, sizes = line.split()
+        pr = P.make(name)
+        assert pr.n == int(n) and pr.A.nnz == int(nnz) and pr.n_gamma == int(ng) and pr.K == int(K)
+        assert list(np.bincount(pr.part[pr.part >= 0])) == [int(x) for x in sizes.split(",")]
+
+
+def test_separator_property_bruteforce():
+    """no entry couples two different blocks (checked entry by entry)."""
+    for name in ["cfg1", "cfg3s", "cfg4s"]:
+        pr = P.make(name)
+        A = pr.A
+        for i in range(0, A.n, 7):
+            for q in range(A.rowptr[i], A.rowptr[i + 1]):
+                j = A.colidx[q]
+                bi, bj = pr.part[i], pr.part[j]
+                assert bi < 0 or bj < 0 or bi == bj
+    # and dbbd rejects a violation
+    A = P.laplacian((4, 4)).to_scipy()
+    part = np.zeros(16, dtype=np.int32)
+    part[1] = 1
+    with pytest.raises(ValueError, match="separator property"):
+        O.dbbd(A, part, 2)
+
+
+# ---------------------------------------------------------------------------
+# S_G
+# ---------------------------------------------------------------------------
+
+def _single_separator(dims, axis, c):
+    """Box with one separator plane at index c along `axis` (reading: SURVEY.md §8(c) pin table)."""
+    pr_A = P.laplacian(dims)
+    idx = np.indices(dims)[axis].ravel()
+    part = np.where(idx < c, 0, np.where(idx > c, 1, -1)).astype(np.int32)
+    return pr_A, part
+
+
+def _closed_form_modes(dims, axis, c):
+    m = dims[axis]
+    w1, w2 = c, m - c - 1
+    plane = [dims[a] for a in range(len(dims)) if a != axis]
+    js = np.meshgrid(*[np.arange(1, p + 1) for p in plane], indexing="ij")
+    js = [j.ravel() for j in js]
+    mu = sum(4 * np.sin(np.pi * j / (2 * (p + 1))) ** 2 for j, p in zip(js, plane))
+    theta = np.arccosh(1 + mu / 2)
+    f = lambda w: np.sinh(w * theta) / np.sinh((w + 1) * theta)  # noqa: E731
+    lam = 2 + mu - f(w1) - f(w2)
+    # eigenvectors: tensor DST-I modes on the plane, Gamma nodes in ascending original index
+    coords = np.meshgrid(*[np.arange(1, p + 1) for p in plane], indexing="ij")
+    coords = [x.ravel() for x in coords]
+    V = np.ones((coords[0].size, js[0].size))
+    for x, j, p in zip(coords, js, plane):
+        V *= np.sin(np.pi * np.outer(x, j) / (p + 1))
+    V /= np.linalg.norm(V, axis=0)
+    return lam, V, mu, f(w1) + f(w2)
+
+
+@pytest.mark.parametrize("dims,axis,c", [((9, 7), 0, 4), ((16, 12), 1, 5), ((64, 64), 0, 32), ((9, 6, 5), 0, 3)])
+def test_schur_single_separator_closed_form(dims, axis, c):
+    """S_G v_j = lambda_j v_j, lambda_j = 2 + mu_j - f(w1) - f(w2)."""
+    A, part = _single_separator(dims, axis, c)
+    d = O.dbbd(A.to_scipy(), part, 2)
+    S = O.SchurOracle(d)
+    lam, V, _, _ = _closed_form_modes(dims, axis, c)
+    SV = S.apply(V)
+    assert np.max(np.abs(SV - V * lam)) < 1e-12 * lam.max()
+
+
+@pytest.mark.parametrize("dims,axis,c", [((9, 7), 0, 4), ((9, 6, 5), 0, 3)])
+def test_related_spectra_closed_form(dims, axis, c):
+    """eig(A_G^{-1} S_G) = 1 - (f1+f2)/(2+mu) in (0,1];
+    eig(B_H) = (2+mu)(f1+f2)/(2+mu-f1-f2), B_H = A_GI S_I^{-1} A_IG."""
+    A, part = _single_separator(dims, axis, c)
+    d = O.dbbd(A.to_scipy(), part, 2)
+    S = O.SchurOracle(d)
+    lam, V, mu, ff = _closed_form_modes(dims, axis, c)
+    Sd = S.dense()
+    AG = d.A_G.toarray()
+    ev = np.sort(np.linalg.eigvals(np.linalg.solve(AG, Sd)).real)
+    assert np.allclose(ev, np.sort(1 - ff / (2 + mu)), atol=1e-12)
+    assert ev.max() <= 1 + 1e-12
+    BH = AG @ np.linalg.solve(Sd, AG) - AG          # finding 1: B_H = A_G S_G^{-1} A_G - A_G
+    eb = np.sort(np.linalg.eigvalsh(0.5 * (BH + BH.T)))
+    assert np.allclose(eb, np.sort((2 + mu) * ff / (2 + mu - ff)), rtol=1e-10, atol=1e-12)
+
+
+def _gauss_eliminate_schur(Afull, nI):
+    """Brute force: Gaussian elimination (pure Python loops) of the first nI unknowns."""
+    n = len(Afull)
+    M = [list(map(float, row)) for row in Afull]
+    for k in range(nI):
+        piv = M[k][k]
+        for i in range(k + 1, n):
+            if M[i][k] != 0.0:
+                l = M[i][k] / piv
+                for j in range(k, n):
+                    M[i][j] -= l * M[k][j]
+    return np.array([row[nI:] for row in M[nI:]])
+
+
+@pytest.mark.parametrize("dims,K", [((7, 6), 4), ((5, 4, 4), 4)])
+def test_schur_bruteforce_elimination(dims, K):
+    """north_star: dense brute-force S_G by Gaussian elimination on tiny grids."""
+    A = P.laplacian(dims).to_scipy()
+    part = P.geometric_nd(dims, K)
+    d = O.dbbd(A, part, K)
+    Ad = A.toarray()[np.ix_(d.perm, d.perm)]
+    S_bf = _gauss_eliminate_schur(Ad.tolist(), d.n - d.n_gamma)
+    S = O.SchurOracle(d)
+    assert np.max(np.abs(S.dense() - S_bf)) < 1e-13 * np.abs(S_bf).max()
+    X = np.random.default_rng(0).standard_normal((d.n_gamma, 3))
+    assert np.max(np.abs(S.apply(X) - S_bf @ X)) < 1e-13 * np.abs(S_bf @ X).max()
+    rows = np.array([0, d.n_gamma // 2, d.n_gamma - 1])
+    assert np.max(np.abs(S.apply_rows(X, rows) - (S_bf @ X)[rows])) < 1e-13 * np.abs(S_bf @ X).max()
+
+
+def test_schur_decoupled_and_arrow():
+    """A_GI = 0 -> S_G = A_G; arrow matrix -> a_GG - sum a_i^2/d_i."""
+    A = sp.csr_matrix(np.diag([2.0, 3.0, 4.0, 5.0]))
+    d = O.dbbd(A, np.array([0, 0, 1, -1], dtype=np.int32), 2)
+    assert np.allclose(O.SchurOracle(d).dense(), [[5.0]])
+    dvals = np.array([2.0, 3.0, 4.0, 5.0])
+    a = np.array([0.5, -1.0, 0.25, 0.75])
+    Ad = np.zeros((5, 5))
+    Ad[:4, :4] = np.diag(dvals)
+    Ad[4, :4] = Ad[:4, 4] = a
+    Ad[4, 4] = 10.0
+    d = O.dbbd(sp.csr_matrix(Ad), np.array([0, 1, 2, 3, -1], dtype=np.int32), 4)
+    assert abs(O.SchurOracle(d).dense()[0, 0] - (10.0 - np.sum(a * a / dvals))) < 1e-14
+
+
+def _dense_blocks(d):
+    nI = d.n - d.n_gamma
+    AI = np.zeros((nI, nI))
+    AIG = np.zeros((nI, d.n_gamma))
+    o = 0
+    for j in range(d.K):
+        m = d.blocks[j].size
+        AI[o:o + m, o:o + m] = d.A_I[j].toarray()
+        AIG[o:o + m] = d.A_IG[j].toarray()
+        o += m
+    return AI, AIG, d.A_G.toarray()
+
+
+def test_woodbury_and_reading_C1_identity():
+    """eq:S-1 and reading C1: A_G S_G^{-1} K_G Om = A_GI S_I^{-1} A_IG Om."""
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    AI, AIG, AG = _dense_blocks(d)
+    SI = AI - AIG @ np.linalg.solve(AG, AIG.T)                      # eq:SI
+    Sg = AG - AIG.T @ np.linalg.solve(AI, AIG)                       # eq:schur_complement
+    lhs = np.linalg.inv(Sg)
+    rhs = np.linalg.inv(AG) + np.linalg.solve(AG, AIG.T @ np.linalg.solve(SI, AIG @ np.linalg.inv(AG)))
+    assert np.max(np.abs(lhs - rhs)) < 1e-12 * np.abs(lhs).max()
+    Om = pr.omega()
+    Y_paper = AIG.T @ np.linalg.solve(SI, AIG @ Om)                  # Alg. 2 steps 2-4 literally
+    Y_c1 = AG @ np.linalg.solve(Sg, S.k_gamma(Om))                   # reading C1
+    assert np.max(np.abs(Y_paper - Y_c1)) < 1e-12 * np.abs(Y_paper).max()
+
+
+# ---------------------------------------------------------------------------
+# block CG
+# ---------------------------------------------------------------------------
+
+def test_bcg_exact_termination_cfg1():
+    """north_star: block CG converges within ceil(n_G/s) iterations in exact arithmetic;
+    active widths sum to n_G (30+30+30+30+7 = 127)."""
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    B = S.k_gamma(pr.omega())
+    X, info = O.bf_bcg(S.apply, B, 1e-12, 50)
+    assert info["status"] == NSP_OK
+    assert info["iters"] <= math.ceil(d.n_gamma / pr.s)
+    assert sum(info["widths"]) == d.n_gamma
+    assert np.max(np.abs(X - np.linalg.solve(S.dense(), B))) < 1e-10 * np.abs(X).max()
+    X1, info1 = O.bf_bcg(S.apply, B, pr.tol_bcg, 50)
+    assert info1["iters"] == 5 and info1["widths"] == [30, 30, 30, 30, 7]
+
+
+def test_bcg_s1_is_textbook_cg():
+    """block CG with s = 1 produces the CG iterates."""
+    pr = P.make("cfg2s")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    b = pr.omega()[:, :1]
+    for k in [3, 10, 25]:
+        Xb, ib = O.bf_bcg(S.apply, b, 0.0, k)
+        xc, ic = O.pcg(lambda v: S.apply(v[:, None])[:, 0], b[:, 0], 0.0, k)
+        assert ib["iters"] == ic["iters"] == k
+        assert np.max(np.abs(Xb[:, 0] - xc)) < 1e-10 * np.abs(xc).max()
+
+
+def test_bcg_identity_and_duplicates():
+    """S = I -> 1 iteration; two identical columns -> width drops by one."""
+    B = np.random.default_rng(1).standard_normal((40, 5))
+    X, info = O.bf_bcg(lambda V: V, B, 1e-12, 10)
+    assert info["iters"] == 1 and np.allclose(X, B)
+    Dg = np.arange(1.0, 21.0)
+    B = np.random.default_rng(2).standard_normal((20, 4))
+    B[:, 3] = B[:, 1]
+    X, info = O.bf_bcg(lambda V: Dg[:, None] * V, B, 1e-10, 30)
+    assert info["status"] == NSP_OK
+    assert info["widths"][0] == 3
+    assert np.allclose(X[:, 3], X[:, 1])
+    assert np.max(np.abs(X - B / Dg[:, None])) < 1e-9
+
+
+def test_bcg_zero_rhs_and_stagnation():
+    B = np.zeros((10, 3))
+    X, info = O.bf_bcg(lambda V: V, B, 0.1, 5)
+    assert info["status"] == NSP_OK and info["iters"] == 0
+    # directions all deflated: S = 0 on the span -> D singular is reported, not hidden
+    B = np.random.default_rng(0).standard_normal((10, 2))
+    _, info = O.bf_bcg(lambda V: 0 * V, B, 1e-3, 5)
+    assert info["status"] != NSP_OK
+
+
+def test_orth_fallback_rank():
+    rng = np.random.default_rng(3)
+    W = rng.standard_normal((50, 6))
+    W[:, 5] = W[:, 0] + W[:, 2]
+    P_, w, fb = O.orth(W)
+    assert fb and w == 5
+    assert np.allclose(P_.T @ P_, np.eye(5), atol=1e-12)
+    P2, w2, fb2 = O.orth(W[:, :5])
+    assert not fb2 and w2 == 5 and np.allclose(P2.T @ P2, np.eye(5), atol=1e-12)
+
+
+def test_pcg_cg_error_bound():
+    """eq:k-th_error_cg at every step, unpreconditioned CG on S_G."""
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    Sd = S.dense()
+    ev = np.linalg.eigvalsh(Sd)
+    kap = ev.max() / ev.min()
+    f = pr.omega()[:, 0]
+    xs = np.linalg.solve(Sd, f)
+    _, info = O.pcg(lambda v: Sd @ v, f, 1e-12, 200, record_x=True)
+    e0 = math.sqrt(xs @ Sd @ xs)
+    rho = (math.sqrt(kap) - 1) / (math.sqrt(kap) + 1)
+    for k, x in enumerate(info["xs"], start=1):
+        e = x - xs
+        assert math.sqrt(e @ Sd @ e) <= 2 * e0 * rho ** k * (1 + 1e-8) + 1e-12
+
+
+# ---------------------------------------------------------------------------
+# Nystrom, M_2, PCG
+# ---------------------------------------------------------------------------
+
+def test_nystrom_rank1_and_exactness():
+    """SPEC.md:342/356; exact on rank <= k; rank = min(r, k)."""
+    rng = np.random.default_rng(4)
+    u = rng.standard_normal(30)
+    u /= np.linalg.norm(u)
+    Bm = np.outer(u, u)
+    Om = rng.standard_normal((30, 3))
+    U, sig, rC = nystrom_from_Y(Om, Bm @ Om, 1)
+    assert rC == 1 and abs(sig[0] - 1) < 1e-12 and abs(abs(U[:, 0] @ u) - 1) < 1e-12
+    V = np.linalg.qr(rng.standard_normal((30, 4)))[0]
+    Bm = V @ np.diag([5.0, 3.0, 2.0, 0.5]) @ V.T
+    Om = rng.standard_normal((30, 7))
+    U, sig, rC = nystrom_from_Y(Om, Bm @ Om, 7)
+    assert rC == 4 and U.shape[1] == 4
+    assert np.max(np.abs(U @ np.diag(sig) @ U.T - Bm)) < 1e-12
+
+
+def test_nystrom_exact_on_single_separator_line():
+    """north_star: exact Nystrom reconstruction when s >= rank(B_H) with an exact inner
+    solve (24-node separator line); top eigenvalues match the closed form of eig(B_H)."""
+    dims, axis, c = (13, 24), 0, 6
+    A, part = _single_separator(dims, axis, c)
+    d = O.dbbd(A.to_scipy(), part, 2)
+    S = O.SchurOracle(d)
+    nG = d.n_gamma
+    Om = philox.gaussian_block(0, 0, nG, nG)
+    res = O.nystrom_schur(S, Om, nG, exact_inner=True)
+    AG = d.A_G.toarray()
+    BH = AG @ np.linalg.solve(S.dense(), AG) - AG
+    rec = res.U @ np.diag(res.sigma) @ res.U.T
+    assert np.max(np.abs(rec - BH)) < 1e-9 * np.abs(BH).max()
+    _, _, mu, ff = _closed_form_modes(dims, axis, c)
+    lam_bh = np.sort((2 + mu) * ff / (2 + mu - ff))[::-1]
+    assert np.allclose(res.sigma[:5], lam_bh[:5], rtol=1e-9)
+
+
+def test_m2_exact_gives_one_pcg_iteration_and_Z0():
+    """eq:S-1: with k = n_G and an exact inner solve, M_2 = S_G^{-1} -> PCG converges in 1
+    iteration; with Z = 0, M_2 = A_G^{-1}."""
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    Om = philox.gaussian_block(0, 0, d.n_gamma, d.n_gamma)
+    res = O.nystrom_schur(S, Om, d.n_gamma, exact_inner=True)
+    M = lambda r: apply_M2(S, res.Z, res.sigma, r)  # noqa: E731
+    Sd = S.dense()
+    assert np.max(np.abs(M(np.eye(d.n_gamma)) @ Sd - np.eye(d.n_gamma))) < 1e-9
+    f = pr.omega()[:, 0]
+    _, info = O.pcg(S.apply, f, 1e-8, 10, M)
+    assert info["iters"] == 1
+    r = pr.omega()[:, 1]
+    assert np.allclose(apply_M2(S, np.zeros((d.n_gamma, 0)), np.zeros(0), r), np.linalg.solve(d.A_G.toarray(), r))
+
+
+def test_full_solve_matches_dense_direct():
+    """solve_full_system vs a dense direct solve."""
+    pr = P.make("cfg1")
+    A = pr.A.to_scipy()
+    d = O.dbbd(A, pr.part, pr.K)
+    S = O.SchurOracle(d)
+    xs = pr.xstar()
+    b = A @ xs
+    res = O.nystrom_schur(S, pr.omega(), pr.rank, pr.tol_bcg)
+    M = lambda r: apply_M2(S, res.Z, res.sigma, r)  # noqa: E731
+    x, info = O.solve_full_system(S, b, 1e-12, 500, M)
+    xd = np.linalg.solve(A.toarray(), b)
+    assert info["status"] == 0
+    assert np.linalg.norm(x - xd) / np.linalg.norm(xd) < 1e-10
+    # M_2 is symmetric (SPEC.md:463 probe)
+    rng = np.random.default_rng(5)
+    u, v = rng.standard_normal(d.n_gamma), rng.standard_normal(d.n_gamma)
+    assert abs(u @ M(v) - v @ M(u)) < 1e-12 * abs(u @ M(v))
