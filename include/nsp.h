@@ -1,0 +1,154 @@
+/* nsp.h - C ABI of the B200-native Nystrom-Schur block-CG hot path
+ * (arXiv 2101.12164, "Nystrom-Schur two-level preconditioner").
+ *
+ * Problem (§1 eq:linear_system): A x = b, A sparse SPD, permuted
+ * to doubly bordered block diagonal (DBBD) form by a caller-supplied partition
+ * (§2.3 eq:perm_A):
+ *     P^T A P = [[A_I, A_IG], [A_GI, A_G]],   A_I = diag(A_I_0, ..., A_I_{K-1}).
+ * Border Schur complement (eq:schur_complement):
+ *     S_G = A_G - sum_j A_GI_j A_I_j^{-1} A_I_jG.
+ * Nystrom-Schur preconditioner M_2 = A_G^{-1} + Z Sigma Z^T (PAPER.md:937-943
+ * eq:left_prec_mat, Alg. 2).
+ *
+ * Conventions (all entry points):
+ *  - Host inputs (nsp_csr arrays, part) are copied by nsp_setup; the caller may
+ *    free them on return.
+ *  - Blocks X, Y, B, Omega are DEVICE pointers owned by the caller, on
+ *    opts.device, fp64, ROW-MAJOR with leading dimension s, n_gamma_local rows,
+ *    Gamma rows ordered as nsp_gamma_index() reports (single rank: ascending
+ *    original node id, reading C10).
+ *  - All work is enqueued on opts.stream (a cudaStream_t, may be NULL = legacy
+ *    default stream).  nsp_schur_apply / nsp_kgamma_apply are asynchronous; the
+ *    solvers synchronise the stream once per iteration (a small status read)
+ *    and at exit.
+ *  - ws: optional caller-owned device workspace of nsp_workspace_bytes(s)
+ *    bytes; NULL makes the context allocate (and keep) its own.
+ *  - Errors: every call returns an nsp_status; on a negative status
+ *    nsp_last_error(ctx) holds a one-line message.  No CPU fallback exists: if
+ *    the CUDA device or kernels are unavailable the calls fail with NSP_ERR_CUDA.
+ */
+#ifndef NSP_H
+#define NSP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NSP_OK = 0,
+  NSP_NOT_CONVERGED = 1,        /* maxit reached; not an error */
+  NSP_ERR_ARG = -1,             /* invalid argument / malformed CSR / partition */
+  NSP_ERR_NOT_SPD = -2,         /* Cholesky pivot <= 0 in A_I_j or A_G */
+  NSP_ERR_INDEFINITE = -3,      /* block CG: chol(P^T S P) failed; PCG: p^T S p <= 0 */
+  NSP_ERR_STAGNATION = -4,      /* all search directions deflated before convergence */
+  NSP_ERR_RANK_COLLAPSE = -5,   /* Nystrom: no eigenvalue of C >= eps (M_2 -> A_G^{-1}) */
+  NSP_ERR_NUMERICAL = -6,       /* non-finite values */
+  NSP_ERR_STATE = -7,           /* call order (e.g. pcg with M_2 before nsp_nystrom) */
+  NSP_ERR_CUDA = -8,
+  NSP_ERR_NCCL = -9,
+  NSP_ERR_OOM = -10
+} nsp_status;
+
+typedef struct nsp_ctx nsp_ctx;
+
+/* Sparse SPD matrix, full symmetric storage, HOST arrays.  rowptr int64[n+1],
+ * colidx int32[nnz] strictly increasing within each row, val fp64[nnz]. */
+typedef struct {
+  int64_t n;
+  const int64_t* rowptr;
+  const int32_t* colidx;
+  const double* val;
+} nsp_csr;
+
+typedef struct {
+  int device;            /* CUDA device ordinal */
+  void* stream;          /* cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) */
+  int nranks, rank;      /* multi-GPU: ranks own contiguous ranges of block ids */
+  const void* nccl_id;   /* 128-byte ncclUniqueId shared by all ranks; NULL if nranks == 1 */
+  int bcg_precond;       /* block-CG preconditioner: 0 = none (M = I), 1 = A_G^{-1} (reading C2) */
+  int factor_gamma;      /* 1 = factor A_G in nsp_setup (needed by M_2, bcg_precond=1, pcg) */
+  double orth_tau;       /* rank-revealing threshold tau of orth() (reading C3), default 1e-14 */
+  double nys_eps_rel;    /* Nystrom eigenvalue split eps = nys_eps_rel * lambda_max(C) (reading C6), 1e-12 */
+  size_t scratch_bytes;  /* device scratch budget for the setup factorisation; 0 = auto */
+  int verbose;
+} nsp_opts;
+
+/* Solver / setup report; caller-owned.  hist / widths are optional caller
+ * buffers (NULL or cap 0 = not recorded). */
+typedef struct {
+  int iters;             /* S_G applications inside the loop (reading C4) */
+  int converged;
+  int status;
+  double relres;         /* final max_j ||R_j|| / ||B_j||  (block CG) or ||r||/||f|| (PCG) */
+  double* hist;  int hist_cap;     /* relres per iteration (index 0 = initial) */
+  int* widths;   int widths_cap;   /* active direction-block width per iteration */
+  int bad_block;                   /* NOT_SPD: block id (-1 = A_G) */
+  long long bad_pivot;             /* NOT_SPD: original node id of the failing pivot */
+  int rank;                        /* Nystrom: rank of the approximation (min(r, k)) */
+  int fallbacks;                   /* block CG: eigen-fallback orthonormalisations */
+  double t_ms[8];                  /* setup: [0] host analysis, [1] H2D, [2] GPU factor, [3] A_G factor */
+} nsp_report;
+
+void nsp_default_opts(nsp_opts* o);
+
+/* nsp_setup: validate A and part (NSP_ERR_ARG names the offending entry:
+ * unsorted / out-of-range colidx, asymmetry, part outside {-1} U [0,K),
+ * separator property violation (i, j, b_i, b_j)); build the DBBD permutation
+ * (blocks 0..K-1 in ascending original index, then Gamma ascending; PAPER.md
+ * eq:perm_A); order each block interior-first / boundary-layer-last; copy to
+ * the device and run the GPU numeric factorisation of every A_I_j in one
+ * launch per batch ("factorized cheaply in parallel"), plus
+ * A_G (eq:cholesky PAPER.md:443-446) when opts.factor_gamma.  rep may be NULL;
+ * on NSP_ERR_NOT_SPD it receives bad_block / bad_pivot. */
+nsp_status nsp_setup(const nsp_csr* A, const int32_t* part, int K, const nsp_opts* opts,
+                     nsp_ctx** out, nsp_report* rep);
+
+nsp_status nsp_dims(const nsp_ctx* ctx, int64_t* n, int64_t* n_gamma, int64_t* n_gamma_local,
+                    int* K_local);
+/* orig_index: host int64[n_gamma_local]; local Gamma row -> original node id. */
+nsp_status nsp_gamma_index(const nsp_ctx* ctx, int64_t* orig_index);
+nsp_status nsp_workspace_bytes(const nsp_ctx* ctx, int s, size_t* bytes);
+/* factor statistics: host int64[8] = {n_I, n_boundary_layer, L22 entries streamed per apply,
+ * factor tiles, nnz(A_G), nnz(A_GI), max b_j, A_G bandwidth} */
+nsp_status nsp_stats(const nsp_ctx* ctx, int64_t* stats8);
+
+/* Y = S_G X (eq:schur_complement), X, Y device n_gamma_local x s row-major; X != Y.
+ * Steps: W = A_IG X (boundary-layer rows), V = L_j^{-1} W, U = L_j^{-T} V for all
+ * blocks in one launch, Y = A_G X - A_GI U (north_star (a), (b)). */
+nsp_status nsp_schur_apply(nsp_ctx* ctx, const double* X, double* Y, int s, void* ws);
+/* Y = K_G X = A_GI A_I^{-1} A_IG X (the border contribution; Alg. 2 steps 2-4 via reading C1). */
+nsp_status nsp_kgamma_apply(nsp_ctx* ctx, const double* X, double* Y, int s, void* ws);
+
+/* Breakdown-free block CG on S_G X = B (reading C3/C4),
+ * X0 = 0, stop when max_j ||R_j||/||B_j|| <= tol.  Returns NSP_OK,
+ * NSP_NOT_CONVERGED, NSP_ERR_INDEFINITE, NSP_ERR_STAGNATION or NSP_ERR_NUMERICAL. */
+nsp_status nsp_block_cg(nsp_ctx* ctx, const double* B, double* X, int s, double tol, int maxit,
+                        void* ws, nsp_report* rep);
+
+/* Alg. 2 steps 1-12: B = K_G Omega; block CG to tol_inner; Y = A_G X; thin
+ * Cholesky-QR2 of Y; C = sym(Omega^T Y); EVD split at eps; T; EVD of T;
+ * U~ = Q W(:,1:k); Z = A_G^{-1} U~; keeps (Z, Sigma) in ctx for nsp_pcg.
+ * Omega: device n_gamma_local x (rank+oversample). */
+nsp_status nsp_nystrom(nsp_ctx* ctx, int rank, int oversample, const double* Omega, double tol_inner,
+                       int maxit_inner, void* ws, nsp_report* rep);
+/* sigma: host double[>= rank]; rank_out: approximation rank. */
+nsp_status nsp_nystrom_sigma(const nsp_ctx* ctx, double* sigma, int* rank_out);
+/* Y = M X for M in {0: identity, 1: A_G^{-1}, 2: M_2}; device n_gamma_local x s. */
+nsp_status nsp_precond_apply(nsp_ctx* ctx, int which, const double* X, double* Y, int s, void* ws);
+
+/* Full solve A x = b through eq:A_LDLT: f = b_G - A_GI A_I^{-1} b_I; PCG on
+ * S_G w = f (eq:Sx=b) with precond {0 none, 1 A_G^{-1} (S~_1), 2 M_2}; x_I =
+ * A_I^{-1}(b_I - A_IG w); un-permute.  b, x: device fp64[n] in ORIGINAL order. */
+nsp_status nsp_pcg(nsp_ctx* ctx, const double* b, double* x, double tol, int maxit, int precond,
+                   void* ws, nsp_report* rep);
+
+const char* nsp_last_error(const nsp_ctx* ctx);
+void nsp_destroy(nsp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSP_H */

@@ -1,0 +1,133 @@
+// Context queries, workspace management and the S_G / K_G block applies (§8(a) rows a0-a5).
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "nsp_internal.h"
+#include "nsp_solver.h"
+
+namespace nspi {
+
+int pick_cw(const nsp_ctx* c, int s) {
+  const int tiles64 = (s + 63) / 64;
+  return (s > 32 && (int64_t)c->nsub * tiles64 >= 2 * 148) ? 64 : 32;
+}
+
+int ld_pad(int s, int cw) { return ((s + cw - 1) / cw) * cw; }
+
+size_t apply_ws_bytes(const nsp_ctx* c, int s) {
+  const int cw = pick_cw(c, s);
+  return (size_t)c->wvu_rows * ld_pad(s, cw) * 8 + 256;
+}
+
+nsp_status get_ws(nsp_ctx* c, void* ws, size_t need, char** out) {
+  if (ws) {
+    *out = (char*)ws;
+    return NSP_OK;
+  }
+  if (c->ws_int_bytes < need) {
+    if (c->ws_int) cudaFree(c->ws_int);
+    c->ws_int = nullptr;
+    c->ws_int_bytes = 0;
+    NSP_CUDA_TRY(c, cudaMalloc(&c->ws_int, need));
+    c->ws_int_bytes = need;
+  }
+  *out = (char*)c->ws_int;
+  return NSP_OK;
+}
+
+// Y = S_G X (mode 1) or K_G X (mode 2); wvu: workspace of apply_ws_bytes.
+nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, int mode, double* wvu) {
+  const int cw = pick_cw(c, s);
+  const int ldw = ld_pad(s, cw);
+  // a1: W = A_IG X on the boundary-layer rows (zero padding rows / columns)
+  nspk::spmm(c->A2G, X, ldx, nullptr, 0, 0, wvu, ldw, s, 0, true, c->stream);
+  // a2 + a3: V = L22^{-1} W, U = L22^{-T} V for every block, one launch
+  nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, wvu, ldw, cw, c->stream);
+  // a4 + a5: Y = A_G X - A_GI U (fused), or Y = A_GI U
+  nspk::spmm(c->AGG2, X, ldx, wvu, ldw, c->nG, Y, ldy, s, mode, false, c->stream);
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  return NSP_OK;
+}
+
+}  // namespace nspi
+
+using namespace nspi;
+
+extern "C" {
+
+nsp_status nsp_dims(const nsp_ctx* c, int64_t* n, int64_t* n_gamma, int64_t* n_gamma_local, int* K_local) {
+  if (!c) return NSP_ERR_ARG;
+  if (n) *n = c->n;
+  if (n_gamma) *n_gamma = c->nG_global;
+  if (n_gamma_local) *n_gamma_local = c->nG;
+  if (K_local) *K_local = c->nsub;
+  return NSP_OK;
+}
+
+nsp_status nsp_gamma_index(const nsp_ctx* c, int64_t* orig) {
+  if (!c || !orig) return NSP_ERR_ARG;
+  std::memcpy(orig, c->gamma.data(), c->gamma.size() * sizeof(int64_t));
+  return NSP_OK;
+}
+
+nsp_status nsp_stats(const nsp_ctx* c, int64_t* st) {
+  if (!c || !st) return NSP_ERR_ARG;
+  int64_t l22 = 0;
+  for (const FacSub& f : c->subs) l22 += (int64_t)f.ntb * (f.ntb + 1) / 2 * NSP_TILE_ELEMS;
+  st[0] = c->n_I;
+  st[1] = c->n_bl;
+  st[2] = l22;
+  st[3] = c->band_tiles + c->dense_tiles;
+  st[4] = c->nnz_AG;
+  st[5] = c->nnz_AGI;
+  st[6] = c->max_b;
+  st[7] = c->ag_bw;
+  return NSP_OK;
+}
+
+nsp_status nsp_workspace_bytes(const nsp_ctx* c, int s, size_t* bytes) {
+  if (!c || !bytes || s <= 0) return NSP_ERR_ARG;
+  *bytes = solver_ws_bytes(c, s);
+  return NSP_OK;
+}
+
+nsp_status nsp_schur_apply(nsp_ctx* c, const double* X, double* Y, int s, void* ws) {
+  if (!c || !X || !Y || s <= 0 || s > 256) return NSP_ERR_ARG;
+  char* w;
+  nsp_status st = get_ws(c, ws, apply_ws_bytes(c, s), &w);
+  if (st != NSP_OK) return st;
+  return apply_into(c, X, s, Y, s, s, 1, (double*)w);
+}
+
+nsp_status nsp_kgamma_apply(nsp_ctx* c, const double* X, double* Y, int s, void* ws) {
+  if (!c || !X || !Y || s <= 0 || s > 256) return NSP_ERR_ARG;
+  char* w;
+  nsp_status st = get_ws(c, ws, apply_ws_bytes(c, s), &w);
+  if (st != NSP_OK) return st;
+  return apply_into(c, X, s, Y, s, s, 2, (double*)w);
+}
+
+const char* nsp_last_error(const nsp_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+void nsp_destroy(nsp_ctx* c) {
+  if (!c) return;
+  auto fr = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  fr(c->d_subs);
+  fr(c->d_band);
+  fr(c->d_dense);
+  fr(c->d_border_first);
+  for (DevCSR* m : {&c->A2G, &c->AGG2}) {
+    fr(m->rowptr);
+    fr(m->col);
+    fr(m->val);
+  }
+  fr(c->ws_int);
+  if (c->h_status) cudaFreeHost(c->h_status);
+  solver_free(c);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// fp64 tensor-pipe helpers: mma.sync m8n8k4 f64 (SASS DMMA.8x8x4 on sm_100a; tcgen05 has
+// no f64 kind, SURVEY.md §0 finding 4) and cp.async staging.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nspd {
+
+// D = A(8x4, row) * B(4x8, col) + C.  Fragment ownership (lane = 4*g + t):
+//   a = A[g][t], b = B[t][g], c = {C[g][2t], C[g][2t+1]}.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// CTA (8 warps) computes a 64 x (16*NF) product tile:
+//   acc += A(64 x K) * B(K x 16NF),
+//   A[m][k] = TA ? As[k*lda + m] : As[m*lda + k];  B[k][n] = TB ? Bs[n*ldb + k] : Bs[k*ldb + n].
+// Warp w owns rows 16*(w>>1) .. +16 (2 m-fragments) and cols 8*NF*(w&1) .. +8NF (NF n-fragments).
+// acc[i][j][e] <-> C[16*(w>>1) + 8i + g][8*NF*(w&1) + 8j + 2t + e].
+template <int NF, bool TA, bool TB>
+__device__ __forceinline__ void cta_mma(const double* __restrict__ As, int lda, const double* __restrict__ Bs,
+                                        int ldb, double (&acc)[2][NF][2], int K = 64) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int m0 = (warp >> 1) * 16, n0 = (warp & 1) * NF * 8;
+#pragma unroll 4
+  for (int k = 0; k < K; k += 4) {
+    double a[2], b[NF];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int m = m0 + i * 8 + g, kk = k + t;
+      a[i] = TA ? As[kk * lda + m] : As[m * lda + kk];
+    }
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+      const int n = n0 + j * 8 + g, kk = k + t;
+      b[j] = TB ? Bs[n * ldb + kk] : Bs[kk * ldb + n];
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+}
+
+template <int NF>
+__device__ __forceinline__ void acc_zero(double (&acc)[2][NF][2]) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+// Row / column of accumulator element (i, j, e) for the calling thread.
+template <int NF>
+__device__ __forceinline__ int acc_row(int i) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  return (warp >> 1) * 16 + i * 8 + (lane >> 2);
+}
+template <int NF>
+__device__ __forceinline__ int acc_col(int j) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  return (warp & 1) * NF * 8 + j * 8 + 2 * (lane & 3);
+}
+
+// Async copy of a rows x cols (cols multiple of 2) row-major global block (ld gld) into smem (ld sld).
+__device__ __forceinline__ void cp_block(double* s, int sld, const double* g, int64_t gld, int rows, int cols) {
+  const int chunks_per_row = cols / 2;
+  const int total = rows * chunks_per_row;
+  for (int c = threadIdx.x; c < total; c += blockDim.x) {
+    const int r = c / chunks_per_row, q = c - r * chunks_per_row;
+    cp_async16(s + r * sld + 2 * q, g + r * gld + 2 * q);
+  }
+}
+
+}  // namespace nspd

@@ -1,0 +1,103 @@
+// Internal data layout of the nsp context (DESIGN.md §"Data layout in HBM").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/nsp.h"
+
+#define NSP_TILE 64          // factor tile edge (rows = cols)
+#define NSP_TILE_ELEMS (NSP_TILE * NSP_TILE)
+
+// Per-block factor layout (one entry per local block j, and one for A_G).
+// Local ordering of block j: [I1 (band order, n1 rows, padded to nt1*64)]
+// [B = boundary layer (b rows, padded to ntb*64)].  Tiles are 64x64 row-major.
+//  band tile (I, K), 0 <= I-K <= wb, I < nt1:   band[band_off + K*(wb+1) + (I-K)]
+//  border tile (I', K), I' < ntb, K < nt1:      scratch[border_off + I'*nt1 + K]
+//  dense tile (I', J'), J' <= I' < ntb:         dense[dense_off + I'(I'+1)/2 + J']
+// Diagonal tiles hold inv(L_KK) after factorisation.
+struct FacSub {
+  int nt1, ntb, wb, pad_;
+  int64_t band_off;      // tiles
+  int64_t dense_off;     // tiles
+  int64_t border_off;    // tiles, relative to the batch scratch base (-1 if none)
+  int64_t wvu_row;       // first row of this block in the W/V/U buffer (ntb*64 rows)
+  int n1, b;             // true sizes
+  int border_first_off;  // index into border_first[] (ntb entries)
+  int status_idx;        // index into the factor status array
+};
+
+struct DevCSR {   // device CSR with int32 row pointers (nnz < 2^31 checked)
+  int64_t rows = 0, nnz = 0;
+  int32_t* rowptr = nullptr;
+  int32_t* col = nullptr;
+  double* val = nullptr;
+};
+
+struct HostCSR32 {
+  std::vector<int32_t> rowptr, col;
+  std::vector<double> val;
+};
+
+struct nsp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  nsp_opts opts{};
+  int nranks = 1, rank = 0;
+  int64_t n = 0, nG = 0;          // global n, local Gamma rows
+  int64_t nG_global = 0;
+  int K = 0, nsub = 0, blk0 = 0;  // local blocks [blk0, blk0+nsub)
+  std::string err;
+
+  std::vector<int64_t> gamma;     // local Gamma row -> original id
+  std::vector<FacSub> subs;       // host copy
+  std::vector<int64_t> sub_n;     // |block j|
+
+  // device factor storage
+  FacSub* d_subs = nullptr;
+  double* d_band = nullptr;   int64_t band_tiles = 0;
+  double* d_dense = nullptr;  int64_t dense_tiles = 0;
+  int* d_border_first = nullptr;
+  int64_t wvu_rows = 0;       // total W/V/U rows (sum ntb*64)
+  int max_ntb = 0;
+
+  // Gamma-side sparse operators
+  DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
+  DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
+
+  // statistics
+  int64_t n_I = 0, n_bl = 0, nnz_AG = 0, nnz_AGI = 0, max_b = 0, ag_bw = 0;
+
+  // internal workspace (when caller passes ws == NULL)
+  void* ws_int = nullptr; size_t ws_int_bytes = 0;
+  // small pinned host status
+  void* h_status = nullptr;
+};
+
+// kernel launchers (nsp_kernels.cu)
+namespace nspk {
+void scatter(double* base, const int64_t* idx, const double* val, int64_t cnt, cudaStream_t st);
+void set_pad_identity(double* base, const int64_t* tile_idx, const int* first_row, int cnt, cudaStream_t st);
+void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, double* scratch,
+                   const int* border_first, int* status, cudaStream_t st);
+// Y[r, c] (c < s) = sum_k val_k * X(col_k, c); mode 0: Y = A X (X ld ldx);
+// mode 1: Y = A [X ; U] with cols >= split reading U (ld ldu) at col-split;
+// mode 2: Y = -(cols >= split part only)  (K_G apply)
+// Y ld ldy; columns s..ldy-1 of Y are written with 0 when zero_pad.
+void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split,
+          double* Y, int ldy, int s, int mode, bool zero_pad, cudaStream_t st);
+void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw,
+             cudaStream_t st);
+}  // namespace nspk
+
+#define NSP_CUDA_TRY(ctx, call)                                                   \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      (ctx)->err = std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                   __FILE__ + ":" + std::to_string(__LINE__);                     \
+      return NSP_ERR_CUDA;                                                        \
+    }                                                                             \
+  } while (0)

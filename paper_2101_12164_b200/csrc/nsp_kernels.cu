@@ -1,0 +1,453 @@
+// Device kernels of the S_G apply and the setup factorisation (north_star (a), (b); §8(a) rows
+// a1-a5, s0).  fp64 throughout; dense tile products on the DMMA pipe (mma.sync f64).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nsp_dmma.cuh"
+#include "nsp_internal.h"
+
+using namespace nspd;
+
+namespace {
+
+constexpr int LDT = 68;  // smem row stride (doubles) of a 64x64 tile: conflict-free fragment loads
+
+// ---------------------------------------------------------------------------------------------
+// setup helpers
+// ---------------------------------------------------------------------------------------------
+__global__ void k_scatter(double* base, const int64_t* idx, const double* val, int64_t cnt) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < cnt) base[idx[i]] = val[i];
+}
+
+__global__ void k_pad_identity(double* base, const int64_t* tile_idx, const int* first_row, int cnt) {
+  int t = blockIdx.x;
+  if (t >= cnt) return;
+  double* T = base + tile_idx[t] * NSP_TILE_ELEMS;
+  for (int r = first_row[t] + threadIdx.x; r < NSP_TILE; r += blockDim.x) T[r * NSP_TILE + r] = 1.0;
+}
+
+// ---------------------------------------------------------------------------------------------
+// s0: right-looking tile Cholesky of one block per CTA (eq:cholesky).
+// Column tile K: potrf(L_KK) in smem -> inv(L_KK) stored in the diagonal slot; panel
+// L_IK = A_IK inv(L_KK)^T for every structurally nonzero tile below; trailing update
+// A_ab -= L_aK L_bK^T for all panel pairs a >= b.  Structural pattern: band tiles
+// (0 < I-K <= wb), border tiles (I' with border_first[I'] <= K), then the dense tail.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ double* band_tile(const FacSub& sb, double* band, int I, int K) {
+  return band + (sb.band_off + (int64_t)K * (sb.wb + 1) + (I - K)) * NSP_TILE_ELEMS;
+}
+__device__ __forceinline__ double* border_tile(const FacSub& sb, double* scratch, int Ib, int K) {
+  return scratch + (sb.border_off + (int64_t)Ib * sb.nt1 + K) * NSP_TILE_ELEMS;
+}
+__device__ __forceinline__ double* dense_tile(const FacSub& sb, double* dense, int I, int J) {
+  return dense + (sb.dense_off + (int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS;
+}
+
+__global__ void __launch_bounds__(256) k_tile_cholesky(const FacSub* __restrict__ subs, double* band,
+                                                       double* dense, double* scratch,
+                                                       const int* __restrict__ border_first, int* status) {
+  extern __shared__ double sm[];
+  double* Ds = sm;                    // diag tile / factor
+  double* Li = sm + 64 * LDT;         // inv(L_KK)
+  double* As = sm + 2 * 64 * LDT;     // panel operand a
+  double* Bs0 = sm + 3 * 64 * LDT;    // panel operand b (double buffered)
+  double* Bs1 = sm + 4 * 64 * LDT;
+  __shared__ double colv[64];
+  __shared__ int s_fail;
+  __shared__ short plist[2048];       // panel list: encoded tile refs (band: I-K in [1,wb]; border: 4096+I')
+
+  const FacSub sb = subs[blockIdx.x];
+  const int* bfirst = border_first + sb.border_first_off;
+  const int NT = sb.nt1 + sb.ntb;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_fail = 0;
+
+  for (int K = 0; K < NT; ++K) {
+    const bool dphase = K >= sb.nt1;
+    const int Kd = K - sb.nt1;
+    double* Dg = dphase ? dense_tile(sb, dense, Kd, Kd) : band_tile(sb, band, K, K);
+    // ---- load diag tile (lower part used)
+    for (int e = tid; e < 4096; e += 256) Ds[(e >> 6) * LDT + (e & 63)] = Dg[e];
+    __syncthreads();
+    // ---- unblocked Cholesky (2 barriers per column)
+    for (int c = 0; c < 64; ++c) {
+      const double d = Ds[c * LDT + c];
+      if (!(d > 0.0)) {
+        if (tid == 0) {
+          s_fail = 1;
+          status[sb.status_idx] = K * 64 + c + 1;  // 1-based local row in the padded ordering
+        }
+        break;
+      }
+      const double l = sqrt(d);
+      if (tid > c && tid < 64) colv[tid] = Ds[tid * LDT + c] / l;
+      __syncthreads();
+      for (int e = tid; e < 64 * 64; e += 256) {
+        const int r = e >> 6, q = e & 63;
+        if (q > c && r >= q) Ds[r * LDT + q] -= colv[r] * colv[q];
+      }
+      if (tid > c && tid < 64) Ds[tid * LDT + c] = colv[tid];
+      if (tid == 0) Ds[c * LDT + c] = l;
+      __syncthreads();
+    }
+    __syncthreads();
+    if (s_fail) return;
+    // ---- inverse of the lower-triangular factor: thread j < 64 solves L x = e_j (column j of inv)
+    if (tid < 64) {
+      const int j = tid;
+      for (int i = 0; i < 64; ++i) {
+        double v;
+        if (i < j) {
+          v = 0.0;
+        } else {
+          double sacc = (i == j) ? 1.0 : 0.0;
+          for (int k = j; k < i; ++k) sacc -= Ds[i * LDT + k] * Li[k * LDT + j];
+          v = sacc / Ds[i * LDT + i];
+        }
+        Li[i * LDT + j] = v;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < 4096; e += 256) Dg[e] = Li[(e >> 6) * LDT + (e & 63)];
+    // ---- panel list
+    int np = 0;
+    if (!dphase) {
+      const int imax = min(K + sb.wb, sb.nt1 - 1);
+      for (int I = K + 1; I <= imax; ++I) {
+        if (tid == 0) plist[np] = (short)(I - K);
+        ++np;
+      }
+      for (int Ib = 0; Ib < sb.ntb; ++Ib)
+        if (bfirst[Ib] <= K) {
+          if (tid == 0) plist[np] = (short)(4096 + Ib);
+          ++np;
+        }
+    } else {
+      for (int Ib = Kd + 1; Ib < sb.ntb; ++Ib) {
+        if (tid == 0) plist[np] = (short)(4096 + Ib);
+        ++np;
+      }
+    }
+    __syncthreads();
+    auto ptile = [&](int p) -> double* {
+      const int code = plist[p];
+      if (code < 4096) return band_tile(sb, band, K + code, K);
+      const int Ib = code - 4096;
+      return dphase ? dense_tile(sb, dense, Ib, Kd) : border_tile(sb, scratch, Ib, K);
+    };
+    // ---- panel solve: T <- T inv(L_KK)^T
+    for (int p = 0; p < np; ++p) {
+      double* Tg = ptile(p);
+      cp_block(As, LDT, Tg, 64, 64, 64);
+      cp_commit();
+      cp_wait<0>();
+      __syncthreads();
+      double acc[2][4][2];
+      acc_zero(acc);
+      cta_mma<4, false, true>(As, LDT, Li, LDT, acc);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = acc_row<4>(i), c = acc_col<4>(j);
+          *reinterpret_cast<double2*>(Tg + r * 64 + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+        }
+      __syncthreads();
+    }
+    __threadfence();
+    __syncthreads();
+    // ---- trailing update: dest(a, b) -= P_a P_b^T, a >= b
+    for (int a = 0; a < np; ++a) {
+      const int ca = plist[a];
+      cp_block(As, LDT, ptile(a), 64, 64, 64);
+      cp_block(Bs0, LDT, ptile(0), 64, 64, 64);
+      cp_commit();
+      for (int b = 0; b <= a; ++b) {
+        double* Bcur = (b & 1) ? Bs1 : Bs0;
+        if (b + 1 <= a) {
+          cp_block((b & 1) ? Bs0 : Bs1, LDT, ptile(b + 1), 64, 64, 64);
+          cp_commit();
+          cp_wait<1>();
+        } else {
+          cp_wait<0>();
+        }
+        __syncthreads();
+        // destination tile
+        const int cb = plist[b];
+        double* dst;
+        if (ca < 4096) {                        // band x band
+          dst = band_tile(sb, band, K + ca, K + cb);
+        } else if (!dphase && cb < 4096) {      // border x band
+          dst = border_tile(sb, scratch, ca - 4096, K + cb);
+        } else if (!dphase) {                   // border x border -> dense (S22)
+          dst = dense_tile(sb, dense, ca - 4096, cb - 4096);
+        } else {
+          dst = dense_tile(sb, dense, ca - 4096, cb - 4096);
+        }
+        double acc[2][4][2];
+        acc_zero(acc);
+        cta_mma<4, false, true>(As, LDT, Bcur, LDT, acc);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = acc_row<4>(i), c = acc_col<4>(j);
+            double2* q = reinterpret_cast<double2*>(dst + r * 64 + c);
+            double2 v = *q;
+            v.x -= acc[i][j][0];
+            v.y -= acc[i][j][1];
+            *q = v;
+          }
+        __syncthreads();
+      }
+    }
+    __threadfence();
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// a1 / a4 / a5: CSR SpMM on row-major s-wide fp64 blocks.  Warp per row; the row's column
+// indices and values are loaded once lane-parallel and broadcast by shuffle (register staging);
+// each lane owns columns lane, lane+32, ... so every X-row read is a coalesced 8s-byte segment.
+// ---------------------------------------------------------------------------------------------
+template <int NQ>
+__global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __restrict__ rp,
+                                              const int32_t* __restrict__ ci, const double* __restrict__ va,
+                                              const double* __restrict__ X, int ldx,
+                                              const double* __restrict__ U, int ldu, int64_t split,
+                                              double* __restrict__ Y, int ldy, int s, int mode, int zero_pad) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int beg = rp[row], end = rp[row + 1];
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  for (int base = beg; base < end; base += 32) {
+    const int k = base + lane;
+    const int c = k < end ? ci[k] : 0;
+    const double v = k < end ? va[k] : 0.0;
+    const int cnt = min(32, end - base);
+    for (int q = 0; q < cnt; ++q) {
+      const int64_t col = __shfl_sync(0xffffffffu, c, q);
+      double a = __shfl_sync(0xffffffffu, v, q);
+      const double* src;
+      if (mode == 0 || col < split) {
+        if (mode == 2) continue;
+        src = X + col * ldx;
+      } else {
+        src = U + (col - split) * ldu;
+        if (mode == 2) a = -a;
+      }
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq) {
+        const int cc = lane + 32 * qq;
+        if (cc < s) acc[qq] = fma(a, __ldg(src + cc), acc[qq]);
+      }
+    }
+  }
+  double* y = Y + row * ldy;
+#pragma unroll
+  for (int qq = 0; qq < NQ; ++qq) {
+    const int cc = lane + 32 * qq;
+    if (cc < s) y[cc] = acc[qq];
+    else if (zero_pad && cc < ldy) y[cc] = 0.0;
+  }
+  if (zero_pad)
+    for (int cc = 32 * NQ + lane; cc < ldy; cc += 32) y[cc] = 0.0;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a2 + a3: batched forward and backward triangular solves with the boundary-layer factor
+// L22_j of every block, all blocks (x column chunks) in one launch.  Blocked by 64-row tiles
+// ("levels"): V_I = inv(L_II) (W_I - sum_{J<I} L_IJ V_J);  U_I = inv(L_II)^T (V_I - sum_{J>I}
+// L_JI^T U_J).  In place in the W/V/U buffer.  (L_II^{-1} precomputed by the setup.)
+// ---------------------------------------------------------------------------------------------
+template <int CW>
+__global__ void __launch_bounds__(256) k_trsm_fb(const FacSub* __restrict__ subs,
+                                                 const double* __restrict__ dense, double* wvu, int ldw) {
+  constexpr int NF = CW / 16;
+  constexpr int LDV = CW + 4;
+  extern __shared__ double sm[];
+  double* Ls0 = sm;
+  double* Ls1 = sm + 64 * LDT;
+  double* Vs0 = sm + 2 * 64 * LDT;
+  double* Vs1 = Vs0 + 64 * LDV;
+  const FacSub sb = subs[blockIdx.x];
+  const int ntb = sb.ntb;
+  if (ntb == 0) return;
+  const int c0 = blockIdx.y * CW;
+  const double* T = dense + sb.dense_off * NSP_TILE_ELEMS;
+  double* Wb = wvu + sb.wvu_row * (int64_t)ldw + c0;
+  auto tile = [&](int I, int J) { return T + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS; };
+  double acc[2][NF][2];
+
+  // ------------------------- forward sweep
+  for (int I = 0; I < ntb; ++I) {
+    acc_zero(acc);
+    if (I > 0) {
+      cp_block(Ls0, LDT, tile(I, 0), 64, 64, 64);
+      cp_block(Vs0, LDV, Wb, ldw, 64, CW);
+      cp_commit();
+      for (int J = 0; J < I; ++J) {
+        double* Lc = (J & 1) ? Ls1 : Ls0;
+        double* Vc = (J & 1) ? Vs1 : Vs0;
+        if (J + 1 < I) {
+          cp_block((J & 1) ? Ls0 : Ls1, LDT, tile(I, J + 1), 64, 64, 64);
+          cp_block((J & 1) ? Vs0 : Vs1, LDV, Wb + (int64_t)(J + 1) * 64 * ldw, ldw, 64, CW);
+          cp_commit();
+          cp_wait<1>();
+        } else {
+          cp_wait<0>();
+        }
+        __syncthreads();
+        cta_mma<NF, false, false>(Lc, LDT, Vc, LDV, acc);
+        __syncthreads();
+      }
+    }
+    // residual R = W_I - acc (in Vs1), then V_I = inv(L_II) R
+    cp_block(Ls0, LDT, tile(I, I), 64, 64, 64);
+    cp_block(Vs0, LDV, Wb + (int64_t)I * 64 * ldw, ldw, 64, CW);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+        Vs1[r * LDV + c] = Vs0[r * LDV + c] - acc[i][j][0];
+        Vs1[r * LDV + c + 1] = Vs0[r * LDV + c + 1] - acc[i][j][1];
+      }
+    __syncthreads();
+    acc_zero(acc);
+    cta_mma<NF, false, false>(Ls0, LDT, Vs1, LDV, acc);
+    double* out = Wb + (int64_t)I * 64 * ldw;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+        *reinterpret_cast<double2*>(out + (int64_t)r * ldw + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    __threadfence();
+    __syncthreads();
+  }
+  // ------------------------- backward sweep
+  for (int I = ntb - 1; I >= 0; --I) {
+    acc_zero(acc);
+    if (I < ntb - 1) {
+      cp_block(Ls0, LDT, tile(I + 1, I), 64, 64, 64);
+      cp_block(Vs0, LDV, Wb + (int64_t)(I + 1) * 64 * ldw, ldw, 64, CW);
+      cp_commit();
+      int it = 0;
+      for (int J = I + 1; J < ntb; ++J, ++it) {
+        double* Lc = (it & 1) ? Ls1 : Ls0;
+        double* Vc = (it & 1) ? Vs1 : Vs0;
+        if (J + 1 < ntb) {
+          cp_block((it & 1) ? Ls0 : Ls1, LDT, tile(J + 1, I), 64, 64, 64);
+          cp_block((it & 1) ? Vs0 : Vs1, LDV, Wb + (int64_t)(J + 1) * 64 * ldw, ldw, 64, CW);
+          cp_commit();
+          cp_wait<1>();
+        } else {
+          cp_wait<0>();
+        }
+        __syncthreads();
+        cta_mma<NF, true, false>(Lc, LDT, Vc, LDV, acc);
+        __syncthreads();
+      }
+    }
+    cp_block(Ls0, LDT, tile(I, I), 64, 64, 64);
+    cp_block(Vs0, LDV, Wb + (int64_t)I * 64 * ldw, ldw, 64, CW);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+        Vs1[r * LDV + c] = Vs0[r * LDV + c] - acc[i][j][0];
+        Vs1[r * LDV + c + 1] = Vs0[r * LDV + c + 1] - acc[i][j][1];
+      }
+    __syncthreads();
+    acc_zero(acc);
+    cta_mma<NF, true, false>(Ls0, LDT, Vs1, LDV, acc);
+    double* out = Wb + (int64_t)I * 64 * ldw;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+        *reinterpret_cast<double2*>(out + (int64_t)r * ldw + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    __threadfence();
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+namespace nspk {
+
+void scatter(double* base, const int64_t* idx, const double* val, int64_t cnt, cudaStream_t st) {
+  if (cnt <= 0) return;
+  k_scatter<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(base, idx, val, cnt);
+}
+
+void set_pad_identity(double* base, const int64_t* tile_idx, const int* first_row, int cnt, cudaStream_t st) {
+  if (cnt <= 0) return;
+  k_pad_identity<<<cnt, 64, 0, st>>>(base, tile_idx, first_row, cnt);
+}
+
+void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, double* scratch,
+                   const int* border_first, int* status, cudaStream_t st) {
+  if (nsub <= 0) return;
+  const size_t smem = 5 * 64 * LDT * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tile_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_tile_cholesky<<<nsub, 256, smem, st>>>(subs, band, dense, scratch, border_first, status);
+}
+
+void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split, double* Y,
+          int ldy, int s, int mode, bool zero_pad, cudaStream_t st) {
+  if (A.rows <= 0) return;
+  const unsigned blocks = (unsigned)((A.rows * 32 + 255) / 256);
+  if (s <= 32)
+    k_spmm<1><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad);
+  else if (s <= 64)
+    k_spmm<2><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad);
+  else if (s <= 128)
+    k_spmm<4><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad);
+  else
+    k_spmm<8><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad);
+}
+
+void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw, cudaStream_t st) {
+  if (nsub <= 0) return;
+  dim3 grid(nsub, ldw / cw);
+  if (cw == 64) {
+    const size_t smem = (2 * 64 * LDT + 2 * 64 * (64 + 4)) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_trsm_fb<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_trsm_fb<64><<<grid, 256, smem, st>>>(subs, dense, wvu, ldw);
+  } else {
+    const size_t smem = (2 * 64 * LDT + 2 * 64 * (32 + 4)) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_trsm_fb<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_trsm_fb<32><<<grid, 256, smem, st>>>(subs, dense, wvu, ldw);
+  }
+}
+
+}  // namespace nspk

@@ -1,0 +1,643 @@
+// nsp_setup: host analysis (validation, DBBD permutation, per-block ordering, tile layout), the
+// host->device copy, and the GPU numeric factorisation (§8(a) row s0).
+//
+// DBBD (PAPER.md:369-378 eq:perm_A): blocks 0..K-1 in ascending original index, then Gamma in
+// ascending original index (reading C10).  Inside block j the interior is split into
+//   I1 = nodes with no Gamma neighbour (ordered natural or RCM, whichever has the smaller
+//        bandwidth) and
+//   B  = boundary layer (nodes with a Gamma neighbour), ordered last.
+// Since A_I_jG is nonzero only on the B rows, L_j^{-1} A_I_jG X is nonzero only on the B rows
+// and equals L22^{-1} W_B, where L22 = chol(A_BB - A_B1 A_11^{-1} A_1B) is the trailing block of
+// the Cholesky factor of A_I_j in this ordering; A_GI_j reads only the B rows of
+// L_j^{-T} L_j^{-1} (.) which equal L22^{-T} L22^{-1} W_B.  The hot path therefore streams only
+// the dense trailing factor L22.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include <omp.h>
+
+#include "nsp_internal.h"
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+// Reverse Cuthill-McKee on a local graph (adjacency in CSR), George-Liu pseudo-peripheral root.
+std::vector<int> rcm_order(int n, const std::vector<int>& rp, const std::vector<int>& ci) {
+  std::vector<int> order;
+  order.reserve(n);
+  std::vector<char> vis(n, 0);
+  std::vector<int> deg(n);
+  for (int i = 0; i < n; ++i) deg[i] = rp[i + 1] - rp[i];
+  std::vector<int> level(n, -1), q;
+  auto bfs_levels = [&](int root, int& ecc, int& last_min) {
+    // BFS restricted to unvisited component; returns eccentricity and min-degree node of last level
+    q.clear();
+    q.push_back(root);
+    level[root] = 0;
+    size_t h = 0;
+    while (h < q.size()) {
+      int v = q[h++];
+      for (int k = rp[v]; k < rp[v + 1]; ++k) {
+        int u = ci[k];
+        if (!vis[u] && level[u] < 0) {
+          level[u] = level[v] + 1;
+          q.push_back(u);
+        }
+      }
+    }
+    ecc = level[q.back()];
+    last_min = q.back();
+    for (int v : q)
+      if (level[v] == ecc && deg[v] < deg[last_min]) last_min = v;
+    for (int v : q) level[v] = -1;
+  };
+  for (int start = 0; start < n; ++start) {
+    if (vis[start]) continue;
+    // min degree node of this component
+    int root = start;
+    {
+      int e, lm;
+      bfs_levels(start, e, lm);
+      for (int v : q)
+        if (deg[v] < deg[root]) root = v;
+    }
+    int ecc, lm;
+    bfs_levels(root, ecc, lm);
+    for (int it = 0; it < 8; ++it) {
+      int ecc2, lm2;
+      bfs_levels(lm, ecc2, lm2);
+      if (ecc2 > ecc) {
+        root = lm;
+        ecc = ecc2;
+        lm = lm2;
+      } else {
+        break;
+      }
+    }
+    // Cuthill-McKee BFS from root, neighbours by ascending degree
+    size_t h = order.size();
+    order.push_back(root);
+    vis[root] = 1;
+    std::vector<int> nb;
+    while (h < order.size()) {
+      int v = order[h++];
+      nb.clear();
+      for (int k = rp[v]; k < rp[v + 1]; ++k)
+        if (!vis[ci[k]]) nb.push_back(ci[k]);
+      std::sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] != deg[b] ? deg[a] < deg[b] : a < b; });
+      for (int u : nb)
+        if (!vis[u]) {
+          vis[u] = 1;
+          order.push_back(u);
+        }
+    }
+  }
+  std::reverse(order.begin(), order.end());
+  return order;
+}
+
+int bandwidth(int n, const std::vector<int>& rp, const std::vector<int>& ci, const std::vector<int>& pos) {
+  int bw = 0;
+  for (int v = 0; v < n; ++v)
+    for (int k = rp[v]; k < rp[v + 1]; ++k) bw = std::max(bw, std::abs(pos[v] - pos[ci[k]]));
+  return bw;
+}
+
+struct SubHost {
+  int j = 0;                       // global block id
+  std::vector<int64_t> nodes;      // original ids in the new local order: I1 (n1) then B (b)
+  int n1 = 0, b = 0, bw = 0, wb = 0, nt1 = 0, ntb = 0;
+  bool rcm = false;
+  std::vector<int> border_first;   // per B tile: first column tile with a nonzero
+  // entries (lower triangle) in tile storage, indices relative to the region base
+  std::vector<int64_t> band_idx, dense_idx, border_idx;
+  std::vector<double> band_val, dense_val, border_val;
+};
+
+template <class T>
+nsp_status upload(nsp_ctx* c, T** dptr, const std::vector<T>& h) {
+  *dptr = nullptr;
+  if (h.empty()) return NSP_OK;
+  NSP_CUDA_TRY(c, cudaMalloc((void**)dptr, h.size() * sizeof(T)));
+  NSP_CUDA_TRY(c, cudaMemcpy(*dptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return NSP_OK;
+}
+
+nsp_status upload_csr(nsp_ctx* c, DevCSR& d, const HostCSR32& h) {
+  d.rows = (int64_t)h.rowptr.size() - 1;
+  d.nnz = (int64_t)h.col.size();
+  nsp_status st;
+  if ((st = upload(c, &d.rowptr, h.rowptr)) != NSP_OK) return st;
+  if ((st = upload(c, &d.col, h.col)) != NSP_OK) return st;
+  if ((st = upload(c, &d.val, h.val)) != NSP_OK) return st;
+  return NSP_OK;
+}
+
+}  // namespace
+
+extern "C" void nsp_default_opts(nsp_opts* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->device = 0;
+  o->stream = nullptr;
+  o->nranks = 1;
+  o->rank = 0;
+  o->nccl_id = nullptr;
+  o->bcg_precond = 0;
+  o->factor_gamma = 0;
+  o->orth_tau = 1e-14;
+  o->nys_eps_rel = 1e-12;
+  o->scratch_bytes = 0;
+  o->verbose = 0;
+}
+
+static nsp_status fail(nsp_ctx* c, nsp_status st, const std::string& msg) {
+  c->err = msg;
+  return st;
+}
+
+nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K, nsp_report* rep);
+
+extern "C" nsp_status nsp_setup(const nsp_csr* A, const int32_t* part, int K, const nsp_opts* opts,
+                                nsp_ctx** out, nsp_report* rep) {
+  if (!out) return NSP_ERR_ARG;
+  *out = nullptr;
+  nsp_ctx* c = new nsp_ctx();
+  if (opts) c->opts = *opts;
+  else nsp_default_opts(&c->opts);
+  *out = c;
+  if (!A || !part || K <= 0) return fail(c, NSP_ERR_ARG, "nsp_setup: null A/part or K <= 0");
+  c->device = c->opts.device;
+  c->stream = (cudaStream_t)c->opts.stream;
+  c->nranks = c->opts.nranks > 0 ? c->opts.nranks : 1;
+  c->rank = c->opts.rank;
+  if (c->nranks != 1) return fail(c, NSP_ERR_ARG, "nsp_setup: multi-rank setup not built in this version");
+  NSP_CUDA_TRY(c, cudaSetDevice(c->device));
+  return nsp_setup_impl(c, A, part, K, rep);
+}
+
+nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K, nsp_report* rep) {
+  auto t0 = Clock::now();
+  const int64_t n = A->n;
+  const int64_t* rp = A->rowptr;
+  const int32_t* ci = A->colidx;
+  const double* va = A->val;
+  if (n <= 0 || !rp || !ci || !va) return fail(c, NSP_ERR_ARG, "nsp_setup: empty or null CSR");
+  if (rp[0] != 0) return fail(c, NSP_ERR_ARG, "nsp_setup: rowptr[0] != 0");
+  c->n = n;
+  c->K = K;
+  // ---------------- validation
+  std::string verr;
+  int64_t bad_row = -1;
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t i = 0; i < n; ++i) {
+    if (bad_row >= 0) continue;
+    bool ok = rp[i + 1] >= rp[i];
+    for (int64_t q = rp[i]; ok && q < rp[i + 1]; ++q) {
+      if (ci[q] < 0 || ci[q] >= n) ok = false;
+      else if (q > rp[i] && ci[q] <= ci[q - 1]) ok = false;
+    }
+    if (!ok) {
+#pragma omp critical
+      if (bad_row < 0 || i < bad_row) bad_row = i;
+    }
+  }
+  if (bad_row >= 0)
+    return fail(c, NSP_ERR_ARG, "nsp_setup: row " + std::to_string(bad_row) +
+                                    " has out-of-range or unsorted column indices");
+  for (int64_t i = 0; i < n; ++i)
+    if (part[i] < -1 || part[i] >= K)
+      return fail(c, NSP_ERR_ARG, "nsp_setup: part[" + std::to_string(i) + "] = " + std::to_string(part[i]) +
+                                      " not in {-1} U [0, K)");
+  int64_t asym = -1, asym_j = -1, sep_i = -1, sep_j = -1;
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+      const int64_t j = ci[q];
+      // symmetric value check via binary search in row j
+      const int32_t* b = ci + rp[j];
+      const int32_t* e = ci + rp[j + 1];
+      const int32_t* f = std::lower_bound(b, e, (int32_t)i);
+      if (f == e || *f != i || va[rp[j] + (f - b)] != va[q]) {
+#pragma omp critical
+        if (asym < 0) {
+          asym = i;
+          asym_j = j;
+        }
+      }
+      if (va[q] != 0.0 && part[i] >= 0 && part[j] >= 0 && part[i] != part[j]) {
+#pragma omp critical
+        if (sep_i < 0) {
+          sep_i = i;
+          sep_j = j;
+        }
+      }
+    }
+  }
+  if (asym >= 0)
+    return fail(c, NSP_ERR_ARG, "nsp_setup: matrix not symmetric at (" + std::to_string(asym) + ", " +
+                                    std::to_string(asym_j) + ")");
+  if (sep_i >= 0)
+    return fail(c, NSP_ERR_ARG, "nsp_setup: separator property violated at entry (" + std::to_string(sep_i) +
+                                    ", " + std::to_string(sep_j) + ") between blocks " +
+                                    std::to_string(part[sep_i]) + " and " + std::to_string(part[sep_j]));
+
+  // ---------------- DBBD index maps
+  std::vector<int32_t> gpos(n, -1), lpos(n, -1), bidx(n, -1);
+  std::vector<std::vector<int64_t>> blocks(K);
+  for (int64_t i = 0; i < n; ++i) {
+    if (part[i] < 0) {
+      gpos[i] = (int32_t)c->gamma.size();
+      c->gamma.push_back(i);
+    } else {
+      blocks[part[i]].push_back(i);
+    }
+  }
+  c->nG = (int64_t)c->gamma.size();
+  c->nG_global = c->nG;
+  c->blk0 = 0;
+  c->nsub = K;
+  std::vector<SubHost> sh(K);
+  c->sub_n.resize(K);
+  for (int j = 0; j < K; ++j) c->sub_n[j] = (int64_t)blocks[j].size();
+
+  // ---------------- per-block ordering (I1 band order, B last)
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int j = 0; j < K; ++j) {
+    SubHost& S = sh[j];
+    S.j = j;
+    const auto& nodes = blocks[j];
+    const int nj = (int)nodes.size();
+    std::vector<int64_t> I1, Bn;
+    for (int64_t v : nodes) {
+      bool bl = false;
+      for (int64_t q = rp[v]; q < rp[v + 1]; ++q)
+        if (part[ci[q]] < 0 && va[q] != 0.0) {
+          bl = true;
+          break;
+        }
+      (bl ? Bn : I1).push_back(v);
+    }
+    S.n1 = (int)I1.size();
+    S.b = (int)Bn.size();
+    // local index of I1 nodes (natural order)
+    for (int k = 0; k < S.n1; ++k) lpos[I1[k]] = k;
+    std::vector<int> arp(S.n1 + 1, 0), aci;
+    for (int k = 0; k < S.n1; ++k) {
+      const int64_t v = I1[k];
+      for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
+        const int64_t u = ci[q];
+        if (u != v && part[u] == j && lpos[u] >= 0 && va[q] != 0.0) {
+          // u in I1? (B nodes have lpos -1 at this point)
+          aci.push_back(lpos[u]);
+        }
+      }
+      arp[k + 1] = (int)aci.size();
+    }
+    std::vector<int> pos_nat(S.n1);
+    std::iota(pos_nat.begin(), pos_nat.end(), 0);
+    const int bw_nat = bandwidth(S.n1, arp, aci, pos_nat);
+    std::vector<int> ord = rcm_order(S.n1, arp, aci);
+    std::vector<int> pos_rcm(S.n1);
+    for (int k = 0; k < S.n1; ++k) pos_rcm[ord[k]] = k;
+    const int bw_rcm = bandwidth(S.n1, arp, aci, pos_rcm);
+    S.rcm = bw_rcm < bw_nat;
+    const std::vector<int>& pos = S.rcm ? pos_rcm : pos_nat;
+    S.bw = S.rcm ? bw_rcm : bw_nat;
+    S.nodes.assign(nj, -1);
+    for (int k = 0; k < S.n1; ++k) S.nodes[pos[k]] = I1[k];
+    for (int k = 0; k < S.n1; ++k) lpos[S.nodes[k]] = k;  // final I1 positions
+    // B order: by first I1 coupling position, then original id
+    std::vector<std::pair<int, int64_t>> bkey(S.b);
+    for (int k = 0; k < S.b; ++k) {
+      const int64_t v = Bn[k];
+      int first = S.n1;
+      for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
+        const int64_t u = ci[q];
+        if (part[u] == j && lpos[u] >= 0 && va[q] != 0.0) first = std::min(first, lpos[u]);
+      }
+      bkey[k] = {first, v};
+    }
+    std::sort(bkey.begin(), bkey.end());
+    S.nt1 = (S.n1 + NSP_TILE - 1) / NSP_TILE;
+    S.ntb = (S.b + NSP_TILE - 1) / NSP_TILE;
+    S.wb = S.nt1 > 0 ? std::min(S.nt1 - 1, (S.bw + NSP_TILE - 1) / NSP_TILE) : 0;
+    S.border_first.assign(S.ntb, S.nt1);
+    for (int k = 0; k < S.b; ++k) {
+      S.nodes[S.n1 + k] = bkey[k].second;
+      lpos[bkey[k].second] = S.nt1 * NSP_TILE + k;  // padded local index
+      bidx[bkey[k].second] = k;
+      const int ft = bkey[k].first < S.n1 ? bkey[k].first / NSP_TILE : S.nt1;
+      S.border_first[k / NSP_TILE] = std::min(S.border_first[k / NSP_TILE], ft);
+    }
+  }
+
+  // ---------------- offsets, scratch batches
+  c->subs.resize(K);
+  int64_t band_tiles = 0, dense_tiles = 0, wvu_rows = 0;
+  std::vector<int> border_first_all;
+  c->max_ntb = 0;
+  c->n_I = 0;
+  c->n_bl = 0;
+  c->max_b = 0;
+  for (int j = 0; j < K; ++j) {
+    const SubHost& S = sh[j];
+    FacSub& F = c->subs[j];
+    F.nt1 = S.nt1;
+    F.ntb = S.ntb;
+    F.wb = S.wb;
+    F.pad_ = 0;
+    F.n1 = S.n1;
+    F.b = S.b;
+    F.band_off = band_tiles;
+    F.dense_off = dense_tiles;
+    F.wvu_row = wvu_rows;
+    F.border_first_off = (int)border_first_all.size();
+    F.status_idx = j;
+    F.border_off = -1;
+    border_first_all.insert(border_first_all.end(), S.border_first.begin(), S.border_first.end());
+    band_tiles += (int64_t)S.nt1 * (S.wb + 1);
+    dense_tiles += (int64_t)S.ntb * (S.ntb + 1) / 2;
+    wvu_rows += (int64_t)S.ntb * NSP_TILE;
+    c->max_ntb = std::max(c->max_ntb, S.ntb);
+    c->n_I += S.n1 + S.b;
+    c->n_bl += S.b;
+    c->max_b = std::max<int64_t>(c->max_b, S.b);
+  }
+  c->band_tiles = band_tiles;
+  c->dense_tiles = dense_tiles;
+  c->wvu_rows = wvu_rows;
+  size_t free_b = 0, total_b = 0;
+  NSP_CUDA_TRY(c, cudaMemGetInfo(&free_b, &total_b));
+  const size_t persist = (size_t)(band_tiles + dense_tiles) * NSP_TILE_ELEMS * 8;
+  if (persist > free_b) return fail(c, NSP_ERR_OOM, "nsp_setup: factor storage exceeds free device memory");
+  size_t budget = c->opts.scratch_bytes;
+  if (budget == 0) budget = (size_t)((free_b - persist) * 0.5);
+  std::vector<std::pair<int, int>> batches;  // [j0, j1)
+  {
+    int j0 = 0;
+    int64_t acc = 0;
+    for (int j = 0; j < K; ++j) {
+      const int64_t t = (int64_t)sh[j].ntb * sh[j].nt1;
+      if (j > j0 && (size_t)(acc + t) * NSP_TILE_ELEMS * 8 > budget) {
+        batches.push_back({j0, j});
+        j0 = j;
+        acc = 0;
+      }
+      c->subs[j].border_off = acc;
+      acc += t;
+    }
+    batches.push_back({j0, K});
+  }
+  int64_t max_batch_tiles = 0;
+  for (auto& bt : batches) {
+    int64_t acc = 0;
+    for (int j = bt.first; j < bt.second; ++j) acc += (int64_t)sh[j].ntb * sh[j].nt1;
+    max_batch_tiles = std::max(max_batch_tiles, acc);
+  }
+  if ((size_t)max_batch_tiles * NSP_TILE_ELEMS * 8 > free_b - persist)
+    return fail(c, NSP_ERR_OOM, "nsp_setup: a single block's border scratch exceeds free device memory");
+
+  // ---------------- tile entries (lower triangle of A_I_j in the new ordering)
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int j = 0; j < K; ++j) {
+    SubHost& S = sh[j];
+    const FacSub& F = c->subs[j];
+    const int nj = (int)S.nodes.size();
+    const int off1 = S.nt1 * NSP_TILE;
+    for (int k = 0; k < nj; ++k) {
+      const int64_t v = S.nodes[k];
+      const int li = lpos[v];
+      for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
+        const int64_t u = ci[q];
+        if (part[u] != j) continue;
+        const int lj = lpos[u];
+        if (lj > li) continue;
+        const double a = va[q];
+        if (li < off1) {  // I1 x I1 -> band
+          const int I = li / NSP_TILE, Kt = lj / NSP_TILE;
+          S.band_idx.push_back((F.band_off + (int64_t)Kt * (S.wb + 1) + (I - Kt)) * NSP_TILE_ELEMS +
+                               (li % NSP_TILE) * NSP_TILE + lj % NSP_TILE);
+          S.band_val.push_back(a);
+        } else if (lj < off1) {  // B x I1 -> border scratch (batch relative)
+          const int bi = li - off1;
+          const int Ib = bi / NSP_TILE, Kt = lj / NSP_TILE;
+          S.border_idx.push_back((F.border_off + (int64_t)Ib * S.nt1 + Kt) * NSP_TILE_ELEMS +
+                                 (bi % NSP_TILE) * NSP_TILE + lj % NSP_TILE);
+          S.border_val.push_back(a);
+        } else {  // B x B -> dense
+          const int bi = li - off1, bj = lj - off1;
+          const int Ib = bi / NSP_TILE, Jb = bj / NSP_TILE;
+          S.dense_idx.push_back((F.dense_off + (int64_t)Ib * (Ib + 1) / 2 + Jb) * NSP_TILE_ELEMS +
+                                (bi % NSP_TILE) * NSP_TILE + bj % NSP_TILE);
+          S.dense_val.push_back(a);
+        }
+      }
+    }
+  }
+
+  // ---------------- Gamma-side CSRs
+  HostCSR32 A2G, AGG2;
+  A2G.rowptr.assign(wvu_rows + 1, 0);
+  {
+    // rows of W/V/U: block j, border k -> row wvu_row + k; padded rows empty
+    std::vector<int64_t> rowsrc(wvu_rows, -1);
+    for (int j = 0; j < K; ++j)
+      for (int k = 0; k < sh[j].b; ++k) rowsrc[c->subs[j].wvu_row + k] = sh[j].nodes[sh[j].n1 + k];
+    std::vector<std::pair<int32_t, double>> ent;
+    for (int64_t r = 0; r < wvu_rows; ++r) {
+      const int64_t v = rowsrc[r];
+      if (v >= 0) {
+        ent.clear();
+        for (int64_t q = rp[v]; q < rp[v + 1]; ++q)
+          if (part[ci[q]] < 0 && va[q] != 0.0) ent.push_back({gpos[ci[q]], va[q]});
+        std::sort(ent.begin(), ent.end());
+        for (auto& e : ent) {
+          A2G.col.push_back(e.first);
+          A2G.val.push_back(e.second);
+        }
+      }
+      A2G.rowptr[r + 1] = (int32_t)A2G.col.size();
+    }
+  }
+  AGG2.rowptr.assign(c->nG + 1, 0);
+  c->nnz_AG = 0;
+  c->nnz_AGI = 0;
+  {
+    std::vector<std::pair<int64_t, double>> ent;
+    for (int64_t g = 0; g < c->nG; ++g) {
+      const int64_t v = c->gamma[g];
+      ent.clear();
+      for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
+        const int64_t u = ci[q];
+        if (va[q] == 0.0 && u != v) continue;
+        if (part[u] < 0) {
+          ent.push_back({gpos[u], va[q]});
+          c->nnz_AG++;
+        } else {
+          ent.push_back({c->nG + c->subs[part[u]].wvu_row + bidx[u], -va[q]});
+          c->nnz_AGI++;
+        }
+      }
+      std::sort(ent.begin(), ent.end());
+      for (auto& e : ent) {
+        if (e.first > INT32_MAX) return fail(c, NSP_ERR_ARG, "nsp_setup: W/V/U index exceeds int32");
+        AGG2.col.push_back((int32_t)e.first);
+        AGG2.val.push_back(e.second);
+      }
+      AGG2.rowptr[g + 1] = (int32_t)AGG2.col.size();
+    }
+  }
+  const double t_host = ms_since(t0);
+
+  // ---------------- device upload
+  auto t1 = Clock::now();
+  nsp_status st;
+  if ((st = upload_csr(c, c->A2G, A2G)) != NSP_OK) return st;
+  if ((st = upload_csr(c, c->AGG2, AGG2)) != NSP_OK) return st;
+  if ((st = upload(c, &c->d_subs, c->subs)) != NSP_OK) return st;
+  std::vector<int> bf = border_first_all;
+  if (bf.empty()) bf.push_back(0);
+  if ((st = upload(c, &c->d_border_first, bf)) != NSP_OK) return st;
+  if (band_tiles > 0) {
+    NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_band, (size_t)band_tiles * NSP_TILE_ELEMS * 8));
+    NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_band, 0, (size_t)band_tiles * NSP_TILE_ELEMS * 8, c->stream));
+  }
+  if (dense_tiles > 0) {
+    NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_dense, (size_t)dense_tiles * NSP_TILE_ELEMS * 8));
+    NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_dense, 0, (size_t)dense_tiles * NSP_TILE_ELEMS * 8, c->stream));
+  }
+  // entries: upload in chunks through one staging pair
+  const int64_t CH = 1 << 24;
+  int64_t* d_idx = nullptr;
+  double* d_val = nullptr;
+  NSP_CUDA_TRY(c, cudaMalloc((void**)&d_idx, CH * 8));
+  NSP_CUDA_TRY(c, cudaMalloc((void**)&d_val, CH * 8));
+  std::vector<int64_t> hidx;
+  std::vector<double> hval;
+  auto flush_entries = [&](double* base) -> nsp_status {
+    for (int64_t s0 = 0; s0 < (int64_t)hidx.size(); s0 += CH) {
+      const int64_t cnt = std::min<int64_t>(CH, (int64_t)hidx.size() - s0);
+      NSP_CUDA_TRY(c, cudaMemcpyAsync(d_idx, hidx.data() + s0, cnt * 8, cudaMemcpyHostToDevice, c->stream));
+      NSP_CUDA_TRY(c, cudaMemcpyAsync(d_val, hval.data() + s0, cnt * 8, cudaMemcpyHostToDevice, c->stream));
+      nspk::scatter(base, d_idx, d_val, cnt, c->stream);
+      NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+    hidx.clear();
+    hval.clear();
+    return NSP_OK;
+  };
+  for (int j = 0; j < K; ++j) {
+    hidx.insert(hidx.end(), sh[j].band_idx.begin(), sh[j].band_idx.end());
+    hval.insert(hval.end(), sh[j].band_val.begin(), sh[j].band_val.end());
+    std::vector<int64_t>().swap(sh[j].band_idx);
+    std::vector<double>().swap(sh[j].band_val);
+  }
+  if ((st = flush_entries(c->d_band)) != NSP_OK) return st;
+  for (int j = 0; j < K; ++j) {
+    hidx.insert(hidx.end(), sh[j].dense_idx.begin(), sh[j].dense_idx.end());
+    hval.insert(hval.end(), sh[j].dense_val.begin(), sh[j].dense_val.end());
+    std::vector<int64_t>().swap(sh[j].dense_idx);
+    std::vector<double>().swap(sh[j].dense_val);
+  }
+  if ((st = flush_entries(c->d_dense)) != NSP_OK) return st;
+  // identity on padded diagonal rows
+  {
+    std::vector<int64_t> bt, dt;
+    std::vector<int> bfr, dfr;
+    for (int j = 0; j < K; ++j) {
+      const SubHost& S = sh[j];
+      if (S.nt1 > 0 && S.n1 % NSP_TILE) {
+        bt.push_back(c->subs[j].band_off + (int64_t)(S.nt1 - 1) * (S.wb + 1));
+        bfr.push_back(S.n1 % NSP_TILE);
+      }
+      if (S.ntb > 0 && S.b % NSP_TILE) {
+        const int I = S.ntb - 1;
+        dt.push_back(c->subs[j].dense_off + (int64_t)I * (I + 1) / 2 + I);
+        dfr.push_back(S.b % NSP_TILE);
+      }
+    }
+    int64_t* d_t = nullptr;
+    int* d_f = nullptr;
+    if (!bt.empty()) {
+      if ((st = upload(c, &d_t, bt)) != NSP_OK) return st;
+      if ((st = upload(c, &d_f, bfr)) != NSP_OK) return st;
+      nspk::set_pad_identity(c->d_band, d_t, d_f, (int)bt.size(), c->stream);
+      NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      cudaFree(d_t);
+      cudaFree(d_f);
+    }
+    if (!dt.empty()) {
+      if ((st = upload(c, &d_t, dt)) != NSP_OK) return st;
+      if ((st = upload(c, &d_f, dfr)) != NSP_OK) return st;
+      nspk::set_pad_identity(c->d_dense, d_t, d_f, (int)dt.size(), c->stream);
+      NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      cudaFree(d_t);
+      cudaFree(d_f);
+    }
+  }
+  const double t_h2d = ms_since(t1);
+
+  // ---------------- GPU factorisation, batch by batch
+  auto t2 = Clock::now();
+  double* d_scratch = nullptr;
+  if (max_batch_tiles > 0)
+    NSP_CUDA_TRY(c, cudaMalloc((void**)&d_scratch, (size_t)max_batch_tiles * NSP_TILE_ELEMS * 8));
+  int* d_status = nullptr;
+  NSP_CUDA_TRY(c, cudaMalloc((void**)&d_status, K * sizeof(int)));
+  NSP_CUDA_TRY(c, cudaMemsetAsync(d_status, 0, K * sizeof(int), c->stream));
+  for (auto& bt : batches) {
+    int64_t tiles = 0;
+    for (int j = bt.first; j < bt.second; ++j) {
+      tiles += (int64_t)sh[j].ntb * sh[j].nt1;
+      hidx.insert(hidx.end(), sh[j].border_idx.begin(), sh[j].border_idx.end());
+      hval.insert(hval.end(), sh[j].border_val.begin(), sh[j].border_val.end());
+      std::vector<int64_t>().swap(sh[j].border_idx);
+      std::vector<double>().swap(sh[j].border_val);
+    }
+    if (tiles > 0) NSP_CUDA_TRY(c, cudaMemsetAsync(d_scratch, 0, (size_t)tiles * NSP_TILE_ELEMS * 8, c->stream));
+    if ((st = flush_entries(d_scratch)) != NSP_OK) return st;
+    nspk::tile_cholesky(c->d_subs + bt.first, bt.second - bt.first, c->d_band, c->d_dense, d_scratch,
+                        c->d_border_first, d_status, c->stream);
+    NSP_CUDA_TRY(c, cudaGetLastError());
+  }
+  NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  std::vector<int> hstat(K);
+  NSP_CUDA_TRY(c, cudaMemcpy(hstat.data(), d_status, K * sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(d_status);
+  cudaFree(d_scratch);
+  cudaFree(d_idx);
+  cudaFree(d_val);
+  const double t_fac = ms_since(t2);
+  for (int j = 0; j < K; ++j)
+    if (hstat[j] != 0) {
+      const int lrow = hstat[j] - 1;
+      const SubHost& S = sh[j];
+      int64_t orig = -1;
+      if (lrow < S.n1) orig = S.nodes[lrow];
+      else if (lrow >= S.nt1 * NSP_TILE && lrow - S.nt1 * NSP_TILE < S.b) orig = S.nodes[S.n1 + lrow - S.nt1 * NSP_TILE];
+      if (rep) {
+        rep->bad_block = j;
+        rep->bad_pivot = orig;
+        rep->status = NSP_ERR_NOT_SPD;
+      }
+      return fail(c, NSP_ERR_NOT_SPD, "nsp_setup: A_I_" + std::to_string(j) + " not SPD (pivot at node " +
+                                          std::to_string(orig) + ")");
+    }
+  if (rep) {
+    rep->status = NSP_OK;
+    rep->t_ms[0] = t_host;
+    rep->t_ms[1] = t_h2d;
+    rep->t_ms[2] = t_fac;
+  }
+  NSP_CUDA_TRY(c, cudaMallocHost(&c->h_status, 4096));
+  return NSP_OK;
+}

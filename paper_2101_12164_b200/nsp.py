@@ -1,0 +1,237 @@
+"""Thin ctypes binding of include/nsp.h (same names, argument marshalling only).
+
+Device blocks are torch CUDA float64 tensors (PyTorch supplies device memory and
+streams - plumbing, not compute); every step of the path runs in libnsp.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnsp.so")
+
+NSP_STATUS = {0: "NSP_OK", 1: "NSP_NOT_CONVERGED", -1: "NSP_ERR_ARG", -2: "NSP_ERR_NOT_SPD",
+              -3: "NSP_ERR_INDEFINITE", -4: "NSP_ERR_STAGNATION", -5: "NSP_ERR_RANK_COLLAPSE",
+              -6: "NSP_ERR_NUMERICAL", -7: "NSP_ERR_STATE", -8: "NSP_ERR_CUDA", -9: "NSP_ERR_NCCL",
+              -10: "NSP_ERR_OOM"}
+
+EXPORTED = ["nsp_default_opts", "nsp_setup", "nsp_dims", "nsp_gamma_index", "nsp_workspace_bytes",
+            "nsp_stats", "nsp_schur_apply", "nsp_kgamma_apply", "nsp_block_cg", "nsp_nystrom",
+            "nsp_nystrom_sigma", "nsp_precond_apply", "nsp_pcg", "nsp_last_error", "nsp_destroy"]
+
+
+class nsp_csr(C.Structure):
+    _fields_ = [("n", C.c_int64), ("rowptr", C.c_void_p), ("colidx", C.c_void_p), ("val", C.c_void_p)]
+
+
+class nsp_opts(C.Structure):
+    _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("nranks", C.c_int), ("rank", C.c_int),
+                ("nccl_id", C.c_void_p), ("bcg_precond", C.c_int), ("factor_gamma", C.c_int),
+                ("orth_tau", C.c_double), ("nys_eps_rel", C.c_double), ("scratch_bytes", C.c_size_t),
+                ("verbose", C.c_int)]
+
+
+class nsp_report(C.Structure):
+    _fields_ = [("iters", C.c_int), ("converged", C.c_int), ("status", C.c_int), ("relres", C.c_double),
+                ("hist", C.c_void_p), ("hist_cap", C.c_int), ("widths", C.c_void_p), ("widths_cap", C.c_int),
+                ("bad_block", C.c_int), ("bad_pivot", C.c_longlong), ("rank", C.c_int), ("fallbacks", C.c_int),
+                ("t_ms", C.c_double * 8)]
+
+
+class NspError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{NSP_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libnsp.so; raises if it is missing (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} not built: run `python -m paper_2101_12164_b200.build`")
+    lib = C.CDLL(path)
+    P, I64, I, D = C.c_void_p, C.c_int64, C.c_int, C.c_double
+    lib.nsp_default_opts.argtypes = [P]
+    lib.nsp_default_opts.restype = None
+    lib.nsp_setup.argtypes = [P, P, I, P, P, P]
+    lib.nsp_dims.argtypes = [P, P, P, P, P]
+    lib.nsp_gamma_index.argtypes = [P, P]
+    lib.nsp_workspace_bytes.argtypes = [P, I, P]
+    lib.nsp_stats.argtypes = [P, P]
+    lib.nsp_schur_apply.argtypes = [P, P, P, I, P]
+    lib.nsp_kgamma_apply.argtypes = [P, P, P, I, P]
+    lib.nsp_block_cg.argtypes = [P, P, P, I, D, I, P, P]
+    lib.nsp_nystrom.argtypes = [P, I, I, P, D, I, P, P]
+    lib.nsp_nystrom_sigma.argtypes = [P, P, P]
+    lib.nsp_precond_apply.argtypes = [P, I, P, P, I, P]
+    lib.nsp_pcg.argtypes = [P, P, P, D, I, I, P, P]
+    lib.nsp_last_error.argtypes = [P]
+    lib.nsp_last_error.restype = C.c_char_p
+    lib.nsp_destroy.argtypes = [P]
+    lib.nsp_destroy.restype = None
+    for f in EXPORTED:
+        if f not in ("nsp_default_opts", "nsp_last_error", "nsp_destroy"):
+            getattr(lib, f).restype = C.c_int
+    _lib = lib
+    return lib
+
+
+def _ptr(t) -> int:
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise TypeError("expected a contiguous CUDA float64 tensor")
+    return t.data_ptr()
+
+
+class Report(dict):
+    pass
+
+
+def _report(rep: nsp_report, hist, widths) -> Report:
+    r = Report(iters=rep.iters, converged=bool(rep.converged), status=rep.status, relres=rep.relres,
+               bad_block=rep.bad_block, bad_pivot=rep.bad_pivot, rank=rep.rank, fallbacks=rep.fallbacks,
+               t_ms=list(rep.t_ms))
+    n = rep.iters + 1
+    if hist is not None:
+        r["hist"] = list(hist[: min(n, len(hist))])
+    if widths is not None:
+        r["widths"] = list(widths[: min(rep.iters, len(widths))])
+    return r
+
+
+class Context:
+    """nsp_ctx owner.  A: (rowptr int64, colidx int32, val float64) host arrays."""
+
+    def __init__(self, rowptr, colidx, val, part, K, device=0, stream=None, bcg_precond=0,
+                 factor_gamma=False, orth_tau=1e-14, nys_eps_rel=1e-12, nranks=1, rank=0,
+                 nccl_id: bytes | None = None, scratch_bytes=0):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("CUDA device required (no CPU fallback)")
+        self.lib = load_library()
+        self._rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+        self._colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+        self._val = np.ascontiguousarray(val, dtype=np.float64)
+        self._part = np.ascontiguousarray(part, dtype=np.int32)
+        csr = nsp_csr(self._rowptr.size - 1, self._rowptr.ctypes.data, self._colidx.ctypes.data,
+                      self._val.ctypes.data)
+        o = nsp_opts()
+        self.lib.nsp_default_opts(C.byref(o))
+        o.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+        o.stream = stream
+        o.nranks, o.rank = nranks, rank
+        self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        o.nccl_id = C.addressof(self._nccl_id) if self._nccl_id is not None else None
+        o.bcg_precond = bcg_precond
+        o.factor_gamma = int(bool(factor_gamma or bcg_precond))
+        o.orth_tau, o.nys_eps_rel, o.scratch_bytes = orth_tau, nys_eps_rel, scratch_bytes
+        self.opts = o
+        self.ctx = C.c_void_p()
+        rep = nsp_report()
+        st = self.lib.nsp_setup(C.byref(csr), self._part.ctypes.data, K, C.byref(o), C.byref(self.ctx),
+                                C.byref(rep))
+        self.setup_report = _report(rep, None, None)
+        if st != 0:
+            msg = self.lib.nsp_last_error(self.ctx).decode()
+            self.close()
+            raise NspError(st, msg)
+        n, ng, ngl, kl = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        self._check(self.lib.nsp_dims(self.ctx, C.byref(n), C.byref(ng), C.byref(ngl), C.byref(kl)))
+        self.n, self.n_gamma, self.n_gamma_local, self.K_local = n.value, ng.value, ngl.value, kl.value
+
+    def _check(self, st):
+        if st < 0:
+            raise NspError(st, self.lib.nsp_last_error(self.ctx).decode())
+        return st
+
+    def gamma_index(self) -> np.ndarray:
+        out = np.empty(self.n_gamma_local, dtype=np.int64)
+        self._check(self.lib.nsp_gamma_index(self.ctx, out.ctypes.data))
+        return out
+
+    def stats(self) -> dict:
+        out = np.zeros(8, dtype=np.int64)
+        self._check(self.lib.nsp_stats(self.ctx, out.ctypes.data))
+        keys = ["n_I", "n_boundary_layer", "l22_entries", "factor_tiles", "nnz_AG", "nnz_AGI", "max_b", "ag_bw"]
+        return dict(zip(keys, [int(x) for x in out]))
+
+    def workspace_bytes(self, s: int) -> int:
+        b = C.c_size_t()
+        self._check(self.lib.nsp_workspace_bytes(self.ctx, s, C.byref(b)))
+        return b.value
+
+    def schur_apply(self, X, Y, ws=None):
+        s = X.shape[1]
+        self._check(self.lib.nsp_schur_apply(self.ctx, _ptr(X), _ptr(Y), s, None if ws is None else ws.data_ptr()))
+
+    def kgamma_apply(self, X, Y, ws=None):
+        s = X.shape[1]
+        self._check(self.lib.nsp_kgamma_apply(self.ctx, _ptr(X), _ptr(Y), s, None if ws is None else ws.data_ptr()))
+
+    def block_cg(self, B, X, tol, maxit, ws=None, hist_cap=None):
+        s = B.shape[1]
+        cap = maxit + 1 if hist_cap is None else hist_cap
+        hist = (C.c_double * cap)()
+        widths = (C.c_int * cap)()
+        rep = nsp_report()
+        rep.hist, rep.hist_cap = C.addressof(hist), cap
+        rep.widths, rep.widths_cap = C.addressof(widths), cap
+        st = self.lib.nsp_block_cg(self.ctx, _ptr(B), _ptr(X), s, tol, maxit,
+                                   None if ws is None else ws.data_ptr(), C.byref(rep))
+        self._check(st)
+        return _report(rep, hist, widths)
+
+    def nystrom(self, rank, oversample, Omega, tol_inner, maxit_inner, ws=None):
+        cap = maxit_inner + 1
+        hist = (C.c_double * cap)()
+        widths = (C.c_int * cap)()
+        rep = nsp_report()
+        rep.hist, rep.hist_cap = C.addressof(hist), cap
+        rep.widths, rep.widths_cap = C.addressof(widths), cap
+        st = self.lib.nsp_nystrom(self.ctx, rank, oversample, _ptr(Omega), tol_inner, maxit_inner,
+                                  None if ws is None else ws.data_ptr(), C.byref(rep))
+        self._check(st)
+        r = _report(rep, hist, widths)
+        r["status_code"] = st
+        return r
+
+    def nystrom_sigma(self, cap=4096) -> np.ndarray:
+        out = np.zeros(cap)
+        r = C.c_int()
+        self._check(self.lib.nsp_nystrom_sigma(self.ctx, out.ctypes.data, C.byref(r)))
+        return out[: r.value]
+
+    def precond_apply(self, which, X, Y, ws=None):
+        self._check(self.lib.nsp_precond_apply(self.ctx, which, _ptr(X), _ptr(Y), X.shape[1],
+                                               None if ws is None else ws.data_ptr()))
+
+    def pcg(self, b, x, tol, maxit, precond=2, ws=None):
+        cap = maxit + 1
+        hist = (C.c_double * cap)()
+        rep = nsp_report()
+        rep.hist, rep.hist_cap = C.addressof(hist), cap
+        st = self.lib.nsp_pcg(self.ctx, _ptr(b), _ptr(x), tol, maxit, precond,
+                              None if ws is None else ws.data_ptr(), C.byref(rep))
+        self._check(st)
+        return _report(rep, hist, None)
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None and self.ctx.value:
+            self.lib.nsp_destroy(self.ctx)
+        self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
