@@ -45,7 +45,7 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   // a2 + a3: V = L22^{-1} W, U = L22^{-T} V for every block, one launch
   nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, wvu, ldw, cw, c->stream);
   // a4 + a5: Y = A_G X - A_GI U (fused), or Y = A_GI U
-  nspk::spmm(c->AGG2, X, ldx, wvu, ldw, c->nG, Y, ldy, s, mode, false, c->stream);
+  nspk::spmm(c->AGG2, X, ldx, wvu, ldw, c->nG, Y, ldy, s, mode, true, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());
   return NSP_OK;
 }

@@ -1,0 +1,43 @@
+// Tall-skinny / small dense fp64 kernels (nsp_blas.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+// device-resident per-solve status (read back once per iteration)
+struct BcgStatus {
+  int width;        // active direction-block width s'
+  int indefinite;   // chol(P^T S P) failed
+  int fallback;     // orth used the eigen fallback
+  int converged;
+  int nonfinite;
+  int pad_[3];
+  double relres;    // max_j ||R_j|| / ||B_j||
+  double scalar[6]; // PCG scalars
+};
+
+namespace nspb {
+int gram_chunks(int64_t n, int ntiles);
+size_t gram_ws_doubles(int64_t n, int sa, int sb);
+// out (ld ldo) = Xa(n x sa)^T Xb(n x sb); sa, sb multiples of 64 (columns padded)
+void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, int64_t n, double* out, int ldo,
+          double* ws, cudaStream_t st);
+// Out = Cin + sgn * In(n x kdim) M(kdim x ncols); ncols multiple of 64, kdim multiple of 32
+void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
+           int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st);
+void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st);
+void colsq_reduce(const double* part, int ntiles, int ldp, double* out, cudaStream_t st);
+void sqrt_vec(const double* in, double* out, int n, cudaStream_t st);
+void converge(const double* rsq, const double* bnorm, int s, double tol, BcgStatus* stt, double* hist_slot,
+              cudaStream_t st);
+// mode 0: D (pivot <= 0 -> indefinite); mode 1: orth Gram (pivot test -> fallback).
+// nact < 0: active width read from stt->width; rows/cols >= nact are replaced by the identity.
+void small_chol(const double* A, int sp, int mode, int nact, double tau, double* L, double* Linv, double* T,
+                BcgStatus* stt, cudaStream_t st);
+void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* lam, double* Vsorted,
+               const int* gate, cudaStream_t st);
+void orth_from_eig(const double* lam, const double* Vs, int n, int sp, double tau, double* T, BcgStatus* stt,
+                   cudaStream_t st);
+void small_gemm(int m, int n, int k, double alpha, const double* A, int lda, bool ta, const double* B, int ldb,
+                bool tb, double beta, double* C, int ldc, cudaStream_t st);
+void copy_pad(const double* src, int lds, double* dst, int ldd, int64_t n, int s, double scale, cudaStream_t st);
+}  // namespace nspb

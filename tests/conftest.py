@@ -11,3 +11,10 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run with -m gpu)")
     config.addinivalue_line("markers", "slow: long CPU test")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built_library():
+    """Build libnsp.so (in-tree, sm_100a) once if any source is newer than it."""
+    from paper_2101_12164_b200 import build as B
+    B.build()
