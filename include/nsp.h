@@ -111,9 +111,15 @@ nsp_status nsp_dims(const nsp_ctx* ctx, int64_t* n, int64_t* n_gamma, int64_t* n
 /* orig_index: host int64[n_gamma_local]; local Gamma row -> original node id. */
 nsp_status nsp_gamma_index(const nsp_ctx* ctx, int64_t* orig_index);
 nsp_status nsp_workspace_bytes(const nsp_ctx* ctx, int s, size_t* bytes);
-/* factor statistics: host int64[8] = {n_I, n_boundary_layer, L22 entries streamed per apply,
- * factor tiles, nnz(A_G), nnz(A_GI), max b_j, A_G bandwidth} */
-nsp_status nsp_stats(const nsp_ctx* ctx, int64_t* stats8);
+/* factor statistics: host int64[12] = {n_I, n_boundary_layer (sum b_j), L22 entries streamed per
+ * apply (padded tiles), factor tiles, nnz(A_G), nnz(A_GI), max b_j, A_G bandwidth, sum b_j^2,
+ * sum b_j, local blocks, W/V/U rows} */
+nsp_status nsp_stats(const nsp_ctx* ctx, int64_t* stats12);
+/* Live timing of the batched factor-sweep kernel (a2+a3): enable = 1 records a CUDA event pair
+ * around every launch on the context stream; nsp_profile_read synchronises the stream and
+ * returns the summed duration and launch count since the last read. */
+nsp_status nsp_profile(nsp_ctx* ctx, int enable);
+nsp_status nsp_profile_read(nsp_ctx* ctx, double* sweep_ms, long long* sweeps);
 
 /* Y = S_G X (eq:schur_complement), X, Y device n_gamma_local x s row-major; X != Y.
  * Steps: W = A_IG X (boundary-layer rows), V = L_j^{-1} W, U = L_j^{-T} V for all
@@ -121,6 +127,9 @@ nsp_status nsp_stats(const nsp_ctx* ctx, int64_t* stats8);
 nsp_status nsp_schur_apply(nsp_ctx* ctx, const double* X, double* Y, int s, void* ws);
 /* Y = K_G X = A_GI A_I^{-1} A_IG X (the border contribution; Alg. 2 steps 2-4 via reading C1). */
 nsp_status nsp_kgamma_apply(nsp_ctx* ctx, const double* X, double* Y, int s, void* ws);
+
+/* Y = A_G X (Alg. 2 step 4 under reading C1: Y = A_G X after the border solve). */
+nsp_status nsp_gamma_apply(nsp_ctx* ctx, const double* X, double* Y, int s);
 
 /* Breakdown-free block CG on S_G X = B (reading C3/C4),
  * X0 = 0, stop when max_j ||R_j||/||B_j|| <= tol.  Returns NSP_OK,
@@ -146,6 +155,8 @@ nsp_status nsp_pcg(nsp_ctx* ctx, const double* b, double* x, double tol, int max
                    void* ws, nsp_report* rep);
 
 const char* nsp_last_error(const nsp_ctx* ctx);
+/* Number of device kernels this library has launched in the process (evidence counter). */
+long long nsp_kernel_launches(void);
 void nsp_destroy(nsp_ctx* ctx);
 
 #ifdef __cplusplus

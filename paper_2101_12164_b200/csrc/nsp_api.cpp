@@ -43,7 +43,13 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   // a1: W = A_IG X on the boundary-layer rows (zero padding rows / columns)
   nspk::spmm(c->A2G, X, ldx, nullptr, 0, 0, wvu, ldw, s, 0, true, c->stream);
   // a2 + a3: V = L22^{-1} W, U = L22^{-T} V for every block, one launch
+  const bool prof = c->prof_on && (size_t)(c->prof_used + 2) <= c->prof_ev.size();
+  if (prof) cudaEventRecord(c->prof_ev[c->prof_used], c->stream);
   nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, wvu, ldw, cw, c->stream);
+  if (prof) {
+    cudaEventRecord(c->prof_ev[c->prof_used + 1], c->stream);
+    c->prof_used += 2;
+  }
   // a4 + a5: Y = A_G X - A_GI U (fused), or Y = A_GI U
   nspk::spmm(c->AGG2, X, ldx, wvu, ldw, c->nG, Y, ldy, s, mode, true, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());
@@ -71,6 +77,32 @@ nsp_status nsp_gamma_index(const nsp_ctx* c, int64_t* orig) {
   return NSP_OK;
 }
 
+nsp_status nsp_profile(nsp_ctx* c, int enable) {
+  if (!c) return NSP_ERR_ARG;
+  if (enable && c->prof_ev.empty()) {
+    c->prof_ev.resize(2 * 4096);
+    for (auto& e : c->prof_ev) NSP_CUDA_TRY(c, cudaEventCreate(&e));
+  }
+  c->prof_on = enable;
+  c->prof_used = 0;
+  return NSP_OK;
+}
+
+nsp_status nsp_profile_read(nsp_ctx* c, double* sweep_ms, long long* sweeps) {
+  if (!c) return NSP_ERR_ARG;
+  NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  double tot = 0.0;
+  for (int k = 0; k + 1 < c->prof_used; k += 2) {
+    float ms = 0.f;
+    NSP_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->prof_ev[k], c->prof_ev[k + 1]));
+    tot += ms;
+  }
+  if (sweep_ms) *sweep_ms = tot;
+  if (sweeps) *sweeps = c->prof_used / 2;
+  c->prof_used = 0;
+  return NSP_OK;
+}
+
 nsp_status nsp_stats(const nsp_ctx* c, int64_t* st) {
   if (!c || !st) return NSP_ERR_ARG;
   int64_t l22 = 0;
@@ -83,6 +115,10 @@ nsp_status nsp_stats(const nsp_ctx* c, int64_t* st) {
   st[5] = c->nnz_AGI;
   st[6] = c->max_b;
   st[7] = c->ag_bw;
+  st[8] = c->sum_b2;
+  st[9] = c->sum_b;
+  st[10] = c->nsub;
+  st[11] = c->wvu_rows;
   return NSP_OK;
 }
 
@@ -108,6 +144,13 @@ nsp_status nsp_kgamma_apply(nsp_ctx* c, const double* X, double* Y, int s, void*
   return apply_into(c, X, s, Y, s, s, 2, (double*)w);
 }
 
+nsp_status nsp_gamma_apply(nsp_ctx* c, const double* X, double* Y, int s) {
+  if (!c || !X || !Y || s <= 0 || s > 256) return NSP_ERR_ARG;
+  nspk::spmm(c->AGG2, X, s, nullptr, 0, c->nG, Y, s, s, 3, false, c->stream);
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  return NSP_OK;
+}
+
 const char* nsp_last_error(const nsp_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 void nsp_destroy(nsp_ctx* c) {
@@ -125,9 +168,15 @@ void nsp_destroy(nsp_ctx* c) {
     fr(m->val);
   }
   fr(c->ws_int);
+  for (auto& e : c->prof_ev) cudaEventDestroy(e);
   if (c->h_status) cudaFreeHost(c->h_status);
   solver_free(c);
   delete c;
 }
 
 }  // extern "C"
+
+#include <atomic>
+static std::atomic<long long> g_launches{0};
+void nsp_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+extern "C" long long nsp_kernel_launches(void) { return g_launches.load(); }

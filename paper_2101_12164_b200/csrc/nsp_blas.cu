@@ -506,8 +506,8 @@ void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, 
     set_smem((const void*)k_gram_partial, smem);
     attr = true;
   }
-  k_gram_partial<<<dim3(ntm * ntn, nch), 256, smem, st>>>(Xa, lda, Xb, ldb, n, rpc, ws, ntm, ntn);
-  k_gram_reduce<<<dim3(ntn * 4, ntm * 4), dim3(16, 16), 0, st>>>(ws, nch, ntm, ntn, out, ldo);
+  { nsp_count_launch(); k_gram_partial<<<dim3(ntm * ntn, nch), 256, smem, st>>>(Xa, lda, Xb, ldb, n, rpc, ws, ntm, ntn); }
+  { nsp_count_launch(); k_gram_reduce<<<dim3(ntn * 4, ntm * 4), dim3(16, 16), 0, st>>>(ws, nch, ntm, ntn, out, ldo); }
 }
 
 void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
@@ -520,33 +520,33 @@ void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, i
     attr = true;
   }
   dim3 grid((unsigned)((n + 63) / 64), (ncols + 63) / 64);
-  k_panel<<<grid, 256, smem, st>>>(Out, ldo, Cin, ldc, In, ldi, M, ldm, kdim, n, sgn, normpart);
+  { nsp_count_launch(); k_panel<<<grid, 256, smem, st>>>(Out, ldo, Cin, ldc, In, ldi, M, ldm, kdim, n, sgn, normpart); }
 }
 
 void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st) {
   const int nt = (int)((n + 63) / 64);
-  k_colsq_partial<<<nt, ldp, 0, st>>>(X, ldx, n, s, part, ldp);
-  k_colsq_reduce<<<1, ldp, 0, st>>>(part, nt, ldp, out);
+  { nsp_count_launch(); k_colsq_partial<<<nt, ldp, 0, st>>>(X, ldx, n, s, part, ldp); }
+  { nsp_count_launch(); k_colsq_reduce<<<1, ldp, 0, st>>>(part, nt, ldp, out); }
 }
 
 void colsq_reduce(const double* part, int ntiles, int ldp, double* out, cudaStream_t st) {
-  k_colsq_reduce<<<1, ldp, 0, st>>>(part, ntiles, ldp, out);
+  { nsp_count_launch(); k_colsq_reduce<<<1, ldp, 0, st>>>(part, ntiles, ldp, out); }
 }
 
 void sqrt_vec(const double* in, double* out, int n, cudaStream_t st) {
-  k_sqrt_vec<<<(n + 255) / 256, 256, 0, st>>>(in, out, n);
+  { nsp_count_launch(); k_sqrt_vec<<<(n + 255) / 256, 256, 0, st>>>(in, out, n); }
 }
 
 void converge(const double* rsq, const double* bnorm, int s, double tol, BcgStatus* stt, double* hist_slot,
               cudaStream_t st) {
-  k_converge<<<1, 256, 0, st>>>(rsq, bnorm, s, tol, stt, hist_slot);
+  { nsp_count_launch(); k_converge<<<1, 256, 0, st>>>(rsq, bnorm, s, tol, stt, hist_slot); }
 }
 
 void small_chol(const double* A, int sp, int mode, int nact, double tau, double* L, double* Linv, double* T,
                 BcgStatus* stt, cudaStream_t st) {
   const size_t smem = ((size_t)sp * (sp + 1) + (size_t)sp * (sp + 1) / 2) * sizeof(double);
   set_smem((const void*)k_small_chol, smem);
-  k_small_chol<<<1, 1024, smem, st>>>(A, sp, mode, nact, tau, L, Linv, T, stt);
+  { nsp_count_launch(); k_small_chol<<<1, 1024, smem, st>>>(A, sp, mode, nact, tau, L, Linv, T, stt); }
 }
 
 void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* lam, double* Vsorted,
@@ -554,24 +554,24 @@ void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* 
   const int ne = n + (n & 1);
   const size_t smem = (size_t)ne * (ne + 1) * sizeof(double);
   set_smem((const void*)k_small_eig, smem);
-  k_small_eig<<<1, 1024, smem, st>>>(A, lda, n, Vwork, ldv, lam, Vsorted, gate);
+  { nsp_count_launch(); k_small_eig<<<1, 1024, smem, st>>>(A, lda, n, Vwork, ldv, lam, Vsorted, gate); }
 }
 
 void orth_from_eig(const double* lam, const double* Vs, int n, int sp, double tau, double* T, BcgStatus* stt,
                    cudaStream_t st) {
-  k_orth_from_eig<<<1, 1024, 0, st>>>(lam, Vs, n, sp, tau, T, stt);
+  { nsp_count_launch(); k_orth_from_eig<<<1, 1024, 0, st>>>(lam, Vs, n, sp, tau, T, stt); }
 }
 
 void small_gemm(int m, int n, int k, double alpha, const double* A, int lda, bool ta, const double* B, int ldb,
                 bool tb, double beta, double* C, int ldc, cudaStream_t st) {
   dim3 grid((n + 15) / 16, (m + 15) / 16);
-  k_small_gemm<<<grid, dim3(16, 16), 0, st>>>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc);
+  { nsp_count_launch(); k_small_gemm<<<grid, dim3(16, 16), 0, st>>>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc); }
 }
 
 void copy_pad(const double* src, int lds, double* dst, int ldd, int64_t n, int s, double scale, cudaStream_t st) {
   const int64_t tot = n * ldd;
   if (tot <= 0) return;
-  k_copy_pad<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, lds, dst, ldd, n, s, scale);
+  { nsp_count_launch(); k_copy_pad<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, lds, dst, ldd, n, s, scale); }
 }
 
 }  // namespace nspb

@@ -15,6 +15,8 @@ struct BcgStatus {
   double scalar[6]; // PCG scalars
 };
 
+void nsp_count_launch();
+
 namespace nspb {
 int gram_chunks(int64_t n, int ntiles);
 size_t gram_ws_doubles(int64_t n, int sa, int sb);

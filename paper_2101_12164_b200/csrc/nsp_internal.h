@@ -74,7 +74,16 @@ struct nsp_ctx {
   void* ws_int = nullptr; size_t ws_int_bytes = 0;
   // small pinned host status
   void* h_status = nullptr;
+
+  // live kernel timing (nsp_profile): event pairs around the factor-sweep launches
+  int prof_on = 0;
+  std::vector<cudaEvent_t> prof_ev;   // 2 per record
+  int prof_used = 0;
+  int64_t sum_b2 = 0, sum_b = 0;
 };
+
+// number of device kernels launched by this library (evidence counter)
+void nsp_count_launch();
 
 // kernel launchers (nsp_kernels.cu)
 namespace nspk {
@@ -84,7 +93,7 @@ void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, do
                    const int* border_first, int* status, cudaStream_t st);
 // Y[r, c] (c < s) = sum_k val_k * X(col_k, c); mode 0: Y = A X (X ld ldx);
 // mode 1: Y = A [X ; U] with cols >= split reading U (ld ldu) at col-split;
-// mode 2: Y = -(cols >= split part only)  (K_G apply)
+// mode 2: Y = -(cols >= split part only)  (K_G apply); mode 3: cols < split only (A_G X)
 // Y ld ldy; columns s..ldy-1 of Y are written with 0 when zero_pad.
 void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split,
           double* Y, int ldy, int s, int mode, bool zero_pad, cudaStream_t st);

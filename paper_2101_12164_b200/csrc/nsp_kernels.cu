@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __res
         if (mode == 2) continue;
         src = X + col * ldx;
       } else {
+        if (mode == 3) continue;
         src = U + (col - split) * ldu;
         if (mode == 2) a = -a;
       }
@@ -394,12 +395,12 @@ namespace nspk {
 
 void scatter(double* base, const int64_t* idx, const double* val, int64_t cnt, cudaStream_t st) {
   if (cnt <= 0) return;
-  k_scatter<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(base, idx, val, cnt);
+  { nsp_count_launch(); k_scatter<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(base, idx, val, cnt); }
 }
 
 void set_pad_identity(double* base, const int64_t* tile_idx, const int* first_row, int cnt, cudaStream_t st) {
   if (cnt <= 0) return;
-  k_pad_identity<<<cnt, 64, 0, st>>>(base, tile_idx, first_row, cnt);
+  { nsp_count_launch(); k_pad_identity<<<cnt, 64, 0, st>>>(base, tile_idx, first_row, cnt); }
 }
 
 void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, double* scratch,
@@ -411,7 +412,7 @@ void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, do
     cudaFuncSetAttribute(k_tile_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_tile_cholesky<<<nsub, 256, smem, st>>>(subs, band, dense, scratch, border_first, status);
+  { nsp_count_launch(); k_tile_cholesky<<<nsub, 256, smem, st>>>(subs, band, dense, scratch, border_first, status); }
 }
 
 void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split, double* Y,
@@ -419,13 +420,13 @@ void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, i
   if (A.rows <= 0) return;
   const unsigned blocks = (unsigned)((A.rows * 32 + 255) / 256);
   if (s <= 32)
-    k_spmm<1><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad);
+    { nsp_count_launch(); k_spmm<1><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
   else if (s <= 64)
-    k_spmm<2><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad);
+    { nsp_count_launch(); k_spmm<2><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
   else if (s <= 128)
-    k_spmm<4><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad);
+    { nsp_count_launch(); k_spmm<4><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
   else
-    k_spmm<8><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad);
+    { nsp_count_launch(); k_spmm<8><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
 }
 
 void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw, cudaStream_t st) {
@@ -438,7 +439,7 @@ void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int
       cudaFuncSetAttribute(k_trsm_fb<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    k_trsm_fb<64><<<grid, 256, smem, st>>>(subs, dense, wvu, ldw);
+    { nsp_count_launch(); k_trsm_fb<64><<<grid, 256, smem, st>>>(subs, dense, wvu, ldw); }
   } else {
     const size_t smem = (2 * 64 * LDT + 2 * 64 * (32 + 4)) * sizeof(double);
     static bool attr = false;
@@ -446,7 +447,7 @@ void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int
       cudaFuncSetAttribute(k_trsm_fb<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    k_trsm_fb<32><<<grid, 256, smem, st>>>(subs, dense, wvu, ldw);
+    { nsp_count_launch(); k_trsm_fb<32><<<grid, 256, smem, st>>>(subs, dense, wvu, ldw); }
   }
 }
 

@@ -371,6 +371,8 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
     c->n_I += S.n1 + S.b;
     c->n_bl += S.b;
     c->max_b = std::max<int64_t>(c->max_b, S.b);
+    c->sum_b2 += (int64_t)S.b * S.b;
+    c->sum_b += S.b;
   }
   c->band_tiles = band_tiles;
   c->dense_tiles = dense_tiles;

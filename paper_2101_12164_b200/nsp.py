@@ -20,7 +20,8 @@ NSP_STATUS = {0: "NSP_OK", 1: "NSP_NOT_CONVERGED", -1: "NSP_ERR_ARG", -2: "NSP_E
 
 EXPORTED = ["nsp_default_opts", "nsp_setup", "nsp_dims", "nsp_gamma_index", "nsp_workspace_bytes",
             "nsp_stats", "nsp_schur_apply", "nsp_kgamma_apply", "nsp_block_cg", "nsp_nystrom",
-            "nsp_nystrom_sigma", "nsp_precond_apply", "nsp_pcg", "nsp_last_error", "nsp_destroy"]
+            "nsp_nystrom_sigma", "nsp_precond_apply", "nsp_pcg", "nsp_last_error", "nsp_destroy",
+            "nsp_gamma_apply", "nsp_kernel_launches", "nsp_profile", "nsp_profile_read"]
 
 
 class nsp_csr(C.Structure):
@@ -75,10 +76,15 @@ def load_library(path: str = LIB_PATH):
     lib.nsp_pcg.argtypes = [P, P, P, D, I, I, P, P]
     lib.nsp_last_error.argtypes = [P]
     lib.nsp_last_error.restype = C.c_char_p
+    lib.nsp_gamma_apply.argtypes = [P, P, P, I]
+    lib.nsp_profile.argtypes = [P, I]
+    lib.nsp_profile_read.argtypes = [P, P, P]
+    lib.nsp_kernel_launches.argtypes = []
+    lib.nsp_kernel_launches.restype = C.c_longlong
     lib.nsp_destroy.argtypes = [P]
     lib.nsp_destroy.restype = None
     for f in EXPORTED:
-        if f not in ("nsp_default_opts", "nsp_last_error", "nsp_destroy"):
+        if f not in ("nsp_default_opts", "nsp_last_error", "nsp_destroy", "nsp_kernel_launches"):
             getattr(lib, f).restype = C.c_int
     _lib = lib
     return lib
@@ -105,6 +111,10 @@ def _report(rep: nsp_report, hist, widths) -> Report:
     if widths is not None:
         r["widths"] = list(widths[: min(rep.iters, len(widths))])
     return r
+
+
+def kernel_launches() -> int:
+    return int(load_library().nsp_kernel_launches())
 
 
 class Context:
@@ -160,9 +170,10 @@ class Context:
         return out
 
     def stats(self) -> dict:
-        out = np.zeros(8, dtype=np.int64)
+        out = np.zeros(12, dtype=np.int64)
         self._check(self.lib.nsp_stats(self.ctx, out.ctypes.data))
-        keys = ["n_I", "n_boundary_layer", "l22_entries", "factor_tiles", "nnz_AG", "nnz_AGI", "max_b", "ag_bw"]
+        keys = ["n_I", "n_boundary_layer", "l22_entries", "factor_tiles", "nnz_AG", "nnz_AGI", "max_b", "ag_bw",
+                "sum_b2", "sum_b", "n_sub", "wvu_rows"]
         return dict(zip(keys, [int(x) for x in out]))
 
     def workspace_bytes(self, s: int) -> int:
@@ -177,6 +188,17 @@ class Context:
     def kgamma_apply(self, X, Y, ws=None):
         s = X.shape[1]
         self._check(self.lib.nsp_kgamma_apply(self.ctx, _ptr(X), _ptr(Y), s, None if ws is None else ws.data_ptr()))
+
+    def profile(self, enable=True):
+        self._check(self.lib.nsp_profile(self.ctx, int(enable)))
+
+    def profile_read(self):
+        ms, cnt = C.c_double(), C.c_longlong()
+        self._check(self.lib.nsp_profile_read(self.ctx, C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
+    def gamma_apply(self, X, Y):
+        self._check(self.lib.nsp_gamma_apply(self.ctx, _ptr(X), _ptr(Y), X.shape[1]))
 
     def block_cg(self, B, X, tol, maxit, ws=None, hist_cap=None):
         s = B.shape[1]
