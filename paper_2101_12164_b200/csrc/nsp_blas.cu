@@ -37,7 +37,8 @@ constexpr int LDS = 68;    // smem stride for 64-wide tiles
 // part[(chunk * ntm * ntn + tm * ntn + tn) * 4096 + i * 64 + j]
 //   = sum_{r in chunk} Xa[r][64 tm + i] * Xb[r][64 tn + j]
 __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__ Xa, int lda,
-                                                      const double* __restrict__ Xb, int ldb, int64_t n,
+                                                      const double* __restrict__ Xb, const double* __restrict__ Xb2,
+                                                      int ldb, int ntn1, int64_t n,
                                                       int64_t rows_per_chunk, double* __restrict__ part, int ntm,
                                                       int ntn) {
   extern __shared__ double sm[];
@@ -50,7 +51,7 @@ __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__
   double acc[2][4][2];
   acc_zero(acc);
   const double* A0 = Xa + 64 * tm;
-  const double* B0 = Xb + 64 * tn;
+  const double* B0 = tn < ntn1 ? Xb + 64 * tn : Xb2 + 64 * (tn - ntn1);
   int buf = 0;
   if (r0 < r1) {
     cp_block_zf(As[0], LDS, A0 + r0 * lda, lda, GR, 64, r1 - r0);
@@ -82,23 +83,43 @@ __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__
     }
 }
 
-__global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int ntm, int ntn, double* out,
-                              int ldo) {
+// out (or out2 for column tiles >= ntn1) = sum over chunks, 4 chunk groups per element combined
+// in fixed order (deterministic)
+__global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int ntm, int ntn, int ntn1,
+                              double* out, double* out2, int ldo) {
+  __shared__ double red[4][16][17];
   const int i = blockIdx.y * 16 + threadIdx.y;
   const int j = blockIdx.x * 16 + threadIdx.x;
-  if (i >= ntm * 64 || j >= ntn * 64) return;
-  const int64_t off = (int64_t)((i >> 6) * ntn + (j >> 6)) * 4096 + (i & 63) * 64 + (j & 63);
-  const int64_t stride = (int64_t)ntm * ntn * 4096;
+  const int g = threadIdx.z;
   double s = 0.0;
-  for (int c = 0; c < nchunks; ++c) s += part[off + c * stride];
-  out[(int64_t)i * ldo + j] = s;
+  if (i < ntm * 64 && j < ntn * 64) {
+    const int64_t off = (int64_t)((i >> 6) * ntn + (j >> 6)) * 4096 + (i & 63) * 64 + (j & 63);
+    const int64_t stride = (int64_t)ntm * ntn * 4096;
+    for (int c = g; c < nchunks; c += 4) s += part[off + c * stride];
+  }
+  red[g][threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (g == 0 && i < ntm * 64 && j < ntn * 64) {
+    const double v = red[0][threadIdx.y][threadIdx.x] + red[1][threadIdx.y][threadIdx.x] +
+                     red[2][threadIdx.y][threadIdx.x] + red[3][threadIdx.y][threadIdx.x];
+    const int j1 = j - ntn1 * 64;
+    if (j1 < 0) out[(int64_t)i * ldo + j] = v;
+    else out2[(int64_t)i * ldo + j1] = v;
+  }
 }
 
 // Out[r][c] = (Cin ? Cin[r][c] : 0) + sgn * sum_k In[r][k] M[k][c];   r < n, c in this 64-col tile.
+// blockIdx.z selects one of two independent argument sets (X += P alpha and R -= Q alpha in one launch).
 // normpart (optional): normpart[rowtile * ldo + c] = sum over the tile's rows of Out[r][c]^2.
-__global__ void __launch_bounds__(256) k_panel(double* Out, int ldo, const double* Cin, int ldc,
-                                               const double* __restrict__ In, int ldi, const double* __restrict__ M,
-                                               int ldm, int kdim, int64_t n, double sgn, double* normpart) {
+__global__ void __launch_bounds__(256) k_panel(PanelArgs pa0, PanelArgs pa1, int kdim, int64_t n) {
+  const PanelArgs& pa = blockIdx.z ? pa1 : pa0;
+  double* Out = pa.Out;
+  const int ldo = pa.ldo, ldc = pa.ldc, ldi = pa.ldi, ldm = pa.ldm;
+  const double* Cin = pa.Cin;
+  const double* __restrict__ In = pa.In;
+  const double* __restrict__ M = pa.M;
+  const double sgn = pa.sgn;
+  double* normpart = pa.normpart;
   extern __shared__ double sm[];
   constexpr int LDA = 36;
   double* As[2] = {sm, sm + 64 * LDA};
@@ -175,13 +196,21 @@ __global__ void k_colsq_partial(const double* __restrict__ X, int ldx, int64_t n
   part[blockIdx.x * (int64_t)ldp + c] = acc;
 }
 
-// sum over row tiles -> out[c]
+// sum over row tiles -> out[c]; thread (c, g) sums tiles t = g mod 8 in order, then the 8
+// group sums are added in fixed order (deterministic)
 __global__ void k_colsq_reduce(const double* __restrict__ part, int ntiles, int ldp, double* out) {
-  const int c = threadIdx.x;
-  if (c >= ldp) return;
+  __shared__ double red[8][128];
+  const int c = threadIdx.x, g = threadIdx.y;
   double s = 0.0;
-  for (int t = 0; t < ntiles; ++t) s += part[t * (int64_t)ldp + c];
-  out[c] = s;
+  if (c < ldp)
+    for (int t = g; t < ntiles; t += 8) s += part[t * (int64_t)ldp + c];
+  red[g][c] = s;
+  __syncthreads();
+  if (g == 0 && c < ldp) {
+    double v = 0.0;
+    for (int q = 0; q < 8; ++q) v += red[q][c];
+    out[c] = v;
+  }
 }
 
 // convergence: relres_j = sqrt(rsq_j) / bnorm_j; max over j < s (columns with bnorm 0 count as 0)
@@ -216,94 +245,226 @@ __global__ void k_sqrt_vec(const double* in, double* out, int n) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// one-CTA Cholesky of an sp x sp SPD matrix with pivot record, and the inverse of its factor.
-// mode 0 (D = P^T S P): rows/cols >= width replaced by identity; pivot <= 0 -> indefinite flag.
-// mode 1 (G = W^T W, orth): pivot test  min d_i > tau * max d_i  (reading C3); failure -> fallback.
-// Outputs: L (lower, ld sp), Linv (lower, ld sp); mode 1 also T = Linv^T (P = W T = W R^{-1}).
+// one-CTA (8 warps) blocked Cholesky of an sp x sp SPD matrix (sp <= 128, multiple of 8) and of
+// the inverse of its factor, latency-oriented: 8x8 diagonal blocks are factored (and inverted)
+// by one thread entirely in registers (rsqrt.approx + 2 Newton steps, no divisions); the 8-column
+// panel is solved row-parallel; the rank-8 trailing update runs on the DMMA pipe (m8n8k4 tiles);
+// X = L^{-1} is formed block row by block row on the DMMA pipe.  3 barriers per 8 columns.
+// Rows / cols >= nact (nact < 0: st->width) are replaced by the identity.
+//  mode 0 (D = P^T S P): pivot <= 0 -> st->indefinite; Out = D^{-1} = X^T X.
+//  mode 1 (G = W^T W, orth): pivot test min d_i > tau max d_i (reading C3) else st->fallback;
+//          Out = T = X^T (so that P = W T = W R^{-1}, G = R^T R).
+// Storage: As (lower) = L; As (upper, off-diagonal 8x8 blocks) = T = X^T; Di[b] = X_bb (8x8).
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_small_chol(const double* __restrict__ Ain, int sp, int mode, int nact,
-                                                     double tau, double* Lout, double* Linv, double* Tout,
-                                                     BcgStatus* st) {
+namespace sc {
+constexpr int LDA = 132;
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  const double h = 0.5 * d;
+  r = r * fma(-h * r, r, 1.5);
+  r = r * fma(-h * r, r, 1.5);
+  return r;
+}
+}  // namespace sc
+
+__global__ void __launch_bounds__(256) k_small_chol(const double* __restrict__ Ain, int sp, int mode, int nact,
+                                                    double tau, double* __restrict__ Out, BcgStatus* st) {
+  using sc::LDA;
   extern __shared__ double sm[];
-  const int ld = sp + 1;
-  double* A = sm;                       // sp x ld
-  double* X = sm + sp * ld;             // packed lower: row i at i(i+1)/2
-  __shared__ double colv[256];
-  __shared__ double piv[256];
-  __shared__ int fail;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  double* As = sm;                  // sp x LDA
+  double* Di = sm + 128 * LDA;      // 16 x 64: X_bb = inv(L_bb), row-major 8x8
+  double* Sc = Di + 16 * 64;        // 8 warps x 64 scratch
+  __shared__ double piv[128];
+  __shared__ int s_fail;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int NB = sp / 8;
   const int width = nact < 0 ? st->width : nact;
-  if (tid == 0) fail = 0;
-  for (int e = tid; e < sp * sp; e += nt) {
+  if (tid == 0) s_fail = 0;
+  for (int e = tid; e < sp * sp; e += 256) {
     const int i = e / sp, j = e - i * sp;
     double v = Ain[e];
     if (i >= width || j >= width) v = (i == j) ? 1.0 : 0.0;
-    A[i * ld + j] = v;
+    As[i * LDA + j] = v;
   }
   __syncthreads();
-  for (int c = 0; c < sp; ++c) {
-    const double d = A[c * ld + c];
-    if (tid == 0) piv[c] = d;
-    if (!(d > 0.0)) {
-      if (tid == 0) fail = 1;
-      break;
+  // ============================ Cholesky
+  for (int kb = 0; kb < NB; ++kb) {
+    const int c0 = 8 * kb;
+    if (tid == 0) {
+      double a[8][8], x[8][8], il[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[i][j] = (j <= i) ? As[(c0 + i) * LDA + c0 + j] : 0.0;
+      bool fail = false;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        double d = a[c][c];
+        piv[c0 + c] = d;
+        if (!(d > 0.0)) {
+          fail = true;
+          d = 1.0;
+        }
+        const double r = sc::rsqrt_nr(d);
+        il[c] = r;
+        a[c][c] = d * r;
+#pragma unroll
+        for (int i = c + 1; i < 8; ++i) a[i][c] *= r;
+#pragma unroll
+        for (int j = c + 1; j < 8; ++j)
+#pragma unroll
+          for (int i = j; i < 8; ++i) a[i][j] = fma(-a[i][c], a[j][c], a[i][j]);
+      }
+      // x = inv(L) (lower), right-looking
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[i][j] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+#pragma unroll
+        for (int j = 0; j <= k; ++j) x[k][j] *= il[k];
+#pragma unroll
+        for (int i = k + 1; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j <= k; ++j) x[i][j] = fma(-a[i][k], x[k][j], x[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          As[(c0 + i) * LDA + c0 + j] = (j <= i) ? a[i][j] : 0.0;
+          Di[kb * 64 + i * 8 + j] = (j <= i) ? x[i][j] : 0.0;
+        }
+      if (fail) s_fail = 1;
     }
-    const double l = sqrt(d);
-    for (int i = c + 1 + tid; i < sp; i += nt) colv[i] = A[i * ld + c] / l;
     __syncthreads();
-    const int m = sp - c - 1;
-    for (int e = tid; e < m * m; e += nt) {
-      const int i = c + 1 + e / m, j = c + 1 + e % m;
-      if (j <= i) A[i * ld + j] -= colv[i] * colv[j];
+    if (s_fail) break;
+    // panel: L[i][c0..c0+8) = A[i][c0..c0+8) X_kk^T, one row per thread
+    for (int i = c0 + 8 + tid; i < sp; i += 256) {
+      double a[8], o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = As[i * LDA + c0 + k];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int k = 0; k <= j; ++k) sacc = fma(a[k], Di[kb * 64 + j * 8 + k], sacc);
+        o[j] = sacc;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) As[i * LDA + c0 + j] = o[j];
     }
-    for (int i = c + 1 + tid; i < sp; i += nt) A[i * ld + c] = colv[i];
-    if (tid == 0) A[c * ld + c] = l;
+    __syncthreads();
+    // trailing update on 8x8 tiles: A_IJ -= L_I,kb L_J,kb^T (I >= J > kb), one tile per warp-task
+    const int m = NB - 1 - kb;
+    const int ntile = m * (m + 1) / 2;
+    for (int task = warp; task < ntile; task += 8) {
+      // decode (q, p), p <= q, from the linear index
+      int q = (int)((sqrtf(8.0f * task + 1.0f) - 1.0f) * 0.5f);
+      while (q * (q + 1) / 2 > task) --q;
+      while ((q + 1) * (q + 2) / 2 <= task) ++q;
+      const int p = task - q * (q + 1) / 2;
+      const int I = kb + 1 + q, J = kb + 1 + p;
+      const double* LI = As + (8 * I) * LDA + c0;
+      const double* LJ = As + (8 * J) * LDA + c0;
+      double c0v = 0.0, c1v = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; k += 4) dmma(c0v, c1v, LI[g * LDA + k + t], LJ[g * LDA + k + t]);
+      double* dst = As + (8 * I + g) * LDA + 8 * J + 2 * t;
+      dst[0] -= c0v;
+      dst[1] -= c1v;
+    }
     __syncthreads();
   }
-  __syncthreads();
-  bool ok = !fail;
-  if (ok && mode == 1) {
-    double mn = piv[0], mx = piv[0];
-    for (int i = 1; i < width; ++i) {
-      mn = fmin(mn, piv[i]);
-      mx = fmax(mx, piv[i]);
-    }
-    ok = mn > tau * mx;
-  }
-  if (!ok) {
+  if (s_fail) {
     if (tid == 0) {
       if (mode == 0) st->indefinite = 1;
       else st->fallback = 1;
     }
     return;
   }
-  if (tid == 0 && mode == 1) {
-    st->fallback = 0;
-    st->width = width;
+  if (mode == 1) {
+    double mn = piv[0], mx = piv[0];
+    for (int i = 1; i < width; ++i) {
+      mn = fmin(mn, piv[i]);
+      mx = fmax(mx, piv[i]);
+    }
+    if (!(mn > tau * mx)) {
+      if (tid == 0) st->fallback = 1;
+      return;
+    }
+    if (tid == 0) {
+      st->fallback = 0;
+      st->width = width;
+    }
   }
-  // inverse of lower L: right-looking forward substitution on X = I
-  for (int e = tid; e < sp * (sp + 1) / 2; e += nt) X[e] = 0.0;
-  __syncthreads();
-  for (int i = tid; i < sp; i += nt) X[i * (i + 1) / 2 + i] = 1.0;
-  __syncthreads();
-  for (int k = 0; k < sp; ++k) {
-    const double lkk = A[k * ld + k];
-    for (int cc = tid; cc <= k; cc += nt) X[k * (k + 1) / 2 + cc] /= lkk;
-    __syncthreads();
-    const int m = sp - k - 1;
-    for (int e = tid; e < m * (k + 1); e += nt) {
-      const int i = k + 1 + e / (k + 1), cc = e % (k + 1);
-      X[i * (i + 1) / 2 + cc] -= A[i * ld + k] * X[k * (k + 1) / 2 + cc];
+  // ============================ X = L^{-1}, block row by block row:
+  // X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ  (J < I);  stored transposed: As[8J + c][8I + r] = X_IJ[r][c]
+  double* scr = Sc + warp * 64;
+  for (int I = 1; I < NB; ++I) {
+    for (int J = warp; J < I; J += 8) {
+      double c0v = 0.0, c1v = 0.0;
+      for (int K = J; K < I; ++K) {
+        const double* LIK = As + (8 * I) * LDA + 8 * K;          // A[m][k] = LIK[m][k]
+#pragma unroll
+        for (int k = 0; k < 8; k += 4) {
+          // B[k][n] = X_KJ[k][n]: K == J -> Di[J]; else T block (J, K): X_KJ[k][n] = As[8J + n][8K + k]
+          const double b = (K == J) ? Di[J * 64 + (k + t) * 8 + g] : As[(8 * J + g) * LDA + 8 * K + k + t];
+          dmma(c0v, c1v, LIK[g * LDA + k + t], b);
+        }
+      }
+      // scr = tmp (8x8, row-major), then X_IJ = -X_II tmp
+      scr[g * 8 + 2 * t] = c0v;
+      scr[g * 8 + 2 * t + 1] = c1v;
+      __syncwarp();
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; k += 4) dmma(d0, d1, Di[I * 64 + g * 8 + k + t], scr[(k + t) * 8 + g]);
+      __syncwarp();
+      As[(8 * J + 2 * t) * LDA + 8 * I + g] = -d0;
+      As[(8 * J + 2 * t + 1) * LDA + 8 * I + g] = -d1;
     }
     __syncthreads();
   }
-  for (int e = tid; e < sp * sp; e += nt) {
-    const int i = e / sp, j = e - i * sp;
-    const double lv = (j <= i) ? A[i * ld + j] : 0.0;
-    const double xv = (j <= i) ? X[i * (i + 1) / 2 + j] : 0.0;
-    if (Lout) Lout[e] = lv;
-    if (Linv) Linv[e] = xv;
-    if (Tout) Tout[j * sp + i] = xv;  // T = Linv^T
+  // T[p][q] = X[q][p]
+  auto Tval = [&](int p, int q) -> double {
+    const int bp = p >> 3, bq = q >> 3;
+    if (bp == bq) return Di[bp * 64 + (q & 7) * 8 + (p & 7)];
+    if (bp < bq) return As[p * LDA + q];
+    return 0.0;
+  };
+  if (mode == 1) {
+    for (int e = tid; e < sp * sp; e += 256) {
+      const int p = e / sp, q = e - p * sp;
+      Out[e] = Tval(p, q);
+    }
+    return;
+  }
+  // D^{-1} = X^T X on 8x8 tiles: Dinv_IJ = sum_{K >= J} X_KI^T X_KJ   (I <= J), mirrored
+  const int ntile = NB * (NB + 1) / 2;
+  for (int task = warp; task < ntile; task += 8) {
+    int q = (int)((sqrtf(8.0f * task + 1.0f) - 1.0f) * 0.5f);
+    while (q * (q + 1) / 2 > task) --q;
+    while ((q + 1) * (q + 2) / 2 <= task) ++q;
+    const int I = task - q * (q + 1) / 2, J = q;  // I <= J
+    double c0v = 0.0, c1v = 0.0;
+    for (int K = J; K < NB; ++K) {
+#pragma unroll
+      for (int k = 0; k < 8; k += 4) {
+        // A[m][k] = X_KI[k][m] = T[8I + m][8K + k];  B[k][n] = X_KJ[k][n] = T[8J + n][8K + k]
+        const double a = Tval(8 * I + g, 8 * K + k + t);
+        const double b = Tval(8 * J + g, 8 * K + k + t);
+        dmma(c0v, c1v, a, b);
+      }
+    }
+    const int r = 8 * I + g, cc = 8 * J + 2 * t;
+    Out[r * sp + cc] = c0v;
+    Out[r * sp + cc + 1] = c1v;
+    Out[cc * sp + r] = c0v;
+    Out[(cc + 1) * sp + r] = c1v;
   }
 }
 
@@ -357,7 +518,7 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
     }
     const double tots = red[0];
     __syncthreads();
-    if (!(offs > 1e-32 * tots) || tots == 0.0) break;
+    if (!(offs > 1e-28 * tots) || tots == 0.0) break;
     for (int round = 0; round < ne - 1; ++round) {
       // tournament pairing: positions 0..ne-1, element 0 fixed, others rotate
       if (tid < npair) {
@@ -372,7 +533,7 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
         qq[tid] = q;
         const double apq = A[p * ld + q];
         double c = 1.0, s = 0.0;
-        if (fabs(apq) > 1e-300) {
+        if (fabs(apq) > 1e-300 && fabs(apq) > 1e-18 * sqrt(fabs(A[p * ld + p] * A[q * ld + q]))) {
           const double th = (A[q * ld + q] - A[p * ld + p]) / (2.0 * apq);
           const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
           c = 1.0 / sqrt(t * t + 1.0);
@@ -490,13 +651,14 @@ int gram_chunks(int64_t n, int ntiles) {
 }
 
 size_t gram_ws_doubles(int64_t n, int sa, int sb) {
-  const int ntm = (sa + 63) / 64, ntn = (sb + 63) / 64;
+  const int ntm = (sa + 63) / 64, ntn = 2 * ((sb + 63) / 64);
   return (size_t)gram_chunks(n, ntm * ntn) * ntm * ntn * 4096;
 }
 
-void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, int64_t n, double* out, int ldo,
-          double* ws, cudaStream_t st) {
-  const int ntm = (sa + 63) / 64, ntn = (sb + 63) / 64;
+void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb2, int ldb, int sb, int64_t n,
+           double* out, double* out2, int ldo, double* ws, cudaStream_t st) {
+  const int ntm = (sa + 63) / 64, ntn1 = (sb + 63) / 64;
+  const int ntn = Xb2 ? 2 * ntn1 : ntn1;
   const int nch = gram_chunks(n, ntm * ntn);
   int64_t rpc = (n + nch - 1) / nch;
   rpc = ((rpc + GR - 1) / GR) * GR;
@@ -506,12 +668,16 @@ void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, 
     set_smem((const void*)k_gram_partial, smem);
     attr = true;
   }
-  { nsp_count_launch(); k_gram_partial<<<dim3(ntm * ntn, nch), 256, smem, st>>>(Xa, lda, Xb, ldb, n, rpc, ws, ntm, ntn); }
-  { nsp_count_launch(); k_gram_reduce<<<dim3(ntn * 4, ntm * 4), dim3(16, 16), 0, st>>>(ws, nch, ntm, ntn, out, ldo); }
+  { nsp_count_launch(); k_gram_partial<<<dim3(ntm * ntn, nch), 256, smem, st>>>(Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn); }
+  { nsp_count_launch(); k_gram_reduce<<<dim3(ntn * 4, ntm * 4), dim3(16, 16, 4), 0, st>>>(ws, nch, ntm, ntn, ntn1, out, out2, ldo); }
 }
 
-void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
-           int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st) {
+void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, int64_t n, double* out, int ldo,
+          double* ws, cudaStream_t st) {
+  gram2(Xa, lda, sa, Xb, nullptr, ldb, sb, n, out, nullptr, ldo, ws, st);
+}
+
+void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   const size_t smem = (2 * 64 * 36 + 2 * 32 * LDS) * sizeof(double);
   static bool attr = false;
@@ -519,18 +685,24 @@ void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, i
     set_smem((const void*)k_panel, smem);
     attr = true;
   }
-  dim3 grid((unsigned)((n + 63) / 64), (ncols + 63) / 64);
-  { nsp_count_launch(); k_panel<<<grid, 256, smem, st>>>(Out, ldo, Cin, ldc, In, ldi, M, ldm, kdim, n, sgn, normpart); }
+  dim3 grid((unsigned)((n + 63) / 64), (ncols + 63) / 64, a1 ? 2 : 1);
+  { nsp_count_launch(); k_panel<<<grid, 256, smem, st>>>(a0, a1 ? *a1 : a0, kdim, n); }
+}
+
+void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
+           int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st) {
+  PanelArgs a{Out, ldo, Cin, ldc, In, ldi, M, ldm, sgn, normpart};
+  panel2(a, nullptr, kdim, ncols, n, st);
 }
 
 void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st) {
   const int nt = (int)((n + 63) / 64);
   { nsp_count_launch(); k_colsq_partial<<<nt, ldp, 0, st>>>(X, ldx, n, s, part, ldp); }
-  { nsp_count_launch(); k_colsq_reduce<<<1, ldp, 0, st>>>(part, nt, ldp, out); }
+  { nsp_count_launch(); k_colsq_reduce<<<1, dim3(128, 8), 0, st>>>(part, nt, ldp, out); }
 }
 
 void colsq_reduce(const double* part, int ntiles, int ldp, double* out, cudaStream_t st) {
-  { nsp_count_launch(); k_colsq_reduce<<<1, ldp, 0, st>>>(part, ntiles, ldp, out); }
+  { nsp_count_launch(); k_colsq_reduce<<<1, dim3(128, 8), 0, st>>>(part, ntiles, ldp, out); }
 }
 
 void sqrt_vec(const double* in, double* out, int n, cudaStream_t st) {
@@ -542,11 +714,11 @@ void converge(const double* rsq, const double* bnorm, int s, double tol, BcgStat
   { nsp_count_launch(); k_converge<<<1, 256, 0, st>>>(rsq, bnorm, s, tol, stt, hist_slot); }
 }
 
-void small_chol(const double* A, int sp, int mode, int nact, double tau, double* L, double* Linv, double* T,
-                BcgStatus* stt, cudaStream_t st) {
-  const size_t smem = ((size_t)sp * (sp + 1) + (size_t)sp * (sp + 1) / 2) * sizeof(double);
+void small_chol(const double* A, int sp, int mode, int nact, double tau, double* Out, BcgStatus* stt,
+                cudaStream_t st) {
+  const size_t smem = (size_t)(128 * sc::LDA + 16 * 64 + 8 * 64) * sizeof(double);
   set_smem((const void*)k_small_chol, smem);
-  { nsp_count_launch(); k_small_chol<<<1, 1024, smem, st>>>(A, sp, mode, nact, tau, L, Linv, T, stt); }
+  { nsp_count_launch(); k_small_chol<<<1, 256, smem, st>>>(A, sp, mode, nact, tau, Out, stt); }
 }
 
 void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* lam, double* Vsorted,

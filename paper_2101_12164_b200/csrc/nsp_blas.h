@@ -17,6 +17,19 @@ struct BcgStatus {
 
 void nsp_count_launch();
 
+struct PanelArgs {
+  double* Out;
+  int ldo;
+  const double* Cin;
+  int ldc;
+  const double* In;
+  int ldi;
+  const double* M;
+  int ldm;
+  double sgn;
+  double* normpart;
+};
+
 namespace nspb {
 int gram_chunks(int64_t n, int ntiles);
 size_t gram_ws_doubles(int64_t n, int sa, int sb);
@@ -24,6 +37,11 @@ size_t gram_ws_doubles(int64_t n, int sa, int sb);
 void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, int64_t n, double* out, int ldo,
           double* ws, cudaStream_t st);
 // Out = Cin + sgn * In(n x kdim) M(kdim x ncols); ncols multiple of 64, kdim multiple of 32
+// out = Xa^T Xb, out2 = Xa^T Xb2 (shared left operand, one pass)
+void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb2, int ldb, int sb, int64_t n,
+           double* out, double* out2, int ldo, double* ws, cudaStream_t st);
+// two independent panels in one launch (a1 may be null)
+void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64_t n, cudaStream_t st);
 void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
            int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st);
 void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st);
@@ -31,10 +49,11 @@ void colsq_reduce(const double* part, int ntiles, int ldp, double* out, cudaStre
 void sqrt_vec(const double* in, double* out, int n, cudaStream_t st);
 void converge(const double* rsq, const double* bnorm, int s, double tol, BcgStatus* stt, double* hist_slot,
               cudaStream_t st);
-// mode 0: D (pivot <= 0 -> indefinite); mode 1: orth Gram (pivot test -> fallback).
-// nact < 0: active width read from stt->width; rows/cols >= nact are replaced by the identity.
-void small_chol(const double* A, int sp, int mode, int nact, double tau, double* L, double* Linv, double* T,
-                BcgStatus* stt, cudaStream_t st);
+// mode 0: D (pivot <= 0 -> indefinite), Out = D^{-1}; mode 1: orth Gram (pivot test -> fallback),
+// Out = T = R^{-1} with G = R^T R.  nact < 0: active width read from stt->width; rows/cols >= nact
+// are replaced by the identity.  sp <= 128, multiple of 32.
+void small_chol(const double* A, int sp, int mode, int nact, double tau, double* Out, BcgStatus* stt,
+                cudaStream_t st);
 void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* lam, double* Vsorted,
                const int* gate, cudaStream_t st);
 void orth_from_eig(const double* lam, const double* Vs, int n, int sp, double tau, double* T, BcgStatus* stt,

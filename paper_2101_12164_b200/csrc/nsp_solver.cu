@@ -3,7 +3,12 @@
 // drivers enqueueing the device kernels on the context stream.  One small device->host status
 // read per iteration (the convergence / breakdown flags); everything else stays on the device.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <vector>
 #include <cstring>
 #include <string>
 
@@ -11,6 +16,53 @@
 #include "nsp_solver.h"
 
 namespace nspi {
+
+// NSP_TRACE=1: CUDA-event phase timing of block CG, printed to stderr at exit (diagnostics only)
+struct Tracer {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> lab;
+  std::vector<double> host_us;
+  std::chrono::steady_clock::time_point t0;
+  void init(cudaStream_t s) {
+    const char* e = getenv("NSP_TRACE");
+    on = e && e[0] == '1';
+    st = s;
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* l) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+    lab.push_back(l);
+    host_us.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+  }
+  void report() {
+    if (!on || ev.size() < 2) return;
+    cudaStreamSynchronize(st);
+    std::map<std::string, std::pair<double, int>> agg, hagg;
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      auto& a = agg[lab[i]];
+      a.first += ms;
+      a.second++;
+      auto& h = hagg[lab[i]];
+      h.first += host_us[i] - host_us[i - 1];
+      h.second++;
+    }
+    for (auto& kv : agg)
+      fprintf(stderr, "[nsp trace] %-14s gpu %9.3f ms  host %9.3f ms  n=%d\n", kv.first.c_str(), kv.second.first,
+              hagg[kv.first].first / 1000.0, kv.second.second);
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+    lab.clear();
+    host_us.clear();
+  }
+};
 
 struct Carver {
   char* p;
@@ -86,7 +138,7 @@ static void orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Pout) {
   const int64_t n = c->nG;
   cudaStream_t st = c->stream;
   nspb::gram(Wm, sp, sp, Wm, sp, sp, n, w.G, sp, w.gram, st);
-  nspb::small_chol(w.G, sp, 1, s, c->opts.orth_tau, nullptr, nullptr, w.T, w.st, st);
+  nspb::small_chol(w.G, sp, 1, s, c->opts.orth_tau, w.T, w.st, st);
   nspb::small_eig(w.G, sp, s, w.Vw, sp + 1, w.lam, w.Vs, &w.st->fallback, st);
   nspb::orth_from_eig(w.lam, w.Vs, s, sp, c->opts.orth_tau, w.T, w.st, st);
   nspb::panel(Pout, sp, nullptr, 0, Wm, sp, w.T, sp, sp, sp, n, 1.0, nullptr, st);
@@ -104,6 +156,9 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   const bool usem = c->opts.bcg_precond != 0;
   int iters = 0, fallbacks = 0;
   nsp_status ret = NSP_NOT_CONVERGED;
+  Tracer tr;
+  tr.init(st);
+  tr.mark("start");
   // init: X = 0, R = B, bnorm
   NSP_CUDA_TRY(c, cudaMemsetAsync(w.X, 0, (size_t)n * sp * 8, st));
   nspb::copy_pad(B, ldb, w.R, sp, n, s, 1.0, st);
@@ -129,22 +184,30 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     orth(c, w, Zr, s, w.P);
     for (int it = 0; it < maxit; ++it) {
       // a1-a5: Q = S_G P
+      tr.mark("loop");
       if ((e = apply_into(c, w.P, sp, w.Q, sp, s, 1, w.wvu)) != NSP_OK) return e;
+      tr.mark("apply");
       // a6: D = P^T Q, E = P^T R
-      nspb::gram(w.P, sp, sp, w.Q, sp, sp, n, w.D, sp, w.gram, st);
-      nspb::gram(w.P, sp, sp, w.R, sp, sp, n, w.E, sp, w.gram, st);
+      nspb::gram2(w.P, sp, sp, w.Q, w.R, sp, sp, n, w.D, w.E, sp, w.gram, st);
+      tr.mark("gram_DE");
       // a7: chol(D), alpha = D^{-1} E
-      nspb::small_chol(w.D, sp, 0, -1, 0.0, w.Ld, w.Ldi, nullptr, w.st, st);
-      nspb::small_gemm(sp, sp, sp, 1.0, w.Ldi, sp, false, w.E, sp, false, 0.0, w.tmp, sp, st);
-      nspb::small_gemm(sp, sp, sp, 1.0, w.Ldi, sp, true, w.tmp, sp, false, 0.0, w.al, sp, st);
+      nspb::small_chol(w.D, sp, 0, -1, 0.0, w.Ldi, w.st, st);   // Ldi = D^{-1}
+      tr.mark("chol_D");
+      nspb::panel(w.al, sp, nullptr, 0, w.Ldi, sp, w.E, sp, sp, sp, sp, 1.0, nullptr, st);
+      tr.mark("alpha");
       // a8: X += P alpha, R -= Q alpha, column norms
-      nspb::panel(w.X, sp, w.X, sp, w.P, sp, w.al, sp, sp, sp, n, 1.0, nullptr, st);
-      nspb::panel(w.R, sp, w.R, sp, w.Q, sp, w.al, sp, sp, sp, n, -1.0, w.npart, st);
+      {
+        PanelArgs px{w.X, sp, w.X, sp, w.P, sp, w.al, sp, 1.0, nullptr};
+        PanelArgs pr{w.R, sp, w.R, sp, w.Q, sp, w.al, sp, -1.0, w.npart};
+        nspb::panel2(px, &pr, sp, sp, n, st);
+      }
       nspb::colsq_reduce(w.npart, (int)((n + 63) / 64), sp, w.rsq, st);
       double* hslot = nullptr;
       nspb::converge(w.rsq, w.bnorm, s, tol, w.st, hslot, st);
+      tr.mark("XR_update");
       NSP_CUDA_TRY(c, cudaGetLastError());
       if ((e = read_status(c, w.st, hs)) != NSP_OK) return e;
+      tr.mark("sync");
       iters = it + 1;
       fallbacks += hs->fallback;
       relres = hs->relres;
@@ -177,15 +240,19 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
       }
       // a10: F = Q^T Z, beta = -D^{-1} F, W = Z + P beta
       nspb::gram(w.Q, sp, sp, Zr, sp, sp, n, w.F, sp, w.gram, st);
-      nspb::small_gemm(sp, sp, sp, 1.0, w.Ldi, sp, false, w.F, sp, false, 0.0, w.tmp, sp, st);
-      nspb::small_gemm(sp, sp, sp, -1.0, w.Ldi, sp, true, w.tmp, sp, false, 0.0, w.be, sp, st);
+      nspb::panel(w.be, sp, nullptr, 0, w.Ldi, sp, w.F, sp, sp, sp, sp, -1.0, nullptr, st);
+      tr.mark("beta");
       nspb::panel(w.W, sp, Zr, sp, w.P, sp, w.be, sp, sp, sp, n, 1.0, nullptr, st);
+      tr.mark("W");
       // a11: P = orth(W)
       orth(c, w, w.W, s, w.P);
+      tr.mark("orth");
     }
   }
   // copy X out
   nspb::copy_pad(w.X, sp, Xout, ldx, n, s, 1.0, st);
+  tr.mark("end");
+  tr.report();
   NSP_CUDA_TRY(c, cudaStreamSynchronize(st));
   NSP_CUDA_TRY(c, cudaGetLastError());
   if (rep) {
