@@ -162,6 +162,10 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_band);
   fr(c->d_dense);
   fr(c->d_border_first);
+  fr(c->d_gband);
+  fr(c->d_gsys);
+  fr(c->d_gperm);
+  fr(c->d_gperm_inv);
   for (DevCSR* m : {&c->A2G, &c->AGG2}) {
     fr(m->rowptr);
     fr(m->col);

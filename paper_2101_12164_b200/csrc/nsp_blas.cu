@@ -401,6 +401,14 @@ __global__ void __launch_bounds__(256) k_small_chol(const double* __restrict__ A
       st->width = width;
     }
   }
+  if (mode == 2) {  // R = L^T (upper), G = R^T R
+    if (tid == 0) st->fallback = 0;
+    for (int e = tid; e < sp * sp; e += 256) {
+      const int p = e / sp, q = e - p * sp;
+      Out[e] = (q >= p) ? As[q * LDA + p] : 0.0;
+    }
+    return;
+  }
   // ============================ X = L^{-1}, block row by block row:
   // X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ  (J < I);  stored transposed: As[8J + c][8I + r] = X_IJ[r][c]
   double* scr = Sc + warp * 64;
@@ -626,6 +634,34 @@ __global__ void k_small_gemm(int m, int n, int k, double alpha, const double* A,
   Cm[i * ldc + j] = alpha * s + (beta != 0.0 ? beta * Cm[i * ldc + j] : 0.0);
 }
 
+// A <- (A + A^T) / 2 (n x n, ld), plus shift on the diagonal
+__global__ void k_small_sym(double* A, int n, int ld, double shift) {
+  const int i = blockIdx.y * 16 + threadIdx.y, j = blockIdx.x * 16 + threadIdx.x;
+  if (i >= n || j > i) return;
+  const double v = 0.5 * (A[i * ld + j] + A[j * ld + i]);
+  A[i * ld + j] = v + (i == j ? shift : 0.0);
+  A[j * ld + i] = v + (i == j ? shift : 0.0);
+}
+// M[i][k] = V[i][k] * colscale[k] for k < r, 0 for k >= r (n rows, ld)
+__global__ void k_scale_cols(const double* V, int ldv, const double* colscale, int r, int n, int ncols, double* M,
+                             int ldm, int mode) {
+  const int i = blockIdx.y * 16 + threadIdx.y, k = blockIdx.x * 16 + threadIdx.x;
+  if (i >= n || k >= ncols) return;
+  double v = 0.0;
+  if (k < r) {
+    const double sc = colscale[k];
+    v = mode == 3 ? V[i * ldv + k] : V[i * ldv + k] * (mode == 0 ? sc : (mode == 1 ? 1.0 / sqrt(sc) : sqrt(sc)));
+  }
+  M[i * ldm + k] = v;
+}
+
+// rows i < r scaled by d[i], rows r <= i < nrows zeroed
+__global__ void k_scale_rows(double* G, int ld, const double* d, int r, int nrows, int ncols) {
+  const int i = blockIdx.y * 16 + threadIdx.y, j = blockIdx.x * 16 + threadIdx.x;
+  if (i >= nrows || j >= ncols) return;
+  G[i * ld + j] = i < r ? G[i * ld + j] * d[i] : 0.0;
+}
+
 // copy with ld change and zero padding: dst[r][c] = c < s ? src[r][c] : 0 (c < ldd)
 __global__ void k_copy_pad(const double* src, int lds, double* dst, int ldd, int64_t n, int s, double scale) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -744,6 +780,22 @@ void copy_pad(const double* src, int lds, double* dst, int ldd, int64_t n, int s
   const int64_t tot = n * ldd;
   if (tot <= 0) return;
   { nsp_count_launch(); k_copy_pad<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, lds, dst, ldd, n, s, scale); }
+}
+
+void scale_rows(double* G, int ld, const double* d, int r, int nrows, int ncols, cudaStream_t st) {
+  dim3 grid((ncols + 15) / 16, (nrows + 15) / 16);
+  { nsp_count_launch(); k_scale_rows<<<grid, dim3(16, 16), 0, st>>>(G, ld, d, r, nrows, ncols); }
+}
+
+void small_sym(double* A, int n, int ld, double shift, cudaStream_t st) {
+  dim3 grid((n + 15) / 16, (n + 15) / 16);
+  { nsp_count_launch(); k_small_sym<<<grid, dim3(16, 16), 0, st>>>(A, n, ld, shift); }
+}
+
+void scale_cols(const double* V, int ldv, const double* colscale, int r, int n, int ncols, double* M, int ldm,
+                int mode, cudaStream_t st) {
+  dim3 grid((ncols + 15) / 16, (n + 15) / 16);
+  { nsp_count_launch(); k_scale_cols<<<grid, dim3(16, 16), 0, st>>>(V, ldv, colscale, r, n, ncols, M, ldm, mode); }
 }
 
 }  // namespace nspb

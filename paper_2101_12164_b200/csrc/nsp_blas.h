@@ -50,7 +50,7 @@ void sqrt_vec(const double* in, double* out, int n, cudaStream_t st);
 void converge(const double* rsq, const double* bnorm, int s, double tol, BcgStatus* stt, double* hist_slot,
               cudaStream_t st);
 // mode 0: D (pivot <= 0 -> indefinite), Out = D^{-1}; mode 1: orth Gram (pivot test -> fallback),
-// Out = T = R^{-1} with G = R^T R.  nact < 0: active width read from stt->width; rows/cols >= nact
+// Out = T = R^{-1} with G = R^T R; mode 2: Out = R (upper), pivot <= 0 -> fallback.  nact < 0: active width read from stt->width; rows/cols >= nact
 // are replaced by the identity.  sp <= 128, multiple of 32.
 void small_chol(const double* A, int sp, int mode, int nact, double tau, double* Out, BcgStatus* stt,
                 cudaStream_t st);
@@ -60,5 +60,10 @@ void orth_from_eig(const double* lam, const double* Vs, int n, int sp, double ta
                    cudaStream_t st);
 void small_gemm(int m, int n, int k, double alpha, const double* A, int lda, bool ta, const double* B, int ldb,
                 bool tb, double beta, double* C, int ldc, cudaStream_t st);
+void scale_rows(double* G, int ld, const double* d, int r, int nrows, int ncols, cudaStream_t st);
+void small_sym(double* A, int n, int ld, double shift, cudaStream_t st);
+// M[:, k] = V[:, k] * f(colscale[k]) for k < r (f: mode 0 x, 1 1/sqrt(x), 2 sqrt(x), 3 copy), zero for r <= k < ncols
+void scale_cols(const double* V, int ldv, const double* colscale, int r, int n, int ncols, double* M, int ldm,
+                int mode, cudaStream_t st);
 void copy_pad(const double* src, int lds, double* dst, int ldd, int64_t n, int s, double scale, cudaStream_t st);
 }  // namespace nspb

@@ -29,6 +29,14 @@ struct FacSub {
   int status_idx;        // index into the factor status array
 };
 
+// A batched triangular system for k_tri_fb: tiles at T (dense lower if wb < 0, else band of
+// half-width wb tiles), nt tile rows, rows row0.. of the right-hand-side buffer.
+struct TriSys {
+  const double* T;
+  int nt, wb;
+  int64_t row0;
+};
+
 struct DevCSR {   // device CSR with int32 row pointers (nnz < 2^31 checked)
   int64_t rows = 0, nnz = 0;
   int32_t* rowptr = nullptr;
@@ -67,6 +75,19 @@ struct nsp_ctx {
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
 
+  // A_G factor (band, RCM order): rows of the band buffer -> local Gamma index (-1 = padding)
+  bool has_ag = false;
+  double* d_gband = nullptr;  int64_t gband_tiles = 0;
+  TriSys* d_gsys = nullptr;   int g_nt = 0, g_wb = 0;
+  int32_t* d_gperm = nullptr;     // band row -> Gamma row (size g_nt*64)
+  int32_t* d_gperm_inv = nullptr; // Gamma row -> band row
+
+  // Nystrom-Schur M_2 = A_G^{-1} + Z Sigma Z^T (Alg. 2 steps 11-12)
+  double* d_Z = nullptr;          // nG x nys_ld
+  double* d_sigma = nullptr;      // nys_ld
+  int nys_rank = -1, nys_ld = 0;
+  std::vector<double> h_sigma;
+
   // statistics
   int64_t n_I = 0, n_bl = 0, nnz_AG = 0, nnz_AGI = 0, max_b = 0, ag_bw = 0;
 
@@ -99,6 +120,11 @@ void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, i
           double* Y, int ldy, int s, int mode, bool zero_pad, cudaStream_t st);
 void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw,
              cudaStream_t st);
+void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st);
+void gather_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,
+                 double scale, cudaStream_t st);
+void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,
+                  bool accumulate, cudaStream_t st);
 }  // namespace nspk
 
 #define NSP_CUDA_TRY(ctx, call)                                                   \

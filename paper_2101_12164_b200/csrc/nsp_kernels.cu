@@ -389,6 +389,162 @@ __global__ void __launch_bounds__(256) k_trsm_fb(const FacSub* __restrict__ subs
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Generic batched forward + backward triangular solves on tiled factors (one system per blockIdx.x,
+// column chunks on blockIdx.y): dense lower tiles (wb < 0: tile(I,J) = T + I(I+1)/2 + J) or band
+// tiles (tile(I,J) = T + J(wb+1) + (I-J), 0 <= I-J <= wb).  Used for A_G^{-1} (band) and for the
+// interior blocks A_11 (band) of the full A_I solves; diagonal tiles hold inv(L_II).
+// ---------------------------------------------------------------------------------------------
+template <int CW>
+__global__ void __launch_bounds__(256) k_tri_fb(const TriSys* __restrict__ sys, double* buf, int ldw, int fwd,
+                                                int bwd) {
+  constexpr int NF = CW / 16;
+  constexpr int LDV = CW + 4;
+  extern __shared__ double sm[];
+  double* Ls0 = sm;
+  double* Ls1 = sm + 64 * LDT;
+  double* Vs0 = sm + 2 * 64 * LDT;
+  double* Vs1 = Vs0 + 64 * LDV;
+  const TriSys sy = sys[blockIdx.x];
+  const int nt = sy.nt, wb = sy.wb;
+  if (nt == 0) return;
+  const int c0 = blockIdx.y * CW;
+  const double* T = sy.T;
+  double* Wb = buf + sy.row0 * (int64_t)ldw + c0;
+  auto tile = [&](int I, int J) -> const double* {
+    return wb < 0 ? T + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS
+                  : T + ((int64_t)J * (wb + 1) + (I - J)) * NSP_TILE_ELEMS;
+  };
+  double acc[2][NF][2];
+  if (fwd)
+    for (int I = 0; I < nt; ++I) {
+      acc_zero(acc);
+      const int jlo = wb < 0 ? 0 : max(0, I - wb);
+      if (I > jlo) {
+        cp_block(Ls0, LDT, tile(I, jlo), 64, 64, 64);
+        cp_block(Vs0, LDV, Wb + (int64_t)jlo * 64 * ldw, ldw, 64, CW);
+        cp_commit();
+        for (int J = jlo, it = 0; J < I; ++J, ++it) {
+          double* Lc = (it & 1) ? Ls1 : Ls0;
+          double* Vc = (it & 1) ? Vs1 : Vs0;
+          if (J + 1 < I) {
+            cp_block((it & 1) ? Ls0 : Ls1, LDT, tile(I, J + 1), 64, 64, 64);
+            cp_block((it & 1) ? Vs0 : Vs1, LDV, Wb + (int64_t)(J + 1) * 64 * ldw, ldw, 64, CW);
+            cp_commit();
+            cp_wait<1>();
+          } else {
+            cp_wait<0>();
+          }
+          __syncthreads();
+          cta_mma<NF, false, false>(Lc, LDT, Vc, LDV, acc);
+          __syncthreads();
+        }
+      }
+      cp_block(Ls0, LDT, tile(I, I), 64, 64, 64);
+      cp_block(Vs0, LDV, Wb + (int64_t)I * 64 * ldw, ldw, 64, CW);
+      cp_commit();
+      cp_wait<0>();
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+          Vs1[r * LDV + c] = Vs0[r * LDV + c] - acc[i][j][0];
+          Vs1[r * LDV + c + 1] = Vs0[r * LDV + c + 1] - acc[i][j][1];
+        }
+      __syncthreads();
+      acc_zero(acc);
+      cta_mma<NF, false, false>(Ls0, LDT, Vs1, LDV, acc);
+      double* out = Wb + (int64_t)I * 64 * ldw;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+          *reinterpret_cast<double2*>(out + (int64_t)r * ldw + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+        }
+      __threadfence();
+      __syncthreads();
+    }
+  if (bwd)
+    for (int I = nt - 1; I >= 0; --I) {
+      acc_zero(acc);
+      const int jhi = wb < 0 ? nt - 1 : min(nt - 1, I + wb);
+      if (I < jhi) {
+        cp_block(Ls0, LDT, tile(I + 1, I), 64, 64, 64);
+        cp_block(Vs0, LDV, Wb + (int64_t)(I + 1) * 64 * ldw, ldw, 64, CW);
+        cp_commit();
+        int it = 0;
+        for (int J = I + 1; J <= jhi; ++J, ++it) {
+          double* Lc = (it & 1) ? Ls1 : Ls0;
+          double* Vc = (it & 1) ? Vs1 : Vs0;
+          if (J + 1 <= jhi) {
+            cp_block((it & 1) ? Ls0 : Ls1, LDT, tile(J + 1, I), 64, 64, 64);
+            cp_block((it & 1) ? Vs0 : Vs1, LDV, Wb + (int64_t)(J + 1) * 64 * ldw, ldw, 64, CW);
+            cp_commit();
+            cp_wait<1>();
+          } else {
+            cp_wait<0>();
+          }
+          __syncthreads();
+          cta_mma<NF, true, false>(Lc, LDT, Vc, LDV, acc);
+          __syncthreads();
+        }
+      }
+      cp_block(Ls0, LDT, tile(I, I), 64, 64, 64);
+      cp_block(Vs0, LDV, Wb + (int64_t)I * 64 * ldw, ldw, 64, CW);
+      cp_commit();
+      cp_wait<0>();
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+          Vs1[r * LDV + c] = Vs0[r * LDV + c] - acc[i][j][0];
+          Vs1[r * LDV + c + 1] = Vs0[r * LDV + c + 1] - acc[i][j][1];
+        }
+      __syncthreads();
+      acc_zero(acc);
+      cta_mma<NF, true, false>(Ls0, LDT, Vs1, LDV, acc);
+      double* out = Wb + (int64_t)I * 64 * ldw;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+          *reinterpret_cast<double2*>(out + (int64_t)r * ldw + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+        }
+      __threadfence();
+      __syncthreads();
+    }
+}
+
+// row gather / scatter between an n x s block (ld lds) and a padded buffer (ld ldd):
+// gather: dst[r][c] = idx[r] >= 0 && c < s ? scale * src[idx[r]][c] : 0  for r < rows, c < ldd
+// scatter: dst[idx[r]][c] = src[r][c]   (c < s, idx[r] >= 0)
+__global__ void k_gather_rows(const double* __restrict__ src, int lds, const int32_t* __restrict__ idx, int64_t rows,
+                              double* dst, int ldd, int s, double scale) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r = e / ldd;
+  const int c = (int)(e - r * ldd);
+  if (r >= rows) return;
+  const int32_t k = idx[r];
+  dst[r * ldd + c] = (k >= 0 && c < s) ? scale * src[(int64_t)k * lds + c] : 0.0;
+}
+__global__ void k_scatter_rows(const double* __restrict__ src, int lds, const int32_t* __restrict__ idx, int64_t rows,
+                               double* dst, int ldd, int s, int accumulate) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r = e / s;
+  const int c = (int)(e - r * s);
+  if (r >= rows) return;
+  const int32_t k = idx[r];
+  if (k < 0) return;
+  if (accumulate) dst[(int64_t)k * ldd + c] += src[r * lds + c];
+  else dst[(int64_t)k * ldd + c] = src[r * lds + c];
+}
+
 }  // namespace
 
 namespace nspk {
@@ -427,6 +583,34 @@ void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, i
     { nsp_count_launch(); k_spmm<4><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
   else
     { nsp_count_launch(); k_spmm<8><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
+}
+
+void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st) {
+  if (nsys <= 0) return;
+  dim3 grid(nsys, ldw / cw);
+  if (cw == 64) {
+    const size_t smem = (2 * 64 * LDT + 2 * 64 * (64 + 4)) * sizeof(double);
+    cudaFuncSetAttribute(k_tri_fb<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    { nsp_count_launch(); k_tri_fb<64><<<grid, 256, smem, st>>>(sys, buf, ldw, fwd, bwd); }
+  } else {
+    const size_t smem = (2 * 64 * LDT + 2 * 64 * (32 + 4)) * sizeof(double);
+    cudaFuncSetAttribute(k_tri_fb<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    { nsp_count_launch(); k_tri_fb<32><<<grid, 256, smem, st>>>(sys, buf, ldw, fwd, bwd); }
+  }
+}
+
+void gather_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,
+                 double scale, cudaStream_t st) {
+  const int64_t tot = rows * ldd;
+  if (tot <= 0) return;
+  { nsp_count_launch(); k_gather_rows<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, lds, idx, rows, dst, ldd, s, scale); }
+}
+
+void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,
+                  bool accumulate, cudaStream_t st) {
+  const int64_t tot = rows * s;
+  if (tot <= 0) return;
+  { nsp_count_launch(); k_scatter_rows<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, lds, idx, rows, dst, ldd, s, accumulate); }
 }
 
 void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw, cudaStream_t st) {

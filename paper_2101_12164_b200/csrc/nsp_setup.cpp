@@ -166,6 +166,125 @@ static nsp_status fail(nsp_ctx* c, nsp_status st, const std::string& msg) {
 
 nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K, nsp_report* rep);
 
+// Cholesky factor of A_G (eq:cholesky) for the first-level preconditioner
+// S~_1^{-1} = A_G^{-1} (eq:S1) and M_2: RCM band ordering of the Gamma graph, band tiles, the same
+// GPU tile-Cholesky kernel as the blocks (a band-only block).
+static nsp_status setup_gamma_factor(nsp_ctx* c, const nsp_csr* A, const int32_t* part,
+                                     const std::vector<int32_t>& gpos, nsp_report* rep) {
+  const int64_t nG = c->nG;
+  if (nG == 0) return NSP_OK;
+  if (nG > INT32_MAX) return fail(c, NSP_ERR_ARG, "A_G too large");
+  const int64_t* rp = A->rowptr;
+  const int32_t* ci = A->colidx;
+  const double* va = A->val;
+  std::vector<int> arp(nG + 1, 0), aci;
+  for (int64_t g = 0; g < nG; ++g) {
+    const int64_t v = c->gamma[g];
+    for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
+      const int64_t u = ci[q];
+      if (u != v && part[u] < 0 && va[q] != 0.0) aci.push_back(gpos[u]);
+    }
+    arp[g + 1] = (int)aci.size();
+  }
+  std::vector<int> ord = rcm_order((int)nG, arp, aci);
+  std::vector<int> pos(nG);
+  for (int64_t k = 0; k < nG; ++k) pos[ord[k]] = (int)k;
+  const int bw = bandwidth((int)nG, arp, aci, pos);
+  c->ag_bw = bw;
+  const int nt = (int)((nG + NSP_TILE - 1) / NSP_TILE);
+  const int wb = std::min(nt - 1, (bw + NSP_TILE - 1) / NSP_TILE);
+  const int64_t tiles = (int64_t)nt * (wb + 1);
+  size_t free_b = 0, total_b = 0;
+  NSP_CUDA_TRY(c, cudaMemGetInfo(&free_b, &total_b));
+  if ((double)tiles * NSP_TILE_ELEMS * 8 > 0.4 * (double)free_b)
+    return fail(c, NSP_ERR_OOM, "nsp_setup: A_G band factor (RCM bandwidth " + std::to_string(bw) +
+                                    ") exceeds the device budget");
+  std::vector<int64_t> idx;
+  std::vector<double> val;
+  for (int64_t g = 0; g < nG; ++g) {
+    const int64_t v = c->gamma[g];
+    const int li = pos[g];
+    for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
+      const int64_t u = ci[q];
+      if (part[u] >= 0) continue;
+      const int lj = pos[gpos[u]];
+      if (lj > li) continue;
+      const int I = li / NSP_TILE, Kt = lj / NSP_TILE;
+      idx.push_back(((int64_t)Kt * (wb + 1) + (I - Kt)) * NSP_TILE_ELEMS + (li % NSP_TILE) * NSP_TILE + lj % NSP_TILE);
+      val.push_back(va[q]);
+    }
+  }
+  NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_gband, (size_t)tiles * NSP_TILE_ELEMS * 8));
+  NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_gband, 0, (size_t)tiles * NSP_TILE_ELEMS * 8, c->stream));
+  c->gband_tiles = tiles;
+  int64_t* d_idx = nullptr;
+  double* d_val = nullptr;
+  nsp_status st;
+  if ((st = upload(c, &d_idx, idx)) != NSP_OK) return st;
+  if ((st = upload(c, &d_val, val)) != NSP_OK) return st;
+  nspk::scatter(c->d_gband, d_idx, d_val, (int64_t)idx.size(), c->stream);
+  if (nG % NSP_TILE) {
+    std::vector<int64_t> ti{(int64_t)(nt - 1) * (wb + 1)};
+    std::vector<int> fr{(int)(nG % NSP_TILE)};
+    int64_t* d_t = nullptr;
+    int* d_f = nullptr;
+    if ((st = upload(c, &d_t, ti)) != NSP_OK) return st;
+    if ((st = upload(c, &d_f, fr)) != NSP_OK) return st;
+    nspk::set_pad_identity(c->d_gband, d_t, d_f, 1, c->stream);
+    NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    cudaFree(d_t);
+    cudaFree(d_f);
+  }
+  FacSub F{};
+  F.nt1 = nt;
+  F.ntb = 0;
+  F.wb = wb;
+  F.n1 = (int)nG;
+  F.status_idx = 0;
+  std::vector<FacSub> fv{F};
+  std::vector<int> bf{0};
+  FacSub* d_f = nullptr;
+  int* d_bf = nullptr;
+  int* d_stat = nullptr;
+  if ((st = upload(c, &d_f, fv)) != NSP_OK) return st;
+  if ((st = upload(c, &d_bf, bf)) != NSP_OK) return st;
+  NSP_CUDA_TRY(c, cudaMalloc((void**)&d_stat, sizeof(int)));
+  NSP_CUDA_TRY(c, cudaMemsetAsync(d_stat, 0, sizeof(int), c->stream));
+  nspk::tile_cholesky(d_f, 1, c->d_gband, nullptr, nullptr, d_bf, d_stat, c->stream);
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  int hstat = 0;
+  NSP_CUDA_TRY(c, cudaMemcpyAsync(&hstat, d_stat, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d_idx);
+  cudaFree(d_val);
+  cudaFree(d_f);
+  cudaFree(d_bf);
+  cudaFree(d_stat);
+  if (hstat != 0) {
+    const int r = hstat - 1;
+    const int64_t orig = r < nG ? c->gamma[ord[r]] : -1;
+    if (rep) {
+      rep->bad_block = -1;
+      rep->bad_pivot = orig;
+      rep->status = NSP_ERR_NOT_SPD;
+    }
+    return fail(c, NSP_ERR_NOT_SPD, "nsp_setup: A_G not SPD (pivot at node " + std::to_string(orig) + ")");
+  }
+  std::vector<int32_t> gp((size_t)nt * NSP_TILE, -1), gpi(nG);
+  for (int64_t g = 0; g < nG; ++g) {
+    gp[pos[g]] = (int32_t)g;
+    gpi[g] = pos[g];
+  }
+  if ((st = upload(c, &c->d_gperm, gp)) != NSP_OK) return st;
+  if ((st = upload(c, &c->d_gperm_inv, gpi)) != NSP_OK) return st;
+  std::vector<TriSys> ts{TriSys{c->d_gband, nt, wb, 0}};
+  if ((st = upload(c, &c->d_gsys, ts)) != NSP_OK) return st;
+  c->g_nt = nt;
+  c->g_wb = wb;
+  c->has_ag = true;
+  return NSP_OK;
+}
+
 extern "C" nsp_status nsp_setup(const nsp_csr* A, const int32_t* part, int K, const nsp_opts* opts,
                                 nsp_ctx** out, nsp_report* rep) {
   if (!out) return NSP_ERR_ARG;
@@ -634,8 +753,16 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       return fail(c, NSP_ERR_NOT_SPD, "nsp_setup: A_I_" + std::to_string(j) + " not SPD (pivot at node " +
                                           std::to_string(orig) + ")");
     }
+  double t_ag = 0.0;
+  if (c->opts.factor_gamma) {
+    auto t3 = Clock::now();
+    nsp_status sg = setup_gamma_factor(c, A, part, gpos, rep);
+    if (sg != NSP_OK) return sg;
+    t_ag = ms_since(t3);
+  }
   if (rep) {
     rep->status = NSP_OK;
+    rep->t_ms[3] = t_ag;
     rep->t_ms[0] = t_host;
     rep->t_ms[1] = t_h2d;
     rep->t_ms[2] = t_fac;

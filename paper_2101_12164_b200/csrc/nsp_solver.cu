@@ -84,6 +84,7 @@ struct BcgWs {
 };
 
 static int sp_of(int s) { return ((s + 63) / 64) * 64; }
+size_t ag_ws_doubles(const nsp_ctx* c, int s);
 
 static size_t bcg_layout(const nsp_ctx* c, int s, char* base, BcgWs* w) {
   const int sp = sp_of(s);
@@ -116,7 +117,7 @@ static size_t bcg_layout(const nsp_ctx* c, int s, char* base, BcgWs* w) {
   t.rsq = cv.take(sp);
   t.gram = cv.take(nspb::gram_ws_doubles(n, sp, sp));
   t.npart = cv.take((size_t)((n + 63) / 64 + 1) * sp);
-  t.wvu = cv.take(apply_ws_bytes(c, sp) / 8 + 1);
+  t.wvu = cv.take(std::max(apply_ws_bytes(c, sp) / 8 + 1, c->has_ag ? ag_ws_doubles(c, sp) : 0));
   t.st = (BcgStatus*)cv.take(sizeof(BcgStatus) / 8 + 1);
   if (w) *w = t;
   return cv.off + 256;
@@ -178,6 +179,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   } else {
     double* Zr = w.R;
     if (usem) {
+      NSP_CUDA_TRY(c, cudaMemsetAsync(w.Z, 0, (size_t)n * sp * 8, st));
       if ((e = precond(c, w.R, w.Z, sp, s, w.wvu)) != NSP_OK) return e;
       Zr = w.Z;
     }
@@ -265,14 +267,46 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   return ret;
 }
 
-static nsp_status precond(nsp_ctx* c, const double* R, double* Z, int ld, int s, double* wvu) {
-  (void)R;
-  (void)Z;
-  (void)ld;
-  (void)s;
-  (void)wvu;
-  c->err = "block-CG preconditioner A_G^{-1} requires the A_G factor (not built)";
-  return NSP_ERR_STATE;
+// ---------------------------------------------------------------------------------------------
+// A_G^{-1} X (eq:S1): rows gathered into RCM band order, band forward + backward sweeps, scattered
+// back.  buf: g_nt*64 x ld_pad(s, 32) doubles.
+// ---------------------------------------------------------------------------------------------
+size_t ag_ws_doubles(const nsp_ctx* c, int s) { return (size_t)c->g_nt * 64 * ld_pad(s, 32) + 64; }
+
+nsp_status ag_solve(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, double* buf) {
+  if (!c->has_ag) {
+    c->err = "A_G^{-1} needs the A_G factor: set opts.factor_gamma = 1";
+    return NSP_ERR_STATE;
+  }
+  const int ldw = ld_pad(s, 32);
+  const int64_t rows = (int64_t)c->g_nt * 64;
+  nspk::gather_rows(X, ldx, c->d_gperm, rows, buf, ldw, s, 1.0, c->stream);
+  nspk::tri_fb(c->d_gsys, 1, buf, ldw, 32, true, true, c->stream);
+  nspk::scatter_rows(buf, ldw, c->d_gperm, rows, Y, ldy, s, false, c->stream);
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  return NSP_OK;
+}
+
+// Y = M_2 X = A_G^{-1} X + Z (Sigma (Z^T X))   (Alg. 2 step 12, eq:left_prec_mat)
+// ws: ag_ws + 2 * 64*64... small buffers carved by the caller
+nsp_status m2_apply(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, double* buf, double* gsm,
+                    double* gws) {
+  nsp_status e = ag_solve(c, X, ldx, Y, ldy, s, buf);
+  if (e != NSP_OK) return e;
+  if (c->nys_rank > 0) {
+    // G = Z^T X (nys_ld x sp), G <- diag(sigma) G, Y += Z G
+    const int sp = ((s + 63) / 64) * 64;
+    nspb::gram(c->d_Z, c->nys_ld, c->nys_ld, X, ldx, sp, c->nG, gsm, sp, gws, c->stream);
+    nspb::scale_rows(gsm, sp, c->d_sigma, c->nys_rank, c->nys_ld, sp, c->stream);
+    PanelArgs pa{Y, ldy, Y, ldy, c->d_Z, c->nys_ld, gsm, sp, 1.0, nullptr};
+    nspb::panel2(pa, nullptr, c->nys_ld, sp, c->nG, c->stream);
+  }
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  return NSP_OK;
+}
+
+static nsp_status precond(nsp_ctx* c, const double* R, double* Z, int ld, int s, double* buf) {
+  return ag_solve(c, R, ld, Z, ld, s, buf);
 }
 
 }  // namespace nspi
@@ -295,11 +329,213 @@ nsp_status nsp_block_cg(nsp_ctx* c, const double* B, double* X, int s, double to
   return block_cg_impl(c, B, s, X, s, s, tol, maxit, w, rep);
 }
 
-nsp_status nsp_nystrom(nsp_ctx* c, int, int, const double*, double, int, void*, nsp_report*) {
-  if (c) c->err = "nsp_nystrom: not built";
-  return NSP_ERR_STATE;
+// Alg. 2 with readings C1 (border system), C5 (U~ = Q W), C6 (symmetrised C,
+// eps split, descending T eigenpairs, rank = min(r, k)).
+nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega, double tol_inner, int maxit_inner,
+                       void* ws, nsp_report* rep) {
+  const int s = rank + oversample;
+  if (!c || !Omega || rank <= 0 || oversample < 0 || s > 128 || maxit_inner < 0) {
+    if (c) c->err = "nsp_nystrom: bad arguments (rank > 0, rank + oversample <= 128)";
+    return NSP_ERR_ARG;
+  }
+  if (!c->has_ag) {
+    c->err = "nsp_nystrom: M_2 needs the A_G factor (opts.factor_gamma = 1)";
+    return NSP_ERR_STATE;
+  }
+  const int sp = sp_of(s);
+  const int64_t n = c->nG;
+  cudaStream_t st = c->stream;
+  const size_t blk = (size_t)std::max<int64_t>(n, 1) * sp, sm = (size_t)sp * sp;
+  const size_t bcg_bytes = bcg_layout(c, s, nullptr, nullptr);
+  const size_t extra = (6 * blk + 16 * sm + 8 * sp + (size_t)(sp + 1) * (sp + 1)) * 8 + 64 * 256;
+  char* base;
+  nsp_status e = get_ws(c, ws, bcg_bytes + extra, &base);
+  if (e != NSP_OK) return e;
+  BcgWs w;
+  bcg_layout(c, s, base, &w);
+  Carver cv(base + bcg_bytes);
+  double* Om = cv.take(blk);
+  double* Bn = cv.take(blk);
+  double* Xn = cv.take(blk);
+  double* Y = cv.take(blk);
+  double* Qa = cv.take(blk);
+  double* Qb = cv.take(blk);
+  double* G = cv.take(sm);
+  double* Rk = cv.take(sm);
+  double* Tk = cv.take(sm);
+  double* Racc = cv.take(sm);
+  double* Rtmp = cv.take(sm);
+  double* C = cv.take(sm);
+  double* VC = cv.take(sm);
+  double* Vsc = cv.take(sm);
+  double* M1 = cv.take(sm);
+  double* Tm = cv.take(sm);
+  double* VT = cv.take(sm);
+  double* Wc = cv.take(sm);
+  double* Vw = cv.take((size_t)(sp + 1) * (sp + 1));
+  double* lamC = cv.take(sp);
+  double* lamT = cv.take(sp);
+  BcgStatus* hs = (BcgStatus*)c->h_status;
+  // steps 1-2: B = K_G Omega  (reading C1)
+  nspb::copy_pad(Omega, s, Om, sp, n, s, 1.0, st);
+  if ((e = apply_into(c, Om, sp, Bn, sp, s, 2, w.wvu)) != NSP_OK) return e;
+  // step 3: S_G X = B by breakdown-free block CG to tol_inner
+  nsp_report brep{};
+  if (rep) {
+    brep.hist = rep->hist;
+    brep.hist_cap = rep->hist_cap;
+    brep.widths = rep->widths;
+    brep.widths_cap = rep->widths_cap;
+  }
+  nsp_status sb = block_cg_impl(c, Bn, sp, Xn, sp, s, tol_inner, maxit_inner, w, &brep);
+  if (sb < 0) return sb;
+  // step 4: Y = A_G X
+  nspk::spmm(c->AGG2, Xn, sp, nullptr, 0, n, Y, sp, s, 3, true, st);
+  // step 5: Y = Q R by Cholesky-QR2 (shifted Cholesky-QR3 when the first Gram is numerically singular)
+  NSP_CUDA_TRY(c, cudaMemsetAsync(Racc, 0, sm * 8, st));
+  const double* Qin = Y;
+  double* Qout = Qa;
+  int passes = 2;
+  for (int pass = 0; pass < passes; ++pass) {
+    nspb::gram(Qin, sp, sp, Qin, sp, sp, n, G, sp, w.gram, st);
+    nspb::small_chol(G, sp, 2, s, 0.0, Rk, w.st, st);
+    if (pass == 0) {
+      if ((e = read_status(c, w.st, hs)) != NSP_OK) return e;
+      if (hs->fallback) {  // shift = 11 (n s + s(s+1)) u ||Y||_F^2 (shifted CholeskyQR)
+        std::vector<double> gd(sm);
+        NSP_CUDA_TRY(c, cudaMemcpy(gd.data(), G, sm * 8, cudaMemcpyDeviceToHost));
+        double tr = 0.0;
+        for (int i = 0; i < s; ++i) tr += gd[(size_t)i * sp + i];
+        const double shift = 11.0 * ((double)n * s + (double)s * (s + 1)) * 1.1102230246251565e-16 * tr;
+        nspb::small_sym(G, s, sp, shift, st);
+        nspb::small_chol(G, sp, 2, s, 0.0, Rk, w.st, st);
+        passes = 3;
+      }
+    }
+    nspb::small_chol(G, sp, 1, s, 0.0, Tk, w.st, st);      // T = R^{-1}
+    PanelArgs pa{Qout, sp, nullptr, 0, Qin, sp, Tk, sp, 1.0, nullptr};
+    nspb::panel2(pa, nullptr, sp, sp, n, st);
+    if (pass == 0) {
+      NSP_CUDA_TRY(c, cudaMemcpyAsync(Racc, Rk, sm * 8, cudaMemcpyDeviceToDevice, st));
+    } else {
+      nspb::small_gemm(s, s, s, 1.0, Rk, sp, false, Racc, sp, false, 0.0, Rtmp, sp, st);
+      NSP_CUDA_TRY(c, cudaMemcpyAsync(Racc, Rtmp, sm * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    Qin = Qout;
+    Qout = (Qout == Qa) ? Qb : Qa;
+  }
+  const double* Q = Qin;
+  if ((e = read_status(c, w.st, hs)) != NSP_OK) return e;
+  if (hs->fallback) {
+    c->err = "nsp_nystrom: Cholesky-QR of Y failed";
+    return NSP_ERR_NUMERICAL;
+  }
+  // step 6: C = Omega^T Y, symmetrised (reading C6)
+  nspb::gram(Om, sp, sp, Y, sp, sp, n, C, sp, w.gram, st);
+  nspb::small_sym(C, s, sp, 0.0, st);
+  // step 7: EVD of C, split at eps = nys_eps_rel * lambda_max
+  nspb::small_eig(C, sp, s, Vw, sp + 1, lamC, VC, nullptr, st);
+  std::vector<double> hl(s);
+  NSP_CUDA_TRY(c, cudaMemcpyAsync(hl.data(), lamC, s * 8, cudaMemcpyDeviceToHost, st));
+  NSP_CUDA_TRY(c, cudaStreamSynchronize(st));
+  int r = 0;
+  if (hl[0] > 0.0)
+    for (int i = 0; i < s; ++i)
+      if (hl[i] >= c->opts.nys_eps_rel * hl[0]) ++r;
+  const int rk = std::min(r, rank);
+  // release any previous approximation
+  if (c->d_Z) cudaFree(c->d_Z);
+  if (c->d_sigma) cudaFree(c->d_sigma);
+  c->d_Z = nullptr;
+  c->d_sigma = nullptr;
+  c->nys_rank = 0;
+  c->h_sigma.clear();
+  nsp_status ret = sb == NSP_NOT_CONVERGED ? NSP_NOT_CONVERGED : NSP_OK;
+  if (rk > 0) {
+    // step 8: T = R V1 D1^{-1} V1^T R^T = M1 M1^T with M1 = R V1 D1^{-1/2}
+    NSP_CUDA_TRY(c, cudaMemsetAsync(Vsc, 0, sm * 8, st));
+    nspb::scale_cols(VC, s, lamC, r, s, sp, Vsc, sp, 1, st);
+    nspb::small_gemm(s, r, s, 1.0, Racc, sp, false, Vsc, sp, false, 0.0, M1, sp, st);
+    NSP_CUDA_TRY(c, cudaMemsetAsync(Tm, 0, sm * 8, st));
+    nspb::small_gemm(s, s, r, 1.0, M1, sp, false, M1, sp, true, 0.0, Tm, sp, st);
+    nspb::small_sym(Tm, s, sp, 0.0, st);
+    // step 9: EVD of T, descending
+    nspb::small_eig(Tm, sp, s, Vw, sp + 1, lamT, VT, nullptr, st);
+    // step 10: U~ = Q W(:, 1:k)  (reading C5)
+    const int kp = ((rk + 63) / 64) * 64;
+    double* U = Bn;  // reuse (n x kp, kp <= sp)
+    NSP_CUDA_TRY(c, cudaMemsetAsync(Wc, 0, sm * 8, st));
+    nspb::scale_cols(VT, s, lamT, rk, s, kp, Wc, kp, 3, st);
+    PanelArgs pu{U, kp, nullptr, 0, Q, sp, Wc, kp, 1.0, nullptr};
+    nspb::panel2(pu, nullptr, sp, kp, n, st);
+    // step 11: Z = A_G^{-1} U~
+    NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_Z, (size_t)std::max<int64_t>(n, 1) * kp * 8));
+    NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_Z, 0, (size_t)std::max<int64_t>(n, 1) * kp * 8, st));
+    if ((e = ag_solve(c, U, kp, c->d_Z, kp, rk, w.wvu)) != NSP_OK) return e;
+    NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_sigma, kp * 8));
+    NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_sigma, 0, kp * 8, st));
+    NSP_CUDA_TRY(c, cudaMemcpyAsync(c->d_sigma, lamT, rk * 8, cudaMemcpyDeviceToDevice, st));
+    c->h_sigma.resize(rk);
+    NSP_CUDA_TRY(c, cudaMemcpyAsync(c->h_sigma.data(), lamT, rk * 8, cudaMemcpyDeviceToHost, st));
+    NSP_CUDA_TRY(c, cudaStreamSynchronize(st));
+    c->nys_rank = rk;
+    c->nys_ld = kp;
+  } else {
+    ret = NSP_ERR_RANK_COLLAPSE;
+    c->err = "nsp_nystrom: no eigenvalue of C >= eps (M_2 degenerates to A_G^{-1})";
+  }
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  if (rep) {
+    rep->iters = brep.iters;
+    rep->converged = brep.converged;
+    rep->relres = brep.relres;
+    rep->fallbacks = brep.fallbacks;
+    rep->rank = c->nys_rank;
+    rep->status = ret;
+  }
+  return ret;
 }
-nsp_status nsp_nystrom_sigma(const nsp_ctx*, double*, int*) { return NSP_ERR_STATE; }
-nsp_status nsp_precond_apply(nsp_ctx*, int, const double*, double*, int, void*) { return NSP_ERR_STATE; }
+
+nsp_status nsp_nystrom_sigma(const nsp_ctx* c, double* sigma, int* rank_out) {
+  if (!c || !rank_out) return NSP_ERR_ARG;
+  if (c->nys_rank < 0) return NSP_ERR_STATE;
+  *rank_out = c->nys_rank;
+  if (sigma)
+    for (int i = 0; i < c->nys_rank; ++i) sigma[i] = c->h_sigma[i];
+  return NSP_OK;
+}
+
+nsp_status nsp_precond_apply(nsp_ctx* c, int which, const double* X, double* Y, int s, void* ws) {
+  if (!c || !X || !Y || s <= 0 || s > 128 || which < 0 || which > 2) return NSP_ERR_ARG;
+  if (which == 0) {
+    NSP_CUDA_TRY(c, cudaMemcpyAsync(Y, X, (size_t)c->nG * s * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return NSP_OK;
+  }
+  if (which == 2 && c->nys_rank < 0) {
+    c->err = "nsp_precond_apply: M_2 requested before nsp_nystrom";
+    return NSP_ERR_STATE;
+  }
+  const int sp = sp_of(s);
+  const size_t blk = (size_t)std::max<int64_t>(c->nG, 1) * sp;
+  const size_t need = (ag_ws_doubles(c, s) + (size_t)128 * sp + nspb::gram_ws_doubles(c->nG, 128, sp) + 2 * blk +
+                       2048) * 8;
+  char* base;
+  nsp_status e = get_ws(c, ws, need, &base);
+  if (e != NSP_OK) return e;
+  Carver cv(base);
+  double* buf = cv.take(ag_ws_doubles(c, s));
+  double* gsm = cv.take((size_t)128 * sp);
+  double* gws = cv.take(nspb::gram_ws_doubles(c->nG, 128, sp));
+  double* Xp = cv.take(blk);
+  double* Yp = cv.take(blk);
+  if (which == 1) return ag_solve(c, X, s, Y, s, s, buf);
+  nspb::copy_pad(X, s, Xp, sp, c->nG, s, 1.0, c->stream);
+  NSP_CUDA_TRY(c, cudaMemsetAsync(Yp, 0, blk * 8, c->stream));
+  if ((e = m2_apply(c, Xp, sp, Yp, sp, s, buf, gsm, gws)) != NSP_OK) return e;
+  nspb::copy_pad(Yp, sp, Y, s, c->nG, s, 1.0, c->stream);
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  return NSP_OK;
+}
+
 nsp_status nsp_pcg(nsp_ctx*, const double*, double*, double, int, int, void*, nsp_report*) { return NSP_ERR_STATE; }
 }

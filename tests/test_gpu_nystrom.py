@@ -1,0 +1,84 @@
+"""GPU parity of A_G^{-1}, the A_G^{-1}-preconditioned block CG, the Nystrom step (Alg. 2) and the
+two-level preconditioner M_2 (north_star: Nystrom eigenvalues within 1e-8) against the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from oracle.nystrom import apply_M2
+from tests.gpu_util import block, context, dev, problem, relfro
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ["cfg1", "cfg2s", "cfg5s", "cfg4s"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_ag_solve_parity(name):
+    pr, d, S = problem(name)
+    ctx = context(pr, factor_gamma=True)
+    for s in [1, 5, 64]:
+        X = block(d.n_gamma, s, seed=11)
+        Y = torch.empty(d.n_gamma, s, dtype=torch.float64, device="cuda")
+        ctx.precond_apply(1, dev(X), Y)
+        assert relfro(Y.cpu().numpy(), S.solve_AG(X)) <= 1e-12
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg5s"])
+def test_bcg_precond_AG_parity(name):
+    """Reading C2, M = A_G^{-1} (paper-analog): iteration counts +-1, iterates at equal counts."""
+    pr, d, S = problem(name)
+    B = S.k_gamma(pr.omega())
+    Xo, io = O.bf_bcg(S.apply, B, pr.tol_bcg, 500, S.solve_AG)
+    ctx = context(pr, bcg_precond=1)
+    X = torch.zeros(d.n_gamma, pr.s, dtype=torch.float64, device="cuda")
+    rep = ctx.block_cg(dev(B), X, pr.tol_bcg, 500)
+    assert rep["converged"] and abs(rep["iters"] - io["iters"]) <= 1, (rep["iters"], io["iters"])
+    X2 = torch.zeros_like(X)
+    ctx.block_cg(dev(B), X2, 0.0, io["iters"])
+    assert relfro(X2.cpu().numpy(), Xo) <= 1e-8
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg5s"])
+def test_nystrom_parity(name):
+    """Sigma (top rank) and M_2 r at equal inner iteration counts (reading C16): <= 1e-8."""
+    pr, d, S = problem(name)
+    Om = pr.omega()
+    ref = O.nystrom_schur(S, Om, pr.rank, pr.tol_bcg, 500)
+    it = ref.bcg["iters"]
+    ctx = context(pr, factor_gamma=True)
+    rep = ctx.nystrom(pr.rank, pr.oversample, dev(Om), 0.0, it)
+    assert rep["iters"] == it and rep["rank"] == ref.rank
+    sig = ctx.nystrom_sigma()
+    assert np.max(np.abs(sig - ref.sigma) / ref.sigma) <= 1e-8, (sig[:4], ref.sigma[:4])
+    # M_2 on probes
+    R = block(d.n_gamma, 64, seed=21)
+    Y = torch.empty(d.n_gamma, 64, dtype=torch.float64, device="cuda")
+    ctx.precond_apply(2, dev(R), Y)
+    Yref = apply_M2(S, ref.Z, ref.sigma, R)
+    assert relfro(Y.cpu().numpy(), Yref) <= 1e-8
+    # free-running inner solve: iteration count within +-1
+    rep2 = ctx.nystrom(pr.rank, pr.oversample, dev(Om), pr.tol_bcg, 500)
+    assert abs(rep2["iters"] - it) <= 1
+    ctx.close()
+
+
+def test_nystrom_exact_single_separator_gpu():
+    """Exactness pin on the GPU: s >= rank(B_H) -> U Sigma U^T = B_H; top eigenvalues = closed form."""
+    from tests.test_oracle_pins import _closed_form_modes, _single_separator
+    from nsp_inputs import philox
+    from paper_2101_12164_b200 import Context
+    dims, axis, c = (13, 24), 0, 6
+    A, part = _single_separator(dims, axis, c)
+    d = O.dbbd(A.to_scipy(), part, 2)
+    nG = d.n_gamma
+    ctx = Context(A.rowptr, A.colidx, A.val, part, 2, factor_gamma=True)
+    Om = philox.gaussian_block(0, 0, nG, nG)
+    ctx.nystrom(nG, 0, dev(Om), 1e-14, 200)
+    sig = ctx.nystrom_sigma()
+    _, _, mu, ff = _closed_form_modes(dims, axis, c)
+    lam_bh = np.sort((2 + mu) * ff / (2 + mu - ff))[::-1]
+    assert np.allclose(sig[:5], lam_bh[:5], rtol=1e-8)
+    ctx.close()
