@@ -82,6 +82,16 @@ class Problem:
     def xstar(self, seed: int = 1) -> np.ndarray:
         return philox.gaussian(seed, philox.STREAM_XSTAR, self.n)
 
+    def rhs(self, seed: int = 1) -> np.ndarray:
+        """Right-hand side of the full solve (reading C8): b ~ N(0,1) directly for the cfg2 family
+        ("seeded Gaussian Omega and b"), b = A x* with x* = xstar(seed) otherwise.  The product
+        A x* is input assembly (a plain CSR matvec), not the method's arithmetic."""
+        if self.name.startswith("cfg2"):
+            return self.xstar(seed)
+        x = self.xstar(seed)
+        rows = np.repeat(np.arange(self.n), np.diff(self.A.rowptr))
+        return np.bincount(rows, weights=self.A.val * x[self.A.colidx], minlength=self.n)
+
 
 # ----------------------------------------------------------------------------
 # structured grids

@@ -166,7 +166,13 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_gsys);
   fr(c->d_gperm);
   fr(c->d_gperm_inv);
-  for (DevCSR* m : {&c->A2G, &c->AGG2}) {
+  fr(c->d_i1sys);
+  fr(c->d_i1_src);
+  fr(c->d_b_src);
+  fr(c->d_g_src);
+  fr(c->d_Z);
+  fr(c->d_sigma);
+  for (DevCSR* m : {&c->A2G, &c->AGG2, &c->CB, &c->C1}) {
     fr(m->rowptr);
     fr(m->col);
     fr(m->val);

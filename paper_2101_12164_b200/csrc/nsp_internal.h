@@ -88,6 +88,18 @@ struct nsp_ctx {
   int nys_rank = -1, nys_ld = 0;
   std::vector<double> h_sigma;
 
+  // full-system solve (nsp_pcg; eq:A_LDLT PAPER.md:381-385): every block's interior rows I1 in
+  // band order (padded to nt1*64 rows, blocks concatenated), its band factor L11 as a TriSys,
+  // original-id maps, and the block couplings as CSRs with a leading identity part:
+  //   CB rows = W/V/U rows:  [ I | -A_B1 ]  (cols < wvu_rows: identity, cols >= wvu_rows: band row)
+  //   C1 rows = band rows:   [ I | -A_1B ]  (cols < i1_rows: identity, cols >= i1_rows: W/V/U row)
+  int64_t i1_rows = 0;
+  TriSys* d_i1sys = nullptr;
+  int32_t* d_i1_src = nullptr;
+  int32_t* d_b_src = nullptr;
+  int32_t* d_g_src = nullptr;
+  DevCSR CB, C1;
+
   // statistics
   int64_t n_I = 0, n_bl = 0, nnz_AG = 0, nnz_AGI = 0, max_b = 0, ag_bw = 0;
 

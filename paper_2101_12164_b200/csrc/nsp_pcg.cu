@@ -1,0 +1,391 @@
+// Outer PCG on the border system and the full solve of A x = b (§8(a) row d3):
+//   f   = b_G - A_GI A_I^{-1} b_I                       (eq:A_LDLT PAPER.md:381-385, eq:Sx=b PAPER.md:415-420)
+//   w   = PCG(S_G, f, M),  M in {I, A_G^{-1} (eq:S1), M_2 = A_G^{-1} + Z Sigma Z^T (eq:left_prec_mat)}
+//   x_I = A_I^{-1} (b_I - A_IG w),  x_G = w,  un-permuted to the original order.
+// PCG is the textbook preconditioned CG, x_0 = 0, stopping on the recurrence residual
+// ||r_k|| / ||f|| <= tol (reading C9); iteration count = S_G applications.
+//
+// A_I_j^{-1} on a full interior vector uses the block elimination of the setup's ordering
+// (I1 = interior rows, B = boundary layer, L22 L22^T = A_BB - A_B1 A_11^{-1} A_1B):
+//   y_B = L22^{-T} L22^{-1} (r_B - A_B1 A_11^{-1} r_1),   y_1 = A_11^{-1} (r_1 - A_1B y_B)
+// with A_11^{-1} the band factor (k_tri_fb) and L22 the dense trailing factor (k_trsm_fb).
+// Every scalar of the iteration stays on the device; one small status read per iteration.
+// All reductions are fixed-order two-stage (no fp64 atomics; reading C17).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "nsp_blas.h"
+#include "nsp_solver.h"
+
+namespace {
+
+constexpr int RT = 256;             // threads per reduction CTA
+constexpr int RPB = 2048;           // rows per partial-sum chunk
+constexpr int GT_ROWS = 512;        // rows per Z^T r chunk
+
+// part[b*2 + q] = sum over chunk b of a_q . b_q (q = 0, 1; a2 may be null)
+__global__ void __launch_bounds__(RT) k_dot2_partial(const double* __restrict__ a1, const double* __restrict__ b1,
+                                                     const double* __restrict__ a2, const double* __restrict__ b2,
+                                                     int64_t n, double* __restrict__ part) {
+  __shared__ double red[2][RT];
+  const int64_t r0 = (int64_t)blockIdx.x * RPB;
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t r = r0 + threadIdx.x; r < min(n, r0 + RPB); r += RT) {
+    s1 = fma(a1[r], b1[r], s1);
+    if (a2) s2 = fma(a2[r], b2[r], s2);
+  }
+  red[0][threadIdx.x] = s1;
+  red[1][threadIdx.x] = s2;
+  __syncthreads();
+  for (int w = RT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + w];
+      red[1][threadIdx.x] += red[1][threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 2] = red[0][0];
+    part[blockIdx.x * 2 + 1] = red[1][0];
+  }
+}
+
+// Scalar slots of the iteration (device doubles):
+//   sc[0], sc[1]: r.z (ping-pong by iteration parity)   sc[2]: p.q   sc[3]: r.r   sc[4]: ||f||
+// mode 0: out slot = sum (q = 0);   mode 1: out slot = sum (q = 0), status relres / converged from
+// sum = r.r;  mode 2: ||f|| (sqrt of sum) and the initial status.
+__global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ part, int nblk, double* sc, int slot,
+                                                   int mode, double tol, BcgStatus* st) {
+  __shared__ double red[RT];
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += RT) s += part[b * 2];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = RT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  const double v = red[0];
+  if (mode == 0) {
+    sc[slot] = v;
+  } else if (mode == 1) {
+    sc[slot] = v;
+    const double fn = sc[4];
+    const double rel = fn > 0.0 ? sqrt(v) / fn : 0.0;
+    st->relres = rel;
+    st->converged = rel <= tol ? 1 : 0;
+    if (!isfinite(v)) st->nonfinite = 1;
+  } else {
+    sc[4] = sqrt(v);
+    st->relres = v > 0.0 ? 1.0 : 0.0;
+    st->converged = v > 0.0 ? 0 : 1;
+    if (!isfinite(v)) st->nonfinite = 1;
+  }
+}
+
+// alpha = (r.z) / (p.q);  x += alpha p;  r -= alpha q;  partial r.r.  p.q <= 0 -> indefinite.
+__global__ void __launch_bounds__(RT) k_pcg_xr(double* __restrict__ x, double* __restrict__ r,
+                                               const double* __restrict__ p, const double* __restrict__ q,
+                                               int64_t n, const double* sc, int cur, double* __restrict__ part,
+                                               BcgStatus* st) {
+  __shared__ double red[RT];
+  const double pq = sc[2];
+  const double alpha = pq > 0.0 ? sc[cur] / pq : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !(pq > 0.0)) st->indefinite = 1;
+  const int64_t r0 = (int64_t)blockIdx.x * RPB;
+  double s = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < min(n, r0 + RPB); i += RT) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double v = fma(-alpha, q[i], r[i]);
+    r[i] = v;
+    s = fma(v, v, s);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = RT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x * 2] = red[0];
+}
+
+// p = z + beta p, beta = (r.z)_new / (r.z)_old
+__global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ z, int64_t n, const double* sc, int cur) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double beta = sc[cur ^ 1] / sc[cur];
+  p[i] = fma(beta, p[i], z[i]);
+}
+
+// y[i*ldy] = a[i*lda] + alpha * b[i*ldb]
+__global__ void k_axpy_strided(double* y, int ldy, const double* a, int lda, const double* b, int ldb, double alpha,
+                               int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i * ldy] = fma(alpha, b[i * ldb], a[i * lda]);
+}
+
+// part[chunk*128 + k] = sum over chunk rows of Z[row][k] * r[row]  (k < rk)
+__global__ void __launch_bounds__(128) k_gemvt_partial(const double* __restrict__ Z, int ldz,
+                                                       const double* __restrict__ r, int64_t n, int rk,
+                                                       double* __restrict__ part) {
+  const int k = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * GT_ROWS;
+  double s = 0.0;
+  if (k < rk)
+    for (int64_t i = r0; i < min(n, r0 + GT_ROWS); ++i) s = fma(Z[i * ldz + k], r[i], s);
+  part[blockIdx.x * 128 + k] = s;
+}
+
+// g[k] = sigma[k] * sum_chunks part[chunk][k]  (fixed order)
+__global__ void k_gemvt_reduce(const double* __restrict__ part, int nchunks, const double* __restrict__ sigma, int rk,
+                               double* __restrict__ g) {
+  const int k = threadIdx.x;
+  if (k >= rk) return;
+  double s = 0.0;
+  for (int b = 0; b < nchunks; ++b) s += part[b * 128 + k];
+  g[k] = sigma[k] * s;
+}
+
+// y[row] += sum_k Z[row][k] g[k]   (warp per row, butterfly sum)
+__global__ void k_gemv_add(const double* __restrict__ Z, int ldz, const double* __restrict__ g, int rk, int64_t n,
+                           double* __restrict__ y) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int k = lane; k < rk; k += 32) s = fma(Z[row * ldz + k], g[k], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) y[row] += s;
+}
+
+unsigned nblk_of(int64_t n) { return (unsigned)std::max<int64_t>(1, (n + RPB - 1) / RPB); }
+unsigned grid1(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+}  // namespace
+
+namespace nspi {
+
+struct PcgWs {
+  double *f, *w, *r, *z, *p, *q, *tmp;     // n_G vectors
+  double *bB, *wvu, *tmpB;                 // W/V/U rows x 32
+  double *i1r, *i1buf;                     // band rows x 32
+  double *agbuf, *apply_wvu, *part, *gpart, *g, *sc;
+  BcgStatus* st;
+};
+
+static size_t pcg_layout(const nsp_ctx* c, char* base, PcgWs* out) {
+  size_t off = 0;
+  auto take = [&](size_t nd) {
+    off = (off + 255) & ~size_t(255);
+    double* p = base ? (double*)(base + off) : nullptr;
+    off += nd * 8;
+    return p;
+  };
+  PcgWs w{};
+  const size_t nG = (size_t)std::max<int64_t>(c->nG, 1);
+  w.f = take(nG);
+  w.w = take(nG);
+  w.r = take(nG);
+  w.z = take(nG);
+  w.p = take(nG);
+  w.q = take(nG);
+  w.tmp = take(nG);
+  const size_t wr = (size_t)std::max<int64_t>(c->wvu_rows, 1) * 32;
+  w.bB = take(wr);
+  w.wvu = take(wr);
+  w.tmpB = take(wr);
+  const size_t ir = (size_t)std::max<int64_t>(c->i1_rows, 1) * 32;
+  w.i1r = take(ir);
+  w.i1buf = take(ir);
+  w.agbuf = take(c->has_ag ? ag_ws_doubles(c, 1) : 1);
+  w.apply_wvu = take(apply_ws_bytes(c, 1) / 8 + 1);
+  w.part = take((size_t)2 * nblk_of(std::max<int64_t>(c->nG, 1)) + 2);
+  w.gpart = take((size_t)128 * grid1(std::max<int64_t>(c->nG, 1), GT_ROWS));
+  w.g = take(128);
+  w.sc = take(16);
+  w.st = (BcgStatus*)take(sizeof(BcgStatus) / 8 + 1);
+  if (out) *out = w;
+  return off + 256;
+}
+
+size_t pcg_ws_bytes(const nsp_ctx* c) { return pcg_layout(c, nullptr, nullptr); }
+
+// out slot = a . b
+static void dot(nsp_ctx* c, const double* a, const double* b, int64_t n, PcgWs& w, int slot) {
+  const unsigned nb = nblk_of(n);
+  nsp_count_launch();
+  k_dot2_partial<<<nb, RT, 0, c->stream>>>(a, b, nullptr, nullptr, n, w.part);
+  nsp_count_launch();
+  k_dot_reduce<<<1, RT, 0, c->stream>>>(w.part, (int)nb, w.sc, slot, 0, 0.0, w.st);
+}
+
+// z = M r for the PCG preconditioner (0: identity copy, 1: A_G^{-1}, 2: M_2)
+static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z, PcgWs& w) {
+  const int64_t n = c->nG;
+  if (which == 0) {
+    NSP_CUDA_TRY(c, cudaMemcpyAsync(z, r, (size_t)n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return NSP_OK;
+  }
+  nsp_status e = ag_solve(c, r, 1, z, 1, 1, w.agbuf);
+  if (e != NSP_OK) return e;
+  if (which == 2 && c->nys_rank > 0) {
+    const unsigned nch = grid1(n, GT_ROWS);
+    nsp_count_launch();
+    k_gemvt_partial<<<nch, 128, 0, c->stream>>>(c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart);
+    nsp_count_launch();
+    k_gemvt_reduce<<<1, 128, 0, c->stream>>>(w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
+    nsp_count_launch();
+    k_gemv_add<<<grid1(n * 32, 256), 256, 0, c->stream>>>(c->d_Z, c->nys_ld, w.g, c->nys_rank, n, z);
+  }
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  return NSP_OK;
+}
+
+// wvu (W/V/U rows, ld 32) = A_I^{-1}-restricted-to-B of (rB ; r1):  y_B = L22^{-T} L22^{-1}(r_B - A_B1 A_11^{-1} r_1)
+// i1r holds r_1 (band rows, ld 32), bB holds r_B; i1buf is overwritten with A_11^{-1} r_1.
+static nsp_status interior_boundary_solve(nsp_ctx* c, PcgWs& w) {
+  NSP_CUDA_TRY(c, cudaMemcpyAsync(w.i1buf, w.i1r, (size_t)c->i1_rows * 32 * 8, cudaMemcpyDeviceToDevice, c->stream));
+  nspk::tri_fb(c->d_i1sys, c->nsub, w.i1buf, 32, 32, true, true, c->stream);
+  nspk::spmm(c->CB, w.bB, 32, w.i1buf, 32, c->wvu_rows, w.wvu, 32, 1, 1, true, c->stream);
+  nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, w.wvu, 32, 32, c->stream);
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  return NSP_OK;
+}
+
+static nsp_status read_st(nsp_ctx* c, BcgStatus* d, BcgStatus* h) {
+  NSP_CUDA_TRY(c, cudaMemcpyAsync(h, d, sizeof(BcgStatus), cudaMemcpyDeviceToHost, c->stream));
+  NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return NSP_OK;
+}
+
+nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxit, int precond, PcgWs& w,
+                    nsp_report* rep) {
+  cudaStream_t st = c->stream;
+  const int64_t n = c->nG;
+  BcgStatus* hs = (BcgStatus*)c->h_status;
+  nsp_status e;
+  // ---- reduction to the border: f = b_G - A_GI A_I^{-1} b_I
+  nspk::gather_rows(b, 1, c->d_i1_src, c->i1_rows, w.i1r, 32, 1, 1.0, st);
+  nspk::gather_rows(b, 1, c->d_b_src, c->wvu_rows, w.bB, 32, 1, 1.0, st);
+  if ((e = interior_boundary_solve(c, w)) != NSP_OK) return e;
+  nspk::spmm(c->AGG2, nullptr, 0, w.wvu, 32, n, w.tmp, 1, 1, 2, false, st);      // K-part: A_GI y_B
+  nspk::gather_rows(b, 1, c->d_g_src, n, w.f, 1, 1, 1.0, st);
+  if (n > 0) {
+    nsp_count_launch();
+    k_axpy_strided<<<grid1(n, 256), 256, 0, st>>>(w.f, 1, w.f, 1, w.tmp, 1, -1.0, n);
+  }
+  // ---- PCG on S_G w = f
+  BcgStatus init{};
+  std::memcpy(hs, &init, sizeof(init));
+  NSP_CUDA_TRY(c, cudaMemcpyAsync(w.st, hs, sizeof(BcgStatus), cudaMemcpyHostToDevice, st));
+  NSP_CUDA_TRY(c, cudaMemsetAsync(w.w, 0, (size_t)std::max<int64_t>(n, 1) * 8, st));
+  NSP_CUDA_TRY(c, cudaMemcpyAsync(w.r, w.f, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+  {
+    const unsigned nb = nblk_of(n);
+    nsp_count_launch();
+    k_dot2_partial<<<nb, RT, 0, st>>>(w.f, w.f, nullptr, nullptr, n, w.part);
+    nsp_count_launch();
+    k_dot_reduce<<<1, RT, 0, st>>>(w.part, (int)nb, w.sc, 4, 2, tol, w.st);
+  }
+  if ((e = read_st(c, w.st, hs)) != NSP_OK) return e;
+  if (rep && rep->hist && rep->hist_cap > 0) rep->hist[0] = hs->relres;
+  int iters = 0;
+  double relres = hs->relres;
+  nsp_status ret = hs->converged ? NSP_OK : NSP_NOT_CONVERGED;
+  if (!hs->converged) {
+    if ((e = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e;
+    NSP_CUDA_TRY(c, cudaMemcpyAsync(w.p, w.z, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+    dot(c, w.r, w.z, n, w, 0);
+    int cur = 0;
+    for (int it = 0; it < maxit; ++it) {
+      if ((e = apply_into(c, w.p, 1, w.q, 1, 1, 1, w.apply_wvu)) != NSP_OK) return e;   // q = S_G p
+      dot(c, w.p, w.q, n, w, 2);
+      const unsigned nb = nblk_of(n);
+      nsp_count_launch();
+      k_pcg_xr<<<nb, RT, 0, st>>>(w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, w.st);
+      nsp_count_launch();
+      k_dot_reduce<<<1, RT, 0, st>>>(w.part, (int)nb, w.sc, 3, 1, tol, w.st);
+      if ((e = read_st(c, w.st, hs)) != NSP_OK) return e;
+      iters = it + 1;
+      relres = hs->relres;
+      if (rep && rep->hist && it + 1 < rep->hist_cap) rep->hist[it + 1] = relres;
+      if (hs->indefinite) {
+        ret = NSP_ERR_INDEFINITE;
+        c->err = "nsp_pcg: p^T S_G p <= 0";
+        break;
+      }
+      if (hs->nonfinite) {
+        ret = NSP_ERR_NUMERICAL;
+        c->err = "nsp_pcg: non-finite residual";
+        break;
+      }
+      if (hs->converged) {
+        ret = NSP_OK;
+        break;
+      }
+      if ((e = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e;
+      dot(c, w.r, w.z, n, w, cur ^ 1);
+      nsp_count_launch();
+      k_pcg_p<<<grid1(n, 256), 256, 0, st>>>(w.p, w.z, n, w.sc, cur);
+      cur ^= 1;
+    }
+  }
+  // ---- back-substitution: x_I = A_I^{-1}(b_I - A_IG w), x_G = w, un-permute
+  nspk::gather_rows(b, 1, c->d_i1_src, c->i1_rows, w.i1r, 32, 1, 1.0, st);
+  nspk::gather_rows(b, 1, c->d_b_src, c->wvu_rows, w.bB, 32, 1, 1.0, st);
+  nspk::spmm(c->A2G, w.w, 1, nullptr, 0, 0, w.tmpB, 32, 1, 0, true, st);            // A_IG w (B rows)
+  if (c->wvu_rows > 0) {
+    nsp_count_launch();
+    k_axpy_strided<<<grid1(c->wvu_rows, 256), 256, 0, st>>>(w.bB, 32, w.bB, 32, w.tmpB, 32, -1.0, c->wvu_rows);
+  }
+  if ((e = interior_boundary_solve(c, w)) != NSP_OK) return e;                       // y_B in wvu
+  nspk::spmm(c->C1, w.i1r, 32, w.wvu, 32, c->i1_rows, w.i1buf, 32, 1, 1, true, st); // r_1 - A_1B y_B
+  nspk::tri_fb(c->d_i1sys, c->nsub, w.i1buf, 32, 32, true, true, st);               // y_1
+  nspk::scatter_rows(w.i1buf, 32, c->d_i1_src, c->i1_rows, x, 1, 1, false, st);
+  nspk::scatter_rows(w.wvu, 32, c->d_b_src, c->wvu_rows, x, 1, 1, false, st);
+  nspk::scatter_rows(w.w, 1, c->d_g_src, n, x, 1, 1, false, st);
+  NSP_CUDA_TRY(c, cudaStreamSynchronize(st));
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  if (rep) {
+    rep->iters = iters;
+    rep->converged = ret == NSP_OK;
+    rep->status = ret;
+    rep->relres = relres;
+  }
+  return ret;
+}
+
+}  // namespace nspi
+
+using namespace nspi;
+
+extern "C" nsp_status nsp_pcg(nsp_ctx* c, const double* b, double* x, double tol, int maxit, int precond, void* ws,
+                              nsp_report* rep) {
+  if (!c || !b || !x || maxit < 0 || precond < 0 || precond > 2) {
+    if (c) c->err = "nsp_pcg: bad arguments (precond in {0, 1, 2})";
+    return NSP_ERR_ARG;
+  }
+  if (c->nranks != 1) {
+    c->err = "nsp_pcg: multi-rank full solve not built";
+    return NSP_ERR_STATE;
+  }
+  if (precond >= 1 && !c->has_ag) {
+    c->err = "nsp_pcg: the A_G^{-1} / M_2 preconditioner needs the A_G factor (opts.factor_gamma = 1)";
+    return NSP_ERR_STATE;
+  }
+  if (precond == 2 && c->nys_rank < 0) {
+    c->err = "nsp_pcg: M_2 requested before nsp_nystrom";
+    return NSP_ERR_STATE;
+  }
+  char* base;
+  nsp_status e = get_ws(c, ws, pcg_ws_bytes(c), &base);
+  if (e != NSP_OK) return e;
+  PcgWs w;
+  pcg_layout(c, base, &w);
+  return pcg_impl(c, b, x, tol, maxit, precond, w, rep);
+}

@@ -617,6 +617,67 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       AGG2.rowptr[g + 1] = (int32_t)AGG2.col.size();
     }
   }
+  // ---------------- full-system solve maps (nsp_pcg): band rows, original-id maps, [I | -A_B1], [I | -A_1B]
+  std::vector<int64_t> i1_row0(K);
+  int64_t i1_rows = 0;
+  for (int j = 0; j < K; ++j) {
+    i1_row0[j] = i1_rows;
+    i1_rows += (int64_t)sh[j].nt1 * NSP_TILE;
+  }
+  if (i1_rows + wvu_rows > INT32_MAX) return fail(c, NSP_ERR_ARG, "nsp_setup: interior rows exceed int32");
+  c->i1_rows = i1_rows;
+  std::vector<int32_t> i1_src(i1_rows, -1), b_src(wvu_rows, -1), g_src(c->nG);
+  for (int64_t g = 0; g < c->nG; ++g) g_src[g] = (int32_t)c->gamma[g];
+  HostCSR32 CB, C1;
+  CB.rowptr.assign(wvu_rows + 1, 0);
+  C1.rowptr.assign(i1_rows + 1, 0);
+  {
+    std::vector<int32_t> cnt_b(wvu_rows, 0), cnt_1(i1_rows, 0);
+    for (int j = 0; j < K; ++j) {
+      const SubHost& S = sh[j];
+      for (int k = 0; k < S.n1; ++k) i1_src[i1_row0[j] + k] = (int32_t)S.nodes[k];
+      for (int k = 0; k < S.b; ++k) b_src[c->subs[j].wvu_row + k] = (int32_t)S.nodes[S.n1 + k];
+    }
+    // row r of CB: identity then -A_B1 (band columns ascending); row of C1: identity then -A_1B
+    auto row_entries = [&](int64_t v, int j, bool from_b, std::vector<std::pair<int32_t, double>>& ent) {
+      ent.clear();
+      for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
+        const int64_t u = ci[q];
+        if (part[u] != j || u == v || va[q] == 0.0) continue;
+        const bool u_b = bidx[u] >= 0;
+        if (from_b && !u_b) ent.push_back({(int32_t)(wvu_rows + i1_row0[j] + lpos[u]), -va[q]});
+        if (!from_b && u_b) ent.push_back({(int32_t)(i1_rows + c->subs[j].wvu_row + bidx[u]), -va[q]});
+      }
+      std::sort(ent.begin(), ent.end());
+    };
+    std::vector<std::pair<int32_t, double>> ent;
+    for (int64_t r = 0; r < wvu_rows; ++r) {
+      if (b_src[r] >= 0) {
+        const int64_t v = b_src[r];
+        CB.col.push_back((int32_t)r);
+        CB.val.push_back(1.0);
+        row_entries(v, part[v], true, ent);
+        for (auto& e : ent) {
+          CB.col.push_back(e.first);
+          CB.val.push_back(e.second);
+        }
+      }
+      CB.rowptr[r + 1] = (int32_t)CB.col.size();
+    }
+    for (int64_t r = 0; r < i1_rows; ++r) {
+      if (i1_src[r] >= 0) {
+        const int64_t v = i1_src[r];
+        C1.col.push_back((int32_t)r);
+        C1.val.push_back(1.0);
+        row_entries(v, part[v], false, ent);
+        for (auto& e : ent) {
+          C1.col.push_back(e.first);
+          C1.val.push_back(e.second);
+        }
+      }
+      C1.rowptr[r + 1] = (int32_t)C1.col.size();
+    }
+  }
   const double t_host = ms_since(t0);
 
   // ---------------- device upload
@@ -624,6 +685,11 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   nsp_status st;
   if ((st = upload_csr(c, c->A2G, A2G)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->AGG2, AGG2)) != NSP_OK) return st;
+  if ((st = upload_csr(c, c->CB, CB)) != NSP_OK) return st;
+  if ((st = upload_csr(c, c->C1, C1)) != NSP_OK) return st;
+  if ((st = upload(c, &c->d_i1_src, i1_src)) != NSP_OK) return st;
+  if ((st = upload(c, &c->d_b_src, b_src)) != NSP_OK) return st;
+  if ((st = upload(c, &c->d_g_src, g_src)) != NSP_OK) return st;
   if ((st = upload(c, &c->d_subs, c->subs)) != NSP_OK) return st;
   std::vector<int> bf = border_first_all;
   if (bf.empty()) bf.push_back(0);
@@ -631,6 +697,13 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   if (band_tiles > 0) {
     NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_band, (size_t)band_tiles * NSP_TILE_ELEMS * 8));
     NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_band, 0, (size_t)band_tiles * NSP_TILE_ELEMS * 8, c->stream));
+  }
+  {
+    std::vector<TriSys> ts(K);
+    for (int j = 0; j < K; ++j)
+      ts[j] = TriSys{c->d_band ? c->d_band + c->subs[j].band_off * NSP_TILE_ELEMS : nullptr, sh[j].nt1, sh[j].wb,
+                     i1_row0[j]};
+    if ((st = upload(c, &c->d_i1sys, ts)) != NSP_OK) return st;
   }
   if (dense_tiles > 0) {
     NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_dense, (size_t)dense_tiles * NSP_TILE_ELEMS * 8));

@@ -537,5 +537,4 @@ nsp_status nsp_precond_apply(nsp_ctx* c, int which, const double* X, double* Y, 
   return NSP_OK;
 }
 
-nsp_status nsp_pcg(nsp_ctx*, const double*, double*, double, int, int, void*, nsp_report*) { return NSP_ERR_STATE; }
 }

@@ -11,3 +11,9 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
 size_t solver_ws_bytes(const nsp_ctx* c, int s);
 void solver_free(nsp_ctx* c);
 }  // namespace nspi
+
+namespace nspi {
+size_t ag_ws_doubles(const nsp_ctx* c, int s);
+// Y = A_G^{-1} X (band factor of A_G; eq:S1), buf: ag_ws_doubles(c, s) doubles
+nsp_status ag_solve(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, double* buf);
+}  // namespace nspi

@@ -1,0 +1,98 @@
+"""GPU parity of the outer PCG and the full solve of A x = b (§8(a) row d3; eq:A_LDLT PAPER.md:381-385,
+eq:Sx=b PAPER.md:415-420) against the oracle (north_star: PCG iteration counts within +-1, final
+solutions within 1e-8), through the C ABI, for every preconditioner (none, A_G^{-1}, M_2)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from oracle.nystrom import apply_M2
+from tests.gpu_util import context, dev, problem
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ["cfg1", "cfg2s", "cfg5s", "cfg3s"]
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _oracle_M(S, precond, nys=None):
+    if precond == 0:
+        return None
+    if precond == 1:
+        return S.solve_AG
+    return lambda r: apply_M2(S, nys.Z, nys.sigma, r)
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("precond", [0, 1, 2])
+def test_pcg_full_solve_parity(name, precond):
+    pr, d, S = problem(name)
+    tol = pr.tol_pcg or 1e-8
+    b = pr.rhs()
+    ctx = context(pr, factor_gamma=True)
+    nys = None
+    if precond == 2:
+        Om = pr.omega()
+        nys = O.nystrom_schur(S, Om, pr.rank, pr.tol_bcg, 500)
+        rep_n = ctx.nystrom(pr.rank, pr.oversample, dev(Om), 0.0, nys.bcg["iters"])
+        assert rep_n["iters"] == nys.bcg["iters"]
+    xo, io = O.solve_full_system(S, b, tol, 2000, _oracle_M(S, precond, nys))
+    assert io["status"] == 0
+    x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
+    rep = ctx.pcg(dev(b), x, tol, 2000, precond=precond)
+    assert rep["converged"] and abs(rep["iters"] - io["iters"]) <= 1, (rep["iters"], io["iters"])
+    xg = x.cpu().numpy()
+    A = pr.A.to_scipy()
+    assert np.linalg.norm(b - A @ xg) / np.linalg.norm(b) <= 1e-6
+    # equal iteration counts (reading C16): solutions within 1e-8
+    x2 = torch.zeros_like(x)
+    rep2 = ctx.pcg(dev(b), x2, 0.0, io["iters"], precond=precond)
+    assert rep2["iters"] == io["iters"]
+    assert _rel(x2.cpu().numpy(), xo) <= 1e-8, _rel(x2.cpu().numpy(), xo)
+    if not name.startswith("cfg2"):
+        print(f"{name} M{precond}: {rep['iters']} its, ||x - x*||/||x*|| = {_rel(xg, pr.xstar()):.2e}")
+    ctx.close()
+
+
+def test_pcg_zero_rhs_and_state_errors():
+    pr, d, S = problem("cfg1")
+    ctx = context(pr, factor_gamma=True)
+    x = torch.ones(pr.n, dtype=torch.float64, device="cuda")
+    rep = ctx.pcg(torch.zeros(pr.n, dtype=torch.float64, device="cuda"), x, 1e-8, 100, precond=1)
+    assert rep["iters"] == 0 and rep["converged"] and float(x.abs().max()) == 0.0
+    from paper_2101_12164_b200.nsp import NspError
+    with pytest.raises(NspError) as ei:
+        ctx.pcg(dev(pr.rhs()), x, 1e-8, 100, precond=2)
+    assert ei.value.status == -7
+    ctx.close()
+    ctx0 = context(pr)            # no A_G factor
+    with pytest.raises(NspError):
+        ctx0.pcg(dev(pr.rhs()), x, 1e-8, 100, precond=1)
+    rep0 = ctx0.pcg(dev(pr.rhs()), x, 1e-8, 500, precond=0)
+    assert rep0["converged"]
+    ctx0.close()
+
+
+def test_pcg_exact_m2_one_iteration_gpu():
+    """Pin (eq:S-1 PAPER.md:810-811): k = n_G and an exact inner solve give M_2 = S_G^{-1}, so the
+    outer PCG converges in one iteration."""
+    from tests.test_oracle_pins import _single_separator
+    from nsp_inputs import philox
+    from paper_2101_12164_b200 import Context
+    dims, axis, c = (13, 24), 0, 6
+    A, part = _single_separator(dims, axis, c)
+    d = O.dbbd(A.to_scipy(), part, 2)
+    nG = d.n_gamma
+    ctx = Context(A.rowptr, A.colidx, A.val, part, 2, factor_gamma=True)
+    Om = philox.gaussian_block(0, 0, nG, nG)
+    ctx.nystrom(nG, 0, dev(Om), 1e-14, 200)
+    b = philox.gaussian(5, 1, A.n)
+    x = torch.zeros(A.n, dtype=torch.float64, device="cuda")
+    rep = ctx.pcg(dev(b), x, 1e-8, 50, precond=2)
+    assert rep["converged"] and rep["iters"] <= 2, rep["iters"]
+    xd = np.linalg.solve(A.to_scipy().toarray(), b)
+    assert _rel(x.cpu().numpy(), xd) <= 1e-9
+    ctx.close()
