@@ -31,6 +31,16 @@ UNIT = "RHS-applies/s"
 FP64_PEAK_TFLOPS = 37.05  # DMMA m8n8k4 microbenchmark, tools/fp64_peak.cu -> profiles/r01_fp64_peak.txt
 
 
+def _traffic(workload):
+    """dram bytes per launch of the dominant kernel from one committed `ncu --set full` capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(workload)
+        return (t["dram_bytes_per_launch"], t["source"]) if t else (None, None)
+    except Exception:
+        return None, None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -267,9 +277,11 @@ def run_ours(args, ws, rank, local):
     sweep_avg_ms = sweep_ms / max(sweeps, 1)
     flops_per_launch = 2.0 * st["sum_b2"] * s      # forward + backward: 2 * b_j^2 * s per block
     achieved = flops_per_launch / (sweep_avg_ms * 1e-3) / 1e12
-    l22_bytes = st["l22_entries"] * 8
-    hbm_alg = (2 * l22_bytes / 2 + 2 * st["sum_b"] * s * 8)   # L22 lower half each sweep + W in / U out
+    # algorithmic bytes: the unpadded lower triangle of every L22 streamed once per sweep (2 sweeps)
+    # + W in + U out (s-wide boundary-layer rows)
+    hbm_alg = 2 * 8 * (st["sum_b2"] + st["sum_b"]) / 2 + 2 * 8 * s * st["sum_b"]
     peaks = _peaks()
+    traffic, traffic_src = _traffic(args.config)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tmax, "higher_is_better": True, "scaling": "weak",
@@ -281,7 +293,8 @@ def run_ours(args, ws, rank, local):
         "apply": {"ms": t_apply, "rhs_applies_per_s": s / (t_apply * 1e-3)},
         "roofline": {"kernel": "k_trsm_fb (a2+a3 batched L22 sweeps)", "bound": "tensor",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": hbm_alg,
                      "peak_source": "fp64 DMMA microbenchmark tools/fp64_peak.cu (profiles/r01_fp64_peak.txt)",
                      "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": sweep_avg_ms,
                      "launches": sweeps,

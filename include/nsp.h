@@ -74,6 +74,8 @@ typedef struct {
   double nys_eps_rel;    /* Nystrom eigenvalue split eps = nys_eps_rel * lambda_max(C) (reading C6), 1e-12 */
   size_t scratch_bytes;  /* device scratch budget for the setup factorisation; 0 = auto */
   int verbose;
+  void* local_group;     /* testing only: nsp_local_group_create(nranks) handle shared by nranks host
+                            threads driving ranks on ONE device (replaces NCCL); NULL otherwise */
 } nsp_opts;
 
 /* Solver / setup report; caller-owned.  hist / widths are optional caller
@@ -108,6 +110,30 @@ nsp_status nsp_setup(const nsp_csr* A, const int32_t* part, int K, const nsp_opt
 
 nsp_status nsp_dims(const nsp_ctx* ctx, int64_t* n, int64_t* n_gamma, int64_t* n_gamma_local,
                     int* K_local);
+
+/* ---- multi-GPU sharding ----
+ * Rank r of G owns the contiguous block range [rK/G, (r+1)K/G) (a subtree of a depth-first ND leaf
+ * numbering).  Its local Gamma rows are its PRIVATE rows (every adjacent block is its own and no
+ * A_G neighbour is private to another rank) followed by the SHARED rows (all other Gamma rows,
+ * replicated on every rank), each group in ascending original id.  Per S_G apply the shared rows'
+ * per-rank partials are summed by one allreduce; Gram matrices and column norms are summed over
+ * the private rows of every rank plus the shared rows once (rank 0's partial).
+ * nsp_shard_plan: HOST-ONLY (no device needed) computation of that plan for (nranks, rank):
+ * gamma_local (nullable, capacity >= n_private + n_shared) receives the original ids.
+ * Returns NSP_ERR_ARG on a malformed part / rank. */
+nsp_status nsp_shard_plan(const nsp_csr* A, const int32_t* part, int K, int nranks, int rank,
+                          int64_t* n_private, int64_t* n_shared, int64_t* gamma_local, int* blk0, int* nblk);
+/* n_private / n_shared local Gamma rows and the local block range of a context. */
+nsp_status nsp_shard_info(const nsp_ctx* ctx, int64_t* n_private, int64_t* n_shared, int* blk0, int* nblk);
+/* 128-byte ncclUniqueId for opts.nccl_id (call on one rank, broadcast to all); NSP_ERR_NCCL if
+ * libnccl.so.2 cannot be loaded. */
+nsp_status nsp_nccl_unique_id(void* out128);
+/* Testing the sharded path on one device: a group for nranks (<= 16) host threads; each thread sets
+ * opts.local_group, opts.nranks, opts.rank and calls nsp_setup / the solvers concurrently.  The
+ * allreduce is then two host barriers around a rank-ordered device sum (no kernel waits on another
+ * rank's kernel).  Destroy after every context of the group. */
+void* nsp_local_group_create(int nranks);
+void nsp_local_group_destroy(void* group);
 /* orig_index: host int64[n_gamma_local]; local Gamma row -> original node id. */
 nsp_status nsp_gamma_index(const nsp_ctx* ctx, int64_t* orig_index);
 nsp_status nsp_workspace_bytes(const nsp_ctx* ctx, int s, size_t* bytes);

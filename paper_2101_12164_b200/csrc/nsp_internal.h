@@ -74,6 +74,9 @@ struct nsp_ctx {
   // Gamma-side sparse operators
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
+  DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)
+  int64_t n_priv = 0;         // local Gamma rows [0, n_priv) private, [n_priv, nG) shared (replicated)
+  struct NspComm* comm = nullptr;
 
   // A_G factor (band, RCM order): rows of the band buffer -> local Gamma index (-1 = padding)
   bool has_ag = false;

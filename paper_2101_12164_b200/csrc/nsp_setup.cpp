@@ -285,6 +285,99 @@ static nsp_status setup_gamma_factor(nsp_ctx* c, const nsp_csr* A, const int32_t
   return NSP_OK;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Shard plan: rank r owns the contiguous block range [rK/G, (r+1)K/G) - a subtree of
+// the depth-first ND leaf numbering.  A Gamma row is PRIVATE to r when every block adjacent to it is
+// owned by r and none of its A_G neighbours is private to another rank; every other Gamma row is
+// SHARED (replicated on all ranks, its S_G value completed by one allreduce of per-rank partials).
+// With G = 1 every Gamma row is private (ascending original id, reading C10).  Host only.
+// ---------------------------------------------------------------------------------------------
+struct ShardPlan {
+  int blk0 = 0, nblk = 0;
+  std::vector<int64_t> priv, shared;   // original ids, ascending
+};
+
+static int block_owner_of(int j, int K, int G) {
+  // largest q with floor(qK/G) <= j
+  int q = (int)(((int64_t)j * G + G - 1) / K);
+  while (q > 0 && (int64_t)q * K / G > j) --q;
+  while (q + 1 < G && (int64_t)(q + 1) * K / G <= j) ++q;
+  return q;
+}
+
+static bool make_shard_plan(const nsp_csr* A, const int32_t* part, int K, int G, int r, ShardPlan& P,
+                            std::string& err) {
+  if (G < 1 || G > 64 || r < 0 || r >= G) {
+    err = "nsp_setup: nranks must be in [1, 64] and 0 <= rank < nranks";
+    return false;
+  }
+  const int64_t n = A->n;
+  const int64_t* rp = A->rowptr;
+  const int32_t* ci = A->colidx;
+  const double* va = A->val;
+  P.blk0 = (int)((int64_t)r * K / G);
+  P.nblk = (int)((int64_t)(r + 1) * K / G) - P.blk0;
+  P.priv.clear();
+  P.shared.clear();
+  if (G == 1) {
+    for (int64_t i = 0; i < n; ++i)
+      if (part[i] < 0) P.priv.push_back(i);
+    return true;
+  }
+  std::vector<int> owner(K);
+  for (int j = 0; j < K; ++j) owner[j] = block_owner_of(j, K, G);
+  std::vector<int> cand(n, -2);   // -2: not Gamma, -1: shared, >= 0: private candidate of that rank
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t g = 0; g < n; ++g) {
+    if (part[g] >= 0) continue;
+    uint64_t mask = 0;
+    for (int64_t q = rp[g]; q < rp[g + 1]; ++q) {
+      const int64_t u = ci[q];
+      if (part[u] >= 0 && va[q] != 0.0) mask |= 1ull << owner[part[u]];
+    }
+    cand[g] = __builtin_popcountll(mask) == 1 ? __builtin_ctzll(mask) : -1;
+  }
+  std::vector<char> demote(n, 0);
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t g = 0; g < n; ++g) {
+    if (cand[g] < 0) continue;
+    for (int64_t q = rp[g]; q < rp[g + 1]; ++q) {
+      const int64_t h = ci[q];
+      if (h != g && cand[h] >= 0 && cand[h] != cand[g] && va[q] != 0.0) {
+        demote[g] = 1;
+        break;
+      }
+    }
+  }
+  for (int64_t g = 0; g < n; ++g) {
+    if (cand[g] == -2) continue;
+    const int o = demote[g] ? -1 : cand[g];
+    if (o < 0) P.shared.push_back(g);
+    else if (o == r) P.priv.push_back(g);
+  }
+  return true;
+}
+
+extern "C" nsp_status nsp_shard_plan(const nsp_csr* A, const int32_t* part, int K, int nranks, int rank,
+                                     int64_t* n_private, int64_t* n_shared, int64_t* gamma_local, int* blk0,
+                                     int* nblk) {
+  if (!A || !part || K <= 0 || A->n <= 0) return NSP_ERR_ARG;
+  for (int64_t i = 0; i < A->n; ++i)
+    if (part[i] < -1 || part[i] >= K) return NSP_ERR_ARG;
+  ShardPlan P;
+  std::string err;
+  if (!make_shard_plan(A, part, K, nranks, rank, P, err)) return NSP_ERR_ARG;
+  if (n_private) *n_private = (int64_t)P.priv.size();
+  if (n_shared) *n_shared = (int64_t)P.shared.size();
+  if (gamma_local) {
+    std::copy(P.priv.begin(), P.priv.end(), gamma_local);
+    std::copy(P.shared.begin(), P.shared.end(), gamma_local + P.priv.size());
+  }
+  if (blk0) *blk0 = P.blk0;
+  if (nblk) *nblk = P.nblk;
+  return NSP_OK;
+}
+
 extern "C" nsp_status nsp_setup(const nsp_csr* A, const int32_t* part, int K, const nsp_opts* opts,
                                 nsp_ctx** out, nsp_report* rep) {
   if (!out) return NSP_ERR_ARG;
@@ -298,9 +391,13 @@ extern "C" nsp_status nsp_setup(const nsp_csr* A, const int32_t* part, int K, co
   c->stream = (cudaStream_t)c->opts.stream;
   c->nranks = c->opts.nranks > 0 ? c->opts.nranks : 1;
   c->rank = c->opts.rank;
-  if (c->nranks != 1) return fail(c, NSP_ERR_ARG, "nsp_setup: multi-rank setup not built in this version");
+  if (c->nranks > 1 && (c->opts.factor_gamma || c->opts.bcg_precond))
+    return fail(c, NSP_ERR_ARG, "nsp_setup: the A_G factor (M = A_G^{-1}, M_2, PCG) is single-rank in this "
+                                "version; multi-rank runs use bcg_precond = 0 (reading C2)");
   NSP_CUDA_TRY(c, cudaSetDevice(c->device));
-  return nsp_setup_impl(c, A, part, K, rep);
+  nsp_status st = nsp_setup_impl(c, A, part, K, rep);
+  if (st != NSP_OK) return st;
+  return comm_init(c);
 }
 
 nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K, nsp_report* rep) {
@@ -369,30 +466,38 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
                                     ", " + std::to_string(sep_j) + ") between blocks " +
                                     std::to_string(part[sep_i]) + " and " + std::to_string(part[sep_j]));
 
-  // ---------------- DBBD index maps
+  // ---------------- shard plan + DBBD index maps (local blocks [B0, B0 + KL), local Gamma rows =
+  // private then shared)
+  ShardPlan plan;
+  {
+    std::string perr;
+    if (!make_shard_plan(A, part, K, c->nranks, c->rank, plan, perr)) return fail(c, NSP_ERR_ARG, perr);
+  }
+  const int B0 = plan.blk0, KL = plan.nblk;
   std::vector<int32_t> gpos(n, -1), lpos(n, -1), bidx(n, -1);
-  std::vector<std::vector<int64_t>> blocks(K);
+  std::vector<std::vector<int64_t>> blocks(KL);
+  c->gamma = plan.priv;
+  c->gamma.insert(c->gamma.end(), plan.shared.begin(), plan.shared.end());
+  for (size_t g = 0; g < c->gamma.size(); ++g) gpos[c->gamma[g]] = (int32_t)g;
+  int64_t nG_global = 0;
   for (int64_t i = 0; i < n; ++i) {
-    if (part[i] < 0) {
-      gpos[i] = (int32_t)c->gamma.size();
-      c->gamma.push_back(i);
-    } else {
-      blocks[part[i]].push_back(i);
-    }
+    if (part[i] < 0) ++nG_global;
+    else if (part[i] >= B0 && part[i] < B0 + KL) blocks[part[i] - B0].push_back(i);
   }
   c->nG = (int64_t)c->gamma.size();
-  c->nG_global = c->nG;
-  c->blk0 = 0;
-  c->nsub = K;
-  std::vector<SubHost> sh(K);
-  c->sub_n.resize(K);
-  for (int j = 0; j < K; ++j) c->sub_n[j] = (int64_t)blocks[j].size();
+  c->nG_global = nG_global;
+  c->n_priv = (int64_t)plan.priv.size();
+  c->blk0 = B0;
+  c->nsub = KL;
+  std::vector<SubHost> sh(KL);
+  c->sub_n.resize(KL);
+  for (int j = 0; j < KL; ++j) c->sub_n[j] = (int64_t)blocks[j].size();
 
   // ---------------- per-block ordering (I1 band order, B last)
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int j = 0; j < K; ++j) {
+  for (int j = 0; j < KL; ++j) {
     SubHost& S = sh[j];
-    S.j = j;
+    S.j = B0 + j;
     const auto& nodes = blocks[j];
     const int nj = (int)nodes.size();
     std::vector<int64_t> I1, Bn;
@@ -414,7 +519,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       const int64_t v = I1[k];
       for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
         const int64_t u = ci[q];
-        if (u != v && part[u] == j && lpos[u] >= 0 && va[q] != 0.0) {
+        if (u != v && part[u] == S.j && lpos[u] >= 0 && va[q] != 0.0) {
           // u in I1? (B nodes have lpos -1 at this point)
           aci.push_back(lpos[u]);
         }
@@ -441,7 +546,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       int first = S.n1;
       for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
         const int64_t u = ci[q];
-        if (part[u] == j && lpos[u] >= 0 && va[q] != 0.0) first = std::min(first, lpos[u]);
+        if (part[u] == S.j && lpos[u] >= 0 && va[q] != 0.0) first = std::min(first, lpos[u]);
       }
       bkey[k] = {first, v};
     }
@@ -460,14 +565,14 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   }
 
   // ---------------- offsets, scratch batches
-  c->subs.resize(K);
+  c->subs.resize(KL);
   int64_t band_tiles = 0, dense_tiles = 0, wvu_rows = 0;
   std::vector<int> border_first_all;
   c->max_ntb = 0;
   c->n_I = 0;
   c->n_bl = 0;
   c->max_b = 0;
-  for (int j = 0; j < K; ++j) {
+  for (int j = 0; j < KL; ++j) {
     const SubHost& S = sh[j];
     FacSub& F = c->subs[j];
     F.nt1 = S.nt1;
@@ -506,7 +611,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   {
     int j0 = 0;
     int64_t acc = 0;
-    for (int j = 0; j < K; ++j) {
+    for (int j = 0; j < KL; ++j) {
       const int64_t t = (int64_t)sh[j].ntb * sh[j].nt1;
       if (j > j0 && (size_t)(acc + t) * NSP_TILE_ELEMS * 8 > budget) {
         batches.push_back({j0, j});
@@ -516,7 +621,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       c->subs[j].border_off = acc;
       acc += t;
     }
-    batches.push_back({j0, K});
+    batches.push_back({j0, KL});
   }
   int64_t max_batch_tiles = 0;
   for (auto& bt : batches) {
@@ -529,7 +634,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
 
   // ---------------- tile entries (lower triangle of A_I_j in the new ordering)
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int j = 0; j < K; ++j) {
+  for (int j = 0; j < KL; ++j) {
     SubHost& S = sh[j];
     const FacSub& F = c->subs[j];
     const int nj = (int)S.nodes.size();
@@ -539,7 +644,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       const int li = lpos[v];
       for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
         const int64_t u = ci[q];
-        if (part[u] != j) continue;
+        if (part[u] != B0 + j) continue;
         const int lj = lpos[u];
         if (lj > li) continue;
         const double a = va[q];
@@ -571,7 +676,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   {
     // rows of W/V/U: block j, border k -> row wvu_row + k; padded rows empty
     std::vector<int64_t> rowsrc(wvu_rows, -1);
-    for (int j = 0; j < K; ++j)
+    for (int j = 0; j < KL; ++j)
       for (int k = 0; k < sh[j].b; ++k) rowsrc[c->subs[j].wvu_row + k] = sh[j].nodes[sh[j].n1 + k];
     std::vector<std::pair<int32_t, double>> ent;
     for (int64_t r = 0; r < wvu_rows; ++r) {
@@ -579,7 +684,10 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       if (v >= 0) {
         ent.clear();
         for (int64_t q = rp[v]; q < rp[v + 1]; ++q)
-          if (part[ci[q]] < 0 && va[q] != 0.0) ent.push_back({gpos[ci[q]], va[q]});
+          if (part[ci[q]] < 0 && va[q] != 0.0) {
+            if (gpos[ci[q]] < 0) return fail(c, NSP_ERR_ARG, "nsp_setup: shard plan misses a Gamma neighbour");
+            ent.push_back({gpos[ci[q]], va[q]});
+          }
         std::sort(ent.begin(), ent.end());
         for (auto& e : ent) {
           A2G.col.push_back(e.first);
@@ -589,24 +697,46 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       A2G.rowptr[r + 1] = (int32_t)A2G.col.size();
     }
   }
+  // AGG2: private rows hold every entry; shared rows hold this rank's PARTIAL (A_G entries to its
+  // private rows, -A_GI entries to its own blocks); the shared x shared part of A_G goes to AGSH,
+  // applied after the allreduce of the partials (identically on every rank).
   AGG2.rowptr.assign(c->nG + 1, 0);
+  HostCSR32 AGSH;
+  const int64_t nsh = c->nG - c->n_priv;
+  AGSH.rowptr.assign(nsh + 1, 0);
   c->nnz_AG = 0;
   c->nnz_AGI = 0;
   {
-    std::vector<std::pair<int64_t, double>> ent;
+    std::vector<std::pair<int64_t, double>> ent, esh;
     for (int64_t g = 0; g < c->nG; ++g) {
       const int64_t v = c->gamma[g];
+      const bool shared_row = g >= c->n_priv;
       ent.clear();
+      esh.clear();
       for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
         const int64_t u = ci[q];
         if (va[q] == 0.0 && u != v) continue;
         if (part[u] < 0) {
-          ent.push_back({gpos[u], va[q]});
+          if (gpos[u] < 0) continue;                            // private row of another rank
+          if (shared_row && gpos[u] >= c->n_priv) {
+            esh.push_back({gpos[u] - c->n_priv, va[q]});
+          } else {
+            ent.push_back({gpos[u], va[q]});
+          }
           c->nnz_AG++;
         } else {
-          ent.push_back({c->nG + c->subs[part[u]].wvu_row + bidx[u], -va[q]});
+          if (part[u] < B0 || part[u] >= B0 + KL) continue;     // block of another rank
+          ent.push_back({c->nG + c->subs[part[u] - B0].wvu_row + bidx[u], -va[q]});
           c->nnz_AGI++;
         }
+      }
+      if (shared_row) {
+        std::sort(esh.begin(), esh.end());
+        for (auto& e : esh) {
+          AGSH.col.push_back((int32_t)e.first);
+          AGSH.val.push_back(e.second);
+        }
+        AGSH.rowptr[g - c->n_priv + 1] = (int32_t)AGSH.col.size();
       }
       std::sort(ent.begin(), ent.end());
       for (auto& e : ent) {
@@ -618,9 +748,9 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
     }
   }
   // ---------------- full-system solve maps (nsp_pcg): band rows, original-id maps, [I | -A_B1], [I | -A_1B]
-  std::vector<int64_t> i1_row0(K);
+  std::vector<int64_t> i1_row0(KL);
   int64_t i1_rows = 0;
-  for (int j = 0; j < K; ++j) {
+  for (int j = 0; j < KL; ++j) {
     i1_row0[j] = i1_rows;
     i1_rows += (int64_t)sh[j].nt1 * NSP_TILE;
   }
@@ -633,7 +763,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   C1.rowptr.assign(i1_rows + 1, 0);
   {
     std::vector<int32_t> cnt_b(wvu_rows, 0), cnt_1(i1_rows, 0);
-    for (int j = 0; j < K; ++j) {
+    for (int j = 0; j < KL; ++j) {
       const SubHost& S = sh[j];
       for (int k = 0; k < S.n1; ++k) i1_src[i1_row0[j] + k] = (int32_t)S.nodes[k];
       for (int k = 0; k < S.b; ++k) b_src[c->subs[j].wvu_row + k] = (int32_t)S.nodes[S.n1 + k];
@@ -643,7 +773,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       ent.clear();
       for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
         const int64_t u = ci[q];
-        if (part[u] != j || u == v || va[q] == 0.0) continue;
+        if (part[u] != B0 + j || u == v || va[q] == 0.0) continue;
         const bool u_b = bidx[u] >= 0;
         if (from_b && !u_b) ent.push_back({(int32_t)(wvu_rows + i1_row0[j] + lpos[u]), -va[q]});
         if (!from_b && u_b) ent.push_back({(int32_t)(i1_rows + c->subs[j].wvu_row + bidx[u]), -va[q]});
@@ -656,7 +786,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
         const int64_t v = b_src[r];
         CB.col.push_back((int32_t)r);
         CB.val.push_back(1.0);
-        row_entries(v, part[v], true, ent);
+        row_entries(v, part[v] - B0, true, ent);
         for (auto& e : ent) {
           CB.col.push_back(e.first);
           CB.val.push_back(e.second);
@@ -669,7 +799,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
         const int64_t v = i1_src[r];
         C1.col.push_back((int32_t)r);
         C1.val.push_back(1.0);
-        row_entries(v, part[v], false, ent);
+        row_entries(v, part[v] - B0, false, ent);
         for (auto& e : ent) {
           C1.col.push_back(e.first);
           C1.val.push_back(e.second);
@@ -685,6 +815,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   nsp_status st;
   if ((st = upload_csr(c, c->A2G, A2G)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->AGG2, AGG2)) != NSP_OK) return st;
+  if ((st = upload_csr(c, c->AGSH, AGSH)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->CB, CB)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->C1, C1)) != NSP_OK) return st;
   if ((st = upload(c, &c->d_i1_src, i1_src)) != NSP_OK) return st;
@@ -699,8 +830,8 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
     NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_band, 0, (size_t)band_tiles * NSP_TILE_ELEMS * 8, c->stream));
   }
   {
-    std::vector<TriSys> ts(K);
-    for (int j = 0; j < K; ++j)
+    std::vector<TriSys> ts(KL);
+    for (int j = 0; j < KL; ++j)
       ts[j] = TriSys{c->d_band ? c->d_band + c->subs[j].band_off * NSP_TILE_ELEMS : nullptr, sh[j].nt1, sh[j].wb,
                      i1_row0[j]};
     if ((st = upload(c, &c->d_i1sys, ts)) != NSP_OK) return st;
@@ -729,14 +860,14 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
     hval.clear();
     return NSP_OK;
   };
-  for (int j = 0; j < K; ++j) {
+  for (int j = 0; j < KL; ++j) {
     hidx.insert(hidx.end(), sh[j].band_idx.begin(), sh[j].band_idx.end());
     hval.insert(hval.end(), sh[j].band_val.begin(), sh[j].band_val.end());
     std::vector<int64_t>().swap(sh[j].band_idx);
     std::vector<double>().swap(sh[j].band_val);
   }
   if ((st = flush_entries(c->d_band)) != NSP_OK) return st;
-  for (int j = 0; j < K; ++j) {
+  for (int j = 0; j < KL; ++j) {
     hidx.insert(hidx.end(), sh[j].dense_idx.begin(), sh[j].dense_idx.end());
     hval.insert(hval.end(), sh[j].dense_val.begin(), sh[j].dense_val.end());
     std::vector<int64_t>().swap(sh[j].dense_idx);
@@ -747,7 +878,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   {
     std::vector<int64_t> bt, dt;
     std::vector<int> bfr, dfr;
-    for (int j = 0; j < K; ++j) {
+    for (int j = 0; j < KL; ++j) {
       const SubHost& S = sh[j];
       if (S.nt1 > 0 && S.n1 % NSP_TILE) {
         bt.push_back(c->subs[j].band_off + (int64_t)(S.nt1 - 1) * (S.wb + 1));
@@ -786,8 +917,8 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   if (max_batch_tiles > 0)
     NSP_CUDA_TRY(c, cudaMalloc((void**)&d_scratch, (size_t)max_batch_tiles * NSP_TILE_ELEMS * 8));
   int* d_status = nullptr;
-  NSP_CUDA_TRY(c, cudaMalloc((void**)&d_status, K * sizeof(int)));
-  NSP_CUDA_TRY(c, cudaMemsetAsync(d_status, 0, K * sizeof(int), c->stream));
+  NSP_CUDA_TRY(c, cudaMalloc((void**)&d_status, KL * sizeof(int)));
+  NSP_CUDA_TRY(c, cudaMemsetAsync(d_status, 0, KL * sizeof(int), c->stream));
   for (auto& bt : batches) {
     int64_t tiles = 0;
     for (int j = bt.first; j < bt.second; ++j) {
@@ -804,14 +935,14 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
     NSP_CUDA_TRY(c, cudaGetLastError());
   }
   NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  std::vector<int> hstat(K);
-  NSP_CUDA_TRY(c, cudaMemcpy(hstat.data(), d_status, K * sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<int> hstat(KL);
+  NSP_CUDA_TRY(c, cudaMemcpy(hstat.data(), d_status, KL * sizeof(int), cudaMemcpyDeviceToHost));
   cudaFree(d_status);
   cudaFree(d_scratch);
   cudaFree(d_idx);
   cudaFree(d_val);
   const double t_fac = ms_since(t2);
-  for (int j = 0; j < K; ++j)
+  for (int j = 0; j < KL; ++j)
     if (hstat[j] != 0) {
       const int lrow = hstat[j] - 1;
       const SubHost& S = sh[j];
@@ -819,7 +950,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       if (lrow < S.n1) orig = S.nodes[lrow];
       else if (lrow >= S.nt1 * NSP_TILE && lrow - S.nt1 * NSP_TILE < S.b) orig = S.nodes[S.n1 + lrow - S.nt1 * NSP_TILE];
       if (rep) {
-        rep->bad_block = j;
+        rep->bad_block = B0 + j;
         rep->bad_pivot = orig;
         rep->status = NSP_ERR_NOT_SPD;
       }
