@@ -3,6 +3,7 @@
 #include <cstring>
 #include <string>
 
+#include "nsp_comm.h"
 #include "nsp_internal.h"
 #include "nsp_solver.h"
 
@@ -53,6 +54,21 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   // a4 + a5: Y = A_G X - A_GI U (fused), or Y = A_GI U
   nspk::spmm(c->AGG2, X, ldx, wvu, ldw, c->nG, Y, ldy, s, mode, true, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());
+  return finish_shared_rows(c, X, ldx, Y, ldy, s, mode != 2);
+}
+
+// Multi-rank: the shared rows of Y hold this rank's partial; sum the partials over ranks (one
+// allreduce) and add the shared x shared A_G term (identically on every rank).  No-op for 1 rank.
+nsp_status finish_shared_rows(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, bool ag_term) {
+  if (c->nranks <= 1) return NSP_OK;
+  const int64_t nsh = c->nG - c->n_priv;
+  if (nsh <= 0) return NSP_OK;
+  nsp_status e = comm_allreduce(c, Y + c->n_priv * (int64_t)ldy, (size_t)nsh * ldy);
+  if (e != NSP_OK) return e;
+  if (ag_term)
+    nspk::spmm(c->AGSH, X + c->n_priv * (int64_t)ldx, ldx, nullptr, 0, 0, Y + c->n_priv * (int64_t)ldy, ldy, s, 4,
+               false, c->stream);
+  NSP_CUDA_TRY(c, cudaGetLastError());
   return NSP_OK;
 }
 
@@ -68,6 +84,15 @@ nsp_status nsp_dims(const nsp_ctx* c, int64_t* n, int64_t* n_gamma, int64_t* n_g
   if (n_gamma) *n_gamma = c->nG_global;
   if (n_gamma_local) *n_gamma_local = c->nG;
   if (K_local) *K_local = c->nsub;
+  return NSP_OK;
+}
+
+nsp_status nsp_shard_info(const nsp_ctx* c, int64_t* n_private, int64_t* n_shared, int* blk0, int* nblk) {
+  if (!c) return NSP_ERR_ARG;
+  if (n_private) *n_private = c->n_priv;
+  if (n_shared) *n_shared = c->nG - c->n_priv;
+  if (blk0) *blk0 = c->blk0;
+  if (nblk) *nblk = c->nsub;
   return NSP_OK;
 }
 
@@ -148,7 +173,7 @@ nsp_status nsp_gamma_apply(nsp_ctx* c, const double* X, double* Y, int s) {
   if (!c || !X || !Y || s <= 0 || s > 256) return NSP_ERR_ARG;
   nspk::spmm(c->AGG2, X, s, nullptr, 0, c->nG, Y, s, s, 3, false, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());
-  return NSP_OK;
+  return finish_shared_rows(c, X, s, Y, s, s, true);
 }
 
 const char* nsp_last_error(const nsp_ctx* c) { return c ? c->err.c_str() : "null context"; }
@@ -172,7 +197,8 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_g_src);
   fr(c->d_Z);
   fr(c->d_sigma);
-  for (DevCSR* m : {&c->A2G, &c->AGG2, &c->CB, &c->C1}) {
+  comm_free(c);
+  for (DevCSR* m : {&c->A2G, &c->AGG2, &c->AGSH, &c->CB, &c->C1}) {
     fr(m->rowptr);
     fr(m->col);
     fr(m->val);

@@ -129,7 +129,8 @@ void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, do
                    const int* border_first, int* status, cudaStream_t st);
 // Y[r, c] (c < s) = sum_k val_k * X(col_k, c); mode 0: Y = A X (X ld ldx);
 // mode 1: Y = A [X ; U] with cols >= split reading U (ld ldu) at col-split;
-// mode 2: Y = -(cols >= split part only)  (K_G apply); mode 3: cols < split only (A_G X)
+// mode 2: Y = -(cols >= split part only)  (K_G apply); mode 3: cols < split only (A_G X);
+// mode 4: Y += A X
 // Y ld ldy; columns s..ldy-1 of Y are written with 0 when zero_pad.
 void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split,
           double* Y, int ldy, int s, int mode, bool zero_pad, cudaStream_t st);

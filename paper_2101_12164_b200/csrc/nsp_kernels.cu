@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __res
       const int64_t col = __shfl_sync(0xffffffffu, c, q);
       double a = __shfl_sync(0xffffffffu, v, q);
       const double* src;
-      if (mode == 0 || col < split) {
+      if (mode == 0 || mode == 4 || col < split) {
         if (mode == 2) continue;
         src = X + col * ldx;
       } else {
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __res
 #pragma unroll
   for (int qq = 0; qq < NQ; ++qq) {
     const int cc = lane + 32 * qq;
-    if (cc < s) y[cc] = acc[qq];
+    if (cc < s) y[cc] = mode == 4 ? y[cc] + acc[qq] : acc[qq];
     else if (zero_pad && cc < ldy) y[cc] = 0.0;
   }
   if (zero_pad)

@@ -21,7 +21,10 @@
 
 #include <omp.h>
 
+#include "nsp_comm.h"
 #include "nsp_internal.h"
+
+using nspi::comm_init;
 
 namespace {
 

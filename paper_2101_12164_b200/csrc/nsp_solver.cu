@@ -13,6 +13,7 @@
 #include <string>
 
 #include "nsp_blas.h"
+#include "nsp_comm.h"
 #include "nsp_solver.h"
 
 namespace nspi {
@@ -133,16 +134,23 @@ static nsp_status read_status(nsp_ctx* c, BcgStatus* d, BcgStatus* h) {
   return NSP_OK;
 }
 
+// Rows of the local block that enter Grams and norms: all local rows on one rank; with several
+// ranks the private rows of every rank plus the shared rows once (rank 0), SURVEY.md §8(e).
+static int64_t gram_rows(const nsp_ctx* c) { return (c->nranks <= 1 || c->rank == 0) ? c->nG : c->n_priv; }
+
 // orth(Wm): Gram, Cholesky-QR with pivot test, eigen fallback; P = Wm T (reading C3)
-static void orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Pout) {
+static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Pout) {
   const int sp = w.sp;
   const int64_t n = c->nG;
   cudaStream_t st = c->stream;
-  nspb::gram(Wm, sp, sp, Wm, sp, sp, n, w.G, sp, w.gram, st);
+  nspb::gram(Wm, sp, sp, Wm, sp, sp, gram_rows(c), w.G, sp, w.gram, st);
+  nsp_status e = comm_allreduce(c, w.G, (size_t)sp * sp);
+  if (e != NSP_OK) return e;
   nspb::small_chol(w.G, sp, 1, s, c->opts.orth_tau, w.T, w.st, st);
   nspb::small_eig(w.G, sp, s, w.Vw, sp + 1, w.lam, w.Vs, &w.st->fallback, st);
   nspb::orth_from_eig(w.lam, w.Vs, s, sp, c->opts.orth_tau, w.T, w.st, st);
   nspb::panel(Pout, sp, nullptr, 0, Wm, sp, w.T, sp, sp, sp, n, 1.0, nullptr, st);
+  return NSP_OK;
 }
 
 // Z = M R
@@ -163,14 +171,18 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   // init: X = 0, R = B, bnorm
   NSP_CUDA_TRY(c, cudaMemsetAsync(w.X, 0, (size_t)n * sp * 8, st));
   nspb::copy_pad(B, ldb, w.R, sp, n, s, 1.0, st);
-  nspb::colsq(w.R, sp, n, s, sp, w.npart, w.rsq, st);
+  const int64_t ng = gram_rows(c);
+  const bool multi = c->nranks > 1;
+  nsp_status e;
+  nspb::colsq(w.R, sp, ng, s, sp, w.npart, w.rsq, st);
+  if ((e = comm_allreduce(c, w.rsq, sp)) != NSP_OK) return e;
   nspb::sqrt_vec(w.rsq, w.bnorm, sp, st);
   BcgStatus init{};
   init.width = s;
   std::memcpy(hs, &init, sizeof(init));
   NSP_CUDA_TRY(c, cudaMemcpyAsync(w.st, hs, sizeof(BcgStatus), cudaMemcpyHostToDevice, st));
   nspb::converge(w.rsq, w.bnorm, s, tol, w.st, nullptr, st);
-  nsp_status e = read_status(c, w.st, hs);
+  e = read_status(c, w.st, hs);
   if (e != NSP_OK) return e;
   if (rep && rep->hist && rep->hist_cap > 0) rep->hist[0] = hs->relres;
   double relres = hs->relres;
@@ -183,14 +195,17 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
       if ((e = precond(c, w.R, w.Z, sp, s, w.wvu)) != NSP_OK) return e;
       Zr = w.Z;
     }
-    orth(c, w, Zr, s, w.P);
+    if ((e = orth(c, w, Zr, s, w.P)) != NSP_OK) return e;
     for (int it = 0; it < maxit; ++it) {
       // a1-a5: Q = S_G P
       tr.mark("loop");
       if ((e = apply_into(c, w.P, sp, w.Q, sp, s, 1, w.wvu)) != NSP_OK) return e;
       tr.mark("apply");
       // a6: D = P^T Q, E = P^T R
-      nspb::gram2(w.P, sp, sp, w.Q, w.R, sp, sp, n, w.D, w.E, sp, w.gram, st);
+      nspb::gram2(w.P, sp, sp, w.Q, w.R, sp, sp, ng, w.D, w.E, sp, w.gram, st);
+      if (multi) {   // D and E are adjacent in the workspace: one allreduce
+        if ((e = comm_allreduce(c, w.D, (size_t)2 * sp * sp)) != NSP_OK) return e;
+      }
       tr.mark("gram_DE");
       // a7: chol(D), alpha = D^{-1} E
       nspb::small_chol(w.D, sp, 0, -1, 0.0, w.Ldi, w.st, st);   // Ldi = D^{-1}
@@ -200,10 +215,15 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
       // a8: X += P alpha, R -= Q alpha, column norms
       {
         PanelArgs px{w.X, sp, w.X, sp, w.P, sp, w.al, sp, 1.0, nullptr};
-        PanelArgs pr{w.R, sp, w.R, sp, w.Q, sp, w.al, sp, -1.0, w.npart};
+        PanelArgs pr{w.R, sp, w.R, sp, w.Q, sp, w.al, sp, -1.0, multi ? nullptr : w.npart};
         nspb::panel2(px, &pr, sp, sp, n, st);
       }
-      nspb::colsq_reduce(w.npart, (int)((n + 63) / 64), sp, w.rsq, st);
+      if (multi) {
+        nspb::colsq(w.R, sp, ng, s, sp, w.npart, w.rsq, st);
+        if ((e = comm_allreduce(c, w.rsq, sp)) != NSP_OK) return e;
+      } else {
+        nspb::colsq_reduce(w.npart, (int)((n + 63) / 64), sp, w.rsq, st);
+      }
       double* hslot = nullptr;
       nspb::converge(w.rsq, w.bnorm, s, tol, w.st, hslot, st);
       tr.mark("XR_update");
@@ -241,13 +261,14 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
         Zr = w.Z;
       }
       // a10: F = Q^T Z, beta = -D^{-1} F, W = Z + P beta
-      nspb::gram(w.Q, sp, sp, Zr, sp, sp, n, w.F, sp, w.gram, st);
+      nspb::gram(w.Q, sp, sp, Zr, sp, sp, ng, w.F, sp, w.gram, st);
+      if ((e = comm_allreduce(c, w.F, (size_t)sp * sp)) != NSP_OK) return e;
       nspb::panel(w.be, sp, nullptr, 0, w.Ldi, sp, w.F, sp, sp, sp, sp, -1.0, nullptr, st);
       tr.mark("beta");
       nspb::panel(w.W, sp, Zr, sp, w.P, sp, w.be, sp, sp, sp, n, 1.0, nullptr, st);
       tr.mark("W");
       // a11: P = orth(W)
-      orth(c, w, w.W, s, w.P);
+      if ((e = orth(c, w, w.W, s, w.P)) != NSP_OK) return e;
       tr.mark("orth");
     }
   }

@@ -21,7 +21,8 @@ NSP_STATUS = {0: "NSP_OK", 1: "NSP_NOT_CONVERGED", -1: "NSP_ERR_ARG", -2: "NSP_E
 EXPORTED = ["nsp_default_opts", "nsp_setup", "nsp_dims", "nsp_gamma_index", "nsp_workspace_bytes",
             "nsp_stats", "nsp_schur_apply", "nsp_kgamma_apply", "nsp_block_cg", "nsp_nystrom",
             "nsp_nystrom_sigma", "nsp_precond_apply", "nsp_pcg", "nsp_last_error", "nsp_destroy",
-            "nsp_gamma_apply", "nsp_kernel_launches", "nsp_profile", "nsp_profile_read"]
+            "nsp_gamma_apply", "nsp_kernel_launches", "nsp_profile", "nsp_profile_read", "nsp_shard_plan",
+            "nsp_shard_info", "nsp_nccl_unique_id", "nsp_local_group_create", "nsp_local_group_destroy"]
 
 
 class nsp_csr(C.Structure):
@@ -32,7 +33,7 @@ class nsp_opts(C.Structure):
     _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("nranks", C.c_int), ("rank", C.c_int),
                 ("nccl_id", C.c_void_p), ("bcg_precond", C.c_int), ("factor_gamma", C.c_int),
                 ("orth_tau", C.c_double), ("nys_eps_rel", C.c_double), ("scratch_bytes", C.c_size_t),
-                ("verbose", C.c_int)]
+                ("verbose", C.c_int), ("local_group", C.c_void_p)]
 
 
 class nsp_report(C.Structure):
@@ -79,12 +80,20 @@ def load_library(path: str = LIB_PATH):
     lib.nsp_gamma_apply.argtypes = [P, P, P, I]
     lib.nsp_profile.argtypes = [P, I]
     lib.nsp_profile_read.argtypes = [P, P, P]
+    lib.nsp_shard_plan.argtypes = [P, P, I, I, I, P, P, P, P, P]
+    lib.nsp_shard_info.argtypes = [P, P, P, P, P]
+    lib.nsp_nccl_unique_id.argtypes = [P]
+    lib.nsp_local_group_create.argtypes = [I]
+    lib.nsp_local_group_create.restype = C.c_void_p
+    lib.nsp_local_group_destroy.argtypes = [P]
+    lib.nsp_local_group_destroy.restype = None
     lib.nsp_kernel_launches.argtypes = []
     lib.nsp_kernel_launches.restype = C.c_longlong
     lib.nsp_destroy.argtypes = [P]
     lib.nsp_destroy.restype = None
     for f in EXPORTED:
-        if f not in ("nsp_default_opts", "nsp_last_error", "nsp_destroy", "nsp_kernel_launches"):
+        if f not in ("nsp_default_opts", "nsp_last_error", "nsp_destroy", "nsp_kernel_launches",
+                     "nsp_local_group_create", "nsp_local_group_destroy"):
             getattr(lib, f).restype = C.c_int
     _lib = lib
     return lib
@@ -117,12 +126,53 @@ def kernel_launches() -> int:
     return int(load_library().nsp_kernel_launches())
 
 
+def shard_plan(rowptr, colidx, val, part, K, nranks, rank):
+    """Host-only shard plan (no device needed): dict(n_private, n_shared, gamma_local, blk0, nblk)."""
+    lib = load_library()
+    rp = np.ascontiguousarray(rowptr, dtype=np.int64)
+    ci = np.ascontiguousarray(colidx, dtype=np.int32)
+    va = np.ascontiguousarray(val, dtype=np.float64)
+    pa = np.ascontiguousarray(part, dtype=np.int32)
+    csr = nsp_csr(rp.size - 1, rp.ctypes.data, ci.ctypes.data, va.ctypes.data)
+    npv, nsh, b0, nb = C.c_int64(), C.c_int64(), C.c_int(), C.c_int()
+    st = lib.nsp_shard_plan(C.byref(csr), pa.ctypes.data, K, nranks, rank, C.byref(npv), C.byref(nsh), None,
+                            C.byref(b0), C.byref(nb))
+    if st != 0:
+        raise NspError(st, "nsp_shard_plan failed")
+    gl = np.empty(npv.value + nsh.value, dtype=np.int64)
+    lib.nsp_shard_plan(C.byref(csr), pa.ctypes.data, K, nranks, rank, None, None, gl.ctypes.data, None, None)
+    return dict(n_private=npv.value, n_shared=nsh.value, gamma_local=gl, blk0=b0.value, nblk=nb.value)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = load_library().nsp_nccl_unique_id(buf)
+    if st != 0:
+        raise NspError(st, "nsp_nccl_unique_id: libnccl.so.2 not loadable")
+    return buf.raw
+
+
+class LocalGroup:
+    """nranks host threads driving ranks on ONE device (testing the sharded path; no NCCL)."""
+
+    def __init__(self, nranks):
+        self.lib = load_library()
+        self.handle = self.lib.nsp_local_group_create(nranks)
+        if not self.handle:
+            raise ValueError("nranks must be in [1, 16]")
+
+    def close(self):
+        if self.handle:
+            self.lib.nsp_local_group_destroy(self.handle)
+            self.handle = None
+
+
 class Context:
     """nsp_ctx owner.  A: (rowptr int64, colidx int32, val float64) host arrays."""
 
     def __init__(self, rowptr, colidx, val, part, K, device=0, stream=None, bcg_precond=0,
                  factor_gamma=False, orth_tau=1e-14, nys_eps_rel=1e-12, nranks=1, rank=0,
-                 nccl_id: bytes | None = None, scratch_bytes=0):
+                 nccl_id: bytes | None = None, scratch_bytes=0, local_group: "LocalGroup | None" = None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("CUDA device required (no CPU fallback)")
@@ -145,6 +195,7 @@ class Context:
         o.bcg_precond = bcg_precond
         o.factor_gamma = int(bool(factor_gamma or bcg_precond))
         o.orth_tau, o.nys_eps_rel, o.scratch_bytes = orth_tau, nys_eps_rel, scratch_bytes
+        o.local_group = local_group.handle if local_group is not None else None
         self.opts = o
         self.ctx = C.c_void_p()
         rep = nsp_report()
@@ -158,6 +209,9 @@ class Context:
         n, ng, ngl, kl = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
         self._check(self.lib.nsp_dims(self.ctx, C.byref(n), C.byref(ng), C.byref(ngl), C.byref(kl)))
         self.n, self.n_gamma, self.n_gamma_local, self.K_local = n.value, ng.value, ngl.value, kl.value
+        npv, nsh, b0, nb = C.c_int64(), C.c_int64(), C.c_int(), C.c_int()
+        self._check(self.lib.nsp_shard_info(self.ctx, C.byref(npv), C.byref(nsh), C.byref(b0), C.byref(nb)))
+        self.n_private, self.n_shared, self.blk0 = npv.value, nsh.value, b0.value
 
     def _check(self, st):
         if st < 0:
