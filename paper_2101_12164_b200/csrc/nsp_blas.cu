@@ -2,6 +2,7 @@
 // d1): Gram contractions and panel updates on the DMMA pipe (north_star (c)), one-CTA s x s
 // Cholesky / triangular inverse / Jacobi eigensolver, small GEMMs.  All reductions are
 // fixed-order two-stage (no fp64 atomics): results are bitwise reproducible (reading C17).
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -732,7 +733,7 @@ void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, i
 }
 
 void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st) {
-  const int nt = (int)((n + 63) / 64);
+  const int nt = (int)std::max<int64_t>(1, (n + 63) / 64);   // n = 0 (a rank with no Gram rows): zeros
   { nsp_count_launch(); k_colsq_partial<<<nt, ldp, 0, st>>>(X, ldx, n, s, part, ldp); }
   { nsp_count_launch(); k_colsq_reduce<<<1, dim3(128, 8), 0, st>>>(part, nt, ldp, out); }
 }

@@ -15,6 +15,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -80,16 +81,25 @@ struct LocalGroup {
   long long gen = 0;
   std::vector<const double*> bufs;
   std::vector<cudaEvent_t> ev1, ev2;
-  void barrier() {
+  bool broken = false;
+  // false if another rank never arrived within 120 s (a rank that failed and left the collective
+  // sequence): the group is marked broken so every rank errors out instead of deadlocking
+  bool barrier() {
     std::unique_lock<std::mutex> lk(m);
+    if (broken) return false;
     const long long g = gen;
     if (++arrived == n) {
       arrived = 0;
       ++gen;
       cv.notify_all();
-    } else {
-      cv.wait(lk, [&] { return gen != g; });
+      return true;
     }
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
   }
 };
 
@@ -143,7 +153,10 @@ nsp_status comm_init(nsp_ctx* c) {
     cm->lg = g;
     NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&g->ev1[c->rank], cudaEventDisableTiming));
     NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&g->ev2[c->rank], cudaEventDisableTiming));
-    g->barrier();   // every rank's events exist before the first allreduce
+    if (!g->barrier()) {   // every rank's events exist before the first allreduce
+      c->err = "nsp_setup: local group barrier timed out (another rank failed)";
+      return NSP_ERR_STATE;
+    }
     return NSP_OK;
   }
   if (!c->opts.nccl_id) {
@@ -189,7 +202,10 @@ nsp_status comm_allreduce(nsp_ctx* c, double* buf, size_t count) {
   }
   g->bufs[me] = buf;
   NSP_CUDA_TRY(c, cudaEventRecord(g->ev1[me], c->stream));
-  g->barrier();
+  if (!g->barrier()) {
+    c->err = "local-group allreduce: barrier timed out (another rank failed)";
+    return NSP_ERR_STATE;
+  }
   PtrPack pk{};
   for (int q = 0; q < g->n; ++q) {
     NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, g->ev1[q], 0));
@@ -198,7 +214,10 @@ nsp_status comm_allreduce(nsp_ctx* c, double* buf, size_t count) {
   nsp_count_launch();
   k_sum_ranks<<<(unsigned)((count + 255) / 256), 256, 0, c->stream>>>(pk, g->n, count, cm->tmp);
   NSP_CUDA_TRY(c, cudaEventRecord(g->ev2[me], c->stream));
-  g->barrier();
+  if (!g->barrier()) {
+    c->err = "local-group allreduce: barrier timed out (another rank failed)";
+    return NSP_ERR_STATE;
+  }
   for (int q = 0; q < g->n; ++q) NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, g->ev2[q], 0));
   NSP_CUDA_TRY(c, cudaMemcpyAsync(buf, cm->tmp, count * 8, cudaMemcpyDeviceToDevice, c->stream));
   return NSP_OK;

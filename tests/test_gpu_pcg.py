@@ -11,7 +11,9 @@ from tests.gpu_util import context, dev, problem
 
 pytestmark = pytest.mark.gpu
 
-NAMES = ["cfg1", "cfg2s", "cfg5s", "cfg3s"]
+# the configs BASELINE.json runs the outer PCG on (cfg1, cfg2, cfg5: "outer PCG tol 1e-8"); cfg3 / cfg4
+# run block CG only
+NAMES = ["cfg1", "cfg2s", "cfg5s"]
 
 
 def _rel(a, b):
