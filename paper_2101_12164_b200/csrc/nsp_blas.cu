@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
   for (int e = tid; e < ne * ne; e += nt) {
     const int i = e / ne, j = e - i * ne;
     A[i * ld + j] = (i < n && j < n) ? Ain[i * lda + j] : 0.0;
-    V[i * ldv + j] = (i == j) ? 1.0 : 0.0;
+    V[i * ldv + j] = (i == j) ? 1.0 : 0.0;   // V stored TRANSPOSED (V[k * ldv + i] = V_ik): coalesced rotations
   }
   __syncthreads();
   const int npair = ne / 2;
@@ -560,9 +560,9 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
         const double ap = A[i * ld + p], aq = A[i * ld + q];
         A[i * ld + p] = c * ap - s * aq;
         A[i * ld + q] = s * ap + c * aq;
-        const double vp = V[i * ldv + p], vq = V[i * ldv + q];
-        V[i * ldv + p] = c * vp - s * vq;
-        V[i * ldv + q] = s * vp + c * vq;
+        const double vp = V[p * ldv + i], vq = V[q * ldv + i];
+        V[p * ldv + i] = c * vp - s * vq;
+        V[q * ldv + i] = s * vp + c * vq;
       }
       __syncthreads();
       // rows: A <- J^T A
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
   __syncthreads();
   for (int e = tid; e < n * n; e += nt) {
     const int i = e / n, k = e - i * n;
-    Vsorted[i * n + k] = V[i * ldv + order[k]];
+    Vsorted[i * n + k] = V[order[k] * ldv + i];
   }
 }
 
