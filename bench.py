@@ -31,12 +31,12 @@ UNIT = "RHS-applies/s"
 FP64_PEAK_TFLOPS = 37.05  # DMMA m8n8k4 microbenchmark, tools/fp64_peak.cu -> profiles/r01_fp64_peak.txt
 
 
-def _traffic(workload):
+def _traffic(workload, kernel="k_symm"):
     """dram bytes per launch of the dominant kernel from one committed `ncu --set full` capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f).get(workload)
-        return (t["dram_bytes_per_launch"], t["source"]) if t else (None, None)
+        return (t["dram_bytes_per_launch"], t["source"]) if t and t.get("kernel") == kernel else (None, None)
     except Exception:
         return None, None
 
@@ -258,6 +258,25 @@ def run_ours(args, ws, rank, local):
         if i >= 3:
             at.append(ev0.elapsed_time(ev1))
     t_apply = statistics.median(at)
+    # the same apply with the two batched L22 triangular sweeps (north_star (b) literal kernel)
+    ctx_sw = nsp.Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, device=local,
+                         stream=stream.cuda_stream, nranks=ws, rank=rank, nccl_id=nccl_id, apply_kernel=1) \
+        if ws == 1 else None
+    t_apply_sweeps = None
+    if ctx_sw is not None:
+        ws_sw = torch.empty(ctx_sw.workspace_bytes(s), dtype=torch.uint8, device=dev)
+        at2 = []
+        for i in range(args.apply_reps + 3):
+            flush.zero_()
+            ev0.record(stream)
+            ctx_sw.schur_apply(P_, Q_, ws_sw)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            if i >= 3:
+                at2.append(ev0.elapsed_time(ev1))
+        t_apply_sweeps = statistics.median(at2)
+        ctx_sw.close()
+        del ws_sw
     # e2e: Omega from pinned host memory, Y back to pinned host memory, inside the timed region
     et = []
     for _ in range(max(1, args.steps)):
@@ -283,9 +302,9 @@ def run_ours(args, ws, rank, local):
     sweep_avg_ms = sweep_ms / max(sweeps, 1)
     flops_per_launch = 2.0 * st["sum_b2"] * s      # forward + backward: 2 * b_j^2 * s per block
     achieved = flops_per_launch / (sweep_avg_ms * 1e-3) / 1e12
-    # algorithmic bytes: the unpadded lower triangle of every L22 streamed once per sweep (2 sweeps)
-    # + W in + U out (s-wide boundary-layer rows)
-    hbm_alg = 2 * 8 * (st["sum_b2"] + st["sum_b"]) / 2 + 2 * 8 * s * st["sum_b"]
+    # algorithmic bytes: the unpadded lower triangle of every S_j^{-1} streamed once (k_symm: each
+    # stored tile serves two output rows) + W in + U out (s-wide boundary-layer rows)
+    hbm_alg = 8 * (st["sum_b2"] + st["sum_b"]) / 2 + 2 * 8 * s * st["sum_b"]
     peaks = _peaks()
     traffic, traffic_src = _traffic(args.config)
     line = {
@@ -298,8 +317,10 @@ def run_ours(args, ws, rank, local):
                    else "1gpu", "n_gamma_global": ctx.n_gamma, "shared_rows": ctx.n_shared,
                    "l2": "flushed (256 MiB write) before every timed step"},
         "time_to_tol_ms": tmax, "bcg_iters": it_mean,
-        "apply": {"ms": t_apply, "rhs_applies_per_s": s / (t_apply * 1e-3)},
-        "roofline": {"kernel": "k_trsm_fb (a2+a3 batched L22 sweeps)", "bound": "tensor",
+        "apply": {"ms": t_apply, "rhs_applies_per_s": s / (t_apply * 1e-3), "a2a3": "k_symm (explicit S_j^-1 tiles)",
+                  "sweeps_ms": t_apply_sweeps,
+                  "sweeps_rhs_applies_per_s": s / (t_apply_sweeps * 1e-3) if t_apply_sweeps else None},
+        "roofline": {"kernel": "k_symm (a2+a3: U_j = S_j^-1 W_j, all blocks one launch)", "bound": "tensor",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": hbm_alg,

@@ -76,6 +76,9 @@ typedef struct {
   int verbose;
   void* local_group;     /* testing only: nsp_local_group_create(nranks) handle shared by nranks host
                             threads driving ranks on ONE device (replaces NCCL); NULL otherwise */
+  int apply_kernel;      /* a2+a3 of the S_G apply: 0 = one symmetric product with the explicit
+                            S_j^{-1} = L22^{-T} L22^{-1} tiles formed in setup (default); 1 = the
+                            two batched triangular sweeps with L22 (no extra memory) */
 } nsp_opts;
 
 /* Solver / setup report; caller-owned.  hist / widths are optional caller
@@ -91,7 +94,8 @@ typedef struct {
   long long bad_pivot;             /* NOT_SPD: original node id of the failing pivot */
   int rank;                        /* Nystrom: rank of the approximation (min(r, k)) */
   int fallbacks;                   /* block CG: eigen-fallback orthonormalisations */
-  double t_ms[8];                  /* setup: [0] host analysis, [1] H2D, [2] GPU factor, [3] A_G factor */
+  double t_ms[8];                  /* setup: [0] host analysis, [1] H2D, [2] GPU factor, [3] A_G factor,
+                                      [4] S_j^{-1} tiles (apply_kernel 0) */
 } nsp_report;
 
 void nsp_default_opts(nsp_opts* o);

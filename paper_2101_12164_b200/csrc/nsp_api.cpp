@@ -1,5 +1,6 @@
 // Context queries, workspace management and the S_G / K_G block applies (§8(a) rows a0-a5).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -11,14 +12,16 @@ namespace nspi {
 
 int pick_cw(const nsp_ctx* c, int s) {
   const int tiles64 = (s + 63) / 64;
-  return (s > 32 && (int64_t)c->nsub * tiles64 >= 2 * 148) ? 64 : 32;
+  if (const char* e = getenv("NSP_CW")) return atoi(e) == 64 && s > 32 ? 64 : 32;   // tuning override
+  const int64_t work = c->d_minv ? (int64_t)c->n_items : (int64_t)c->nsub;
+  return (s > 32 && work * tiles64 >= 2 * 148) ? 64 : 32;
 }
 
 int ld_pad(int s, int cw) { return ((s + cw - 1) / cw) * cw; }
 
 size_t apply_ws_bytes(const nsp_ctx* c, int s) {
   const int cw = pick_cw(c, s);
-  return (size_t)c->wvu_rows * ld_pad(s, cw) * 8 + 256;
+  return (size_t)c->wvu_rows * ld_pad(s, cw) * 8 * (c->d_minv ? 2 : 1) + 512;
 }
 
 nsp_status get_ws(nsp_ctx* c, void* ws, size_t need, char** out) {
@@ -43,16 +46,23 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   const int ldw = ld_pad(s, cw);
   // a1: W = A_IG X on the boundary-layer rows (zero padding rows / columns)
   nspk::spmm(c->A2G, X, ldx, nullptr, 0, 0, wvu, ldw, s, 0, true, c->stream);
-  // a2 + a3: V = L22^{-1} W, U = L22^{-T} V for every block, one launch
+  // a2 + a3: U = L22^{-T} L22^{-1} W for every block, one launch: either as one symmetric product
+  // with the setup's S_j^{-1} tiles (k_symm, no dependency chain) or as the two batched sweeps
   const bool prof = c->prof_on && (size_t)(c->prof_used + 2) <= c->prof_ev.size();
   if (prof) cudaEventRecord(c->prof_ev[c->prof_used], c->stream);
-  nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, wvu, ldw, cw, c->stream);
+  double* U = wvu;
+  if (c->d_minv) {
+    U = wvu + c->wvu_rows * (int64_t)ldw;
+    nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream);
+  } else {
+    nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, wvu, ldw, cw, c->stream);
+  }
   if (prof) {
     cudaEventRecord(c->prof_ev[c->prof_used + 1], c->stream);
     c->prof_used += 2;
   }
   // a4 + a5: Y = A_G X - A_GI U (fused), or Y = A_GI U
-  nspk::spmm(c->AGG2, X, ldx, wvu, ldw, c->nG, Y, ldy, s, mode, true, c->stream);
+  nspk::spmm(c->AGG2, X, ldx, U, ldw, c->nG, Y, ldy, s, mode, true, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());
   return finish_shared_rows(c, X, ldx, Y, ldy, s, mode != 2);
 }
@@ -192,6 +202,8 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_gperm);
   fr(c->d_gperm_inv);
   fr(c->d_i1sys);
+  fr(c->d_minv);
+  fr(c->d_items);
   fr(c->d_i1_src);
   fr(c->d_b_src);
   fr(c->d_g_src);

@@ -72,6 +72,10 @@ struct nsp_ctx {
   int max_ntb = 0;
 
   // Gamma-side sparse operators
+  // a2+a3 as one symmetric product (opts.apply_kernel = 0): M_j = S_j^{-1} tiles + work items
+  double* d_minv = nullptr;
+  int2* d_items = nullptr;
+  int n_items = 0;
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
   DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)
@@ -136,6 +140,11 @@ void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, i
           double* Y, int ldy, int s, int mode, bool zero_pad, cudaStream_t st);
 void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw,
              cudaStream_t st);
+// setup: M_j = S_j^{-1} = L22^{-T} L22^{-1} tiles (same layout as the L22 tiles)
+void l22_inverse(const FacSub* subs, int nsub, int max_ntb, const double* dense, double* minv, cudaStream_t st);
+// a2+a3 as U_j = M_j W_j (items = (block, tile row)), W -> U out of place
+void symm(const FacSub* subs, const int2* items, int nitems, const double* minv, const double* W, double* U, int ldw,
+          int cw, cudaStream_t st);
 void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st);
 void gather_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,
                  double scale, cudaStream_t st);

@@ -390,6 +390,189 @@ __global__ void __launch_bounds__(256) k_trsm_fb(const FacSub* __restrict__ subs
 }
 
 // ---------------------------------------------------------------------------------------------
+// s0 (setup, after the factorisation): explicit M_j = S_j^{-1} = L22^{-T} L22^{-1} of every block's
+// boundary-layer Schur complement, lower tiles in the L22 tile layout (diagonal tiles full).
+// One CTA per (block, tile column C): tile column C of M = L^{-T} L^{-1} E_C computed in place in
+// M's own tile column (forward sweep from tile row C, backward sweep down to C).
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ subs, const double* __restrict__ dense,
+                                                     double* minv) {
+  constexpr int NF = 4;
+  constexpr int LDV = 68;
+  extern __shared__ double sm[];
+  double* Ls0 = sm;
+  double* Ls1 = sm + 64 * LDT;
+  double* Vs0 = sm + 2 * 64 * LDT;
+  double* Vs1 = Vs0 + 64 * LDV;
+  const FacSub sb = subs[blockIdx.x];
+  const int ntb = sb.ntb, C = blockIdx.y;
+  if (C >= ntb) return;
+  const double* T = dense + sb.dense_off * NSP_TILE_ELEMS;
+  double* Mb = minv + sb.dense_off * NSP_TILE_ELEMS;
+  auto tile = [&](int I, int J) { return T + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS; };
+  auto vt = [&](int I) { return Mb + ((int64_t)I * (I + 1) / 2 + C) * NSP_TILE_ELEMS; };   // row tile I of the RHS
+  for (int I = C; I < ntb; ++I)
+    for (int e = threadIdx.x; e < 4096; e += 256) vt(I)[e] = (I == C && (e >> 6) == (e & 63)) ? 1.0 : 0.0;
+  __threadfence_block();
+  __syncthreads();
+  double acc[2][NF][2];
+  for (int I = C; I < ntb; ++I) {   // forward: V_I = inv(L_II) (E_I - sum_{C<=J<I} L_IJ V_J)
+    acc_zero(acc);
+    if (I > C) {
+      cp_block(Ls0, LDT, tile(I, C), 64, 64, 64);
+      cp_block(Vs0, LDV, vt(C), 64, 64, 64);
+      cp_commit();
+      for (int J = C, it = 0; J < I; ++J, ++it) {
+        double* Lc = (it & 1) ? Ls1 : Ls0;
+        double* Vc = (it & 1) ? Vs1 : Vs0;
+        if (J + 1 < I) {
+          cp_block((it & 1) ? Ls0 : Ls1, LDT, tile(I, J + 1), 64, 64, 64);
+          cp_block((it & 1) ? Vs0 : Vs1, LDV, vt(J + 1), 64, 64, 64);
+          cp_commit();
+          cp_wait<1>();
+        } else {
+          cp_wait<0>();
+        }
+        __syncthreads();
+        cta_mma<NF, false, false>(Lc, LDT, Vc, LDV, acc);
+        __syncthreads();
+      }
+    }
+    cp_block(Ls0, LDT, tile(I, I), 64, 64, 64);
+    cp_block(Vs0, LDV, vt(I), 64, 64, 64);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+        Vs1[r * LDV + c] = Vs0[r * LDV + c] - acc[i][j][0];
+        Vs1[r * LDV + c + 1] = Vs0[r * LDV + c + 1] - acc[i][j][1];
+      }
+    __syncthreads();
+    acc_zero(acc);
+    cta_mma<NF, false, false>(Ls0, LDT, Vs1, LDV, acc);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+        *reinterpret_cast<double2*>(vt(I) + r * 64 + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    __threadfence_block();
+    __syncthreads();
+  }
+  for (int I = ntb - 1; I >= C; --I) {   // backward: U_I = inv(L_II)^T (V_I - sum_{J>I} L_JI^T U_J)
+    acc_zero(acc);
+    if (I < ntb - 1) {
+      cp_block(Ls0, LDT, tile(I + 1, I), 64, 64, 64);
+      cp_block(Vs0, LDV, vt(I + 1), 64, 64, 64);
+      cp_commit();
+      int it = 0;
+      for (int J = I + 1; J < ntb; ++J, ++it) {
+        double* Lc = (it & 1) ? Ls1 : Ls0;
+        double* Vc = (it & 1) ? Vs1 : Vs0;
+        if (J + 1 < ntb) {
+          cp_block((it & 1) ? Ls0 : Ls1, LDT, tile(J + 1, I), 64, 64, 64);
+          cp_block((it & 1) ? Vs0 : Vs1, LDV, vt(J + 1), 64, 64, 64);
+          cp_commit();
+          cp_wait<1>();
+        } else {
+          cp_wait<0>();
+        }
+        __syncthreads();
+        cta_mma<NF, true, false>(Lc, LDT, Vc, LDV, acc);
+        __syncthreads();
+      }
+    }
+    cp_block(Ls0, LDT, tile(I, I), 64, 64, 64);
+    cp_block(Vs0, LDV, vt(I), 64, 64, 64);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+        Vs1[r * LDV + c] = Vs0[r * LDV + c] - acc[i][j][0];
+        Vs1[r * LDV + c + 1] = Vs0[r * LDV + c + 1] - acc[i][j][1];
+      }
+    __syncthreads();
+    acc_zero(acc);
+    cta_mma<NF, true, false>(Ls0, LDT, Vs1, LDV, acc);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+        *reinterpret_cast<double2*>(vt(I) + r * 64 + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    __threadfence_block();
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// a2 + a3 as ONE symmetric product per block: U_j = M_j W_j, M_j = S_j^{-1} (= L22^{-T} L22^{-1}
+// W_j, the two triangular sweeps of north_star (b) with the factor's inverse precomputed in the
+// setup).  No dependency chain: one CTA per (block, output tile row I, column chunk) computes
+// U_I = sum_{J<=I} M_IJ W_J + sum_{J>I} M_JI^T W_J from the stored lower tiles (each stored tile
+// serves two output rows; they meet in L2).  Same flops as the sweeps, half the factor bytes.
+// items[x] = (block, I); W, U: W/V/U-layout buffers (ld ldw), out of place.
+// ---------------------------------------------------------------------------------------------
+template <int CW>
+__global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                              const double* __restrict__ minv, const double* __restrict__ W,
+                                              double* __restrict__ U, int ldw) {
+  constexpr int NF = CW / 16;
+  constexpr int LDV = CW + 4;
+  extern __shared__ double sm[];
+  double* Ms[2] = {sm, sm + 64 * LDT};
+  double* Ws[2] = {sm + 2 * 64 * LDT, sm + 2 * 64 * LDT + 64 * LDV};
+  const int2 it = items[blockIdx.x];
+  const FacSub sb = subs[it.x];
+  const int I = it.y, ntb = sb.ntb;
+  const int c0 = blockIdx.y * CW;
+  const double* Mb = minv + sb.dense_off * NSP_TILE_ELEMS;
+  const double* Wb = W + sb.wvu_row * (int64_t)ldw + c0;
+  auto mt = [&](int J) {   // stored tile holding block (I, J) (transposed when J > I)
+    return J <= I ? Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS
+                  : Mb + ((int64_t)J * (J + 1) / 2 + I) * NSP_TILE_ELEMS;
+  };
+  double acc[2][NF][2];
+  acc_zero(acc);
+  cp_block(Ms[0], LDT, mt(0), 64, 64, 64);
+  cp_block(Ws[0], LDV, Wb, ldw, 64, CW);
+  cp_commit();
+  for (int J = 0; J < ntb; ++J) {
+    const int b = J & 1;
+    if (J + 1 < ntb) {
+      cp_block(Ms[b ^ 1], LDT, mt(J + 1), 64, 64, 64);
+      cp_block(Ws[b ^ 1], LDV, Wb + (int64_t)(J + 1) * 64 * ldw, ldw, 64, CW);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    if (J <= I) cta_mma<NF, false, false>(Ms[b], LDT, Ws[b], LDV, acc);
+    else cta_mma<NF, true, false>(Ms[b], LDT, Ws[b], LDV, acc);
+    __syncthreads();
+  }
+  double* out = U + (sb.wvu_row + (int64_t)I * 64) * ldw + c0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+      const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+      *reinterpret_cast<double2*>(out + (int64_t)r * ldw + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Generic batched forward + backward triangular solves on tiled factors (one system per blockIdx.x,
 // column chunks on blockIdx.y): dense lower tiles (wb < 0: tile(I,J) = T + I(I+1)/2 + J) or band
 // tiles (tile(I,J) = T + J(wb+1) + (I-J), 0 <= I-J <= wb).  Used for A_G^{-1} (band) and for the
@@ -611,6 +794,36 @@ void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, 
   const int64_t tot = rows * s;
   if (tot <= 0) return;
   { nsp_count_launch(); k_scatter_rows<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, lds, idx, rows, dst, ldd, s, accumulate); }
+}
+
+void l22_inverse(const FacSub* subs, int nsub, int max_ntb, const double* dense, double* minv, cudaStream_t st) {
+  if (nsub <= 0 || max_ntb <= 0) return;
+  const size_t smem = (2 * 64 * LDT + 2 * 64 * 68) * sizeof(double);
+  cudaFuncSetAttribute(k_l22_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  { nsp_count_launch(); k_l22_inverse<<<dim3(nsub, max_ntb), 256, smem, st>>>(subs, dense, minv); }
+}
+
+void symm(const FacSub* subs, const int2* items, int nitems, const double* minv, const double* W, double* U, int ldw,
+          int cw, cudaStream_t st) {
+  if (nitems <= 0) return;
+  dim3 grid(nitems, ldw / cw);
+  if (cw == 64) {
+    const size_t smem = (2 * 64 * LDT + 2 * 64 * (64 + 4)) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_symm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    { nsp_count_launch(); k_symm<64><<<grid, 256, smem, st>>>(subs, items, minv, W, U, ldw); }
+  } else {
+    const size_t smem = (2 * 64 * LDT + 2 * 64 * (32 + 4)) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_symm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    { nsp_count_launch(); k_symm<32><<<grid, 256, smem, st>>>(subs, items, minv, W, U, ldw); }
+  }
 }
 
 void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw, cudaStream_t st) {

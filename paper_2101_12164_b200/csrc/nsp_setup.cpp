@@ -960,6 +960,24 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       return fail(c, NSP_ERR_NOT_SPD, "nsp_setup: A_I_" + std::to_string(j) + " not SPD (pivot at node " +
                                           std::to_string(orig) + ")");
     }
+  // ---------------- explicit S_j^{-1} tiles for the one-product a2+a3 (opts.apply_kernel == 0)
+  if (c->opts.apply_kernel == 0 && dense_tiles > 0) {
+    const size_t bytes = (size_t)dense_tiles * NSP_TILE_ELEMS * 8;
+    size_t fr = 0, tot = 0;
+    NSP_CUDA_TRY(c, cudaMemGetInfo(&fr, &tot));
+    if (bytes < fr / 2) {   // otherwise stay with the L22 sweeps (apply_kernel 1)
+      NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_minv, bytes));
+      nspk::l22_inverse(c->d_subs, c->nsub, c->max_ntb, c->d_dense, c->d_minv, c->stream);
+      NSP_CUDA_TRY(c, cudaGetLastError());
+      std::vector<int2> items;
+      for (int j = 0; j < KL; ++j)
+        for (int I = 0; I < sh[j].ntb; ++I) items.push_back(make_int2(j, I));
+      c->n_items = (int)items.size();
+      if ((st = upload(c, &c->d_items, items)) != NSP_OK) return st;
+      NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+  }
+  const double t_fac_all = ms_since(t2);
   double t_ag = 0.0;
   if (c->opts.factor_gamma) {
     auto t3 = Clock::now();
@@ -973,6 +991,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
     rep->t_ms[0] = t_host;
     rep->t_ms[1] = t_h2d;
     rep->t_ms[2] = t_fac;
+    rep->t_ms[4] = t_fac_all - t_fac;   // S_j^{-1} tiles
   }
   NSP_CUDA_TRY(c, cudaMallocHost(&c->h_status, 4096));
   return NSP_OK;

@@ -13,10 +13,12 @@ CASES = [("cfg1", 30), ("cfg1", 1), ("cfg1", 7), ("cfg2s", 32), ("cfg2s", 100), 
          ("cfg3s", 64), ("cfg4s", 24), ("cfg5s", 32), ("cfg5s", 128)]
 
 
+@pytest.mark.parametrize("apply_kernel", [0, 1])
 @pytest.mark.parametrize("name,s", CASES)
-def test_schur_apply_parity(name, s):
+def test_schur_apply_parity(name, s, apply_kernel):
+    """apply_kernel 0: a2+a3 as one product with the explicit S_j^{-1} tiles; 1: the L22 sweeps."""
     pr, d, S = problem(name)
-    ctx = context(pr)
+    ctx = context(pr, apply_kernel=apply_kernel)
     X = block(d.n_gamma, s)
     Y = torch.empty(d.n_gamma, s, dtype=torch.float64, device="cuda")
     ctx.schur_apply(dev(X), Y)
@@ -43,9 +45,10 @@ def test_schur_apply_closed_form(dims, axis, c):
     ctx.close()
 
 
-def test_apply_deterministic():
+@pytest.mark.parametrize("apply_kernel", [0, 1])
+def test_apply_deterministic(apply_kernel):
     pr, d, S = problem("cfg2s")
-    ctx = context(pr)
+    ctx = context(pr, apply_kernel=apply_kernel)
     X = dev(block(d.n_gamma, 32))
     Y1 = torch.empty_like(X)
     Y2 = torch.empty_like(X)
