@@ -54,6 +54,15 @@ void converge(const double* rsq, const double* bnorm, int s, double tol, BcgStat
 // are replaced by the identity.  sp <= 128, multiple of 32.
 void small_chol(const double* A, int sp, int mode, int nact, double tau, double* Out, BcgStatus* stt,
                 cudaStream_t st);
+// latency-oriented s x s Cholesky (nsp_small.cu): Lp = L with the 16 x 16 diagonal blocks replaced
+// by their inverses.  mode 0: pivot <= 0 -> indefinite; mode 1: pivot test (tau) -> fallback, else
+// width = nact.  sp multiple of 16, <= 128.
+void chol_fac(const double* A, int sp, int mode, int nact, double tau, double* Lp, BcgStatus* stt,
+              cudaStream_t st);
+// Out = sgn * op(B) (B == nullptr: identity), op = L^{-T}L^{-1} (fwd && bwd), L^{-1} (fwd), L^{-T} (bwd);
+// sp / 8 CTAs (8 columns each); skipped when gate && *gate.
+void chol_solve(const double* Lp, int sp, const double* B, int ldb, double* Out, int ldo, double sgn, bool fwd,
+                bool bwd, const int* gate, cudaStream_t st);
 void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* lam, double* Vsorted,
                const int* gate, cudaStream_t st);
 void orth_from_eig(const double* lam, const double* Vs, int n, int sp, double tau, double* T, BcgStatus* stt,

@@ -1,0 +1,400 @@
+// a7 / a10 / a11 s x s Cholesky and its application (§8(a) rows a7, a10, a11; north_star (c) "small
+// s x s Cholesky and solve kernels"), latency-oriented for s <= 128:
+//  k_chol16   one CTA, 8 warps.  16-column blocks; the 16 x 16 diagonal block is factored by ONE warp
+//             in registers (no CTA barrier inside) together with X_kk = L_kk^{-1}; the panel
+//             L_ik = A_ik X_kk^T and the rank-16 trailing update run on the DMMA pipe.  Look-ahead:
+//             warp 0 updates and factors the NEXT diagonal block while warps 1-7 finish the trailing
+//             update, so the serial chain per block is one warp factorisation + the panel.  The
+//             diagonal factorisation has a single call site (instruction-cache friendly).
+//  k_chol_solve  sp/8 CTAs, each solving for 8 right-hand-side columns with L staged in shared
+//             memory; 16-row blocks, the diagonal block as a product with X_kk, the off-diagonal
+//             updates on the DMMA pipe.
+// Pivot semantics follow reading C3 (orth: min pivot > tau * max pivot) and SPEC.md:263 (D: a
+// pivot <= 0 is an indefinite search space).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nsp_blas.h"
+#include "nsp_dmma.cuh"
+
+using namespace nspd;
+
+namespace {
+
+constexpr int LDA = 132;   // smem row stride of the s x s matrix
+
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  const double h = 0.5 * d;
+  r = r * fma(-h * r, r, 1.5);
+  r = r * fma(-h * r, r, 1.5);
+  return r;
+}
+
+// One warp: factor the 16 x 16 diagonal block at (c0, c0) of As in place (lower = L), write
+// X = L^{-1} (16 x 16 row-major, lower) to Xd and the pivots (before the square root) to piv.  A
+// non-positive pivot is replaced by 1 (deterministic continuation) and reported by `false`.
+// Lane l holds row l >> 1, columns 8 (l & 1) .. + 7 in registers.
+__device__ __noinline__ bool warp_chol16(double* As, int c0, double* Xd, double* piv, double* colv, double* invd) {
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 1, h = lane & 1;
+  double* B = As + c0 * LDA + c0;
+  double v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int j = 8 * h + q;
+    v[q] = (j <= r) ? B[r * LDA + j] : 0.0;
+  }
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const int hc = c >> 3, qc = c & 7;
+    const double held = v[qc];
+    double d = __shfl_sync(0xffffffffu, held, 2 * c + hc);
+    if (lane == 0) piv[c0 + c] = d;
+    if (!(d > 0.0)) {
+      ok = false;
+      d = 1.0;
+    }
+    const double rs = rsqrt_nr(d);
+    if (h == hc) {
+      if (r > c) v[qc] = held * rs;
+      else if (r == c) v[qc] = d * rs;
+      colv[r] = (r >= c) ? v[qc] : 0.0;
+    }
+    if (lane == 0) invd[c] = rs;
+    __syncwarp();
+    const double li = colv[r];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = 8 * h + q;
+      if (j > c && j <= r) v[q] = fma(-li, colv[j], v[q]);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int j = 8 * h + q;
+    if (j <= r) B[r * LDA + j] = v[q];
+  }
+  __syncwarp();
+  // X = L^{-1} by 8 x 8 blocks: lanes 0-7 / 8-15 invert L11 / L22 (one column each), then
+  // X21 = -X22 (L21 X11) on all 32 lanes (two entries each)
+  if (lane < 16) {
+    const int blk = lane >> 3, j = lane & 7, o = 8 * blk;
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double s = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k)
+        if (k >= j) s = fma(-B[(o + i) * LDA + o + k], x[k], s);
+      x[i] = (i >= j) ? s * invd[o + i] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      Xd[(o + i) * 16 + o + j] = x[i];
+      Xd[(o + i) * 16 + 8 * (1 - blk) + j] = 0.0;
+    }
+  }
+  __syncwarp();
+  {
+    const int i = lane >> 2, jj = 2 * (lane & 3);
+    double m0 = 0.0, m1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double l = B[(8 + i) * LDA + k];
+      m0 = fma(l, Xd[k * 16 + jj], m0);
+      m1 = fma(l, Xd[k * 16 + jj + 1], m1);
+    }
+    __syncwarp();
+    Xd[(8 + i) * 16 + jj] = m0;
+    Xd[(8 + i) * 16 + jj + 1] = m1;
+    __syncwarp();
+    double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double xk = Xd[(8 + i) * 16 + 8 + k];
+      x0 = fma(xk, Xd[(8 + k) * 16 + jj], x0);
+      x1 = fma(xk, Xd[(8 + k) * 16 + jj + 1], x1);
+    }
+    __syncwarp();
+    Xd[(8 + i) * 16 + jj] = -x0;
+    Xd[(8 + i) * 16 + jj + 1] = -x1;
+  }
+  __syncwarp();
+  return ok;
+}
+
+#ifdef NSP_CHOL_PROF
+__device__ long long g_chol_prof[64];
+#define CPROF(i) \
+  if (threadIdx.x == 0) g_chol_prof[i] = clock64();
+#else
+#define CPROF(i)
+#endif
+
+// Output Lp (sp x sp): strictly-lower off-diagonal blocks = L, diagonal 16 x 16 blocks = X_kk
+// (lower), upper = 0.  Rows / cols >= nact (nact < 0: st->width) are replaced by the identity.
+//  mode 0: a pivot <= 0 -> st->indefinite.
+//  mode 1: pivot test min d_i > tau max d_i over i < nact (reading C3), else st->fallback = 1;
+//          success: st->fallback = 0, st->width = nact.
+__global__ void __launch_bounds__(256) k_chol16(const double* __restrict__ Ain, int sp, int mode, int nact,
+                                                double tau, double* __restrict__ Lp, BcgStatus* st) {
+  extern __shared__ double sm[];
+  double* As = sm;                 // 128 x LDA
+  double* Di = sm + 128 * LDA;     // 8 x 256: X_kk
+  __shared__ double piv[128];
+  __shared__ double colv[16], invd[16];
+  __shared__ int s_fail;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int width = nact < 0 ? st->width : nact;
+  const int NB = sp / 16;
+  CPROF(0)
+  {  // async 16-byte staging (all loads in flight at once), then the identity fix-up
+    const int cpr = sp / 2;
+    for (int e = tid; e < sp * cpr; e += 256) {
+      const int i = e / cpr, q = e - i * cpr;
+      if (2 * q <= i) cp_async16(As + i * LDA + 2 * q, Ain + (int64_t)i * sp + 2 * q);
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+    if (width < sp)
+      for (int e = tid; e < sp * sp; e += 256) {
+        const int i = e / sp, j = e - i * sp;
+        if (j <= i && (i >= width || j >= width)) As[i * LDA + j] = (i == j) ? 1.0 : 0.0;
+      }
+  }
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  CPROF(1)
+  auto tile_update = [&](int I, int J, int c0) {   // A_IJ -= L_I,kb L_J,kb^T (8 x 8, k = 16)
+    double c0v = 0.0, c1v = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; k += 4)
+      dmma(c0v, c1v, As[(8 * I + g) * LDA + c0 + k + t], As[(8 * J + g) * LDA + c0 + k + t]);
+    double* dst = As + (8 * I + g) * LDA + 8 * J + 2 * t;
+    dst[0] -= c0v;
+    dst[1] -= c1v;
+  };
+  for (int step = 0; step < NB; ++step) {
+    // (C) trailing update with panel step-1; warp 0: next diagonal block first, then factor it (A)
+    if (step > 0) {
+      const int kb = step - 1, c0 = 16 * kb;
+      const int b8 = 2 * step, m = 2 * NB - b8;
+      if (warp == 0) {
+        tile_update(b8, b8, c0);
+        tile_update(b8 + 1, b8, c0);
+        tile_update(b8 + 1, b8 + 1, c0);
+        __syncwarp();
+      } else {
+        const int ntile = m * (m + 1) / 2;
+        for (int task = warp - 1; task < ntile; task += 7) {
+          int q = (int)((sqrtf(8.0f * task + 1.0f) - 1.0f) * 0.5f);
+          while (q * (q + 1) / 2 > task) --q;
+          while ((q + 1) * (q + 2) / 2 <= task) ++q;
+          const int p = task - q * (q + 1) / 2;
+          if (q <= 1) continue;   // tiles of the next diagonal block: warp 0
+          tile_update(b8 + q, b8 + p, c0);
+        }
+      }
+    }
+    if (warp == 0) {   // (A) the only call site of the diagonal factorisation
+      const bool ok = warp_chol16(As, 16 * step, Di + step * 256, piv, colv, invd);
+      if (!ok && lane == 0) s_fail = 1;
+    }
+    __syncthreads();
+    CPROF(2 + 2 * step)
+    if (s_fail) break;
+    // (B) panel: L_ik = A_ik X_kk^T for the rows below the block, 8-row groups, in place
+    const int c0 = 16 * step;
+    const int ngrp = (sp - c0 - 16) / 8;
+    for (int grp = warp; grp < ngrp; grp += 8) {
+      const int row0 = c0 + 16 + 8 * grp;
+      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int k = 0; k < 16; k += 4) {
+        const double a = As[(row0 + g) * LDA + c0 + k + t];
+#pragma unroll
+        for (int nf = 0; nf < 2; ++nf) dmma(acc[nf][0], acc[nf][1], a, Di[step * 256 + (nf * 8 + g) * 16 + k + t]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int nf = 0; nf < 2; ++nf) {
+        As[(row0 + g) * LDA + c0 + nf * 8 + 2 * t] = acc[nf][0];
+        As[(row0 + g) * LDA + c0 + nf * 8 + 2 * t + 1] = acc[nf][1];
+      }
+    }
+    __syncthreads();
+    CPROF(3 + 2 * step)
+  }
+  if (warp == 0) {   // status: warp-parallel min / max of the pivots
+    if (mode == 0) {
+      if (lane == 0 && s_fail) st->indefinite = 1;
+    } else {
+      double mn = 1e308, mx = 0.0;
+      for (int i = lane; i < width; i += 32) {
+        mn = fmin(mn, piv[i]);
+        mx = fmax(mx, piv[i]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if (lane == 0) {
+        const bool fb = s_fail != 0 || !(mn > tau * mx);
+        st->fallback = fb ? 1 : 0;
+        if (!fb) st->width = width;
+      }
+    }
+  }
+  // output, two doubles per thread per step (sp is 64 or 128: shifts, no division)
+  const int lsp = sp == 128 ? 7 : 6;
+  for (int e = 2 * tid; e < sp * sp; e += 512) {
+    const int i = e >> lsp, j = e & (sp - 1);
+    const int bi = i >> 4, bj = j >> 4;
+    double2 v = make_double2(0.0, 0.0);
+    if (bi == bj) {
+      const double* xr = Di + bi * 256 + (i & 15) * 16 + (j & 15);
+      v.x = ((j & 15) <= (i & 15)) ? xr[0] : 0.0;
+      v.y = (((j + 1) & 15) <= (i & 15)) ? xr[1] : 0.0;
+    } else if (bi > bj) {
+      v = make_double2(As[i * LDA + j], As[i * LDA + j + 1]);
+    }
+    *reinterpret_cast<double2*>(Lp + e) = v;
+  }
+  CPROF(40)
+}
+
+// Out[:, 8b..8b+8) = sgn * op(B)[:, 8b..8b+8), op = L^{-T} L^{-1} (fwd && bwd), L^{-1} (fwd) or L^{-T}
+// (bwd); B == nullptr: the identity.  One CTA (4 warps) per 8 right-hand-side columns.  Lp staged
+// in smem; per 16-row block: x_kb <- X_kk x_kb (16 x 16 x 8 product, 2 DMMA m-fragments), then
+// the remaining rows x_i -= L_i,kb x_kb on the DMMA pipe (8-row fragments over the 4 warps).
+// gate (optional): skip when *gate != 0.
+__global__ void __launch_bounds__(128) k_chol_solve(const double* __restrict__ Lp, int sp,
+                                                    const double* __restrict__ B, int ldb, double* __restrict__ Out,
+                                                    int ldo, double sgn, int fwd, int bwd, const int* gate) {
+  if (gate && *gate) return;
+  extern __shared__ double sm[];
+  const int LD = sp + 2;
+  double* Ls = sm;                 // sp x LD (zero above the diagonal)
+  double* x = sm + sp * LD;        // sp x 8 (+pad 2 -> ld 10)
+  constexpr int LX = 10;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int c0 = blockIdx.x * 8;
+  {
+    const int cpr = sp / 2;
+    for (int e = tid; e < sp * cpr; e += 128) {
+      const int i = e / cpr, q = e - i * cpr;
+      if (2 * q <= i) cp_async16(Ls + i * LD + 2 * q, Lp + (int64_t)i * sp + 2 * q);
+      else {
+        Ls[i * LD + 2 * q] = 0.0;
+        Ls[i * LD + 2 * q + 1] = 0.0;
+      }
+    }
+    cp_commit();
+  }
+  for (int e = tid; e < sp * 8; e += 128) {
+    const int i = e >> 3, c = e & 7;
+    x[i * LX + c] = B ? B[(int64_t)i * ldb + c0 + c] : (i == c0 + c ? 1.0 : 0.0);
+  }
+  cp_wait<0>();
+  __syncthreads();
+  const int NB = sp / 16;
+  if (fwd)
+    for (int kb = 0; kb < NB; ++kb) {
+      const int b0 = 16 * kb;
+      // x_kb <- X_kk x_kb : warps 0, 1 take the two 8-row halves (m8 n8 k16)
+      double d0 = 0.0, d1 = 0.0;
+      if (warp < 2) {
+#pragma unroll
+        for (int k = 0; k < 16; k += 4)
+          dmma(d0, d1, Ls[(b0 + 8 * warp + g) * LD + b0 + k + t], x[(b0 + k + t) * LX + g]);
+      }
+      __syncthreads();
+      if (warp < 2) {
+        x[(b0 + 8 * warp + g) * LX + 2 * t] = d0;
+        x[(b0 + 8 * warp + g) * LX + 2 * t + 1] = d1;
+      }
+      __syncthreads();
+      // x_i -= L_i,kb x_kb for the rows below, 8-row groups
+      for (int grp = warp; grp < (sp - b0 - 16) / 8; grp += 4) {
+        const int row0 = b0 + 16 + 8 * grp;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; k += 4)
+          dmma(a0, a1, Ls[(row0 + g) * LD + b0 + k + t], x[(b0 + k + t) * LX + g]);
+        x[(row0 + g) * LX + 2 * t] -= a0;
+        x[(row0 + g) * LX + 2 * t + 1] -= a1;
+      }
+      __syncthreads();
+    }
+  if (bwd)
+    for (int kb = NB - 1; kb >= 0; --kb) {
+      const int b0 = 16 * kb;
+      // x_kb <- X_kk^T x_kb
+      double d0 = 0.0, d1 = 0.0;
+      if (warp < 2) {
+#pragma unroll
+        for (int k = 0; k < 16; k += 4)
+          dmma(d0, d1, Ls[(b0 + k + t) * LD + b0 + 8 * warp + g], x[(b0 + k + t) * LX + g]);
+      }
+      __syncthreads();
+      if (warp < 2) {
+        x[(b0 + 8 * warp + g) * LX + 2 * t] = d0;
+        x[(b0 + 8 * warp + g) * LX + 2 * t + 1] = d1;
+      }
+      __syncthreads();
+      // x_i -= L_kb,i^T x_kb for the rows above
+      for (int grp = warp; grp < b0 / 8; grp += 4) {
+        const int row0 = 8 * grp;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; k += 4)
+          dmma(a0, a1, Ls[(b0 + k + t) * LD + row0 + g], x[(b0 + k + t) * LX + g]);
+        x[(row0 + g) * LX + 2 * t] -= a0;
+        x[(row0 + g) * LX + 2 * t + 1] -= a1;
+      }
+      __syncthreads();
+    }
+  for (int e = tid; e < sp * 8; e += 128) {
+    const int i = e >> 3, cc = e & 7;
+    Out[(int64_t)i * ldo + c0 + cc] = sgn * x[i * LX + cc];
+  }
+}
+
+}  // namespace
+
+namespace nspb {
+
+void chol_fac(const double* A, int sp, int mode, int nact, double tau, double* Lp, BcgStatus* stt, cudaStream_t st) {
+  // sp = s rounded up to 64 (the block-CG padding): 64 or 128
+  const size_t smem = (size_t)(128 * LDA + 8 * 256) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_chol16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  nsp_count_launch();
+  k_chol16<<<1, 256, smem, st>>>(A, sp, mode, nact, tau, Lp, stt);
+}
+
+void chol_solve(const double* Lp, int sp, const double* B, int ldb, double* Out, int ldo, double sgn, bool fwd,
+                bool bwd, const int* gate, cudaStream_t st) {
+  const size_t smem = (size_t)(sp * (sp + 2) + sp * 10) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((128 * 130 + 128 * 10) * sizeof(double)));
+    attr = true;
+  }
+  nsp_count_launch();
+  k_chol_solve<<<sp / 8, 128, smem, st>>>(Lp, sp, B, ldb, Out, ldo, sgn, fwd, bwd, gate);
+}
+
+}  // namespace nspb

@@ -146,7 +146,9 @@ static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Po
   nspb::gram(Wm, sp, sp, Wm, sp, sp, gram_rows(c), w.G, sp, w.gram, st);
   nsp_status e = comm_allreduce(c, w.G, (size_t)sp * sp);
   if (e != NSP_OK) return e;
-  nspb::small_chol(w.G, sp, 1, s, c->opts.orth_tau, w.T, w.st, st);
+  // CholQR with the pivot test (k_chol16 mode 1), T = R^{-1} = L^{-T} (skipped on fallback)
+  nspb::chol_fac(w.G, sp, 1, s, c->opts.orth_tau, w.Ldi, w.st, st);
+  nspb::chol_solve(w.Ldi, sp, nullptr, 0, w.T, sp, 1.0, false, true, &w.st->fallback, st);
   nspb::small_eig(w.G, sp, s, w.Vw, sp + 1, w.lam, w.Vs, &w.st->fallback, st);
   nspb::orth_from_eig(w.lam, w.Vs, s, sp, c->opts.orth_tau, w.T, w.st, st);
   nspb::panel(Pout, sp, nullptr, 0, Wm, sp, w.T, sp, sp, sp, n, 1.0, nullptr, st);
@@ -208,9 +210,9 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
       }
       tr.mark("gram_DE");
       // a7: chol(D), alpha = D^{-1} E
-      nspb::small_chol(w.D, sp, 0, -1, 0.0, w.Ldi, w.st, st);   // Ldi = D^{-1}
+      nspb::chol_fac(w.D, sp, 0, -1, 0.0, w.Ld, w.st, st);        // D = L L^T
       tr.mark("chol_D");
-      nspb::panel(w.al, sp, nullptr, 0, w.Ldi, sp, w.E, sp, sp, sp, sp, 1.0, nullptr, st);
+      nspb::chol_solve(w.Ld, sp, w.E, sp, w.al, sp, 1.0, true, true, nullptr, st);   // alpha = D^{-1} E
       tr.mark("alpha");
       // a8: X += P alpha, R -= Q alpha, column norms
       {
@@ -263,7 +265,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
       // a10: F = Q^T Z, beta = -D^{-1} F, W = Z + P beta
       nspb::gram(w.Q, sp, sp, Zr, sp, sp, ng, w.F, sp, w.gram, st);
       if ((e = comm_allreduce(c, w.F, (size_t)sp * sp)) != NSP_OK) return e;
-      nspb::panel(w.be, sp, nullptr, 0, w.Ldi, sp, w.F, sp, sp, sp, sp, -1.0, nullptr, st);
+      nspb::chol_solve(w.Ld, sp, w.F, sp, w.be, sp, -1.0, true, true, nullptr, st);  // beta = -D^{-1} F
       tr.mark("beta");
       nspb::panel(w.W, sp, Zr, sp, w.P, sp, w.be, sp, sp, sp, n, 1.0, nullptr, st);
       tr.mark("W");
