@@ -100,3 +100,31 @@ class SchurOracle:
     # --- A_I^{-1} on a full interior vector (block by block) ---------------
     def solve_AI(self, r_I: list) -> list:
         return [self.solve_AI_block(j, r_I[j]) for j in range(self.d.K)]
+
+
+def schur_rows(A: sp.csr_matrix, part: np.ndarray, X: np.ndarray, rows_gamma: np.ndarray) -> np.ndarray:
+    """(S_G X)[g, :] for the given Gamma rows, straight from eq:schur_complement
+    written out row by row:  (A_G X)[g] - sum_{j adjacent to g} A_GI_j[g, :] A_I_j^{-1} A_I_jG X,
+    touching only the blocks adjacent to the sampled rows (for full-size configs where the full
+    DBBD is too large to extract).  X: n_G x s in the Gamma order of ascending original id
+    (reading C10); rows_gamma: original node ids of the sampled Gamma rows."""
+    A = sp.csr_matrix(A)
+    part = np.asarray(part)
+    gamma = np.flatnonzero(part < 0)
+    gpos = np.full(A.shape[0], -1, dtype=np.int64)
+    gpos[gamma] = np.arange(gamma.size)
+    X = np.asarray(X, dtype=np.float64)
+    out = np.zeros((len(rows_gamma), X.shape[1]))
+    for r, g in enumerate(rows_gamma):
+        cols = A.indices[A.indptr[g]:A.indptr[g + 1]]
+        vals = A.data[A.indptr[g]:A.indptr[g + 1]]
+        gam = part[cols] < 0
+        out[r] = vals[gam] @ X[gpos[cols[gam]]]                       # (A_G X)[g]
+        for j in np.unique(part[cols[~gam]]):
+            blk = np.flatnonzero(part == j)
+            AIj = A[blk][:, blk]
+            AjG = A[blk][:, gamma]                                     # A_I_jG
+            U = _lu(AIj).solve(np.ascontiguousarray(AjG @ X))          # A_I_j^{-1} A_I_jG X
+            a_g = A[g][:, blk].toarray().ravel()                       # A_GI_j[g, :]
+            out[r] -= a_g @ U
+    return out

@@ -382,3 +382,16 @@ def test_full_solve_matches_dense_direct():
     rng = np.random.default_rng(5)
     u, v = rng.standard_normal(d.n_gamma), rng.standard_normal(d.n_gamma)
     assert abs(u @ M(v) - v @ M(u)) < 1e-12 * abs(u @ M(v))
+
+
+def test_schur_rows_single_separator_closed_form():
+    """oracle.schur.schur_rows (the row-by-row definition used for full-size sampled parity) against
+    the single-separator closed form S_G v_j = lambda_j v_j (SURVEY.md §8(c) pin table)."""
+    from oracle.schur import schur_rows
+    dims, axis, c = (16, 12), 1, 5
+    A, part = _single_separator(dims, axis, c)
+    lam, V, _, _ = _closed_form_modes(dims, axis, c)
+    gamma = np.flatnonzero(part < 0)
+    rows = gamma[[0, 3, gamma.size - 1]]
+    Y = schur_rows(A.to_scipy(), part, V, rows)
+    assert np.max(np.abs(Y - (V * lam)[[0, 3, gamma.size - 1]])) < 1e-13 * lam.max()
