@@ -19,6 +19,41 @@ from paper_2101_12164_b200 import build as B
 from paper_2101_12164_b200 import nsp
 
 
+def run_pcg(name, maxit=5000):
+    """Nystrom (Alg. 2) + outer PCG with M_2 at full size; x checked against x* (b = A x*) or by the
+    true residual ||b - A x|| / ||b|| (host CSR matvec)."""
+    B.build()
+    pr = P.make(name)
+    t0 = time.perf_counter()
+    ctx = nsp.Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, factor_gamma=True)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    Om = torch.from_numpy(pr.omega()).cuda()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rn = ctx.nystrom(pr.rank, pr.oversample, Om, pr.tol_bcg, 1000)
+    torch.cuda.synchronize()
+    t_nys = time.perf_counter() - t0
+    b = pr.rhs()
+    out = dict(config=name, setup_s=round(t_setup, 2), ag_factor_ms=round(ctx.setup_report["t_ms"][3], 1),
+               nystrom_s=round(t_nys, 3), nystrom_inner_iters=rn["iters"], nystrom_rank=rn["rank"],
+               sigma_top=[float(x) for x in ctx.nystrom_sigma()[:3]])
+    A = pr.A.to_scipy()
+    for prec in (1, 2):
+        x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
+        bd = torch.from_numpy(b).cuda()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = ctx.pcg(bd, x, pr.tol_pcg, maxit, precond=prec)
+        torch.cuda.synchronize()
+        t = time.perf_counter() - t0
+        xh = x.cpu().numpy()
+        out[f"pcg_M{prec}"] = dict(iters=rep["iters"], converged=rep["converged"], s=round(t, 3),
+                                   true_relres=float(np.linalg.norm(b - A @ xh) / np.linalg.norm(b)))
+    ctx.close()
+    return out
+
+
 def run(name, nrows=6, maxit=1000, apply_kernel=0):
     B.build()
     t0 = time.perf_counter()
@@ -82,6 +117,10 @@ def run(name, nrows=6, maxit=1000, apply_kernel=0):
 
 if __name__ == "__main__":
     nrows = int(sys.argv[sys.argv.index("--rows") + 1]) if "--rows" in sys.argv else 6
+    if "--pcg" in sys.argv:
+        for name in [a for a in sys.argv[1:] if a.startswith("cfg")]:
+            print(json.dumps(run_pcg(name)), flush=True)
+        sys.exit(0)
     for name in [a for a in sys.argv[1:] if a.startswith("cfg")]:
         try:
             print(json.dumps(run(name, nrows)), flush=True)
