@@ -168,6 +168,7 @@ static nsp_status fail(nsp_ctx* c, nsp_status st, const std::string& msg) {
 }
 
 nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K, nsp_report* rep);
+static nsp_status validate_inputs(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K);
 
 // Cholesky factor of A_G (eq:cholesky) for the first-level preconditioner
 // S~_1^{-1} = A_G^{-1} (eq:S1) and M_2: RCM band ordering of the Gamma graph, band tiles, the same
@@ -397,22 +398,23 @@ extern "C" nsp_status nsp_setup(const nsp_csr* A, const int32_t* part, int K, co
   if (c->nranks > 1 && (c->opts.factor_gamma || c->opts.bcg_precond))
     return fail(c, NSP_ERR_ARG, "nsp_setup: the A_G factor (M = A_G^{-1}, M_2, PCG) is single-rank in this "
                                 "version; multi-rank runs use bcg_precond = 0 (reading C2)");
+  nsp_status vs = validate_inputs(c, A, part, K);   // host-only: errors reported without a device
+  if (vs != NSP_OK) return vs;
   NSP_CUDA_TRY(c, cudaSetDevice(c->device));
   nsp_status st = nsp_setup_impl(c, A, part, K, rep);
   if (st != NSP_OK) return st;
   return comm_init(c);
 }
 
-nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K, nsp_report* rep) {
-  auto t0 = Clock::now();
+// Host-only input validation (SPEC.md:30-31 CSR, SPEC.md:135 separator property): runs before
+// any device call, so malformed inputs are reported with NSP_ERR_ARG even without a GPU.
+static nsp_status validate_inputs(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K) {
   const int64_t n = A->n;
   const int64_t* rp = A->rowptr;
   const int32_t* ci = A->colidx;
   const double* va = A->val;
   if (n <= 0 || !rp || !ci || !va) return fail(c, NSP_ERR_ARG, "nsp_setup: empty or null CSR");
   if (rp[0] != 0) return fail(c, NSP_ERR_ARG, "nsp_setup: rowptr[0] != 0");
-  c->n = n;
-  c->K = K;
   // ---------------- validation
   std::string verr;
   int64_t bad_row = -1;
@@ -469,6 +471,19 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
                                     ", " + std::to_string(sep_j) + ") between blocks " +
                                     std::to_string(part[sep_i]) + " and " + std::to_string(part[sep_j]));
 
+  return NSP_OK;
+}
+
+nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K, nsp_report* rep) {
+  auto t0 = Clock::now();
+  const int64_t n = A->n;
+  const int64_t* rp = A->rowptr;
+  const int32_t* ci = A->colidx;
+  const double* va = A->val;
+  if (n <= 0 || !rp || !ci || !va) return fail(c, NSP_ERR_ARG, "nsp_setup: empty or null CSR");
+  if (rp[0] != 0) return fail(c, NSP_ERR_ARG, "nsp_setup: rowptr[0] != 0");
+  c->n = n;
+  c->K = K;
   // ---------------- shard plan + DBBD index maps (local blocks [B0, B0 + KL), local Gamma rows =
   // private then shared)
   ShardPlan plan;
