@@ -13,8 +13,8 @@ namespace nspi {
 int pick_cw(const nsp_ctx* c, int s) {
   const int tiles64 = (s + 63) / 64;
   if (const char* e = getenv("NSP_CW")) return atoi(e) == 64 && s > 32 ? 64 : 32;   // tuning override
-  const int64_t work = c->d_minv ? (int64_t)c->n_items : (int64_t)c->nsub;
-  return (s > 32 && work * tiles64 >= 2 * 148) ? 64 : 32;
+  if (c->d_minv) return 32;   // k_symm: 32-wide chunks run 2 CTAs/SM (faster at every measured shape)
+  return (s > 32 && (int64_t)c->nsub * tiles64 >= 2 * 148) ? 64 : 32;
 }
 
 int ld_pad(int s, int cw) { return ((s + cw - 1) / cw) * cw; }

@@ -11,6 +11,15 @@
 
 using namespace nspd;
 
+#ifndef NSP_GR
+#define NSP_GR 32
+#endif
+#ifndef NSP_GNS
+#define NSP_GNS 4
+#endif
+#ifndef NSP_GCTAS
+#define NSP_GCTAS 148
+#endif
 namespace {
 
 __device__ __forceinline__ void cp_async16_zf(void* smem, const void* gmem, bool valid) {
@@ -32,19 +41,22 @@ __device__ __forceinline__ void cp_block_zf(double* s, int sld, const double* g,
   }
 }
 
-constexpr int GR = 32;     // rows per Gram slab
+constexpr int GR = NSP_GR;     // rows per Gram slab
 constexpr int LDS = 68;    // smem stride for 64-wide tiles
 
 // part[(chunk * ntm * ntn + tm * ntn + tn) * 4096 + i * 64 + j]
 //   = sum_{r in chunk} Xa[r][64 tm + i] * Xb[r][64 tn + j]
+// One wave of CTAs (tiles x chunks <= 148, one per SM), each streaming its contiguous row chunk
+// through a GNS-stage cp.async ring of 32-row slabs (one barrier per slab), so the slab loads are
+// in flight GNS-1 slabs ahead of the DMMA work.
+constexpr int GNS = NSP_GNS;
 __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__ Xa, int lda,
                                                       const double* __restrict__ Xb, const double* __restrict__ Xb2,
                                                       int ldb, int ntn1, int64_t n,
                                                       int64_t rows_per_chunk, double* __restrict__ part, int ntm,
                                                       int ntn) {
   extern __shared__ double sm[];
-  double* As[2] = {sm, sm + GR * LDS};
-  double* Bs[2] = {sm + 2 * GR * LDS, sm + 3 * GR * LDS};
+  constexpr int STG = 2 * GR * LDS;
   const int tile = blockIdx.x;
   const int tm = tile / ntn, tn = tile - tm * ntn;
   const int64_t r0 = blockIdx.y * rows_per_chunk;
@@ -53,26 +65,25 @@ __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__
   acc_zero(acc);
   const double* A0 = Xa + 64 * tm;
   const double* B0 = tn < ntn1 ? Xb + 64 * tn : Xb2 + 64 * (tn - ntn1);
-  int buf = 0;
-  if (r0 < r1) {
-    cp_block_zf(As[0], LDS, A0 + r0 * lda, lda, GR, 64, r1 - r0);
-    cp_block_zf(Bs[0], LDS, B0 + r0 * ldb, ldb, GR, 64, r1 - r0);
+  const int nslab = r1 > r0 ? (int)((r1 - r0 + GR - 1) / GR) : 0;
+  auto issue = [&](int q) {
+    double* st = sm + (q % GNS) * STG;
+    const int64_t r = r0 + (int64_t)q * GR;
+    cp_block_zf(st, LDS, A0 + r * lda, lda, GR, 64, r1 - r);
+    cp_block_zf(st + GR * LDS, LDS, B0 + r * ldb, ldb, GR, 64, r1 - r);
+  };
+#pragma unroll
+  for (int q = 0; q < GNS - 1; ++q) {
+    if (q < nslab) issue(q);
     cp_commit();
   }
-  for (int64_t r = r0; r < r1; r += GR) {
-    const int64_t rn = r + GR;
-    if (rn < r1) {
-      cp_block_zf(As[buf ^ 1], LDS, A0 + rn * lda, lda, GR, 64, r1 - rn);
-      cp_block_zf(Bs[buf ^ 1], LDS, B0 + rn * ldb, ldb, GR, 64, r1 - rn);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
+  for (int q = 0; q < nslab; ++q) {
+    cp_wait<GNS - 2>();
     __syncthreads();
-    cta_mma<4, true, false>(As[buf], LDS, Bs[buf], LDS, acc, GR);
-    __syncthreads();
-    buf ^= 1;
+    if (q + GNS - 1 < nslab) issue(q + GNS - 1);
+    cp_commit();
+    const double* st = sm + (q % GNS) * STG;
+    cta_mma<4, true, false>(st, LDS, st + GR * LDS, LDS, acc, GR);
   }
   double* out = part + ((int64_t)blockIdx.y * ntm * ntn + tile) * 4096;
 #pragma unroll
@@ -138,18 +149,16 @@ __global__ void __launch_bounds__(256) k_panel(PanelArgs pa0, PanelArgs pa1, int
   }
   for (int kb = 0; kb < nk; ++kb) {
     const int b = kb & 1;
+    cp_wait<0>();
+    __syncthreads();
     if (kb + 1 < nk) {
       cp_block_zf(As[b ^ 1], LDA, In + r0 * ldi + (kb + 1) * 32, ldi, 64, 32, nv);
       cp_block(Bs[b ^ 1], LDS, M + (int64_t)(kb + 1) * 32 * ldm + c0, ldm, 32, 64);
       cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
     }
-    __syncthreads();
     cta_mma<4, false, false>(As[b], LDA, Bs[b], LDS, acc, 32);
-    __syncthreads();
   }
+  __syncthreads();   // smem reused below
   double* sq = sm;  // reuse: 64 x 65 squares
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -680,9 +689,9 @@ static void set_smem(const void* f, size_t bytes) {
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-int gram_chunks(int64_t n, int ntiles) {
-  int64_t ch = (n + 255) / 256;
-  const int64_t cap = (296 + ntiles - 1) / ntiles;
+int gram_chunks(int64_t n, int ntiles) {   // one wave: tiles x chunks <= 148 CTAs (1 per SM)
+  int64_t ch = (n + GR - 1) / GR;
+  const int64_t cap = NSP_GCTAS / ntiles;
   if (ch > cap) ch = cap;
   return (int)(ch < 1 ? 1 : ch);
 }
@@ -699,7 +708,7 @@ void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb
   const int nch = gram_chunks(n, ntm * ntn);
   int64_t rpc = (n + nch - 1) / nch;
   rpc = ((rpc + GR - 1) / GR) * GR;
-  const size_t smem = 4 * GR * LDS * sizeof(double);
+  const size_t smem = GNS * 2 * GR * LDS * sizeof(double);
   static bool attr = false;
   if (!attr) {
     set_smem((const void*)k_gram_partial, smem);

@@ -523,15 +523,14 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
 // serves two output rows; they meet in L2).  Same flops as the sweeps, half the factor bytes.
 // items[x] = (block, I); W, U: W/V/U-layout buffers (ld ldw), out of place.
 // ---------------------------------------------------------------------------------------------
-template <int CW>
+template <int CW, int NS>
 __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, const int2* __restrict__ items,
                                               const double* __restrict__ minv, const double* __restrict__ W,
                                               double* __restrict__ U, int ldw) {
   constexpr int NF = CW / 16;
   constexpr int LDV = CW + 4;
+  constexpr int STAGE = 64 * LDT + 64 * LDV;   // one (M tile, W tile) pair
   extern __shared__ double sm[];
-  double* Ms[2] = {sm, sm + 64 * LDT};
-  double* Ws[2] = {sm + 2 * 64 * LDT, sm + 2 * 64 * LDT + 64 * LDV};
   const int2 it = items[blockIdx.x];
   const FacSub sb = subs[it.x];
   const int I = it.y, ntb = sb.ntb;
@@ -542,25 +541,27 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
     return J <= I ? Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS
                   : Mb + ((int64_t)J * (J + 1) / 2 + I) * NSP_TILE_ELEMS;
   };
+  auto issue = [&](int J) {   // stage J % NS
+    double* Ms = sm + (J % NS) * STAGE;
+    cp_block(Ms, LDT, mt(J), 64, 64, 64);
+    cp_block(Ms + 64 * LDT, LDV, Wb + (int64_t)J * 64 * ldw, ldw, 64, CW);
+  };
   double acc[2][NF][2];
   acc_zero(acc);
-  cp_block(Ms[0], LDT, mt(0), 64, 64, 64);
-  cp_block(Ws[0], LDV, Wb, ldw, 64, CW);
-  cp_commit();
+  // NS-stage cp.async pipeline: tiles J+1 .. J+NS-1 in flight while J is multiplied
+#pragma unroll
+  for (int p = 0; p < NS - 1; ++p) {
+    if (p < ntb) issue(p);
+    cp_commit();
+  }
   for (int J = 0; J < ntb; ++J) {
-    const int b = J & 1;
-    if (J + 1 < ntb) {
-      cp_block(Ms[b ^ 1], LDT, mt(J + 1), 64, 64, 64);
-      cp_block(Ws[b ^ 1], LDV, Wb + (int64_t)(J + 1) * 64 * ldw, ldw, 64, CW);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
+    cp_wait<NS - 2>();
     __syncthreads();
-    if (J <= I) cta_mma<NF, false, false>(Ms[b], LDT, Ws[b], LDV, acc);
-    else cta_mma<NF, true, false>(Ms[b], LDT, Ws[b], LDV, acc);
-    __syncthreads();
+    if (J + NS - 1 < ntb) issue(J + NS - 1);
+    cp_commit();
+    const double* Ms = sm + (J % NS) * STAGE;
+    if (J <= I) cta_mma<NF, false, false>(Ms, LDT, Ms + 64 * LDT, LDV, acc);
+    else cta_mma<NF, true, false>(Ms, LDT, Ms + 64 * LDT, LDV, acc);
   }
   double* out = U + (sb.wvu_row + (int64_t)I * 64) * ldw + c0;
 #pragma unroll
@@ -807,22 +808,29 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
           int cw, cudaStream_t st) {
   if (nitems <= 0) return;
   dim3 grid(nitems, ldw / cw);
+  // 2-stage cp.async pipeline, one barrier per K step.  Measured on cfg2 shapes (tools/bench_symm.cu):
+  // 32-wide column chunks with 2 CTAs/SM 135 us (24.3 TFLOP/s) vs 64-wide 1 CTA/SM 156 us; 3 stages
+  // force 1 CTA/SM and are slower.
+#ifndef NSP_SYMM_STAGES
+#define NSP_SYMM_STAGES 2
+#endif
+  constexpr int NS = NSP_SYMM_STAGES;
   if (cw == 64) {
-    const size_t smem = (2 * 64 * LDT + 2 * 64 * (64 + 4)) * sizeof(double);
+    const size_t smem = NS * (64 * LDT + 64 * (64 + 4)) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_symm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_symm<64, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    { nsp_count_launch(); k_symm<64><<<grid, 256, smem, st>>>(subs, items, minv, W, U, ldw); }
+    { nsp_count_launch(); k_symm<64, NS><<<grid, 256, smem, st>>>(subs, items, minv, W, U, ldw); }
   } else {
-    const size_t smem = (2 * 64 * LDT + 2 * 64 * (32 + 4)) * sizeof(double);
+    const size_t smem = NS * (64 * LDT + 64 * (32 + 4)) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_symm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_symm<32, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    { nsp_count_launch(); k_symm<32><<<grid, 256, smem, st>>>(subs, items, minv, W, U, ldw); }
+    { nsp_count_launch(); k_symm<32, NS><<<grid, 256, smem, st>>>(subs, items, minv, W, U, ldw); }
   }
 }
 

@@ -19,8 +19,8 @@
 
 #include <algorithm>
 
-#include "nsp_blas.h"
-#include "nsp_dmma.cuh"
+#include "../paper_2101_12164_b200/csrc/nsp_blas.h"
+#include "../paper_2101_12164_b200/csrc/nsp_dmma.cuh"
 
 using namespace nspd;
 
