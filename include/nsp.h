@@ -79,6 +79,8 @@ typedef struct {
   int apply_kernel;      /* a2+a3 of the S_G apply: 0 = one symmetric product with the explicit
                             S_j^{-1} = L22^{-T} L22^{-1} tiles formed in setup (default); 1 = the
                             two batched triangular sweeps with L22 (no extra memory) */
+  int nys_power;         /* q >= 0: q-power iteration Nystrom (eq:power PAPER.md:204-212), G = B_H^q Omega
+                            with the columns orthonormalised between applications; 0 = Alg. 2 as written */
 } nsp_opts;
 
 /* Solver / setup report; caller-owned.  hist / widths are optional caller
@@ -167,7 +169,8 @@ nsp_status nsp_gamma_apply(nsp_ctx* ctx, const double* X, double* Y, int s);
 nsp_status nsp_block_cg(nsp_ctx* ctx, const double* B, double* X, int s, double tol, int maxit,
                         void* ws, nsp_report* rep);
 
-/* Alg. 2 steps 1-12: B = K_G Omega; block CG to tol_inner; Y = A_G X; thin
+/* Alg. 2 steps 1-12 (opts.nys_power = q > 0: first q power steps G <- orth(B_H G), each one block
+ * solve; rep->iters = total inner iterations): B = K_G Omega; block CG to tol_inner; Y = A_G X; thin
  * Cholesky-QR2 of Y; C = sym(Omega^T Y); EVD split at eps; T; EVD of T;
  * U~ = Q W(:,1:k); Z = A_G^{-1} U~; keeps (Z, Sigma) in ctx for nsp_pcg.
  * Omega: device n_gamma_local x (rank+oversample). */

@@ -60,19 +60,42 @@ def nystrom_from_Y(Omega: np.ndarray, Y: np.ndarray, k: int, eps_rel: float = 1e
     return U, e[:r], int(keep.sum())
 
 
-def nystrom_schur(S: SchurOracle, Omega: np.ndarray, k: int, tol_inner: float = 0.1,
-                  maxit_inner: int = 1000, precond: str = "none", tau: float = 1e-14,
-                  eps_rel: float = 1e-12, exact_inner: bool = False) -> NystromResult:
-    d = S.d
-    B = S.k_gamma(Omega)                                  # steps 1-2 (reading C1)
+def orthonormalize(Y: np.ndarray) -> np.ndarray:
+    """Q factor of a Householder QR with diag(R) >= 0 (the orthonormalisation between power steps,
+    PAPER.md:209-211 "orthonormalize the columns between applications of B")."""
+    Q, R = np.linalg.qr(Y)
+    return Q * np.where(np.diag(R) < 0, -1.0, 1.0)
+
+
+def apply_BH(S: SchurOracle, G: np.ndarray, tol_inner, maxit_inner, precond, tau, exact_inner):
+    """Y = B_H G = A_GI S_I^{-1} A_IG G through the border system (reading C1): B = K_G G, solve
+    S_G X = B (BF block CG to tol_inner, or exactly), Y = A_G X.  Returns (Y, block-CG info)."""
+    B = S.k_gamma(G)
     if exact_inner:
         X = np.linalg.solve(S.dense(), B)
         info = {"iters": 0, "status": 0, "widths": []}
     else:
         M = S.solve_AG if precond == "AG" else None
-        X, info = bf_bcg(S.apply, B, tol_inner, maxit_inner, M, tau)   # step 3
-    Y = d.A_G @ X                                         # step 4
-    U, sigma, rC = nystrom_from_Y(Omega, Y, k, eps_rel)
+        X, info = bf_bcg(S.apply, B, tol_inner, maxit_inner, M, tau)
+    return S.d.A_G @ X, info
+
+
+def nystrom_schur(S: SchurOracle, Omega: np.ndarray, k: int, tol_inner: float = 0.1,
+                  maxit_inner: int = 1000, precond: str = "none", tau: float = 1e-14,
+                  eps_rel: float = 1e-12, exact_inner: bool = False, q: int = 0) -> NystromResult:
+    """q >= 0: q-power iteration Nystrom (eq:power PAPER.md:204-212): G = B_H^q Omega with the
+    columns orthonormalised between applications of B_H; q = 0 is Alg. 2 as written.  bcg['iters'] is
+    the total inner iteration count over the q + 1 block solves, bcg['iters_each'] the list."""
+    G = Omega
+    its = []
+    for _ in range(q):                                    # power steps
+        Yp, info = apply_BH(S, G, tol_inner, maxit_inner, precond, tau, exact_inner)
+        its.append(info["iters"])
+        G = orthonormalize(Yp)
+    Y, info = apply_BH(S, G, tol_inner, maxit_inner, precond, tau, exact_inner)   # steps 1-4
+    its.append(info["iters"])
+    info = dict(info, iters=sum(its), iters_each=its)
+    U, sigma, rC = nystrom_from_Y(G, Y, k, eps_rel)
     status = 0 if rC > 0 else NSP_ERR_RANK_COLLAPSE
     Z = S.solve_AG(U) if U.shape[1] else U               # step 11
     return NystromResult(Z, sigma, U, U.shape[1], info, status)

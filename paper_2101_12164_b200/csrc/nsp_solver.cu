@@ -399,60 +399,84 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   double* lamC = cv.take(sp);
   double* lamT = cv.take(sp);
   BcgStatus* hs = (BcgStatus*)c->h_status;
-  // steps 1-2: B = K_G Omega  (reading C1)
-  nspb::copy_pad(Omega, s, Om, sp, n, s, 1.0, st);
-  if ((e = apply_into(c, Om, sp, Bn, sp, s, 2, w.wvu)) != NSP_OK) return e;
-  // step 3: S_G X = B by breakdown-free block CG to tol_inner
-  nsp_report brep{};
-  if (rep) {
-    brep.hist = rep->hist;
-    brep.hist_cap = rep->hist_cap;
-    brep.widths = rep->widths;
-    brep.widths_cap = rep->widths_cap;
-  }
-  nsp_status sb = block_cg_impl(c, Bn, sp, Xn, sp, s, tol_inner, maxit_inner, w, &brep);
-  if (sb < 0) return sb;
-  // step 4: Y = A_G X
-  nspk::spmm(c->AGG2, Xn, sp, nullptr, 0, n, Y, sp, s, 3, true, st);
-  // step 5: Y = Q R by Cholesky-QR2 (shifted Cholesky-QR3 when the first Gram is numerically singular)
-  NSP_CUDA_TRY(c, cudaMemsetAsync(Racc, 0, sm * 8, st));
-  const double* Qin = Y;
-  double* Qout = Qa;
-  int passes = 2;
-  for (int pass = 0; pass < passes; ++pass) {
-    nspb::gram(Qin, sp, sp, Qin, sp, sp, n, G, sp, w.gram, st);
-    nspb::small_chol(G, sp, 2, s, 0.0, Rk, w.st, st);
-    if (pass == 0) {
-      if ((e = read_status(c, w.st, hs)) != NSP_OK) return e;
-      if (hs->fallback) {  // shift = 11 (n s + s(s+1)) u ||Y||_F^2 (shifted CholeskyQR)
-        std::vector<double> gd(sm);
-        NSP_CUDA_TRY(c, cudaMemcpy(gd.data(), G, sm * 8, cudaMemcpyDeviceToHost));
-        double tr = 0.0;
-        for (int i = 0; i < s; ++i) tr += gd[(size_t)i * sp + i];
-        const double shift = 11.0 * ((double)n * s + (double)s * (s + 1)) * 1.1102230246251565e-16 * tr;
-        nspb::small_sym(G, s, sp, shift, st);
-        nspb::small_chol(G, sp, 2, s, 0.0, Rk, w.st, st);
-        passes = 3;
+  // Cholesky-QR2 of Yin -> Q (returned, one of Qa / Qb), R in Racc (shifted Cholesky-QR3 when the
+  // first Gram is numerically singular)
+  auto cholqr = [&](const double* Yin, const double** Qres) -> nsp_status {
+    NSP_CUDA_TRY(c, cudaMemsetAsync(Racc, 0, sm * 8, st));
+    const double* Qin = Yin;
+    double* Qout = Qa;
+    int passes = 2;
+    for (int pass = 0; pass < passes; ++pass) {
+      nspb::gram(Qin, sp, sp, Qin, sp, sp, n, G, sp, w.gram, st);
+      nspb::small_chol(G, sp, 2, s, 0.0, Rk, w.st, st);
+      if (pass == 0) {
+        nsp_status e2 = read_status(c, w.st, hs);
+        if (e2 != NSP_OK) return e2;
+        if (hs->fallback) {  // shift = 11 (n s + s(s+1)) u ||Y||_F^2 (shifted CholeskyQR)
+          std::vector<double> gd(sm);
+          NSP_CUDA_TRY(c, cudaMemcpy(gd.data(), G, sm * 8, cudaMemcpyDeviceToHost));
+          double tr = 0.0;
+          for (int i = 0; i < s; ++i) tr += gd[(size_t)i * sp + i];
+          const double shift = 11.0 * ((double)n * s + (double)s * (s + 1)) * 1.1102230246251565e-16 * tr;
+          nspb::small_sym(G, s, sp, shift, st);
+          nspb::small_chol(G, sp, 2, s, 0.0, Rk, w.st, st);
+          passes = 3;
+        }
       }
+      nspb::small_chol(G, sp, 1, s, 0.0, Tk, w.st, st);      // T = R^{-1}
+      PanelArgs pa{Qout, sp, nullptr, 0, Qin, sp, Tk, sp, 1.0, nullptr};
+      nspb::panel2(pa, nullptr, sp, sp, n, st);
+      if (pass == 0) {
+        NSP_CUDA_TRY(c, cudaMemcpyAsync(Racc, Rk, sm * 8, cudaMemcpyDeviceToDevice, st));
+      } else {
+        nspb::small_gemm(s, s, s, 1.0, Rk, sp, false, Racc, sp, false, 0.0, Rtmp, sp, st);
+        NSP_CUDA_TRY(c, cudaMemcpyAsync(Racc, Rtmp, sm * 8, cudaMemcpyDeviceToDevice, st));
+      }
+      Qin = Qout;
+      Qout = (Qout == Qa) ? Qb : Qa;
     }
-    nspb::small_chol(G, sp, 1, s, 0.0, Tk, w.st, st);      // T = R^{-1}
-    PanelArgs pa{Qout, sp, nullptr, 0, Qin, sp, Tk, sp, 1.0, nullptr};
-    nspb::panel2(pa, nullptr, sp, sp, n, st);
-    if (pass == 0) {
-      NSP_CUDA_TRY(c, cudaMemcpyAsync(Racc, Rk, sm * 8, cudaMemcpyDeviceToDevice, st));
-    } else {
-      nspb::small_gemm(s, s, s, 1.0, Rk, sp, false, Racc, sp, false, 0.0, Rtmp, sp, st);
-      NSP_CUDA_TRY(c, cudaMemcpyAsync(Racc, Rtmp, sm * 8, cudaMemcpyDeviceToDevice, st));
+    nsp_status e2 = read_status(c, w.st, hs);
+    if (e2 != NSP_OK) return e2;
+    if (hs->fallback) {
+      c->err = "nsp_nystrom: Cholesky-QR failed";
+      return NSP_ERR_NUMERICAL;
     }
-    Qin = Qout;
-    Qout = (Qout == Qa) ? Qb : Qa;
+    *Qres = Qin;
+    return NSP_OK;
+  };
+  // G = Omega; q power steps G <- orth(B_H G) (eq:power PAPER.md:204-212), then Alg. 2 steps 1-4 on G
+  nspb::copy_pad(Omega, s, Om, sp, n, s, 1.0, st);
+  const int q = c->opts.nys_power > 0 ? c->opts.nys_power : 0;
+  nsp_report brep{};
+  int total_iters = 0;
+  nsp_status sb = NSP_OK;
+  for (int pw = 0; pw <= q; ++pw) {
+    // steps 1-2: B = K_G G  (reading C1)
+    if ((e = apply_into(c, Om, sp, Bn, sp, s, 2, w.wvu)) != NSP_OK) return e;
+    // step 3: S_G X = B by breakdown-free block CG to tol_inner
+    brep = nsp_report{};
+    if (rep && pw == q) {
+      brep.hist = rep->hist;
+      brep.hist_cap = rep->hist_cap;
+      brep.widths = rep->widths;
+      brep.widths_cap = rep->widths_cap;
+    }
+    nsp_status sbi = block_cg_impl(c, Bn, sp, Xn, sp, s, tol_inner, maxit_inner, w, &brep);
+    if (sbi < 0) return sbi;
+    if (sbi == NSP_NOT_CONVERGED) sb = NSP_NOT_CONVERGED;
+    total_iters += brep.iters;
+    // step 4: Y = A_G X
+    nspk::spmm(c->AGG2, Xn, sp, nullptr, 0, n, Y, sp, s, 3, true, st);
+    if (pw < q) {   // power step: G <- orthonormal basis of Y
+      const double* Qp = nullptr;
+      if ((e = cholqr(Y, &Qp)) != NSP_OK) return e;
+      NSP_CUDA_TRY(c, cudaMemcpyAsync(Om, Qp, blk * 8, cudaMemcpyDeviceToDevice, st));
+    }
   }
-  const double* Q = Qin;
-  if ((e = read_status(c, w.st, hs)) != NSP_OK) return e;
-  if (hs->fallback) {
-    c->err = "nsp_nystrom: Cholesky-QR of Y failed";
-    return NSP_ERR_NUMERICAL;
-  }
+  brep.iters = total_iters;
+  // step 5: Y = Q R
+  const double* Q = nullptr;
+  if ((e = cholqr(Y, &Q)) != NSP_OK) return e;
   // step 6: C = Omega^T Y, symmetrised (reading C6)
   nspb::gram(Om, sp, sp, Y, sp, sp, n, C, sp, w.gram, st);
   nspb::small_sym(C, s, sp, 0.0, st);

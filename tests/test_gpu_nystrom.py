@@ -82,3 +82,25 @@ def test_nystrom_exact_single_separator_gpu():
     lam_bh = np.sort((2 + mu) * ff / (2 + mu - ff))[::-1]
     assert np.allclose(sig[:5], lam_bh[:5], rtol=1e-8)
     ctx.close()
+
+
+@pytest.mark.parametrize("name,kfix", [("cfg1", 3), ("cfg2s", 5), ("cfg5s", 4)])
+def test_nystrom_power_parity(name, kfix):
+    """q-power Nystrom (eq:power PAPER.md:204-212), q = 1 and 2: Sigma and M_2 probes at equal inner
+    iteration counts (kfix per block solve, tol 0) within 1e-8 of the oracle."""
+    from paper_2101_12164_b200 import Context
+    pr, d, S = problem(name)
+    Om = pr.omega()
+    R = block(d.n_gamma, 16, seed=23)
+    for q in (1, 2):
+        ref = O.nystrom_schur(S, Om, pr.rank, 0.0, kfix, q=q)
+        assert ref.bcg["iters_each"] == [kfix] * (q + 1)
+        ctx = Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, factor_gamma=True, nys_power=q)
+        rep = ctx.nystrom(pr.rank, pr.oversample, dev(Om), 0.0, kfix)
+        assert rep["iters"] == (q + 1) * kfix and rep["rank"] == ref.rank
+        sig = ctx.nystrom_sigma()
+        assert np.max(np.abs(sig - ref.sigma) / ref.sigma) <= 1e-8, (q, sig[:3], ref.sigma[:3])
+        Y = torch.empty(d.n_gamma, 16, dtype=torch.float64, device="cuda")
+        ctx.precond_apply(2, dev(R), Y)
+        assert relfro(Y.cpu().numpy(), apply_M2(S, ref.Z, ref.sigma, R)) <= 1e-8
+        ctx.close()

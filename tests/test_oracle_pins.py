@@ -395,3 +395,22 @@ def test_schur_rows_single_separator_closed_form():
     rows = gamma[[0, 3, gamma.size - 1]]
     Y = schur_rows(A.to_scipy(), part, V, rows)
     assert np.max(np.abs(Y - (V * lam)[[0, 3, gamma.size - 1]])) < 1e-13 * lam.max()
+
+
+def test_power_nystrom_converges_to_closed_form():
+    """eq:power: with exact inner solves, q-power iteration with s < rank(B_H)
+    approaches the closed-form top eigenvalues of B_H monotonically in q (the top-k subspace is
+    resolved better; eq:bound_theta_k PAPER.md:1026-1027)."""
+    dims, axis, c = (13, 24), 0, 6
+    A, part = _single_separator(dims, axis, c)
+    d = O.dbbd(A.to_scipy(), part, 2)
+    S = O.SchurOracle(d)
+    _, _, mu, ff = _closed_form_modes(dims, axis, c)
+    lam_bh = np.sort((2 + mu) * ff / (2 + mu - ff))[::-1]
+    Om = philox.gaussian_block(0, 0, d.n_gamma, 8)
+    errs = []
+    for q in range(4):
+        r = O.nystrom_schur(S, Om, 4, exact_inner=True, q=q)
+        errs.append(np.max(np.abs(r.sigma[:4] - lam_bh[:4]) / lam_bh[:4]))
+    assert all(errs[i + 1] <= errs[i] * 1.0001 for i in range(3)), errs
+    assert errs[3] < 1e-2 * errs[0], errs
