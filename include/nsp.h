@@ -81,6 +81,10 @@ typedef struct {
                             two batched triangular sweeps with L22 (no extra memory) */
   int nys_power;         /* q >= 0: q-power iteration Nystrom (eq:power PAPER.md:204-212), G = B_H^q Omega
                             with the columns orthonormalised between applications; 0 = Alg. 2 as written */
+  int nys_form;          /* inner system of nsp_nystrom: 0 = the border system S_G X = K_G G, Y = A_G X
+                            (reading C1, default); 1 = the paper-literal S_I X = A_IG G, Y = A_GI X
+                            (eq:SI) by block PCG preconditioned by A_I;
+                            read by nsp_setup (builds A_I on the interior layout), single rank */
 } nsp_opts;
 
 /* Solver / setup report; caller-owned.  hist / widths are optional caller

@@ -210,7 +210,7 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_Z);
   fr(c->d_sigma);
   comm_free(c);
-  for (DevCSR* m : {&c->A2G, &c->AGG2, &c->AGSH, &c->CB, &c->C1}) {
+  for (DevCSR* m : {&c->A2G, &c->AGG2, &c->AGSH, &c->CB, &c->C1, &c->AII}) {
     fr(m->rowptr);
     fr(m->col);
     fr(m->val);

@@ -826,6 +826,42 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       C1.rowptr[r + 1] = (int32_t)C1.col.size();
     }
   }
+  // ---------------- A_I on the interior layout (band rows, then W/V/U rows) for the paper-literal
+  // S_I inner system (opts.nys_form == 1): every B row carries one extra entry (n_int + row, -1)
+  // so that "A_I P - [0; h_B]" is a single SpMM pass
+  HostCSR32 AII;
+  if (c->opts.nys_form == 1 && c->nranks == 1) {
+    const int64_t n_int = i1_rows + wvu_rows;
+    if (n_int + wvu_rows > INT32_MAX) return fail(c, NSP_ERR_ARG, "nsp_setup: interior rows exceed int32");
+    auto iidx = [&](int64_t u, int jl) -> int32_t {
+      return bidx[u] >= 0 ? (int32_t)(i1_rows + c->subs[jl].wvu_row + bidx[u]) : (int32_t)(i1_row0[jl] + lpos[u]);
+    };
+    AII.rowptr.assign(n_int + 1, 0);
+    std::vector<std::pair<int32_t, double>> ent;
+    for (int64_t r = 0; r < n_int; ++r) {
+      const bool isb = r >= i1_rows;
+      const int64_t v = isb ? b_src[r - i1_rows] : i1_src[r];
+      if (v >= 0) {
+        const int jl = part[v] - B0;
+        ent.clear();
+        for (int64_t q = rp[v]; q < rp[v + 1]; ++q) {
+          const int64_t u = ci[q];
+          if (part[u] != part[v] || (va[q] == 0.0 && u != v)) continue;
+          ent.push_back({iidx(u, jl), va[q]});
+        }
+        std::sort(ent.begin(), ent.end());
+        for (auto& e : ent) {
+          AII.col.push_back(e.first);
+          AII.val.push_back(e.second);
+        }
+        if (isb) {
+          AII.col.push_back((int32_t)(n_int + (r - i1_rows)));
+          AII.val.push_back(-1.0);
+        }
+      }
+      AII.rowptr[r + 1] = (int32_t)AII.col.size();
+    }
+  }
   const double t_host = ms_since(t0);
 
   // ---------------- device upload
@@ -835,6 +871,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   if ((st = upload_csr(c, c->AGG2, AGG2)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->AGSH, AGSH)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->CB, CB)) != NSP_OK) return st;
+  if (!AII.rowptr.empty() && (st = upload_csr(c, c->AII, AII)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->C1, C1)) != NSP_OK) return st;
   if ((st = upload(c, &c->d_i1_src, i1_src)) != NSP_OK) return st;
   if ((st = upload(c, &c->d_b_src, b_src)) != NSP_OK) return st;

@@ -77,9 +77,14 @@ struct Carver {
   }
 };
 
+// Operator of the block CG: kind 0 = S_G on the n_G border rows (reading C1, the default), kind 1 =
+// the paper-literal S_I on the interior rows (eq:SI; interior layout = all blocks' band rows, then
+// all boundary-layer rows; padding rows stay zero) preconditioned by A_I.
 struct BcgWs {
-  int sp;
+  int sp, kind;
+  int64_t n;
   double *X, *R, *P, *Q, *W, *Z;
+  double *tG, *hB, *wB, *agb;   // kind 1 scratch
   double *D, *E, *F, *G, *Ld, *Ldi, *T, *al, *be, *tmp, *Vw, *Vs, *lam, *bnorm, *rsq, *gram, *npart, *wvu;
   BcgStatus* st;
 };
@@ -87,19 +92,27 @@ struct BcgWs {
 static int sp_of(int s) { return ((s + 63) / 64) * 64; }
 size_t ag_ws_doubles(const nsp_ctx* c, int s);
 
-static size_t bcg_layout(const nsp_ctx* c, int s, char* base, BcgWs* w) {
+static size_t bcg_layout(const nsp_ctx* c, int s, char* base, BcgWs* w, int kind = 0) {
   const int sp = sp_of(s);
-  const int64_t n = c->nG;
+  const int64_t n = kind ? c->i1_rows + c->wvu_rows : c->nG;
   Carver cv(base ? base : (char*)nullptr);
   BcgWs t{};
   t.sp = sp;
+  t.kind = kind;
+  t.n = n;
   const size_t blk = (size_t)std::max<int64_t>(n, 1) * sp;
   t.X = cv.take(blk);
   t.R = cv.take(blk);
   t.P = cv.take(blk);
   t.Q = cv.take(blk);
   t.W = cv.take(blk);
-  t.Z = (c->opts.bcg_precond ? cv.take(blk) : nullptr);
+  t.Z = ((kind || c->opts.bcg_precond) ? cv.take(blk) : nullptr);
+  if (kind) {
+    t.tG = cv.take((size_t)std::max<int64_t>(c->nG, 1) * sp);
+    t.hB = cv.take((size_t)std::max<int64_t>(c->wvu_rows, 1) * sp);
+    t.wB = cv.take((size_t)std::max<int64_t>(c->wvu_rows, 1) * sp);
+    t.agb = cv.take(c->has_ag ? ag_ws_doubles(c, sp) : 1);
+  }
   const size_t sm = (size_t)sp * sp;
   t.D = cv.take(sm);
   t.E = cv.take(sm);
@@ -137,13 +150,14 @@ static nsp_status read_status(nsp_ctx* c, BcgStatus* d, BcgStatus* h) {
 // Rows of the local block that enter Grams and norms: all local rows on one rank; with several
 // ranks the private rows of every rank plus the shared rows once (rank 0), SURVEY.md §8(e).
 static int64_t gram_rows(const nsp_ctx* c) { return (c->nranks <= 1 || c->rank == 0) ? c->nG : c->n_priv; }
+static int64_t gram_rows(const nsp_ctx* c, const BcgWs& w) { return w.kind ? w.n : gram_rows(c); }
 
 // orth(Wm): Gram, Cholesky-QR with pivot test, eigen fallback; P = Wm T (reading C3)
 static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Pout) {
   const int sp = w.sp;
-  const int64_t n = c->nG;
+  const int64_t n = w.n;
   cudaStream_t st = c->stream;
-  nspb::gram(Wm, sp, sp, Wm, sp, sp, gram_rows(c), w.G, sp, w.gram, st);
+  nspb::gram(Wm, sp, sp, Wm, sp, sp, gram_rows(c, w), w.G, sp, w.gram, st);
   nsp_status e = comm_allreduce(c, w.G, (size_t)sp * sp);
   if (e != NSP_OK) return e;
   // CholQR with the pivot test (k_chol16 mode 1), T = R^{-1} = L^{-T} (skipped on fallback)
@@ -158,13 +172,62 @@ static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Po
 // Z = M R
 static nsp_status precond(nsp_ctx* c, const double* R, double* Z, int ld, int s, double* wvu);
 
+// A_I^{-1} R on the interior layout, s columns (ld sp): per block, y_B = S_j^{-1}(r_B - A_B1 A_11^{-1}
+// r_1), y_1 = A_11^{-1}(r_1 - A_1B y_B) (the block elimination of reading R3 with s right-hand sides)
+static nsp_status ai_solve(nsp_ctx* c, BcgWs& w, const double* R, double* Z) {
+  const int sp = w.sp;
+  cudaStream_t st = c->stream;
+  const int cw = 32;
+  double* Z1 = Z;
+  double* ZB = Z + c->i1_rows * (int64_t)sp;
+  const double* R1 = R;
+  const double* RB = R + c->i1_rows * (int64_t)sp;
+  NSP_CUDA_TRY(c, cudaMemcpyAsync(Z1, R1, (size_t)c->i1_rows * sp * 8, cudaMemcpyDeviceToDevice, st));
+  nspk::tri_fb(c->d_i1sys, c->nsub, Z1, sp, cw, true, true, st);                              // A_11^{-1} r_1
+  nspk::spmm(c->CB, RB, sp, Z1, sp, c->wvu_rows, w.wB, sp, sp, 1, false, st);                  // r_B - A_B1 t_1
+  if (c->d_minv) {
+    nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, w.wB, ZB, sp, cw, st);           // y_B
+  } else {
+    nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, w.wB, sp, cw, st);
+    NSP_CUDA_TRY(c, cudaMemcpyAsync(ZB, w.wB, (size_t)c->wvu_rows * sp * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  nspk::spmm(c->C1, R1, sp, ZB, sp, c->i1_rows, Z1, sp, sp, 1, false, st);                     // r_1 - A_1B y_B
+  nspk::tri_fb(c->d_i1sys, c->nsub, Z1, sp, cw, true, true, st);                              // y_1
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  return NSP_OK;
+}
+
+// Q = S_I P = A_I P - A_IG A_G^{-1} A_GI P (eq:SI) on the interior layout
+static nsp_status si_apply(nsp_ctx* c, BcgWs& w, const double* P, double* Q, int s) {
+  const int sp = w.sp;
+  cudaStream_t st = c->stream;
+  const double* PB = P + c->i1_rows * (int64_t)sp;
+  nspk::spmm(c->AGG2, nullptr, 0, PB, sp, c->nG, w.tG, sp, s, 2, true, st);                   // A_GI P_B
+  nsp_status e = ag_solve(c, w.tG, sp, w.tG, sp, s, w.agb);                                    // A_G^{-1}
+  if (e != NSP_OK) return e;
+  nspk::spmm(c->A2G, w.tG, sp, nullptr, 0, 0, w.hB, sp, s, 0, true, st);                        // A_IG t
+  nspk::spmm(c->AII, P, sp, w.hB, sp, w.n, Q, sp, s, 1, true, st);                             // A_I P - [0; h_B]
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  return NSP_OK;
+}
+
+static nsp_status op_apply(nsp_ctx* c, BcgWs& w, const double* P, double* Q, int s) {
+  if (w.kind) return si_apply(c, w, P, Q, s);
+  return apply_into(c, P, w.sp, Q, w.sp, s, 1, w.wvu);
+}
+
+static nsp_status op_precond(nsp_ctx* c, BcgWs& w, const double* R, double* Z, int s) {
+  if (w.kind) return ai_solve(c, w, R, Z);
+  return precond(c, R, Z, w.sp, s, w.wvu);
+}
+
 nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int ldx, int s, double tol, int maxit,
                          BcgWs& w, nsp_report* rep) {
   const int sp = w.sp;
-  const int64_t n = c->nG;
+  const int64_t n = w.n;
   cudaStream_t st = c->stream;
   BcgStatus* hs = (BcgStatus*)c->h_status;
-  const bool usem = c->opts.bcg_precond != 0;
+  const bool usem = w.kind ? true : c->opts.bcg_precond != 0;
   int iters = 0, fallbacks = 0;
   nsp_status ret = NSP_NOT_CONVERGED;
   Tracer tr;
@@ -173,7 +236,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   // init: X = 0, R = B, bnorm
   NSP_CUDA_TRY(c, cudaMemsetAsync(w.X, 0, (size_t)n * sp * 8, st));
   nspb::copy_pad(B, ldb, w.R, sp, n, s, 1.0, st);
-  const int64_t ng = gram_rows(c);
+  const int64_t ng = gram_rows(c, w);
   const bool multi = c->nranks > 1;
   nsp_status e;
   nspb::colsq(w.R, sp, ng, s, sp, w.npart, w.rsq, st);
@@ -194,14 +257,14 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     double* Zr = w.R;
     if (usem) {
       NSP_CUDA_TRY(c, cudaMemsetAsync(w.Z, 0, (size_t)n * sp * 8, st));
-      if ((e = precond(c, w.R, w.Z, sp, s, w.wvu)) != NSP_OK) return e;
+      if ((e = op_precond(c, w, w.R, w.Z, s)) != NSP_OK) return e;
       Zr = w.Z;
     }
     if ((e = orth(c, w, Zr, s, w.P)) != NSP_OK) return e;
     for (int it = 0; it < maxit; ++it) {
       // a1-a5: Q = S_G P
       tr.mark("loop");
-      if ((e = apply_into(c, w.P, sp, w.Q, sp, s, 1, w.wvu)) != NSP_OK) return e;
+      if ((e = op_apply(c, w, w.P, w.Q, s)) != NSP_OK) return e;
       tr.mark("apply");
       // a6: D = P^T Q, E = P^T R
       nspb::gram2(w.P, sp, sp, w.Q, w.R, sp, sp, ng, w.D, w.E, sp, w.gram, st);
@@ -259,7 +322,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
       // a9: Z = M R
       Zr = w.R;
       if (usem) {
-        if ((e = precond(c, w.R, w.Z, sp, s, w.wvu)) != NSP_OK) return e;
+        if ((e = op_precond(c, w, w.R, w.Z, s)) != NSP_OK) return e;
         Zr = w.Z;
       }
       // a10: F = Q^T Z, beta = -D^{-1} F, W = Z + P beta
@@ -369,13 +432,20 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   const int64_t n = c->nG;
   cudaStream_t st = c->stream;
   const size_t blk = (size_t)std::max<int64_t>(n, 1) * sp, sm = (size_t)sp * sp;
-  const size_t bcg_bytes = bcg_layout(c, s, nullptr, nullptr);
-  const size_t extra = (6 * blk + 16 * sm + 8 * sp + (size_t)(sp + 1) * (sp + 1)) * 8 + 64 * 256;
+  const int form = c->opts.nys_form == 1 ? 1 : 0;
+  if (form == 1 && (c->nranks != 1 || c->AII.rows == 0)) {
+    c->err = "nsp_nystrom: the S_I form needs opts.nys_form = 1 at nsp_setup (single rank)";
+    return NSP_ERR_STATE;
+  }
+  const int64_t n_int = c->i1_rows + c->wvu_rows;
+  const size_t iblk = form ? (size_t)std::max<int64_t>(n_int, 1) * sp : 0;
+  const size_t bcg_bytes = bcg_layout(c, s, nullptr, nullptr, form);
+  const size_t extra = (6 * blk + 2 * iblk + 16 * sm + 8 * sp + (size_t)(sp + 1) * (sp + 1)) * 8 + 64 * 256;
   char* base;
   nsp_status e = get_ws(c, ws, bcg_bytes + extra, &base);
   if (e != NSP_OK) return e;
   BcgWs w;
-  bcg_layout(c, s, base, &w);
+  bcg_layout(c, s, base, &w, form);
   Carver cv(base + bcg_bytes);
   double* Om = cv.take(blk);
   double* Bn = cv.take(blk);
@@ -398,6 +468,8 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   double* Vw = cv.take((size_t)(sp + 1) * (sp + 1));
   double* lamC = cv.take(sp);
   double* lamT = cv.take(sp);
+  double* Fi = form ? cv.take(iblk) : nullptr;   // S_I form: right-hand side / solution (interior layout)
+  double* Xi = form ? cv.take(iblk) : nullptr;
   BcgStatus* hs = (BcgStatus*)c->h_status;
   // Cholesky-QR2 of Yin -> Q (returned, one of Qa / Qb), R in Racc (shifted Cholesky-QR3 when the
   // first Gram is numerically singular)
@@ -451,6 +523,28 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   int total_iters = 0;
   nsp_status sb = NSP_OK;
   for (int pw = 0; pw <= q; ++pw) {
+    if (form == 1) {   // paper-literal: F = A_IG G, S_I X = F (block PCG, A_I), Y = A_GI X
+      NSP_CUDA_TRY(c, cudaMemsetAsync(Fi, 0, (size_t)c->i1_rows * sp * 8, st));
+      nspk::spmm(c->A2G, Om, sp, nullptr, 0, 0, Fi + c->i1_rows * (int64_t)sp, sp, s, 0, true, st);
+      brep = nsp_report{};
+      if (rep && pw == q) {
+        brep.hist = rep->hist;
+        brep.hist_cap = rep->hist_cap;
+        brep.widths = rep->widths;
+        brep.widths_cap = rep->widths_cap;
+      }
+      nsp_status sbi = block_cg_impl(c, Fi, sp, Xi, sp, s, tol_inner, maxit_inner, w, &brep);
+      if (sbi < 0) return sbi;
+      if (sbi == NSP_NOT_CONVERGED) sb = NSP_NOT_CONVERGED;
+      total_iters += brep.iters;
+      nspk::spmm(c->AGG2, nullptr, 0, Xi + c->i1_rows * (int64_t)sp, sp, n, Y, sp, s, 2, true, st);
+      if (pw < q) {
+        const double* Qp = nullptr;
+        if ((e = cholqr(Y, &Qp)) != NSP_OK) return e;
+        NSP_CUDA_TRY(c, cudaMemcpyAsync(Om, Qp, blk * 8, cudaMemcpyDeviceToDevice, st));
+      }
+      continue;
+    }
     // steps 1-2: B = K_G G  (reading C1)
     if ((e = apply_into(c, Om, sp, Bn, sp, s, 2, w.wvu)) != NSP_OK) return e;
     // step 3: S_G X = B by breakdown-free block CG to tol_inner

@@ -104,3 +104,28 @@ def test_nystrom_power_parity(name, kfix):
         ctx.precond_apply(2, dev(R), Y)
         assert relfro(Y.cpu().numpy(), apply_M2(S, ref.Z, ref.sigma, R)) <= 1e-8
         ctx.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg5s"])
+def test_nystrom_si_form_parity(name):
+    """The paper-literal inner system (eq:SI; Alg. 2 steps 2-4; block PCG preconditioned by A_I,
+    PAPER.md:1181) on the GPU against oracle.si: free-running inner iteration count within +-1, Sigma and
+    M_2 probes within 1e-8 at equal counts (reading C16)."""
+    from paper_2101_12164_b200 import Context
+    pr, d, S = problem(name)
+    Om = pr.omega()
+    ref = O.nystrom_schur_si(S, Om, pr.rank, pr.tol_bcg, 500)
+    ctx = Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, factor_gamma=True, nys_form=1)
+    rep = ctx.nystrom(pr.rank, pr.oversample, dev(Om), pr.tol_bcg, 500)
+    assert rep["converged"] and abs(rep["iters"] - ref.bcg["iters"]) <= 1, (rep["iters"], ref.bcg["iters"])
+    k = ref.bcg["iters"]
+    ref0 = O.nystrom_schur_si(S, Om, pr.rank, 0.0, k)
+    rep0 = ctx.nystrom(pr.rank, pr.oversample, dev(Om), 0.0, k)
+    assert rep0["iters"] == k and rep0["rank"] == ref0.rank
+    sig = ctx.nystrom_sigma()
+    assert np.max(np.abs(sig - ref0.sigma) / ref0.sigma) <= 1e-8, (sig[:3], ref0.sigma[:3])
+    R = block(d.n_gamma, 16, seed=29)
+    Y = torch.empty(d.n_gamma, 16, dtype=torch.float64, device="cuda")
+    ctx.precond_apply(2, dev(R), Y)
+    assert relfro(Y.cpu().numpy(), apply_M2(S, ref0.Z, ref0.sigma, R)) <= 1e-8
+    ctx.close()

@@ -414,3 +414,29 @@ def test_power_nystrom_converges_to_closed_form():
         errs.append(np.max(np.abs(r.sigma[:4] - lam_bh[:4]) / lam_bh[:4]))
     assert all(errs[i + 1] <= errs[i] * 1.0001 for i in range(3)), errs
     assert errs[3] < 1e-2 * errs[0], errs
+
+
+def test_si_formulation_matches_border_formulation():
+    """Reading C1 at the level of the whole Nystrom step: with exact inner solves, the paper-literal
+    S_I system (eq:SI, Alg. 2 steps 2-4) and the border system give the same Y = B_H G, hence the same
+    Sigma; S_I itself is checked against the dense definition A_I - A_IG A_G^{-1} A_GI."""
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    op = O.SIOperator(S)
+    V = philox.gaussian_block(4, 9, op.n_I, 3)
+    SI = op.A_I.toarray() - op.A_IG.toarray() @ np.linalg.solve(d.A_G.toarray(), op.A_IG.T.toarray())
+    assert np.allclose(op.apply(V), SI @ V, rtol=0, atol=1e-12 * np.abs(SI @ V).max())
+    Om = pr.omega()
+    a = O.nystrom_schur_si(S, Om, pr.rank, tol_inner=1e-13, maxit_inner=2000)
+    b = O.nystrom_schur(S, Om, pr.rank, exact_inner=True)
+    assert np.max(np.abs(a.sigma - b.sigma) / b.sigma) < 1e-9
+
+
+def test_si_block_pcg_iterations_cfg1():
+    """Context (parity unpinned): the S_I block PCG (A_I preconditioner) at tol 0.1 converges in a few
+    iterations on cfg1 (the paper's it_SI are 24-72 on its matrices, tab:blockvsclassic)."""
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    r = O.nystrom_schur_si(O.SchurOracle(d), pr.omega(), pr.rank, tol_inner=0.1)
+    assert r.bcg["status"] == 0 and 1 <= r.bcg["iters"] <= 20 and r.rank == pr.rank
