@@ -48,7 +48,11 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   nspk::spmm(c->A2G, X, ldx, nullptr, 0, 0, wvu, ldw, s, 0, true, c->stream);
   // a2 + a3: U = L22^{-T} L22^{-1} W for every block, one launch: either as one symmetric product
   // with the setup's S_j^{-1} tiles (k_symm, no dependency chain) or as the two batched sweeps
-  const bool prof = c->prof_on && (size_t)(c->prof_used + 2) <= c->prof_ev.size();
+  // live timing of the a2+a3 kernel: an event pair per eager call, or (inside the captured block-CG
+  // graph) the context's dedicated pair, read after every graph launch (nsp_solver.cu)
+  const bool gprof = c->prof_on && c->capturing;
+  const bool prof = !gprof && c->prof_on && (size_t)(c->prof_used + 2) <= c->prof_ev.size();
+  if (gprof) cudaEventRecordWithFlags(c->gprof_ev[0], c->stream, cudaEventRecordExternal);   // a graph node
   if (prof) cudaEventRecord(c->prof_ev[c->prof_used], c->stream);
   double* U = wvu;
   if (c->d_minv) {
@@ -56,6 +60,10 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
     nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream);
   } else {
     nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, wvu, ldw, cw, c->stream);
+  }
+  if (gprof) {
+    cudaEventRecordWithFlags(c->gprof_ev[1], c->stream, cudaEventRecordExternal);
+    c->gprof_in_graph = true;
   }
   if (prof) {
     cudaEventRecord(c->prof_ev[c->prof_used + 1], c->stream);
@@ -117,7 +125,14 @@ nsp_status nsp_profile(nsp_ctx* c, int enable) {
   if (enable && c->prof_ev.empty()) {
     c->prof_ev.resize(2 * 4096);
     for (auto& e : c->prof_ev) NSP_CUDA_TRY(c, cudaEventCreate(&e));
+    for (auto& e : c->gprof_ev) NSP_CUDA_TRY(c, cudaEventCreate(&e));
   }
+  if (c->prof_on != enable && c->bcg_graph) {   // the cached graph bakes in (or omits) the timing events
+    cudaGraphExecDestroy(c->bcg_graph);
+    c->bcg_graph = nullptr;
+  }
+  c->gprof_ms = 0.0;
+  c->gprof_n = 0;
   c->prof_on = enable;
   c->prof_used = 0;
   return NSP_OK;
@@ -132,9 +147,11 @@ nsp_status nsp_profile_read(nsp_ctx* c, double* sweep_ms, long long* sweeps) {
     NSP_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->prof_ev[k], c->prof_ev[k + 1]));
     tot += ms;
   }
-  if (sweep_ms) *sweep_ms = tot;
-  if (sweeps) *sweeps = c->prof_used / 2;
+  if (sweep_ms) *sweep_ms = tot + c->gprof_ms;
+  if (sweeps) *sweeps = c->prof_used / 2 + c->gprof_n;
   c->prof_used = 0;
+  c->gprof_ms = 0.0;
+  c->gprof_n = 0;
   return NSP_OK;
 }
 
@@ -210,6 +227,8 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_Z);
   fr(c->d_sigma);
   comm_free(c);
+  if (c->bcg_graph) cudaGraphExecDestroy(c->bcg_graph);
+  if (c->gstream) cudaStreamDestroy(c->gstream);
   for (DevCSR* m : {&c->A2G, &c->AGG2, &c->AGSH, &c->CB, &c->C1, &c->AII}) {
     fr(m->rowptr);
     fr(m->col);
@@ -217,6 +236,8 @@ void nsp_destroy(nsp_ctx* c) {
   }
   fr(c->ws_int);
   for (auto& e : c->prof_ev) cudaEventDestroy(e);
+  if (!c->prof_ev.empty())
+    for (auto& e : c->gprof_ev) cudaEventDestroy(e);
   if (c->h_status) cudaFreeHost(c->h_status);
   solver_free(c);
   delete c;
@@ -227,4 +248,6 @@ void nsp_destroy(nsp_ctx* c) {
 #include <atomic>
 static std::atomic<long long> g_launches{0};
 void nsp_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void nsp_count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+long long nsp_launch_count() { return g_launches.load(); }
 extern "C" long long nsp_kernel_launches(void) { return g_launches.load(); }

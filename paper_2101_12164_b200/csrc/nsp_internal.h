@@ -49,6 +49,19 @@ struct HostCSR32 {
   std::vector<double> val;
 };
 
+// key of the cached block-CG iteration graph (nsp_solver.cu)
+struct GraphKey {
+  const void* X = nullptr;
+  int64_t n = 0;
+  int s = 0;
+  double tol = 0.0;
+  int kind = 0, usem = 0;
+  double tau = 0.0;
+  bool operator==(const GraphKey& o) const {
+    return X == o.X && n == o.n && s == o.s && tol == o.tol && kind == o.kind && usem == o.usem && tau == o.tau;
+  }
+};
+
 struct nsp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -116,6 +129,16 @@ struct nsp_ctx {
   // small pinned host status
   void* h_status = nullptr;
 
+  // cached CUDA graph of one block-CG iteration (tail + head), captured on gstream
+  cudaGraphExec_t bcg_graph = nullptr;
+  GraphKey bcg_key;
+  long long bcg_graph_kernels = 0;   // kernel nodes per launch of bcg_graph (launch evidence counter)
+  cudaStream_t gstream = nullptr;
+  bool capturing = false;          // block CG is capturing its iteration graph
+  bool gprof_in_graph = false;     // the cached graph records gprof_ev around a2+a3
+  cudaEvent_t gprof_ev[2] = {nullptr, nullptr};
+  double gprof_ms = 0.0;
+  long long gprof_n = 0;
   // live kernel timing (nsp_profile): event pairs around the factor-sweep launches
   int prof_on = 0;
   std::vector<cudaEvent_t> prof_ev;   // 2 per record
@@ -125,6 +148,8 @@ struct nsp_ctx {
 
 // number of device kernels launched by this library (evidence counter)
 void nsp_count_launch();
+void nsp_count_launches(long long k);   // kernels executed by a graph launch
+long long nsp_launch_count();
 
 // kernel launchers (nsp_kernels.cu)
 namespace nspk {

@@ -251,49 +251,114 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   if (e != NSP_OK) return e;
   if (rep && rep->hist && rep->hist_cap > 0) rep->hist[0] = hs->relres;
   double relres = hs->relres;
+  double* Zr = usem ? w.Z : w.R;
+  // head: a1-a8 (Q = S P, D|E, chol(D), alpha, X/R update, norms, convergence) + the status copy
+  auto head = [&]() -> nsp_status {
+    cudaStream_t q = c->stream;
+    nsp_status e2;
+    tr.mark("loop");
+    if ((e2 = op_apply(c, w, w.P, w.Q, s)) != NSP_OK) return e2;
+    tr.mark("apply");
+    nspb::gram2(w.P, sp, sp, w.Q, w.R, sp, sp, ng, w.D, w.E, sp, w.gram, q);
+    if (multi) {   // D and E are adjacent in the workspace: one allreduce
+      if ((e2 = comm_allreduce(c, w.D, (size_t)2 * sp * sp)) != NSP_OK) return e2;
+    }
+    tr.mark("gram_DE");
+    nspb::chol_fac(w.D, sp, 0, -1, 0.0, w.Ld, w.st, q);        // D = L L^T
+    tr.mark("chol_D");
+    nspb::chol_solve(w.Ld, sp, w.E, sp, w.al, sp, 1.0, true, true, nullptr, q);   // alpha = D^{-1} E
+    tr.mark("alpha");
+    {
+      PanelArgs px{w.X, sp, w.X, sp, w.P, sp, w.al, sp, 1.0, nullptr};
+      PanelArgs pr{w.R, sp, w.R, sp, w.Q, sp, w.al, sp, -1.0, multi ? nullptr : w.npart};
+      nspb::panel2(px, &pr, sp, sp, n, q);
+    }
+    if (multi) {
+      nspb::colsq(w.R, sp, ng, s, sp, w.npart, w.rsq, q);
+      if ((e2 = comm_allreduce(c, w.rsq, sp)) != NSP_OK) return e2;
+    } else {
+      nspb::colsq_reduce(w.npart, (int)((n + 63) / 64), sp, w.rsq, q);
+    }
+    nspb::converge(w.rsq, w.bnorm, s, tol, w.st, nullptr, q);
+    tr.mark("XR_update");
+    NSP_CUDA_TRY(c, cudaMemcpyAsync(hs, w.st, sizeof(BcgStatus), cudaMemcpyDeviceToHost, q));
+    NSP_CUDA_TRY(c, cudaGetLastError());
+    return NSP_OK;
+  };
+  // tail: a9-a11 (Z = M R, F = Q^T Z, beta, W = Z + P beta, P = orth(W))
+  auto tail = [&]() -> nsp_status {
+    cudaStream_t q = c->stream;
+    nsp_status e2;
+    if (usem && (e2 = op_precond(c, w, w.R, w.Z, s)) != NSP_OK) return e2;
+    nspb::gram(w.Q, sp, sp, Zr, sp, sp, ng, w.F, sp, w.gram, q);
+    if ((e2 = comm_allreduce(c, w.F, (size_t)sp * sp)) != NSP_OK) return e2;
+    nspb::chol_solve(w.Ld, sp, w.F, sp, w.be, sp, -1.0, true, true, nullptr, q);  // beta = -D^{-1} F
+    tr.mark("beta");
+    nspb::panel(w.W, sp, Zr, sp, w.P, sp, w.be, sp, sp, sp, n, 1.0, nullptr, q);
+    tr.mark("W");
+    if ((e2 = orth(c, w, w.W, s, w.P)) != NSP_OK) return e2;
+    tr.mark("orth");
+    return NSP_OK;
+  };
+  // One CUDA graph for tail + head of every iteration after the first (launch-bound loop;
+  // single rank, no tracing, NSP_GRAPH != 0): captured on a private stream, launched on the
+  // context stream, cached in the context while the workspace / s / tol / operator are unchanged.
+  const char* genv = getenv("NSP_GRAPH");
+  const bool use_graph = !multi && !tr.on && !(genv && genv[0] == '0');
+  cudaGraphExec_t gexec = nullptr;
+  if (use_graph) {
+    const GraphKey key{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau};
+    if (c->bcg_graph && c->bcg_key == key) gexec = c->bcg_graph;
+  }
   if (hs->converged) {
     ret = NSP_OK;
   } else {
-    double* Zr = w.R;
     if (usem) {
       NSP_CUDA_TRY(c, cudaMemsetAsync(w.Z, 0, (size_t)n * sp * 8, st));
       if ((e = op_precond(c, w, w.R, w.Z, s)) != NSP_OK) return e;
-      Zr = w.Z;
     }
     if ((e = orth(c, w, Zr, s, w.P)) != NSP_OK) return e;
     for (int it = 0; it < maxit; ++it) {
-      // a1-a5: Q = S_G P
-      tr.mark("loop");
-      if ((e = op_apply(c, w, w.P, w.Q, s)) != NSP_OK) return e;
-      tr.mark("apply");
-      // a6: D = P^T Q, E = P^T R
-      nspb::gram2(w.P, sp, sp, w.Q, w.R, sp, sp, ng, w.D, w.E, sp, w.gram, st);
-      if (multi) {   // D and E are adjacent in the workspace: one allreduce
-        if ((e = comm_allreduce(c, w.D, (size_t)2 * sp * sp)) != NSP_OK) return e;
-      }
-      tr.mark("gram_DE");
-      // a7: chol(D), alpha = D^{-1} E
-      nspb::chol_fac(w.D, sp, 0, -1, 0.0, w.Ld, w.st, st);        // D = L L^T
-      tr.mark("chol_D");
-      nspb::chol_solve(w.Ld, sp, w.E, sp, w.al, sp, 1.0, true, true, nullptr, st);   // alpha = D^{-1} E
-      tr.mark("alpha");
-      // a8: X += P alpha, R -= Q alpha, column norms
-      {
-        PanelArgs px{w.X, sp, w.X, sp, w.P, sp, w.al, sp, 1.0, nullptr};
-        PanelArgs pr{w.R, sp, w.R, sp, w.Q, sp, w.al, sp, -1.0, multi ? nullptr : w.npart};
-        nspb::panel2(px, &pr, sp, sp, n, st);
-      }
-      if (multi) {
-        nspb::colsq(w.R, sp, ng, s, sp, w.npart, w.rsq, st);
-        if ((e = comm_allreduce(c, w.rsq, sp)) != NSP_OK) return e;
+      if (it == 0 || !use_graph) {
+        if (it > 0 && (e = tail()) != NSP_OK) return e;
+        if ((e = head()) != NSP_OK) return e;
       } else {
-        nspb::colsq_reduce(w.npart, (int)((n + 63) / 64), sp, w.rsq, st);
+        if (!gexec) {
+          if (!c->gstream) NSP_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+          if (c->bcg_graph) {
+            cudaGraphExecDestroy(c->bcg_graph);
+            c->bcg_graph = nullptr;
+          }
+          cudaGraph_t g = nullptr;
+          c->stream = c->gstream;
+          c->capturing = true;
+          c->gprof_in_graph = false;
+          const long long l0 = nsp_launch_count();
+          NSP_CUDA_TRY(c, cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeRelaxed));
+          nsp_status ec = tail();
+          if (ec == NSP_OK) ec = head();
+          cudaError_t ce = cudaStreamEndCapture(c->gstream, &g);
+          c->stream = st;
+          c->capturing = false;
+          c->bcg_graph_kernels = nsp_launch_count() - l0;   // captured, not executed
+          nsp_count_launches(-c->bcg_graph_kernels);
+          if (ec != NSP_OK) return ec;
+          NSP_CUDA_TRY(c, ce);
+          NSP_CUDA_TRY(c, cudaGraphInstantiate(&gexec, g, 0));
+          cudaGraphDestroy(g);
+          c->bcg_graph = gexec;
+          c->bcg_key = GraphKey{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau};
+        }
+        NSP_CUDA_TRY(c, cudaGraphLaunch(gexec, st));
+        nsp_count_launches(c->bcg_graph_kernels);
       }
-      double* hslot = nullptr;
-      nspb::converge(w.rsq, w.bnorm, s, tol, w.st, hslot, st);
-      tr.mark("XR_update");
-      NSP_CUDA_TRY(c, cudaGetLastError());
-      if ((e = read_status(c, w.st, hs)) != NSP_OK) return e;
+      NSP_CUDA_TRY(c, cudaStreamSynchronize(st));
+      if (it > 0 && use_graph && c->prof_on && c->gprof_in_graph) {
+        float ms = 0.f;
+        NSP_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->gprof_ev[0], c->gprof_ev[1]));
+        c->gprof_ms += ms;
+        c->gprof_n += 1;
+      }
       tr.mark("sync");
       iters = it + 1;
       fallbacks += hs->fallback;
@@ -319,22 +384,6 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
         ret = NSP_OK;
         break;
       }
-      // a9: Z = M R
-      Zr = w.R;
-      if (usem) {
-        if ((e = op_precond(c, w, w.R, w.Z, s)) != NSP_OK) return e;
-        Zr = w.Z;
-      }
-      // a10: F = Q^T Z, beta = -D^{-1} F, W = Z + P beta
-      nspb::gram(w.Q, sp, sp, Zr, sp, sp, ng, w.F, sp, w.gram, st);
-      if ((e = comm_allreduce(c, w.F, (size_t)sp * sp)) != NSP_OK) return e;
-      nspb::chol_solve(w.Ld, sp, w.F, sp, w.be, sp, -1.0, true, true, nullptr, st);  // beta = -D^{-1} F
-      tr.mark("beta");
-      nspb::panel(w.W, sp, Zr, sp, w.P, sp, w.be, sp, sp, sp, n, 1.0, nullptr, st);
-      tr.mark("W");
-      // a11: P = orth(W)
-      if ((e = orth(c, w, w.W, s, w.P)) != NSP_OK) return e;
-      tr.mark("orth");
     }
   }
   // copy X out

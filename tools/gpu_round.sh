@@ -4,7 +4,7 @@
 #   bash tools/gpu_round.sh [tag] [kernel-regex]
 set -u
 TAG=${1:-r01}
-KREGEX=${2:-trsm_fb}
+KREGEX=${2:-k_symm}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 nvidia-smi > "$OUT/nvidia-smi.txt" 2>&1
