@@ -41,38 +41,6 @@ __device__ __forceinline__ void cta_mma(const double* __restrict__ As, int lda, 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int m0 = (warp >> 1) * 16, n0 = (warp & 1) * NF * 8;
-#ifdef NSP_MMA_PIPE
-  // explicit register double-buffering of the fragments: loads for k+4 issue before the MMAs of k
-  double a[2][2], b[2][NF];
-  auto load = [&](int buf, int k) {
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int m = m0 + i * 8 + g, kk = k + t;
-      a[buf][i] = TA ? As[kk * lda + m] : As[m * lda + kk];
-    }
-#pragma unroll
-    for (int j = 0; j < NF; ++j) {
-      const int n = n0 + j * 8 + g, kk = k + t;
-      b[buf][j] = TB ? Bs[n * ldb + kk] : Bs[kk * ldb + n];
-    }
-  };
-  load(0, 0);
-#pragma unroll 2
-  for (int k = 0; k < K; k += 8) {
-    if (k + 4 < K) load(1, k + 4);
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < NF; ++j) dmma(acc[i][j][0], acc[i][j][1], a[0][i], b[0][j]);
-    if (k + 8 < K) load(0, k + 8);
-    if (k + 4 < K)
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < NF; ++j) dmma(acc[i][j][0], acc[i][j][1], a[1][i], b[1][j]);
-  }
-  return;
-#endif
 #pragma unroll 4
   for (int k = 0; k < K; k += 4) {
     double a[2], b[NF];
