@@ -114,6 +114,7 @@ struct nsp_ctx {
   //   CB rows = W/V/U rows:  [ I | -A_B1 ]  (cols < wvu_rows: identity, cols >= wvu_rows: band row)
   //   C1 rows = band rows:   [ I | -A_1B ]  (cols < i1_rows: identity, cols >= i1_rows: W/V/U row)
   int64_t i1_rows = 0;
+  int i1_wbmax = -1;          // largest band half-width (tiles) of the I1 factors
   TriSys* d_i1sys = nullptr;
   int32_t* d_i1_src = nullptr;
   int32_t* d_b_src = nullptr;
@@ -171,7 +172,9 @@ void l22_inverse(const FacSub* subs, int nsub, int max_ntb, const double* dense,
 // a2+a3 as U_j = M_j W_j (items = (block, tile row)), W -> U out of place
 void symm(const FacSub* subs, const int2* items, int nitems, const double* minv, const double* W, double* U, int ldw,
           int cw, cudaStream_t st);
-void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st);
+// wbmax: largest band half-width (tiles) of the systems, -1 unknown; <= 2 with cw 32 selects k_band_fb
+void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,
+            int wbmax = -1);
 void gather_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,
                  double scale, cudaStream_t st);
 void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,

@@ -1,6 +1,7 @@
 // Device kernels of the S_G apply and the setup factorisation (north_star (a), (b); §8(a) rows
 // a1-a5, s0).  fp64 throughout; dense tile products on the DMMA pipe (mma.sync f64).
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "nsp_dmma.cuh"
@@ -705,6 +706,273 @@ __global__ void __launch_bounds__(256) k_tri_fb(const TriSys* __restrict__ sys, 
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Narrow-band forward + backward triangular solves (wb <= WBM tiles, e.g. the A_G factor of the 2D
+// configs, RCM bandwidth 16): the sweep is a chain of (row I, tile J) products whose factor tiles
+// do not depend on the solution, so they (and the right-hand-side tile of each row) stream through
+// an NS-stage cp.async ring issued NS-1 products ahead, while the last WBM + 1 solution tiles stay
+// in shared memory (no reload).  One barrier per product, one more per row.  Same arithmetic as
+// k_tri_fb (diagonal tiles hold inv(L_II)), bitwise the same products in the same order.
+// ---------------------------------------------------------------------------------------------
+template <int CW, int NS, int WBM>
+__global__ void __launch_bounds__(256) k_band_fb(const TriSys* __restrict__ sys, double* buf, int ldw, int fwd,
+                                                 int bwd) {
+  constexpr int NF = CW / 16;
+  constexpr int LDV = CW + 4;
+  constexpr int NV = WBM + 1;
+  extern __shared__ double sm[];
+  double* Lr = sm;                               // NS x (64 x LDT)
+  double* Wr = sm + NS * 64 * LDT;               // NS x (64 x LDV): right-hand side tile of a diag step
+  double* Vr = Wr + NS * 64 * LDV;               // NV x (64 x LDV): latest solution tiles
+  const TriSys sy = sys[blockIdx.x];
+  const int nt = sy.nt, wb = sy.wb;
+  if (nt == 0) return;
+  const int c0 = blockIdx.y * CW;
+  const double* T = sy.T;
+  double* Wb = buf + sy.row0 * (int64_t)ldw + c0;
+  auto tile = [&](int I, int J) -> const double* { return T + ((int64_t)J * (wb + 1) + (I - J)) * NSP_TILE_ELEMS; };
+  double acc[2][NF][2];
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool fw = pass == 0;
+    if (fw ? !fwd : !bwd) continue;
+    // product cursor over the sweep: row I, then its off-diagonal tiles, then the diagonal
+    // forward: J = max(0, I - wb) .. I - 1, then I;  backward (rows descending): J = I + 1 .. min(nt-1, I + wb), then I
+    auto first_j = [&](int I) { return fw ? max(0, I - wb) : I + 1; };
+    auto last_off = [&](int I) { return fw ? I - 1 : min(nt - 1, I + wb); };
+    auto next_row = [&](int I) { return fw ? I + 1 : I - 1; };
+    int iI = fw ? 0 : nt - 1, iJ = first_j(iI);   // issue cursor (iJ > last_off => diagonal)
+    int ip = 0;
+    auto issue = [&]() {
+      if (fw ? iI >= nt : iI < 0) return;
+      double* Ls = Lr + (ip % NS) * 64 * LDT;
+      const bool diag = iJ > last_off(iI);
+      if (!diag) {
+        cp_block(Ls, LDT, fw ? tile(iI, iJ) : tile(iJ, iI), 64, 64, 64);
+        ++iJ;
+      } else {
+        cp_block(Ls, LDT, tile(iI, iI), 64, 64, 64);
+        cp_block(Wr + (ip % NS) * 64 * LDV, LDV, Wb + (int64_t)iI * 64 * ldw, ldw, 64, CW);
+        iI = next_row(iI);
+        iJ = (fw ? iI < nt : iI >= 0) ? first_j(iI) : 0;
+      }
+      ++ip;
+    };
+#pragma unroll 1
+    for (int p = 0; p < NS - 1; ++p) {
+      issue();
+      cp_commit();
+    }
+    int I = fw ? 0 : nt - 1, J = first_j(I);
+    acc_zero(acc);
+    for (int q = 0;; ++q) {
+      if (fw ? I >= nt : I < 0) break;
+      cp_wait<NS - 2>();
+      __syncthreads();
+      issue();
+      cp_commit();
+      const double* Ls = Lr + (q % NS) * 64 * LDT;
+      if (J <= last_off(I)) {   // acc += L_IJ V_J (forward) / L_JI^T U_J (backward)
+        const double* Vs = Vr + (J % NV) * 64 * LDV;
+        if (fw) cta_mma<NF, false, false>(Ls, LDT, Vs, LDV, acc);
+        else cta_mma<NF, true, false>(Ls, LDT, Vs, LDV, acc);
+        ++J;
+        continue;
+      }
+      // diagonal: R = W_I - acc (in place in the stage), V_I = inv(L_II) R (forward) / inv(L_II)^T R
+      double* Ws = Wr + (q % NS) * 64 * LDV;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+          Ws[r * LDV + c] -= acc[i][j][0];
+          Ws[r * LDV + c + 1] -= acc[i][j][1];
+        }
+      __syncthreads();
+      acc_zero(acc);
+      if (fw) cta_mma<NF, false, false>(Ls, LDT, Ws, LDV, acc);
+      else cta_mma<NF, true, false>(Ls, LDT, Ws, LDV, acc);
+      double* Vs = Vr + (I % NV) * 64 * LDV;
+      double* out = Wb + (int64_t)I * 64 * ldw;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+          Vs[r * LDV + c] = acc[i][j][0];
+          Vs[r * LDV + c + 1] = acc[i][j][1];
+          *reinterpret_cast<double2*>(out + (int64_t)r * ldw + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+        }
+      acc_zero(acc);
+      I = next_row(I);
+      J = (fw ? I < nt : I >= 0) ? first_j(I) : 0;
+    }
+    cp_wait<0>();
+    __threadfence();
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Single right-hand side (s = 1, the outer PCG's A_G^{-1}) narrow-band forward + backward solve:
+// the same product chain as k_band_fb, as 64 x 64 matrix-VECTOR products on the FMA pipe (a DMMA
+// tile product would do 32x the work for one column).  Factor tiles (32 KB, contiguous) and the
+// right-hand-side tile stream into an NS-stage ring by TMA bulk copies (cp.async.bulk + mbarrier,
+// one elected thread), issued NS-1 products ahead; the last WBM + 1 solution vectors stay in shared
+// memory.  Row products (forward): warp w owns rows 8w..8w+7, lanes run along the row (conflict-
+// free), butterfly reduction.  Column products (backward, L^T): thread t owns column t & 63 for a
+// quarter of the rows, the 4 partials meet in shared memory.  Same operations in a fixed order.
+// buf (ld 1) holds the right-hand side on entry and the solution on exit.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_copy(uint64_t* bar, void* dst, const void* src, unsigned bytes) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_add_copy(uint64_t* bar, void* dst, const void* src, unsigned bytes) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(bytes));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W;\n}\n" ::"r"(b),
+               "r"(phase));
+}
+
+template <int NS, int WBM>
+__global__ void __launch_bounds__(256) k_band_fb_vec(const TriSys* __restrict__ sys, double* buf, int fwd, int bwd) {
+  constexpr int NV = WBM + 1;
+  extern __shared__ __align__(128) double sm[];
+  double* Lr = sm;                          // NS x 4096 (contiguous 64 x 64 tiles)
+  double* Wr = sm + NS * 4096;              // NS x 64 (rhs tile of a diagonal step)
+  double* Vr = Wr + NS * 64;                // NV x 64
+  double* Pp = Vr + NV * 64;                // 4 x 64 column partials
+  double* Rs = Pp + 4 * 64;                 // 64 residual
+  __shared__ __align__(8) uint64_t bar[NS];
+  const TriSys sy = sys[blockIdx.x];
+  const int nt = sy.nt, wb = sy.wb;
+  if (nt == 0) return;
+  const double* T = sy.T;
+  double* Wb = buf + sy.row0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int col = tid & 63, grp = tid >> 6;
+  auto tile = [&](int I, int J) -> const double* { return T + ((int64_t)J * (wb + 1) + (I - J)) * NSP_TILE_ELEMS; };
+  if (tid == 0)
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  unsigned uses[NS];   // completed phases per slot (thread-uniform)
+#pragma unroll
+  for (int i = 0; i < NS; ++i) uses[i] = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool fw = pass == 0;
+    if (fw ? !fwd : !bwd) continue;
+    auto first_j = [&](int I) { return fw ? max(0, I - wb) : I + 1; };
+    auto last_off = [&](int I) { return fw ? I - 1 : min(nt - 1, I + wb); };
+    auto next_row = [&](int I) { return fw ? I + 1 : I - 1; };
+    int iI = fw ? 0 : nt - 1, iJ = first_j(iI), ip = 0;
+    auto issue = [&]() {   // one product's tiles into slot ip % NS (thread 0 issues)
+      if (fw ? iI >= nt : iI < 0) return;
+      const int sl = ip % NS;
+      if (iJ <= last_off(iI)) {
+        if (tid == 0) mbar_expect_copy(&bar[sl], Lr + sl * 4096, fw ? tile(iI, iJ) : tile(iJ, iI), 32768);
+        ++iJ;
+      } else {
+        if (tid == 0) {
+          mbar_expect_copy(&bar[sl], Lr + sl * 4096, tile(iI, iI), 32768);
+          mbar_add_copy(&bar[sl], Wr + sl * 64, Wb + (int64_t)iI * 64, 512);
+        }
+        iI = next_row(iI);
+        iJ = (fw ? iI < nt : iI >= 0) ? first_j(iI) : 0;
+      }
+      ++ip;
+    };
+    for (int p = 0; p < NS - 1; ++p) issue();
+    int I = fw ? 0 : nt - 1, J = first_j(I);
+    double racc = 0.0;   // forward: lane j of warp w holds the sum of row 8w + j (after reduction)
+    double cacc = 0.0;   // backward: column partial (col, grp)
+    for (int q = 0;; ++q) {
+      if (fw ? I >= nt : I < 0) break;
+      const int sl = q % NS;
+      mbar_wait(&bar[sl], uses[sl] & 1);
+      ++uses[sl];
+      __syncthreads();          // every thread is done with the slot the next issue overwrites
+      issue();
+      const double* L = Lr + sl * 4096;
+      const bool diag = J > last_off(I);
+      const double* v = diag ? nullptr : Vr + (J % NV) * 64;
+      if (diag) {                // residual R = W_I - acc
+        if (fw) {
+          if (lane < 8) Rs[warp * 8 + lane] = Wr[sl * 64 + warp * 8 + lane] - racc;
+        } else {
+          Pp[grp * 64 + col] = cacc;
+          __syncthreads();
+          if (tid < 64) Rs[tid] = Wr[sl * 64 + tid] - ((Pp[tid] + Pp[64 + tid]) + (Pp[128 + tid] + Pp[192 + tid]));
+        }
+        __syncthreads();
+        v = Rs;
+      }
+      if (fw) {                  // y_r = sum_c L[r][c] v[c], rows 8w .. 8w+7
+        double p8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double* Lrow = L + (warp * 8 + i) * 64;
+          p8[i] = fma(Lrow[lane], v[lane], Lrow[lane + 32] * v[lane + 32]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) p8[i] += __shfl_xor_sync(0xffffffffu, p8[i], o);
+        double mine = p8[0];
+#pragma unroll
+        for (int i = 1; i < 8; ++i)
+          if (lane == i) mine = p8[i];
+        if (!diag) {
+          racc += mine;
+        } else if (lane < 8) {
+          Vr[(I % NV) * 64 + warp * 8 + lane] = mine;
+          Wb[(int64_t)I * 64 + warp * 8 + lane] = mine;
+        }
+      } else {                   // y_c = sum_r L[r][c] v[r], rows 16 grp .. 16 grp + 15
+        double y = 0.0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) y = fma(L[(grp * 16 + i) * 64 + col], v[grp * 16 + i], y);
+        if (!diag) {
+          cacc += y;
+        } else {
+          Pp[grp * 64 + col] = y;
+          __syncthreads();
+          if (tid < 64) {
+            const double u = (Pp[tid] + Pp[64 + tid]) + (Pp[128 + tid] + Pp[192 + tid]);
+            Vr[(I % NV) * 64 + tid] = u;
+            Wb[(int64_t)I * 64 + tid] = u;
+          }
+        }
+      }
+      if (diag) {
+        racc = 0.0;
+        cacc = 0.0;
+        I = next_row(I);
+        J = (fw ? I < nt : I >= 0) ? first_j(I) : 0;
+      } else {
+        ++J;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+  }
+}
+
 // row gather / scatter between an n x s block (ld lds) and a padded buffer (ld ldd):
 // gather: dst[r][c] = idx[r] >= 0 && c < s ? scale * src[idx[r]][c] : 0  for r < rows, c < ldd
 // scatter: dst[idx[r]][c] = src[r][c]   (c < s, idx[r] >= 0)
@@ -769,9 +1037,34 @@ void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, i
     { nsp_count_launch(); k_spmm<8><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
 }
 
-void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st) {
+void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,
+            int wbmax) {
   if (nsys <= 0) return;
   dim3 grid(nsys, ldw / cw);
+  if (wbmax >= 0 && wbmax <= 2 && cw == 1 && ldw == 1 && !getenv("NSP_NO_BAND")) {   // one column: matvec chain
+    constexpr int NS = 4;
+    const size_t smem = (NS * 4096 + NS * 64 + 3 * 64 + 4 * 64 + 64) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_band_fb_vec<NS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    { nsp_count_launch(); k_band_fb_vec<NS, 2><<<nsys, 256, smem, st>>>(sys, buf, fwd, bwd); }
+    return;
+  }
+  if (cw == 1) cw = 32;   // generic kernels: at least one 32-wide column chunk
+  grid = dim3(nsys, ldw >= 32 ? ldw / cw : 1);
+  if (wbmax >= 0 && wbmax <= 2 && cw == 32 && !getenv("NSP_NO_BAND")) {   // narrow band: deep-prefetch kernel
+    constexpr int NS = 3;
+    const size_t smem = (NS * 64 * LDT + NS * 64 * 36 + 3 * 64 * 36) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_band_fb<32, NS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    { nsp_count_launch(); k_band_fb<32, NS, 2><<<grid, 256, smem, st>>>(sys, buf, ldw, fwd, bwd); }
+    return;
+  }
   if (cw == 64) {
     const size_t smem = (2 * 64 * LDT + 2 * 64 * (64 + 4)) * sizeof(double);
     cudaFuncSetAttribute(k_tri_fb<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

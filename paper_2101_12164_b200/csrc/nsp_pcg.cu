@@ -250,7 +250,7 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
 // i1r holds r_1 (band rows, ld 32), bB holds r_B; i1buf is overwritten with A_11^{-1} r_1.
 static nsp_status interior_boundary_solve(nsp_ctx* c, PcgWs& w) {
   NSP_CUDA_TRY(c, cudaMemcpyAsync(w.i1buf, w.i1r, (size_t)c->i1_rows * 32 * 8, cudaMemcpyDeviceToDevice, c->stream));
-  nspk::tri_fb(c->d_i1sys, c->nsub, w.i1buf, 32, 32, true, true, c->stream);
+  nspk::tri_fb(c->d_i1sys, c->nsub, w.i1buf, 32, 32, true, true, c->stream, c->i1_wbmax);
   nspk::spmm(c->CB, w.bB, 32, w.i1buf, 32, c->wvu_rows, w.wvu, 32, 1, 1, true, c->stream);
   nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, w.wvu, 32, 32, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());
@@ -345,7 +345,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
   }
   if ((e = interior_boundary_solve(c, w)) != NSP_OK) return e;                       // y_B in wvu
   nspk::spmm(c->C1, w.i1r, 32, w.wvu, 32, c->i1_rows, w.i1buf, 32, 1, 1, true, st); // r_1 - A_1B y_B
-  nspk::tri_fb(c->d_i1sys, c->nsub, w.i1buf, 32, 32, true, true, st);               // y_1
+  nspk::tri_fb(c->d_i1sys, c->nsub, w.i1buf, 32, 32, true, true, st, c->i1_wbmax);               // y_1
   nspk::scatter_rows(w.i1buf, 32, c->d_i1_src, c->i1_rows, x, 1, 1, false, st);
   nspk::scatter_rows(w.wvu, 32, c->d_b_src, c->wvu_rows, x, 1, 1, false, st);
   nspk::scatter_rows(w.w, 1, c->d_g_src, n, x, 1, 1, false, st);

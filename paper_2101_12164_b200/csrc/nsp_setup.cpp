@@ -774,6 +774,8 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   }
   if (i1_rows + wvu_rows > INT32_MAX) return fail(c, NSP_ERR_ARG, "nsp_setup: interior rows exceed int32");
   c->i1_rows = i1_rows;
+  c->i1_wbmax = 0;
+  for (int j = 0; j < KL; ++j) c->i1_wbmax = std::max(c->i1_wbmax, sh[j].wb);
   std::vector<int32_t> i1_src(i1_rows, -1), b_src(wvu_rows, -1), g_src(c->nG);
   for (int64_t g = 0; g < c->nG; ++g) g_src[g] = (int32_t)c->gamma[g];
   HostCSR32 CB, C1;

@@ -183,7 +183,7 @@ static nsp_status ai_solve(nsp_ctx* c, BcgWs& w, const double* R, double* Z) {
   const double* R1 = R;
   const double* RB = R + c->i1_rows * (int64_t)sp;
   NSP_CUDA_TRY(c, cudaMemcpyAsync(Z1, R1, (size_t)c->i1_rows * sp * 8, cudaMemcpyDeviceToDevice, st));
-  nspk::tri_fb(c->d_i1sys, c->nsub, Z1, sp, cw, true, true, st);                              // A_11^{-1} r_1
+  nspk::tri_fb(c->d_i1sys, c->nsub, Z1, sp, cw, true, true, st, c->i1_wbmax);                              // A_11^{-1} r_1
   nspk::spmm(c->CB, RB, sp, Z1, sp, c->wvu_rows, w.wB, sp, sp, 1, false, st);                  // r_B - A_B1 t_1
   if (c->d_minv) {
     nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, w.wB, ZB, sp, cw, st);           // y_B
@@ -192,7 +192,7 @@ static nsp_status ai_solve(nsp_ctx* c, BcgWs& w, const double* R, double* Z) {
     NSP_CUDA_TRY(c, cudaMemcpyAsync(ZB, w.wB, (size_t)c->wvu_rows * sp * 8, cudaMemcpyDeviceToDevice, st));
   }
   nspk::spmm(c->C1, R1, sp, ZB, sp, c->i1_rows, Z1, sp, sp, 1, false, st);                     // r_1 - A_1B y_B
-  nspk::tri_fb(c->d_i1sys, c->nsub, Z1, sp, cw, true, true, st);                              // y_1
+  nspk::tri_fb(c->d_i1sys, c->nsub, Z1, sp, cw, true, true, st, c->i1_wbmax);                              // y_1
   NSP_CUDA_TRY(c, cudaGetLastError());
   return NSP_OK;
 }
@@ -413,10 +413,11 @@ nsp_status ag_solve(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, in
     c->err = "A_G^{-1} needs the A_G factor: set opts.factor_gamma = 1";
     return NSP_ERR_STATE;
   }
-  const int ldw = ld_pad(s, 32);
+  const bool vec = s == 1 && c->g_wb <= 2;   // one column, narrow band: matrix-vector chain kernel
+  const int ldw = vec ? 1 : ld_pad(s, 32);
   const int64_t rows = (int64_t)c->g_nt * 64;
   nspk::gather_rows(X, ldx, c->d_gperm, rows, buf, ldw, s, 1.0, c->stream);
-  nspk::tri_fb(c->d_gsys, 1, buf, ldw, 32, true, true, c->stream);
+  nspk::tri_fb(c->d_gsys, 1, buf, ldw, vec ? 1 : 32, true, true, c->stream, c->g_wb);
   nspk::scatter_rows(buf, ldw, c->d_gperm, rows, Y, ldy, s, false, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());
   return NSP_OK;
