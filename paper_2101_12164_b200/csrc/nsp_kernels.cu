@@ -1054,6 +1054,18 @@ void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd,
   }
   if (cw == 1) cw = 32;   // generic kernels: at least one 32-wide column chunk
   grid = dim3(nsys, ldw >= 32 ? ldw / cw : 1);
+  if (wbmax >= 0 && wbmax <= 2 && cw == 32 && nsys * (ldw / 32) < 2 * 148 && !getenv("NSP_NO_BAND")) {
+    // few independent sweeps (e.g. the single A_G system): 16-wide column chunks double the CTAs
+    constexpr int NS = 3;
+    const size_t smem = (NS * 64 * LDT + NS * 64 * 20 + 3 * 64 * 20) * sizeof(double);
+    static bool attr16 = false;
+    if (!attr16) {
+      cudaFuncSetAttribute(k_band_fb<16, NS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr16 = true;
+    }
+    { nsp_count_launch(); k_band_fb<16, NS, 2><<<dim3(nsys, ldw / 16), 256, smem, st>>>(sys, buf, ldw, fwd, bwd); }
+    return;
+  }
   if (wbmax >= 0 && wbmax <= 2 && cw == 32 && !getenv("NSP_NO_BAND")) {   // narrow band: deep-prefetch kernel
     constexpr int NS = 3;
     const size_t smem = (NS * 64 * LDT + NS * 64 * 36 + 3 * 64 * 36) * sizeof(double);
