@@ -218,6 +218,11 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_gsys);
   fr(c->d_gperm);
   fr(c->d_gperm_inv);
+  fr(c->d_gchunks);
+  fr(c->d_gchunk_first);
+  fr(c->d_gtile_chunk);
+  fr(c->d_gspkF);
+  fr(c->d_gspkB);
   fr(c->d_i1sys);
   fr(c->d_minv);
   fr(c->d_items);

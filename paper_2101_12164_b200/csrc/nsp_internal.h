@@ -101,6 +101,13 @@ struct nsp_ctx {
   TriSys* d_gsys = nullptr;   int g_nt = 0, g_wb = 0;
   int32_t* d_gperm = nullptr;     // band row -> Gamma row (size g_nt*64)
   int32_t* d_gperm_inv = nullptr; // Gamma row -> band row
+  // partitioned A_G solve (narrow band, setup_gamma_factor): P chunk systems + spikes
+  int g_P = 0;
+  TriSys* d_gchunks = nullptr;
+  int* d_gchunk_first = nullptr;   // P + 1
+  int* d_gtile_chunk = nullptr;    // g_nt
+  double* d_gspkF = nullptr;       // g_nt*64 x 64: S_k rows
+  double* d_gspkB = nullptr;       // g_nt*64 x 64: T_k rows
 
   // Nystrom-Schur M_2 = A_G^{-1} + Z Sigma Z^T (Alg. 2 steps 11-12)
   double* d_Z = nullptr;          // nG x nys_ld
@@ -175,6 +182,11 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
 // wbmax: largest band half-width (tiles) of the systems, -1 unknown; <= 2 with cw 32 selects k_band_fb
 void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,
             int wbmax = -1);
+// partitioned narrow-band solve of the A_G factor: coupling-tile recurrence / parallel spike update
+void spike_tail(const double* spk, const int* chunk_first, int P, double* buf, int ldw, int s, bool fwd,
+                cudaStream_t st);
+void spike_update(const double* spk, const int* chunk_first, const int* tile_chunk, int P, int nt, double* buf,
+                  int ldw, int s, bool fwd, cudaStream_t st);
 void gather_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,
                  double scale, cudaStream_t st);
 void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,

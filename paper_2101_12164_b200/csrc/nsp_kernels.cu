@@ -973,6 +973,85 @@ __global__ void __launch_bounds__(256) k_band_fb_vec(const TriSys* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Partitioned ("spike") narrow-band solve of the A_G factor.  The band rows are cut into P chunks of
+// consecutive 64-row tiles; chunk k couples to chunk k-1 only through one factor tile C_k (first tile
+// row of k x last tile column of k-1).  With the spikes S_k = L_kk^{-1} [C_k; 0] and
+// T_k = L_kk^{-T} [0; C_{k+1}^T] formed in setup:
+//   forward:  y_k = L_kk^{-1} b_k (all chunks in parallel);  x_k = y_k - S_k x_{k-1}[last tile]
+//   backward: z_k = L_kk^{-T} x_k (parallel);                 u_k = z_k - T_k u_{k+1}[first tile]
+// the coupling tiles ride a P-step recurrence (k_spike_tail), the rest is one parallel update
+// (k_spike_update).  Exact in exact arithmetic; a reordering of the same triangular solve.
+// tile_chunk[I] = chunk of tile row I; chunk_first[k] = first tile row of chunk k (chunk_first[P] = nt)
+// spk: rows of the band buffer x 64 (S_k rows for the forward spikes, T_k rows for the backward).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void spike_tile_product(const double* __restrict__ Sg, const double* __restrict__ Xg,
+                                                   int ldw, double* __restrict__ Og, int ncols, double* sm) {
+  // Og (64 x ncols, ld ldw) -= Sg (64 x 64, ld 64) * Xg (64 x ncols, ld ldw); ncols <= 32, both operands
+  // staged in shared memory (dynamic, 50 KB)
+  double* Ss = sm;              // 64 x 65
+  double* Xs = sm + 64 * 65;    // 64 x 33
+  for (int e = threadIdx.x; e < 4096; e += 256) Ss[(e >> 6) * 65 + (e & 63)] = __ldg(Sg + e);
+  for (int e = threadIdx.x; e < 64 * ncols; e += 256) {
+    const int r = e / ncols, cc = e - r * ncols;
+    Xs[r * 33 + cc] = Xg[(int64_t)r * ldw + cc];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 64 * ncols; e += 256) {
+    const int r = e / ncols, cc = e - r * ncols;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < 64; ++k) acc = fma(Ss[r * 65 + k], Xs[k * 33 + cc], acc);
+    Og[(int64_t)r * ldw + cc] -= acc;
+  }
+  __syncthreads();
+}
+
+// sequential over chunks (one CTA per 32-column chunk): the coupling tiles
+__global__ void __launch_bounds__(256) k_spike_tail(const double* __restrict__ spk, const int* __restrict__ chunk_first,
+                                                    int P, double* buf, int ldw, int s, int fwd) {
+  extern __shared__ double sm[];
+  const int c0 = blockIdx.x * 32;
+  const int ncols = min(32, s - c0);
+  if (fwd) {
+    for (int k = 1; k < P; ++k) {   // x_k[last] -= S_k[last rows] x_{k-1}[last]
+      const int last = chunk_first[k + 1] - 1, prev = chunk_first[k] - 1;
+      spike_tile_product(spk + (int64_t)last * 64 * 64, buf + (int64_t)prev * 64 * ldw + c0, ldw,
+                         buf + (int64_t)last * 64 * ldw + c0, ncols, sm);
+      __threadfence_block();
+    }
+  } else {
+    for (int k = P - 2; k >= 0; --k) {   // u_k[first] -= T_k[first rows] u_{k+1}[first]
+      const int first = chunk_first[k], nxt = chunk_first[k + 1];
+      spike_tile_product(spk + (int64_t)first * 64 * 64, buf + (int64_t)nxt * 64 * ldw + c0, ldw,
+                         buf + (int64_t)first * 64 * ldw + c0, ncols, sm);
+      __threadfence_block();
+    }
+  }
+}
+
+// all remaining tile rows in parallel: grid (tile rows, 32-column chunks)
+__global__ void __launch_bounds__(256) k_spike_update(const double* __restrict__ spk, const int* __restrict__ chunk_first,
+                                                      const int* __restrict__ tile_chunk, int P, double* buf, int ldw,
+                                                      int s, int fwd) {
+  extern __shared__ double sm[];
+  const int I = blockIdx.x;
+  const int c0 = blockIdx.y * 32;
+  const int ncols = min(32, s - c0);
+  const int k = tile_chunk[I];
+  if (fwd) {
+    if (k == 0 || I == chunk_first[k + 1] - 1) return;   // chunk 0 is final; the last tile came from the tail
+    const int prev = chunk_first[k] - 1;
+    spike_tile_product(spk + (int64_t)I * 64 * 64, buf + (int64_t)prev * 64 * ldw + c0, ldw,
+                       buf + (int64_t)I * 64 * ldw + c0, ncols, sm);
+  } else {
+    if (k == P - 1 || I == chunk_first[k]) return;
+    const int nxt = chunk_first[k + 1];
+    spike_tile_product(spk + (int64_t)I * 64 * 64, buf + (int64_t)nxt * 64 * ldw + c0, ldw,
+                       buf + (int64_t)I * 64 * ldw + c0, ncols, sm);
+  }
+}
+
 // row gather / scatter between an n x s block (ld lds) and a padded buffer (ld ldd):
 // gather: dst[r][c] = idx[r] >= 0 && c < s ? scale * src[idx[r]][c] : 0  for r < rows, c < ldd
 // scatter: dst[idx[r]][c] = src[r][c]   (c < s, idx[r] >= 0)
@@ -1086,6 +1165,27 @@ void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd,
     cudaFuncSetAttribute(k_tri_fb<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     { nsp_count_launch(); k_tri_fb<32><<<grid, 256, smem, st>>>(sys, buf, ldw, fwd, bwd); }
   }
+}
+
+void spike_tail(const double* spk, const int* chunk_first, int P, double* buf, int ldw, int s, bool fwd,
+                cudaStream_t st) {
+  if (P <= 1) return;
+  const size_t smem = (64 * 65 + 64 * 33) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_spike_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_spike_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  { nsp_count_launch(); k_spike_tail<<<(s + 31) / 32, 256, smem, st>>>(spk, chunk_first, P, buf, ldw, s, fwd); }
+}
+
+void spike_update(const double* spk, const int* chunk_first, const int* tile_chunk, int P, int nt, double* buf,
+                  int ldw, int s, bool fwd, cudaStream_t st) {
+  if (P <= 1) return;
+  const size_t smem = (64 * 65 + 64 * 33) * sizeof(double);   // attribute set with k_spike_tail (called first)
+  { nsp_count_launch(); k_spike_update<<<dim3(nt, (s + 31) / 32), 256, smem, st>>>(spk, chunk_first, tile_chunk, P,
+                                                                                    buf, ldw, s, fwd); }
 }
 
 void gather_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -286,6 +287,44 @@ static nsp_status setup_gamma_factor(nsp_ctx* c, const nsp_csr* A, const int32_t
   c->g_nt = nt;
   c->g_wb = wb;
   c->has_ag = true;
+  // partitioned solve (narrow band: the chunks couple through exactly one factor tile): P chunk
+  // systems and the spikes S_k = L_kk^{-1}[C_k; 0], T_k = L_kk^{-T}[0; C_{k+1}^T] (nsp_kernels.cu)
+  if (wb <= 1 && nt >= 16 && !getenv("NSP_NO_SPIKE")) {
+    int P = (int)std::sqrt((double)nt);
+    P = std::max(2, std::min(32, P));
+    std::vector<int> first(P + 1), tchunk(nt);
+    for (int k = 0; k <= P; ++k) first[k] = (int)((int64_t)k * nt / P);
+    for (int k = 0; k < P; ++k)
+      for (int I = first[k]; I < first[k + 1]; ++I) tchunk[I] = k;
+    std::vector<TriSys> ch(P);
+    for (int k = 0; k < P; ++k)
+      ch[k] = TriSys{c->d_gband + (int64_t)first[k] * (wb + 1) * NSP_TILE_ELEMS, first[k + 1] - first[k], wb,
+                     (int64_t)first[k] * 64};
+    if ((st = upload(c, &c->d_gchunks, ch)) != NSP_OK) return st;
+    if ((st = upload(c, &c->d_gchunk_first, first)) != NSP_OK) return st;
+    if ((st = upload(c, &c->d_gtile_chunk, tchunk)) != NSP_OK) return st;
+    const size_t sb = (size_t)nt * 64 * 64 * 8;
+    NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_gspkF, sb));
+    NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_gspkB, sb));
+    NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_gspkF, 0, sb, c->stream));
+    NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_gspkB, 0, sb, c->stream));
+    std::vector<double> tl(NSP_TILE_ELEMS), tt(NSP_TILE_ELEMS);
+    for (int k = 1; k < P; ++k) {   // C_k = factor tile (first[k], first[k] - 1)
+      const double* Ck = c->d_gband + ((int64_t)(first[k] - 1) * (wb + 1) + 1) * NSP_TILE_ELEMS;
+      NSP_CUDA_TRY(c, cudaMemcpyAsync(c->d_gspkF + (int64_t)first[k] * 64 * 64, Ck, NSP_TILE_ELEMS * 8,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+      NSP_CUDA_TRY(c, cudaMemcpy(tl.data(), Ck, NSP_TILE_ELEMS * 8, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < 64; ++i)
+        for (int j = 0; j < 64; ++j) tt[i * 64 + j] = tl[j * 64 + i];
+      NSP_CUDA_TRY(c, cudaMemcpy(c->d_gspkB + (int64_t)(first[k] - 1) * 64 * 64, tt.data(), NSP_TILE_ELEMS * 8,
+                                 cudaMemcpyHostToDevice));
+    }
+    nspk::tri_fb(c->d_gchunks + 1, P - 1, c->d_gspkF, 64, 32, true, false, c->stream, wb);   // S_k, k >= 1
+    nspk::tri_fb(c->d_gchunks, P - 1, c->d_gspkB, 64, 32, false, true, c->stream, wb);       // T_k, k <= P-2
+    NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    NSP_CUDA_TRY(c, cudaGetLastError());
+    c->g_P = P;
+  }
   return NSP_OK;
 }
 

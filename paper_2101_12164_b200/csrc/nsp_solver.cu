@@ -417,7 +417,17 @@ nsp_status ag_solve(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, in
   const int ldw = vec ? 1 : ld_pad(s, 32);
   const int64_t rows = (int64_t)c->g_nt * 64;
   nspk::gather_rows(X, ldx, c->d_gperm, rows, buf, ldw, s, 1.0, c->stream);
-  nspk::tri_fb(c->d_gsys, 1, buf, ldw, vec ? 1 : 32, true, true, c->stream, c->g_wb);
+  if (c->g_P > 1) {   // partitioned: P chunk sweeps in parallel + spike corrections
+    const int cw = vec ? 1 : 32, P = c->g_P;
+    nspk::tri_fb(c->d_gchunks, P, buf, ldw, cw, true, false, c->stream, c->g_wb);
+    nspk::spike_tail(c->d_gspkF, c->d_gchunk_first, P, buf, ldw, s, true, c->stream);
+    nspk::spike_update(c->d_gspkF, c->d_gchunk_first, c->d_gtile_chunk, P, c->g_nt, buf, ldw, s, true, c->stream);
+    nspk::tri_fb(c->d_gchunks, P, buf, ldw, cw, false, true, c->stream, c->g_wb);
+    nspk::spike_tail(c->d_gspkB, c->d_gchunk_first, P, buf, ldw, s, false, c->stream);
+    nspk::spike_update(c->d_gspkB, c->d_gchunk_first, c->d_gtile_chunk, P, c->g_nt, buf, ldw, s, false, c->stream);
+  } else {
+    nspk::tri_fb(c->d_gsys, 1, buf, ldw, vec ? 1 : 32, true, true, c->stream, c->g_wb);
+  }
   nspk::scatter_rows(buf, ldw, c->d_gperm, rows, Y, ldy, s, false, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());
   return NSP_OK;
