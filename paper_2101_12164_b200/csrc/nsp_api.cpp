@@ -57,7 +57,10 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   double* U = wvu;
   if (c->d_minv) {
     U = wvu + c->wvu_rows * (int64_t)ldw;
-    nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream);
+    if (s == 1)   // one right-hand side (outer PCG): memory-bound matrix-vector form
+      nspk::symv(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, c->stream);
+    else
+      nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream);
   } else {
     nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, wvu, ldw, cw, c->stream);
   }

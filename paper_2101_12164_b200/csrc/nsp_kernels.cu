@@ -575,6 +575,64 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
 }
 
 // ---------------------------------------------------------------------------------------------
+// a2 + a3 for ONE right-hand side (the outer PCG, s = 1): u_j = S_j^{-1} w_j as a symmetric
+// matrix-VECTOR product streaming the stored lower tiles of S_j^{-1} once from HBM / L2 with
+// coalesced loads straight into registers (no DMMA: a tile product would do 32x the work for one
+// column).  One CTA per (block, output tile row I).  J <= I: row dot products (warp w owns rows
+// 8w..8w+7, lanes along the row); J > I: the stored tile (J, I) transposed, column dot products
+// (thread t owns column t & 63 over a quarter of the rows).  Fixed combination order.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_symv(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                              const double* __restrict__ minv, const double* __restrict__ W, int ldw,
+                                              double* __restrict__ U) {
+  extern __shared__ double wv[];            // ntb x 64 right-hand side of the block
+  __shared__ double cpart[4][64];
+  const int2 it = items[blockIdx.x];
+  const FacSub sb = subs[it.x];
+  const int I = it.y, ntb = sb.ntb;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, col = tid & 63, grp = tid >> 6;
+  const double* Mb = minv + sb.dense_off * NSP_TILE_ELEMS;
+  const double* Wb = W + sb.wvu_row * (int64_t)ldw;
+  for (int e = tid; e < ntb * 64; e += 256) wv[e] = Wb[(int64_t)e * ldw];
+  __syncthreads();
+  double r8[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r8[i] = 0.0;
+  double cacc = 0.0;
+  for (int J = 0; J < ntb; ++J) {
+    const double* v = wv + J * 64;
+    if (J <= I) {
+      const double* T = Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double* row = T + (warp * 8 + i) * 64;
+        r8[i] = fma(__ldg(row + lane), v[lane], r8[i]);
+        r8[i] = fma(__ldg(row + lane + 32), v[lane + 32], r8[i]);
+      }
+    } else {
+      const double* T = Mb + ((int64_t)J * (J + 1) / 2 + I) * NSP_TILE_ELEMS;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) cacc = fma(__ldg(T + (grp * 16 + i) * 64 + col), v[grp * 16 + i], cacc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r8[i] += __shfl_xor_sync(0xffffffffu, r8[i], o);
+  cpart[grp][col] = cacc;
+  __syncthreads();
+  if (lane < 8) {
+    const int r = warp * 8 + lane;
+    double mine = r8[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i)
+      if (lane == i) mine = r8[i];
+    const double u = mine + ((cpart[0][r] + cpart[1][r]) + (cpart[2][r] + cpart[3][r]));
+    U[(sb.wvu_row + (int64_t)I * 64 + r) * ldw] = u;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Generic batched forward + backward triangular solves on tiled factors (one system per blockIdx.x,
 // column chunks on blockIdx.y): dense lower tiles (wb < 0: tile(I,J) = T + I(I+1)/2 + J) or band
 // tiles (tile(I,J) = T + J(wb+1) + (I-J), 0 <= I-J <= wb).  Used for A_G^{-1} (band) and for the
@@ -1237,6 +1295,20 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
     }
     { nsp_count_launch(); k_symm<32, NS><<<grid, 256, smem, st>>>(subs, items, minv, W, U, ldw); }
   }
+}
+
+void symv(const FacSub* subs, const int2* items, int nitems, int max_ntb, const double* minv, const double* W, int ldw,
+          double* U, cudaStream_t st) {
+  if (nitems <= 0) return;
+  const size_t smem = (size_t)max_ntb * 64 * sizeof(double);
+  if (smem > 48 * 1024) {
+    static size_t attr = 0;
+    if (attr < smem) {
+      cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
+  }
+  { nsp_count_launch(); k_symv<<<nitems, 256, smem, st>>>(subs, items, minv, W, ldw, U); }
 }
 
 void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw, cudaStream_t st) {

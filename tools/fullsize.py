@@ -54,6 +54,32 @@ def run_pcg(name, maxit=5000):
     return out
 
 
+def run_pcg_plain(name, maxit=20000):
+    """Outer PCG on the full system without a preconditioner (precond 0) at full size - for configs
+    whose A_G band factor does not fit (cfg5): interior band + S_j^{-1} factors only."""
+    B.build()
+    pr = P.make(name)
+    t0 = time.perf_counter()
+    ctx = nsp.Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    b = pr.rhs()
+    x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
+    bd = torch.from_numpy(b).cuda()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = ctx.pcg(bd, x, pr.tol_pcg or 1e-8, maxit, precond=0)
+    torch.cuda.synchronize()
+    t = time.perf_counter() - t0
+    xh = x.cpu().numpy()
+    A = pr.A.to_scipy()
+    out = dict(config=name, setup_s=round(t_setup, 2), pcg_M0=dict(iters=rep["iters"], converged=rep["converged"],
+               s=round(t, 3), true_relres=float(np.linalg.norm(b - A @ xh) / np.linalg.norm(b)),
+               x_err=float(np.linalg.norm(xh - pr.xstar()) / np.linalg.norm(pr.xstar()))))
+    ctx.close()
+    return out
+
+
 def run(name, nrows=6, maxit=1000, apply_kernel=0):
     B.build()
     t0 = time.perf_counter()
@@ -117,6 +143,10 @@ def run(name, nrows=6, maxit=1000, apply_kernel=0):
 
 if __name__ == "__main__":
     nrows = int(sys.argv[sys.argv.index("--rows") + 1]) if "--rows" in sys.argv else 6
+    if "--pcg0" in sys.argv:
+        for name in [a for a in sys.argv[1:] if a.startswith("cfg")]:
+            print(json.dumps(run_pcg_plain(name)), flush=True)
+        sys.exit(0)
     if "--pcg" in sys.argv:
         for name in [a for a in sys.argv[1:] if a.startswith("cfg")]:
             print(json.dumps(run_pcg(name)), flush=True)
