@@ -107,3 +107,16 @@ def apply_M2(S: SchurOracle, Z: np.ndarray, sigma: np.ndarray, r: np.ndarray) ->
     if Z.shape[1]:
         out = out + Z @ (sigma * (Z.T @ r)) if r.ndim == 1 else out + Z @ (sigma[:, None] * (Z.T @ r))
     return out
+
+
+def apply_ADEF2(S: SchurOracle, Z: np.ndarray, r: np.ndarray) -> np.ndarray:
+    """M_A-DEF2 r = A_G^{-1} r + Z E^{-1} Z^T (r - S_G A_G^{-1} r), E = Z^T S_G Z: the adapted-deflation
+    form (eq:adapted_deflation_prec PAPER.md:295-306, eq:deflation_comp_from_low_rank)
+    built from M_2's basis Z = A_G^{-1} W ("in a similar way ... M_A-DEF2"; DESIGN.md
+    reading R5: in the R_G-scaled space Y = R_G^{-T} W, so R_G^{-1} Y = Z and every R_G cancels)."""
+    t = S.solve_AG(r)
+    if Z.shape[1] == 0:
+        return t
+    E = Z.T @ S.apply(Z)
+    E = 0.5 * (E + E.T)
+    return t + Z @ np.linalg.solve(E, Z.T @ (r - S.apply(t)))

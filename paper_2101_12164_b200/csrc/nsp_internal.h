@@ -113,6 +113,8 @@ struct nsp_ctx {
   double* d_Z = nullptr;          // nG x nys_ld
   double* d_sigma = nullptr;      // nys_ld
   int nys_rank = -1, nys_ld = 0;
+  double* d_ELp = nullptr;        // Cholesky (k_chol16 packed) of E = Z^T S_G Z for M_A-DEF2
+  bool adef_ok = false;
   std::vector<double> h_sigma;
 
   // full-system solve (nsp_pcg; eq:A_LDLT PAPER.md:381-385): every block's interior rows I1 in

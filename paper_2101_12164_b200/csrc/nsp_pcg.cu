@@ -147,7 +147,7 @@ __global__ void k_gemvt_reduce(const double* __restrict__ part, int nchunks, con
   if (k >= rk) return;
   double s = 0.0;
   for (int b = 0; b < nchunks; ++b) s += part[b * 128 + k];
-  g[k] = sigma[k] * s;
+  g[k] = sigma ? sigma[k] * s : s;
 }
 
 // y[row] += sum_k Z[row][k] g[k]   (warp per row, butterfly sum)
@@ -171,7 +171,7 @@ unsigned grid1(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t 
 namespace nspi {
 
 struct PcgWs {
-  double *f, *w, *r, *z, *p, *q, *tmp;     // n_G vectors
+  double *f, *w, *r, *z, *p, *q, *tmp, *t2, *eg;   // n_G vectors; eg: k x k (A-DEF2 solve, column 0)
   double *bB, *wvu, *tmpB;                 // W/V/U rows x 32
   double *i1r, *i1buf;                     // band rows x 32
   double *agbuf, *apply_wvu, *part, *gpart, *g, *sc;
@@ -195,6 +195,8 @@ static size_t pcg_layout(const nsp_ctx* c, char* base, PcgWs* out) {
   w.p = take(nG);
   w.q = take(nG);
   w.tmp = take(nG);
+  w.t2 = take(nG);
+  w.eg = take(2 * 128 * 128);
   const size_t wr = (size_t)std::max<int64_t>(c->wvu_rows, 1) * 32;
   w.bB = take(wr);
   w.wvu = take(wr);
@@ -233,6 +235,26 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
   }
   nsp_status e = ag_solve(c, r, 1, z, 1, 1, w.agbuf);
   if (e != NSP_OK) return e;
+  if (which == 3 && c->nys_rank > 0) {
+    // M_A-DEF2 r = A_G^{-1} r + Z E^{-1} Z^T (r - S_G A_G^{-1} r),  E = Z^T S_G Z (reading R5)
+    const int kp = c->nys_ld, rk = c->nys_rank;
+    if ((e = apply_into(c, z, 1, w.t2, 1, 1, 1, w.apply_wvu)) != NSP_OK) return e;     // S_G A_G^{-1} r
+    nsp_count_launch();
+    k_axpy_strided<<<grid1(n, 256), 256, 0, c->stream>>>(w.t2, 1, r, 1, w.t2, 1, -1.0, n);   // d = r - S t
+    const unsigned nch = grid1(n, GT_ROWS);
+    nsp_count_launch();
+    k_gemvt_partial<<<nch, 128, 0, c->stream>>>(c->d_Z, kp, w.t2, n, rk, w.gpart);
+    double* G = w.eg;                 // kp x kp, column 0 = Z^T d
+    double* H = w.eg + 128 * 128;     // kp x kp, column 0 = E^{-1} Z^T d
+    NSP_CUDA_TRY(c, cudaMemsetAsync(G, 0, (size_t)kp * kp * 8, c->stream));
+    nsp_count_launch();
+    k_gemvt_reduce<<<1, 128, 0, c->stream>>>(w.gpart, (int)nch, nullptr, rk, w.g);
+    NSP_CUDA_TRY(c, cudaMemcpy2DAsync(G, kp * 8, w.g, 8, 8, rk, cudaMemcpyDeviceToDevice, c->stream));
+    nspb::chol_solve(c->d_ELp, kp, G, kp, H, kp, 1.0, true, true, nullptr, c->stream);
+    NSP_CUDA_TRY(c, cudaMemcpy2DAsync(w.g, 8, H, kp * 8, 8, rk, cudaMemcpyDeviceToDevice, c->stream));
+    nsp_count_launch();
+    k_gemv_add<<<grid1(n * 32, 256), 256, 0, c->stream>>>(c->d_Z, kp, w.g, rk, n, z);
+  }
   if (which == 2 && c->nys_rank > 0) {
     const unsigned nch = grid1(n, GT_ROWS);
     nsp_count_launch();
@@ -366,8 +388,8 @@ using namespace nspi;
 
 extern "C" nsp_status nsp_pcg(nsp_ctx* c, const double* b, double* x, double tol, int maxit, int precond, void* ws,
                               nsp_report* rep) {
-  if (!c || !b || !x || maxit < 0 || precond < 0 || precond > 2) {
-    if (c) c->err = "nsp_pcg: bad arguments (precond in {0, 1, 2})";
+  if (!c || !b || !x || maxit < 0 || precond < 0 || precond > 3) {
+    if (c) c->err = "nsp_pcg: bad arguments (precond in {0, 1, 2, 3})";
     return NSP_ERR_ARG;
   }
   if (c->nranks != 1) {
@@ -378,7 +400,11 @@ extern "C" nsp_status nsp_pcg(nsp_ctx* c, const double* b, double* x, double tol
     c->err = "nsp_pcg: the A_G^{-1} / M_2 preconditioner needs the A_G factor (opts.factor_gamma = 1)";
     return NSP_ERR_STATE;
   }
-  if (precond == 2 && c->nys_rank < 0) {
+  if (precond == 3 && c->nys_rank > 0 && !c->adef_ok) {
+    c->err = "nsp_pcg: E = Z^T S_G Z not positive definite (M_A-DEF2 unavailable)";
+    return NSP_ERR_STATE;
+  }
+  if (precond >= 2 && c->nys_rank < 0) {
     c->err = "nsp_pcg: M_2 requested before nsp_nystrom";
     return NSP_ERR_STATE;
   }

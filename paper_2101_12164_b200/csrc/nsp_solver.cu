@@ -681,6 +681,21 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
     NSP_CUDA_TRY(c, cudaStreamSynchronize(st));
     c->nys_rank = rk;
     c->nys_ld = kp;
+    // M_A-DEF2 (reading R5): E = Z^T S_G Z (one S_G block apply on Z) and its Cholesky factor
+    {
+      double* SZ = Qa;    // n x kp scratch (reuse)
+      if ((e = apply_into(c, c->d_Z, kp, SZ, kp, rk, 1, w.wvu)) != NSP_OK) return e;
+      nspb::gram(c->d_Z, kp, kp, SZ, kp, kp, n, G, kp, w.gram, st);
+      nspb::small_sym(G, rk, kp, 0.0, st);
+      if (c->d_ELp) cudaFree(c->d_ELp);
+      c->d_ELp = nullptr;
+      NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_ELp, (size_t)kp * kp * 8));
+      nspb::chol_fac(G, kp, 0, rk, 0.0, c->d_ELp, w.st, st);
+      if ((e = read_status(c, w.st, hs)) != NSP_OK) return e;
+      c->adef_ok = !hs->indefinite;
+      hs->indefinite = 0;
+      NSP_CUDA_TRY(c, cudaMemcpyAsync(w.st, hs, sizeof(BcgStatus), cudaMemcpyHostToDevice, st));
+    }
   } else {
     ret = NSP_ERR_RANK_COLLAPSE;
     c->err = "nsp_nystrom: no eigenvalue of C >= eps (M_2 degenerates to A_G^{-1})";

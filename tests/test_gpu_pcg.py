@@ -6,7 +6,7 @@ import pytest
 import torch
 
 import oracle as O
-from oracle.nystrom import apply_M2
+from oracle.nystrom import apply_ADEF2, apply_M2
 from tests.gpu_util import context, dev, problem
 
 pytestmark = pytest.mark.gpu
@@ -25,18 +25,20 @@ def _oracle_M(S, precond, nys=None):
         return None
     if precond == 1:
         return S.solve_AG
+    if precond == 3:
+        return lambda r: apply_ADEF2(S, nys.Z, r)
     return lambda r: apply_M2(S, nys.Z, nys.sigma, r)
 
 
 @pytest.mark.parametrize("name", NAMES)
-@pytest.mark.parametrize("precond", [0, 1, 2])
+@pytest.mark.parametrize("precond", [0, 1, 2, 3])
 def test_pcg_full_solve_parity(name, precond):
     pr, d, S = problem(name)
     tol = pr.tol_pcg or 1e-8
     b = pr.rhs()
     ctx = context(pr, factor_gamma=True)
     nys = None
-    if precond == 2:
+    if precond >= 2:
         Om = pr.omega()
         nys = O.nystrom_schur(S, Om, pr.rank, pr.tol_bcg, 500)
         rep_n = ctx.nystrom(pr.rank, pr.oversample, dev(Om), 0.0, nys.bcg["iters"])

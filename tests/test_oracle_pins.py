@@ -440,3 +440,22 @@ def test_si_block_pcg_iterations_cfg1():
     d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
     r = O.nystrom_schur_si(O.SchurOracle(d), pr.omega(), pr.rank, tol_inner=0.1)
     assert r.bcg["status"] == 0 and 1 <= r.bcg["iters"] <= 20 and r.rank == pr.rank
+
+
+def test_adef2_exact_deflation_space():
+    """M_A-DEF2 (reading R5): if Z spans an exact invariant subspace of A_G^{-1} S_G (the GEVP eq:GEVP
+    eigenvectors), the A-DEF preconditioned operator maps those directions to themselves: M S_G z = z
+    (eq:adapted_deflation_prec: P_A-DEF A Z = Z), and on the complement it equals A_G^{-1} S_G."""
+    import scipy.linalg as sl
+    from oracle.nystrom import apply_ADEF2
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    Sd = S.dense()
+    AG = d.A_G.toarray()
+    lam, V = sl.eigh(Sd, AG)                  # S v = lam A_G v (eq:GEVP)
+    Z = V[:, :6]                              # smallest generalized eigenpairs
+    MS = np.column_stack([apply_ADEF2(S, Z, Sd[:, j]) for j in range(Sd.shape[0])])
+    assert np.allclose(MS @ Z, Z, atol=1e-10)
+    v = V[:, 20]                              # a direction outside span(Z): A_G^{-1} S v = lam v
+    assert np.allclose(MS @ v, lam[20] * v, atol=1e-10 * np.abs(v).max())

@@ -39,7 +39,7 @@ def run_pcg(name, maxit=5000):
                nystrom_s=round(t_nys, 3), nystrom_inner_iters=rn["iters"], nystrom_rank=rn["rank"],
                sigma_top=[float(x) for x in ctx.nystrom_sigma()[:3]])
     A = pr.A.to_scipy()
-    for prec in (1, 2):
+    for prec in (1, 2, 3):   # S~_1, M_2, M_A-DEF2
         x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
         bd = torch.from_numpy(b).cuda()
         torch.cuda.synchronize()
