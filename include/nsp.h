@@ -84,7 +84,11 @@ typedef struct {
   int nys_form;          /* inner system of nsp_nystrom: 0 = the border system S_G X = K_G G, Y = A_G X
                             (reading C1, default); 1 = the paper-literal S_I X = A_IG G, Y = A_GI X
                             (eq:SI) by block PCG preconditioned by A_I;
-                            read by nsp_setup (builds A_I on the interior layout), single rank */
+                            read by nsp_setup (builds A_I on the interior layout), single rank;
+                            2 = M_3: Nystrom of S_I^{-1} itself (eq:internal_term_lr_approximation_2,
+                            eq:left_prec_mat2): Y = S_I^{-1} Omega_I by block PCG, Z = A_G^{-1} A_GI V,
+                            Omega is then n x (rank + oversample) in ORIGINAL order (interior rows used),
+                            no power steps */
 } nsp_opts;
 
 /* Solver / setup report; caller-owned.  hist / widths are optional caller

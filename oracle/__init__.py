@@ -18,4 +18,4 @@ from .schur import SchurOracle  # noqa: F401
 from .bcg import bf_bcg, orth  # noqa: F401
 from .nystrom import nystrom_schur, NystromResult  # noqa: F401
 from .pcg import pcg, solve_full_system  # noqa: F401
-from .si import SIOperator, nystrom_schur_si  # noqa: F401
+from .si import SIOperator, interior_rows, nystrom_schur_si, nystrom_si_inverse  # noqa: F401

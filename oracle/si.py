@@ -62,3 +62,29 @@ def nystrom_schur_si(S: SchurOracle, Omega: np.ndarray, k: int, tol_inner: float
     status = 0 if rC > 0 else NSP_ERR_RANK_COLLAPSE
     Z = S.solve_AG(U) if U.shape[1] else U
     return NystromResult(Z, sigma, U, U.shape[1], info, status)
+
+
+def interior_rows(S: SchurOracle) -> np.ndarray:
+    """Original node ids of the interior rows in the DBBD order (blocks 0..K-1, ascending ids)."""
+    return np.concatenate([b for b in S.d.blocks]) if S.d.K else np.zeros(0, dtype=np.int64)
+
+
+def nystrom_si_inverse(S: SchurOracle, Omega_full: np.ndarray, k: int, tol_inner: float = 0.1,
+                       maxit_inner: int = 1000, precond: bool = True, tau: float = 1e-14,
+                       eps_rel: float = 1e-12, exact_inner: bool = False) -> NystromResult:
+    """M_3 (eq:internal_term_lr_approximation_2, eq:left_prec_mat2): Nystrom of
+    S_I^{-1} ~ V Sigma V^T with the sketch Omega_I (the interior rows of Omega_full, n x s in the
+    original order): Y = S_I^{-1} Omega_I (block PCG, A_I preconditioner), Alg. 1 steps on (Omega_I, Y),
+    then Z^ = A_G^{-1} A_GI V and M_3 = A_G^{-1} + Z^ Sigma Z^^T."""
+    op = SIOperator(S)
+    Om = np.ascontiguousarray(Omega_full[interior_rows(S)])
+    if exact_inner:
+        SI = op.A_I.toarray() - op.A_IG.toarray() @ np.linalg.solve(S.d.A_G.toarray(), op.A_IG.T.toarray())
+        Y = np.linalg.solve(SI, Om)
+        info = {"iters": 0, "status": 0, "widths": []}
+    else:
+        Y, info = bf_bcg(op.apply, Om, tol_inner, maxit_inner, op.solve_AI if precond else None, tau)
+    V, sigma, rC = nystrom_from_Y(Om, Y, k, eps_rel)
+    status = 0 if rC > 0 else NSP_ERR_RANK_COLLAPSE
+    Z = S.solve_AG(op.A_IG.T @ V) if V.shape[1] else V
+    return NystromResult(Z, sigma, V, V.shape[1], info, status)

@@ -234,6 +234,7 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_g_src);
   fr(c->d_Z);
   fr(c->d_ELp);
+  fr(c->d_int_src);
   fr(c->d_sigma);
   comm_free(c);
   if (c->bcg_graph) cudaGraphExecDestroy(c->bcg_graph);

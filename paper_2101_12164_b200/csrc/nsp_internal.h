@@ -129,7 +129,8 @@ struct nsp_ctx {
   int32_t* d_b_src = nullptr;
   int32_t* d_g_src = nullptr;
   DevCSR CB, C1;
-  DevCSR AII;                 // opts.nys_form == 1: A_I on the interior layout (+ the -I coupling of B rows)
+  DevCSR AII;                 // opts.nys_form 1/2: A_I on the interior layout (+ the -I coupling of B rows)
+  int32_t* d_int_src = nullptr;   // interior layout row -> original id (-1 padding)
 
   // statistics
   int64_t n_I = 0, n_bl = 0, nnz_AG = 0, nnz_AGI = 0, max_b = 0, ag_bw = 0;

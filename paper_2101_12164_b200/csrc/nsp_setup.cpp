@@ -871,7 +871,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   // S_I inner system (opts.nys_form == 1): every B row carries one extra entry (n_int + row, -1)
   // so that "A_I P - [0; h_B]" is a single SpMM pass
   HostCSR32 AII;
-  if (c->opts.nys_form == 1 && c->nranks == 1) {
+  if ((c->opts.nys_form == 1 || c->opts.nys_form == 2) && c->nranks == 1) {
     const int64_t n_int = i1_rows + wvu_rows;
     if (n_int + wvu_rows > INT32_MAX) return fail(c, NSP_ERR_ARG, "nsp_setup: interior rows exceed int32");
     auto iidx = [&](int64_t u, int jl) -> int32_t {
@@ -912,7 +912,12 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   if ((st = upload_csr(c, c->AGG2, AGG2)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->AGSH, AGSH)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->CB, CB)) != NSP_OK) return st;
-  if (!AII.rowptr.empty() && (st = upload_csr(c, c->AII, AII)) != NSP_OK) return st;
+  if (!AII.rowptr.empty()) {
+    if ((st = upload_csr(c, c->AII, AII)) != NSP_OK) return st;
+    std::vector<int32_t> isrc(i1_src);   // interior layout row -> original id (-1 padding)
+    isrc.insert(isrc.end(), b_src.begin(), b_src.end());
+    if ((st = upload(c, &c->d_int_src, isrc)) != NSP_OK) return st;
+  }
   if ((st = upload_csr(c, c->C1, C1)) != NSP_OK) return st;
   if ((st = upload(c, &c->d_i1_src, i1_src)) != NSP_OK) return st;
   if ((st = upload(c, &c->d_b_src, b_src)) != NSP_OK) return st;

@@ -492,20 +492,23 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   const int64_t n = c->nG;
   cudaStream_t st = c->stream;
   const size_t blk = (size_t)std::max<int64_t>(n, 1) * sp, sm = (size_t)sp * sp;
-  const int form = c->opts.nys_form == 1 ? 1 : 0;
-  if (form == 1 && (c->nranks != 1 || c->AII.rows == 0)) {
-    c->err = "nsp_nystrom: the S_I form needs opts.nys_form = 1 at nsp_setup (single rank)";
+  // form 0: border system (reading C1); 1: paper-literal S_I system (eq:SI); 2: M_3 - Nystrom of S_I^{-1}
+  // itself (eq:internal_term_lr_approximation_2 / eq:left_prec_mat2), Omega then n x s in original order
+  const int form = (c->opts.nys_form == 1 || c->opts.nys_form == 2) ? c->opts.nys_form : 0;
+  if (form >= 1 && (c->nranks != 1 || c->AII.rows == 0)) {
+    c->err = "nsp_nystrom: the S_I forms need opts.nys_form set at nsp_setup (single rank)";
     return NSP_ERR_STATE;
   }
   const int64_t n_int = c->i1_rows + c->wvu_rows;
   const size_t iblk = form ? (size_t)std::max<int64_t>(n_int, 1) * sp : 0;
-  const size_t bcg_bytes = bcg_layout(c, s, nullptr, nullptr, form);
-  const size_t extra = (6 * blk + 2 * iblk + 16 * sm + 8 * sp + (size_t)(sp + 1) * (sp + 1)) * 8 + 64 * 256;
+  const size_t bcg_bytes = bcg_layout(c, s, nullptr, nullptr, form ? 1 : 0);
+  const size_t extra =
+      (6 * blk + (form == 2 ? 4 : 2) * iblk + 16 * sm + 8 * sp + (size_t)(sp + 1) * (sp + 1)) * 8 + 64 * 256;
   char* base;
   nsp_status e = get_ws(c, ws, bcg_bytes + extra, &base);
   if (e != NSP_OK) return e;
   BcgWs w;
-  bcg_layout(c, s, base, &w, form);
+  bcg_layout(c, s, base, &w, form ? 1 : 0);
   Carver cv(base + bcg_bytes);
   double* Om = cv.take(blk);
   double* Bn = cv.take(blk);
@@ -528,18 +531,26 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   double* Vw = cv.take((size_t)(sp + 1) * (sp + 1));
   double* lamC = cv.take(sp);
   double* lamT = cv.take(sp);
-  double* Fi = form ? cv.take(iblk) : nullptr;   // S_I form: right-hand side / solution (interior layout)
+  double* Fi = form ? cv.take(iblk) : nullptr;   // S_I forms: right-hand side / solution (interior layout)
   double* Xi = form ? cv.take(iblk) : nullptr;
+  double* Qa2 = form == 2 ? cv.take(iblk) : nullptr;   // M_3: Cholesky-QR of the n_int-row Y
+  double* Qb2 = form == 2 ? cv.take(iblk) : nullptr;
   BcgStatus* hs = (BcgStatus*)c->h_status;
   // Cholesky-QR2 of Yin -> Q (returned, one of Qa / Qb), R in Racc (shifted Cholesky-QR3 when the
   // first Gram is numerically singular)
-  auto cholqr = [&](const double* Yin, const double** Qres) -> nsp_status {
+  auto cholqr = [&](const double* Yin, const double** Qres, int64_t nr = -1, double* QA = nullptr,
+                    double* QB = nullptr) -> nsp_status {
+    if (nr < 0) nr = n;
+    if (!QA) {
+      QA = Qa;
+      QB = Qb;
+    }
     NSP_CUDA_TRY(c, cudaMemsetAsync(Racc, 0, sm * 8, st));
     const double* Qin = Yin;
-    double* Qout = Qa;
+    double* Qout = QA;
     int passes = 2;
     for (int pass = 0; pass < passes; ++pass) {
-      nspb::gram(Qin, sp, sp, Qin, sp, sp, n, G, sp, w.gram, st);
+      nspb::gram(Qin, sp, sp, Qin, sp, sp, nr, G, sp, w.gram, st);
       nspb::small_chol(G, sp, 2, s, 0.0, Rk, w.st, st);
       if (pass == 0) {
         nsp_status e2 = read_status(c, w.st, hs);
@@ -549,7 +560,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
           NSP_CUDA_TRY(c, cudaMemcpy(gd.data(), G, sm * 8, cudaMemcpyDeviceToHost));
           double tr = 0.0;
           for (int i = 0; i < s; ++i) tr += gd[(size_t)i * sp + i];
-          const double shift = 11.0 * ((double)n * s + (double)s * (s + 1)) * 1.1102230246251565e-16 * tr;
+          const double shift = 11.0 * ((double)nr * s + (double)s * (s + 1)) * 1.1102230246251565e-16 * tr;
           nspb::small_sym(G, s, sp, shift, st);
           nspb::small_chol(G, sp, 2, s, 0.0, Rk, w.st, st);
           passes = 3;
@@ -557,7 +568,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
       }
       nspb::small_chol(G, sp, 1, s, 0.0, Tk, w.st, st);      // T = R^{-1}
       PanelArgs pa{Qout, sp, nullptr, 0, Qin, sp, Tk, sp, 1.0, nullptr};
-      nspb::panel2(pa, nullptr, sp, sp, n, st);
+      nspb::panel2(pa, nullptr, sp, sp, nr, st);
       if (pass == 0) {
         NSP_CUDA_TRY(c, cudaMemcpyAsync(Racc, Rk, sm * 8, cudaMemcpyDeviceToDevice, st));
       } else {
@@ -565,7 +576,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
         NSP_CUDA_TRY(c, cudaMemcpyAsync(Racc, Rtmp, sm * 8, cudaMemcpyDeviceToDevice, st));
       }
       Qin = Qout;
-      Qout = (Qout == Qa) ? Qb : Qa;
+      Qout = (Qout == QA) ? QB : QA;
     }
     nsp_status e2 = read_status(c, w.st, hs);
     if (e2 != NSP_OK) return e2;
@@ -582,7 +593,21 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   nsp_report brep{};
   int total_iters = 0;
   nsp_status sb = NSP_OK;
-  for (int pw = 0; pw <= q; ++pw) {
+  if (form == 2) {   // M_3: Y = S_I^{-1} Omega_I (block PCG on S_I, A_I preconditioner), no power steps
+    nspk::gather_rows(Omega, s, c->d_int_src, n_int, Fi, sp, s, 1.0, st);
+    brep = nsp_report{};
+    if (rep) {
+      brep.hist = rep->hist;
+      brep.hist_cap = rep->hist_cap;
+      brep.widths = rep->widths;
+      brep.widths_cap = rep->widths_cap;
+    }
+    nsp_status sbi = block_cg_impl(c, Fi, sp, Xi, sp, s, tol_inner, maxit_inner, w, &brep);
+    if (sbi < 0) return sbi;
+    if (sbi == NSP_NOT_CONVERGED) sb = NSP_NOT_CONVERGED;
+    total_iters += brep.iters;
+  }
+  for (int pw = 0; form != 2 && pw <= q; ++pw) {
     if (form == 1) {   // paper-literal: F = A_IG G, S_I X = F (block PCG, A_I), Y = A_GI X
       NSP_CUDA_TRY(c, cudaMemsetAsync(Fi, 0, (size_t)c->i1_rows * sp * 8, st));
       nspk::spmm(c->A2G, Om, sp, nullptr, 0, 0, Fi + c->i1_rows * (int64_t)sp, sp, s, 0, true, st);
@@ -628,11 +653,15 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
     }
   }
   brep.iters = total_iters;
+  // the Nystrom operands: G (sketch) and Y = B G with nY rows (M_3: the interior layout)
+  const int64_t nY = form == 2 ? n_int : n;
+  const double* Gs = form == 2 ? Fi : Om;
+  const double* Ys = form == 2 ? Xi : Y;
   // step 5: Y = Q R
   const double* Q = nullptr;
-  if ((e = cholqr(Y, &Q)) != NSP_OK) return e;
+  if ((e = (form == 2 ? cholqr(Ys, &Q, nY, Qa2, Qb2) : cholqr(Ys, &Q))) != NSP_OK) return e;
   // step 6: C = Omega^T Y, symmetrised (reading C6)
-  nspb::gram(Om, sp, sp, Y, sp, sp, n, C, sp, w.gram, st);
+  nspb::gram(Gs, sp, sp, Ys, sp, sp, nY, C, sp, w.gram, st);
   nspb::small_sym(C, s, sp, 0.0, st);
   // step 7: EVD of C, split at eps = nys_eps_rel * lambda_max
   nspb::small_eig(C, sp, s, Vw, sp + 1, lamC, VC, nullptr, st);
@@ -664,15 +693,20 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
     nspb::small_eig(Tm, sp, s, Vw, sp + 1, lamT, VT, nullptr, st);
     // step 10: U~ = Q W(:, 1:k)  (reading C5)
     const int kp = ((rk + 63) / 64) * 64;
-    double* U = Bn;  // reuse (n x kp, kp <= sp)
+    double* U = form == 2 ? Fi : Bn;  // reuse (nY x kp, kp <= sp; the sketch is no longer needed)
     NSP_CUDA_TRY(c, cudaMemsetAsync(Wc, 0, sm * 8, st));
     nspb::scale_cols(VT, s, lamT, rk, s, kp, Wc, kp, 3, st);
     PanelArgs pu{U, kp, nullptr, 0, Q, sp, Wc, kp, 1.0, nullptr};
-    nspb::panel2(pu, nullptr, sp, kp, n, st);
-    // step 11: Z = A_G^{-1} U~
+    nspb::panel2(pu, nullptr, sp, kp, nY, st);
+    // step 11: Z = A_G^{-1} U~  (M_3: Z^ = A_G^{-1} A_GI V^, eq:left_prec_mat2)
     NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_Z, (size_t)std::max<int64_t>(n, 1) * kp * 8));
     NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_Z, 0, (size_t)std::max<int64_t>(n, 1) * kp * 8, st));
-    if ((e = ag_solve(c, U, kp, c->d_Z, kp, rk, w.wvu)) != NSP_OK) return e;
+    if (form == 2) {
+      nspk::spmm(c->AGG2, nullptr, 0, U + c->i1_rows * (int64_t)kp, kp, n, Bn, kp, rk, 2, true, st);
+      if ((e = ag_solve(c, Bn, kp, c->d_Z, kp, rk, w.wvu)) != NSP_OK) return e;
+    } else if ((e = ag_solve(c, U, kp, c->d_Z, kp, rk, w.wvu)) != NSP_OK) {
+      return e;
+    }
     NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_sigma, kp * 8));
     NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_sigma, 0, kp * 8, st));
     NSP_CUDA_TRY(c, cudaMemcpyAsync(c->d_sigma, lamT, rk * 8, cudaMemcpyDeviceToDevice, st));

@@ -129,3 +129,36 @@ def test_nystrom_si_form_parity(name):
     ctx.precond_apply(2, dev(R), Y)
     assert relfro(Y.cpu().numpy(), apply_M2(S, ref0.Z, ref0.sigma, R)) <= 1e-8
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg5s"])
+def test_nystrom_m3_parity(name):
+    """M_3 (Nystrom of S_I^{-1}, eq:left_prec_mat2; opts.nys_form = 2): inner count within +-1, Sigma and
+    M_3 / M_A-DEF3 probes at equal counts within 1e-8 of oracle.si.nystrom_si_inverse."""
+    from oracle.nystrom import apply_ADEF2
+    from paper_2101_12164_b200 import Context
+    from nsp_inputs import philox
+    pr, d, S = problem(name)
+    Om = philox.gaussian_block(0, 5, pr.n, pr.s)     # n x s sketch in the original order (interior rows used)
+    ref = O.nystrom_si_inverse(S, Om, pr.rank, pr.tol_bcg, 500)
+    ctx = Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, factor_gamma=True, nys_form=2)
+    rep = ctx.nystrom(pr.rank, pr.oversample, dev(Om), pr.tol_bcg, 500)
+    assert rep["converged"] and abs(rep["iters"] - ref.bcg["iters"]) <= 1, (rep["iters"], ref.bcg["iters"])
+    k = ref.bcg["iters"]
+    ref0 = O.nystrom_si_inverse(S, Om, pr.rank, 0.0, k)
+    rep0 = ctx.nystrom(pr.rank, pr.oversample, dev(Om), 0.0, k)
+    assert rep0["iters"] == k and rep0["rank"] == ref0.rank
+    sig = ctx.nystrom_sigma()
+    assert np.max(np.abs(sig - ref0.sigma) / ref0.sigma) <= 1e-8, (sig[:3], ref0.sigma[:3])
+    R = block(d.n_gamma, 8, seed=31)
+    Y = torch.empty(d.n_gamma, 8, dtype=torch.float64, device="cuda")
+    ctx.precond_apply(2, dev(R), Y)
+    assert relfro(Y.cpu().numpy(), apply_M2(S, ref0.Z, ref0.sigma, R)) <= 1e-8
+    # M_A-DEF3 through the full solve at equal PCG counts
+    b = pr.rhs()
+    xo, io = O.solve_full_system(S, b, 1e-8, 2000, lambda r: apply_ADEF2(S, ref0.Z, r))
+    x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
+    rp = ctx.pcg(dev(b), x, 0.0, io["iters"], precond=3)
+    assert rp["iters"] == io["iters"]
+    assert relfro(x.cpu().numpy(), xo) <= 1e-8
+    ctx.close()

@@ -459,3 +459,21 @@ def test_adef2_exact_deflation_space():
     assert np.allclose(MS @ Z, Z, atol=1e-10)
     v = V[:, 20]                              # a direction outside span(Z): A_G^{-1} S v = lam v
     assert np.allclose(MS @ v, lam[20] * v, atol=1e-10 * np.abs(v).max())
+
+
+def test_m3_exact_gives_one_pcg_iteration():
+    """M_3 (eq:left_prec_mat2): with s = n_I and an exact inner solve the Nystrom approximation of S_I^{-1}
+    is exact, so M_3 = A_G^{-1} + A_G^{-1} A_GI S_I^{-1} A_IG A_G^{-1} = S_G^{-1} (Woodbury eq:S-1,
+    PAPER.md:807-813) and the outer PCG converges in one iteration."""
+    from oracle.nystrom import apply_M2
+    dims, axis, c = (5, 9), 0, 2
+    A, part = _single_separator(dims, axis, c)
+    d = O.dbbd(A.to_scipy(), part, 2)
+    S = O.SchurOracle(d)
+    nI = A.n - d.n_gamma
+    Om = philox.gaussian_block(0, 0, A.n, nI)
+    r = O.nystrom_si_inverse(S, Om, nI, exact_inner=True)
+    assert r.rank == nI
+    b = philox.gaussian(5, 1, A.n)
+    x, info = O.solve_full_system(S, b, 1e-10, 50, lambda v: apply_M2(S, r.Z, r.sigma, v))
+    assert info["iters"] <= 1 + 1 and np.allclose(x, np.linalg.solve(A.to_scipy().toarray(), b), atol=1e-9)
