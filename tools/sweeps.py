@@ -35,12 +35,39 @@ def one(ctx, pr, k, p, tol_inner, bcg_precond_ctx=None, maxit=5000):
                 it_PCG=rp["iters"], pcg_converged=rp["converged"], pcg_s=round(t_pcg, 3))
 
 
+def variants(pr, tol_inner=0.1):
+    """tab:compare_variations analog: it_total = inner block-CG iterations + outer
+    PCG iterations for M_2, M_A-DEF2, M_3, M_A-DEF3, and S~_1 (A_G^{-1} alone)."""
+    out = {}
+    b = torch.from_numpy(pr.rhs()).cuda()
+    for form, lab in ((0, "2"), (2, "3")):
+        ctx = nsp.Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, factor_gamma=True, nys_form=form)
+        rows = ctx.n_gamma if form == 0 else pr.n
+        Om = torch.from_numpy(philox.gaussian_block(0, philox.STREAM_OMEGA if form == 0 else 5, rows, pr.s)).cuda()
+        rn = ctx.nystrom(pr.rank, pr.oversample, Om, tol_inner, 1000)
+        for prec, name in ((2, f"M{lab}"), (3, f"M_A-DEF{lab}")):
+            x = torch.zeros_like(b)
+            r = ctx.pcg(b, x, pr.tol_pcg or 1e-8, 20000, precond=prec)
+            out[name] = dict(it_inner=rn["iters"], it_pcg=r["iters"], it_total=rn["iters"] + r["iters"],
+                             converged=r["converged"])
+        if form == 0:
+            x = torch.zeros_like(b)
+            r = ctx.pcg(b, x, pr.tol_pcg or 1e-8, 20000, precond=1)
+            out["S1"] = dict(it_pcg=r["iters"], it_total=r["iters"], converged=r["converged"])
+        ctx.close()
+    return out
+
+
 def main():
     B.build()
     name = sys.argv[1] if len(sys.argv) > 1 and sys.argv[1].startswith("cfg") else "cfg2"
     what = sys.argv[sys.argv.index("--what") + 1].split(",") if "--what" in sys.argv else ["tol", "rank", "over"]
     pr = P.make(name)
     out = {"config": name}
+    if "variants" in what:
+        out["variants"] = variants(pr)
+        print(json.dumps(out), flush=True)
+        return
     for prec in (0, 1):   # reading C2: block CG with M = I and M = A_G^{-1}
         ctx = nsp.Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, factor_gamma=True, bcg_precond=prec)
         k0, p0 = pr.rank, pr.oversample
