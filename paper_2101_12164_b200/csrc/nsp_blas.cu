@@ -487,58 +487,104 @@ __global__ void __launch_bounds__(256) k_small_chol(const double* __restrict__ A
 }
 
 // ---------------------------------------------------------------------------------------------
-// one-CTA cyclic (round-robin) parallel Jacobi eigensolver of a symmetric n x n matrix (n <= 256,
-// padded to even).  A in smem, V in global.  Outputs eigenvalues (descending) and eigenvectors
-// (columns, same order).  `gate` (optional): run only if *gate != 0.
+// one-CTA cyclic (round-robin) parallel Jacobi eigensolver of a symmetric n x n matrix (n <= 128,
+// padded to even ne).  Everything stays in shared memory: A packed upper-triangular (the two-sided
+// rotation keeps it symmetric; 66 KB at ne = 128) and a row slice of V transposed (Vt[k][i - i0] =
+// V_ik).  The grid's CTAs all run the IDENTICAL A iteration (same instructions on the same data, so
+// bitwise the same rotations) and each accumulates only its own rows of V: V's shared-memory
+// traffic, the bound of a one-CTA Jacobi, is split across the grid with no communication.  One
+// round = ne/2 disjoint rotations: phase 1 (one thread per pair) computes (c, s) and rotates its
+// own 2 x 2 diagonal block (Golub-Van Loan Alg. 8.4.1 formulas, a_pq <- 0); phase 2 applies
+// J_k^T B J_l to every off-diagonal 2 x 2 block (k < l) in ONE pass and rotates V.  Two barriers
+// per round.  Outputs eigenvalues (descending) and eigenvectors (columns, same order).  `gate`
+// (optional): run only if *gate != 0.  Vwork is unused (kept for the call signature).
 // ---------------------------------------------------------------------------------------------
+#ifdef NSP_EIG_PROF
+__device__ int g_eig_sweeps;
+#endif
 __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ Ain, int lda, int n,
-                                                    double* V, int ldv, double* lam, double* Vsorted,
+                                                    double* Vwork, int ldv, double* lam, double* Vsorted,
                                                     const int* gate) {
+  (void)Vwork;
+  (void)ldv;
   if (gate && *gate == 0) return;
   extern __shared__ double sm[];
   const int ne = n + (n & 1);
-  const int ld = ne + 1;
-  double* A = sm;
-  __shared__ double cs[128], sn[128];
-  __shared__ int pp[128], qq[128];
-  __shared__ double red[1024];
-  __shared__ int order[256];
+  const int npair = ne / 2;
+  double* Ap = sm;                              // packed upper triangle, ne (ne + 1) / 2
+  const int rp = (ne + gridDim.x - 1) / gridDim.x;      // V rows per CTA
+  const int i0 = blockIdx.x * rp, i1 = min(ne, i0 + rp);
+  double* Vt = sm + ne * (ne + 1) / 2;          // ne x rp, Vt[k * rp + (i - i0)]
+  __shared__ double2 csn[64];                   // (c, s) per pair
+  __shared__ int2 pq[64];                       // (p, q) per pair, p < q
+  __shared__ double red[2][32];
+  __shared__ int order[128];
   const int tid = threadIdx.x, nt = blockDim.x;
+  auto tri = [ne](int a, int b) -> int {      // a <= b
+    return a * ne - (a * (a - 1)) / 2 + (b - a);
+  };
+  auto at = [&](int a, int b) -> double& { return a <= b ? Ap[tri(a, b)] : Ap[tri(b, a)]; };
   for (int e = tid; e < ne * ne; e += nt) {
     const int i = e / ne, j = e - i * ne;
-    A[i * ld + j] = (i < n && j < n) ? Ain[i * lda + j] : 0.0;
-    V[i * ldv + j] = (i == j) ? 1.0 : 0.0;   // V stored TRANSPOSED (V[k * ldv + i] = V_ik): coalesced rotations
+    if (i <= j) Ap[tri(i, j)] = (i < n && j < n) ? Ain[i * lda + j] : 0.0;
+  }
+  for (int e = tid; e < ne * rp; e += nt) {
+    const int k = e / rp, i = i0 + (e - k * rp);
+    Vt[e] = (i == k) ? 1.0 : 0.0;
   }
   __syncthreads();
-  const int npair = ne / 2;
+  const int nblk = npair * (npair - 1) / 2;     // off-diagonal pair blocks k < l (<= 2016 < 2 nt)
+  const int vk_stride = nt / rp, vi = tid % rp, vk0 = tid / rp;   // V rotation: row i0 + vi, pairs vk0 + j stride
+  int bk[2], bl[2];                             // this thread's blocks, fixed across rounds
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    int k = 0, rem = tid + u * nt;
+    while (k < npair && rem >= npair - 1 - k) {
+      rem -= npair - 1 - k;
+      ++k;
+    }
+    bk[u] = k;
+    bl[u] = k + 1 + rem;
+  }
   for (int sweep = 0; sweep < 60; ++sweep) {
-    // off-diagonal and total norms
+    // off-diagonal and total norms (symmetric: off-diagonal entries count twice)
     double off = 0.0, tot = 0.0;
-    for (int e = tid; e < ne * ne; e += nt) {
-      const int i = e / ne, j = e - i * ne;
-      const double v = A[i * ld + j];
+    for (int e = tid; e < ne * (ne + 1) / 2; e += nt) {
+      // recover (i, j) is not needed: diagonal entries sit at tri(i, i)
+      const double v = Ap[e];
       tot += v * v;
-      if (i != j) off += v * v;
+      off += v * v;
     }
-    red[tid] = off;
-    __syncthreads();
-    for (int w = nt / 2; w > 0; w >>= 1) {
-      if (tid < w) red[tid] += red[tid + w];
-      __syncthreads();
+    for (int i = tid; i < ne; i += nt) {
+      const double v = Ap[tri(i, i)];
+      off -= v * v;
     }
-    const double offs = red[0];
-    __syncthreads();
-    red[tid] = tot;
-    __syncthreads();
-    for (int w = nt / 2; w > 0; w >>= 1) {
-      if (tid < w) red[tid] += red[tid + w];
-      __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
     }
-    const double tots = red[0];
+    if ((tid & 31) == 0) {
+      red[0][tid >> 5] = off;
+      red[1][tid >> 5] = tot;
+    }
     __syncthreads();
+    double offs = 0.0, tots = 0.0;
+    for (int w = 0; w < nt / 32; ++w) {       // fixed order: identical on every thread
+      offs += red[0][w];
+      tots += red[1][w];
+    }
+    __syncthreads();
+    // off-diagonal entries stored once: ||A||_F^2 = sum diag^2 + 2 sum upper^2
+    tots = tots + offs;
+    offs = 2.0 * offs;
     if (!(offs > 1e-28 * tots) || tots == 0.0) break;
+#ifdef NSP_EIG_PROF
+    if (tid == 0) g_eig_sweeps = sweep + 1;
+#endif
     for (int round = 0; round < ne - 1; ++round) {
-      // tournament pairing: positions 0..ne-1, element 0 fixed, others rotate
+      // phase 1: tournament pairing (position 0 fixed, the others rotate), rotation parameters,
+      // the pair's own 2 x 2 diagonal block
       if (tid < npair) {
         auto who = [&](int pos) -> int { return pos == 0 ? 0 : 1 + (pos - 1 + round) % (ne - 1); };
         int p = who(tid), q = who(ne - 1 - tid);
@@ -547,61 +593,79 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
           p = q;
           q = t;
         }
-        pp[tid] = p;
-        qq[tid] = q;
-        const double apq = A[p * ld + q];
+        pq[tid] = make_int2(p, q);
+        double& app = Ap[tri(p, p)];
+        double& aqq = Ap[tri(q, q)];
+        double& apq = Ap[tri(p, q)];
         double c = 1.0, s = 0.0;
-        if (fabs(apq) > 1e-300 && fabs(apq) > 1e-18 * sqrt(fabs(A[p * ld + p] * A[q * ld + q]))) {
-          const double th = (A[q * ld + q] - A[p * ld + p]) / (2.0 * apq);
-          const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-          c = 1.0 / sqrt(t * t + 1.0);
+        const double a_pq = apq, a_pp = app, a_qq = aqq;
+        if (fabs(a_pq) > 1e-300 && a_pq * a_pq > 1e-36 * fabs(a_pp * a_qq)) {
+          // t = sign(th) / (|th| + sqrt(th^2 + 1)), th = d / (2 a_pq), d = a_qq - a_pp, written
+          // as t = 2 a_pq sign(d) / (|d| + sqrt(d^2 + 4 a_pq^2)): one sqrt, one divide
+          const double d = a_qq - a_pp;
+          const double num = d >= 0 ? 2.0 * a_pq : -2.0 * a_pq;
+          const double t = num / (fabs(d) + sqrt(d * d + 4.0 * a_pq * a_pq));
+          c = rsqrt(t * t + 1.0);
           s = t * c;
+          app = a_pp - t * a_pq;
+          aqq = a_qq + t * a_pq;
+          apq = 0.0;
         }
-        cs[tid] = c;
-        sn[tid] = s;
+        csn[tid] = make_double2(c, s);
       }
       __syncthreads();
-      // columns: A <- A J ; V <- V J
-      for (int e = tid; e < npair * ne; e += nt) {
-        const int k = e / ne, i = e - k * ne;
-        const int p = pp[k], q = qq[k];
-        const double c = cs[k], s = sn[k];
-        const double ap = A[i * ld + p], aq = A[i * ld + q];
-        A[i * ld + p] = c * ap - s * aq;
-        A[i * ld + q] = s * ap + c * aq;
-        const double vp = V[p * ldv + i], vq = V[q * ldv + i];
-        V[p * ldv + i] = c * vp - s * vq;
-        V[q * ldv + i] = s * vp + c * vq;
+      // phase 2a: off-diagonal blocks B = A[{pk, qk}, {pl, ql}] <- J_k^T B J_l, J = [[c, s], [-s, c]]
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (tid + u * nt >= nblk) break;
+        const int k = bk[u], l = bl[u];
+        const int2 Pk = pq[k], Pl = pq[l];
+        const double2 Ck = csn[k], Cl = csn[l];
+        const int pk = Pk.x, qk = Pk.y, pl = Pl.x, ql = Pl.y;
+        const double ck = Ck.x, sk = Ck.y, cl = Cl.x, sl = Cl.y;
+        double& b00 = at(pk, pl);
+        double& b01 = at(pk, ql);
+        double& b10 = at(qk, pl);
+        double& b11 = at(qk, ql);
+        // rows (J_k^T): r_p = c b_p - s b_q, r_q = s b_p + c b_q
+        const double r00 = ck * b00 - sk * b10, r01 = ck * b01 - sk * b11;
+        const double r10 = sk * b00 + ck * b10, r11 = sk * b01 + ck * b11;
+        // columns (J_l): col_p = c col_p - s col_q, col_q = s col_p + c col_q
+        b00 = cl * r00 - sl * r01;
+        b01 = sl * r00 + cl * r01;
+        b10 = cl * r10 - sl * r11;
+        b11 = sl * r10 + cl * r11;
       }
-      __syncthreads();
-      // rows: A <- J^T A
-      for (int e = tid; e < npair * ne; e += nt) {
-        const int k = e / ne, j = e - k * ne;
-        const int p = pp[k], q = qq[k];
-        const double c = cs[k], s = sn[k];
-        const double ap = A[p * ld + j], aq = A[q * ld + j];
-        A[p * ld + j] = c * ap - s * aq;
-        A[q * ld + j] = s * ap + c * aq;
-      }
+      // phase 2b: V <- V J (V transposed: columns p, q are rows of Vt, contiguous)
+      if (tid < vk_stride * rp)
+        for (int k = vk0; k < npair; k += vk_stride) {
+          const int2 P = pq[k];
+          const double2 C = csn[k];
+          const int p = P.x, q = P.y;
+          const double c = C.x, s = C.y;
+          const double vp = Vt[p * rp + vi], vq = Vt[q * rp + vi];
+          Vt[p * rp + vi] = c * vp - s * vq;
+          Vt[q * rp + vi] = s * vp + c * vq;
+        }
       __syncthreads();
     }
   }
   // sort descending (stable by index) - rank by counting
   if (tid < n) {
-    const double li = A[tid * ld + tid];
+    const double li = Ap[tri(tid, tid)];
     int r = 0;
     for (int j = 0; j < n; ++j) {
-      const double lj = A[j * ld + j];
+      const double lj = Ap[tri(j, j)];
       if (lj > li || (lj == li && j < tid)) ++r;
     }
     order[r] = tid;
   }
   __syncthreads();
-  if (tid < n) lam[tid] = A[order[tid] * ld + order[tid]];
-  __syncthreads();
-  for (int e = tid; e < n * n; e += nt) {
+  if (tid < n && blockIdx.x == 0) lam[tid] = Ap[tri(order[tid], order[tid])];
+  const int nr = max(0, min(i1, n) - i0);
+  for (int e = tid; e < nr * n; e += nt) {
     const int i = e / n, k = e - i * n;
-    Vsorted[i * n + k] = V[order[k] * ldv + i];
+    Vsorted[(i0 + i) * n + k] = Vt[order[k] * rp + i];
   }
 }
 
@@ -770,9 +834,11 @@ void small_chol(const double* A, int sp, int mode, int nact, double tau, double*
 void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* lam, double* Vsorted,
                const int* gate, cudaStream_t st) {
   const int ne = n + (n & 1);
-  const size_t smem = (size_t)ne * (ne + 1) * sizeof(double);
+  const int g = ne >= 128 ? 8 : ne >= 64 ? 4 : 1;   // V row slices (rp = ne / g rows each)
+  const int rp = (ne + g - 1) / g;
+  const size_t smem = (size_t)(ne * (ne + 1) / 2 + ne * rp) * sizeof(double);
   set_smem((const void*)k_small_eig, smem);
-  { nsp_count_launch(); k_small_eig<<<1, 1024, smem, st>>>(A, lda, n, Vwork, ldv, lam, Vsorted, gate); }
+  { nsp_count_launch(); k_small_eig<<<g, 1024, smem, st>>>(A, lda, n, Vwork, ldv, lam, Vsorted, gate); }
 }
 
 void orth_from_eig(const double* lam, const double* Vs, int n, int sp, double tau, double* T, BcgStatus* stt,

@@ -1088,6 +1088,124 @@ __global__ void __launch_bounds__(256) k_spike_tail(const double* __restrict__ s
   }
 }
 
+// 8 dot products per warp: v[rr] (per-lane partials of row rr) -> the full sum of row
+// 4 bit4 + 2 bit3 + bit2 of the lane, in lanes with (lane & 3) == 0 (and their 3 neighbours)
+__device__ __forceinline__ double warp_reduce8(double v[8], int lane) {
+  {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double rcv = __shfl_xor_sync(0xffffffffu, up ? v[i] : v[i + 4], 16);
+      v[i] = (up ? v[i + 4] : v[i]) + rcv;
+    }
+  }
+  {
+    const bool up = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const double rcv = __shfl_xor_sync(0xffffffffu, up ? v[i] : v[i + 2], 8);
+      v[i] = (up ? v[i + 2] : v[i]) + rcv;
+    }
+  }
+  {
+    const bool up = lane & 4;
+    const double rcv = __shfl_xor_sync(0xffffffffu, up ? v[0] : v[1], 4);
+    v[0] = (up ? v[1] : v[0]) + rcv;
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return v[0];
+}
+__device__ __forceinline__ int warp_reduce8_row(int lane) {
+  return 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
+}
+
+// one column (s = 1, ld 1): the same P-step recurrence as a matrix-vector chain.  The spike tiles
+// do not depend on the recurrence, so they stream through a 2-deep TMA ring while the previous
+// step computes; the running 64-vector stays in shared memory; each warp owns 8 rows (coalesced
+// 32-lane row reads, transposed shuffle reduction: 9 shuffles for 8 dot products).
+__global__ void __launch_bounds__(256) k_spike_tail_vec(const double* __restrict__ spk,
+                                                        const int* __restrict__ chunk_first, int P,
+                                                        double* buf, int fwd) {
+  extern __shared__ __align__(128) double sm[];   // 2 x 4096 spike tiles
+  __shared__ double xs[64];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nstep = P - 1;
+  // step j: the tile row updated (and whose spike rows are used) and the tile row it reads
+  auto tile_of = [&](int j) { return fwd ? chunk_first[j + 2] - 1 : chunk_first[P - 2 - j]; };
+  auto src_of = [&](int j) { return fwd ? chunk_first[j + 1] - 1 : chunk_first[P - 1 - j]; };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < 2 && j < nstep; ++j)
+      mbar_expect_copy(&bar[j], sm + j * 4096, spk + (int64_t)tile_of(j) * 4096, 4096 * 8);
+  }
+  if (tid < 64) xs[tid] = buf[(int64_t)src_of(0) * 64 + tid];
+  __syncthreads();
+  const int myrow = 8 * warp + warp_reduce8_row(lane);
+  for (int j = 0; j < nstep; ++j) {
+    const int t = tile_of(j);
+    const double y = (lane & 3) == 0 ? buf[(int64_t)t * 64 + myrow] : 0.0;
+    const int b = j & 1;
+    mbar_wait(&bar[b], (j >> 1) & 1);
+    const double* S = sm + b * 4096;
+    const double x0 = xs[lane], x1 = xs[lane + 32];
+    double v[8];
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) {
+      const double* Sr = S + (8 * warp + rr) * 64;
+      v[rr] = fma(Sr[lane], x0, Sr[lane + 32] * x1);
+    }
+    v[0] = warp_reduce8(v, lane);
+    __syncthreads();   // every read of xs and of ring slot b is done
+    if ((lane & 3) == 0) {
+      const double o = y - v[0];
+      xs[myrow] = o;
+      buf[(int64_t)t * 64 + myrow] = o;
+    }
+    if (tid == 0 && j + 2 < nstep) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_expect_copy(&bar[b], sm + b * 4096, spk + (int64_t)tile_of(j + 2) * 4096, 4096 * 8);
+    }
+    __syncthreads();
+  }
+}
+
+// one column: every remaining tile row in parallel, one CTA per tile row, spike rows read straight
+// from global memory (each warp 8 rows, coalesced), no shared-memory staging
+__global__ void __launch_bounds__(256) k_spike_update_vec(const double* __restrict__ spk,
+                                                          const int* __restrict__ chunk_first,
+                                                          const int* __restrict__ tile_chunk, int P, double* buf,
+                                                          int fwd) {
+  const int I = blockIdx.x;
+  const int k = tile_chunk[I];
+  int src;
+  if (fwd) {
+    if (k == 0 || I == chunk_first[k + 1] - 1) return;
+    src = chunk_first[k] - 1;
+  } else {
+    if (k == P - 1 || I == chunk_first[k]) return;
+    src = chunk_first[k + 1];
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* xg = buf + (int64_t)src * 64;
+  const double x0 = xg[lane], x1 = xg[lane + 32];
+  const double* S = spk + (int64_t)I * 4096;
+  double v[8];
+#pragma unroll
+  for (int rr = 0; rr < 8; ++rr) {
+    const double* Sr = S + (8 * warp + rr) * 64;
+    v[rr] = fma(__ldg(Sr + lane), x0, __ldg(Sr + lane + 32) * x1);
+  }
+  const double d = warp_reduce8(v, lane);
+  if ((lane & 3) == 0) buf[(int64_t)I * 64 + 8 * warp + warp_reduce8_row(lane)] -= d;
+}
+
 // all remaining tile rows in parallel: grid (tile rows, 32-column chunks)
 __global__ void __launch_bounds__(256) k_spike_update(const double* __restrict__ spk, const int* __restrict__ chunk_first,
                                                       const int* __restrict__ tile_chunk, int P, double* buf, int ldw,
@@ -1235,12 +1353,25 @@ void spike_tail(const double* spk, const int* chunk_first, int P, double* buf, i
     cudaFuncSetAttribute(k_spike_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
+  if (s == 1 && ldw == 1) {
+    static bool attr1 = false;
+    if (!attr1) {
+      cudaFuncSetAttribute(k_spike_tail_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 8);
+      attr1 = true;
+    }
+    { nsp_count_launch(); k_spike_tail_vec<<<1, 256, 2 * 4096 * 8, st>>>(spk, chunk_first, P, buf, fwd); }
+    return;
+  }
   { nsp_count_launch(); k_spike_tail<<<(s + 31) / 32, 256, smem, st>>>(spk, chunk_first, P, buf, ldw, s, fwd); }
 }
 
 void spike_update(const double* spk, const int* chunk_first, const int* tile_chunk, int P, int nt, double* buf,
                   int ldw, int s, bool fwd, cudaStream_t st) {
   if (P <= 1) return;
+  if (s == 1 && ldw == 1) {
+    { nsp_count_launch(); k_spike_update_vec<<<nt, 256, 0, st>>>(spk, chunk_first, tile_chunk, P, buf, fwd); }
+    return;
+  }
   const size_t smem = (64 * 65 + 64 * 33) * sizeof(double);   // attribute set with k_spike_tail (called first)
   { nsp_count_launch(); k_spike_update<<<dim3(nt, (s + 31) / 32), 256, smem, st>>>(spk, chunk_first, tile_chunk, P,
                                                                                     buf, ldw, s, fwd); }

@@ -24,7 +24,7 @@ namespace {
 
 constexpr int RT = 256;             // threads per reduction CTA
 constexpr int RPB = 2048;           // rows per partial-sum chunk
-constexpr int GT_ROWS = 512;        // rows per Z^T r chunk
+constexpr int GT_ROWS = 64;         // rows per Z^T r chunk
 
 // part[b*2 + q] = sum over chunk b of a_q . b_q (q = 0, 1; a2 may be null)
 __global__ void __launch_bounds__(RT) k_dot2_partial(const double* __restrict__ a1, const double* __restrict__ b1,
@@ -129,25 +129,54 @@ __global__ void k_axpy_strided(double* y, int ldy, const double* a, int lda, con
 }
 
 // part[chunk*128 + k] = sum over chunk rows of Z[row][k] * r[row]  (k < rk)
-__global__ void __launch_bounds__(128) k_gemvt_partial(const double* __restrict__ Z, int ldz,
+__global__ void __launch_bounds__(256) k_gemvt_partial(const double* __restrict__ Z, int ldz,
                                                        const double* __restrict__ r, int64_t n, int rk,
                                                        double* __restrict__ part) {
-  const int k = threadIdx.x;
+  // chunk of GT_ROWS rows; warp w takes rows w, w + 8, ...; lane covers columns lane + 32 j (j < 4),
+  // so every row read is one coalesced 1 KB line; the 8 warp partials are summed in fixed order
+  __shared__ double red[8][128];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * GT_ROWS;
-  double s = 0.0;
-  if (k < rk)
-    for (int64_t i = r0; i < min(n, r0 + GT_ROWS); ++i) s = fma(Z[i * ldz + k], r[i], s);
-  part[blockIdx.x * 128 + k] = s;
+  const int64_t r1 = min(n, r0 + GT_ROWS);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = r0 + wid; i < r1; i += 8) {
+    const double ri = r[i];
+    const double* zr = Z + i * ldz;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = lane + 32 * j;
+      if (k < rk) acc[j] = fma(__ldg(zr + k), ri, acc[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) red[wid][lane + 32 * j] = acc[j];
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+    part[blockIdx.x * 128 + threadIdx.x] = s;
+  }
 }
 
-// g[k] = sigma[k] * sum_chunks part[chunk][k]  (fixed order)
-__global__ void k_gemvt_reduce(const double* __restrict__ part, int nchunks, const double* __restrict__ sigma, int rk,
-                               double* __restrict__ g) {
-  const int k = threadIdx.x;
-  if (k >= rk) return;
+// g[k] = sigma[k] * sum_chunks part[chunk][k]  (fixed order: 8 interleaved partial sums, combined
+// in group order)
+__global__ void __launch_bounds__(1024) k_gemvt_reduce(const double* __restrict__ part, int nchunks,
+                                                       const double* __restrict__ sigma, int rk,
+                                                       double* __restrict__ g) {
+  __shared__ double red[8][128];
+  const int k = threadIdx.x & 127, grp = threadIdx.x >> 7;
   double s = 0.0;
-  for (int b = 0; b < nchunks; ++b) s += part[b * 128 + k];
-  g[k] = sigma ? sigma[k] * s : s;
+#pragma unroll 4
+  for (int b = grp; b < nchunks; b += 8) s += part[b * 128 + k];
+  red[grp][k] = s;
+  __syncthreads();
+  if (threadIdx.x < rk) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += red[q][k];
+    g[k] = sigma ? sigma[k] * t : t;
+  }
 }
 
 // y[row] += sum_k Z[row][k] g[k]   (warp per row, butterfly sum)
@@ -243,12 +272,12 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
     k_axpy_strided<<<grid1(n, 256), 256, 0, c->stream>>>(w.t2, 1, r, 1, w.t2, 1, -1.0, n);   // d = r - S t
     const unsigned nch = grid1(n, GT_ROWS);
     nsp_count_launch();
-    k_gemvt_partial<<<nch, 128, 0, c->stream>>>(c->d_Z, kp, w.t2, n, rk, w.gpart);
+    k_gemvt_partial<<<nch, 256, 0, c->stream>>>(c->d_Z, kp, w.t2, n, rk, w.gpart);
     double* G = w.eg;                 // kp x kp, column 0 = Z^T d
     double* H = w.eg + 128 * 128;     // kp x kp, column 0 = E^{-1} Z^T d
     NSP_CUDA_TRY(c, cudaMemsetAsync(G, 0, (size_t)kp * kp * 8, c->stream));
     nsp_count_launch();
-    k_gemvt_reduce<<<1, 128, 0, c->stream>>>(w.gpart, (int)nch, nullptr, rk, w.g);
+    k_gemvt_reduce<<<1, 1024, 0, c->stream>>>(w.gpart, (int)nch, nullptr, rk, w.g);
     NSP_CUDA_TRY(c, cudaMemcpy2DAsync(G, kp * 8, w.g, 8, 8, rk, cudaMemcpyDeviceToDevice, c->stream));
     nspb::chol_solve(c->d_ELp, kp, G, kp, H, kp, 1.0, true, true, nullptr, c->stream);
     NSP_CUDA_TRY(c, cudaMemcpy2DAsync(w.g, 8, H, kp * 8, 8, rk, cudaMemcpyDeviceToDevice, c->stream));
@@ -258,9 +287,9 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
   if (which == 2 && c->nys_rank > 0) {
     const unsigned nch = grid1(n, GT_ROWS);
     nsp_count_launch();
-    k_gemvt_partial<<<nch, 128, 0, c->stream>>>(c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart);
+    k_gemvt_partial<<<nch, 256, 0, c->stream>>>(c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart);
     nsp_count_launch();
-    k_gemvt_reduce<<<1, 128, 0, c->stream>>>(w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
+    k_gemvt_reduce<<<1, 1024, 0, c->stream>>>(w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
     nsp_count_launch();
     k_gemv_add<<<grid1(n * 32, 256), 256, 0, c->stream>>>(c->d_Z, c->nys_ld, w.g, c->nys_rank, n, z);
   }
