@@ -238,6 +238,7 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_sigma);
   comm_free(c);
   if (c->bcg_graph) cudaGraphExecDestroy(c->bcg_graph);
+  if (c->pcg_graph) cudaGraphExecDestroy(c->pcg_graph);
   if (c->gstream) cudaStreamDestroy(c->gstream);
   for (DevCSR* m : {&c->A2G, &c->AGG2, &c->AGSH, &c->CB, &c->C1, &c->AII}) {
     fr(m->rowptr);

@@ -10,7 +10,9 @@ struct BcgStatus {
   int fallback;     // orth used the eigen fallback
   int converged;
   int nonfinite;
-  int pad_[3];
+  int done;       // PCG: the iteration stopped (converged / breakdown / maxit); later kernels no-op
+  int iters;      // PCG: iterations taken (device count)
+  int maxit;      // PCG: iteration cap
   double relres;    // max_j ||R_j|| / ||B_j||
   double scalar[6]; // PCG scalars
 };

@@ -50,6 +50,21 @@ struct HostCSR32 {
 };
 
 // key of the cached block-CG iteration graph (nsp_solver.cu)
+struct PcgKey {
+  const double* w = nullptr;
+  int64_t n = 0;
+  int precond = -1;
+  double tol = 0;
+  int maxit = 0;
+  int rank = 0;
+  const void* Z = nullptr;     // Nystrom basis / E factor buffers (re-allocated by a new nsp_nystrom)
+  const void* E = nullptr;
+  long long gen = 0;
+  bool operator==(const PcgKey& o) const {
+    return w == o.w && n == o.n && precond == o.precond && tol == o.tol && maxit == o.maxit && rank == o.rank &&
+           Z == o.Z && E == o.E && gen == o.gen;
+  }
+};
 struct GraphKey {
   const void* X = nullptr;
   int64_t n = 0;
@@ -113,6 +128,7 @@ struct nsp_ctx {
   double* d_Z = nullptr;          // nG x nys_ld
   double* d_sigma = nullptr;      // nys_ld
   int nys_rank = -1, nys_ld = 0;
+  long long nys_gen = 0;   // bumped by every nsp_nystrom
   double* d_ELp = nullptr;        // Cholesky (k_chol16 packed) of E = Z^T S_G Z for M_A-DEF2
   bool adef_ok = false;
   std::vector<double> h_sigma;
@@ -144,6 +160,10 @@ struct nsp_ctx {
   cudaGraphExec_t bcg_graph = nullptr;
   GraphKey bcg_key;
   long long bcg_graph_kernels = 0;   // kernel nodes per launch of bcg_graph (launch evidence counter)
+  // cached CUDA graph of PCG_CHUNK outer-PCG iterations
+  cudaGraphExec_t pcg_graph = nullptr;
+  PcgKey pcg_key;
+  long long pcg_graph_kernels = 0;
   cudaStream_t gstream = nullptr;
   bool capturing = false;          // block CG is capturing its iteration graph
   bool gprof_in_graph = false;     // the cached graph records gprof_ev around a2+a3

@@ -25,6 +25,7 @@ namespace {
 constexpr int RT = 256;             // threads per reduction CTA
 constexpr int RPB = 2048;           // rows per partial-sum chunk
 constexpr int GT_ROWS = 64;         // rows per Z^T r chunk
+constexpr int PCG_CHUNK = 8;        // PCG iterations per host status check (one CUDA graph)
 
 // part[b*2 + q] = sum over chunk b of a_q . b_q (q = 0, 1; a2 may be null)
 __global__ void __launch_bounds__(RT) k_dot2_partial(const double* __restrict__ a1, const double* __restrict__ b1,
@@ -58,8 +59,9 @@ __global__ void __launch_bounds__(RT) k_dot2_partial(const double* __restrict__ 
 // mode 0: out slot = sum (q = 0);   mode 1: out slot = sum (q = 0), status relres / converged from
 // sum = r.r;  mode 2: ||f|| (sqrt of sum) and the initial status.
 __global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ part, int nblk, double* sc, int slot,
-                                                   int mode, double tol, BcgStatus* st) {
+                                                   int mode, double tol, BcgStatus* st, double* hist) {
   __shared__ double red[RT];
+  if (mode == 1 && st->done) return;   // read by every thread before thread 0 can write it
   double s = 0.0;
   for (int b = threadIdx.x; b < nblk; b += RT) s += part[b * 2];
   red[threadIdx.x] = s;
@@ -79,11 +81,16 @@ __global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ pa
     st->relres = rel;
     st->converged = rel <= tol ? 1 : 0;
     if (!isfinite(v)) st->nonfinite = 1;
+    const int it = ++st->iters;
+    hist[(it - 1) % PCG_CHUNK] = rel;
+    st->done = (st->converged || st->nonfinite || st->indefinite || it >= st->maxit) ? 1 : 0;
   } else {
     sc[4] = sqrt(v);
     st->relres = v > 0.0 ? 1.0 : 0.0;
     st->converged = v > 0.0 ? 0 : 1;
     if (!isfinite(v)) st->nonfinite = 1;
+    st->iters = 0;
+    st->done = (st->converged || st->nonfinite || st->maxit <= 0) ? 1 : 0;
   }
 }
 
@@ -93,6 +100,7 @@ __global__ void __launch_bounds__(RT) k_pcg_xr(double* __restrict__ x, double* _
                                                int64_t n, const double* sc, int cur, double* __restrict__ part,
                                                BcgStatus* st) {
   __shared__ double red[RT];
+  if (st->done) return;
   const double pq = sc[2];
   const double alpha = pq > 0.0 ? sc[cur] / pq : 0.0;
   if (blockIdx.x == 0 && threadIdx.x == 0 && !(pq > 0.0)) st->indefinite = 1;
@@ -114,9 +122,10 @@ __global__ void __launch_bounds__(RT) k_pcg_xr(double* __restrict__ x, double* _
 }
 
 // p = z + beta p, beta = (r.z)_new / (r.z)_old
-__global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ z, int64_t n, const double* sc, int cur) {
+__global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ z, int64_t n, const double* sc, int cur,
+                        const BcgStatus* st) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || st->done) return;
   const double beta = sc[cur ^ 1] / sc[cur];
   p[i] = fma(beta, p[i], z[i]);
 }
@@ -203,7 +212,7 @@ struct PcgWs {
   double *f, *w, *r, *z, *p, *q, *tmp, *t2, *eg;   // n_G vectors; eg: k x k (A-DEF2 solve, column 0)
   double *bB, *wvu, *tmpB;                 // W/V/U rows x 32
   double *i1r, *i1buf;                     // band rows x 32
-  double *agbuf, *apply_wvu, *part, *gpart, *g, *sc;
+  double *agbuf, *apply_wvu, *part, *gpart, *g, *sc, *hist;
   BcgStatus* st;
 };
 
@@ -239,6 +248,7 @@ static size_t pcg_layout(const nsp_ctx* c, char* base, PcgWs* out) {
   w.gpart = take((size_t)128 * grid1(std::max<int64_t>(c->nG, 1), GT_ROWS));
   w.g = take(128);
   w.sc = take(16);
+  w.hist = take(PCG_CHUNK);
   w.st = (BcgStatus*)take(sizeof(BcgStatus) / 8 + 1);
   if (out) *out = w;
   return off + 256;
@@ -252,7 +262,7 @@ static void dot(nsp_ctx* c, const double* a, const double* b, int64_t n, PcgWs& 
   nsp_count_launch();
   k_dot2_partial<<<nb, RT, 0, c->stream>>>(a, b, nullptr, nullptr, n, w.part);
   nsp_count_launch();
-  k_dot_reduce<<<1, RT, 0, c->stream>>>(w.part, (int)nb, w.sc, slot, 0, 0.0, w.st);
+  k_dot_reduce<<<1, RT, 0, c->stream>>>(w.part, (int)nb, w.sc, slot, 0, 0.0, w.st, w.hist);
 }
 
 // z = M r for the PCG preconditioner (0: identity copy, 1: A_G^{-1}, 2: M_2)
@@ -332,6 +342,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
   }
   // ---- PCG on S_G w = f
   BcgStatus init{};
+  init.maxit = maxit;
   std::memcpy(hs, &init, sizeof(init));
   NSP_CUDA_TRY(c, cudaMemcpyAsync(w.st, hs, sizeof(BcgStatus), cudaMemcpyHostToDevice, st));
   NSP_CUDA_TRY(c, cudaMemsetAsync(w.w, 0, (size_t)std::max<int64_t>(n, 1) * 8, st));
@@ -341,7 +352,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
     nsp_count_launch();
     k_dot2_partial<<<nb, RT, 0, st>>>(w.f, w.f, nullptr, nullptr, n, w.part);
     nsp_count_launch();
-    k_dot_reduce<<<1, RT, 0, st>>>(w.part, (int)nb, w.sc, 4, 2, tol, w.st);
+    k_dot_reduce<<<1, RT, 0, st>>>(w.part, (int)nb, w.sc, 4, 2, tol, w.st, w.hist);
   }
   if ((e = read_st(c, w.st, hs)) != NSP_OK) return e;
   if (rep && rep->hist && rep->hist_cap > 0) rep->hist[0] = hs->relres;
@@ -353,18 +364,69 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
     NSP_CUDA_TRY(c, cudaMemcpyAsync(w.p, w.z, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
     dot(c, w.r, w.z, n, w, 0);
     int cur = 0;
-    for (int it = 0; it < maxit; ++it) {
-      if ((e = apply_into(c, w.p, 1, w.q, 1, 1, 1, w.apply_wvu)) != NSP_OK) return e;   // q = S_G p
+    // one iteration, enqueued; stops itself on the device once st->done is set (converged, p^T S p
+    // <= 0, non-finite, or maxit), so PCG_CHUNK iterations run between host status checks and the
+    // chunk is one cached CUDA graph (single rank, no profiling, NSP_GRAPH != 0)
+    auto iteration = [&](cudaStream_t q) -> nsp_status {
+      nsp_status e2;
+      if ((e2 = apply_into(c, w.p, 1, w.q, 1, 1, 1, w.apply_wvu)) != NSP_OK) return e2;   // q = S_G p
       dot(c, w.p, w.q, n, w, 2);
       const unsigned nb = nblk_of(n);
       nsp_count_launch();
-      k_pcg_xr<<<nb, RT, 0, st>>>(w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, w.st);
+      k_pcg_xr<<<nb, RT, 0, q>>>(w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, w.st);
       nsp_count_launch();
-      k_dot_reduce<<<1, RT, 0, st>>>(w.part, (int)nb, w.sc, 3, 1, tol, w.st);
+      k_dot_reduce<<<1, RT, 0, q>>>(w.part, (int)nb, w.sc, 3, 1, tol, w.st, w.hist);
+      if ((e2 = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e2;
+      dot(c, w.r, w.z, n, w, cur ^ 1);
+      nsp_count_launch();
+      k_pcg_p<<<grid1(n, 256), 256, 0, q>>>(w.p, w.z, n, w.sc, cur, w.st);
+      cur ^= 1;
+      return NSP_OK;
+    };
+    const char* genv = getenv("NSP_GRAPH");
+    const bool use_graph = !c->prof_on && !(genv && genv[0] == '0');
+    const PcgKey key{w.w, n, precond, tol, maxit, c->nys_rank, c->d_Z, c->d_ELp, c->nys_gen};
+    double hbuf[PCG_CHUNK];
+    while (true) {
+      if (use_graph) {
+        if (!(c->pcg_graph && c->pcg_key == key)) {
+          if (!c->gstream) NSP_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+          if (c->pcg_graph) {
+            cudaGraphExecDestroy(c->pcg_graph);
+            c->pcg_graph = nullptr;
+          }
+          cudaGraph_t g = nullptr;
+          c->stream = c->gstream;
+          c->capturing = true;
+          const long long l0 = nsp_launch_count();
+          NSP_CUDA_TRY(c, cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeRelaxed));
+          nsp_status ec = NSP_OK;
+          for (int j = 0; j < PCG_CHUNK && ec == NSP_OK; ++j) ec = iteration(c->gstream);
+          cudaError_t ce = cudaStreamEndCapture(c->gstream, &g);
+          c->stream = st;
+          c->capturing = false;
+          c->pcg_graph_kernels = nsp_launch_count() - l0;
+          nsp_count_launches(-c->pcg_graph_kernels);
+          if (ec != NSP_OK) return ec;
+          NSP_CUDA_TRY(c, ce);
+          cudaGraphExec_t gx = nullptr;
+          NSP_CUDA_TRY(c, cudaGraphInstantiate(&gx, g, 0));
+          cudaGraphDestroy(g);
+          c->pcg_graph = gx;
+          c->pcg_key = key;
+        }
+        NSP_CUDA_TRY(c, cudaGraphLaunch(c->pcg_graph, st));
+        nsp_count_launches(c->pcg_graph_kernels);
+      } else {
+        for (int j = 0; j < PCG_CHUNK; ++j)
+          if ((e = iteration(st)) != NSP_OK) return e;
+      }
+      NSP_CUDA_TRY(c, cudaMemcpyAsync(hbuf, w.hist, sizeof(hbuf), cudaMemcpyDeviceToHost, st));
       if ((e = read_st(c, w.st, hs)) != NSP_OK) return e;
-      iters = it + 1;
+      for (int it = iters; it < hs->iters; ++it)
+        if (rep && rep->hist && it + 1 < rep->hist_cap) rep->hist[it + 1] = hbuf[it % PCG_CHUNK];
+      iters = hs->iters;
       relres = hs->relres;
-      if (rep && rep->hist && it + 1 < rep->hist_cap) rep->hist[it + 1] = relres;
       if (hs->indefinite) {
         ret = NSP_ERR_INDEFINITE;
         c->err = "nsp_pcg: p^T S_G p <= 0";
@@ -379,11 +441,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
         ret = NSP_OK;
         break;
       }
-      if ((e = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e;
-      dot(c, w.r, w.z, n, w, cur ^ 1);
-      nsp_count_launch();
-      k_pcg_p<<<grid1(n, 256), 256, 0, st>>>(w.p, w.z, n, w.sc, cur);
-      cur ^= 1;
+      if (hs->done || iters >= maxit) break;
     }
   }
   // ---- back-substitution: x_I = A_I^{-1}(b_I - A_IG w), x_G = w, un-permute

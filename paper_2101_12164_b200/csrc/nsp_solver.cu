@@ -679,6 +679,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   c->d_Z = nullptr;
   c->d_sigma = nullptr;
   c->nys_rank = 0;
+  c->nys_gen += 1;   // invalidates the cached PCG graph
   c->h_sigma.clear();
   nsp_status ret = sb == NSP_NOT_CONVERGED ? NSP_NOT_CONVERGED : NSP_OK;
   if (rk > 0) {
