@@ -239,6 +239,9 @@ void nsp_destroy(nsp_ctx* c) {
   comm_free(c);
   if (c->bcg_graph) cudaGraphExecDestroy(c->bcg_graph);
   if (c->pcg_graph) cudaGraphExecDestroy(c->pcg_graph);
+  if (c->bcg_wgraph) cudaGraphExecDestroy(c->bcg_wgraph);
+  if (c->d_bhist) cudaFree(c->d_bhist);
+  if (c->d_bwidth) cudaFree(c->d_bwidth);
   if (c->gstream) cudaStreamDestroy(c->gstream);
   for (DevCSR* m : {&c->A2G, &c->AGG2, &c->AGSH, &c->CB, &c->C1, &c->AII}) {
     fr(m->rowptr);

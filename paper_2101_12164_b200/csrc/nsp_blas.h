@@ -13,6 +13,8 @@ struct BcgStatus {
   int done;       // PCG: the iteration stopped (converged / breakdown / maxit); later kernels no-op
   int iters;      // PCG: iterations taken (device count)
   int maxit;      // PCG: iteration cap
+  int nfallback;  // block CG (device-driven loop): eigen-fallback count
+  int pad_;
   double relres;    // max_j ||R_j|| / ||B_j||
   double scalar[6]; // PCG scalars
 };

@@ -37,8 +37,8 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // acc[i][j][e] <-> C[16*(w>>1) + 8i + g][8*NF*(w&1) + 8j + 2t + e].
 template <int NF, bool TA, bool TB>
 __device__ __forceinline__ void cta_mma(const double* __restrict__ As, int lda, const double* __restrict__ Bs,
-                                        int ldb, double (&acc)[2][NF][2], int K = 64) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                        int ldb, double (&acc)[2][NF][2], int K = 64, int wsel = -1) {
+  const int lane = threadIdx.x & 31, warp = wsel >= 0 ? wsel : (int)(threadIdx.x >> 5);
   const int g = lane >> 2, t = lane & 3;
   const int m0 = (warp >> 1) * 16, n0 = (warp & 1) * NF * 8;
 #pragma unroll 4
@@ -71,13 +71,13 @@ __device__ __forceinline__ void acc_zero(double (&acc)[2][NF][2]) {
 
 // Row / column of accumulator element (i, j, e) for the calling thread.
 template <int NF>
-__device__ __forceinline__ int acc_row(int i) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ int acc_row(int i, int wsel = -1) {
+  const int lane = threadIdx.x & 31, warp = wsel >= 0 ? wsel : (int)(threadIdx.x >> 5);
   return (warp >> 1) * 16 + i * 8 + (lane >> 2);
 }
 template <int NF>
-__device__ __forceinline__ int acc_col(int j) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ int acc_col(int j, int wsel = -1) {
+  const int lane = threadIdx.x & 31, warp = wsel >= 0 ? wsel : (int)(threadIdx.x >> 5);
   return (warp & 1) * NF * 8 + j * 8 + 2 * (lane & 3);
 }
 
@@ -90,5 +90,47 @@ __device__ __forceinline__ void cp_block(double* s, int sld, const double* g, in
     cp_async16(s + r * sld + 2 * q, g + r * gld + 2 * q);
   }
 }
+
+// mbarrier + bulk-copy (TMA, cp.async.bulk) helpers
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_copy(uint64_t* bar, void* dst, const void* src, unsigned bytes) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_add_copy(uint64_t* bar, void* dst, const void* src, unsigned bytes) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(bytes));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W;\n}\n" ::"r"(b),
+               "r"(phase));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
 }  // namespace nspd

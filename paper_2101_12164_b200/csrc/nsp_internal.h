@@ -160,6 +160,16 @@ struct nsp_ctx {
   cudaGraphExec_t bcg_graph = nullptr;
   GraphKey bcg_key;
   long long bcg_graph_kernels = 0;   // kernel nodes per launch of bcg_graph (launch evidence counter)
+  // cached device-driven block-CG loop: one graph whose WHILE node repeats tail + head + loop
+  // control until the device-side stop test fires (one host sync per solve)
+  cudaGraphExec_t bcg_wgraph = nullptr;
+  GraphKey bcg_wkey;
+  int bcg_wmaxit = 0;
+  long long bcg_wbody_kernels = 0;
+  double* d_bhist = nullptr;   // per-iteration relres (device), capacity bhist_cap
+  int* d_bwidth = nullptr;     // per-iteration active width (device)
+  int bhist_cap = 0;
+  bool bcg_no_while = false;   // the WHILE graph could not be built: per-iteration graphs
   // cached CUDA graph of PCG_CHUNK outer-PCG iterations
   cudaGraphExec_t pcg_graph = nullptr;
   PcgKey pcg_key;

@@ -882,31 +882,6 @@ __global__ void __launch_bounds__(256) k_band_fb(const TriSys* __restrict__ sys,
 // quarter of the rows, the 4 partials meet in shared memory.  Same operations in a fixed order.
 // buf (ld 1) holds the right-hand side on entry and the solution on exit.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_copy(uint64_t* bar, void* dst, const void* src, unsigned bytes) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes));
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(bytes), "r"(b)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_add_copy(uint64_t* bar, void* dst, const void* src, unsigned bytes) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(bytes));
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(bytes), "r"(b)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W;\n}\n" ::"r"(b),
-               "r"(phase));
-}
-
 template <int NS, int WBM>
 __global__ void __launch_bounds__(256) k_band_fb_vec(const TriSys* __restrict__ sys, double* buf, int fwd, int bwd) {
   constexpr int NV = WBM + 1;

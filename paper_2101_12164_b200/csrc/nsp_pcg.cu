@@ -251,7 +251,7 @@ static size_t pcg_layout(const nsp_ctx* c, char* base, PcgWs* out) {
   w.hist = take(PCG_CHUNK);
   w.st = (BcgStatus*)take(sizeof(BcgStatus) / 8 + 1);
   if (out) *out = w;
-  return off + 256;
+  return ((off + 255) & ~size_t(255)) + 256;
 }
 
 size_t pcg_ws_bytes(const nsp_ctx* c) { return pcg_layout(c, nullptr, nullptr); }

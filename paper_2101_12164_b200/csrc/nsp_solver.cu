@@ -134,7 +134,7 @@ static size_t bcg_layout(const nsp_ctx* c, int s, char* base, BcgWs* w, int kind
   t.wvu = cv.take(std::max(apply_ws_bytes(c, sp) / 8 + 1, c->has_ag ? ag_ws_doubles(c, sp) : 0));
   t.st = (BcgStatus*)cv.take(sizeof(BcgStatus) / 8 + 1);
   if (w) *w = t;
-  return cv.off + 256;
+  return ((cv.off + 255) & ~size_t(255)) + 256;   // 256-aligned: callers carve more after it
 }
 
 size_t solver_ws_bytes(const nsp_ctx* c, int s) { return bcg_layout(c, s, nullptr, nullptr); }
@@ -221,6 +221,23 @@ static nsp_status op_precond(nsp_ctx* c, BcgWs& w, const double* R, double* Z, i
   return precond(c, R, Z, w.sp, s, w.wvu);
 }
 
+// Device-driven block-CG loop control (end of every iteration of the WHILE-node body): count the
+// iteration, record relres / width / fallback, and stop on the same tests, in the same order, as the
+// host loop (indefinite, non-finite, all directions deflated, converged, maxit).
+__global__ void k_bcg_loop_ctl(BcgStatus* st, double* hist, int* widths, int maxit,
+                               cudaGraphConditionalHandle h) {
+  const int it = ++st->iters;          // completed iterations
+  hist[it] = st->relres;
+  widths[it - 1] = st->width;
+  st->nfallback += st->fallback;
+  const bool stop = st->indefinite || st->nonfinite || st->width == 0 || st->converged || it >= maxit;
+  cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+__global__ void k_bcg_loop_init(BcgStatus* st, int iters) {
+  st->iters = iters;
+  st->nfallback = 0;
+}
+
 nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int ldx, int s, double tol, int maxit,
                          BcgWs& w, nsp_report* rep) {
   const int sp = w.sp;
@@ -253,7 +270,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   double relres = hs->relres;
   double* Zr = usem ? w.Z : w.R;
   // head: a1-a8 (Q = S P, D|E, chol(D), alpha, X/R update, norms, convergence) + the status copy
-  auto head = [&]() -> nsp_status {
+  auto head = [&](bool copy_status) -> nsp_status {
     cudaStream_t q = c->stream;
     nsp_status e2;
     tr.mark("loop");
@@ -281,7 +298,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     }
     nspb::converge(w.rsq, w.bnorm, s, tol, w.st, nullptr, q);
     tr.mark("XR_update");
-    NSP_CUDA_TRY(c, cudaMemcpyAsync(hs, w.st, sizeof(BcgStatus), cudaMemcpyDeviceToHost, q));
+    if (copy_status) NSP_CUDA_TRY(c, cudaMemcpyAsync(hs, w.st, sizeof(BcgStatus), cudaMemcpyDeviceToHost, q));
     NSP_CUDA_TRY(c, cudaGetLastError());
     return NSP_OK;
   };
@@ -318,74 +335,203 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
       if ((e = op_precond(c, w, w.R, w.Z, s)) != NSP_OK) return e;
     }
     if ((e = orth(c, w, Zr, s, w.P)) != NSP_OK) return e;
-    for (int it = 0; it < maxit; ++it) {
-      if (it == 0 || !use_graph) {
-        if (it > 0 && (e = tail()) != NSP_OK) return e;
-        if ((e = head()) != NSP_OK) return e;
-      } else {
-        if (!gexec) {
-          if (!c->gstream) NSP_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
-          if (c->bcg_graph) {
-            cudaGraphExecDestroy(c->bcg_graph);
-            c->bcg_graph = nullptr;
+    // device-driven loop (default; NSP_GRAPH=1 keeps the per-iteration graph, profiling and tracing
+    // use it too): iteration 0 eagerly, then ONE graph launch whose WHILE node runs tail + head +
+    // k_bcg_loop_ctl until the stop test fires
+    const bool use_while = use_graph && !c->prof_on && !(genv && genv[0] == '1') && maxit > 1;
+    bool stop = false;
+    auto run_iters = [&](int it0, int it1) -> nsp_status {
+      nsp_status e;
+      for (int it = it0; it < it1; ++it) {
+        if (it == 0 || !use_graph) {
+          if (it > 0 && (e = tail()) != NSP_OK) return e;
+          if ((e = head(true)) != NSP_OK) return e;
+        } else {
+          if (!gexec) {
+            if (!c->gstream) NSP_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+            if (c->bcg_graph) {
+              cudaGraphExecDestroy(c->bcg_graph);
+              c->bcg_graph = nullptr;
+            }
+            cudaGraph_t g = nullptr;
+            c->stream = c->gstream;
+            c->capturing = true;
+            c->gprof_in_graph = false;
+            const long long l0 = nsp_launch_count();
+            NSP_CUDA_TRY(c, cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeRelaxed));
+            nsp_status ec = tail();
+            if (ec == NSP_OK) ec = head(true);
+            cudaError_t ce = cudaStreamEndCapture(c->gstream, &g);
+            c->stream = st;
+            c->capturing = false;
+            c->bcg_graph_kernels = nsp_launch_count() - l0;   // captured, not executed
+            nsp_count_launches(-c->bcg_graph_kernels);
+            if (ec != NSP_OK) return ec;
+            NSP_CUDA_TRY(c, ce);
+            NSP_CUDA_TRY(c, cudaGraphInstantiate(&gexec, g, 0));
+            cudaGraphDestroy(g);
+            c->bcg_graph = gexec;
+            c->bcg_key = GraphKey{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau};
           }
-          cudaGraph_t g = nullptr;
-          c->stream = c->gstream;
-          c->capturing = true;
-          c->gprof_in_graph = false;
-          const long long l0 = nsp_launch_count();
-          NSP_CUDA_TRY(c, cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeRelaxed));
-          nsp_status ec = tail();
-          if (ec == NSP_OK) ec = head();
-          cudaError_t ce = cudaStreamEndCapture(c->gstream, &g);
-          c->stream = st;
-          c->capturing = false;
-          c->bcg_graph_kernels = nsp_launch_count() - l0;   // captured, not executed
-          nsp_count_launches(-c->bcg_graph_kernels);
-          if (ec != NSP_OK) return ec;
-          NSP_CUDA_TRY(c, ce);
-          NSP_CUDA_TRY(c, cudaGraphInstantiate(&gexec, g, 0));
-          cudaGraphDestroy(g);
-          c->bcg_graph = gexec;
-          c->bcg_key = GraphKey{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau};
+          NSP_CUDA_TRY(c, cudaGraphLaunch(gexec, st));
+          nsp_count_launches(c->bcg_graph_kernels);
         }
-        NSP_CUDA_TRY(c, cudaGraphLaunch(gexec, st));
-        nsp_count_launches(c->bcg_graph_kernels);
+        NSP_CUDA_TRY(c, cudaStreamSynchronize(st));
+        if (it > 0 && use_graph && c->prof_on && c->gprof_in_graph) {
+          float ms = 0.f;
+          NSP_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->gprof_ev[0], c->gprof_ev[1]));
+          c->gprof_ms += ms;
+          c->gprof_n += 1;
+        }
+        tr.mark("sync");
+        iters = it + 1;
+        fallbacks += hs->fallback;
+        relres = hs->relres;
+        if (rep && rep->hist && it + 1 < rep->hist_cap) rep->hist[it + 1] = hs->relres;
+        if (rep && rep->widths && it < rep->widths_cap) rep->widths[it] = hs->width;
+        if (hs->indefinite) {
+          ret = NSP_ERR_INDEFINITE;
+          c->err = "nsp_block_cg: chol(P^T S P) failed (S_G not SPD on the search space)";
+          stop = true;
+          return NSP_OK;
+        }
+        if (hs->nonfinite) {
+          ret = NSP_ERR_NUMERICAL;
+          c->err = "nsp_block_cg: non-finite residual";
+          stop = true;
+          return NSP_OK;
+        }
+        if (hs->width == 0) {
+          ret = NSP_ERR_STAGNATION;
+          c->err = "nsp_block_cg: all search directions deflated";
+          stop = true;
+          return NSP_OK;
+        }
+        if (hs->converged) {
+          ret = NSP_OK;
+          stop = true;
+          return NSP_OK;
+        }
       }
+      return NSP_OK;
+    };
+    if ((e = run_iters(0, use_while ? 1 : maxit)) != NSP_OK) return e;
+    if (use_while && !stop && c->bcg_no_while) {
+      if ((e = run_iters(1, maxit)) != NSP_OK) return e;
+    } else if (use_while && !stop) {
+      if (c->bhist_cap < maxit + 1) {
+        if (c->d_bhist) cudaFree(c->d_bhist);
+        if (c->d_bwidth) cudaFree(c->d_bwidth);
+        c->d_bhist = nullptr;
+        c->d_bwidth = nullptr;
+        c->bhist_cap = 0;
+        NSP_CUDA_TRY(c, cudaMalloc(&c->d_bhist, (size_t)(maxit + 1) * sizeof(double)));
+        NSP_CUDA_TRY(c, cudaMalloc(&c->d_bwidth, (size_t)(maxit + 1) * sizeof(int)));
+        c->bhist_cap = maxit + 1;
+        if (c->bcg_wgraph) {   // baked-in pointers changed
+          cudaGraphExecDestroy(c->bcg_wgraph);
+          c->bcg_wgraph = nullptr;
+        }
+      }
+      const GraphKey key{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau};
+      // build (or reuse) the WHILE graph; any CUDA error while building it (a node type the
+      // conditional body does not support) falls back to the per-iteration graph for good
+      auto build_while = [&]() -> cudaError_t {
+        if (c->bcg_wgraph) {
+          cudaGraphExecDestroy(c->bcg_wgraph);
+          c->bcg_wgraph = nullptr;
+        }
+        cudaError_t ce;
+        if (!c->gstream && (ce = cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking)) != cudaSuccess) return ce;
+        cudaGraph_t g = nullptr;
+        if ((ce = cudaGraphCreate(&g, 0)) != cudaSuccess) return ce;
+        cudaGraphConditionalHandle hcond;
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t wnode;
+        if ((ce = cudaGraphConditionalHandleCreate(&hcond, g, 1, cudaGraphCondAssignDefault)) != cudaSuccess ||
+            (np.conditional.handle = hcond, ce = cudaGraphAddNode(&wnode, g, nullptr, 0, &np)) != cudaSuccess) {
+          cudaGraphDestroy(g);
+          return ce;
+        }
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        if ((ce = cudaStreamBeginCaptureToGraph(c->gstream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) !=
+            cudaSuccess) {
+          cudaGraphDestroy(g);
+          return ce;
+        }
+        c->stream = c->gstream;
+        c->capturing = true;
+        const long long l0 = nsp_launch_count();
+        nsp_status ec = tail();
+        if (ec == NSP_OK) ec = head(false);
+        if (ec == NSP_OK) {
+          nsp_count_launch();
+          k_bcg_loop_ctl<<<1, 1, 0, c->gstream>>>(w.st, c->d_bhist, c->d_bwidth, maxit, hcond);
+        }
+        cudaGraph_t gout = nullptr;
+        const cudaError_t ce2 = cudaStreamEndCapture(c->gstream, &gout);
+        c->stream = st;
+        c->capturing = false;
+        c->bcg_wbody_kernels = nsp_launch_count() - l0;
+        nsp_count_launches(-c->bcg_wbody_kernels);
+        if (ec != NSP_OK || ce2 != cudaSuccess) {
+          cudaGraphDestroy(g);
+          return ce2 != cudaSuccess ? ce2 : cudaErrorUnknown;
+        }
+        cudaGraphExec_t gx = nullptr;
+        ce = cudaGraphInstantiate(&gx, g, 0);
+        cudaGraphDestroy(g);
+        if (ce != cudaSuccess) return ce;
+        c->bcg_wgraph = gx;
+        c->bcg_wkey = key;
+        c->bcg_wmaxit = maxit;
+        return cudaSuccess;
+      };
+      if (!(c->bcg_wgraph && c->bcg_wkey == key && c->bcg_wmaxit == maxit) && build_while() != cudaSuccess) {
+        (void)cudaGetLastError();
+        c->bcg_no_while = true;
+        if (c->opts.verbose) fprintf(stderr, "[nsp] device-driven block-CG loop unavailable; per-iteration graphs\n");
+        if ((e = run_iters(1, maxit)) != NSP_OK) return e;
+        goto copy_out;
+      }
+      nsp_count_launch();
+      k_bcg_loop_init<<<1, 1, 0, st>>>(w.st, 1);
+      NSP_CUDA_TRY(c, cudaGraphLaunch(c->bcg_wgraph, st));
+      NSP_CUDA_TRY(c, cudaMemcpyAsync(hs, w.st, sizeof(BcgStatus), cudaMemcpyDeviceToHost, st));
       NSP_CUDA_TRY(c, cudaStreamSynchronize(st));
-      if (it > 0 && use_graph && c->prof_on && c->gprof_in_graph) {
-        float ms = 0.f;
-        NSP_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->gprof_ev[0], c->gprof_ev[1]));
-        c->gprof_ms += ms;
-        c->gprof_n += 1;
+      const int done = hs->iters;   // >= 2
+      nsp_count_launches(c->bcg_wbody_kernels * (long long)(done - 1));
+      if (rep && rep->hist && rep->hist_cap > 2) {
+        const int m = std::min(done, rep->hist_cap - 1) - 1;   // entries 2 .. min(done, cap-1)
+        if (m > 0) NSP_CUDA_TRY(c, cudaMemcpy(rep->hist + 2, c->d_bhist + 2, (size_t)m * sizeof(double),
+                                              cudaMemcpyDeviceToHost));
       }
-      tr.mark("sync");
-      iters = it + 1;
-      fallbacks += hs->fallback;
+      if (rep && rep->widths && rep->widths_cap > 1) {
+        const int m = std::min(done, rep->widths_cap) - 1;     // entries 1 .. min(done, cap) - 1
+        if (m > 0) NSP_CUDA_TRY(c, cudaMemcpy(rep->widths + 1, c->d_bwidth + 1, (size_t)m * sizeof(int),
+                                              cudaMemcpyDeviceToHost));
+      }
+      iters = done;
+      fallbacks += hs->nfallback;
       relres = hs->relres;
-      if (rep && rep->hist && it + 1 < rep->hist_cap) rep->hist[it + 1] = hs->relres;
-      if (rep && rep->widths && it < rep->widths_cap) rep->widths[it] = hs->width;
       if (hs->indefinite) {
         ret = NSP_ERR_INDEFINITE;
         c->err = "nsp_block_cg: chol(P^T S P) failed (S_G not SPD on the search space)";
-        break;
-      }
-      if (hs->nonfinite) {
+      } else if (hs->nonfinite) {
         ret = NSP_ERR_NUMERICAL;
         c->err = "nsp_block_cg: non-finite residual";
-        break;
-      }
-      if (hs->width == 0) {
+      } else if (hs->width == 0) {
         ret = NSP_ERR_STAGNATION;
         c->err = "nsp_block_cg: all search directions deflated";
-        break;
-      }
-      if (hs->converged) {
+      } else if (hs->converged) {
         ret = NSP_OK;
-        break;
       }
     }
   }
+copy_out:
   // copy X out
   nspb::copy_pad(w.X, sp, Xout, ldx, n, s, 1.0, st);
   tr.mark("end");
