@@ -240,6 +240,8 @@ void nsp_destroy(nsp_ctx* c) {
   if (c->bcg_graph) cudaGraphExecDestroy(c->bcg_graph);
   if (c->pcg_graph) cudaGraphExecDestroy(c->pcg_graph);
   if (c->bcg_wgraph) cudaGraphExecDestroy(c->bcg_wgraph);
+  if (c->pcg_wgraph) cudaGraphExecDestroy(c->pcg_wgraph);
+  if (c->d_phist) cudaFree(c->d_phist);
   if (c->d_bhist) cudaFree(c->d_bhist);
   if (c->d_bwidth) cudaFree(c->d_bwidth);
   if (c->gstream) cudaStreamDestroy(c->gstream);

@@ -170,6 +170,13 @@ struct nsp_ctx {
   int* d_bwidth = nullptr;     // per-iteration active width (device)
   int bhist_cap = 0;
   bool bcg_no_while = false;   // the WHILE graph could not be built: per-iteration graphs
+  // cached device-driven PCG loop (WHILE node around two iterations + loop control)
+  cudaGraphExec_t pcg_wgraph = nullptr;
+  PcgKey pcg_wkey;
+  long long pcg_wbody_kernels = 0;
+  double* d_phist = nullptr;
+  int phist_cap = 0;
+  bool pcg_no_while = false;
   // cached CUDA graph of PCG_CHUNK outer-PCG iterations
   cudaGraphExec_t pcg_graph = nullptr;
   PcgKey pcg_key;

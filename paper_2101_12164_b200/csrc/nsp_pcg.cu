@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(RT) k_dot2_partial(const double* __restrict__ 
 // mode 0: out slot = sum (q = 0);   mode 1: out slot = sum (q = 0), status relres / converged from
 // sum = r.r;  mode 2: ||f|| (sqrt of sum) and the initial status.
 __global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ part, int nblk, double* sc, int slot,
-                                                   int mode, double tol, BcgStatus* st, double* hist) {
+                                                   int mode, double tol, BcgStatus* st, double* hist,
+                                                   int hist_mod) {
   __shared__ double red[RT];
   if (mode == 1 && st->done) return;   // read by every thread before thread 0 can write it
   double s = 0.0;
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ pa
     st->converged = rel <= tol ? 1 : 0;
     if (!isfinite(v)) st->nonfinite = 1;
     const int it = ++st->iters;
-    hist[(it - 1) % PCG_CHUNK] = rel;
+    hist[hist_mod > 0 ? (it - 1) % hist_mod : it - 1] = rel;
     st->done = (st->converged || st->nonfinite || st->indefinite || it >= st->maxit) ? 1 : 0;
   } else {
     sc[4] = sqrt(v);
@@ -201,6 +202,11 @@ __global__ void k_gemv_add(const double* __restrict__ Z, int ldz, const double* 
   if (lane == 0) y[row] += s;
 }
 
+// WHILE-node control of the device-driven PCG loop: repeat until the iteration stopped itself
+__global__ void k_pcg_loop_ctl(const BcgStatus* st, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, st->done ? 0u : 1u);
+}
+
 unsigned nblk_of(int64_t n) { return (unsigned)std::max<int64_t>(1, (n + RPB - 1) / RPB); }
 unsigned grid1(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
@@ -262,7 +268,7 @@ static void dot(nsp_ctx* c, const double* a, const double* b, int64_t n, PcgWs& 
   nsp_count_launch();
   k_dot2_partial<<<nb, RT, 0, c->stream>>>(a, b, nullptr, nullptr, n, w.part);
   nsp_count_launch();
-  k_dot_reduce<<<1, RT, 0, c->stream>>>(w.part, (int)nb, w.sc, slot, 0, 0.0, w.st, w.hist);
+  k_dot_reduce<<<1, RT, 0, c->stream>>>(w.part, (int)nb, w.sc, slot, 0, 0.0, w.st, w.hist, PCG_CHUNK);
 }
 
 // z = M r for the PCG preconditioner (0: identity copy, 1: A_G^{-1}, 2: M_2)
@@ -352,7 +358,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
     nsp_count_launch();
     k_dot2_partial<<<nb, RT, 0, st>>>(w.f, w.f, nullptr, nullptr, n, w.part);
     nsp_count_launch();
-    k_dot_reduce<<<1, RT, 0, st>>>(w.part, (int)nb, w.sc, 4, 2, tol, w.st, w.hist);
+    k_dot_reduce<<<1, RT, 0, st>>>(w.part, (int)nb, w.sc, 4, 2, tol, w.st, w.hist, PCG_CHUNK);
   }
   if ((e = read_st(c, w.st, hs)) != NSP_OK) return e;
   if (rep && rep->hist && rep->hist_cap > 0) rep->hist[0] = hs->relres;
@@ -367,6 +373,8 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
     // one iteration, enqueued; stops itself on the device once st->done is set (converged, p^T S p
     // <= 0, non-finite, or maxit), so PCG_CHUNK iterations run between host status checks and the
     // chunk is one cached CUDA graph (single rank, no profiling, NSP_GRAPH != 0)
+    double* hist_dev = w.hist;   // PCG_CHUNK ring (chunk path) or the full history (WHILE graph)
+    int hist_mod = PCG_CHUNK;
     auto iteration = [&](cudaStream_t q) -> nsp_status {
       nsp_status e2;
       if ((e2 = apply_into(c, w.p, 1, w.q, 1, 1, 1, w.apply_wvu)) != NSP_OK) return e2;   // q = S_G p
@@ -375,7 +383,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
       nsp_count_launch();
       k_pcg_xr<<<nb, RT, 0, q>>>(w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, w.st);
       nsp_count_launch();
-      k_dot_reduce<<<1, RT, 0, q>>>(w.part, (int)nb, w.sc, 3, 1, tol, w.st, w.hist);
+      k_dot_reduce<<<1, RT, 0, q>>>(w.part, (int)nb, w.sc, 3, 1, tol, w.st, hist_dev, hist_mod);
       if ((e2 = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e2;
       dot(c, w.r, w.z, n, w, cur ^ 1);
       nsp_count_launch();
@@ -387,7 +395,109 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
     const bool use_graph = !c->prof_on && !(genv && genv[0] == '0');
     const PcgKey key{w.w, n, precond, tol, maxit, c->nys_rank, c->d_Z, c->d_ELp, c->nys_gen};
     double hbuf[PCG_CHUNK];
-    while (true) {
+    // device-driven loop (default): ONE launch of a graph whose WHILE node repeats the iteration
+    // until st->done; the chunked graph below is the fallback (and NSP_GRAPH=1)
+    bool loop_done = false;
+    if (use_graph && !(genv && genv[0] == '1') && !c->pcg_no_while) {
+      if (c->phist_cap < maxit + 1) {
+        if (c->d_phist) cudaFree(c->d_phist);
+        c->d_phist = nullptr;
+        c->phist_cap = 0;
+        NSP_CUDA_TRY(c, cudaMalloc(&c->d_phist, (size_t)(maxit + 1) * sizeof(double)));
+        c->phist_cap = maxit + 1;
+        if (c->pcg_wgraph) {
+          cudaGraphExecDestroy(c->pcg_wgraph);
+          c->pcg_wgraph = nullptr;
+        }
+      }
+      auto build_while = [&]() -> cudaError_t {
+        if (c->pcg_wgraph) {
+          cudaGraphExecDestroy(c->pcg_wgraph);
+          c->pcg_wgraph = nullptr;
+        }
+        cudaError_t ce;
+        if (!c->gstream && (ce = cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking)) != cudaSuccess) return ce;
+        cudaGraph_t g = nullptr;
+        if ((ce = cudaGraphCreate(&g, 0)) != cudaSuccess) return ce;
+        cudaGraphConditionalHandle hcond;
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t wnode;
+        if ((ce = cudaGraphConditionalHandleCreate(&hcond, g, 1, cudaGraphCondAssignDefault)) != cudaSuccess ||
+            (np.conditional.handle = hcond, ce = cudaGraphAddNode(&wnode, g, nullptr, 0, &np)) != cudaSuccess) {
+          cudaGraphDestroy(g);
+          return ce;
+        }
+        if ((ce = cudaStreamBeginCaptureToGraph(c->gstream, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                cudaStreamCaptureModeRelaxed)) != cudaSuccess) {
+          cudaGraphDestroy(g);
+          return ce;
+        }
+        c->stream = c->gstream;
+        c->capturing = true;
+        hist_dev = c->d_phist;
+        hist_mod = 0;
+        const int cur0 = cur;
+        const long long l0 = nsp_launch_count();
+        nsp_status ec = iteration(c->gstream);
+        if (ec == NSP_OK) ec = iteration(c->gstream);   // two per body: the r.z ping-pong returns to cur0
+        if (ec == NSP_OK) {
+          nsp_count_launch();
+          k_pcg_loop_ctl<<<1, 1, 0, c->gstream>>>(w.st, hcond);
+        }
+        cur = cur0;
+        hist_dev = w.hist;
+        hist_mod = PCG_CHUNK;
+        cudaGraph_t gout = nullptr;
+        const cudaError_t ce2 = cudaStreamEndCapture(c->gstream, &gout);
+        c->stream = st;
+        c->capturing = false;
+        c->pcg_wbody_kernels = nsp_launch_count() - l0;
+        nsp_count_launches(-c->pcg_wbody_kernels);
+        if (ec != NSP_OK || ce2 != cudaSuccess) {
+          cudaGraphDestroy(g);
+          return ce2 != cudaSuccess ? ce2 : cudaErrorUnknown;
+        }
+        cudaGraphExec_t gx = nullptr;
+        ce = cudaGraphInstantiate(&gx, g, 0);
+        cudaGraphDestroy(g);
+        if (ce != cudaSuccess) return ce;
+        c->pcg_wgraph = gx;
+        c->pcg_wkey = key;
+        return cudaSuccess;
+      };
+      if (!(c->pcg_wgraph && c->pcg_wkey == key) && build_while() != cudaSuccess) {
+        (void)cudaGetLastError();
+        c->pcg_no_while = true;
+      } else {
+        NSP_CUDA_TRY(c, cudaGraphLaunch(c->pcg_wgraph, st));
+        if ((e = read_st(c, w.st, hs)) != NSP_OK) return e;
+        const int done = hs->iters;
+        // kernels actually run: two iterations per body pass (the second a no-op pass when the
+        // first stopped); count the body per pass
+        nsp_count_launches(c->pcg_wbody_kernels * (long long)((done + 2) / 2));
+        if (rep && rep->hist && rep->hist_cap > 1) {
+          const int m = std::min(done, rep->hist_cap - 1);
+          if (m > 0) NSP_CUDA_TRY(c, cudaMemcpy(rep->hist + 1, c->d_phist, (size_t)m * sizeof(double),
+                                                cudaMemcpyDeviceToHost));
+        }
+        iters = done;
+        relres = hs->relres;
+        if (hs->indefinite) {
+          ret = NSP_ERR_INDEFINITE;
+          c->err = "nsp_pcg: p^T S_G p <= 0";
+        } else if (hs->nonfinite) {
+          ret = NSP_ERR_NUMERICAL;
+          c->err = "nsp_pcg: non-finite residual";
+        } else if (hs->converged) {
+          ret = NSP_OK;
+        }
+        loop_done = true;
+      }
+    }
+    while (!loop_done) {
       if (use_graph) {
         if (!(c->pcg_graph && c->pcg_key == key)) {
           if (!c->gstream) NSP_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
