@@ -21,6 +21,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import numpy as np
+import scipy.linalg as sla
 
 from .bcg import bf_bcg
 from .schur import SchurOracle
@@ -120,3 +121,53 @@ def apply_ADEF2(S: SchurOracle, Z: np.ndarray, r: np.ndarray) -> np.ndarray:
     E = Z.T @ S.apply(Z)
     E = 0.5 * (E + E.T)
     return t + Z @ np.linalg.solve(E, Z.T @ (r - S.apply(t)))
+
+
+def chol_R_gamma(S: SchurOracle) -> np.ndarray:
+    """R_G: the upper Cholesky factor of A_G = R_G^T R_G (eq:cholesky PAPER.md:443-446) in the Gamma
+    order of the DBBD (dense; oracle sizes)."""
+    return np.linalg.cholesky(S.d.A_G.toarray()).T
+
+
+def nystrom_m1(S: SchurOracle, Omega: np.ndarray, k: int, tol_inner: float = 0.1, maxit_inner: int = 1000,
+               precond: str = "none", tau: float = 1e-14, eps_rel: float = 1e-12, exact_inner: bool = False,
+               q: int = 0) -> NystromResult:
+    """M_1 (eq:prec1S PAPER.md:846-852).  Alg. 1's Nystrom steps applied to the operator
+    R_G^{-T} A_GI S_I^{-1} A_IG R_G^{-1} ~ U Sigma U^T (eq:lr_approximation_S-1_A-I PAPER.md:836-840),
+    R_G the A_G Cholesky factor (chol_R_gamma); Omega lives in R_G's row space.  The operator is applied
+    as R_G^{-T} B_H R_G^{-1} with B_H = A_GI S_I^{-1} A_IG through the border system (reading C1,
+    apply_BH).  Then Z = R_G^{-1} U (eq:prec1S "Z_k = R_G^{-1} U_k") and
+    M_1 r = A_G^{-1} r + Z Sigma Z^T r - the form of apply_M2 with this (Z, Sigma)."""
+    R = chol_R_gamma(S)
+    G = Omega
+    its = []
+
+    def op(Gx):
+        Yp, info = apply_BH(S, sla.solve_triangular(R, Gx, lower=False), tol_inner, maxit_inner, precond, tau,
+                            exact_inner)
+        return sla.solve_triangular(R, Yp, trans="T", lower=False), info
+
+    for _ in range(q):                                    # power steps (eq:power) on the same operator
+        Yp, info = op(G)
+        its.append(info["iters"])
+        G = orthonormalize(Yp)
+    Y, info = op(G)
+    its.append(info["iters"])
+    info = dict(info, iters=sum(its), iters_each=its)
+    U, sigma, rC = nystrom_from_Y(G, Y, k, eps_rel)
+    status = 0 if rC > 0 else NSP_ERR_RANK_COLLAPSE
+    Z = sla.solve_triangular(R, U, lower=False) if U.shape[1] else U
+    return NystromResult(Z, sigma, U, U.shape[1], info, status)
+
+
+def apply_M1(S: SchurOracle, Z: np.ndarray, sigma: np.ndarray, r: np.ndarray) -> np.ndarray:
+    """eq:prec1S: M_1 r = R_G^{-1} (I + U Sigma U^T) R_G^{-T} r = A_G^{-1} r + Z Sigma Z^T r, Z = R_G^{-1} U."""
+    return apply_M2(S, Z, sigma, r)
+
+
+def apply_ADEF1(S: SchurOracle, Z: np.ndarray, r: np.ndarray) -> np.ndarray:
+    """M_A-DEF1 = R_G^{-1} P_A-DEF1 R_G^{-T} (eq:deflation_comp_from_low_rank PAPER.md:871-886,
+    eq:our_two_level_preconditioner PAPER.md:887-893) with Q = U E^{-1} U^T, E = U^T R_G^{-T} S_G R_G^{-1} U:
+    since R_G^{-1} R_G^{-T} = A_G^{-1} and R_G^{-1} U = Z,
+    M r = A_G^{-1} r + Z E^{-1} Z^T (r - S_G A_G^{-1} r), E = Z^T S_G Z - apply_ADEF2's form on M_1's Z."""
+    return apply_ADEF2(S, Z, r)

@@ -477,3 +477,74 @@ def test_m3_exact_gives_one_pcg_iteration():
     b = philox.gaussian(5, 1, A.n)
     x, info = O.solve_full_system(S, b, 1e-10, 50, lambda v: apply_M2(S, r.Z, r.sigma, v))
     assert info["iters"] <= 1 + 1 and np.allclose(x, np.linalg.solve(A.to_scipy().toarray(), b), atol=1e-9)
+
+
+def test_rt_s_inverse_r_identity():
+    """eq:Rt_S-1_R: R_G S_G^{-1} R_G^T = I + R_G^{-T} A_GI S_I^{-1} A_IG R_G^{-1}, checked
+    with dense matrices built by elimination (independent of the Nystrom code), and the eigenvalue map
+    stated below it: (lambda, u) of R_G^{-T} S_G R_G^{-1} <-> (1/lambda - 1, u)."""
+    import scipy.linalg as sl
+    from oracle.nystrom import chol_R_gamma
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    Sd = S.dense()
+    R = chol_R_gamma(S)
+    assert np.allclose(R.T @ R, d.A_G.toarray(), atol=1e-12)
+    A = pr.A.to_scipy().toarray()
+    perm = d.perm
+    Ap = A[np.ix_(perm, perm)]
+    nI = A.shape[0] - d.n_gamma
+    AI, AIG, AGI = Ap[:nI, :nI], Ap[:nI, nI:], Ap[nI:, :nI]
+    SI = AI - AIG @ np.linalg.solve(d.A_G.toarray(), AGI)          # eq:SI
+    Ri = np.linalg.inv(R)
+    lhs = R @ np.linalg.solve(Sd, R.T)
+    rhs = np.eye(d.n_gamma) + Ri.T @ AGI @ np.linalg.solve(SI, AIG) @ Ri
+    assert np.allclose(lhs, rhs, atol=1e-9 * np.abs(lhs).max())
+    lam = np.sort(np.linalg.eigvalsh(Ri.T @ Sd @ Ri))
+    mu = np.sort(np.linalg.eigvalsh(0.5 * (rhs + rhs.T) - np.eye(d.n_gamma)))
+    assert np.allclose(np.sort(1.0 / lam - 1.0), mu, rtol=1e-8, atol=1e-10)
+
+
+def test_m1_full_rank_closed_form_and_exact():
+    """M_1 (eq:prec1S): with s = n_G and an exact inner solve the Nystrom approximation of
+    R_G^{-T} A_GI S_I^{-1} A_IG R_G^{-1} is its EVD, so Sigma equals 1/lambda - 1 for the generalized
+    eigenvalues S_G v = lambda A_G v (eq:GEVP; the map below eq:Rt_S-1_R) and M_1 = S_G^{-1}
+    (M_1 S_G = I)."""
+    import scipy.linalg as sl
+    from oracle.nystrom import apply_M1
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    n = d.n_gamma
+    Om = philox.gaussian_block(3, 0, n, n)
+    r = O.nystrom_m1(S, Om, n, exact_inner=True)
+    lam = sl.eigh(S.dense(), d.A_G.toarray(), eigvals_only=True)   # ascending
+    ref = np.sort(1.0 / lam - 1.0)[::-1]
+    keep = ref > 1e-12 * ref[0]
+    assert r.rank >= keep.sum() - 1
+    m = min(r.rank, int(keep.sum()))
+    assert np.allclose(r.sigma[:m], ref[:m], rtol=1e-7, atol=1e-9 * ref[0])
+    Sd = S.dense()
+    MS = apply_M1(S, r.Z, r.sigma, Sd)
+    assert np.allclose(MS, np.eye(n), atol=1e-7)
+
+
+def test_m1_low_rank_matches_adef1_deflation():
+    """M_A-DEF1 (eq:deflation_comp_from_low_rank / eq:our_two_level_preconditioner) built on an exact
+    truncated EVD (s = n_G, exact inner solve, k < n_G): the preconditioned operator maps span(Z) onto
+    itself identically (P_A-DEF A Z = Z), while M_1 maps it to Z (I + Sigma) / (1 + Sigma) = Z too
+    (the adapted-deflation property stated after eq:prec1S)."""
+    from oracle.nystrom import apply_ADEF1, apply_M1
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    n = d.n_gamma
+    Om = philox.gaussian_block(4, 0, n, n)
+    r = O.nystrom_m1(S, Om, 10, exact_inner=True)
+    assert r.rank == 10
+    Sd = S.dense()
+    MS1 = apply_M1(S, r.Z, r.sigma, Sd @ r.Z)
+    MSd = apply_ADEF1(S, r.Z, Sd @ r.Z)
+    assert np.allclose(MS1, r.Z, atol=1e-8 * np.abs(r.Z).max())
+    assert np.allclose(MSd, r.Z, atol=1e-8 * np.abs(r.Z).max())
