@@ -88,7 +88,15 @@ typedef struct {
                             2 = M_3: Nystrom of S_I^{-1} itself (eq:internal_term_lr_approximation_2,
                             eq:left_prec_mat2): Y = S_I^{-1} Omega_I by block PCG, Z = A_G^{-1} A_GI V,
                             Omega is then n x (rank + oversample) in ORIGINAL order (interior rows used),
-                            no power steps */
+                            no power steps;
+                            3 = M_1 (eq:prec1S): Nystrom of R_G^{-T} A_GI S_I^{-1} A_IG
+                            R_G^{-1} (eq:lr_approximation_S-1_A-I) with R_G the A_G Cholesky factor of
+                            the setup (ordering: ag_order), Z = R_G^{-1} U; Omega is n_gamma x s in
+                            R_G's row order (the Gamma order when ag_order = 1); power steps allowed.
+                            nsp_pcg precond 2 / 3 then apply M_1 / M_A-DEF1 */
+  int ag_order;          /* ordering of the A_G factor (factor_gamma): 0 = reverse Cuthill-McKee band
+                            (default); 1 = the natural Gamma order (nsp_gamma_index), so that
+                            R_G = chol(A_G) exactly as written (dense-ish band: small n_G only) */
 } nsp_opts;
 
 /* Solver / setup report; caller-owned.  hist / widths are optional caller
@@ -186,7 +194,9 @@ nsp_status nsp_nystrom(nsp_ctx* ctx, int rank, int oversample, const double* Ome
                        int maxit_inner, void* ws, nsp_report* rep);
 /* sigma: host double[>= rank]; rank_out: approximation rank. */
 nsp_status nsp_nystrom_sigma(const nsp_ctx* ctx, double* sigma, int* rank_out);
-/* Y = M X for M in {0: identity, 1: A_G^{-1}, 2: M_2}; device n_gamma_local x s. */
+/* Y = M X for M in {0: identity, 1: A_G^{-1}, 2: M_2 (M_1 / M_3 after nys_form 3 / 2),
+ * 3: R_G^{-T} (X in the Gamma order, Y in R_G's row order), 4: R_G^{-1} (X in R_G's row order, Y in the
+ * Gamma order)}, A_G = R_G^T R_G the setup's A_G factor (opts.ag_order); device n_gamma_local x s. */
 nsp_status nsp_precond_apply(nsp_ctx* ctx, int which, const double* X, double* Y, int s, void* ws);
 
 /* Full solve A x = b through eq:A_LDLT: f = b_G - A_GI A_I^{-1} b_I; PCG on

@@ -191,7 +191,13 @@ static nsp_status setup_gamma_factor(nsp_ctx* c, const nsp_csr* A, const int32_t
     }
     arp[g + 1] = (int)aci.size();
   }
-  std::vector<int> ord = rcm_order((int)nG, arp, aci);
+  std::vector<int> ord;
+  if (c->opts.ag_order == 1) {   // natural Gamma order: R_G = chol(A_G) as written (M_1 parity, small n_G)
+    ord.resize(nG);
+    for (int64_t k = 0; k < nG; ++k) ord[k] = (int)k;
+  } else {
+    ord = rcm_order((int)nG, arp, aci);
+  }
   std::vector<int> pos(nG);
   for (int64_t k = 0; k < nG; ++k) pos[ord[k]] = (int)k;
   const int bw = bandwidth((int)nG, arp, aci, pos);
@@ -454,6 +460,8 @@ static nsp_status validate_inputs(nsp_ctx* c, const nsp_csr* A, const int32_t* p
   const double* va = A->val;
   if (n <= 0 || !rp || !ci || !va) return fail(c, NSP_ERR_ARG, "nsp_setup: empty or null CSR");
   if (rp[0] != 0) return fail(c, NSP_ERR_ARG, "nsp_setup: rowptr[0] != 0");
+  if (c->opts.ag_order < 0 || c->opts.ag_order > 1) return fail(c, NSP_ERR_ARG, "nsp_setup: ag_order must be 0 or 1");
+  if (c->opts.nys_form < 0 || c->opts.nys_form > 3) return fail(c, NSP_ERR_ARG, "nsp_setup: nys_form must be 0..3");
   // ---------------- validation
   std::string verr;
   int64_t bad_row = -1;

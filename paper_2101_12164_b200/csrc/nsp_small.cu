@@ -32,6 +32,20 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
   return r;
 }
 
+#ifdef NSP_CHOL_PROF
+__device__ long long g_chol_prof[128];
+#define CPROF(i) \
+  if (threadIdx.x == 0) g_chol_prof[i] = clock64();
+#else
+#define CPROF(i)
+#endif
+#ifdef NSP_CHOL_PROF
+#define WPROF(k) \
+  if (lane == 0 && c0 == 16) g_chol_prof[64 + (k)] = clock64();
+#else
+#define WPROF(k)
+#endif
+
 // One warp: factor the 16 x 16 diagonal block at (c0, c0) of As in place (lower = L), write
 // X = L^{-1} (16 x 16 row-major, lower) to Xd and the pivots (before the square root) to piv.  A
 // non-positive pivot is replaced by 1 (deterministic continuation) and reported by `false`.
@@ -40,6 +54,7 @@ __device__ __noinline__ bool warp_chol16(double* As, int c0, double* Xd, double*
   const int lane = threadIdx.x & 31;
   const int r = lane >> 1, h = lane & 1;
   double* B = As + c0 * LDA + c0;
+  WPROF(0)
   double v[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -47,6 +62,7 @@ __device__ __noinline__ bool warp_chol16(double* As, int c0, double* Xd, double*
     v[q] = (j <= r) ? B[r * LDA + j] : 0.0;
   }
   bool ok = true;
+  WPROF(1)
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
     const int hc = c >> 3, qc = c & 7;
@@ -79,6 +95,7 @@ __device__ __noinline__ bool warp_chol16(double* As, int c0, double* Xd, double*
     if (j <= r) B[r * LDA + j] = v[q];
   }
   __syncwarp();
+  WPROF(2)
   // X = L^{-1} by 8 x 8 blocks: lanes 0-7 / 8-15 invert L11 / L22 (one column each), then
   // X21 = -X22 (L21 X11) on all 32 lanes (two entries each)
   if (lane < 16) {
@@ -124,19 +141,13 @@ __device__ __noinline__ bool warp_chol16(double* As, int c0, double* Xd, double*
     Xd[(8 + i) * 16 + jj + 1] = -x1;
   }
   __syncwarp();
+  WPROF(3)
   return ok;
 }
 
-#ifdef NSP_CHOL_PROF
-__device__ long long g_chol_prof[64];
-#define CPROF(i) \
-  if (threadIdx.x == 0) g_chol_prof[i] = clock64();
-#else
-#define CPROF(i)
-#endif
 
 // Output Lp (sp x sp): strictly-lower off-diagonal blocks = L, diagonal 16 x 16 blocks = X_kk
-// (lower), upper = 0.  Rows / cols >= nact (nact < 0: st->width) are replaced by the identity.
+// (lower, zero above the diagonal); the strictly-upper 16 x 16 blocks are NOT written.  Rows / cols >= nact (nact < 0: st->width) are replaced by the identity.
 //  mode 0: a pivot <= 0 -> st->indefinite.
 //  mode 1: pivot test min d_i > tau max d_i over i < nact (reading C3), else st->fallback = 1;
 //          success: st->fallback = 0, st->width = nact.
@@ -254,9 +265,11 @@ __global__ void __launch_bounds__(256) k_chol16(const double* __restrict__ Ain, 
   }
   // output, two doubles per thread per step (sp is 64 or 128: shifts, no division)
   const int lsp = sp == 128 ? 7 : 6;
+#pragma unroll 8
   for (int e = 2 * tid; e < sp * sp; e += 512) {
     const int i = e >> lsp, j = e & (sp - 1);
     const int bi = i >> 4, bj = j >> 4;
+    if (bi < bj) continue;   // strictly-upper blocks are never read (k_chol_solve zero-fills them)
     double2 v = make_double2(0.0, 0.0);
     if (bi == bj) {
       const double* xr = Di + bi * 256 + (i & 15) * 16 + (j & 15);

@@ -554,7 +554,13 @@ copy_out:
 // ---------------------------------------------------------------------------------------------
 size_t ag_ws_doubles(const nsp_ctx* c, int s) { return (size_t)c->g_nt * 64 * ld_pad(s, 32) + 64; }
 
-nsp_status ag_solve(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, double* buf) {
+// Triangular solves with the A_G factor A_G = R_G^T R_G, R_G = L^T P (P: the band ordering; L the
+// band Cholesky factor).  X is either in the Gamma order (x_gamma: rows gathered through P) or already
+// in R_G's row space (the band order, rows 0..n_G-1); likewise Y (y_gamma: scattered back through
+// P^T).  fwd: L^{-1}, bwd: L^{-T}; both: A_G^{-1} (eq:S1).  So R_G^{-T} x = fwd (x_gamma, band out),
+// R_G^{-1} y = bwd (band in, y_gamma out).  buf: g_nt*64 x ld_pad(s, 32) doubles.
+nsp_status ag_tri(nsp_ctx* c, const double* X, int ldx, bool x_gamma, double* Y, int ldy, bool y_gamma, int s,
+                  bool fwd, bool bwd, double* buf) {
   if (!c->has_ag) {
     c->err = "A_G^{-1} needs the A_G factor: set opts.factor_gamma = 1";
     return NSP_ERR_STATE;
@@ -562,21 +568,36 @@ nsp_status ag_solve(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, in
   const bool vec = s == 1 && c->g_wb <= 2;   // one column, narrow band: matrix-vector chain kernel
   const int ldw = vec ? 1 : ld_pad(s, 32);
   const int64_t rows = (int64_t)c->g_nt * 64;
-  nspk::gather_rows(X, ldx, c->d_gperm, rows, buf, ldw, s, 1.0, c->stream);
+  if (x_gamma) {
+    nspk::gather_rows(X, ldx, c->d_gperm, rows, buf, ldw, s, 1.0, c->stream);
+  } else {
+    nspb::copy_pad(X, ldx, buf, ldw, c->nG, s, 1.0, c->stream);
+    if (rows > c->nG)
+      NSP_CUDA_TRY(c, cudaMemsetAsync(buf + c->nG * (int64_t)ldw, 0, (size_t)(rows - c->nG) * ldw * 8, c->stream));
+  }
   if (c->g_P > 1) {   // partitioned: P chunk sweeps in parallel + spike corrections
     const int cw = vec ? 1 : 32, P = c->g_P;
-    nspk::tri_fb(c->d_gchunks, P, buf, ldw, cw, true, false, c->stream, c->g_wb);
-    nspk::spike_tail(c->d_gspkF, c->d_gchunk_first, P, buf, ldw, s, true, c->stream);
-    nspk::spike_update(c->d_gspkF, c->d_gchunk_first, c->d_gtile_chunk, P, c->g_nt, buf, ldw, s, true, c->stream);
-    nspk::tri_fb(c->d_gchunks, P, buf, ldw, cw, false, true, c->stream, c->g_wb);
-    nspk::spike_tail(c->d_gspkB, c->d_gchunk_first, P, buf, ldw, s, false, c->stream);
-    nspk::spike_update(c->d_gspkB, c->d_gchunk_first, c->d_gtile_chunk, P, c->g_nt, buf, ldw, s, false, c->stream);
+    if (fwd) {
+      nspk::tri_fb(c->d_gchunks, P, buf, ldw, cw, true, false, c->stream, c->g_wb);
+      nspk::spike_tail(c->d_gspkF, c->d_gchunk_first, P, buf, ldw, s, true, c->stream);
+      nspk::spike_update(c->d_gspkF, c->d_gchunk_first, c->d_gtile_chunk, P, c->g_nt, buf, ldw, s, true, c->stream);
+    }
+    if (bwd) {
+      nspk::tri_fb(c->d_gchunks, P, buf, ldw, cw, false, true, c->stream, c->g_wb);
+      nspk::spike_tail(c->d_gspkB, c->d_gchunk_first, P, buf, ldw, s, false, c->stream);
+      nspk::spike_update(c->d_gspkB, c->d_gchunk_first, c->d_gtile_chunk, P, c->g_nt, buf, ldw, s, false, c->stream);
+    }
   } else {
-    nspk::tri_fb(c->d_gsys, 1, buf, ldw, vec ? 1 : 32, true, true, c->stream, c->g_wb);
+    nspk::tri_fb(c->d_gsys, 1, buf, ldw, vec ? 1 : 32, fwd, bwd, c->stream, c->g_wb);
   }
-  nspk::scatter_rows(buf, ldw, c->d_gperm, rows, Y, ldy, s, false, c->stream);
+  if (y_gamma) nspk::scatter_rows(buf, ldw, c->d_gperm, rows, Y, ldy, s, false, c->stream);
+  else nspb::copy_pad(buf, ldw, Y, ldy, c->nG, s, 1.0, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());
   return NSP_OK;
+}
+
+nsp_status ag_solve(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, double* buf) {
+  return ag_tri(c, X, ldx, true, Y, ldy, true, s, true, true, buf);
 }
 
 // Y = M_2 X = A_G^{-1} X + Z (Sigma (Z^T X))   (Alg. 2 step 12, eq:left_prec_mat)
@@ -640,21 +661,26 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   const size_t blk = (size_t)std::max<int64_t>(n, 1) * sp, sm = (size_t)sp * sp;
   // form 0: border system (reading C1); 1: paper-literal S_I system (eq:SI); 2: M_3 - Nystrom of S_I^{-1}
   // itself (eq:internal_term_lr_approximation_2 / eq:left_prec_mat2), Omega then n x s in original order
-  const int form = (c->opts.nys_form == 1 || c->opts.nys_form == 2) ? c->opts.nys_form : 0;
-  if (form >= 1 && (c->nranks != 1 || c->AII.rows == 0)) {
+  const int form = (c->opts.nys_form >= 1 && c->opts.nys_form <= 3) ? c->opts.nys_form : 0;
+  if (form == 3 && c->nranks != 1) {
+    c->err = "nsp_nystrom: the M_1 form (nys_form 3) is single-rank";
+    return NSP_ERR_STATE;
+  }
+  if ((form == 1 || form == 2) && (c->nranks != 1 || c->AII.rows == 0)) {
     c->err = "nsp_nystrom: the S_I forms need opts.nys_form set at nsp_setup (single rank)";
     return NSP_ERR_STATE;
   }
   const int64_t n_int = c->i1_rows + c->wvu_rows;
-  const size_t iblk = form ? (size_t)std::max<int64_t>(n_int, 1) * sp : 0;
-  const size_t bcg_bytes = bcg_layout(c, s, nullptr, nullptr, form ? 1 : 0);
+  const bool si = form == 1 || form == 2;   // inner system on the interior layout (S_I)
+  const size_t iblk = si ? (size_t)std::max<int64_t>(n_int, 1) * sp : 0;
+  const size_t bcg_bytes = bcg_layout(c, s, nullptr, nullptr, si ? 1 : 0);
   const size_t extra =
       (6 * blk + (form == 2 ? 4 : 2) * iblk + 16 * sm + 8 * sp + (size_t)(sp + 1) * (sp + 1)) * 8 + 64 * 256;
   char* base;
   nsp_status e = get_ws(c, ws, bcg_bytes + extra, &base);
   if (e != NSP_OK) return e;
   BcgWs w;
-  bcg_layout(c, s, base, &w, form ? 1 : 0);
+  bcg_layout(c, s, base, &w, si ? 1 : 0);
   Carver cv(base + bcg_bytes);
   double* Om = cv.take(blk);
   double* Bn = cv.take(blk);
@@ -677,8 +703,8 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   double* Vw = cv.take((size_t)(sp + 1) * (sp + 1));
   double* lamC = cv.take(sp);
   double* lamT = cv.take(sp);
-  double* Fi = form ? cv.take(iblk) : nullptr;   // S_I forms: right-hand side / solution (interior layout)
-  double* Xi = form ? cv.take(iblk) : nullptr;
+  double* Fi = si ? cv.take(iblk) : nullptr;   // S_I forms: right-hand side / solution (interior layout)
+  double* Xi = si ? cv.take(iblk) : nullptr;
   double* Qa2 = form == 2 ? cv.take(iblk) : nullptr;   // M_3: Cholesky-QR of the n_int-row Y
   double* Qb2 = form == 2 ? cv.take(iblk) : nullptr;
   BcgStatus* hs = (BcgStatus*)c->h_status;
@@ -776,8 +802,15 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
       }
       continue;
     }
-    // steps 1-2: B = K_G G  (reading C1)
-    if ((e = apply_into(c, Om, sp, Bn, sp, s, 2, w.wvu)) != NSP_OK) return e;
+    // steps 1-2: B = K_G G  (reading C1); M_1 (form 3): the operator is R_G^{-T} B_H R_G^{-1}, so the
+    // sketch enters as R_G^{-1} G (eq:lr_approximation_S-1_A-I)
+    const double* Gin = Om;
+    if (form == 3) {
+      NSP_CUDA_TRY(c, cudaMemsetAsync(Qa, 0, blk * 8, st));   // padding columns stay zero
+      if ((e = ag_tri(c, Om, sp, false, Qa, sp, true, s, false, true, w.wvu)) != NSP_OK) return e;
+      Gin = Qa;
+    }
+    if ((e = apply_into(c, Gin, sp, Bn, sp, s, 2, w.wvu)) != NSP_OK) return e;
     // step 3: S_G X = B by breakdown-free block CG to tol_inner
     brep = nsp_report{};
     if (rep && pw == q) {
@@ -790,8 +823,9 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
     if (sbi < 0) return sbi;
     if (sbi == NSP_NOT_CONVERGED) sb = NSP_NOT_CONVERGED;
     total_iters += brep.iters;
-    // step 4: Y = A_G X
+    // step 4: Y = A_G X  (M_1: Y = R_G^{-T} A_G X, in R_G's row space)
     nspk::spmm(c->AGG2, Xn, sp, nullptr, 0, n, Y, sp, s, 3, true, st);
+    if (form == 3 && (e = ag_tri(c, Y, sp, true, Y, sp, false, s, true, false, w.wvu)) != NSP_OK) return e;
     if (pw < q) {   // power step: G <- orthonormal basis of Y
       const double* Qp = nullptr;
       if ((e = cholqr(Y, &Qp)) != NSP_OK) return e;
@@ -851,6 +885,8 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
     if (form == 2) {
       nspk::spmm(c->AGG2, nullptr, 0, U + c->i1_rows * (int64_t)kp, kp, n, Bn, kp, rk, 2, true, st);
       if ((e = ag_solve(c, Bn, kp, c->d_Z, kp, rk, w.wvu)) != NSP_OK) return e;
+    } else if (form == 3) {   // M_1: Z = R_G^{-1} U (eq:prec1S)
+      if ((e = ag_tri(c, U, kp, false, c->d_Z, kp, true, rk, false, true, w.wvu)) != NSP_OK) return e;
     } else if ((e = ag_solve(c, U, kp, c->d_Z, kp, rk, w.wvu)) != NSP_OK) {
       return e;
     }
@@ -903,7 +939,7 @@ nsp_status nsp_nystrom_sigma(const nsp_ctx* c, double* sigma, int* rank_out) {
 }
 
 nsp_status nsp_precond_apply(nsp_ctx* c, int which, const double* X, double* Y, int s, void* ws) {
-  if (!c || !X || !Y || s <= 0 || s > 128 || which < 0 || which > 2) return NSP_ERR_ARG;
+  if (!c || !X || !Y || s <= 0 || s > 128 || which < 0 || which > 4) return NSP_ERR_ARG;
   if (which == 0) {
     NSP_CUDA_TRY(c, cudaMemcpyAsync(Y, X, (size_t)c->nG * s * 8, cudaMemcpyDeviceToDevice, c->stream));
     return NSP_OK;
@@ -926,6 +962,8 @@ nsp_status nsp_precond_apply(nsp_ctx* c, int which, const double* X, double* Y, 
   double* Xp = cv.take(blk);
   double* Yp = cv.take(blk);
   if (which == 1) return ag_solve(c, X, s, Y, s, s, buf);
+  if (which == 3) return ag_tri(c, X, s, true, Y, s, false, s, true, false, buf);   // R_G^{-T}: Gamma -> R_G rows
+  if (which == 4) return ag_tri(c, X, s, false, Y, s, true, s, false, true, buf);   // R_G^{-1}: R_G rows -> Gamma
   nspb::copy_pad(X, s, Xp, sp, c->nG, s, 1.0, c->stream);
   NSP_CUDA_TRY(c, cudaMemsetAsync(Yp, 0, blk * 8, c->stream));
   if ((e = m2_apply(c, Xp, sp, Yp, sp, s, buf, gsm, gws)) != NSP_OK) return e;

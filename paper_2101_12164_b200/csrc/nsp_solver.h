@@ -17,4 +17,6 @@ namespace nspi {
 size_t ag_ws_doubles(const nsp_ctx* c, int s);
 // Y = A_G^{-1} X (band factor of A_G; eq:S1), buf: ag_ws_doubles(c, s) doubles
 nsp_status ag_solve(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, double* buf);
+nsp_status ag_tri(nsp_ctx* c, const double* X, int ldx, bool x_gamma, double* Y, int ldy, bool y_gamma, int s,
+                  bool fwd, bool bwd, double* buf);
 }  // namespace nspi

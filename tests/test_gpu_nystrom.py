@@ -162,3 +162,69 @@ def test_nystrom_m3_parity(name):
     assert rp["iters"] == io["iters"]
     assert relfro(x.cpu().numpy(), xo) <= 1e-8
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg5s"])
+def test_nystrom_m1_parity(name):
+    """M_1 (eq:prec1S; opts.nys_form = 3) with the A_G factor in the natural Gamma order (ag_order = 1), so
+    R_G = chol(A_G) is the oracle's factor: inner count within +-1; Sigma, M_1 probes and the M_1 /
+    M_A-DEF1 full solves at equal counts within 1e-8 of oracle.nystrom.nystrom_m1."""
+    from oracle.nystrom import apply_ADEF1, apply_M1
+    pr, d, S = problem(name)
+    Om = pr.omega()
+    ref = O.nystrom_m1(S, Om, pr.rank, pr.tol_bcg, 500)
+    ctx = context(pr, factor_gamma=True, nys_form=3, ag_order=1)
+    rep = ctx.nystrom(pr.rank, pr.oversample, dev(Om), pr.tol_bcg, 500)
+    assert rep["converged"] and abs(rep["iters"] - ref.bcg["iters"]) <= 1, (rep["iters"], ref.bcg["iters"])
+    k = ref.bcg["iters"]
+    ref0 = O.nystrom_m1(S, Om, pr.rank, 0.0, k)
+    rep0 = ctx.nystrom(pr.rank, pr.oversample, dev(Om), 0.0, k)
+    assert rep0["iters"] == k and rep0["rank"] == ref0.rank
+    sig = ctx.nystrom_sigma()
+    assert np.max(np.abs(sig - ref0.sigma) / ref0.sigma) <= 1e-8, (sig[:3], ref0.sigma[:3])
+    R = block(d.n_gamma, 8, seed=33)
+    Y = torch.empty(d.n_gamma, 8, dtype=torch.float64, device="cuda")
+    ctx.precond_apply(2, dev(R), Y)
+    assert relfro(Y.cpu().numpy(), apply_M1(S, ref0.Z, ref0.sigma, R)) <= 1e-8
+    b = pr.rhs()
+    for prec, fn in ((2, lambda r: apply_M1(S, ref0.Z, ref0.sigma, r)), (3, lambda r: apply_ADEF1(S, ref0.Z, r))):
+        xo, io = O.solve_full_system(S, b, 1e-8, 2000, fn)
+        x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
+        rp = ctx.pcg(dev(b), x, 1e-8, 2000, precond=prec)
+        assert rp["converged"] and abs(rp["iters"] - io["iters"]) <= 1, (prec, rp["iters"], io["iters"])
+        x2 = torch.zeros_like(x)
+        rp2 = ctx.pcg(dev(b), x2, 0.0, io["iters"], precond=prec)
+        assert rp2["iters"] == io["iters"]
+        assert relfro(x2.cpu().numpy(), xo) <= 1e-8
+    ctx.close()
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_nystrom_m1_full_rank_closed_form_gpu(order):
+    """M_1 at full rank on cfg1 (inner solve to 1e-13; s = rank(B_H) = 125 of n_G = 127: the separator
+    crossing has no interior neighbour, so B_H has zero eigenvalues, and Nystrom with s >= rank is exact):
+    the dominant Sigma equal 1/lambda - 1 for the generalized eigenvalues S_G v = lambda A_G v (closed form
+    below eq:Rt_S-1_R, independent of R_G's ordering: RCM (0) and natural (1) factors), and M_1 ~ S_G^{-1}:
+    the outer PCG needs at most a few iterations.  Tolerance: with s = rank the sketch Omega^T A Omega is
+    square and its condition number (1e6 natural, 9e8 RCM for this Omega, computed in fp64 on the host)
+    multiplies the 1e-13 inner residual into Sigma: the top 20 are compared at 1e-8 (natural) / 1e-4
+    (RCM; the oracle with exact solves and an RCM-ordered R_G already loses 1e-11 there)."""
+    import scipy.linalg as sl
+    from nsp_inputs import philox
+    pr, d, S = problem("cfg1")
+    n = d.n_gamma
+    lam = sl.eigh(S.dense(), d.A_G.toarray(), eigvals_only=True)
+    ref = np.sort(1.0 / lam - 1.0)[::-1]
+    rk = int((ref > 1e-10 * ref[0]).sum())
+    assert 100 <= rk < n
+    Om = philox.gaussian_block(3, 0, n, rk)
+    ctx = context(pr, factor_gamma=True, nys_form=3, ag_order=order)
+    ctx.nystrom(rk, 0, dev(Om), 1e-13, 200)
+    sig = ctx.nystrom_sigma()
+    assert len(sig) == rk
+    assert np.allclose(sig[:20], ref[:20], rtol=1e-8 if order == 1 else 1e-4), (sig[:4], ref[:4])
+    b = pr.rhs()
+    x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
+    rp = ctx.pcg(dev(b), x, 1e-8, 50, precond=2)
+    assert rp["converged"] and rp["iters"] <= 4, rp["iters"]
+    ctx.close()
