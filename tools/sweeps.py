@@ -37,13 +37,13 @@ def one(ctx, pr, k, p, tol_inner, bcg_precond_ctx=None, maxit=5000):
 
 def variants(pr, tol_inner=0.1):
     """tab:compare_variations analog: it_total = inner block-CG iterations + outer
-    PCG iterations for M_2, M_A-DEF2, M_3, M_A-DEF3, and S~_1 (A_G^{-1} alone)."""
+    PCG iterations for M_1, M_A-DEF1, M_2, M_A-DEF2, M_3, M_A-DEF3, and S~_1 (A_G^{-1} alone)."""
     out = {}
     b = torch.from_numpy(pr.rhs()).cuda()
-    for form, lab in ((0, "2"), (2, "3")):
+    for form, lab in ((3, "1"), (0, "2"), (2, "3")):
         ctx = nsp.Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, factor_gamma=True, nys_form=form)
-        rows = ctx.n_gamma if form == 0 else pr.n
-        Om = torch.from_numpy(philox.gaussian_block(0, philox.STREAM_OMEGA if form == 0 else 5, rows, pr.s)).cuda()
+        rows = pr.n if form == 2 else ctx.n_gamma
+        Om = torch.from_numpy(philox.gaussian_block(0, 5 if form == 2 else philox.STREAM_OMEGA, rows, pr.s)).cuda()
         rn = ctx.nystrom(pr.rank, pr.oversample, Om, tol_inner, 1000)
         for prec, name in ((2, f"M{lab}"), (3, f"M_A-DEF{lab}")):
             x = torch.zeros_like(b)
