@@ -97,6 +97,14 @@ typedef struct {
   int ag_order;          /* ordering of the A_G factor (factor_gamma): 0 = reverse Cuthill-McKee band
                             (default); 1 = the natural Gamma order (nsp_gamma_index), so that
                             R_G = chol(A_G) exactly as written (dense-ish band: small n_G only) */
+  int ag_solver;         /* how A_G^{-1} is applied (factor_gamma): 0 = auto (the band Cholesky factor
+                            when it fits the device budget, else 2); 1 = band Cholesky factor only
+                            (NSP_ERR_OOM when it does not fit); 2 = a fixed-degree Chebyshev iteration
+                            on A_G ("an iterative solver to solve linear systems with
+                            A_G ... A_G is typically well conditioned"), spectrum bounds from a setup
+                            Lanczos run, degree for a 1e-15 relative error bound; a fixed polynomial,
+                            so M_2 stays one symmetric operator for the outer PCG.  M_1 (nys_form 3)
+                            needs the factor (1 or a fitting auto). */
 } nsp_opts;
 
 /* Solver / setup report; caller-owned.  hist / widths are optional caller

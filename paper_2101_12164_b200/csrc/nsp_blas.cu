@@ -770,6 +770,19 @@ __global__ void k_scale_rows(double* G, int ld, const double* d, int r, int nrow
 }
 
 // copy with ld change and zero padding: dst[r][c] = c < s ? src[r][c] : 0 (c < ldd)
+// one Chebyshev step after t = A d: x += d; r -= t; d' = c1 d + c2 r (new r)
+__global__ void k_cheb_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ d,
+                              const double* __restrict__ t, double* __restrict__ dn, double c1, double c2, int64_t n,
+                              int want_d) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double di = d[i];
+  x[i] += di;
+  const double ri = r[i] - t[i];
+  r[i] = ri;
+  if (want_d) dn[i] = fma(c1, di, c2 * ri);
+}
+
 __global__ void k_copy_pad(const double* src, int lds, double* dst, int ldd, int64_t n, int s, double scale) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t r = idx / ldd;
@@ -886,6 +899,12 @@ void small_gemm(int m, int n, int k, double alpha, const double* A, int lda, boo
                 bool tb, double beta, double* C, int ldc, cudaStream_t st) {
   dim3 grid((n + 15) / 16, (m + 15) / 16);
   { nsp_count_launch(); k_small_gemm<<<grid, dim3(16, 16), 0, st>>>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc); }
+}
+
+void cheb_update(double* x, double* r, const double* d, const double* t, double* dn, double c1, double c2, int64_t n,
+                 bool want_d, cudaStream_t st) {
+  if (n <= 0) return;
+  { nsp_count_launch(); k_cheb_update<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, r, d, t, dn, c1, c2, n, want_d ? 1 : 0); }
 }
 
 void copy_pad(const double* src, int lds, double* dst, int ldd, int64_t n, int s, double scale, cudaStream_t st) {

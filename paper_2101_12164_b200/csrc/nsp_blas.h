@@ -78,5 +78,7 @@ void small_sym(double* A, int n, int ld, double shift, cudaStream_t st);
 // M[:, k] = V[:, k] * f(colscale[k]) for k < r (f: mode 0 x, 1 1/sqrt(x), 2 sqrt(x), 3 copy), zero for r <= k < ncols
 void scale_cols(const double* V, int ldv, const double* colscale, int r, int n, int ncols, double* M, int ldm,
                 int mode, cudaStream_t st);
+void cheb_update(double* x, double* r, const double* d, const double* t, double* dn, double c1, double c2, int64_t n,
+                 bool want_d, cudaStream_t st);
 void copy_pad(const double* src, int lds, double* dst, int ldd, int64_t n, int s, double scale, cudaStream_t st);
 }  // namespace nspb

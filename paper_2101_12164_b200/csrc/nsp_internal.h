@@ -112,6 +112,12 @@ struct nsp_ctx {
 
   // A_G factor (band, RCM order): rows of the band buffer -> local Gamma index (-1 = padding)
   bool has_ag = false;
+  // or A_G^{-1} by a fixed Chebyshev iteration ("an iterative solver to solve linear
+  // systems with A_G"; opts.ag_solver): spectrum bounds [cheb_a, cheb_b], K steps, per-step coefficients
+  bool ag_cheb = false;
+  double cheb_a = 0.0, cheb_b = 0.0;
+  int cheb_K = 0;
+  std::vector<double> cheb_c1, cheb_c2;
   double* d_gband = nullptr;  int64_t gband_tiles = 0;
   TriSys* d_gsys = nullptr;   int g_nt = 0, g_wb = 0;
   int32_t* d_gperm = nullptr;     // band row -> Gamma row (size g_nt*64)

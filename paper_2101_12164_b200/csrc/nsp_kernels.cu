@@ -261,6 +261,43 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __res
     for (int cc = 32 * NQ + lane; cc < ldy; cc += 32) y[cc] = 0.0;
 }
 
+// One right-hand side (s = 1): the same modes as k_spmm, G lanes per row (several rows per warp),
+// the lanes take the row's nonzeros in parallel (independent gathers of x) and combine them with a
+// G-lane butterfly (fixed order).  k_spmm's lane-over-columns layout would leave 31 of 32 lanes idle
+// and serialise one dependent gather per nonzero.
+template <int G>
+__global__ void __launch_bounds__(256) k_spmv(int64_t rows, const int32_t* __restrict__ rp,
+                                              const int32_t* __restrict__ ci, const double* __restrict__ va,
+                                              const double* __restrict__ X, int ldx,
+                                              const double* __restrict__ U, int ldu, int64_t split,
+                                              double* __restrict__ Y, int ldy, int mode, int zero_pad) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int sub = threadIdx.x & (G - 1);
+  double acc = 0.0;
+  if (row < rows) {
+    const int beg = rp[row], end = rp[row + 1];
+    for (int k = beg + sub; k < end; k += G) {
+      const int64_t col = ci[k];
+      double a = va[k];
+      if (mode == 0 || mode == 4 || col < split) {
+        if (mode == 2) continue;
+        acc = fma(a, __ldg(X + col * ldx), acc);
+      } else {
+        if (mode == 3) continue;
+        if (mode == 2) a = -a;
+        acc = fma(a, __ldg(U + (col - split) * ldu), acc);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (row >= rows) return;
+  double* y = Y + row * ldy;
+  if (sub == 0) y[0] = mode == 4 ? y[0] + acc : acc;
+  if (zero_pad)
+    for (int cc = 1 + sub; cc < ldy; cc += G) y[cc] = 0.0;
+}
+
 // ---------------------------------------------------------------------------------------------
 // a2 + a3: batched forward and backward triangular solves with the boundary-layer factor
 // L22_j of every block, all blocks (x column chunks) in one launch.  Blocked by 64-row tiles
@@ -1257,6 +1294,11 @@ void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, i
           int ldy, int s, int mode, bool zero_pad, cudaStream_t st) {
   if (A.rows <= 0) return;
   const unsigned blocks = (unsigned)((A.rows * 32 + 255) / 256);
+  if (s == 1) {
+    const unsigned b8 = (unsigned)((A.rows * 8 + 255) / 256);
+    { nsp_count_launch(); k_spmv<8><<<b8, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, mode, zero_pad); }
+    return;
+  }
   if (s <= 32)
     { nsp_count_launch(); k_spmm<1><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
   else if (s <= 64)

@@ -171,6 +171,142 @@ static nsp_status fail(nsp_ctx* c, nsp_status st, const std::string& msg) {
 nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K, nsp_report* rep);
 static nsp_status validate_inputs(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int K);
 
+// A_G^{-1} by a fixed Chebyshev iteration.  Host: A_G's rows in the local Gamma
+// order; the upper spectrum bound is min(Gershgorin, 1.05 x the top Lanczos Ritz value), the lower
+// one the bottom Ritz value / 1.05 (Lanczos from a fixed start vector, 120 steps, no
+// reorthogonalisation: the extreme Ritz values converge first); the degree K makes the Chebyshev
+// error bound 2 q^K <= 1e-15, q = (sqrt(kappa) - 1) / (sqrt(kappa) + 1) (Saad, Alg. 12.1).
+static double tridiag_count_below(const std::vector<double>& al, const std::vector<double>& be, double x) {
+  // Sturm count: eigenvalues of the symmetric tridiagonal (al, be) smaller than x
+  int cnt = 0;
+  double d = 1.0;
+  for (size_t i = 0; i < al.size(); ++i) {
+    const double b2 = i ? be[i - 1] * be[i - 1] : 0.0;
+    d = al[i] - x - (i ? b2 / d : 0.0);
+    if (d == 0.0) d = -1e-300;
+    if (d < 0.0) ++cnt;
+  }
+  return cnt;
+}
+
+static nsp_status setup_gamma_cheb(nsp_ctx* c, const nsp_csr* A, const int32_t* part,
+                                   const std::vector<int32_t>& gpos) {
+  const int64_t nG = c->nG;
+  const int64_t* rp = A->rowptr;
+  const int32_t* ci = A->colidx;
+  const double* va = A->val;
+  std::vector<int64_t> grp(nG + 1, 0);
+  for (int64_t g = 0; g < nG; ++g) {
+    const int64_t v = c->gamma[g];
+    int64_t k = 0;
+    for (int64_t q = rp[v]; q < rp[v + 1]; ++q)
+      if (part[ci[q]] < 0) ++k;
+    grp[g + 1] = grp[g] + k;
+  }
+  std::vector<int32_t> gci(grp[nG]);
+  std::vector<double> gva(grp[nG]);
+  double gersh = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : gersh)
+  for (int64_t g = 0; g < nG; ++g) {
+    const int64_t v = c->gamma[g];
+    int64_t k = grp[g];
+    double rs = 0.0;
+    for (int64_t q = rp[v]; q < rp[v + 1]; ++q)
+      if (part[ci[q]] < 0) {
+        gci[k] = gpos[ci[q]];
+        gva[k++] = va[q];
+        rs += std::fabs(va[q]);
+      }
+    gersh = std::max(gersh, rs);
+  }
+  auto spmv = [&](const std::vector<double>& x, std::vector<double>& y) {
+#pragma omp parallel for schedule(static)
+    for (int64_t g = 0; g < nG; ++g) {
+      double s = 0.0;
+      for (int64_t k = grp[g]; k < grp[g + 1]; ++k) s += gva[k] * x[gci[k]];
+      y[g] = s;
+    }
+  };
+  const int m = (int)std::min<int64_t>(120, nG);
+  std::vector<double> v(nG), vp(nG, 0.0), w(nG), al, be;
+  uint64_t st = 0x9E3779B97F4A7C15ull;
+  double nrm = 0.0;
+  for (int64_t g = 0; g < nG; ++g) {
+    st = st * 6364136223846793005ull + 1442695040888963407ull;
+    v[g] = (double)(st >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    nrm += v[g] * v[g];
+  }
+  nrm = std::sqrt(nrm);
+  for (auto& x : v) x /= nrm;
+  double b = 0.0;
+  for (int k = 0; k < m; ++k) {
+    spmv(v, w);
+    double a = 0.0;
+    for (int64_t g = 0; g < nG; ++g) {
+      w[g] -= b * vp[g];
+      a += v[g] * w[g];
+    }
+    double bn = 0.0;
+    for (int64_t g = 0; g < nG; ++g) {
+      w[g] -= a * v[g];
+      bn += w[g] * w[g];
+    }
+    bn = std::sqrt(bn);
+    al.push_back(a);
+    if (k + 1 == m || bn <= 1e-14 * std::fabs(a)) break;
+    be.push_back(bn);
+    b = bn;
+    for (int64_t g = 0; g < nG; ++g) {
+      vp[g] = v[g];
+      v[g] = w[g] / bn;
+    }
+  }
+  be.resize(al.size() - 1);
+  // extreme Ritz values by bisection on the Sturm count
+  double lo = -gersh - 1.0, hi = gersh + 1.0;
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (tridiag_count_below(al, be, mid) >= 1) hi = mid;
+    else lo = mid;
+  }
+  const double tmin = hi;
+  lo = -gersh - 1.0;
+  hi = gersh + 1.0;
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (tridiag_count_below(al, be, mid) >= (double)al.size()) hi = mid;
+    else lo = mid;
+  }
+  const double tmax = hi;
+  if (!(tmin > 0.0)) return fail(c, NSP_ERR_NOT_SPD, "nsp_setup: A_G Lanczos estimate not positive (A_G not SPD?)");
+  const double a = tmin / 1.05, bb = std::min(gersh, 1.05 * tmax);
+  const double kappa = bb / a;
+  const double q = (std::sqrt(kappa) - 1.0) / (std::sqrt(kappa) + 1.0);
+  const int K = (int)std::ceil(std::log(2.0 / 1e-15) / std::log(1.0 / std::max(q, 1e-300)));
+  if (K > 4000)
+    return fail(c, NSP_ERR_OOM, "nsp_setup: A_G too ill-conditioned for the Chebyshev solver (kappa " +
+                                    std::to_string(kappa) + ") and its band factor does not fit");
+  c->cheb_a = a;
+  c->cheb_b = bb;
+  c->cheb_K = std::max(K, 1);
+  const double theta = 0.5 * (bb + a), delta = 0.5 * (bb - a), sigma1 = theta / delta;
+  c->cheb_c1.assign(c->cheb_K, 0.0);
+  c->cheb_c2.assign(c->cheb_K, 0.0);
+  double rho = 1.0 / sigma1;
+  for (int k = 0; k < c->cheb_K; ++k) {   // d_{k+1} = rho_{k+1} rho_k d_k + (2 rho_{k+1} / delta) r_{k+1}
+    const double rn = 1.0 / (2.0 * sigma1 - rho);
+    c->cheb_c1[k] = rn * rho;
+    c->cheb_c2[k] = 2.0 * rn / delta;
+    rho = rn;
+  }
+  c->ag_cheb = true;
+  c->has_ag = true;
+  c->ag_bw = -c->cheb_K;   // nsp_stats: negative = Chebyshev degree
+  if (c->opts.verbose)
+    fprintf(stderr, "[nsp] A_G^{-1}: Chebyshev on [%.4g, %.4g] (kappa %.1f), K = %d\n", a, bb, kappa, c->cheb_K);
+  return NSP_OK;
+}
+
 // Cholesky factor of A_G (eq:cholesky) for the first-level preconditioner
 // S~_1^{-1} = A_G^{-1} (eq:S1) and M_2: RCM band ordering of the Gamma graph, band tiles, the same
 // GPU tile-Cholesky kernel as the blocks (a band-only block).
@@ -209,7 +345,7 @@ static nsp_status setup_gamma_factor(nsp_ctx* c, const nsp_csr* A, const int32_t
   NSP_CUDA_TRY(c, cudaMemGetInfo(&free_b, &total_b));
   if ((double)tiles * NSP_TILE_ELEMS * 8 > 0.4 * (double)free_b)
     return fail(c, NSP_ERR_OOM, "nsp_setup: A_G band factor (RCM bandwidth " + std::to_string(bw) +
-                                    ") exceeds the device budget");
+                                    ") exceeds the device budget (opts.ag_solver 0 / 2: Chebyshev iteration)");
   std::vector<int64_t> idx;
   std::vector<double> val;
   for (int64_t g = 0; g < nG; ++g) {
@@ -461,6 +597,7 @@ static nsp_status validate_inputs(nsp_ctx* c, const nsp_csr* A, const int32_t* p
   if (n <= 0 || !rp || !ci || !va) return fail(c, NSP_ERR_ARG, "nsp_setup: empty or null CSR");
   if (rp[0] != 0) return fail(c, NSP_ERR_ARG, "nsp_setup: rowptr[0] != 0");
   if (c->opts.ag_order < 0 || c->opts.ag_order > 1) return fail(c, NSP_ERR_ARG, "nsp_setup: ag_order must be 0 or 1");
+  if (c->opts.ag_solver < 0 || c->opts.ag_solver > 2) return fail(c, NSP_ERR_ARG, "nsp_setup: ag_solver must be 0..2");
   if (c->opts.nys_form < 0 || c->opts.nys_form > 3) return fail(c, NSP_ERR_ARG, "nsp_setup: nys_form must be 0..3");
   // ---------------- validation
   std::string verr;
@@ -1087,7 +1224,12 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   double t_ag = 0.0;
   if (c->opts.factor_gamma) {
     auto t3 = Clock::now();
-    nsp_status sg = setup_gamma_factor(c, A, part, gpos, rep);
+    nsp_status sg = c->opts.ag_solver == 2 ? NSP_ERR_OOM : setup_gamma_factor(c, A, part, gpos, rep);
+    if (sg == NSP_ERR_OOM && c->opts.ag_solver != 1 && c->nranks == 1) {
+      (void)cudaGetLastError();
+      sg = setup_gamma_cheb(c, A, part, gpos);
+      if (sg == NSP_OK) c->err.clear();
+    }
     if (sg != NSP_OK) return sg;
     t_ag = ms_since(t3);
   }

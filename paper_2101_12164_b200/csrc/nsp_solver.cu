@@ -552,7 +552,39 @@ copy_out:
 // A_G^{-1} X (eq:S1): rows gathered into RCM band order, band forward + backward sweeps, scattered
 // back.  buf: g_nt*64 x ld_pad(s, 32) doubles.
 // ---------------------------------------------------------------------------------------------
-size_t ag_ws_doubles(const nsp_ctx* c, int s) { return (size_t)c->g_nt * 64 * ld_pad(s, 32) + 64; }
+static int cheb_ld(int s) { return s == 1 ? 1 : ld_pad(s, 32); }
+size_t ag_ws_doubles(const nsp_ctx* c, int s) {
+  if (c->ag_cheb) return (size_t)5 * std::max<int64_t>(c->nG, 1) * cheb_ld(s) + 5 * 64;
+  return (size_t)c->g_nt * 64 * ld_pad(s, 32) + 64;
+}
+
+// A_G^{-1} X by the fixed Chebyshev iteration of the setup (Saad Alg. 12.1):
+// r = x0 = X, d = r / theta, then K times { t = A_G d; x += d; r -= t; d' = c1_k d + c2_k r } - one
+// CSR SpMM (A_G part of AGG2) and one fused elementwise pass per step.  X may alias Y.
+static nsp_status ag_cheb(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, double* buf) {
+  const int ld = cheb_ld(s);
+  const int64_t n = c->nG;
+  const size_t blk = (size_t)std::max<int64_t>(n, 1) * ld;
+  double* xw = buf;
+  double* r = buf + blk;
+  double* d0 = buf + 2 * blk;
+  double* d1 = buf + 3 * blk;
+  double* t = buf + 4 * blk;
+  cudaStream_t st = c->stream;
+  if (n == 0) return NSP_OK;
+  nspb::copy_pad(X, ldx, r, ld, n, s, 1.0, st);
+  const double theta = 0.5 * (c->cheb_b + c->cheb_a);
+  nspb::copy_pad(X, ldx, d0, ld, n, s, 1.0 / theta, st);
+  NSP_CUDA_TRY(c, cudaMemsetAsync(xw, 0, blk * 8, st));
+  for (int k = 0; k < c->cheb_K; ++k) {
+    nspk::spmm(c->AGG2, d0, ld, nullptr, 0, n, t, ld, s, 3, true, st);   // t = A_G d
+    nspb::cheb_update(xw, r, d0, t, d1, c->cheb_c1[k], c->cheb_c2[k], (int64_t)n * ld, k + 1 < c->cheb_K, st);
+    std::swap(d0, d1);
+  }
+  nspb::copy_pad(xw, ld, Y, ldy, n, s, 1.0, st);
+  NSP_CUDA_TRY(c, cudaGetLastError());
+  return NSP_OK;
+}
 
 // Triangular solves with the A_G factor A_G = R_G^T R_G, R_G = L^T P (P: the band ordering; L the
 // band Cholesky factor).  X is either in the Gamma order (x_gamma: rows gathered through P) or already
@@ -563,6 +595,11 @@ nsp_status ag_tri(nsp_ctx* c, const double* X, int ldx, bool x_gamma, double* Y,
                   bool fwd, bool bwd, double* buf) {
   if (!c->has_ag) {
     c->err = "A_G^{-1} needs the A_G factor: set opts.factor_gamma = 1";
+    return NSP_ERR_STATE;
+  }
+  if (c->ag_cheb) {
+    if (fwd && bwd && x_gamma && y_gamma) return ag_cheb(c, X, ldx, Y, ldy, s, buf);
+    c->err = "R_G^{-1} / R_G^{-T} need the A_G band factor (opts.ag_solver 1); A_G^{-1} is a Chebyshev iteration here";
     return NSP_ERR_STATE;
   }
   const bool vec = s == 1 && c->g_wb <= 2;   // one column, narrow band: matrix-vector chain kernel

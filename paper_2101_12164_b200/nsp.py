@@ -34,7 +34,8 @@ class nsp_opts(C.Structure):
                 ("nccl_id", C.c_void_p), ("bcg_precond", C.c_int), ("factor_gamma", C.c_int),
                 ("orth_tau", C.c_double), ("nys_eps_rel", C.c_double), ("scratch_bytes", C.c_size_t),
                 ("verbose", C.c_int), ("local_group", C.c_void_p), ("apply_kernel", C.c_int),
-                ("nys_power", C.c_int), ("nys_form", C.c_int), ("ag_order", C.c_int)]
+                ("nys_power", C.c_int), ("nys_form", C.c_int), ("ag_order", C.c_int),
+                ("ag_solver", C.c_int)]
 
 
 class nsp_report(C.Structure):
@@ -174,7 +175,7 @@ class Context:
     def __init__(self, rowptr, colidx, val, part, K, device=0, stream=None, bcg_precond=0,
                  factor_gamma=False, orth_tau=1e-14, nys_eps_rel=1e-12, nranks=1, rank=0,
                  nccl_id: bytes | None = None, scratch_bytes=0, local_group: "LocalGroup | None" = None,
-                 apply_kernel=0, nys_power=0, nys_form=0, ag_order=0):
+                 apply_kernel=0, nys_power=0, nys_form=0, ag_order=0, ag_solver=0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("CUDA device required (no CPU fallback)")
@@ -202,6 +203,7 @@ class Context:
         o.nys_power = nys_power
         o.nys_form = nys_form
         o.ag_order = ag_order
+        o.ag_solver = ag_solver
         self.opts = o
         self.ctx = C.c_void_p()
         rep = nsp_report()

@@ -228,3 +228,43 @@ def test_nystrom_m1_full_rank_closed_form_gpu(order):
     rp = ctx.pcg(dev(b), x, 1e-8, 50, precond=2)
     assert rp["converged"] and rp["iters"] <= 4, rp["iters"]
     ctx.close()
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_ag_chebyshev_parity(name):
+    """A_G^{-1} by the fixed Chebyshev iteration (opts.ag_solver = 2; "an iterative
+    solver to solve linear systems with A_G"): relative error <= 1e-12 against the oracle's direct
+    solve, for s = 1, 5, 64 (the degree is set for a 1e-15 error bound)."""
+    pr, d, S = problem(name)
+    ctx = context(pr, factor_gamma=True, ag_solver=2)
+    assert ctx.stats()["ag_bw"] < 0      # Chebyshev degree reported as -K
+    for s in [1, 5, 64]:
+        X = block(d.n_gamma, s, seed=12)
+        Y = torch.empty(d.n_gamma, s, dtype=torch.float64, device="cuda")
+        ctx.precond_apply(1, dev(X), Y)
+        assert relfro(Y.cpu().numpy(), S.solve_AG(X)) <= 1e-12
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg5s"])
+def test_m2_pcg_with_chebyshev_ag(name):
+    """M_2 built and applied with the Chebyshev A_G^{-1} (the cfg5 route: its band factor does not fit):
+    Sigma, and the outer PCG at equal iteration counts, within 1e-8 of the oracle (direct A_G^{-1})."""
+    pr, d, S = problem(name)
+    Om = pr.omega()
+    ref = O.nystrom_schur(S, Om, pr.rank, pr.tol_bcg, 500)
+    k = ref.bcg["iters"]
+    ctx = context(pr, factor_gamma=True, ag_solver=2)
+    rep = ctx.nystrom(pr.rank, pr.oversample, dev(Om), 0.0, k)
+    assert rep["iters"] == k and rep["rank"] == ref.rank
+    sig = ctx.nystrom_sigma()
+    assert np.max(np.abs(sig - ref.sigma) / ref.sigma) <= 1e-8
+    b = pr.rhs()
+    xo, io = O.solve_full_system(S, b, 1e-8, 2000, lambda r: apply_M2(S, ref.Z, ref.sigma, r))
+    x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
+    rp = ctx.pcg(dev(b), x, 1e-8, 2000, precond=2)
+    assert rp["converged"] and abs(rp["iters"] - io["iters"]) <= 1
+    x2 = torch.zeros_like(x)
+    ctx.pcg(dev(b), x2, 0.0, io["iters"], precond=2)
+    assert relfro(x2.cpu().numpy(), xo) <= 1e-8
+    ctx.close()

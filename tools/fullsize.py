@@ -35,11 +35,14 @@ def run_pcg(name, maxit=5000):
     torch.cuda.synchronize()
     t_nys = time.perf_counter() - t0
     b = pr.rhs()
+    st = ctx.stats()
     out = dict(config=name, setup_s=round(t_setup, 2), ag_factor_ms=round(ctx.setup_report["t_ms"][3], 1),
+               ag_solver=("chebyshev K=%d" % -st["ag_bw"]) if st["ag_bw"] < 0 else "band (RCM bw %d)" % st["ag_bw"],
                nystrom_s=round(t_nys, 3), nystrom_inner_iters=rn["iters"], nystrom_rank=rn["rank"],
                sigma_top=[float(x) for x in ctx.nystrom_sigma()[:3]])
     A = pr.A.to_scipy()
-    for prec in (1, 2, 3):   # S~_1, M_2, M_A-DEF2
+    precs = [int(x) for x in os.environ.get("NSP_PRECS", "1,2,3").split(",")]
+    for prec in precs:   # S~_1, M_2, M_A-DEF2
         x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
         bd = torch.from_numpy(b).cuda()
         torch.cuda.synchronize()
