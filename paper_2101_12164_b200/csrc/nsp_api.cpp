@@ -21,7 +21,10 @@ int ld_pad(int s, int cw) { return ((s + cw - 1) / cw) * cw; }
 
 size_t apply_ws_bytes(const nsp_ctx* c, int s) {
   const int cw = pick_cw(c, s);
-  return (size_t)c->wvu_rows * ld_pad(s, cw) * 8 * (c->d_minv ? 2 : 1) + 512;
+  size_t b = (size_t)c->wvu_rows * ld_pad(s, cw) * 8 * (c->d_minv ? 2 : 1) + 512;
+  // k_symv1 partial slots (s = 1; reserved for every s: callers size one workspace for several widths)
+  if (c->d_minv) b += (size_t)c->wvu_rows * c->max_ntb * 8 + 256;
+  return b;
 }
 
 nsp_status get_ws(nsp_ctx* c, void* ws, size_t need, char** out) {
@@ -57,10 +60,14 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   double* U = wvu;
   if (c->d_minv) {
     U = wvu + c->wvu_rows * (int64_t)ldw;
-    if (s == 1)   // one right-hand side (outer PCG): memory-bound matrix-vector form
-      nspk::symv(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, c->stream);
-    else
+    if (s == 1) {   // one right-hand side (outer PCG): memory-bound matrix-vector form, tiles read once
+      double* P = U + c->wvu_rows * (int64_t)ldw;
+      P = (double*)(((uintptr_t)P + 255) & ~(uintptr_t)255);
+      if (getenv("NSP_SYMV2")) nspk::symv(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, c->stream);
+      else nspk::symv1(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, P, c->stream);
+    } else {
       nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream);
+    }
   } else {
     nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, wvu, ldw, cw, c->stream);
   }

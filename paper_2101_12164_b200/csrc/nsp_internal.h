@@ -229,6 +229,8 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
 // a2+a3 for one column (ld ldw, column 0): u_j = S_j^{-1} w_j, matrix-vector (s = 1)
 void symv(const FacSub* subs, const int2* items, int nitems, int max_ntb, const double* minv, const double* W, int ldw,
           double* U, cudaStream_t st);
+void symv1(const FacSub* subs, const int2* items, int nitems, int max_ntb, const double* minv, const double* W, int ldw,
+           double* U, double* P, cudaStream_t st);
 void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,
             int wbmax = -1);
 // partitioned narrow-band solve of the A_G factor: coupling-tile recurrence / parallel spike update

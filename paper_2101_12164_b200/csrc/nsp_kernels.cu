@@ -669,6 +669,82 @@ __global__ void __launch_bounds__(256) k_symv(const FacSub* __restrict__ subs, c
   }
 }
 
+// Same product reading every stored tile ONCE (k_symv reads each off-diagonal tile twice: as
+// (I, J) for row I and transposed for row J).  The CTA of stored tile row I multiplies each tile
+// (I, J), J <= I, from registers both ways: M_IJ w_J accumulates into output row I, and for J < I the
+// column product M_IJ^T w_I (8 warps' partial sums combined in fixed order) is written to the
+// partial slot P[(tile J) * max_ntb + I]; the row sum goes to P[(tile I) * max_ntb + I].
+// k_symv_reduce then forms u_J = sum_{I >= J} P[J][I] in ascending I (deterministic).
+__global__ void __launch_bounds__(256) k_symv1(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                               const double* __restrict__ minv, const double* __restrict__ W, int ldw,
+                                               int max_ntb, double* __restrict__ P) {
+  extern __shared__ double wv[];            // ntb x 64 right-hand side of the block
+  __shared__ double cpart[8][64];
+  const int2 it = items[blockIdx.x];
+  const FacSub sb = subs[it.x];
+  const int I = it.y, ntb = sb.ntb;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double* Mb = minv + sb.dense_off * NSP_TILE_ELEMS;
+  const double* Wb = W + sb.wvu_row * (int64_t)ldw;
+  const int64_t gt0 = sb.wvu_row / 64;
+  for (int e = tid; e < ntb * 64; e += 256) wv[e] = Wb[(int64_t)e * ldw];
+  __syncthreads();
+  const double* wI = wv + I * 64;
+  double r8[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r8[i] = 0.0;
+  for (int J = 0; J <= I; ++J) {
+    const double* T = Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS;
+    const double* v = wv + J * 64;
+    const double v0 = v[lane], v1 = v[lane + 32];
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = warp * 8 + i;
+      const double t0 = __ldg(T + row * 64 + lane), t1 = __ldg(T + row * 64 + lane + 32);
+      r8[i] = fma(t0, v0, fma(t1, v1, r8[i]));
+      const double wr = wI[row];
+      c0 = fma(t0, wr, c0);
+      c1 = fma(t1, wr, c1);
+    }
+    if (J < I) {
+      cpart[warp][lane] = c0;
+      cpart[warp][lane + 32] = c1;
+      __syncthreads();
+      if (tid < 64) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sum += cpart[w][tid];
+        P[((gt0 + J) * max_ntb + I) * 64 + tid] = sum;
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r8[i] += __shfl_xor_sync(0xffffffffu, r8[i], o);
+  if (lane < 8) {
+    double mine = r8[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i)
+      if (lane == i) mine = r8[i];
+    P[((gt0 + I) * max_ntb + I) * 64 + warp * 8 + lane] = mine;
+  }
+}
+
+__global__ void k_symv_reduce(const FacSub* __restrict__ subs, const int2* __restrict__ items, int max_ntb,
+                              const double* __restrict__ P, double* __restrict__ U, int ldw) {
+  const int2 it = items[blockIdx.x];
+  const FacSub sb = subs[it.x];
+  const int J = it.y, ntb = sb.ntb;
+  const int64_t gt = sb.wvu_row / 64 + J;
+  const double* p = P + gt * max_ntb * 64 + threadIdx.x;
+  double sum = 0.0;
+  for (int I = J; I < ntb; ++I) sum += p[I * 64];
+  U[(sb.wvu_row + (int64_t)J * 64 + threadIdx.x) * ldw] = sum;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Generic batched forward + backward triangular solves on tiled factors (one system per blockIdx.x,
 // column chunks on blockIdx.y): dense lower tiles (wb < 0: tile(I,J) = T + I(I+1)/2 + J) or band
@@ -1457,6 +1533,21 @@ void symv(const FacSub* subs, const int2* items, int nitems, int max_ntb, const 
     }
   }
   { nsp_count_launch(); k_symv<<<nitems, 256, smem, st>>>(subs, items, minv, W, ldw, U); }
+}
+
+void symv1(const FacSub* subs, const int2* items, int nitems, int max_ntb, const double* minv, const double* W, int ldw,
+           double* U, double* P, cudaStream_t st) {
+  if (nitems <= 0) return;
+  const size_t smem = (size_t)max_ntb * 64 * sizeof(double);
+  if (smem > 48 * 1024) {
+    static size_t attr = 0;
+    if (attr < smem) {
+      cudaFuncSetAttribute(k_symv1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
+  }
+  { nsp_count_launch(); k_symv1<<<nitems, 256, smem, st>>>(subs, items, minv, W, ldw, max_ntb, P); }
+  { nsp_count_launch(); k_symv_reduce<<<nitems, 64, 0, st>>>(subs, items, max_ntb, P, U, ldw); }
 }
 
 void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw, cudaStream_t st) {
