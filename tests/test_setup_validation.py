@@ -10,7 +10,7 @@ from nsp_inputs import problems as P
 from paper_2101_12164_b200 import nsp
 
 
-def _setup(rowptr, colidx, val, part, K):
+def _setup(rowptr, colidx, val, part, K, **opts):
     lib = nsp.load_library()
     rp = np.ascontiguousarray(rowptr, dtype=np.int64)
     ci = np.ascontiguousarray(colidx, dtype=np.int32)
@@ -19,6 +19,8 @@ def _setup(rowptr, colidx, val, part, K):
     csr = nsp.nsp_csr(rp.size - 1, rp.ctypes.data, ci.ctypes.data, va.ctypes.data)
     o = nsp.nsp_opts()
     lib.nsp_default_opts(C.byref(o))
+    for k, v in opts.items():
+        setattr(o, k, v)
     ctx = C.c_void_p()
     st = lib.nsp_setup(C.byref(csr), pa.ctypes.data, K, C.byref(o), C.byref(ctx), None)
     msg = lib.nsp_last_error(ctx).decode()
@@ -73,3 +75,11 @@ def test_asymmetric(cfg1):
 def test_empty_matrix():
     st, msg = _setup(np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0), np.zeros(0, np.int32), 1)
     assert st == -1, msg
+
+
+@pytest.mark.parametrize("field,value", [("ag_order", 2), ("ag_order", -1), ("ag_solver", 3), ("nys_form", 4),
+                                         ("nys_form", -1)])
+def test_option_ranges(cfg1, field, value):
+    """Out-of-range options (opts.ag_order 0..1, ag_solver 0..2, nys_form 0..3) are rejected on the host."""
+    st, msg = _setup(cfg1.A.rowptr, cfg1.A.colidx, cfg1.A.val, cfg1.part, cfg1.K, **{field: value})
+    assert st == -1 and field in msg, msg
