@@ -30,6 +30,19 @@ int main(int argc, char** argv) {
   cudaStream_t st; cudaStreamCreate(&st);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   const double flops = 2.0 * nsub * (ntb * 64.0) * (ntb * 64.0) * ld;
+  for (int nit : {74, 148, 222, 296, 370, 444, 448}) {
+    float best = 1e9;
+    for (int r = 0; r < 8; ++r) {
+      cudaMemsetAsync(flush, r, 256 << 20, st);
+      cudaEventRecord(e0, st);
+      nspk::symm(dsub, dit, nit, dM, dW, dU, ld, 32, st);
+      cudaEventRecord(e1, st); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      if (r >= 3) best = std::min(best, ms);
+    }
+    printf("items %d (CTAs %d, waves %.2f): %.1f us, %.2f us per CTA-wave\n", nit, 4 * nit, 4.0 * nit / 296, best * 1e3,
+           best * 1e3 / ((4 * nit + 295) / 296));
+  }
   for (int cw : {64, 32}) {
     float best = 1e9, tot = 0;
     for (int r = 0; r < 13; ++r) {
