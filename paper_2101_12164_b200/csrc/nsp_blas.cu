@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256 * GKS) k_gram_partial(const double* __rest
                                                       int ldb, int ntn1, int64_t n,
                                                       int64_t rows_per_chunk, double* __restrict__ part, int ntm,
                                                       int ntn) {
+  pdl_wait();
   extern __shared__ double sm[];
   constexpr int STG = 2 * GR * LDS;
   const int tile = blockIdx.x;
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(256 * GKS) k_gram_partial(const double* __rest
 // in fixed order (deterministic)
 __global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int ntm, int ntn, int ntn1,
                               double* out, double* out2, int ldo) {
+  pdl_wait();
   __shared__ double red[4][16][17];
   const int i = blockIdx.y * 16 + threadIdx.y;
   const int j = blockIdx.x * 16 + threadIdx.x;
@@ -157,6 +159,7 @@ __global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int 
 // blockIdx.z selects one of two independent argument sets (X += P alpha and R -= Q alpha in one launch).
 // normpart (optional): normpart[rowtile * ldo + c] = sum over the tile's rows of Out[r][c]^2.
 __global__ void __launch_bounds__(256) k_panel(PanelArgs pa0, PanelArgs pa1, int kdim, int64_t n) {
+  pdl_wait();
   const PanelArgs& pa = blockIdx.z ? pa1 : pa0;
   double* Out = pa.Out;
   const int ldo = pa.ldo, ldc = pa.ldc, ldi = pa.ldi, ldm = pa.ldm;
@@ -227,6 +230,7 @@ __global__ void __launch_bounds__(256) k_panel(PanelArgs pa0, PanelArgs pa1, int
 
 // column sums of squares of X (n x s), partial per 64-row tile (fixed order)
 __global__ void k_colsq_partial(const double* __restrict__ X, int ldx, int64_t n, int s, double* part, int ldp) {
+  pdl_wait();
   const int c = threadIdx.x;
   const int64_t r0 = blockIdx.x * 64ll;
   if (c >= ldp) return;
@@ -242,6 +246,7 @@ __global__ void k_colsq_partial(const double* __restrict__ X, int ldx, int64_t n
 // sum over row tiles -> out[c]; thread (c, g) sums tiles t = g mod 8 in order, then the 8
 // group sums are added in fixed order (deterministic)
 __global__ void k_colsq_reduce(const double* __restrict__ part, int ntiles, int ldp, double* out) {
+  pdl_wait();
   __shared__ double red[8][128];
   const int c = threadIdx.x, g = threadIdx.y;
   double s = 0.0;
@@ -259,6 +264,7 @@ __global__ void k_colsq_reduce(const double* __restrict__ part, int ntiles, int 
 // convergence: relres_j = sqrt(rsq_j) / bnorm_j; max over j < s (columns with bnorm 0 count as 0)
 __global__ void k_converge(const double* rsq, const double* bnorm, int s, double tol, BcgStatus* st,
                            double* hist_slot) {
+  pdl_wait();
   __shared__ double red[256];
   double m = 0.0;
   bool bad = false;
@@ -538,6 +544,7 @@ __device__ int g_eig_sweeps;
 __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ Ain, int lda, int n,
                                                     double* Vwork, int ldv, double* lam, double* Vsorted,
                                                     const int* gate) {
+  pdl_wait();
   (void)Vwork;
   (void)ldv;
   if (gate && *gate == 0) return;
@@ -706,6 +713,7 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
 // T[:, k] = V[:, k] / sqrt(lam_k) for k < width, zero otherwise.
 __global__ void k_orth_from_eig(const double* lam, const double* Vs, int n, int sp, double tau, double* T,
                                 BcgStatus* st) {
+  pdl_wait();
   if (!st->fallback) return;
   __shared__ int w;
   if (threadIdx.x == 0) {
@@ -826,9 +834,9 @@ void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb
   }
   {
     nsp_count_launch();
-    k_gram_partial<<<dim3(ntm * ntn, nch), 256 * GKS, smem, st>>>(Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn);
+    launch_k(k_gram_partial, dim3(dim3(ntm * ntn, nch)), dim3(256 * GKS), smem, st, Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn);
   }
-  { nsp_count_launch(); k_gram_reduce<<<dim3(ntn * 4, ntm * 4), dim3(16, 16, 4), 0, st>>>(ws, nch, ntm, ntn, ntn1, out, out2, ldo); }
+  { nsp_count_launch(); launch_k(k_gram_reduce, dim3(dim3(ntn * 4, ntm * 4)), dim3(dim3(16, 16, 4)), 0, st, ws, nch, ntm, ntn, ntn1, out, out2, ldo); }
 }
 
 void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, int64_t n, double* out, int ldo,
@@ -845,7 +853,7 @@ void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64
     attr = true;
   }
   dim3 grid((unsigned)((n + 63) / 64), (ncols + 63) / 64, a1 ? 2 : 1);
-  { nsp_count_launch(); k_panel<<<grid, 256, smem, st>>>(a0, a1 ? *a1 : a0, kdim, n); }
+  { nsp_count_launch(); launch_k(k_panel, dim3(grid), dim3(256), smem, st, a0, a1 ? *a1 : a0, kdim, n); }
 }
 
 void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
@@ -856,12 +864,12 @@ void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, i
 
 void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st) {
   const int nt = (int)std::max<int64_t>(1, (n + 63) / 64);   // n = 0 (a rank with no Gram rows): zeros
-  { nsp_count_launch(); k_colsq_partial<<<nt, ldp, 0, st>>>(X, ldx, n, s, part, ldp); }
-  { nsp_count_launch(); k_colsq_reduce<<<1, dim3(128, 8), 0, st>>>(part, nt, ldp, out); }
+  { nsp_count_launch(); launch_k(k_colsq_partial, dim3(nt), dim3(ldp), 0, st, X, ldx, n, s, part, ldp); }
+  { nsp_count_launch(); launch_k(k_colsq_reduce, dim3(1), dim3(dim3(128, 8)), 0, st, part, nt, ldp, out); }
 }
 
 void colsq_reduce(const double* part, int ntiles, int ldp, double* out, cudaStream_t st) {
-  { nsp_count_launch(); k_colsq_reduce<<<1, dim3(128, 8), 0, st>>>(part, ntiles, ldp, out); }
+  { nsp_count_launch(); launch_k(k_colsq_reduce, dim3(1), dim3(dim3(128, 8)), 0, st, part, ntiles, ldp, out); }
 }
 
 void sqrt_vec(const double* in, double* out, int n, cudaStream_t st) {
@@ -870,7 +878,7 @@ void sqrt_vec(const double* in, double* out, int n, cudaStream_t st) {
 
 void converge(const double* rsq, const double* bnorm, int s, double tol, BcgStatus* stt, double* hist_slot,
               cudaStream_t st) {
-  { nsp_count_launch(); k_converge<<<1, 256, 0, st>>>(rsq, bnorm, s, tol, stt, hist_slot); }
+  { nsp_count_launch(); launch_k(k_converge, dim3(1), dim3(256), 0, st, rsq, bnorm, s, tol, stt, hist_slot); }
 }
 
 void small_chol(const double* A, int sp, int mode, int nact, double tau, double* Out, BcgStatus* stt,
@@ -887,12 +895,12 @@ void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* 
   const int rp = (ne + g - 1) / g;
   const size_t smem = (size_t)(ne * (ne + 1) / 2 + ne * rp) * sizeof(double);
   set_smem((const void*)k_small_eig, smem);
-  { nsp_count_launch(); k_small_eig<<<g, 1024, smem, st>>>(A, lda, n, Vwork, ldv, lam, Vsorted, gate); }
+  { nsp_count_launch(); launch_k(k_small_eig, dim3(g), dim3(1024), smem, st, A, lda, n, Vwork, ldv, lam, Vsorted, gate); }
 }
 
 void orth_from_eig(const double* lam, const double* Vs, int n, int sp, double tau, double* T, BcgStatus* stt,
                    cudaStream_t st) {
-  { nsp_count_launch(); k_orth_from_eig<<<1, 1024, 0, st>>>(lam, Vs, n, sp, tau, T, stt); }
+  { nsp_count_launch(); launch_k(k_orth_from_eig, dim3(1), dim3(1024), 0, st, lam, Vs, n, sp, tau, T, stt); }
 }
 
 void small_gemm(int m, int n, int k, double alpha, const double* A, int lda, bool ta, const double* B, int ldb,

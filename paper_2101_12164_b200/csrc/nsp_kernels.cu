@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __res
                                               const double* __restrict__ X, int ldx,
                                               const double* __restrict__ U, int ldu, int64_t split,
                                               double* __restrict__ Y, int ldy, int s, int mode, int zero_pad) {
+  pdl_wait();
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t rows, const int32_t* __res
                                               const double* __restrict__ X, int ldx,
                                               const double* __restrict__ U, int ldu, int64_t split,
                                               double* __restrict__ Y, int ldy, int mode, int zero_pad) {
+  pdl_wait();
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
   const int sub = threadIdx.x & (G - 1);
   double acc = 0.0;
@@ -565,6 +567,7 @@ template <int CW, int NS>
 __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, const int2* __restrict__ items,
                                               const double* __restrict__ minv, const double* __restrict__ W,
                                               double* __restrict__ U, int ldw) {
+  pdl_wait();
   constexpr int NF = CW / 16;
   constexpr int LDV = CW + 4;
   constexpr int STAGE = 64 * LDT + 64 * LDV;   // one (M tile, W tile) pair
@@ -678,6 +681,7 @@ __global__ void __launch_bounds__(256) k_symv(const FacSub* __restrict__ subs, c
 __global__ void __launch_bounds__(256) k_symv1(const FacSub* __restrict__ subs, const int2* __restrict__ items,
                                                const double* __restrict__ minv, const double* __restrict__ W, int ldw,
                                                int max_ntb, double* __restrict__ P) {
+  pdl_wait();
   extern __shared__ double wv[];            // ntb x 64 right-hand side of the block
   __shared__ double cpart[8][64];
   const int2 it = items[blockIdx.x];
@@ -735,6 +739,7 @@ __global__ void __launch_bounds__(256) k_symv1(const FacSub* __restrict__ subs, 
 
 __global__ void k_symv_reduce(const FacSub* __restrict__ subs, const int2* __restrict__ items, int max_ntb,
                               const double* __restrict__ P, double* __restrict__ U, int ldw) {
+  pdl_wait();
   const int2 it = items[blockIdx.x];
   const FacSub sb = subs[it.x];
   const int J = it.y, ntb = sb.ntb;
@@ -1372,17 +1377,17 @@ void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, i
   const unsigned blocks = (unsigned)((A.rows * 32 + 255) / 256);
   if (s == 1) {
     const unsigned b8 = (unsigned)((A.rows * 8 + 255) / 256);
-    { nsp_count_launch(); k_spmv<8><<<b8, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, mode, zero_pad); }
+    { nsp_count_launch(); launch_k(k_spmv<8>, dim3(b8), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, mode, zero_pad); }
     return;
   }
   if (s <= 32)
-    { nsp_count_launch(); k_spmm<1><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
+    { nsp_count_launch(); launch_k(k_spmm<1>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
   else if (s <= 64)
-    { nsp_count_launch(); k_spmm<2><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
+    { nsp_count_launch(); launch_k(k_spmm<2>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
   else if (s <= 128)
-    { nsp_count_launch(); k_spmm<4><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
+    { nsp_count_launch(); launch_k(k_spmm<4>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
   else
-    { nsp_count_launch(); k_spmm<8><<<blocks, 256, 0, st>>>(A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
+    { nsp_count_launch(); launch_k(k_spmm<8>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
 }
 
 void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,
@@ -1509,7 +1514,7 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
       cudaFuncSetAttribute(k_symm<64, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    { nsp_count_launch(); k_symm<64, NS><<<grid, 256, smem, st>>>(subs, items, minv, W, U, ldw); }
+    { nsp_count_launch(); launch_k(k_symm<64, NS>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw); }
   } else {
     const size_t smem = NS * (64 * LDT + 64 * (32 + 4)) * sizeof(double);
     static bool attr = false;
@@ -1517,7 +1522,7 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
       cudaFuncSetAttribute(k_symm<32, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    { nsp_count_launch(); k_symm<32, NS><<<grid, 256, smem, st>>>(subs, items, minv, W, U, ldw); }
+    { nsp_count_launch(); launch_k(k_symm<32, NS>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw); }
   }
 }
 
@@ -1546,8 +1551,8 @@ void symv1(const FacSub* subs, const int2* items, int nitems, int max_ntb, const
       attr = smem;
     }
   }
-  { nsp_count_launch(); k_symv1<<<nitems, 256, smem, st>>>(subs, items, minv, W, ldw, max_ntb, P); }
-  { nsp_count_launch(); k_symv_reduce<<<nitems, 64, 0, st>>>(subs, items, max_ntb, P, U, ldw); }
+  { nsp_count_launch(); launch_k(k_symv1, dim3(nitems), dim3(256), smem, st, subs, items, minv, W, ldw, max_ntb, P); }
+  { nsp_count_launch(); launch_k(k_symv_reduce, dim3(nitems), dim3(64), 0, st, subs, items, max_ntb, P, U, ldw); }
 }
 
 void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw, cudaStream_t st) {

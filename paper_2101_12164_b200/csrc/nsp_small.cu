@@ -153,6 +153,7 @@ __device__ __noinline__ bool warp_chol16(double* As, int c0, double* Xd, double*
 //          success: st->fallback = 0, st->width = nact.
 __global__ void __launch_bounds__(256) k_chol16(const double* __restrict__ Ain, int sp, int mode, int nact,
                                                 double tau, double* __restrict__ Lp, BcgStatus* st) {
+  pdl_wait();
   extern __shared__ double sm[];
   double* As = sm;                 // 128 x LDA
   double* Di = sm + 128 * LDA;     // 8 x 256: X_kk
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(256) k_chol16(const double* __restrict__ Ain, 
 __global__ void __launch_bounds__(128) k_chol_solve(const double* __restrict__ Lp, int sp,
                                                     const double* __restrict__ B, int ldb, double* __restrict__ Out,
                                                     int ldo, double sgn, int fwd, int bwd, const int* gate) {
+  pdl_wait();
   if (gate && *gate) return;
   extern __shared__ double sm[];
   const int LD = sp + 2;
@@ -394,7 +396,7 @@ void chol_fac(const double* A, int sp, int mode, int nact, double tau, double* L
     attr = true;
   }
   nsp_count_launch();
-  k_chol16<<<1, 256, smem, st>>>(A, sp, mode, nact, tau, Lp, stt);
+  launch_k(k_chol16, dim3(1), dim3(256), smem, st, A, sp, mode, nact, tau, Lp, stt);
 }
 
 void chol_solve(const double* Lp, int sp, const double* B, int ldb, double* Out, int ldo, double sgn, bool fwd,
@@ -407,7 +409,7 @@ void chol_solve(const double* Lp, int sp, const double* B, int ldb, double* Out,
     attr = true;
   }
   nsp_count_launch();
-  k_chol_solve<<<sp / 8, 128, smem, st>>>(Lp, sp, B, ldb, Out, ldo, sgn, fwd, bwd, gate);
+  launch_k(k_chol_solve, dim3(sp / 8), dim3(128), smem, st, Lp, sp, B, ldb, Out, ldo, sgn, fwd, bwd, gate);
 }
 
 }  // namespace nspb

@@ -226,6 +226,7 @@ static nsp_status op_precond(nsp_ctx* c, BcgWs& w, const double* R, double* Z, i
 // host loop (indefinite, non-finite, all directions deflated, converged, maxit).
 __global__ void k_bcg_loop_ctl(BcgStatus* st, double* hist, int* widths, int maxit,
                                cudaGraphConditionalHandle h) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int it = ++st->iters;          // completed iterations
   hist[it] = st->relres;
   widths[it - 1] = st->width;
