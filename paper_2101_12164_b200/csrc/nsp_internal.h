@@ -10,6 +10,10 @@
 
 #define NSP_TILE 64          // factor tile edge (rows = cols)
 #define NSP_TILE_ELEMS (NSP_TILE * NSP_TILE)
+// S_j^{-1} tiles are stored PADDED (64 rows x 68 doubles): one stored tile is one contiguous bulk copy
+// (TMA) into the bank-conflict-free shared-memory layout of the DMMA fragments
+#define NSP_MINV_LD 68
+#define NSP_MINV_TILE (NSP_TILE * NSP_MINV_LD)
 
 // Per-block factor layout (one entry per local block j, and one for A_G).
 // Local ordering of block j: [I1 (band order, n1 rows, padded to nt1*64)]

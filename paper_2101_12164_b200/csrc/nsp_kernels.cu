@@ -448,11 +448,12 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
   const int ntb = sb.ntb, C = blockIdx.y;
   if (C >= ntb) return;
   const double* T = dense + sb.dense_off * NSP_TILE_ELEMS;
-  double* Mb = minv + sb.dense_off * NSP_TILE_ELEMS;
+  double* Mb = minv + sb.dense_off * NSP_MINV_TILE;
   auto tile = [&](int I, int J) { return T + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS; };
-  auto vt = [&](int I) { return Mb + ((int64_t)I * (I + 1) / 2 + C) * NSP_TILE_ELEMS; };   // row tile I of the RHS
+  auto vt = [&](int I) { return Mb + ((int64_t)I * (I + 1) / 2 + C) * NSP_MINV_TILE; };   // row tile I of the RHS
   for (int I = C; I < ntb; ++I)
-    for (int e = threadIdx.x; e < 4096; e += 256) vt(I)[e] = (I == C && (e >> 6) == (e & 63)) ? 1.0 : 0.0;
+    for (int e = threadIdx.x; e < 4096; e += 256)
+      vt(I)[(e >> 6) * NSP_MINV_LD + (e & 63)] = (I == C && (e >> 6) == (e & 63)) ? 1.0 : 0.0;
   __threadfence_block();
   __syncthreads();
   double acc[2][NF][2];
@@ -460,14 +461,14 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
     acc_zero(acc);
     if (I > C) {
       cp_block(Ls0, LDT, tile(I, C), 64, 64, 64);
-      cp_block(Vs0, LDV, vt(C), 64, 64, 64);
+      cp_block(Vs0, LDV, vt(C), NSP_MINV_LD, 64, 64);
       cp_commit();
       for (int J = C, it = 0; J < I; ++J, ++it) {
         double* Lc = (it & 1) ? Ls1 : Ls0;
         double* Vc = (it & 1) ? Vs1 : Vs0;
         if (J + 1 < I) {
           cp_block((it & 1) ? Ls0 : Ls1, LDT, tile(I, J + 1), 64, 64, 64);
-          cp_block((it & 1) ? Vs0 : Vs1, LDV, vt(J + 1), 64, 64, 64);
+          cp_block((it & 1) ? Vs0 : Vs1, LDV, vt(J + 1), NSP_MINV_LD, 64, 64);
           cp_commit();
           cp_wait<1>();
         } else {
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
       }
     }
     cp_block(Ls0, LDT, tile(I, I), 64, 64, 64);
-    cp_block(Vs0, LDV, vt(I), 64, 64, 64);
+    cp_block(Vs0, LDV, vt(I), NSP_MINV_LD, 64, 64);
     cp_commit();
     cp_wait<0>();
     __syncthreads();
@@ -499,7 +500,7 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
 #pragma unroll
       for (int j = 0; j < NF; ++j) {
         const int r = acc_row<NF>(i), c = acc_col<NF>(j);
-        *reinterpret_cast<double2*>(vt(I) + r * 64 + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+        *reinterpret_cast<double2*>(vt(I) + r * NSP_MINV_LD + c) = make_double2(acc[i][j][0], acc[i][j][1]);
       }
     __threadfence_block();
     __syncthreads();
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
     acc_zero(acc);
     if (I < ntb - 1) {
       cp_block(Ls0, LDT, tile(I + 1, I), 64, 64, 64);
-      cp_block(Vs0, LDV, vt(I + 1), 64, 64, 64);
+      cp_block(Vs0, LDV, vt(I + 1), NSP_MINV_LD, 64, 64);
       cp_commit();
       int it = 0;
       for (int J = I + 1; J < ntb; ++J, ++it) {
@@ -516,7 +517,7 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
         double* Vc = (it & 1) ? Vs1 : Vs0;
         if (J + 1 < ntb) {
           cp_block((it & 1) ? Ls0 : Ls1, LDT, tile(J + 1, I), 64, 64, 64);
-          cp_block((it & 1) ? Vs0 : Vs1, LDV, vt(J + 1), 64, 64, 64);
+          cp_block((it & 1) ? Vs0 : Vs1, LDV, vt(J + 1), NSP_MINV_LD, 64, 64);
           cp_commit();
           cp_wait<1>();
         } else {
@@ -528,7 +529,7 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
       }
     }
     cp_block(Ls0, LDT, tile(I, I), 64, 64, 64);
-    cp_block(Vs0, LDV, vt(I), 64, 64, 64);
+    cp_block(Vs0, LDV, vt(I), NSP_MINV_LD, 64, 64);
     cp_commit();
     cp_wait<0>();
     __syncthreads();
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
 #pragma unroll
       for (int j = 0; j < NF; ++j) {
         const int r = acc_row<NF>(i), c = acc_col<NF>(j);
-        *reinterpret_cast<double2*>(vt(I) + r * 64 + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+        *reinterpret_cast<double2*>(vt(I) + r * NSP_MINV_LD + c) = make_double2(acc[i][j][0], acc[i][j][1]);
       }
     __threadfence_block();
     __syncthreads();
@@ -563,46 +564,54 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
 // serves two output rows; they meet in L2).  Same flops as the sweeps, half the factor bytes.
 // items[x] = (block, I); W, U: W/V/U-layout buffers (ld ldw), out of place.
 // ---------------------------------------------------------------------------------------------
-template <int CW, int NS>
+template <int CW>
 __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, const int2* __restrict__ items,
                                               const double* __restrict__ minv, const double* __restrict__ W,
                                               double* __restrict__ U, int ldw) {
   pdl_wait();
   constexpr int NF = CW / 16;
   constexpr int LDV = CW + 4;
-  constexpr int STAGE = 64 * LDT + 64 * LDV;   // one (M tile, W tile) pair
-  extern __shared__ double sm[];
+  constexpr int STAGE = NSP_MINV_TILE + 64 * LDV;   // one (M tile, W tile) pair
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[2];
   const int2 it = items[blockIdx.x];
   const FacSub sb = subs[it.x];
   const int I = it.y, ntb = sb.ntb;
   const int c0 = blockIdx.y * CW;
-  const double* Mb = minv + sb.dense_off * NSP_TILE_ELEMS;
+  const double* Mb = minv + sb.dense_off * NSP_MINV_TILE;
   const double* Wb = W + sb.wvu_row * (int64_t)ldw + c0;
   auto mt = [&](int J) {   // stored tile holding block (I, J) (transposed when J > I)
-    return J <= I ? Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS
-                  : Mb + ((int64_t)J * (J + 1) / 2 + I) * NSP_TILE_ELEMS;
+    return J <= I ? Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_MINV_TILE
+                  : Mb + ((int64_t)J * (J + 1) / 2 + I) * NSP_MINV_TILE;
   };
-  auto issue = [&](int J) {   // stage J % NS
-    double* Ms = sm + (J % NS) * STAGE;
-    cp_block(Ms, LDT, mt(J), 64, 64, 64);
-    cp_block(Ms + 64 * LDT, LDV, Wb + (int64_t)J * 64 * ldw, ldw, 64, CW);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // stage J & 1: the padded M tile by ONE bulk copy (TMA, completes on bar), the W tile by cp.async
+  auto issue = [&](int J) {
+    double* Ms = sm + (J & 1) * STAGE;
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      mbar_expect_copy(&bar[J & 1], Ms, mt(J), NSP_MINV_TILE * 8);
+    }
+    cp_block(Ms + NSP_MINV_TILE, LDV, Wb + (int64_t)J * 64 * ldw, ldw, 64, CW);
   };
   double acc[2][NF][2];
   acc_zero(acc);
-  // NS-stage cp.async pipeline: tiles J+1 .. J+NS-1 in flight while J is multiplied
-#pragma unroll
-  for (int p = 0; p < NS - 1; ++p) {
-    if (p < ntb) issue(p);
-    cp_commit();
-  }
+  issue(0);
+  cp_commit();
   for (int J = 0; J < ntb; ++J) {
-    cp_wait<NS - 2>();
-    __syncthreads();
-    if (J + NS - 1 < ntb) issue(J + NS - 1);
+    cp_wait<0>();
+    mbar_wait(&bar[J & 1], (J >> 1) & 1);
+    __syncthreads();   // stage J complete for every thread; stage J + 1 free (its last reader was J - 1)
+    if (J + 1 < ntb) issue(J + 1);
     cp_commit();
-    const double* Ms = sm + (J % NS) * STAGE;
-    if (J <= I) cta_mma<NF, false, false>(Ms, LDT, Ms + 64 * LDT, LDV, acc);
-    else cta_mma<NF, true, false>(Ms, LDT, Ms + 64 * LDT, LDV, acc);
+    const double* Ms = sm + (J & 1) * STAGE;
+    if (J <= I) cta_mma<NF, false, false>(Ms, NSP_MINV_LD, Ms + NSP_MINV_TILE, LDV, acc);
+    else cta_mma<NF, true, false>(Ms, NSP_MINV_LD, Ms + NSP_MINV_TILE, LDV, acc);
   }
   double* out = U + (sb.wvu_row + (int64_t)I * 64) * ldw + c0;
 #pragma unroll
@@ -631,7 +640,7 @@ __global__ void __launch_bounds__(256) k_symv(const FacSub* __restrict__ subs, c
   const FacSub sb = subs[it.x];
   const int I = it.y, ntb = sb.ntb;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, col = tid & 63, grp = tid >> 6;
-  const double* Mb = minv + sb.dense_off * NSP_TILE_ELEMS;
+  const double* Mb = minv + sb.dense_off * NSP_MINV_TILE;
   const double* Wb = W + sb.wvu_row * (int64_t)ldw;
   for (int e = tid; e < ntb * 64; e += 256) wv[e] = Wb[(int64_t)e * ldw];
   __syncthreads();
@@ -642,17 +651,17 @@ __global__ void __launch_bounds__(256) k_symv(const FacSub* __restrict__ subs, c
   for (int J = 0; J < ntb; ++J) {
     const double* v = wv + J * 64;
     if (J <= I) {
-      const double* T = Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS;
+      const double* T = Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_MINV_TILE;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const double* row = T + (warp * 8 + i) * 64;
+        const double* row = T + (warp * 8 + i) * NSP_MINV_LD;
         r8[i] = fma(__ldg(row + lane), v[lane], r8[i]);
         r8[i] = fma(__ldg(row + lane + 32), v[lane + 32], r8[i]);
       }
     } else {
-      const double* T = Mb + ((int64_t)J * (J + 1) / 2 + I) * NSP_TILE_ELEMS;
+      const double* T = Mb + ((int64_t)J * (J + 1) / 2 + I) * NSP_MINV_TILE;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) cacc = fma(__ldg(T + (grp * 16 + i) * 64 + col), v[grp * 16 + i], cacc);
+      for (int i = 0; i < 16; ++i) cacc = fma(__ldg(T + (grp * 16 + i) * NSP_MINV_LD + col), v[grp * 16 + i], cacc);
     }
   }
 #pragma unroll
@@ -688,7 +697,7 @@ __global__ void __launch_bounds__(256) k_symv1(const FacSub* __restrict__ subs, 
   const FacSub sb = subs[it.x];
   const int I = it.y, ntb = sb.ntb;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const double* Mb = minv + sb.dense_off * NSP_TILE_ELEMS;
+  const double* Mb = minv + sb.dense_off * NSP_MINV_TILE;
   const double* Wb = W + sb.wvu_row * (int64_t)ldw;
   const int64_t gt0 = sb.wvu_row / 64;
   for (int e = tid; e < ntb * 64; e += 256) wv[e] = Wb[(int64_t)e * ldw];
@@ -698,14 +707,14 @@ __global__ void __launch_bounds__(256) k_symv1(const FacSub* __restrict__ subs, 
 #pragma unroll
   for (int i = 0; i < 8; ++i) r8[i] = 0.0;
   for (int J = 0; J <= I; ++J) {
-    const double* T = Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_TILE_ELEMS;
+    const double* T = Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_MINV_TILE;
     const double* v = wv + J * 64;
     const double v0 = v[lane], v1 = v[lane + 32];
     double c0 = 0.0, c1 = 0.0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int row = warp * 8 + i;
-      const double t0 = __ldg(T + row * 64 + lane), t1 = __ldg(T + row * 64 + lane + 32);
+      const double t0 = __ldg(T + row * NSP_MINV_LD + lane), t1 = __ldg(T + row * NSP_MINV_LD + lane + 32);
       r8[i] = fma(t0, v0, fma(t1, v1, r8[i]));
       const double wr = wI[row];
       c0 = fma(t0, wr, c0);
@@ -1500,29 +1509,26 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
           int cw, cudaStream_t st) {
   if (nitems <= 0) return;
   dim3 grid(nitems, ldw / cw);
-  // 2-stage cp.async pipeline, one barrier per K step.  Measured on cfg2 shapes (tools/bench_symm.cu):
-  // 32-wide column chunks with 2 CTAs/SM 135 us (24.3 TFLOP/s) vs 64-wide 1 CTA/SM 156 us; 3 stages
-  // force 1 CTA/SM and are slower.
-#ifndef NSP_SYMM_STAGES
-#define NSP_SYMM_STAGES 2
-#endif
-  constexpr int NS = NSP_SYMM_STAGES;
+  // 2 stages: the padded M tile by one bulk copy (TMA) + the W tile by cp.async, one barrier per K step.
+  // Measured on cfg2 shapes (tools/bench_symm.cu, tools/bench_symm_tma.cu): 32-wide column chunks at
+  // 2 CTAs/SM 122.9 us (26.8 TFLOP/s; 135.1 us with the M tile by cp.async); 64-wide / 3-stage /
+  // half-tile variants are slower.
   if (cw == 64) {
-    const size_t smem = NS * (64 * LDT + 64 * (64 + 4)) * sizeof(double);
+    const size_t smem = 2 * (NSP_MINV_TILE + 64 * (64 + 4)) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_symm<64, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_symm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    { nsp_count_launch(); launch_k(k_symm<64, NS>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw); }
+    { nsp_count_launch(); launch_k(k_symm<64>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw); }
   } else {
-    const size_t smem = NS * (64 * LDT + 64 * (32 + 4)) * sizeof(double);
+    const size_t smem = 2 * (NSP_MINV_TILE + 64 * (32 + 4)) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_symm<32, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_symm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    { nsp_count_launch(); launch_k(k_symm<32, NS>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw); }
+    { nsp_count_launch(); launch_k(k_symm<32>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw); }
   }
 }
 

@@ -1205,7 +1205,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
     }
   // ---------------- explicit S_j^{-1} tiles for the one-product a2+a3 (opts.apply_kernel == 0)
   if (c->opts.apply_kernel == 0 && dense_tiles > 0) {
-    const size_t bytes = (size_t)dense_tiles * NSP_TILE_ELEMS * 8;
+    const size_t bytes = (size_t)dense_tiles * NSP_MINV_TILE * 8;
     size_t fr = 0, tot = 0;
     NSP_CUDA_TRY(c, cudaMemGetInfo(&fr, &tot));
     if (bytes < fr / 2) {   // otherwise stay with the L22 sweeps (apply_kernel 1)

@@ -15,7 +15,7 @@ int main(int argc, char** argv) {
     subs[j] = f; dense_tiles += ntb * (ntb + 1) / 2; rows += ntb * 64;
     for (int I = 0; I < ntb; ++I) items.push_back(make_int2(j, I));
   }
-  std::vector<double> M(dense_tiles * 4096), W(rows * ld);
+  std::vector<double> M(dense_tiles * NSP_MINV_TILE), W(rows * ld);
   std::mt19937_64 g(1); std::normal_distribution<double> nd;
   for (auto& x : M) x = nd(g);
   for (auto& x : W) x = nd(g);

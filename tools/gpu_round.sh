@@ -13,7 +13,7 @@ python -c "import __graft_entry__ as g; g.build(); g.smoke()" > "$OUT/smoke.log"
 timeout 1500 python -m pytest tests -q -m gpu -x > "$OUT/pytest_gpu.log" 2>&1; echo "pytest exit $?" >> "$OUT/pytest_gpu.log"
 timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench exit $?" >> "$OUT/bench.err"
 SHORT="python bench.py --steps 1 --warmup 3 --apply-reps 2 --no-cpu-baseline"
-$SHORT > "$OUT/short_plain.log" 2>&1 && \
+$SHORT > "$OUT/short_plain.log" 2>&1 && NSP_GRAPH=1 \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv \
       --log-file "$OUT/launches.csv" $SHORT > "$OUT/ncu_launches.log" 2>&1
 echo "ncu launches exit $?" >> "$OUT/ncu_launches.log"
