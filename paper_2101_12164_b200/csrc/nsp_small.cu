@@ -63,6 +63,46 @@ __device__ __noinline__ bool warp_chol16(double* As, int c0, double* Xd, double*
   }
   bool ok = true;
   WPROF(1)
+#ifndef NSP_CHOL_NOPIPE
+  // software-pipelined: the owner of row c+1 forms the next pivot from its own registers right after
+  // column c is scaled (d_{c+1} = a_{c+1,c+1} - l_{c+1,c}^2, bitwise the value the trailing update
+  // below produces), so the next pivot broadcast + rsqrt overlap this column's smem broadcast/update.
+  double d = __shfl_sync(0xffffffffu, v[0], 0);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const int hc = c >> 3, qc = c & 7;
+    const double held = v[qc];
+    if (lane == 0) piv[c0 + c] = d;
+    if (!(d > 0.0)) {
+      ok = false;
+      d = 1.0;
+    }
+    const double rs = rsqrt_nr(d);
+    double lv = 0.0;   // L(r, c) on the lanes holding column c (zero above the diagonal)
+    if (h == hc) lv = (r > c) ? held * rs : ((r == c) ? d * rs : 0.0);
+    double dnext = 0.0;
+    if (c < 15) {
+      const int c1 = c + 1, h1 = c1 >> 3, q1 = c1 & 7;
+      const double l1 = __shfl_sync(0xffffffffu, lv, 2 * c1 + hc);    // L(c+1, c)
+      const double dn = fma(-l1, l1, v[q1]);                           // valid on lane 2(c+1)+h1
+      dnext = __shfl_sync(0xffffffffu, dn, 2 * c1 + h1);
+    }
+    if (h == hc) {
+      if (r >= c) v[qc] = lv;
+      colv[r] = lv;
+    }
+    if (lane == 0) invd[c] = rs;
+    __syncwarp();
+    const double li = colv[r];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = 8 * h + q;
+      if (j > c && j <= r) v[q] = fma(-li, colv[j], v[q]);
+    }
+    __syncwarp();
+    d = dnext;
+  }
+#else
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
     const int hc = c >> 3, qc = c & 7;
@@ -89,6 +129,7 @@ __device__ __noinline__ bool warp_chol16(double* As, int c0, double* Xd, double*
     }
     __syncwarp();
   }
+#endif
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int j = 8 * h + q;
