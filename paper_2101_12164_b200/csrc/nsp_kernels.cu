@@ -568,7 +568,6 @@ template <int CW>
 __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, const int2* __restrict__ items,
                                               const double* __restrict__ minv, const double* __restrict__ W,
                                               double* __restrict__ U, int ldw) {
-  pdl_wait();
   constexpr int NF = CW / 16;
   constexpr int LDV = CW + 4;
   constexpr int STAGE = NSP_MINV_TILE + 64 * LDV;   // one (M tile, W tile) pair
@@ -601,7 +600,11 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
   };
   double acc[2][NF][2];
   acc_zero(acc);
-  issue(0);
+  // the S_j^{-1} tiles are constant: stage 0's M tile is requested BEFORE waiting for the producer of
+  // W (programmatic dependent launch), so its latency hides behind the previous kernel's tail
+  if (threadIdx.x == 0) mbar_expect_copy(&bar[0], sm, mt(0), NSP_MINV_TILE * 8);
+  pdl_wait();
+  cp_block(sm + NSP_MINV_TILE, LDV, Wb, ldw, 64, CW);
   cp_commit();
   for (int J = 0; J < ntb; ++J) {
     cp_wait<0>();
