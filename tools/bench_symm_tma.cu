@@ -73,7 +73,7 @@ int main() {
     subs[j] = f; dense_tiles += ntb * (ntb + 1) / 2; rows += ntb * 64;
     for (int I = 0; I < ntb; ++I) items.push_back(make_int2(j, I));
   }
-  std::vector<double> M(dense_tiles * 4096), Mp(dense_tiles * TPAD, 0.0), W(rows * ld);
+  std::vector<double> M(dense_tiles * 4096), Mp(dense_tiles * TPAD, 0.0), W(rows * ld);   // library: padded
   std::mt19937_64 g(1); std::normal_distribution<double> nd;
   for (auto& x : M) x = nd(g);
   for (auto& x : W) x = nd(g);
@@ -92,19 +92,22 @@ int main() {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   const double flops = 2.0 * nsub * (ntb * 64.0) * (ntb * 64.0) * ld;
   const size_t smem = 2 * (TPAD + 64 * 36) * sizeof(double);
+  const size_t smem64 = 2 * (TPAD + 64 * 68) * sizeof(double);
   cudaFuncSetAttribute(k_symm_t<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int v = 0; v < 2; ++v) {
+  cudaFuncSetAttribute(k_symm_t<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64);
+  for (int v = 0; v < 3; ++v) {
     float best = 1e9;
     for (int r = 0; r < 13; ++r) {
       cudaMemsetAsync(flush, r, 256 << 20, st);
       cudaEventRecord(e0, st);
-      if (v == 0) nspk::symm(dsub, dit, (int)items.size(), dM, dW, dU, ld, 32, st);
-      else k_symm_t<32><<<dim3((unsigned)items.size(), ld / 32), 256, smem, st>>>(dsub, dit, dMp, dW, dU2, ld);
+      if (v == 0) nspk::symm(dsub, dit, (int)items.size(), dMp, dW, dU, ld, 32, st);
+      else if (v == 1) k_symm_t<32><<<dim3((unsigned)items.size(), ld / 32), 256, smem, st>>>(dsub, dit, dMp, dW, dU2, ld);
+      else k_symm_t<64><<<dim3((unsigned)items.size(), ld / 64), 256, smem64, st>>>(dsub, dit, dMp, dW, dU2, ld);
       cudaEventRecord(e1, st); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
       if (r >= 3) best = std::min(best, ms);
     }
-    printf("%s: best %.1f us (%.2f TFLOP/s)  %s\n", v ? "TMA-M (padded tiles)" : "k_symm<32,2>", best * 1e3,
+    printf("%s: best %.1f us (%.2f TFLOP/s)  %s\n", v == 2 ? "TMA-M cw 64" : v ? "TMA-M (padded tiles)" : "library k_symm", best * 1e3,
            flops / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   }
   std::vector<double> U(W.size()), U2(W.size());
