@@ -1225,6 +1225,96 @@ __device__ __forceinline__ int warp_reduce8_row(int lane) {
   return 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
 }
 
+// s > 1 (32-column chunks, ldw a multiple of 32 with zero padding columns): the P-step recurrence on
+// the DMMA pipe.  The spike tiles and the right-hand-side tiles do not depend on the recurrence, so
+// they stream through a 2-deep cp.async ring one step ahead; the running 64 x 32 coupling block stays
+// in shared memory.  One CTA per column chunk.
+__global__ void __launch_bounds__(256) k_spike_tail_mma(const double* __restrict__ spk,
+                                                        const int* __restrict__ chunk_first, int P, double* buf,
+                                                        int ldw, int fwd) {
+  pdl_wait();
+  constexpr int LDX = 36;
+  extern __shared__ __align__(16) double sm[];
+  double* Ss = sm;                       // 2 x 64 x LDT
+  double* Ys = sm + 2 * 64 * LDT;        // 2 x 64 x LDX (right-hand side tile of the step)
+  double* Xs = Ys + 2 * 64 * LDX;        // 64 x LDX: the previous step's result
+  const int c0 = blockIdx.x * 32;
+  const int nstep = P - 1;
+  auto tile_of = [&](int j) { return fwd ? chunk_first[j + 2] - 1 : chunk_first[P - 2 - j]; };
+  auto src_of = [&](int j) { return fwd ? chunk_first[j + 1] - 1 : chunk_first[P - 1 - j]; };
+  auto issue = [&](int j) {
+    const int t = tile_of(j);
+    cp_block(Ss + (j & 1) * 64 * LDT, LDT, spk + (int64_t)t * 4096, 64, 64, 64);
+    cp_block(Ys + (j & 1) * 64 * LDX, LDX, buf + (int64_t)t * 64 * ldw + c0, ldw, 64, 32);
+  };
+  cp_block(Xs, LDX, buf + (int64_t)src_of(0) * 64 * ldw + c0, ldw, 64, 32);
+  issue(0);
+  cp_commit();
+  double acc[2][2][2];
+  for (int j = 0; j < nstep; ++j) {
+    cp_wait<0>();
+    __syncthreads();
+    if (j + 1 < nstep) issue(j + 1);
+    cp_commit();
+    acc_zero(acc);
+    cta_mma<2, false, false>(Ss + (j & 1) * 64 * LDT, LDT, Xs, LDX, acc, 64);
+    __syncthreads();   // every read of Xs done
+    const double* Y = Ys + (j & 1) * 64 * LDX;
+    double* out = buf + (int64_t)tile_of(j) * 64 * ldw + c0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = acc_row<2>(i), c = acc_col<2>(q);
+        const double v0 = Y[r * LDX + c] - acc[i][q][0], v1 = Y[r * LDX + c + 1] - acc[i][q][1];
+        Xs[r * LDX + c] = v0;
+        Xs[r * LDX + c + 1] = v1;
+        *reinterpret_cast<double2*>(out + (int64_t)r * ldw + c) = make_double2(v0, v1);
+      }
+  }
+}
+
+// s > 1: every remaining tile row in parallel, grid (tile rows, 32-column chunks), DMMA product
+__global__ void __launch_bounds__(256) k_spike_update_mma(const double* __restrict__ spk,
+                                                          const int* __restrict__ chunk_first,
+                                                          const int* __restrict__ tile_chunk, int P, double* buf,
+                                                          int ldw, int fwd) {
+  pdl_wait();
+  constexpr int LDX = 36;
+  extern __shared__ __align__(16) double sm[];
+  double* Ss = sm;
+  double* Xs = sm + 64 * LDT;
+  const int I = blockIdx.x;
+  const int c0 = blockIdx.y * 32;
+  const int k = tile_chunk[I];
+  int src;
+  if (fwd) {
+    if (k == 0 || I == chunk_first[k + 1] - 1) return;
+    src = chunk_first[k] - 1;
+  } else {
+    if (k == P - 1 || I == chunk_first[k]) return;
+    src = chunk_first[k + 1];
+  }
+  cp_block(Ss, LDT, spk + (int64_t)I * 4096, 64, 64, 64);
+  cp_block(Xs, LDX, buf + (int64_t)src * 64 * ldw + c0, ldw, 64, 32);
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  double acc[2][2][2];
+  acc_zero(acc);
+  cta_mma<2, false, false>(Ss, LDT, Xs, LDX, acc, 64);
+  double* out = buf + (int64_t)I * 64 * ldw + c0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int r = acc_row<2>(i), c = acc_col<2>(q);
+      double2* o = reinterpret_cast<double2*>(out + (int64_t)r * ldw + c);
+      const double2 cur = *o;
+      *o = make_double2(cur.x - acc[i][q][0], cur.y - acc[i][q][1]);
+    }
+}
+
 // one column (s = 1, ld 1): the same P-step recurrence as a matrix-vector chain.  The spike tiles
 // do not depend on the recurrence, so they stream through a 2-deep TMA ring while the previous
 // step computes; the running 64-vector stays in shared memory; each warp owns 8 rows (coalesced
@@ -1472,6 +1562,16 @@ void spike_tail(const double* spk, const int* chunk_first, int P, double* buf, i
     { nsp_count_launch(); k_spike_tail_vec<<<1, 256, 2 * 4096 * 8, st>>>(spk, chunk_first, P, buf, fwd); }
     return;
   }
+  if (ldw % 32 == 0 && !getenv("NSP_SPIKE_OLD")) {
+    const size_t sm2 = (2 * 64 * LDT + 3 * 64 * 36) * sizeof(double);
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(k_spike_tail_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      attr2 = true;
+    }
+    { nsp_count_launch(); launch_k(k_spike_tail_mma, dim3(ldw / 32), dim3(256), sm2, st, spk, chunk_first, P, buf, ldw, fwd ? 1 : 0); }
+    return;
+  }
   { nsp_count_launch(); k_spike_tail<<<(s + 31) / 32, 256, smem, st>>>(spk, chunk_first, P, buf, ldw, s, fwd); }
 }
 
@@ -1480,6 +1580,16 @@ void spike_update(const double* spk, const int* chunk_first, const int* tile_chu
   if (P <= 1) return;
   if (s == 1 && ldw == 1) {
     { nsp_count_launch(); k_spike_update_vec<<<nt, 256, 0, st>>>(spk, chunk_first, tile_chunk, P, buf, fwd); }
+    return;
+  }
+  if (ldw % 32 == 0 && !getenv("NSP_SPIKE_OLD")) {
+    const size_t sm2 = (64 * LDT + 64 * 36) * sizeof(double);
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(k_spike_update_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      attr2 = true;
+    }
+    { nsp_count_launch(); launch_k(k_spike_update_mma, dim3(nt, ldw / 32), dim3(256), sm2, st, spk, chunk_first, tile_chunk, P, buf, ldw, fwd ? 1 : 0); }
     return;
   }
   const size_t smem = (64 * 65 + 64 * 33) * sizeof(double);   // attribute set with k_spike_tail (called first)
