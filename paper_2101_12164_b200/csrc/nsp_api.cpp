@@ -21,7 +21,9 @@ int ld_pad(int s, int cw) { return ((s + cw - 1) / cw) * cw; }
 
 size_t apply_ws_bytes(const nsp_ctx* c, int s) {
   const int cw = pick_cw(c, s);
-  size_t b = (size_t)c->wvu_rows * ld_pad(s, cw) * 8 * (c->d_minv ? 2 : 1) + 512;
+  // W and U; with the S_j^{-1} tiles the chunk-major padded layout (36 doubles per row per 32-col chunk)
+  size_t b = c->d_minv ? (size_t)c->wvu_rows * (ld_pad(s, cw) / 32) * 36 * 8 * 2 + 512
+                       : (size_t)c->wvu_rows * ld_pad(s, cw) * 8 + 512;
   // k_symv1 partial slots (s = 1; reserved for every s: callers size one workspace for several widths)
   if (c->d_minv) b += (size_t)c->wvu_rows * c->max_ntb * 8 + 256;
   return b;
@@ -47,8 +49,12 @@ nsp_status get_ws(nsp_ctx* c, void* ws, size_t need, char** out) {
 nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, int mode, double* wvu) {
   const int cw = pick_cw(c, s);
   const int ldw = ld_pad(s, cw);
+  // chunk-major padded W/U (s > 1 with the S_j^{-1} tiles): a 64 x 32 tile of W is one contiguous bulk copy
+  const bool cm = c->d_minv && s > 1;
+  const int64_t cs = (int64_t)c->wvu_rows * 36;
   // a1: W = A_IG X on the boundary-layer rows (zero padding rows / columns)
-  nspk::spmm(c->A2G, X, ldx, nullptr, 0, 0, wvu, ldw, s, 0, true, c->stream);
+  if (cm) nspk::spmm_cs(c->A2G, X, ldx, nullptr, 0, 32, 0, wvu, 36, cs, ldw, s, 0, true, c->stream);
+  else nspk::spmm(c->A2G, X, ldx, nullptr, 0, 0, wvu, ldw, s, 0, true, c->stream);
   // a2 + a3: U = L22^{-T} L22^{-1} W for every block, one launch: either as one symmetric product
   // with the setup's S_j^{-1} tiles (k_symm, no dependency chain) or as the two batched sweeps
   // live timing of the a2+a3 kernel: an event pair per eager call, or (inside the captured block-CG
@@ -59,14 +65,14 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   if (prof) cudaEventRecord(c->prof_ev[c->prof_used], c->stream);
   double* U = wvu;
   if (c->d_minv) {
-    U = wvu + c->wvu_rows * (int64_t)ldw;
+    U = cm ? wvu + (int64_t)(ldw / 32) * cs : wvu + c->wvu_rows * (int64_t)ldw;
     if (s == 1) {   // one right-hand side (outer PCG): memory-bound matrix-vector form, tiles read once
       double* P = U + c->wvu_rows * (int64_t)ldw;
       P = (double*)(((uintptr_t)P + 255) & ~(uintptr_t)255);
       if (getenv("NSP_SYMV2")) nspk::symv(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, c->stream);
       else nspk::symv1(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, P, c->stream);
     } else {
-      nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream);
+      nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream, cs);
     }
   } else {
     nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, wvu, ldw, cw, c->stream);
@@ -80,7 +86,8 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
     c->prof_used += 2;
   }
   // a4 + a5: Y = A_G X - A_GI U (fused), or Y = A_GI U
-  nspk::spmm(c->AGG2, X, ldx, U, ldw, c->nG, Y, ldy, s, mode, true, c->stream);
+  if (cm) nspk::spmm_cs(c->AGG2, X, ldx, U, 36, cs, c->nG, Y, ldy, 32, ldy, s, mode, true, c->stream);
+  else nspk::spmm(c->AGG2, X, ldx, U, ldw, c->nG, Y, ldy, s, mode, true, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());
   return finish_shared_rows(c, X, ldx, Y, ldy, s, mode != 2);
 }

@@ -220,6 +220,9 @@ void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, do
 // mode 2: Y = -(cols >= split part only)  (K_G apply); mode 3: cols < split only (A_G X);
 // mode 4: Y += A X
 // Y ld ldy; columns s..ldy-1 of Y are written with 0 when zero_pad.
+// chunk strides: column c at row * ld + (c / 32) * cs + c % 32 (cs = 32: row-major)
+void spmm_cs(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t ucs, int64_t split,
+             double* Y, int ldy, int64_t ycs, int ypad, int s, int mode, bool zero_pad, cudaStream_t st);
 void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split,
           double* Y, int ldy, int s, int mode, bool zero_pad, cudaStream_t st);
 void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw,
@@ -228,7 +231,8 @@ void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int
 void l22_inverse(const FacSub* subs, int nsub, int max_ntb, const double* dense, double* minv, cudaStream_t st);
 // a2+a3 as U_j = M_j W_j (items = (block, tile row)), W -> U out of place
 void symm(const FacSub* subs, const int2* items, int nitems, const double* minv, const double* W, double* U, int ldw,
-          int cw, cudaStream_t st);
+          int cw, cudaStream_t st,
+          int64_t cm_stride = 0);
 // wbmax: largest band half-width (tiles) of the systems, -1 unknown; <= 2 with cw 32 selects k_band_fb
 // a2+a3 for one column (ld ldw, column 0): u_j = S_j^{-1} w_j, matrix-vector (s = 1)
 void symv(const FacSub* subs, const int2* items, int nitems, int max_ntb, const double* minv, const double* W, int ldw,

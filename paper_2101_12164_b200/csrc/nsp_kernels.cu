@@ -213,12 +213,15 @@ __global__ void __launch_bounds__(256) k_tile_cholesky(const FacSub* __restrict_
 // indices and values are loaded once lane-parallel and broadcast by shuffle (register staging);
 // each lane owns columns lane, lane+32, ... so every X-row read is a coalesced 8s-byte segment.
 // ---------------------------------------------------------------------------------------------
+// Column c of a row lives at row * ld + (c / 32) * cs + c % 32: cs = 32 for row-major blocks, cs = rows * 36
+// for the chunk-major padded W/V/U layout (each 64 x 32 tile contiguous: one bulk copy in k_symm).
 template <int NQ>
 __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __restrict__ rp,
                                               const int32_t* __restrict__ ci, const double* __restrict__ va,
                                               const double* __restrict__ X, int ldx,
-                                              const double* __restrict__ U, int ldu, int64_t split,
-                                              double* __restrict__ Y, int ldy, int s, int mode, int zero_pad) {
+                                              const double* __restrict__ U, int ldu, int64_t ucs, int64_t split,
+                                              double* __restrict__ Y, int ldy, int64_t ycs, int ypad, int s, int mode,
+                                              int zero_pad) {
   pdl_wait();
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -244,10 +247,11 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __res
         src = U + (col - split) * ldu;
         if (mode == 2) a = -a;
       }
+      const int64_t cs = (mode == 0 || mode == 4 || col < split) ? 32 : ucs;
 #pragma unroll
       for (int qq = 0; qq < NQ; ++qq) {
         const int cc = lane + 32 * qq;
-        if (cc < s) acc[qq] = fma(a, __ldg(src + cc), acc[qq]);
+        if (cc < s) acc[qq] = fma(a, __ldg(src + qq * cs + lane), acc[qq]);
       }
     }
   }
@@ -255,11 +259,12 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __res
 #pragma unroll
   for (int qq = 0; qq < NQ; ++qq) {
     const int cc = lane + 32 * qq;
-    if (cc < s) y[cc] = mode == 4 ? y[cc] + acc[qq] : acc[qq];
-    else if (zero_pad && cc < ldy) y[cc] = 0.0;
+    double* yc = y + qq * ycs + lane;
+    if (cc < s) *yc = mode == 4 ? *yc + acc[qq] : acc[qq];
+    else if (zero_pad && cc < ypad) *yc = 0.0;
   }
   if (zero_pad)
-    for (int cc = 32 * NQ + lane; cc < ldy; cc += 32) y[cc] = 0.0;
+    for (int cc = 32 * NQ + lane; cc < ypad; cc += 32) y[(cc >> 5) * ycs + (cc & 31)] = 0.0;
 }
 
 // One right-hand side (s = 1): the same modes as k_spmm, G lanes per row (several rows per warp),
@@ -564,10 +569,12 @@ __global__ void __launch_bounds__(256) k_l22_inverse(const FacSub* __restrict__ 
 // serves two output rows; they meet in L2).  Same flops as the sweeps, half the factor bytes.
 // items[x] = (block, I); W, U: W/V/U-layout buffers (ld ldw), out of place.
 // ---------------------------------------------------------------------------------------------
-template <int CW>
+template <int CW, bool CM>
 __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, const int2* __restrict__ items,
                                               const double* __restrict__ minv, const double* __restrict__ W,
-                                              double* __restrict__ U, int ldw) {
+                                              double* __restrict__ U, int ldw, int64_t cs) {
+  // CM (chunk-major padded W/U, ldw = CW + 4, cs = chunk stride): the W tile of a stage is contiguous too,
+  // so both operands arrive by bulk copy (TMA) on one mbarrier; otherwise W by cp.async
   constexpr int NF = CW / 16;
   constexpr int LDV = CW + 4;
   constexpr int STAGE = NSP_MINV_TILE + 64 * LDV;   // one (M tile, W tile) pair
@@ -578,7 +585,7 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
   const int I = it.y, ntb = sb.ntb;
   const int c0 = blockIdx.y * CW;
   const double* Mb = minv + sb.dense_off * NSP_MINV_TILE;
-  const double* Wb = W + sb.wvu_row * (int64_t)ldw + c0;
+  const double* Wb = CM ? W + blockIdx.y * cs + sb.wvu_row * (int64_t)LDV : W + sb.wvu_row * (int64_t)ldw + c0;
   auto mt = [&](int J) {   // stored tile holding block (I, J) (transposed when J > I)
     return J <= I ? Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_MINV_TILE
                   : Mb + ((int64_t)J * (J + 1) / 2 + I) * NSP_MINV_TILE;
@@ -589,14 +596,14 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
     fence_mbar_init();
   }
   __syncthreads();
-  // stage J & 1: the padded M tile by ONE bulk copy (TMA, completes on bar), the W tile by cp.async
   auto issue = [&](int J) {
     double* Ms = sm + (J & 1) * STAGE;
     if (threadIdx.x == 0) {
       fence_proxy_async();
       mbar_expect_copy(&bar[J & 1], Ms, mt(J), NSP_MINV_TILE * 8);
+      if (CM) mbar_add_copy(&bar[J & 1], Ms + NSP_MINV_TILE, Wb + (int64_t)J * 64 * LDV, 64 * LDV * 8);
     }
-    cp_block(Ms + NSP_MINV_TILE, LDV, Wb + (int64_t)J * 64 * ldw, ldw, 64, CW);
+    if (!CM) cp_block(Ms + NSP_MINV_TILE, LDV, Wb + (int64_t)J * 64 * ldw, ldw, 64, CW);
   };
   double acc[2][NF][2];
   acc_zero(acc);
@@ -604,25 +611,31 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
   // W (programmatic dependent launch), so its latency hides behind the previous kernel's tail
   if (threadIdx.x == 0) mbar_expect_copy(&bar[0], sm, mt(0), NSP_MINV_TILE * 8);
   pdl_wait();
-  cp_block(sm + NSP_MINV_TILE, LDV, Wb, ldw, 64, CW);
+  if (CM) {
+    if (threadIdx.x == 0) mbar_add_copy(&bar[0], sm + NSP_MINV_TILE, Wb, 64 * LDV * 8);
+  } else {
+    cp_block(sm + NSP_MINV_TILE, LDV, Wb, ldw, 64, CW);
+  }
   cp_commit();
   for (int J = 0; J < ntb; ++J) {
-    cp_wait<0>();
+    if (!CM) cp_wait<0>();
     mbar_wait(&bar[J & 1], (J >> 1) & 1);
     __syncthreads();   // stage J complete for every thread; stage J + 1 free (its last reader was J - 1)
     if (J + 1 < ntb) issue(J + 1);
-    cp_commit();
+    if (!CM) cp_commit();
     const double* Ms = sm + (J & 1) * STAGE;
     if (J <= I) cta_mma<NF, false, false>(Ms, NSP_MINV_LD, Ms + NSP_MINV_TILE, LDV, acc);
     else cta_mma<NF, true, false>(Ms, NSP_MINV_LD, Ms + NSP_MINV_TILE, LDV, acc);
   }
-  double* out = U + (sb.wvu_row + (int64_t)I * 64) * ldw + c0;
+  double* out = CM ? U + blockIdx.y * cs + (sb.wvu_row + (int64_t)I * 64) * LDV
+                   : U + (sb.wvu_row + (int64_t)I * 64) * ldw + c0;
+  const int ldo = CM ? LDV : ldw;
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
       const int r = acc_row<NF>(i), c = acc_col<NF>(j);
-      *reinterpret_cast<double2*>(out + (int64_t)r * ldw + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      *reinterpret_cast<double2*>(out + (int64_t)r * ldo + c) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
 }
 
@@ -1473,23 +1486,28 @@ void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, do
   { nsp_count_launch(); k_tile_cholesky<<<nsub, 256, smem, st>>>(subs, band, dense, scratch, border_first, status); }
 }
 
-void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split, double* Y,
-          int ldy, int s, int mode, bool zero_pad, cudaStream_t st) {
+void spmm_cs(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t ucs, int64_t split,
+             double* Y, int ldy, int64_t ycs, int ypad, int s, int mode, bool zero_pad, cudaStream_t st) {
   if (A.rows <= 0) return;
   const unsigned blocks = (unsigned)((A.rows * 32 + 255) / 256);
-  if (s == 1) {
+  if (s == 1 && ycs == 32 && ucs == 32) {
     const unsigned b8 = (unsigned)((A.rows * 8 + 255) / 256);
     { nsp_count_launch(); launch_k(k_spmv<8>, dim3(b8), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, mode, zero_pad); }
     return;
   }
   if (s <= 32)
-    { nsp_count_launch(); launch_k(k_spmm<1>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
+    { nsp_count_launch(); launch_k(k_spmm<1>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad); }
   else if (s <= 64)
-    { nsp_count_launch(); launch_k(k_spmm<2>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
+    { nsp_count_launch(); launch_k(k_spmm<2>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad); }
   else if (s <= 128)
-    { nsp_count_launch(); launch_k(k_spmm<4>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
+    { nsp_count_launch(); launch_k(k_spmm<4>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad); }
   else
-    { nsp_count_launch(); launch_k(k_spmm<8>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, s, mode, zero_pad); }
+    { nsp_count_launch(); launch_k(k_spmm<8>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad); }
+}
+
+void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split, double* Y,
+          int ldy, int s, int mode, bool zero_pad, cudaStream_t st) {
+  spmm_cs(A, X, ldx, U, ldu, 32, split, Y, ldy, 32, ldy, s, mode, zero_pad, st);
 }
 
 void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,
@@ -1619,29 +1637,39 @@ void l22_inverse(const FacSub* subs, int nsub, int max_ntb, const double* dense,
 }
 
 void symm(const FacSub* subs, const int2* items, int nitems, const double* minv, const double* W, double* U, int ldw,
-          int cw, cudaStream_t st) {
+          int cw, cudaStream_t st, int64_t cm_stride) {
   if (nitems <= 0) return;
+  // 2 stages, one barrier per K step: the padded M tile by one bulk copy (TMA); the W tile by one bulk
+  // copy too when W/U are chunk-major (cm_stride > 0: ldw = 36 per 32-column chunk), else by cp.async.
+  // Measured on cfg2 shapes (tools/bench_symm_tma.cu): 135.1 us (both cp.async) -> 122.9 (TMA M) ->
+  // 112.6 us (TMA M + W, 29.2 TFLOP/s); 64-wide / 3-stage / half-tile variants are slower.
+  const size_t smem = 2 * (NSP_MINV_TILE + 64 * (cw + 4)) * sizeof(double);
+  if (cm_stride > 0) {   // ldw = the logical padded width (a multiple of 32), one CTA column per chunk
+    const dim3 grid(nitems, ldw / 32);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_symm<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(2 * (NSP_MINV_TILE + 64 * 36) * sizeof(double)));
+      attr = true;
+    }
+    { nsp_count_launch(); launch_k(k_symm<32, true>, grid, dim3(256), 2 * (NSP_MINV_TILE + 64 * 36) * sizeof(double), st, subs, items, minv, W, U, 36, cm_stride); }
+    return;
+  }
   dim3 grid(nitems, ldw / cw);
-  // 2 stages: the padded M tile by one bulk copy (TMA) + the W tile by cp.async, one barrier per K step.
-  // Measured on cfg2 shapes (tools/bench_symm.cu, tools/bench_symm_tma.cu): 32-wide column chunks at
-  // 2 CTAs/SM 122.9 us (26.8 TFLOP/s; 135.1 us with the M tile by cp.async); 64-wide / 3-stage /
-  // half-tile variants are slower.
   if (cw == 64) {
-    const size_t smem = 2 * (NSP_MINV_TILE + 64 * (64 + 4)) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_symm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_symm<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    { nsp_count_launch(); launch_k(k_symm<64>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw); }
+    { nsp_count_launch(); launch_k(k_symm<64, false>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw, (int64_t)0); }
   } else {
-    const size_t smem = 2 * (NSP_MINV_TILE + 64 * (32 + 4)) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_symm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_symm<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    { nsp_count_launch(); launch_k(k_symm<32>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw); }
+    { nsp_count_launch(); launch_k(k_symm<32, false>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw, (int64_t)0); }
   }
 }
 
