@@ -50,11 +50,7 @@ constexpr int LDS = 68;    // smem stride for 64-wide tiles
 // through a GNS-stage cp.async ring of 32-row slabs (one barrier per slab), so the slab loads are
 // in flight GNS-1 slabs ahead of the DMMA work.
 constexpr int GNS = NSP_GNS;
-#ifndef NSP_GKS
-#define NSP_GKS 1
-#endif
-constexpr int GKS = NSP_GKS;   // warp groups splitting each slab's rows (8 warps per group)
-__global__ void __launch_bounds__(256 * GKS) k_gram_partial(const double* __restrict__ Xa, int lda,
+__global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__ Xa, int lda,
                                                       const double* __restrict__ Xb, const double* __restrict__ Xb2,
                                                       int ldb, int ntn1, int64_t n,
                                                       int64_t rows_per_chunk, double* __restrict__ part, int ntm,
@@ -64,7 +60,6 @@ __global__ void __launch_bounds__(256 * GKS) k_gram_partial(const double* __rest
   constexpr int STG = 2 * GR * LDS;
   const int tile = blockIdx.x;
   const int tm = tile / ntn, tn = tile - tm * ntn;
-  const int w8 = (threadIdx.x >> 5) & 7, kgrp = threadIdx.x >> 8;
   const int64_t r0 = blockIdx.y * rows_per_chunk;
   const int64_t r1 = min(n, r0 + rows_per_chunk);
   double acc[2][4][2];
@@ -86,45 +81,17 @@ __global__ void __launch_bounds__(256 * GKS) k_gram_partial(const double* __rest
   for (int q = 0; q < nslab; ++q) {
     cp_wait<GNS - 2>();
     __syncthreads();
-#ifndef NSP_GRAM_NOLOAD
     if (q + GNS - 1 < nslab) issue(q + GNS - 1);
-#endif
     cp_commit();
     const double* st = sm + (q % GNS) * STG;
-    constexpr int KR = GR / GKS;   // slab rows per warp group
-    cta_mma<4, true, false>(st + kgrp * KR * LDS, LDS, st + GR * LDS + kgrp * KR * LDS, LDS, acc, KR, w8);
+    cta_mma<4, true, false>(st, LDS, st + GR * LDS, LDS, acc, GR);
   }
   double* out = part + ((int64_t)blockIdx.y * ntm * ntn + tile) * 4096;
-  if (GKS > 1) {   // groups 1.. park their partial tiles in (now idle) shared memory, group 0 sums in order
-    cp_wait<0>();
-    __syncthreads();
-    if (kgrp > 0)
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int rr = acc_row<4>(i, w8), cc = acc_col<4>(j, w8);
-          *reinterpret_cast<double2*>(sm + (kgrp - 1) * 4096 + rr * 64 + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
-        }
-    __syncthreads();
-    if (kgrp > 0) return;
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int rr = acc_row<4>(i, w8), cc = acc_col<4>(j, w8);
-        for (int q2 = 0; q2 < GKS - 1; ++q2) {
-          const double2 v = *reinterpret_cast<const double2*>(sm + q2 * 4096 + rr * 64 + cc);
-          acc[i][j][0] += v.x;
-          acc[i][j][1] += v.y;
-        }
-      }
-  }
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int rr = acc_row<4>(i, w8), cc = acc_col<4>(j, w8);
+      const int rr = acc_row<4>(i), cc = acc_col<4>(j);
       *reinterpret_cast<double2*>(out + rr * 64 + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
 }
@@ -834,7 +801,7 @@ void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb
   }
   {
     nsp_count_launch();
-    launch_k(k_gram_partial, dim3(dim3(ntm * ntn, nch)), dim3(256 * GKS), smem, st, Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn);
+    launch_k(k_gram_partial, dim3(dim3(ntm * ntn, nch)), dim3(256), smem, st, Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn);
   }
   { nsp_count_launch(); launch_k(k_gram_reduce, dim3(dim3(ntn * 4, ntm * 4)), dim3(dim3(16, 16, 4)), 0, st, ws, nch, ntm, ntn, ntn1, out, out2, ldo); }
 }
