@@ -364,6 +364,8 @@ def make(name: str) -> Problem:
     # small analogues
     if name == "cfg2s":
         return _grid_problem("cfg2s", (160, 160), 16, 24, 8, 1e-1, 1e-8, coef=[1.0, 1e-3])
+    if name == "cfg2m":   # mid-size 2-D analogue whose A_G band solve is partitioned (spikes)
+        return _grid_problem("cfg2m", (384, 384), 16, 24, 8, 1e-1, 1e-8, coef=[1.0, 1e-3])
     if name == "cfg3s":
         return _grid_problem("cfg3s", (24, 24, 24), 8, 12, 4, 1e-1, None, kind="lognormal")
     if name == "cfg4s":

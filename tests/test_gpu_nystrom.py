@@ -268,3 +268,44 @@ def test_m2_pcg_with_chebyshev_ag(name):
     ctx.pcg(dev(b), x2, 0.0, io["iters"], precond=2)
     assert relfro(x2.cpu().numpy(), xo) <= 1e-8
     ctx.close()
+
+
+@pytest.mark.parametrize("spikes", [True, False])
+def test_ag_partitioned_band_parity(spikes, monkeypatch):
+    """The partitioned ("spike") A_G band solve (nt >= 16 tile rows, band <= 1 tile: cfg2m) against the
+    oracle's direct solve and against the unpartitioned sweep (NSP_NO_SPIKE=1): s = 1 (matrix-vector
+    chain kernels), 7 and 64 (DMMA spike recurrence / update), relative error <= 1e-12."""
+    if not spikes:
+        monkeypatch.setenv("NSP_NO_SPIKE", "1")
+    pr, d, S = problem("cfg2m")
+    assert d.n_gamma >= 16 * 64
+    ctx = context(pr, factor_gamma=True, ag_solver=1)
+    assert 0 < ctx.stats()["ag_bw"] <= 64        # band of at most one tile: the partition applies
+    for s in [1, 7, 64]:
+        X = block(d.n_gamma, s, seed=13)
+        Y = torch.empty(d.n_gamma, s, dtype=torch.float64, device="cuda")
+        ctx.precond_apply(1, dev(X), Y)
+        assert relfro(Y.cpu().numpy(), S.solve_AG(X)) <= 1e-12, s
+        # the halves (M_1): R^{-T} then R^{-1} gives A_G^{-1} too
+        Z = torch.empty_like(Y)
+        W = torch.empty_like(Y)
+        ctx.precond_apply(3, dev(X), Z)
+        ctx.precond_apply(4, Z, W)
+        assert relfro(W.cpu().numpy(), S.solve_AG(X)) <= 1e-12, s
+    ctx.close()
+
+
+def test_bcg_paper_analog_cfg2m():
+    """Block CG with M = A_G^{-1} (reading C2) through the partitioned band solve at s = 32: iteration
+    count within +-1 of the oracle, iterates at equal counts within 1e-8."""
+    pr, d, S = problem("cfg2m")
+    B = S.k_gamma(pr.omega())
+    Xo, io = O.bf_bcg(S.apply, B, pr.tol_bcg, 500, S.solve_AG)
+    ctx = context(pr, bcg_precond=1)
+    X = torch.zeros(d.n_gamma, pr.s, dtype=torch.float64, device="cuda")
+    rep = ctx.block_cg(dev(B), X, pr.tol_bcg, 500)
+    assert rep["converged"] and abs(rep["iters"] - io["iters"]) <= 1, (rep["iters"], io["iters"])
+    X2 = torch.zeros_like(X)
+    ctx.block_cg(dev(B), X2, 0.0, io["iters"])
+    assert relfro(X2.cpu().numpy(), Xo) <= 1e-8
+    ctx.close()
