@@ -259,6 +259,9 @@ void nsp_destroy(nsp_ctx* c) {
   if (c->d_bhist) cudaFree(c->d_bhist);
   if (c->d_bwidth) cudaFree(c->d_bwidth);
   if (c->gstream) cudaStreamDestroy(c->gstream);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   for (DevCSR* m : {&c->A2G, &c->AGG2, &c->AGSH, &c->CB, &c->C1, &c->AII}) {
     fr(m->rowptr);
     fr(m->col);

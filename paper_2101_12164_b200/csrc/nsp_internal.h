@@ -192,6 +192,8 @@ struct nsp_ctx {
   PcgKey pcg_key;
   long long pcg_graph_kernels = 0;
   cudaStream_t gstream = nullptr;
+  cudaStream_t side_stream = nullptr;   // block CG: the deferred X update (forked, joined before orth)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool capturing = false;          // block CG is capturing its iteration graph
   bool gprof_in_graph = false;     // the cached graph records gprof_ev around a2+a3
   cudaEvent_t gprof_ev[2] = {nullptr, nullptr};

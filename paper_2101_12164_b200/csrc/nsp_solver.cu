@@ -153,7 +153,8 @@ static int64_t gram_rows(const nsp_ctx* c) { return (c->nranks <= 1 || c->rank =
 static int64_t gram_rows(const nsp_ctx* c, const BcgWs& w) { return w.kind ? w.n : gram_rows(c); }
 
 // orth(Wm): Gram, Cholesky-QR with pivot test, eigen fallback; P = Wm T (reading C3)
-static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Pout) {
+static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Pout,
+                       cudaEvent_t join_before_panel = nullptr) {
   const int sp = w.sp;
   const int64_t n = w.n;
   cudaStream_t st = c->stream;
@@ -165,6 +166,7 @@ static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Po
   nspb::chol_solve(w.Ldi, sp, nullptr, 0, w.T, sp, 1.0, false, true, &w.st->fallback, st);
   nspb::small_eig(w.G, sp, s, w.Vw, sp + 1, w.lam, w.Vs, &w.st->fallback, st);
   nspb::orth_from_eig(w.lam, w.Vs, s, sp, c->opts.orth_tau, w.T, w.st, st);
+  if (join_before_panel) NSP_CUDA_TRY(c, cudaStreamWaitEvent(st, join_before_panel, 0));   // X += P alpha done
   nspb::panel(Pout, sp, nullptr, 0, Wm, sp, w.T, sp, sp, sp, n, 1.0, nullptr, st);
   return NSP_OK;
 }
@@ -286,11 +288,8 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     tr.mark("chol_D");
     nspb::chol_solve(w.Ld, sp, w.E, sp, w.al, sp, 1.0, true, true, nullptr, q);   // alpha = D^{-1} E
     tr.mark("alpha");
-    {
-      PanelArgs px{w.X, sp, w.X, sp, w.P, sp, w.al, sp, 1.0, nullptr};
-      PanelArgs pr{w.R, sp, w.R, sp, w.Q, sp, w.al, sp, -1.0, multi ? nullptr : w.npart};
-      nspb::panel2(px, &pr, sp, sp, n, q);
-    }
+    // R -= Q alpha here; X += P alpha is deferred to the next tail (x_update), off the critical path
+    nspb::panel(w.R, sp, w.R, sp, w.Q, sp, w.al, sp, sp, sp, n, -1.0, multi ? nullptr : w.npart, q);
     if (multi) {
       nspb::colsq(w.R, sp, ng, s, sp, w.npart, w.rsq, q);
       if ((e2 = comm_allreduce(c, w.rsq, sp)) != NSP_OK) return e2;
@@ -303,10 +302,34 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     NSP_CUDA_TRY(c, cudaGetLastError());
     return NSP_OK;
   };
-  // tail: a9-a11 (Z = M R, F = Q^T Z, beta, W = Z + P beta, P = orth(W))
+  // X += P alpha of the previous head.  X is read by nothing inside the loop, so (single rank, no
+  // tracing) the panel runs on a side stream forked from the context stream and joined only before
+  // orth overwrites P: it overlaps the tail's small s x s kernels.  Inside a captured graph the
+  // fork / join become graph edges.
+  const char* xfe = getenv("NSP_XFORK");
+  const bool xfork = !multi && !tr.on && !(xfe && xfe[0] == '0');
+  if (xfork) {
+    if (!c->side_stream) NSP_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    if (!c->ev_fork) NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    if (!c->ev_join) NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
+  auto x_update = [&](bool fork) -> nsp_status {
+    PanelArgs px{w.X, sp, w.X, sp, w.P, sp, w.al, sp, 1.0, nullptr};
+    if (!fork) {
+      nspb::panel2(px, nullptr, sp, sp, n, c->stream);
+      return NSP_OK;
+    }
+    NSP_CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
+    NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+    nspb::panel2(px, nullptr, sp, sp, n, c->side_stream);
+    NSP_CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side_stream));
+    return NSP_OK;
+  };
+  // tail: a9-a11 (X += P alpha, Z = M R, F = Q^T Z, beta, W = Z + P beta, P = orth(W))
   auto tail = [&]() -> nsp_status {
     cudaStream_t q = c->stream;
     nsp_status e2;
+    if ((e2 = x_update(xfork)) != NSP_OK) return e2;
     if (usem && (e2 = op_precond(c, w, w.R, w.Z, s)) != NSP_OK) return e2;
     nspb::gram(w.Q, sp, sp, Zr, sp, sp, ng, w.F, sp, w.gram, q);
     if ((e2 = comm_allreduce(c, w.F, (size_t)sp * sp)) != NSP_OK) return e2;
@@ -314,7 +337,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     tr.mark("beta");
     nspb::panel(w.W, sp, Zr, sp, w.P, sp, w.be, sp, sp, sp, n, 1.0, nullptr, q);
     tr.mark("W");
-    if ((e2 = orth(c, w, w.W, s, w.P)) != NSP_OK) return e2;
+    if ((e2 = orth(c, w, w.W, s, w.P, xfork ? c->ev_join : nullptr)) != NSP_OK) return e2;
     tr.mark("orth");
     return NSP_OK;
   };
@@ -328,6 +351,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     const GraphKey key{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau};
     if (c->bcg_graph && c->bcg_key == key) gexec = c->bcg_graph;
   }
+  const bool heads_run = !hs->converged && maxit > 0;
   if (hs->converged) {
     ret = NSP_OK;
   } else {
@@ -533,6 +557,10 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     }
   }
 copy_out:
+  // the last head's X += P alpha (every earlier one ran in the following tail)
+  if (heads_run) {
+    if ((e = x_update(false)) != NSP_OK) return e;
+  }
   // copy X out
   nspb::copy_pad(w.X, sp, Xout, ldx, n, s, 1.0, st);
   tr.mark("end");
