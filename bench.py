@@ -277,11 +277,10 @@ def run_ours(args, ws, rank, local):
     if ws > 1:
         torch.distributed.barrier()
     launches0 = nsp.kernel_launches()
-    ctx.profile(True)
-    ctx.profile_read()
     times, iters = [], []
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    # the timed region runs the production path (the device-driven loop graph, no per-kernel events)
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
@@ -291,9 +290,18 @@ def run_ours(args, ws, rank, local):
             torch.cuda.synchronize()
             times.append(ev0.elapsed_time(ev1))
             iters.append(rep["iters"])
+    launches = (nsp.kernel_launches() - launches0) / args.steps
+    # live duration of the dominant kernel: the same K steps again with a CUDA event pair around every
+    # a2+a3 launch on the context stream (the loop then runs as one graph per iteration, which carries
+    # the event pair; the events bracket only that kernel)
+    ctx.profile(True)
+    ctx.profile_read()
+    for _ in range(args.steps):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
     sweep_ms, sweeps = ctx.profile_read()
     ctx.profile(False)
-    launches = (nsp.kernel_launches() - launches0) / args.steps
     # apply-only timing (K1/K2 pipeline), same stream, L2 flushed
     P_ = torch.randn(nG, s, dtype=torch.float64, device=dev)
     Q_ = torch.empty_like(P_)
@@ -404,6 +412,9 @@ def run_ours(args, ws, rank, local):
                      "algorithmic_bytes_per_launch": hbm_alg,
                      "peak_source": "fp64 DMMA microbenchmark tools/fp64_peak.cu (profiles/r01_fp64_peak.txt)",
                      "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": sweep_avg_ms,
+                     "timing": "CUDA events around each a2+a3 launch on the context stream, in a pass of the "
+                               "same K steps right after the timed region (the timed region itself runs "
+                               "the event-free device-driven loop graph)",
                      "launches": sweeps,
                      "hbm_gbs_at_alg_bytes": hbm_alg / (sweep_avg_ms * 1e-3) / 1e9,
                      "hbm_peak_gbs": peaks.get("hbm_gbs")},
