@@ -278,8 +278,29 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
     NSP_CUDA_TRY(c, cudaMemcpyAsync(z, r, (size_t)n * 8, cudaMemcpyDeviceToDevice, c->stream));
     return NSP_OK;
   }
+  // M_2: the low-rank coefficient g = Sigma Z^T r does not depend on A_G^{-1} r, so it runs on a forked
+  // side stream (a graph branch when captured) while the A_G solve - a latency-bound chain on a few
+  // SMs - runs on the context stream; z += Z g after the join
+  const bool fork2 = which == 2 && c->nys_rank > 0 && c->side_stream && c->ev_fork && c->ev_join;
+  if (fork2) {
+    NSP_CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
+    NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+    const unsigned nch = grid1(n, GT_ROWS);
+    nsp_count_launch();
+    k_gemvt_partial<<<nch, 256, 0, c->side_stream>>>(c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart);
+    nsp_count_launch();
+    k_gemvt_reduce<<<1, 1024, 0, c->side_stream>>>(w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
+    NSP_CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side_stream));
+  }
   nsp_status e = ag_solve(c, r, 1, z, 1, 1, w.agbuf);
   if (e != NSP_OK) return e;
+  if (fork2) {
+    NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    nsp_count_launch();
+    k_gemv_add<<<grid1(n * 32, 256), 256, 0, c->stream>>>(c->d_Z, c->nys_ld, w.g, c->nys_rank, n, z);
+    NSP_CUDA_TRY(c, cudaGetLastError());
+    return NSP_OK;
+  }
   if (which == 3 && c->nys_rank > 0) {
     // M_A-DEF2 r = A_G^{-1} r + Z E^{-1} Z^T (r - S_G A_G^{-1} r),  E = Z^T S_G Z (reading R5)
     const int kp = c->nys_ld, rk = c->nys_rank;
@@ -333,6 +354,14 @@ static nsp_status read_st(nsp_ctx* c, BcgStatus* d, BcgStatus* h) {
 nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxit, int precond, PcgWs& w,
                     nsp_report* rep) {
   cudaStream_t st = c->stream;
+  {
+    const char* xfe = getenv("NSP_XFORK");
+    if (precond == 2 && !(xfe && xfe[0] == '0')) {   // side stream for the M_2 low-rank branch
+      if (!c->side_stream) NSP_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+      if (!c->ev_fork) NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      if (!c->ev_join) NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+  }
   const int64_t n = c->nG;
   BcgStatus* hs = (BcgStatus*)c->h_status;
   nsp_status e;
