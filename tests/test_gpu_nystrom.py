@@ -309,3 +309,44 @@ def test_bcg_paper_analog_cfg2m():
     ctx.block_cg(dev(B), X2, 0.0, io["iters"])
     assert relfro(X2.cpu().numpy(), Xo) <= 1e-8
     ctx.close()
+
+
+@pytest.mark.parametrize("name,kfix", [("cfg1", 3), ("cfg5s", 4)])
+def test_nystrom_m1_power_parity(name, kfix):
+    """M_1 (nys_form 3, natural-order R_G) with q = 1 power step (eq:power on R_G^{-T} B_H R_G^{-1}): Sigma
+    and M_1 probes at equal inner counts within 1e-8 of oracle.nystrom.nystrom_m1(q=1)."""
+    from oracle.nystrom import apply_M1
+    pr, d, S = problem(name)
+    Om = pr.omega()
+    ref = O.nystrom_m1(S, Om, pr.rank, 0.0, kfix, q=1)
+    ctx = context(pr, factor_gamma=True, nys_form=3, ag_order=1, nys_power=1)
+    rep = ctx.nystrom(pr.rank, pr.oversample, dev(Om), 0.0, kfix)
+    assert rep["iters"] == 2 * kfix and rep["rank"] == ref.rank
+    sig = ctx.nystrom_sigma()
+    assert np.max(np.abs(sig - ref.sigma) / ref.sigma) <= 1e-8, (sig[:3], ref.sigma[:3])
+    R = block(d.n_gamma, 8, seed=29)
+    Y = torch.empty(d.n_gamma, 8, dtype=torch.float64, device="cuda")
+    ctx.precond_apply(2, dev(R), Y)
+    assert relfro(Y.cpu().numpy(), apply_M1(S, ref.Z, ref.sigma, R)) <= 1e-8
+    ctx.close()
+
+
+def test_m1_rcm_factor_pcg_cfg5s():
+    """M_1 with the default RCM-ordered factor (its Nystrom approximation differs from the oracle's by
+    the orthogonal similarity between the two R_G, reading R6): the outer PCG converges with a true
+    residual <= 1e-6 and within 20 % of the natural-order M_1's iteration count."""
+    pr, d, S = problem("cfg5s")
+    b = pr.rhs()
+    its = {}
+    for order in (0, 1):
+        ctx = context(pr, factor_gamma=True, nys_form=3, ag_order=order)
+        ctx.nystrom(pr.rank, pr.oversample, dev(pr.omega()), pr.tol_bcg, 500)
+        x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
+        rp = ctx.pcg(dev(b), x, 1e-8, 2000, precond=2)
+        assert rp["converged"]
+        A = pr.A.to_scipy()
+        xg = x.cpu().numpy()
+        assert np.linalg.norm(b - A @ xg) / np.linalg.norm(b) <= 1e-6
+        its[order] = rp["iters"]
+        ctx.close()
+    assert abs(its[0] - its[1]) <= max(2, 0.2 * its[1]), its
