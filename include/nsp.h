@@ -210,8 +210,11 @@ nsp_status nsp_precond_apply(nsp_ctx* ctx, int which, const double* X, double* Y
 /* Full solve A x = b through eq:A_LDLT: f = b_G - A_GI A_I^{-1} b_I; PCG on
  * S_G w = f (eq:Sx=b) with precond {0 none, 1 A_G^{-1} (S~_1), 2 M_2, 3 M_A-DEF2 =
  * A_G^{-1} + Z E^{-1} Z^T (I - S_G A_G^{-1}), E = Z^T S_G Z (the adapted-deflation variant of M_2,
- * eq:deflation_comp_from_low_rank / PAPER.md:961-962, reading R5; non-symmetric)}; x_I =
- * A_I^{-1}(b_I - A_IG w); un-permute.  b, x: device fp64[n] in ORIGINAL order.
+ * eq:deflation_comp_from_low_rank / PAPER.md:961-962, reading R5; non-symmetric)}; with
+ * opts.nys_form 2 / 3 the pair (2, 3) is (M_3, M_A-DEF3) / (M_1, M_A-DEF1) - the same forms built on
+ * that variant's Z; x_I = A_I^{-1}(b_I - A_IG w); un-permute.  b, x: device fp64[n] in ORIGINAL order.
+ * The iteration runs as one device-driven CUDA graph (single rank); rep->hist gets the recurrence
+ * residual of every iteration.  Single rank only (NSP_ERR_STATE for nranks > 1).
  * Returns NSP_ERR_STATE for 2 / 3 before nsp_nystrom. */
 nsp_status nsp_pcg(nsp_ctx* ctx, const double* b, double* x, double tol, int maxit, int precond,
                    void* ws, nsp_report* rep);
