@@ -61,6 +61,8 @@ def orth(W: np.ndarray, tau: float = 1e-14):
 
 def bf_bcg(apply_S, B: np.ndarray, tol: float, maxit: int, apply_M=None, tau: float = 1e-14,
            X0=None):
+    """Breakdown-free block (P)CG of the module docstring (reading C3 step by step,
+    stopping rule reading C4): returns (X, info) with info = iters, status, relres history, widths."""
     B = np.asarray(B, dtype=np.float64)
     n, s = B.shape
     X = np.zeros_like(B) if X0 is None else np.array(X0, dtype=np.float64)

@@ -27,14 +27,18 @@ class DBBD:
 
     @property
     def n_gamma(self) -> int:
+        """Size of the border Gamma (eq:perm_A PAPER.md:371-380)."""
         return int(self.gamma.size)
 
     @property
     def A_GI(self) -> list:
+        """The border rows A_{Gamma I_j} = A_{I_j Gamma}^T of eq:perm_A."""
         return [m.T.tocsr() for m in self.A_IG]
 
 
 def dbbd(A: sp.csr_matrix, part: np.ndarray, K: int) -> DBBD:
+    """Doubly bordered block diagonal form of A (eq:perm_A PAPER.md:371-380): the K interior blocks
+    A_I_j (part == j), the border Gamma (part == -1, ascending id; reading C10) and the couplings."""
     A = sp.csr_matrix(A)
     n = A.shape[0]
     if A.shape != (n, n):

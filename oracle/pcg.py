@@ -19,6 +19,8 @@ from .schur import SchurOracle
 
 
 def pcg(apply_S, f: np.ndarray, tol: float, maxit: int, apply_M=None, record_x=False):
+    """Preconditioned CG on S_Gamma w = f (the CG of PAPER.md:37-58 / eq:k-th_error_cg; the paper gives no
+    pseudo-code, so textbook PCG, reading C9): x_0 = 0, stop on ||r_k|| / ||f|| <= tol (recurrence residual)."""
     f = np.asarray(f, dtype=np.float64)
     x = np.zeros_like(f)
     r = f.copy()
@@ -55,6 +57,8 @@ def pcg(apply_S, f: np.ndarray, tol: float, maxit: int, apply_M=None, record_x=F
 
 
 def solve_full_system(S: SchurOracle, b: np.ndarray, tol: float, maxit: int, apply_M=None):
+    """Full solve A x = b through the block factorisation eq:A_LDLT and eq:Sx=b
+    (PAPER.md:415-420): f = b_G - A_GI A_I^{-1} b_I, PCG on S_Gamma w = f, x_I = A_I^{-1}(b_I - A_IG w)."""
     d = S.d
     b = np.asarray(b, dtype=np.float64)
     b_G = b[d.gamma]

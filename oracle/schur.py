@@ -32,17 +32,20 @@ class SchurOracle:
 
     # --- A_I_j^{-1} -----------------------------------------------------
     def lu_block(self, j: int):
+        """Factor A_I_j (sparse LU as a library primitive; "factorized cheaply in parallel")."""
         if j not in self._lu:
             self._lu[j] = _lu(self.d.A_I[j]) if self.d.A_I[j].shape[0] > 0 else None
         return self._lu[j]
 
     def solve_AI_block(self, j: int, R: np.ndarray) -> np.ndarray:
+        """A_I_j^{-1} R with the block factor."""
         lu = self.lu_block(j)
         if lu is None:
             return np.zeros_like(R)
         return lu.solve(np.ascontiguousarray(R))
 
     def A_GI(self, j: int) -> sp.csr_matrix:
+        """A_{Gamma I_j} = A_{I_j Gamma}^T (eq:perm_A PAPER.md:371-380)."""
         if self._A_GI is None:
             self._A_GI = [None] * self.d.K
         if self._A_GI[j] is None:
@@ -51,6 +54,7 @@ class SchurOracle:
 
     # --- K_G X = A_GI A_I^{-1} A_IG X -------------------------------------
     def k_gamma(self, X: np.ndarray) -> np.ndarray:
+        """K_Gamma X = sum_j A_GI_j A_I_j^{-1} A_I_j_G X (reading C1, the A_Gamma-free part of eq:schur_complement)."""
         X = np.asarray(X, dtype=np.float64)
         out = np.zeros((self.d.n_gamma,) + X.shape[1:])
         for j in range(self.d.K):
@@ -63,6 +67,7 @@ class SchurOracle:
 
     # --- S_G X (eq:schur_complement) ---------------------------------------
     def apply(self, X: np.ndarray) -> np.ndarray:
+        """S_Gamma X = A_Gamma X - K_Gamma X (eq:schur_complement PAPER.md:387-390), implicitly."""
         return self.d.A_G @ np.asarray(X, dtype=np.float64) - self.k_gamma(X)
 
     def apply_rows(self, X: np.ndarray, rows: np.ndarray) -> np.ndarray:
@@ -82,6 +87,7 @@ class SchurOracle:
 
     # --- explicit dense S_G (tiny cases only) ------------------------------
     def dense(self) -> np.ndarray:
+        """The explicit S_Gamma (eq:schur_complement PAPER.md:387-390) by dense elimination, tiny cases only."""
         S = self.d.A_G.toarray()
         for j in range(self.d.K):
             if self.d.A_I[j].shape[0] == 0:
@@ -93,12 +99,14 @@ class SchurOracle:
 
     # --- A_G^{-1} (eq:S1) ---------------------------------------------------
     def solve_AG(self, R: np.ndarray) -> np.ndarray:
+        """A_Gamma^{-1} R (S~_1 of eq:S1) by a direct sparse solve."""
         if self._lu_G is None:
             self._lu_G = _lu(self.d.A_G)
         return self._lu_G.solve(np.ascontiguousarray(R, dtype=np.float64))
 
     # --- A_I^{-1} on a full interior vector (block by block) ---------------
     def solve_AI(self, r_I: list) -> list:
+        """Block-diagonal A_I^{-1} applied block by block."""
         return [self.solve_AI_block(j, r_I[j]) for j in range(self.d.K)]
 
 

@@ -46,6 +46,9 @@ class SIOperator:
 def nystrom_schur_si(S: SchurOracle, Omega: np.ndarray, k: int, tol_inner: float = 0.1,
                      maxit_inner: int = 1000, precond: bool = True, tau: float = 1e-14,
                      eps_rel: float = 1e-12, q: int = 0) -> NystromResult:
+    """Alg. 2 with the paper-literal inner system: F = A_IG G, S_I X = F by the block
+    PCG preconditioned by A_I (eq:SI PAPER.md:814-819), Y = A_GI X,
+    then steps 5-12 as nystrom.nystrom_schur."""
     op = SIOperator(S)
     G = Omega
     its = []
