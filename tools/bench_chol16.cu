@@ -39,8 +39,9 @@ int main() {
          hb.fallback, hb.indefinite, hb.width, cudaGetErrorString(cudaGetLastError()));
   for (int r = 0; r < 3; ++r) nspb::chol_fac(dG, sp, 1, sp, 1e-14, dL, dst, st);
   cudaStreamSynchronize(st);
-  long long pr[64];
+  long long pr[128];
   cudaMemcpyFromSymbol(pr, g_chol_prof, sizeof(pr));
+  printf("warp_chol16 (block 1): load %lld  columns %lld  X %lld\n", pr[65] - pr[64], pr[66] - pr[65], pr[67] - pr[66]);
   printf("load %lld\n", pr[1] - pr[0]);
   long long prev = pr[1];
   for (int s = 0; s < 8; ++s) { printf("step %d: C+A %lld  panel %lld\n", s, pr[2 + 2 * s] - prev, pr[3 + 2 * s] - pr[2 + 2 * s]); prev = pr[3 + 2 * s]; }
