@@ -1025,187 +1025,6 @@ __global__ void __launch_bounds__(256) k_band_fb(const TriSys* __restrict__ sys,
 // quarter of the rows, the 4 partials meet in shared memory.  Same operations in a fixed order.
 // buf (ld 1) holds the right-hand side on entry and the solution on exit.
 // ---------------------------------------------------------------------------------------------
-template <int NS, int WBM>
-__global__ void __launch_bounds__(256) k_band_fb_vec(const TriSys* __restrict__ sys, double* buf, int fwd, int bwd) {
-  constexpr int NV = WBM + 1;
-  extern __shared__ __align__(128) double sm[];
-  double* Lr = sm;                          // NS x 4096 (contiguous 64 x 64 tiles)
-  double* Wr = sm + NS * 4096;              // NS x 64 (rhs tile of a diagonal step)
-  double* Vr = Wr + NS * 64;                // NV x 64
-  double* Pp = Vr + NV * 64;                // 4 x 64 column partials
-  double* Rs = Pp + 4 * 64;                 // 64 residual
-  __shared__ __align__(8) uint64_t bar[NS];
-  const TriSys sy = sys[blockIdx.x];
-  const int nt = sy.nt, wb = sy.wb;
-  if (nt == 0) return;
-  const double* T = sy.T;
-  double* Wb = buf + sy.row0;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int col = tid & 63, grp = tid >> 6;
-  auto tile = [&](int I, int J) -> const double* { return T + ((int64_t)J * (wb + 1) + (I - J)) * NSP_TILE_ELEMS; };
-  if (tid == 0)
-    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  __syncthreads();
-  unsigned uses[NS];   // completed phases per slot (thread-uniform)
-#pragma unroll
-  for (int i = 0; i < NS; ++i) uses[i] = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    const bool fw = pass == 0;
-    if (fw ? !fwd : !bwd) continue;
-    auto first_j = [&](int I) { return fw ? max(0, I - wb) : I + 1; };
-    auto last_off = [&](int I) { return fw ? I - 1 : min(nt - 1, I + wb); };
-    auto next_row = [&](int I) { return fw ? I + 1 : I - 1; };
-    int iI = fw ? 0 : nt - 1, iJ = first_j(iI), ip = 0;
-    auto issue = [&]() {   // one product's tiles into slot ip % NS (thread 0 issues)
-      if (fw ? iI >= nt : iI < 0) return;
-      const int sl = ip % NS;
-      if (iJ <= last_off(iI)) {
-        if (tid == 0) mbar_expect_copy(&bar[sl], Lr + sl * 4096, fw ? tile(iI, iJ) : tile(iJ, iI), 32768);
-        ++iJ;
-      } else {
-        if (tid == 0) {
-          mbar_expect_copy(&bar[sl], Lr + sl * 4096, tile(iI, iI), 32768);
-          mbar_add_copy(&bar[sl], Wr + sl * 64, Wb + (int64_t)iI * 64, 512);
-        }
-        iI = next_row(iI);
-        iJ = (fw ? iI < nt : iI >= 0) ? first_j(iI) : 0;
-      }
-      ++ip;
-    };
-    for (int p = 0; p < NS - 1; ++p) issue();
-    int I = fw ? 0 : nt - 1, J = first_j(I);
-    double racc = 0.0;   // forward: lane j of warp w holds the sum of row 8w + j (after reduction)
-    double cacc = 0.0;   // backward: column partial (col, grp)
-    for (int q = 0;; ++q) {
-      if (fw ? I >= nt : I < 0) break;
-      const int sl = q % NS;
-      mbar_wait(&bar[sl], uses[sl] & 1);
-      ++uses[sl];
-      __syncthreads();          // every thread is done with the slot the next issue overwrites
-      issue();
-      const double* L = Lr + sl * 4096;
-      const bool diag = J > last_off(I);
-      const double* v = diag ? nullptr : Vr + (J % NV) * 64;
-      if (diag) {                // residual R = W_I - acc
-        if (fw) {
-          if (lane < 8) Rs[warp * 8 + lane] = Wr[sl * 64 + warp * 8 + lane] - racc;
-        } else {
-          Pp[grp * 64 + col] = cacc;
-          __syncthreads();
-          if (tid < 64) Rs[tid] = Wr[sl * 64 + tid] - ((Pp[tid] + Pp[64 + tid]) + (Pp[128 + tid] + Pp[192 + tid]));
-        }
-        __syncthreads();
-        v = Rs;
-      }
-      if (fw) {                  // y_r = sum_c L[r][c] v[c], rows 8w .. 8w+7
-        double p8[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const double* Lrow = L + (warp * 8 + i) * 64;
-          p8[i] = fma(Lrow[lane], v[lane], Lrow[lane + 32] * v[lane + 32]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) p8[i] += __shfl_xor_sync(0xffffffffu, p8[i], o);
-        double mine = p8[0];
-#pragma unroll
-        for (int i = 1; i < 8; ++i)
-          if (lane == i) mine = p8[i];
-        if (!diag) {
-          racc += mine;
-        } else if (lane < 8) {
-          Vr[(I % NV) * 64 + warp * 8 + lane] = mine;
-          Wb[(int64_t)I * 64 + warp * 8 + lane] = mine;
-        }
-      } else {                   // y_c = sum_r L[r][c] v[r], rows 16 grp .. 16 grp + 15
-        double y = 0.0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) y = fma(L[(grp * 16 + i) * 64 + col], v[grp * 16 + i], y);
-        if (!diag) {
-          cacc += y;
-        } else {
-          Pp[grp * 64 + col] = y;
-          __syncthreads();
-          if (tid < 64) {
-            const double u = (Pp[tid] + Pp[64 + tid]) + (Pp[128 + tid] + Pp[192 + tid]);
-            Vr[(I % NV) * 64 + tid] = u;
-            Wb[(int64_t)I * 64 + tid] = u;
-          }
-        }
-      }
-      if (diag) {
-        racc = 0.0;
-        cacc = 0.0;
-        I = next_row(I);
-        J = (fw ? I < nt : I >= 0) ? first_j(I) : 0;
-      } else {
-        ++J;
-      }
-    }
-    __threadfence();
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Partitioned ("spike") narrow-band solve of the A_G factor.  The band rows are cut into P chunks of
-// consecutive 64-row tiles; chunk k couples to chunk k-1 only through one factor tile C_k (first tile
-// row of k x last tile column of k-1).  With the spikes S_k = L_kk^{-1} [C_k; 0] and
-// T_k = L_kk^{-T} [0; C_{k+1}^T] formed in setup:
-//   forward:  y_k = L_kk^{-1} b_k (all chunks in parallel);  x_k = y_k - S_k x_{k-1}[last tile]
-//   backward: z_k = L_kk^{-T} x_k (parallel);                 u_k = z_k - T_k u_{k+1}[first tile]
-// the coupling tiles ride a P-step recurrence (k_spike_tail), the rest is one parallel update
-// (k_spike_update).  Exact in exact arithmetic; a reordering of the same triangular solve.
-// tile_chunk[I] = chunk of tile row I; chunk_first[k] = first tile row of chunk k (chunk_first[P] = nt)
-// spk: rows of the band buffer x 64 (S_k rows for the forward spikes, T_k rows for the backward).
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void spike_tile_product(const double* __restrict__ Sg, const double* __restrict__ Xg,
-                                                   int ldw, double* __restrict__ Og, int ncols, double* sm) {
-  // Og (64 x ncols, ld ldw) -= Sg (64 x 64, ld 64) * Xg (64 x ncols, ld ldw); ncols <= 32, both operands
-  // staged in shared memory (dynamic, 50 KB)
-  double* Ss = sm;              // 64 x 65
-  double* Xs = sm + 64 * 65;    // 64 x 33
-  for (int e = threadIdx.x; e < 4096; e += 256) Ss[(e >> 6) * 65 + (e & 63)] = __ldg(Sg + e);
-  for (int e = threadIdx.x; e < 64 * ncols; e += 256) {
-    const int r = e / ncols, cc = e - r * ncols;
-    Xs[r * 33 + cc] = Xg[(int64_t)r * ldw + cc];
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < 64 * ncols; e += 256) {
-    const int r = e / ncols, cc = e - r * ncols;
-    double acc = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < 64; ++k) acc = fma(Ss[r * 65 + k], Xs[k * 33 + cc], acc);
-    Og[(int64_t)r * ldw + cc] -= acc;
-  }
-  __syncthreads();
-}
-
-// sequential over chunks (one CTA per 32-column chunk): the coupling tiles
-__global__ void __launch_bounds__(256) k_spike_tail(const double* __restrict__ spk, const int* __restrict__ chunk_first,
-                                                    int P, double* buf, int ldw, int s, int fwd) {
-  extern __shared__ double sm[];
-  const int c0 = blockIdx.x * 32;
-  const int ncols = min(32, s - c0);
-  if (fwd) {
-    for (int k = 1; k < P; ++k) {   // x_k[last] -= S_k[last rows] x_{k-1}[last]
-      const int last = chunk_first[k + 1] - 1, prev = chunk_first[k] - 1;
-      spike_tile_product(spk + (int64_t)last * 64 * 64, buf + (int64_t)prev * 64 * ldw + c0, ldw,
-                         buf + (int64_t)last * 64 * ldw + c0, ncols, sm);
-      __threadfence_block();
-    }
-  } else {
-    for (int k = P - 2; k >= 0; --k) {   // u_k[first] -= T_k[first rows] u_{k+1}[first]
-      const int first = chunk_first[k], nxt = chunk_first[k + 1];
-      spike_tile_product(spk + (int64_t)first * 64 * 64, buf + (int64_t)nxt * 64 * ldw + c0, ldw,
-                         buf + (int64_t)first * 64 * ldw + c0, ncols, sm);
-      __threadfence_block();
-    }
-  }
-}
-
 // 8 dot products per warp: v[rr] (per-lane partials of row rr) -> the full sum of row
 // 4 bit4 + 2 bit3 + bit2 of the lane, in lanes with (lane & 3) == 0 (and their 3 neighbours)
 __device__ __forceinline__ double warp_reduce8(double v[8], int lane) {
@@ -1326,6 +1145,182 @@ __global__ void __launch_bounds__(256) k_spike_update_mma(const double* __restri
       const double2 cur = *o;
       *o = make_double2(cur.x - acc[i][q][0], cur.y - acc[i][q][1]);
     }
+}
+
+template <int NS, int WBM>
+__global__ void __launch_bounds__(256) k_band_fb_vec(const TriSys* __restrict__ sys, double* buf, int fwd, int bwd) {
+  constexpr int NV = WBM + 1;
+  extern __shared__ __align__(128) double sm[];
+  double* Lr = sm;                          // NS x 4096 (contiguous 64 x 64 tiles)
+  double* Wr = sm + NS * 4096;              // NS x 64 (rhs tile of a diagonal step)
+  double* Vr = Wr + NS * 64;                // NV x 64
+  double* Pp = Vr + NV * 64;                // 4 x 64 column partials
+  double* Rs = Pp + 4 * 64;                 // 64 residual
+  __shared__ __align__(8) uint64_t bar[NS];
+  const TriSys sy = sys[blockIdx.x];
+  const int nt = sy.nt, wb = sy.wb;
+  if (nt == 0) return;
+  const double* T = sy.T;
+  double* Wb = buf + sy.row0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int col = tid & 63, grp = tid >> 6;
+  const int myrow = warp_reduce8_row(lane);   // forward: the row whose sum this lane holds
+  auto tile = [&](int I, int J) -> const double* { return T + ((int64_t)J * (wb + 1) + (I - J)) * NSP_TILE_ELEMS; };
+  if (tid == 0)
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  unsigned uses[NS];   // completed phases per slot (thread-uniform)
+#pragma unroll
+  for (int i = 0; i < NS; ++i) uses[i] = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool fw = pass == 0;
+    if (fw ? !fwd : !bwd) continue;
+    auto first_j = [&](int I) { return fw ? max(0, I - wb) : I + 1; };
+    auto last_off = [&](int I) { return fw ? I - 1 : min(nt - 1, I + wb); };
+    auto next_row = [&](int I) { return fw ? I + 1 : I - 1; };
+    int iI = fw ? 0 : nt - 1, iJ = first_j(iI), ip = 0;
+    auto issue = [&]() {   // one product's tiles into slot ip % NS (thread 0 issues)
+      if (fw ? iI >= nt : iI < 0) return;
+      const int sl = ip % NS;
+      if (iJ <= last_off(iI)) {
+        if (tid == 0) mbar_expect_copy(&bar[sl], Lr + sl * 4096, fw ? tile(iI, iJ) : tile(iJ, iI), 32768);
+        ++iJ;
+      } else {
+        if (tid == 0) {
+          mbar_expect_copy(&bar[sl], Lr + sl * 4096, tile(iI, iI), 32768);
+          mbar_add_copy(&bar[sl], Wr + sl * 64, Wb + (int64_t)iI * 64, 512);
+        }
+        iI = next_row(iI);
+        iJ = (fw ? iI < nt : iI >= 0) ? first_j(iI) : 0;
+      }
+      ++ip;
+    };
+    for (int p = 0; p < NS - 1; ++p) issue();
+    int I = fw ? 0 : nt - 1, J = first_j(I);
+    double racc = 0.0;   // forward: lane j of warp w holds the sum of row 8w + j (after reduction)
+    double cacc = 0.0;   // backward: column partial (col, grp)
+    for (int q = 0;; ++q) {
+      if (fw ? I >= nt : I < 0) break;
+      const int sl = q % NS;
+      mbar_wait(&bar[sl], uses[sl] & 1);
+      ++uses[sl];
+      __syncthreads();          // every thread is done with the slot the next issue overwrites
+      issue();
+      const double* L = Lr + sl * 4096;
+      const bool diag = J > last_off(I);
+      const double* v = diag ? nullptr : Vr + (J % NV) * 64;
+      if (diag) {                // residual R = W_I - acc
+        if (fw) {
+          if ((lane & 3) == 0) Rs[warp * 8 + myrow] = Wr[sl * 64 + warp * 8 + myrow] - racc;
+        } else {
+          Pp[grp * 64 + col] = cacc;
+          __syncthreads();
+          if (tid < 64) Rs[tid] = Wr[sl * 64 + tid] - ((Pp[tid] + Pp[64 + tid]) + (Pp[128 + tid] + Pp[192 + tid]));
+        }
+        __syncthreads();
+        v = Rs;
+      }
+      if (fw) {                  // y_r = sum_c L[r][c] v[c], rows 8w .. 8w+7
+        double p8[8];
+        const double v0 = v[lane], v1 = v[lane + 32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double* Lrow = L + (warp * 8 + i) * 64;
+          p8[i] = fma(Lrow[lane], v0, Lrow[lane + 32] * v1);
+        }
+        const double mine = warp_reduce8(p8, lane);   // row 8 warp + myrow, on lanes with (lane & 3) == 0
+        if (!diag) {
+          racc += mine;
+        } else if ((lane & 3) == 0) {
+          Vr[(I % NV) * 64 + warp * 8 + myrow] = mine;
+          Wb[(int64_t)I * 64 + warp * 8 + myrow] = mine;
+        }
+      } else {                   // y_c = sum_r L[r][c] v[r], rows 16 grp .. 16 grp + 15
+        double y = 0.0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) y = fma(L[(grp * 16 + i) * 64 + col], v[grp * 16 + i], y);
+        if (!diag) {
+          cacc += y;
+        } else {
+          Pp[grp * 64 + col] = y;
+          __syncthreads();
+          if (tid < 64) {
+            const double u = (Pp[tid] + Pp[64 + tid]) + (Pp[128 + tid] + Pp[192 + tid]);
+            Vr[(I % NV) * 64 + tid] = u;
+            Wb[(int64_t)I * 64 + tid] = u;
+          }
+        }
+      }
+      if (diag) {
+        racc = 0.0;
+        cacc = 0.0;
+        I = next_row(I);
+        J = (fw ? I < nt : I >= 0) ? first_j(I) : 0;
+      } else {
+        ++J;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Partitioned ("spike") narrow-band solve of the A_G factor.  The band rows are cut into P chunks of
+// consecutive 64-row tiles; chunk k couples to chunk k-1 only through one factor tile C_k (first tile
+// row of k x last tile column of k-1).  With the spikes S_k = L_kk^{-1} [C_k; 0] and
+// T_k = L_kk^{-T} [0; C_{k+1}^T] formed in setup:
+//   forward:  y_k = L_kk^{-1} b_k (all chunks in parallel);  x_k = y_k - S_k x_{k-1}[last tile]
+//   backward: z_k = L_kk^{-T} x_k (parallel);                 u_k = z_k - T_k u_{k+1}[first tile]
+// the coupling tiles ride a P-step recurrence (k_spike_tail), the rest is one parallel update
+// (k_spike_update).  Exact in exact arithmetic; a reordering of the same triangular solve.
+// tile_chunk[I] = chunk of tile row I; chunk_first[k] = first tile row of chunk k (chunk_first[P] = nt)
+// spk: rows of the band buffer x 64 (S_k rows for the forward spikes, T_k rows for the backward).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void spike_tile_product(const double* __restrict__ Sg, const double* __restrict__ Xg,
+                                                   int ldw, double* __restrict__ Og, int ncols, double* sm) {
+  // Og (64 x ncols, ld ldw) -= Sg (64 x 64, ld 64) * Xg (64 x ncols, ld ldw); ncols <= 32, both operands
+  // staged in shared memory (dynamic, 50 KB)
+  double* Ss = sm;              // 64 x 65
+  double* Xs = sm + 64 * 65;    // 64 x 33
+  for (int e = threadIdx.x; e < 4096; e += 256) Ss[(e >> 6) * 65 + (e & 63)] = __ldg(Sg + e);
+  for (int e = threadIdx.x; e < 64 * ncols; e += 256) {
+    const int r = e / ncols, cc = e - r * ncols;
+    Xs[r * 33 + cc] = Xg[(int64_t)r * ldw + cc];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 64 * ncols; e += 256) {
+    const int r = e / ncols, cc = e - r * ncols;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < 64; ++k) acc = fma(Ss[r * 65 + k], Xs[k * 33 + cc], acc);
+    Og[(int64_t)r * ldw + cc] -= acc;
+  }
+  __syncthreads();
+}
+
+// sequential over chunks (one CTA per 32-column chunk): the coupling tiles
+__global__ void __launch_bounds__(256) k_spike_tail(const double* __restrict__ spk, const int* __restrict__ chunk_first,
+                                                    int P, double* buf, int ldw, int s, int fwd) {
+  extern __shared__ double sm[];
+  const int c0 = blockIdx.x * 32;
+  const int ncols = min(32, s - c0);
+  if (fwd) {
+    for (int k = 1; k < P; ++k) {   // x_k[last] -= S_k[last rows] x_{k-1}[last]
+      const int last = chunk_first[k + 1] - 1, prev = chunk_first[k] - 1;
+      spike_tile_product(spk + (int64_t)last * 64 * 64, buf + (int64_t)prev * 64 * ldw + c0, ldw,
+                         buf + (int64_t)last * 64 * ldw + c0, ncols, sm);
+      __threadfence_block();
+    }
+  } else {
+    for (int k = P - 2; k >= 0; --k) {   // u_k[first] -= T_k[first rows] u_{k+1}[first]
+      const int first = chunk_first[k], nxt = chunk_first[k + 1];
+      spike_tile_product(spk + (int64_t)first * 64 * 64, buf + (int64_t)nxt * 64 * ldw + c0, ldw,
+                         buf + (int64_t)first * 64 * ldw + c0, ncols, sm);
+      __threadfence_block();
+    }
+  }
 }
 
 // one column (s = 1, ld 1): the same P-step recurrence as a matrix-vector chain.  The spike tiles
