@@ -23,7 +23,7 @@
 namespace {
 
 constexpr int RT = 256;             // threads per reduction CTA
-constexpr int RPB = 2048;           // rows per partial-sum chunk
+constexpr int RPB = 512;            // rows per partial-sum chunk (2 per thread: many CTAs, short chains)
 constexpr int GT_ROWS = 64;         // rows per Z^T r chunk
 constexpr int PCG_CHUNK = 8;        // PCG iterations per host status check (one CUDA graph)
 
