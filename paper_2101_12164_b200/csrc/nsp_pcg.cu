@@ -95,16 +95,36 @@ __global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ pa
   }
 }
 
-// alpha = (r.z) / (p.q);  x += alpha p;  r -= alpha q;  partial r.r.  p.q <= 0 -> indefinite.
-__global__ void __launch_bounds__(RT) k_pcg_xr(double* __restrict__ x, double* __restrict__ r,
-                                               const double* __restrict__ p, const double* __restrict__ q,
-                                               int64_t n, const double* sc, int cur, double* __restrict__ part,
-                                               BcgStatus* st) {
+// Fixed-order sum of nblk chunk partials (stride 2), evaluated identically by every CTA that needs
+// it: warp 0 loads lane-strided, then a fixed xor tree; the result is broadcast through smem.
+__device__ __forceinline__ double cta_sum_partials(const double* __restrict__ part, int nblk, double* bcast) {
+  if (threadIdx.x < 32) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += 32) v += part[b * 2];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) *bcast = v;
+  }
+  __syncthreads();
+  return *bcast;
+}
+
+// alpha = (r.z) / (p.q) with the p.q reduction folded in (sum of the partials);  x += alpha p;
+// r -= alpha q;  partial r.r.  p.q <= 0 -> indefinite.
+__global__ void __launch_bounds__(RT) k_pcg_xr_f(double* __restrict__ x, double* __restrict__ r,
+                                                 const double* __restrict__ p, const double* __restrict__ q,
+                                                 int64_t n, double* sc, int cur,
+                                                 const double* __restrict__ pq_part, int nblk,
+                                                 double* __restrict__ part, BcgStatus* st) {
   __shared__ double red[RT];
+  __shared__ double bc;
   if (st->done) return;
-  const double pq = sc[2];
+  const double pq = cta_sum_partials(pq_part, nblk, &bc);
   const double alpha = pq > 0.0 ? sc[cur] / pq : 0.0;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && !(pq > 0.0)) st->indefinite = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc[2] = pq;
+    if (!(pq > 0.0)) st->indefinite = 1;
+  }
   const int64_t r0 = (int64_t)blockIdx.x * RPB;
   double s = 0.0;
   for (int64_t i = r0 + threadIdx.x; i < min(n, r0 + RPB); i += RT) {
@@ -122,13 +142,18 @@ __global__ void __launch_bounds__(RT) k_pcg_xr(double* __restrict__ x, double* _
   if (threadIdx.x == 0) part[blockIdx.x * 2] = red[0];
 }
 
-// p = z + beta p, beta = (r.z)_new / (r.z)_old
-__global__ void k_pcg_p(double* __restrict__ p, const double* __restrict__ z, int64_t n, const double* sc, int cur,
-                        const BcgStatus* st) {
+// p = z + beta p with the r.z reduction folded in: rz_new = sum(partials), beta = rz_new / sc[cur];
+// CTA 0 stores rz_new in sc[cur ^ 1] for the next iteration's alpha
+__global__ void __launch_bounds__(RT) k_pcg_p_f(double* __restrict__ p, const double* __restrict__ z, int64_t n,
+                                                double* sc, int cur, const double* __restrict__ rz_part, int nblk,
+                                                const BcgStatus* st) {
+  __shared__ double bc;
+  if (st->done) return;
+  const double rz = cta_sum_partials(rz_part, nblk, &bc);
+  const double beta = rz / sc[cur];
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[cur ^ 1] = rz;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n || st->done) return;
-  const double beta = sc[cur ^ 1] / sc[cur];
-  p[i] = fma(beta, p[i], z[i]);
+  if (i < n) p[i] = fma(beta, p[i], z[i]);
 }
 
 // y[i*ldy] = a[i*lda] + alpha * b[i*ldb]
@@ -218,7 +243,7 @@ struct PcgWs {
   double *f, *w, *r, *z, *p, *q, *tmp, *t2, *eg;   // n_G vectors; eg: k x k (A-DEF2 solve, column 0)
   double *bB, *wvu, *tmpB;                 // W/V/U rows x 32
   double *i1r, *i1buf;                     // band rows x 32
-  double *agbuf, *apply_wvu, *part, *gpart, *g, *sc, *hist;
+  double *agbuf, *apply_wvu, *part, *part2, *gpart, *g, *sc, *hist;
   BcgStatus* st;
 };
 
@@ -251,6 +276,7 @@ static size_t pcg_layout(const nsp_ctx* c, char* base, PcgWs* out) {
   w.agbuf = take(c->has_ag ? ag_ws_doubles(c, 1) : 1);
   w.apply_wvu = take(apply_ws_bytes(c, 1) / 8 + 1);
   w.part = take((size_t)2 * nblk_of(std::max<int64_t>(c->nG, 1)) + 2);
+  w.part2 = take((size_t)2 * nblk_of(std::max<int64_t>(c->nG, 1)) + 2);
   w.gpart = take((size_t)128 * grid1(std::max<int64_t>(c->nG, 1), GT_ROWS));
   w.g = take(128);
   w.sc = take(16);
@@ -407,16 +433,20 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
     auto iteration = [&](cudaStream_t q) -> nsp_status {
       nsp_status e2;
       if ((e2 = apply_into(c, w.p, 1, w.q, 1, 1, 1, w.apply_wvu)) != NSP_OK) return e2;   // q = S_G p
-      dot(c, w.p, w.q, n, w, 2);
       const unsigned nb = nblk_of(n);
+      // p.q partials; their sum is taken inside k_pcg_xr_f (every CTA, same order)
       nsp_count_launch();
-      k_pcg_xr<<<nb, RT, 0, q>>>(w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, w.st);
+      k_dot2_partial<<<nb, RT, 0, q>>>(w.p, w.q, nullptr, nullptr, n, w.part);
       nsp_count_launch();
-      k_dot_reduce<<<1, RT, 0, q>>>(w.part, (int)nb, w.sc, 3, 1, tol, w.st, hist_dev, hist_mod);
+      k_pcg_xr_f<<<nb, RT, 0, q>>>(w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, (int)nb, w.part2, w.st);
+      nsp_count_launch();
+      k_dot_reduce<<<1, RT, 0, q>>>(w.part2, (int)nb, w.sc, 3, 1, tol, w.st, hist_dev, hist_mod);
       if ((e2 = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e2;
-      dot(c, w.r, w.z, n, w, cur ^ 1);
+      // r.z partials; the sum (and beta) inside k_pcg_p_f
       nsp_count_launch();
-      k_pcg_p<<<grid1(n, 256), 256, 0, q>>>(w.p, w.z, n, w.sc, cur, w.st);
+      k_dot2_partial<<<nb, RT, 0, q>>>(w.r, w.z, nullptr, nullptr, n, w.part);
+      nsp_count_launch();
+      k_pcg_p_f<<<grid1(n, RT), RT, 0, q>>>(w.p, w.z, n, w.sc, cur, w.part, (int)nb, w.st);
       cur ^= 1;
       return NSP_OK;
     };
