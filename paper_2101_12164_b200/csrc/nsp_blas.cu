@@ -255,6 +255,45 @@ __global__ void k_converge(const double* rsq, const double* bnorm, int s, double
   }
 }
 
+// k_colsq_reduce + k_converge in one launch (single rank: the column norms need no allreduce)
+__global__ void k_colsq_converge(const double* __restrict__ part, int ntiles, int ldp, double* rsq,
+                                 const double* __restrict__ bnorm, int s, double tol, BcgStatus* st) {
+  pdl_wait();
+  __shared__ double red[8][128];
+  __shared__ double mx[128];
+  const int c = threadIdx.x, g = threadIdx.y;
+  double sum = 0.0;
+  if (c < ldp)
+    for (int t = g; t < ntiles; t += 8) sum += part[t * (int64_t)ldp + c];
+  red[g][c] = sum;
+  __syncthreads();
+  if (g == 0) {
+    double v = 0.0, m = 0.0;
+    bool bad = false;
+    if (c < ldp) {
+      for (int q = 0; q < 8; ++q) v += red[q][c];
+      rsq[c] = v;
+      if (c < s) {
+        const double r = sqrt(v);
+        if (!isfinite(r)) bad = true;
+        m = bnorm[c] > 0.0 ? r / bnorm[c] : 0.0;
+      }
+    }
+    if (bad) st->nonfinite = 1;
+    mx[c] = m;
+  }
+  __syncthreads();
+  if (g == 0 && c < 32) {
+    double m = fmax(fmax(mx[c], mx[c + 32]), fmax(mx[c + 64], mx[c + 96]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (c == 0) {
+      st->relres = m;
+      st->converged = m <= tol ? 1 : 0;
+    }
+  }
+}
+
 __global__ void k_sqrt_vec(const double* in, double* out, int n) {
   const int i = threadIdx.x + blockIdx.x * blockDim.x;
   if (i < n) out[i] = sqrt(in[i]);
@@ -841,6 +880,11 @@ void colsq_reduce(const double* part, int ntiles, int ldp, double* out, cudaStre
 
 void sqrt_vec(const double* in, double* out, int n, cudaStream_t st) {
   { nsp_count_launch(); k_sqrt_vec<<<(n + 255) / 256, 256, 0, st>>>(in, out, n); }
+}
+
+void colsq_converge(const double* part, int ntiles, int ldp, double* rsq, const double* bnorm, int s, double tol,
+                    BcgStatus* stt, cudaStream_t st) {
+  { nsp_count_launch(); launch_k(k_colsq_converge, dim3(1), dim3(128, 8), 0, st, part, ntiles, ldp, rsq, bnorm, s, tol, stt); }
 }
 
 void converge(const double* rsq, const double* bnorm, int s, double tol, BcgStatus* stt, double* hist_slot,

@@ -51,6 +51,8 @@ void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, i
 void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st);
 void colsq_reduce(const double* part, int ntiles, int ldp, double* out, cudaStream_t st);
 void sqrt_vec(const double* in, double* out, int n, cudaStream_t st);
+void colsq_converge(const double* part, int ntiles, int ldp, double* rsq, const double* bnorm, int s, double tol,
+                    BcgStatus* stt, cudaStream_t st);
 void converge(const double* rsq, const double* bnorm, int s, double tol, BcgStatus* stt, double* hist_slot,
               cudaStream_t st);
 // mode 0: D (pivot <= 0 -> indefinite), Out = D^{-1}; mode 1: orth Gram (pivot test -> fallback),

@@ -293,10 +293,10 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     if (multi) {
       nspb::colsq(w.R, sp, ng, s, sp, w.npart, w.rsq, q);
       if ((e2 = comm_allreduce(c, w.rsq, sp)) != NSP_OK) return e2;
+      nspb::converge(w.rsq, w.bnorm, s, tol, w.st, nullptr, q);
     } else {
-      nspb::colsq_reduce(w.npart, (int)((n + 63) / 64), sp, w.rsq, q);
+      nspb::colsq_converge(w.npart, (int)((n + 63) / 64), sp, w.rsq, w.bnorm, s, tol, w.st, q);
     }
-    nspb::converge(w.rsq, w.bnorm, s, tol, w.st, nullptr, q);
     tr.mark("XR_update");
     if (copy_status) NSP_CUDA_TRY(c, cudaMemcpyAsync(hs, w.st, sizeof(BcgStatus), cudaMemcpyDeviceToHost, q));
     NSP_CUDA_TRY(c, cudaGetLastError());
