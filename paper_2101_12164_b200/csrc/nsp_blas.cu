@@ -549,7 +549,8 @@ __device__ int g_eig_sweeps;
 #endif
 __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ Ain, int lda, int n,
                                                     double* Vwork, int ldv, double* lam, double* Vsorted,
-                                                    const int* gate) {
+                                                    const int* gate, double tau, double* Tout, int spT,
+                                                    BcgStatus* stw) {
   pdl_wait();
   (void)Vwork;
   (void)ldv;
@@ -713,32 +714,30 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
     const int i = e / n, k = e - i * n;
     Vsorted[(i0 + i) * n + k] = Vt[order[k] * rp + i];
   }
+  if (Tout) {   // orth's eigen fallback (reading C3): keep lambda > tau lambda_max, T = V_keep Lambda^{-1/2}
+    __shared__ double ls[128];
+    __shared__ int wk;
+    if (tid < n) ls[tid] = Ap[tri(order[tid], order[tid])];
+    __syncthreads();
+    if (tid == 0) {
+      int cnt = 0;
+      if (ls[0] > 0)
+        for (int k = 0; k < n; ++k)
+          if (ls[k] > tau * ls[0]) ++cnt;
+      wk = cnt;
+      if (blockIdx.x == 0) stw->width = cnt;
+    }
+    __syncthreads();
+    const int w = wk;
+    for (int e = tid; e < nr * spT; e += nt) {   // this CTA's rows of V
+      const int i = e / spT, k = e - i * spT;
+      Tout[(int64_t)(i0 + i) * spT + k] = k < w ? Vt[order[k] * rp + i] / sqrt(ls[k]) : 0.0;
+    }
+    if (blockIdx.x == 0)
+      for (int e = tid; e < (spT - n) * spT; e += nt) Tout[(int64_t)n * spT + e] = 0.0;   // rows >= n
+  }
 }
 
-// orth fallback: keep eigenvalues > tau * lambda_max (lam descending, only the first s are real);
-// T[:, k] = V[:, k] / sqrt(lam_k) for k < width, zero otherwise.
-__global__ void k_orth_from_eig(const double* lam, const double* Vs, int n, int sp, double tau, double* T,
-                                BcgStatus* st) {
-  pdl_wait();
-  if (!st->fallback) return;
-  __shared__ int w;
-  if (threadIdx.x == 0) {
-    const double lmax = lam[0];
-    int c = 0;
-    if (lmax > 0)
-      for (int k = 0; k < n; ++k)
-        if (lam[k] > tau * lmax) ++c;
-    w = c;
-    st->width = c;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < sp * sp; e += blockDim.x) {
-    const int i = e / sp, k = e - i * sp;
-    double v = 0.0;
-    if (i < n && k < w) v = Vs[i * n + k] / sqrt(lam[k]);
-    T[e] = v;
-  }
-}
 
 // C = alpha * op(A) op(B) + beta * C, all sp-ish small (m x n, inner k), row-major, FMA.
 __global__ void k_small_gemm(int m, int n, int k, double alpha, const double* A, int lda, int ta, const double* B,
@@ -900,19 +899,15 @@ void small_chol(const double* A, int sp, int mode, int nact, double tau, double*
 }
 
 void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* lam, double* Vsorted,
-               const int* gate, cudaStream_t st) {
+               const int* gate, cudaStream_t st, double tau, double* T, int spT, BcgStatus* stw) {
   const int ne = n + (n & 1);
   const int g = ne >= 128 ? 8 : ne >= 64 ? 4 : 1;   // V row slices (rp = ne / g rows each)
   const int rp = (ne + g - 1) / g;
   const size_t smem = (size_t)(ne * (ne + 1) / 2 + ne * rp) * sizeof(double);
   set_smem((const void*)k_small_eig, smem);
-  { nsp_count_launch(); launch_k(k_small_eig, dim3(g), dim3(1024), smem, st, A, lda, n, Vwork, ldv, lam, Vsorted, gate); }
+  { nsp_count_launch(); launch_k(k_small_eig, dim3(g), dim3(1024), smem, st, A, lda, n, Vwork, ldv, lam, Vsorted, gate, tau, T, spT, stw); }
 }
 
-void orth_from_eig(const double* lam, const double* Vs, int n, int sp, double tau, double* T, BcgStatus* stt,
-                   cudaStream_t st) {
-  { nsp_count_launch(); launch_k(k_orth_from_eig, dim3(1), dim3(1024), 0, st, lam, Vs, n, sp, tau, T, stt); }
-}
 
 void small_gemm(int m, int n, int k, double alpha, const double* A, int lda, bool ta, const double* B, int ldb,
                 bool tb, double beta, double* C, int ldc, cudaStream_t st) {

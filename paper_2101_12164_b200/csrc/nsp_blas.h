@@ -70,9 +70,8 @@ void chol_fac(const double* A, int sp, int mode, int nact, double tau, double* L
 void chol_solve(const double* Lp, int sp, const double* B, int ldb, double* Out, int ldo, double sgn, bool fwd,
                 bool bwd, const int* gate, cudaStream_t st);
 void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* lam, double* Vsorted,
-               const int* gate, cudaStream_t st);
-void orth_from_eig(const double* lam, const double* Vs, int n, int sp, double tau, double* T, BcgStatus* stt,
-                   cudaStream_t st);
+               const int* gate, cudaStream_t st,
+               double tau = 0.0, double* T = nullptr, int spT = 0, BcgStatus* stw = nullptr);
 void small_gemm(int m, int n, int k, double alpha, const double* A, int lda, bool ta, const double* B, int ldb,
                 bool tb, double beta, double* C, int ldc, cudaStream_t st);
 void scale_rows(double* G, int ld, const double* d, int r, int nrows, int ncols, cudaStream_t st);

@@ -164,8 +164,8 @@ static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Po
   // CholQR with the pivot test (k_chol16 mode 1), T = R^{-1} = L^{-T} (skipped on fallback)
   nspb::chol_fac(w.G, sp, 1, s, c->opts.orth_tau, w.Ldi, w.st, st);
   nspb::chol_solve(w.Ldi, sp, nullptr, 0, w.T, sp, 1.0, false, true, &w.st->fallback, st);
-  nspb::small_eig(w.G, sp, s, w.Vw, sp + 1, w.lam, w.Vs, &w.st->fallback, st);
-  nspb::orth_from_eig(w.lam, w.Vs, s, sp, c->opts.orth_tau, w.T, w.st, st);
+  // eigen fallback (gated on the pivot test): EVD and T = V_keep Lambda^{-1/2} in one launch
+  nspb::small_eig(w.G, sp, s, w.Vw, sp + 1, w.lam, w.Vs, &w.st->fallback, st, c->opts.orth_tau, w.T, sp, w.st);
   if (join_before_panel) NSP_CUDA_TRY(c, cudaStreamWaitEvent(st, join_before_panel, 0));   // X += P alpha done
   nspb::panel(Pout, sp, nullptr, 0, Wm, sp, w.T, sp, sp, sp, n, 1.0, nullptr, st);
   return NSP_OK;
