@@ -49,7 +49,6 @@ int main() {
   timeit("small_chol mode1", [&] { nspb::small_chol(dG, sp, 1, sp, 1e-14, dT, dst, st); });
   timeit("small_chol mode0", [&] { nspb::small_chol(dG, sp, 0, -1, 0.0, dT, dst, st); });
   timeit("small_eig gated", [&] { nspb::small_eig(dG, sp, sp, dP, sp + 1, dT, dT, &dst->fallback, st); });
-  timeit("orth_from_eig", [&] { nspb::orth_from_eig(dT, dT, sp, sp, 1e-14, dT, dst, st); });
   timeit("panel n x s", [&] { nspb::panel(dP, sp, nullptr, 0, dW, sp, dT, sp, sp, sp, n, 1.0, nullptr, st); });
   timeit("panel s x s", [&] { nspb::panel(dP, sp, nullptr, 0, dG, sp, dT, sp, sp, sp, sp, 1.0, nullptr, st); });
   h.fallback = 1; cudaMemcpy(dst, &h, sizeof(h), cudaMemcpyHostToDevice);
