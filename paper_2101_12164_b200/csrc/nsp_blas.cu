@@ -195,6 +195,122 @@ __global__ void __launch_bounds__(256) k_panel(PanelArgs pa0, PanelArgs pa1, int
   }
 }
 
+// The same panel for the 128-column case (s x s multiplier M with s = 128) as ONE wave: one CTA per
+// SM, each owning a contiguous range of 16-row groups (balanced to +-1 group, where 64-row tiles
+// quantise to 2 tiles on some SMs and 1 on others), M resident in shared memory (read once per CTA),
+// In streamed through a PNS-stage ring of 64 x 32 chunks, 16 warps = 4 row groups x 4 column quarters
+// of a 64 x 128 pass; Cin prefetched into registers at the start of each pass.  normpart (optional):
+// one row per CTA, the column sums of squares over its rows (fixed order).
+#ifndef NSP_PANEL_NW
+#define NSP_PANEL_NW 16
+#endif
+#ifndef NSP_PNS
+#define NSP_PNS 4
+#endif
+constexpr int PLDM = 132, PLDA = 36, PNS = NSP_PNS;
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t n, int64_t ngroups) {
+  // NW = 16: warps = 4 row groups x 4 column quarters (16 x 32 per warp); NW = 8: 4 row groups x 2
+  // column halves (16 x 64 per warp: twice the products per loaded A fragment)
+  constexpr int NF = NW == 16 ? 4 : 8;
+  pdl_wait();
+  extern __shared__ __align__(16) double sm[];
+  double* Ms = sm;                  // 128 x PLDM
+  double* Ar = sm + 128 * PLDM;     // PNS x 64 x PLDA
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rg = NW == 16 ? warp >> 2 : warp >> 1;
+  const int cb = NW == 16 ? (warp & 3) * 32 : (warp & 1) * 64;
+  const int64_t g0 = (int64_t)blockIdx.x * ngroups / gridDim.x;
+  const int64_t g1 = (int64_t)(blockIdx.x + 1) * ngroups / gridDim.x;
+  const int64_t r0 = g0 * 16, r1 = min(n, g1 * 16);
+  const int npass = r1 > r0 ? (int)((r1 - r0 + 63) / 64) : 0;
+  const int nsteps = npass * 4;
+  const double* __restrict__ In = pa.In;
+  auto issue = [&](int q) {
+    const int64_t rp = r0 + (int64_t)(q >> 2) * 64;
+    cp_block_zf(Ar + (q % PNS) * 64 * PLDA, PLDA, In + rp * pa.ldi + (q & 3) * 32, pa.ldi, 64, 32, r1 - rp);
+  };
+  cp_block(Ms, PLDM, pa.M, pa.ldm, 128, 128);
+#pragma unroll
+  for (int q = 0; q < PNS - 1; ++q) {
+    if (q < nsteps) issue(q);
+    cp_commit();
+  }
+  double acc[2][NF][2];
+  acc_zero(acc);
+  double sq[NF][2];
+#pragma unroll
+  for (int j = 0; j < NF; ++j) sq[j][0] = sq[j][1] = 0.0;
+  double2 cin[2][NF];
+  for (int q = 0; q < nsteps; ++q) {
+    const int kc = q & 3;
+    const int64_t rp = r0 + (int64_t)(q >> 2) * 64;
+    if (kc == 0) {   // this pass's Cin, in flight behind the pass's four chunk products
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int64_t r = rp + rg * 16 + acc_row<NF>(i, 0);
+          const int c = cb + acc_col<NF>(j, 0);
+          cin[i][j] = (pa.Cin && r < r1) ? *reinterpret_cast<const double2*>(pa.Cin + r * pa.ldc + c)
+                                         : make_double2(0.0, 0.0);
+        }
+    }
+    cp_wait<PNS - 2>();
+    __syncthreads();
+    if (q + PNS - 1 < nsteps) issue(q + PNS - 1);
+    cp_commit();
+    const double* As = Ar + (q % PNS) * 64 * PLDA;
+    // a warp whose 16-row group lies past the range skips its products (the DMMA pipe is the limit)
+    if (rp + rg * 16 < r1)
+      cta_mma<NF, false, false>(As + rg * 16 * PLDA, PLDA, Ms + kc * 32 * PLDM + cb, PLDM, acc, 32, 0);
+    if (kc == 3) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int64_t r = rp + rg * 16 + acc_row<NF>(i, 0);
+          const int c = cb + acc_col<NF>(j, 0);
+          if (r < r1) {
+            const double v0 = pa.sgn * acc[i][j][0] + cin[i][j].x;
+            const double v1 = pa.sgn * acc[i][j][1] + cin[i][j].y;
+            *reinterpret_cast<double2*>(pa.Out + r * pa.ldo + c) = make_double2(v0, v1);
+            sq[j][0] += v0 * v0;
+            sq[j][1] += v1 * v1;
+          }
+        }
+      acc_zero(acc);
+    }
+  }
+  if (!pa.normpart) return;
+  // column sums of squares: butterfly over the 8 row lanes, then the 4 row-group warps in order
+#pragma unroll
+  for (int j = 0; j < NF; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double v = sq[j][e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      sq[j][e] = v;
+    }
+  cp_wait<0>();
+  __syncthreads();   // the ring is free
+  double* red = Ar;  // 4 x 128
+  if (lane < 4) {
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+      const int c = cb + acc_col<NF>(j, 0);
+      red[rg * 128 + c] = sq[j][0];
+      red[rg * 128 + c + 1] = sq[j][1];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 128)
+    pa.normpart[blockIdx.x * (int64_t)pa.ldo + threadIdx.x] =
+        ((red[threadIdx.x] + red[128 + threadIdx.x]) + red[256 + threadIdx.x]) + red[384 + threadIdx.x];
+}
+
 // column sums of squares of X (n x s), partial per 64-row tile (fixed order)
 __global__ void k_colsq_partial(const double* __restrict__ X, int ldx, int64_t n, int s, double* part, int ldp) {
   pdl_wait();
@@ -861,10 +977,32 @@ void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64
   { nsp_count_launch(); launch_k(k_panel, dim3(grid), dim3(256), smem, st, a0, a1 ? *a1 : a0, kdim, n); }
 }
 
-void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
-           int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st) {
+int panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
+          int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st) {
   PanelArgs a{Out, ldo, Cin, ldc, In, ldi, M, ldm, sgn, normpart};
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static const bool rows_off = [] {
+    const char* e = getenv("NSP_PANEL_ROWS");
+    return e && e[0] == '0';
+  }();
+  // one-wave row-range panel: s = 128 and at least one 64-row pass per SM (normpart rows = CTAs)
+  if (!rows_off && kdim == 128 && ncols == 128 && n >= (int64_t)64 * nsm && ldo >= 128) {
+    const size_t smem = (128 * PLDM + PNS * 64 * PLDA) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      set_smem((const void*)k_panel_rows<NSP_PANEL_NW>, smem);
+      attr = true;
+    }
+    { nsp_count_launch(); launch_k(k_panel_rows<NSP_PANEL_NW>, dim3(nsm), dim3(NSP_PANEL_NW * 32), smem, st, a, n, (n + 15) / 16); }
+    return nsm;
+  }
   panel2(a, nullptr, kdim, ncols, n, st);
+  return (int)((n + 63) / 64);
 }
 
 void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st) {

@@ -46,8 +46,9 @@ void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb
            double* out, double* out2, int ldo, double* ws, cudaStream_t st);
 // two independent panels in one launch (a1 may be null)
 void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64_t n, cudaStream_t st);
-void panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
-           int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st);
+// returns the number of normpart rows written (row tiles, or CTAs of the one-wave s = 128 kernel)
+int panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
+          int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st);
 void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st);
 void colsq_reduce(const double* part, int ntiles, int ldp, double* out, cudaStream_t st);
 void sqrt_vec(const double* in, double* out, int n, cudaStream_t st);

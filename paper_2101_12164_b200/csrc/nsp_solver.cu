@@ -289,13 +289,13 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     nspb::chol_solve(w.Ld, sp, w.E, sp, w.al, sp, 1.0, true, true, nullptr, q);   // alpha = D^{-1} E
     tr.mark("alpha");
     // R -= Q alpha here; X += P alpha is deferred to the next tail (x_update), off the critical path
-    nspb::panel(w.R, sp, w.R, sp, w.Q, sp, w.al, sp, sp, sp, n, -1.0, multi ? nullptr : w.npart, q);
+    const int npt = nspb::panel(w.R, sp, w.R, sp, w.Q, sp, w.al, sp, sp, sp, n, -1.0, multi ? nullptr : w.npart, q);
     if (multi) {
       nspb::colsq(w.R, sp, ng, s, sp, w.npart, w.rsq, q);
       if ((e2 = comm_allreduce(c, w.rsq, sp)) != NSP_OK) return e2;
       nspb::converge(w.rsq, w.bnorm, s, tol, w.st, nullptr, q);
     } else {
-      nspb::colsq_converge(w.npart, (int)((n + 63) / 64), sp, w.rsq, w.bnorm, s, tol, w.st, q);
+      nspb::colsq_converge(w.npart, npt, sp, w.rsq, w.bnorm, s, tol, w.st, q);
     }
     tr.mark("XR_update");
     if (copy_status) NSP_CUDA_TRY(c, cudaMemcpyAsync(hs, w.st, sizeof(BcgStatus), cudaMemcpyDeviceToHost, q));
