@@ -314,14 +314,13 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     if (!c->ev_join) NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   }
   auto x_update = [&](bool fork) -> nsp_status {
-    PanelArgs px{w.X, sp, w.X, sp, w.P, sp, w.al, sp, 1.0, nullptr};
     if (!fork) {
-      nspb::panel2(px, nullptr, sp, sp, n, c->stream);
+      nspb::panel(w.X, sp, w.X, sp, w.P, sp, w.al, sp, sp, sp, n, 1.0, nullptr, c->stream);
       return NSP_OK;
     }
     NSP_CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
     NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
-    nspb::panel2(px, nullptr, sp, sp, n, c->side_stream);
+    nspb::panel(w.X, sp, w.X, sp, w.P, sp, w.al, sp, sp, sp, n, 1.0, nullptr, c->side_stream);
     NSP_CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side_stream));
     return NSP_OK;
   };
