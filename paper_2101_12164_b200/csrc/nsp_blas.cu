@@ -54,12 +54,21 @@ __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__
                                                       const double* __restrict__ Xb, const double* __restrict__ Xb2,
                                                       int ldb, int ntn1, int64_t n,
                                                       int64_t rows_per_chunk, double* __restrict__ part, int ntm,
-                                                      int ntn) {
+                                                      int ntn, int sym) {
   pdl_wait();
   extern __shared__ double sm[];
   constexpr int STG = 2 * GR * LDS;
   const int tile = blockIdx.x;
-  const int tm = tile / ntn, tn = tile - tm * ntn;
+  int tm = tile / ntn, tn = tile - tm * ntn;
+  if (sym) {   // Xa == Xb: only the tiles tm <= tn, enumerated row by row
+    tm = 0;
+    int rem = tile;
+    while (rem >= ntn - tm) {
+      rem -= ntn - tm;
+      ++tm;
+    }
+    tn = tm + rem;
+  }
   const int64_t r0 = blockIdx.y * rows_per_chunk;
   const int64_t r1 = min(n, r0 + rows_per_chunk);
   double acc[2][4][2];
@@ -86,7 +95,7 @@ __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__
     const double* st = sm + (q % GNS) * STG;
     cta_mma<4, true, false>(st, LDS, st + GR * LDS, LDS, acc, GR);
   }
-  double* out = part + ((int64_t)blockIdx.y * ntm * ntn + tile) * 4096;
+  double* out = part + ((int64_t)blockIdx.y * gridDim.x + tile) * 4096;
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -98,17 +107,32 @@ __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__
 
 // out (or out2 for column tiles >= ntn1) = sum over chunks, 4 chunk groups per element combined
 // in fixed order (deterministic)
+// sym: the partials hold only the tiles tm <= tn (Xa == Xb); element (i, j) of a lower tile is read
+// transposed from its upper partner, so the output is exactly symmetric
 __global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int ntm, int ntn, int ntn1,
-                              double* out, double* out2, int ldo) {
+                              double* out, double* out2, int ldo, int sym) {
   pdl_wait();
   __shared__ double red[4][16][17];
-  const int i = blockIdx.y * 16 + threadIdx.y;
-  const int j = blockIdx.x * 16 + threadIdx.x;
+  // a 16 x 16 output block below the diagonal (sym) is read transposed from its upper partner with the
+  // threads swapped (coalesced reads) and written transposed; diagonal blocks pick (min, max) per element
+  const int bi = blockIdx.y * 16, bj = blockIdx.x * 16;
+  const bool tr = sym && bi > bj;
+  const int i = tr ? bi + threadIdx.x : bi + threadIdx.y;
+  const int j = tr ? bj + threadIdx.y : bj + threadIdx.x;
   const int g = threadIdx.z;
   double s = 0.0;
   if (i < ntm * 64 && j < ntn * 64) {
-    const int64_t off = (int64_t)((i >> 6) * ntn + (j >> 6)) * 4096 + (i & 63) * 64 + (j & 63);
-    const int64_t stride = (int64_t)ntm * ntn * 4096;
+    int64_t off;
+    int64_t stride;
+    if (sym) {
+      const int a = min(i, j), b = max(i, j);   // (i, j) and (j, i) read the same partial entry
+      const int ta = a >> 6, tb = b >> 6;
+      off = (int64_t)(ta * ntn - ta * (ta - 1) / 2 + (tb - ta)) * 4096 + (a & 63) * 64 + (b & 63);
+      stride = (int64_t)(ntm * (ntm + 1) / 2) * 4096;
+    } else {
+      off = (int64_t)((i >> 6) * ntn + (j >> 6)) * 4096 + (i & 63) * 64 + (j & 63);
+      stride = (int64_t)ntm * ntn * 4096;
+    }
     for (int c = g; c < nchunks; c += 4) s += part[off + c * stride];
   }
   red[g][threadIdx.y][threadIdx.x] = s;
@@ -936,15 +960,22 @@ int gram_chunks(int64_t n, int ntiles) {   // one wave: tiles x chunks <= 148 CT
 }
 
 size_t gram_ws_doubles(int64_t n, int sa, int sb) {
+  // every launch uses chunks x tiles <= max(NSP_GCTAS, tiles) partial tiles (the symmetric Gram has
+  // fewer tiles and so more chunks than the two-operand one)
   const int ntm = (sa + 63) / 64, ntn = 2 * ((sb + 63) / 64);
-  return (size_t)gram_chunks(n, ntm * ntn) * ntm * ntn * 4096;
+  (void)n;
+  return (size_t)std::max(NSP_GCTAS, ntm * ntn) * 4096;
 }
 
 void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb2, int ldb, int sb, int64_t n,
            double* out, double* out2, int ldo, double* ws, cudaStream_t st) {
   const int ntm = (sa + 63) / 64, ntn1 = (sb + 63) / 64;
   const int ntn = Xb2 ? 2 * ntn1 : ntn1;
-  const int nch = gram_chunks(n, ntm * ntn);
+  // Xa == Xb (W^T W, Y^T Y): only the tiles on and above the diagonal (3 of 4 at s = 128)
+  static const bool sym_off = getenv("NSP_GRAM_NOSYM") != nullptr;
+  const int sym = (!sym_off && !Xb2 && Xa == Xb && lda == ldb && sa == sb && ntm > 1) ? 1 : 0;
+  const int ntiles = sym ? ntm * (ntm + 1) / 2 : ntm * ntn;
+  const int nch = gram_chunks(n, ntiles);
   int64_t rpc = (n + nch - 1) / nch;
   rpc = ((rpc + GR - 1) / GR) * GR;
   const size_t smem = GNS * 2 * GR * LDS * sizeof(double);
@@ -955,9 +986,9 @@ void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb
   }
   {
     nsp_count_launch();
-    launch_k(k_gram_partial, dim3(dim3(ntm * ntn, nch)), dim3(256), smem, st, Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn);
+    launch_k(k_gram_partial, dim3(dim3(ntiles, nch)), dim3(256), smem, st, Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn, sym);
   }
-  { nsp_count_launch(); launch_k(k_gram_reduce, dim3(dim3(ntn * 4, ntm * 4)), dim3(dim3(16, 16, 4)), 0, st, ws, nch, ntm, ntn, ntn1, out, out2, ldo); }
+  { nsp_count_launch(); launch_k(k_gram_reduce, dim3(dim3(ntn * 4, ntm * 4)), dim3(dim3(16, 16, 4)), 0, st, ws, nch, ntm, ntn, ntn1, out, out2, ldo, sym); }
 }
 
 void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, int64_t n, double* out, int ldo,
