@@ -1267,6 +1267,107 @@ __global__ void __launch_bounds__(256) k_band_fb_vec(const TriSys* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------------------------
+// One-column chunk sweeps of the partitioned A_G solve (wb <= 1) as ONE matrix-vector product per tile
+// row: forward y_I = X_II w_I - G_I y_{I-1} with G_I = X_II L_{I,I-1}; backward y_I = X_II^T w_I -
+// H_I y_{I+1} with H_I = X_II^T L_{I+1,I}^T (X_II = L_II^{-1}; Xd / Gc tiles formed in setup by
+// k_band_prep, row-dot layout for both directions).  The same triangular solve reassociated: the
+// recurrence carries one product per row instead of two, and the row's two products are one fused dot
+// product (one warp reduction).  One CTA per chunk; the tiles and the rhs tile of the next NS - 1 rows
+// stream in by TMA bulk copies.
+// ---------------------------------------------------------------------------------------------
+template <int NS>
+__global__ void __launch_bounds__(256) k_band_rec_vec(const TriSys* __restrict__ sys, const double* __restrict__ Xd,
+                                                      const double* __restrict__ Gc, double* buf, int fwd) {
+  extern __shared__ __align__(128) double sm[];
+  double* Tr = sm;                 // NS x (Xd tile, Gc tile)
+  double* Wr = sm + NS * 8192;     // NS x 64 rhs
+  double* Vr = Wr + NS * 64;       // 2 x 64: y of the previous row (ping-pong)
+  __shared__ __align__(8) uint64_t bar[NS];
+  const TriSys sy = sys[blockIdx.x];
+  const int nt = sy.nt;
+  if (nt == 0) return;
+  const int64_t t0 = sy.row0 / 64;   // global tile index of the chunk's first row
+  double* Wb = buf + sy.row0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int myrow = warp_reduce8_row(lane);
+  if (tid == 0)
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  auto row_of = [&](int q) { return fwd ? q : nt - 1 - q; };   // q-th step's local tile row
+  auto issue = [&](int q) {
+    if (q >= nt || tid != 0) return;
+    const int sl = q % NS, I = row_of(q);
+    mbar_expect_copy(&bar[sl], Tr + sl * 8192, Xd + (t0 + I) * 4096, 32768);
+    if (q > 0) mbar_add_copy(&bar[sl], Tr + sl * 8192 + 4096, Gc + (t0 + I) * 4096, 32768);
+    mbar_add_copy(&bar[sl], Wr + sl * 64, Wb + (int64_t)I * 64, 512);
+  };
+  for (int q = 0; q < NS - 1; ++q) issue(q);
+  for (int q = 0; q < nt; ++q) {
+    const int sl = q % NS, I = row_of(q);
+    mbar_wait(&bar[sl], (q / NS) & 1);
+    __syncthreads();   // the slot issued next was last read at step q - 1; y_{q-1} is in Vr
+    issue(q + NS - 1);
+    const double* X = Tr + sl * 8192;
+    const double* G = X + 4096;
+    const double* w = Wr + sl * 64;
+    const double* yp = Vr + ((q + 1) & 1) * 64;
+    const double w0 = w[lane], w1 = w[lane + 32];
+    double p8[8];
+    if (q > 0) {
+      const double y0 = yp[lane], y1 = yp[lane + 32];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double* xr = X + (warp * 8 + i) * 64;
+        const double* gr = G + (warp * 8 + i) * 64;
+        p8[i] = fma(xr[lane], w0, fma(xr[lane + 32], w1, -fma(gr[lane], y0, gr[lane + 32] * y1)));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double* xr = X + (warp * 8 + i) * 64;
+        p8[i] = fma(xr[lane], w0, xr[lane + 32] * w1);
+      }
+    }
+    const double y = warp_reduce8(p8, lane);
+    if ((lane & 3) == 0) {
+      Vr[(q & 1) * 64 + warp * 8 + myrow] = y;
+      Wb[(int64_t)I * 64 + warp * 8 + myrow] = y;
+    }
+  }
+  __threadfence();
+}
+
+// Setup for k_band_rec_vec: per tile row I of the band (wb <= 1, diagonal tiles hold X_II = L_II^{-1})
+//   XF_I = X_II, GF_I = X_II L_{I,I-1} (I >= 1), XB_I = X_II^T, GB_I = X_II^T L_{I+1,I}^T (I <= nt - 2)
+// one CTA per tile row, plain FMA products (setup).
+__global__ void __launch_bounds__(256) k_band_prep(const double* __restrict__ T, int nt, int wb, double* XF, double* GF,
+                                                   double* XB, double* GB) {
+  __shared__ double Xs[64][65];
+  const int I = blockIdx.x, tid = threadIdx.x;
+  auto tile = [&](int r, int c) { return T + ((int64_t)c * (wb + 1) + (r - c)) * NSP_TILE_ELEMS; };
+  const double* Xg = tile(I, I);
+  for (int e = tid; e < 4096; e += 256) {
+    Xs[e >> 6][e & 63] = Xg[e];
+    XF[(int64_t)I * 4096 + e] = Xg[e];
+    XB[(int64_t)I * 4096 + e] = Xg[(e & 63) * 64 + (e >> 6)];
+  }
+  __syncthreads();
+  const double* Lf = (wb >= 1 && I >= 1) ? tile(I, I - 1) : nullptr;        // L_{I,I-1}
+  const double* Lb = (wb >= 1 && I + 1 < nt) ? tile(I + 1, I) : nullptr;    // L_{I+1,I}
+  for (int e = tid; e < 4096; e += 256) {
+    const int r = e >> 6, cc = e & 63;
+    double gf = 0.0, gb = 0.0;
+    for (int k = 0; k < 64; ++k) {
+      if (Lf) gf = fma(Xs[r][k], Lf[k * 64 + cc], gf);    // (X_II L_{I,I-1})[r][c]
+      if (Lb) gb = fma(Xs[k][r], Lb[cc * 64 + k], gb);    // (X_II^T L_{I+1,I}^T)[r][c]
+    }
+    GF[(int64_t)I * 4096 + e] = gf;
+    GB[(int64_t)I * 4096 + e] = gb;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Partitioned ("spike") narrow-band solve of the A_G factor.  The band rows are cut into P chunks of
 // consecutive 64-row tiles; chunk k couples to chunk k-1 only through one factor tile C_k (first tile
 // row of k x last tile column of k-1).  With the spikes S_k = L_kk^{-1} [C_k; 0] and
@@ -1503,6 +1604,25 @@ void spmm_cs(const DevCSR& A, const double* X, int ldx, const double* U, int ldu
 void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split, double* Y,
           int ldy, int s, int mode, bool zero_pad, cudaStream_t st) {
   spmm_cs(A, X, ldx, U, ldu, 32, split, Y, ldy, 32, ldy, s, mode, zero_pad, st);
+}
+
+void band_prep(const double* T, int nt, int wb, double* XF, double* GF, double* XB, double* GB, cudaStream_t st) {
+  if (nt <= 0) return;
+  nsp_count_launch();
+  k_band_prep<<<nt, 256, 0, st>>>(T, nt, wb, XF, GF, XB, GB);
+}
+
+void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, double* buf, bool fwd, cudaStream_t st) {
+  if (nsys <= 0) return;
+  constexpr int NS = 3;
+  const size_t smem = (NS * 8192 + NS * 64 + 2 * 64) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_band_rec_vec<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  nsp_count_launch();
+  k_band_rec_vec<NS><<<nsys, 256, smem, st>>>(sys, Xd, Gc, buf, fwd ? 1 : 0);
 }
 
 void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,

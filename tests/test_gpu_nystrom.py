@@ -274,7 +274,8 @@ def test_m2_pcg_with_chebyshev_ag(name):
 def test_ag_partitioned_band_parity(spikes, monkeypatch):
     """The partitioned ("spike") A_G band solve (nt >= 16 tile rows, band <= 1 tile: cfg2m) against the
     oracle's direct solve and against the unpartitioned sweep (NSP_NO_SPIKE=1): s = 1 (matrix-vector
-    chain kernels), 7 and 64 (DMMA spike recurrence / update), relative error <= 1e-12."""
+    chain kernels; partitioned: the reassociated one-product recurrence k_band_rec_vec), 7 and 64 (DMMA
+    spike recurrence / update), relative error <= 1e-12."""
     if not spikes:
         monkeypatch.setenv("NSP_NO_SPIKE", "1")
     pr, d, S = problem("cfg2m")
