@@ -1431,34 +1431,33 @@ __global__ void __launch_bounds__(256) k_spike_tail(const double* __restrict__ s
 __global__ void __launch_bounds__(256) k_spike_tail_vec(const double* __restrict__ spk,
                                                         const int* __restrict__ chunk_first, int P,
                                                         double* buf, int fwd) {
-  extern __shared__ __align__(128) double sm[];   // 2 x 4096 spike tiles
-  __shared__ double xs[64];
-  __shared__ __align__(8) uint64_t bar[2];
+  extern __shared__ __align__(128) double sm[];   // 3 x 4096 spike tiles (ring)
+  __shared__ double xs[2][64];                     // ping-pong: the coupling vector of the previous step
+  __shared__ __align__(8) uint64_t bar[3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nstep = P - 1;
   // step j: the tile row updated (and whose spike rows are used) and the tile row it reads
   auto tile_of = [&](int j) { return fwd ? chunk_first[j + 2] - 1 : chunk_first[P - 2 - j]; };
   auto src_of = [&](int j) { return fwd ? chunk_first[j + 1] - 1 : chunk_first[P - 1 - j]; };
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   if (tid == 0) {
-    for (int j = 0; j < 2 && j < nstep; ++j)
+    for (int j = 0; j < 3 && j < nstep; ++j)
       mbar_expect_copy(&bar[j], sm + j * 4096, spk + (int64_t)tile_of(j) * 4096, 4096 * 8);
   }
-  if (tid < 64) xs[tid] = buf[(int64_t)src_of(0) * 64 + tid];
+  if (tid < 64) xs[0][tid] = buf[(int64_t)src_of(0) * 64 + tid];
   __syncthreads();
   const int myrow = 8 * warp + warp_reduce8_row(lane);
   for (int j = 0; j < nstep; ++j) {
     const int t = tile_of(j);
     const double y = (lane & 3) == 0 ? buf[(int64_t)t * 64 + myrow] : 0.0;
-    const int b = j & 1;
-    mbar_wait(&bar[b], (j >> 1) & 1);
+    const int b = j % 3;
+    mbar_wait(&bar[b], (j / 3) & 1);
     const double* S = sm + b * 4096;
-    const double x0 = xs[lane], x1 = xs[lane + 32];
+    const double x0 = xs[j & 1][lane], x1 = xs[j & 1][lane + 32];
     double v[8];
 #pragma unroll
     for (int rr = 0; rr < 8; ++rr) {
@@ -1466,17 +1465,16 @@ __global__ void __launch_bounds__(256) k_spike_tail_vec(const double* __restrict
       v[rr] = fma(Sr[lane], x0, Sr[lane + 32] * x1);
     }
     v[0] = warp_reduce8(v, lane);
-    __syncthreads();   // every read of xs and of ring slot b is done
     if ((lane & 3) == 0) {
       const double o = y - v[0];
-      xs[myrow] = o;
+      xs[(j + 1) & 1][myrow] = o;
       buf[(int64_t)t * 64 + myrow] = o;
     }
-    if (tid == 0 && j + 2 < nstep) {
+    __syncthreads();   // xs of this step visible; every read of ring slot b (and of xs[j & 1]) is done
+    if (tid == 0 && j + 3 < nstep) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      mbar_expect_copy(&bar[b], sm + b * 4096, spk + (int64_t)tile_of(j + 2) * 4096, 4096 * 8);
+      mbar_expect_copy(&bar[b], sm + b * 4096, spk + (int64_t)tile_of(j + 3) * 4096, 4096 * 8);
     }
-    __syncthreads();
   }
 }
 
@@ -1689,10 +1687,10 @@ void spike_tail(const double* spk, const int* chunk_first, int P, double* buf, i
   if (s == 1 && ldw == 1) {
     static bool attr1 = false;
     if (!attr1) {
-      cudaFuncSetAttribute(k_spike_tail_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 8);
+      cudaFuncSetAttribute(k_spike_tail_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4096 * 8);
       attr1 = true;
     }
-    { nsp_count_launch(); k_spike_tail_vec<<<1, 256, 2 * 4096 * 8, st>>>(spk, chunk_first, P, buf, fwd); }
+    { nsp_count_launch(); k_spike_tail_vec<<<1, 256, 3 * 4096 * 8, st>>>(spk, chunk_first, P, buf, fwd); }
     return;
   }
   if (ldw % 32 == 0 && !getenv("NSP_SPIKE_OLD")) {
