@@ -248,6 +248,8 @@ void symv1(const FacSub* subs, const int2* items, int nitems, int max_ntb, const
 // partitioned A_G solve, one column: the reassociated chunk sweeps (k_band_rec_vec) and their setup
 void band_prep(const double* T, int nt, int wb, double* XF, double* GF, double* XB, double* GB, cudaStream_t st);
 void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, double* buf, bool fwd, cudaStream_t st);
+void band_rec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, double* buf, int ldw, bool fwd,
+              cudaStream_t st);
 void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,
             int wbmax = -1);
 // partitioned narrow-band solve of the A_G factor: coupling-tile recurrence / parallel spike update

@@ -1338,6 +1338,64 @@ __global__ void __launch_bounds__(256) k_band_rec_vec(const TriSys* __restrict__
   __threadfence();
 }
 
+// The same reassociated chunk sweep for s > 1 (CW-column slices, DMMA): per tile row
+// V_I = Xd_I W_I - Gc_I V_prev as two 64 x 64 x CW tile products into two accumulators, one CTA
+// barrier per row; the next row's two tiles and rhs tile are staged by cp.async behind this row's
+// products (2 stages).  Xd / Gc as in k_band_rec_vec.
+template <int CW>
+__global__ void __launch_bounds__(256) k_band_rec(const TriSys* __restrict__ sys, const double* __restrict__ Xd,
+                                                  const double* __restrict__ Gc, double* buf, int ldw, int fwd) {
+  constexpr int NF = CW / 16;
+  constexpr int LDV = CW + 4;
+  extern __shared__ double sm[];
+  double* Xs = sm;                    // 2 x 64 x LDT
+  double* Gs = Xs + 2 * 64 * LDT;     // 2 x 64 x LDT
+  double* Ws = Gs + 2 * 64 * LDT;     // 2 x 64 x LDV
+  double* Vs = Ws + 2 * 64 * LDV;     // 2 x 64 x LDV (ping-pong: the previous row's solution)
+  const TriSys sy = sys[blockIdx.x];
+  const int nt = sy.nt;
+  if (nt == 0) return;
+  const int64_t t0 = sy.row0 / 64;
+  const int c0 = blockIdx.y * CW;
+  double* Wb = buf + sy.row0 * (int64_t)ldw + c0;
+  auto row_of = [&](int q) { return fwd ? q : nt - 1 - q; };
+  auto issue = [&](int q) {
+    if (q >= nt) return;
+    const int sl = q & 1, I = row_of(q);
+    cp_block(Xs + sl * 64 * LDT, LDT, Xd + (t0 + I) * 4096, 64, 64, 64);
+    if (q > 0) cp_block(Gs + sl * 64 * LDT, LDT, Gc + (t0 + I) * 4096, 64, 64, 64);
+    cp_block(Ws + sl * 64 * LDV, LDV, Wb + (int64_t)I * 64 * ldw, ldw, 64, CW);
+  };
+  issue(0);
+  cp_commit();
+  for (int q = 0; q < nt; ++q) {
+    const int sl = q & 1, I = row_of(q);
+    cp_wait<0>();
+    __syncthreads();   // stage q landed; V of row q - 1 visible; stage q + 1's slot was last read at q - 1
+    issue(q + 1);
+    cp_commit();
+    double acc[2][NF][2], accg[2][NF][2];
+    acc_zero(acc);
+    acc_zero(accg);
+    cta_mma<NF, false, false>(Xs + sl * 64 * LDT, LDT, Ws + sl * 64 * LDV, LDV, acc);
+    if (q > 0) cta_mma<NF, false, false>(Gs + sl * 64 * LDT, LDT, Vs + ((q + 1) & 1) * 64 * LDV, LDV, accg);
+    double* Vo = Vs + (q & 1) * 64 * LDV;
+    double* out = Wb + (int64_t)I * 64 * ldw;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+        const double v0 = acc[i][j][0] - accg[i][j][0], v1 = acc[i][j][1] - accg[i][j][1];
+        Vo[r * LDV + c] = v0;
+        Vo[r * LDV + c + 1] = v1;
+        *reinterpret_cast<double2*>(out + (int64_t)r * ldw + c) = make_double2(v0, v1);
+      }
+  }
+  cp_wait<0>();
+  __threadfence();
+}
+
 // Setup for k_band_rec_vec: per tile row I of the band (wb <= 1, diagonal tiles hold X_II = L_II^{-1})
 //   XF_I = X_II, GF_I = X_II L_{I,I-1} (I >= 1), XB_I = X_II^T, GB_I = X_II^T L_{I+1,I}^T (I <= nt - 2)
 // one CTA per tile row, plain FMA products (setup).
@@ -1608,6 +1666,31 @@ void band_prep(const double* T, int nt, int wb, double* XF, double* GF, double* 
   if (nt <= 0) return;
   nsp_count_launch();
   k_band_prep<<<nt, 256, 0, st>>>(T, nt, wb, XF, GF, XB, GB);
+}
+
+void band_rec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, double* buf, int ldw, bool fwd,
+              cudaStream_t st) {
+  if (nsys <= 0) return;
+  // few independent sweeps: 16-wide column slices double the CTAs (as in tri_fb)
+  if (nsys * (ldw / 32) < 2 * 148) {
+    const size_t smem = (4 * 64 * LDT + 4 * 64 * 20) * sizeof(double);
+    static bool attr16 = false;
+    if (!attr16) {
+      cudaFuncSetAttribute(k_band_rec<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr16 = true;
+    }
+    nsp_count_launch();
+    k_band_rec<16><<<dim3(nsys, ldw / 16), 256, smem, st>>>(sys, Xd, Gc, buf, ldw, fwd ? 1 : 0);
+    return;
+  }
+  const size_t smem = (4 * 64 * LDT + 4 * 64 * 36) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_band_rec<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  nsp_count_launch();
+  k_band_rec<32><<<dim3(nsys, ldw / 32), 256, smem, st>>>(sys, Xd, Gc, buf, ldw, fwd ? 1 : 0);
 }
 
 void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, double* buf, bool fwd, cudaStream_t st) {
