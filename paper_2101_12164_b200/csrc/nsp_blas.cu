@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__
   constexpr int STG = 2 * GR * LDS;
   const int tile = blockIdx.x;
   int tm = tile / ntn, tn = tile - tm * ntn;
-  if (sym) {   // Xa == Xb: only the tiles tm <= tn, enumerated row by row
+  if (sym == 1) {   // Xa == Xb: only the tiles tm <= tn, enumerated row by row
     tm = 0;
     int rem = tile;
     while (rem >= ntn - tm) {
@@ -68,6 +68,17 @@ __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__
       ++tm;
     }
     tn = tm + rem;
+  } else if (sym == 2) {   // [D | E]: the lower tiles tn <= tm of D (its only consumer is chol), then all of E
+    const int nlo = ntm * (ntm + 1) / 2;
+    if (tile < nlo) {
+      tm = 0;
+      while ((tm + 1) * (tm + 2) / 2 <= tile) ++tm;
+      tn = tile - tm * (tm + 1) / 2;
+    } else {
+      const int u = tile - nlo;
+      tm = u / ntn1;
+      tn = ntn1 + (u - tm * ntn1);
+    }
   }
   const int64_t r0 = blockIdx.y * rows_per_chunk;
   const int64_t r1 = min(n, r0 + rows_per_chunk);
@@ -116,7 +127,7 @@ __global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int 
   // a 16 x 16 output block below the diagonal (sym) is read transposed from its upper partner with the
   // threads swapped (coalesced reads) and written transposed; diagonal blocks pick (min, max) per element
   const int bi = blockIdx.y * 16, bj = blockIdx.x * 16;
-  const bool tr = sym && bi > bj;
+  const bool tr = (sym == 1 && bi > bj) || (sym == 2 && bi < bj && bj < ntn1 * 64);   // mirrored blocks
   const int i = tr ? bi + threadIdx.x : bi + threadIdx.y;
   const int j = tr ? bj + threadIdx.y : bj + threadIdx.x;
   const int g = threadIdx.z;
@@ -124,11 +135,21 @@ __global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int 
   if (i < ntm * 64 && j < ntn * 64) {
     int64_t off;
     int64_t stride;
-    if (sym) {
+    if (sym == 1) {
       const int a = min(i, j), b = max(i, j);   // (i, j) and (j, i) read the same partial entry
       const int ta = a >> 6, tb = b >> 6;
       off = (int64_t)(ta * ntn - ta * (ta - 1) / 2 + (tb - ta)) * 4096 + (a & 63) * 64 + (b & 63);
       stride = (int64_t)(ntm * (ntm + 1) / 2) * 4096;
+    } else if (sym == 2) {
+      const int nlo = ntm * (ntm + 1) / 2;
+      if (j < ntn1 * 64) {                        // D: the lower partial, mirrored above the diagonal
+        const int a = max(i, j), b = min(i, j);
+        const int ta = a >> 6, tb = b >> 6;
+        off = (int64_t)(ta * (ta + 1) / 2 + tb) * 4096 + (a & 63) * 64 + (b & 63);
+      } else {
+        off = (int64_t)(nlo + (i >> 6) * ntn1 + ((j >> 6) - ntn1)) * 4096 + (i & 63) * 64 + (j & 63);
+      }
+      stride = (int64_t)(nlo + ntm * ntn1) * 4096;
     } else {
       off = (int64_t)((i >> 6) * ntn + (j >> 6)) * 4096 + (i & 63) * 64 + (j & 63);
       stride = (int64_t)ntm * ntn * 4096;
@@ -968,13 +989,15 @@ size_t gram_ws_doubles(int64_t n, int sa, int sb) {
 }
 
 void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb2, int ldb, int sb, int64_t n,
-           double* out, double* out2, int ldo, double* ws, cudaStream_t st) {
+           double* out, double* out2, int ldo, double* ws, cudaStream_t st, bool lower_first) {
   const int ntm = (sa + 63) / 64, ntn1 = (sb + 63) / 64;
   const int ntn = Xb2 ? 2 * ntn1 : ntn1;
   // Xa == Xb (W^T W, Y^T Y): only the tiles on and above the diagonal (3 of 4 at s = 128)
   static const bool sym_off = getenv("NSP_GRAM_NOSYM") != nullptr;
-  const int sym = (!sym_off && !Xb2 && Xa == Xb && lda == ldb && sa == sb && ntm > 1) ? 1 : 0;
-  const int ntiles = sym ? ntm * (ntm + 1) / 2 : ntm * ntn;
+  int sym = (!sym_off && !Xb2 && Xa == Xb && lda == ldb && sa == sb && ntm > 1) ? 1 : 0;
+  // [D | E] with D read only through its lower triangle: D's upper tiles are mirrored, not computed
+  if (!sym_off && lower_first && Xb2 && ntn1 == ntm && ntm > 1) sym = 2;
+  const int ntiles = sym == 1 ? ntm * (ntm + 1) / 2 : sym == 2 ? ntm * (ntm + 1) / 2 + ntm * ntn1 : ntm * ntn;
   const int nch = gram_chunks(n, ntiles);
   int64_t rpc = (n + nch - 1) / nch;
   rpc = ((rpc + GR - 1) / GR) * GR;

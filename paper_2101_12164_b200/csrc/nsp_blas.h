@@ -43,7 +43,7 @@ void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, 
 // Out = Cin + sgn * In(n x kdim) M(kdim x ncols); ncols multiple of 64, kdim multiple of 32
 // out = Xa^T Xb, out2 = Xa^T Xb2 (shared left operand, one pass)
 void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb2, int ldb, int sb, int64_t n,
-           double* out, double* out2, int ldo, double* ws, cudaStream_t st);
+           double* out, double* out2, int ldo, double* ws, cudaStream_t st, bool lower_first = false);
 // two independent panels in one launch (a1 may be null)
 void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64_t n, cudaStream_t st);
 // returns the number of normpart rows written (row tiles, or CTAs of the one-wave s = 128 kernel)

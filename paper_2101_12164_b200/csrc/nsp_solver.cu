@@ -279,7 +279,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     tr.mark("loop");
     if ((e2 = op_apply(c, w, w.P, w.Q, s)) != NSP_OK) return e2;
     tr.mark("apply");
-    nspb::gram2(w.P, sp, sp, w.Q, w.R, sp, sp, ng, w.D, w.E, sp, w.gram, q);
+    nspb::gram2(w.P, sp, sp, w.Q, w.R, sp, sp, ng, w.D, w.E, sp, w.gram, q, true);   // D: lower tiles (chol)
     if (multi) {   // D and E are adjacent in the workspace: one allreduce
       if ((e2 = comm_allreduce(c, w.D, (size_t)2 * sp * sp)) != NSP_OK) return e2;
     }
