@@ -93,6 +93,19 @@ __device__ __forceinline__ void cp_block(double* s, int sld, const double* g, in
   }
 }
 
+// bulk shared -> global store (TMA store, bulk-group completion); 16-byte aligned, size % 16 == 0.
+// The writing threads fence their shared-memory stores to the async proxy (fence_proxy_async) and
+// synchronise before the issue; the issuing thread waits for its group before the kernel exits.
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"((unsigned)__cvta_generic_to_shared(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store_commit_wait() {   // the source may be reused / the CTA may exit
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
 // mbarrier + bulk-copy (TMA, cp.async.bulk) helpers
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));

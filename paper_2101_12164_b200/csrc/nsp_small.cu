@@ -206,14 +206,15 @@ __global__ void __launch_bounds__(256) k_chol16(const double* __restrict__ Ain, 
   const int width = nact < 0 ? st->width : nact;
   const int NB = sp / 16;
   CPROF(0)
-  {  // async 16-byte staging (all loads in flight at once), then the identity fix-up
-    const int cpr = sp / 2;
-    for (int e = tid; e < sp * cpr; e += 256) {
-      const int i = e / cpr, q = e - i * cpr;
-      if (2 * q <= i) cp_async16(As + i * LDA + 2 * q, Ain + (int64_t)i * sp + 2 * q);
+  {  // one bulk copy (TMA) per row of the lower triangle, all on one mbarrier, then the identity fix-up
+    __shared__ __align__(8) uint64_t lbar;
+    if (tid == 0) {
+      mbar_init(&lbar, sp);
+      fence_mbar_init();
     }
-    cp_commit();
-    cp_wait<0>();
+    __syncthreads();
+    if (tid < sp) mbar_expect_copy(&lbar, As + tid * LDA, Ain + (int64_t)tid * sp, 8u * ((tid + 2) & ~1));
+    mbar_wait(&lbar, 0);
     __syncthreads();
     if (width < sp)
       for (int e = tid; e < sp * sp; e += 256) {
@@ -305,22 +306,17 @@ __global__ void __launch_bounds__(256) k_chol16(const double* __restrict__ Ain, 
       }
     }
   }
-  // output, two doubles per thread per step (sp is 64 or 128: shifts, no division)
-  const int lsp = sp == 128 ? 7 : 6;
-#pragma unroll 8
-  for (int e = 2 * tid; e < sp * sp; e += 512) {
-    const int i = e >> lsp, j = e & (sp - 1);
-    const int bi = i >> 4, bj = j >> 4;
-    if (bi < bj) continue;   // strictly-upper blocks are never read (k_chol_solve zero-fills them)
-    double2 v = make_double2(0.0, 0.0);
-    if (bi == bj) {
-      const double* xr = Di + bi * 256 + (i & 15) * 16 + (j & 15);
-      v.x = ((j & 15) <= (i & 15)) ? xr[0] : 0.0;
-      v.y = (((j + 1) & 15) <= (i & 15)) ? xr[1] : 0.0;
-    } else if (bi > bj) {
-      v = make_double2(As[i * LDA + j], As[i * LDA + j + 1]);
-    }
-    *reinterpret_cast<double2*>(Lp + e) = v;
+  // output: X_kk (zero above its diagonal) overwrites L_kk in As, then every row's stored part
+  // (columns < 16 (bi + 1); the strictly-upper blocks are not written) leaves by one bulk copy
+  for (int e = tid; e < NB * 256; e += 256) {
+    const int b = e >> 8, r = (e >> 4) & 15, c2 = e & 15;
+    As[(16 * b + r) * LDA + 16 * b + c2] = c2 <= r ? Di[b * 256 + r * 16 + c2] : 0.0;
+  }
+  fence_proxy_async();
+  __syncthreads();
+  if (tid < sp) {
+    bulk_store(Lp + (int64_t)tid * sp, As + tid * LDA, 16u * ((tid >> 4) + 1) * 8u);
+    bulk_store_commit_wait();
   }
   CPROF(40)
 }
