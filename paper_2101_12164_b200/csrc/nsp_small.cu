@@ -339,23 +339,24 @@ __global__ void __launch_bounds__(128) k_chol_solve(const double* __restrict__ L
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int c0 = blockIdx.x * 8;
-  {
-    const int cpr = sp / 2;
-    for (int e = tid; e < sp * cpr; e += 128) {
-      const int i = e / cpr, q = e - i * cpr;
-      if (2 * q <= i) cp_async16(Ls + i * LD + 2 * q, Lp + (int64_t)i * sp + 2 * q);
-      else {
-        Ls[i * LD + 2 * q] = 0.0;
-        Ls[i * LD + 2 * q + 1] = 0.0;
-      }
-    }
-    cp_commit();
+  // Lp row i up to the end of its diagonal block by one bulk copy (TMA, one mbarrier); the columns
+  // beyond (the strictly-upper blocks, never written by k_chol16) are zero-filled
+  __shared__ __align__(8) uint64_t lbar;
+  if (tid == 0) {
+    mbar_init(&lbar, sp);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  for (int i = tid; i < sp; i += 128) {
+    const int w = 16 * ((i >> 4) + 1);
+    mbar_expect_copy(&lbar, Ls + i * LD, Lp + (int64_t)i * sp, 8u * w);
+    for (int j = w; j < sp; ++j) Ls[i * LD + j] = 0.0;
   }
   for (int e = tid; e < sp * 8; e += 128) {
     const int i = e >> 3, c = e & 7;
     x[i * LX + c] = B ? B[(int64_t)i * ldb + c0 + c] : (i == c0 + c ? 1.0 : 0.0);
   }
-  cp_wait<0>();
+  mbar_wait(&lbar, 0);
   __syncthreads();
   const int NB = sp / 16;
   if (fwd)
