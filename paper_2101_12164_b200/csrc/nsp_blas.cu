@@ -243,16 +243,21 @@ __global__ void __launch_bounds__(256) k_panel(PanelArgs pa0, PanelArgs pa1, int
 // The same panel for the 128-column case (s x s multiplier M with s = 128) as ONE wave: one CTA per
 // SM, each owning a contiguous range of 16-row groups (balanced to +-1 group, where 64-row tiles
 // quantise to 2 tiles on some SMs and 1 on others), M resident in shared memory (read once per CTA),
-// In streamed through a PNS-stage ring of 64 x 32 chunks, 16 warps = 4 row groups x 4 column quarters
+// In streamed through a PNS-stage ring of 64 x PKC chunks (64 x 64, 2 stages: half the barriers of
+// 64 x 32 x 4 stages, panel 30.5 -> 29.9 us, cfg2 25.85 -> 25.58 ms), 16 warps = 4 row groups x 4 column quarters
 // of a 64 x 128 pass; Cin prefetched into registers at the start of each pass.  normpart (optional):
 // one row per CTA, the column sums of squares over its rows (fixed order).
 #ifndef NSP_PANEL_NW
 #define NSP_PANEL_NW 16
 #endif
 #ifndef NSP_PNS
-#define NSP_PNS 4
+#define NSP_PNS 2
 #endif
-constexpr int PLDM = 132, PLDA = 36, PNS = NSP_PNS;
+#ifndef NSP_PKC
+#define NSP_PKC 64
+#endif
+constexpr int PKC = NSP_PKC, PSPP = 128 / PKC;   // chunk width, chunks per 64-row pass
+constexpr int PLDM = 132, PLDA = PKC + 4, PNS = NSP_PNS;
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t n, int64_t ngroups) {
   // NW = 16: warps = 4 row groups x 4 column quarters (16 x 32 per warp); NW = 8: 4 row groups x 2
@@ -269,11 +274,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t
   const int64_t g1 = (int64_t)(blockIdx.x + 1) * ngroups / gridDim.x;
   const int64_t r0 = g0 * 16, r1 = min(n, g1 * 16);
   const int npass = r1 > r0 ? (int)((r1 - r0 + 63) / 64) : 0;
-  const int nsteps = npass * 4;
+  const int nsteps = npass * PSPP;
   const double* __restrict__ In = pa.In;
   auto issue = [&](int q) {
-    const int64_t rp = r0 + (int64_t)(q >> 2) * 64;
-    cp_block_zf(Ar + (q % PNS) * 64 * PLDA, PLDA, In + rp * pa.ldi + (q & 3) * 32, pa.ldi, 64, 32, r1 - rp);
+    const int64_t rp = r0 + (int64_t)(q / PSPP) * 64;
+    cp_block_zf(Ar + (q % PNS) * 64 * PLDA, PLDA, In + rp * pa.ldi + (q % PSPP) * PKC, pa.ldi, 64, PKC, r1 - rp);
   };
   cp_block(Ms, PLDM, pa.M, pa.ldm, 128, 128);
 #pragma unroll
@@ -288,8 +293,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t
   for (int j = 0; j < NF; ++j) sq[j][0] = sq[j][1] = 0.0;
   double2 cin[2][NF];
   for (int q = 0; q < nsteps; ++q) {
-    const int kc = q & 3;
-    const int64_t rp = r0 + (int64_t)(q >> 2) * 64;
+    const int kc = q % PSPP;
+    const int64_t rp = r0 + (int64_t)(q / PSPP) * 64;
     if (kc == 0) {   // this pass's Cin, in flight behind the pass's four chunk products
 #pragma unroll
       for (int i = 0; i < 2; ++i)
@@ -308,8 +313,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t
     const double* As = Ar + (q % PNS) * 64 * PLDA;
     // a warp whose 16-row group lies past the range skips its products (the DMMA pipe is the limit)
     if (rp + rg * 16 < r1)
-      cta_mma<NF, false, false>(As + rg * 16 * PLDA, PLDA, Ms + kc * 32 * PLDM + cb, PLDM, acc, 32, 0);
-    if (kc == 3) {
+      cta_mma<NF, false, false>(As + rg * 16 * PLDA, PLDA, Ms + kc * PKC * PLDM + cb, PLDM, acc, PKC, 0);
+    if (kc == PSPP - 1) {
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
