@@ -239,7 +239,6 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_gchunk_first);
   fr(c->d_gtile_chunk);
   fr(c->d_gspkF);
-  fr(c->d_gXF);
   fr(c->d_gGF);
   fr(c->d_gXB);
   fr(c->d_gGB);

@@ -131,8 +131,7 @@ struct nsp_ctx {
   TriSys* d_gchunks = nullptr;
   int* d_gchunk_first = nullptr;   // P + 1
   int* d_gtile_chunk = nullptr;    // g_nt
-  double* d_gXF = nullptr;         // g_nt tiles each (g_P > 1, wb <= 1): k_band_rec_vec operands
-  double* d_gGF = nullptr;
+  double* d_gGF = nullptr;         // g_nt tiles each (g_P > 1, wb <= 1): k_band_rec operands
   double* d_gXB = nullptr;
   double* d_gGB = nullptr;
   double* d_gspkF = nullptr;       // g_nt*64 x 64: S_k rows
@@ -247,9 +246,11 @@ void symv1(const FacSub* subs, const int2* items, int nitems, int max_ntb, const
            double* U, double* P, cudaStream_t st);
 // partitioned A_G solve, one column: the reassociated chunk sweeps (k_band_rec_vec) and their setup
 void band_prep(const double* T, int nt, int wb, double* XF, double* GF, double* XB, double* GB, cudaStream_t st);
-void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, double* buf, bool fwd, cudaStream_t st);
-void band_rec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, double* buf, int ldw, bool fwd,
-              cudaStream_t st);
+// Xd tile of row I at Xd + I * xstride * 4096 (the band's own diagonal tiles: xstride = wb + 1)
+void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, int64_t xstride, const double* Gc, double* buf, bool fwd,
+                  cudaStream_t st);
+void band_rec(const TriSys* sys, int nsys, const double* Xd, int64_t xstride, const double* Gc, double* buf, int ldw,
+              bool fwd, cudaStream_t st);
 void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,
             int wbmax = -1);
 // partitioned narrow-band solve of the A_G factor: coupling-tile recurrence / parallel spike update

@@ -1277,7 +1277,8 @@ __global__ void __launch_bounds__(256) k_band_fb_vec(const TriSys* __restrict__ 
 // ---------------------------------------------------------------------------------------------
 template <int NS>
 __global__ void __launch_bounds__(256) k_band_rec_vec(const TriSys* __restrict__ sys, const double* __restrict__ Xd,
-                                                      const double* __restrict__ Gc, double* buf, int fwd) {
+                                                      int64_t xstride, const double* __restrict__ Gc, double* buf,
+                                                      int fwd) {
   extern __shared__ __align__(128) double sm[];
   double* Tr = sm;                 // NS x (Xd tile, Gc tile)
   double* Wr = sm + NS * 8192;     // NS x 64 rhs
@@ -1298,7 +1299,7 @@ __global__ void __launch_bounds__(256) k_band_rec_vec(const TriSys* __restrict__
   auto issue = [&](int q) {
     if (q >= nt || tid != 0) return;
     const int sl = q % NS, I = row_of(q);
-    mbar_expect_copy(&bar[sl], Tr + sl * 8192, Xd + (t0 + I) * 4096, 32768);
+    mbar_expect_copy(&bar[sl], Tr + sl * 8192, Xd + (t0 + I) * xstride * 4096, 32768);
     if (q > 0) mbar_add_copy(&bar[sl], Tr + sl * 8192 + 4096, Gc + (t0 + I) * 4096, 32768);
     mbar_add_copy(&bar[sl], Wr + sl * 64, Wb + (int64_t)I * 64, 512);
   };
@@ -1344,7 +1345,8 @@ __global__ void __launch_bounds__(256) k_band_rec_vec(const TriSys* __restrict__
 // products (2 stages).  Xd / Gc as in k_band_rec_vec.
 template <int CW>
 __global__ void __launch_bounds__(256) k_band_rec(const TriSys* __restrict__ sys, const double* __restrict__ Xd,
-                                                  const double* __restrict__ Gc, double* buf, int ldw, int fwd) {
+                                                  int64_t xstride, const double* __restrict__ Gc, double* buf, int ldw,
+                                                  int fwd) {
   constexpr int NF = CW / 16;
   constexpr int LDV = CW + 4;
   extern __shared__ double sm[];
@@ -1362,7 +1364,7 @@ __global__ void __launch_bounds__(256) k_band_rec(const TriSys* __restrict__ sys
   auto issue = [&](int q) {
     if (q >= nt) return;
     const int sl = q & 1, I = row_of(q);
-    cp_block(Xs + sl * 64 * LDT, LDT, Xd + (t0 + I) * 4096, 64, 64, 64);
+    cp_block(Xs + sl * 64 * LDT, LDT, Xd + (t0 + I) * xstride * 4096, 64, 64, 64);
     if (q > 0) cp_block(Gs + sl * 64 * LDT, LDT, Gc + (t0 + I) * 4096, 64, 64, 64);
     cp_block(Ws + sl * 64 * LDV, LDV, Wb + (int64_t)I * 64 * ldw, ldw, 64, CW);
   };
@@ -1407,7 +1409,7 @@ __global__ void __launch_bounds__(256) k_band_prep(const double* __restrict__ T,
   const double* Xg = tile(I, I);
   for (int e = tid; e < 4096; e += 256) {
     Xs[e >> 6][e & 63] = Xg[e];
-    XF[(int64_t)I * 4096 + e] = Xg[e];
+    if (XF) XF[(int64_t)I * 4096 + e] = Xg[e];
     XB[(int64_t)I * 4096 + e] = Xg[(e & 63) * 64 + (e >> 6)];
   }
   __syncthreads();
@@ -1668,8 +1670,8 @@ void band_prep(const double* T, int nt, int wb, double* XF, double* GF, double* 
   k_band_prep<<<nt, 256, 0, st>>>(T, nt, wb, XF, GF, XB, GB);
 }
 
-void band_rec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, double* buf, int ldw, bool fwd,
-              cudaStream_t st) {
+void band_rec(const TriSys* sys, int nsys, const double* Xd, int64_t xstride, const double* Gc, double* buf, int ldw,
+              bool fwd, cudaStream_t st) {
   if (nsys <= 0) return;
   // few independent sweeps: 16-wide column slices double the CTAs (as in tri_fb)
   if (nsys * (ldw / 32) < 2 * 148) {
@@ -1680,7 +1682,7 @@ void band_rec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, d
       attr16 = true;
     }
     nsp_count_launch();
-    k_band_rec<16><<<dim3(nsys, ldw / 16), 256, smem, st>>>(sys, Xd, Gc, buf, ldw, fwd ? 1 : 0);
+    k_band_rec<16><<<dim3(nsys, ldw / 16), 256, smem, st>>>(sys, Xd, xstride, Gc, buf, ldw, fwd ? 1 : 0);
     return;
   }
   const size_t smem = (4 * 64 * LDT + 4 * 64 * 36) * sizeof(double);
@@ -1690,10 +1692,11 @@ void band_rec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, d
     attr = true;
   }
   nsp_count_launch();
-  k_band_rec<32><<<dim3(nsys, ldw / 32), 256, smem, st>>>(sys, Xd, Gc, buf, ldw, fwd ? 1 : 0);
+  k_band_rec<32><<<dim3(nsys, ldw / 32), 256, smem, st>>>(sys, Xd, xstride, Gc, buf, ldw, fwd ? 1 : 0);
 }
 
-void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, const double* Gc, double* buf, bool fwd, cudaStream_t st) {
+void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, int64_t xstride, const double* Gc, double* buf, bool fwd,
+                  cudaStream_t st) {
   if (nsys <= 0) return;
   constexpr int NS = 3;
   const size_t smem = (NS * 8192 + NS * 64 + 2 * 64) * sizeof(double);
@@ -1703,7 +1706,7 @@ void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, const double* G
     attr = true;
   }
   nsp_count_launch();
-  k_band_rec_vec<NS><<<nsys, 256, smem, st>>>(sys, Xd, Gc, buf, fwd ? 1 : 0);
+  k_band_rec_vec<NS><<<nsys, 256, smem, st>>>(sys, Xd, xstride, Gc, buf, fwd ? 1 : 0);
 }
 
 void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,

@@ -463,13 +463,12 @@ static nsp_status setup_gamma_factor(nsp_ctx* c, const nsp_csr* A, const int32_t
     }
     nspk::tri_fb(c->d_gchunks + 1, P - 1, c->d_gspkF, 64, 32, true, false, c->stream, wb);   // S_k, k >= 1
     nspk::tri_fb(c->d_gchunks, P - 1, c->d_gspkB, 64, 32, false, true, c->stream, wb);       // T_k, k <= P-2
-    // one-column sweeps: X_II, X_II L_{I,I-1}, X_II^T, X_II^T L_{I+1,I}^T per tile row (k_band_rec_vec)
+    // reassociated sweeps: X_II L_{I,I-1}, X_II^T, X_II^T L_{I+1,I}^T per tile row (X_II: the band's own)
     const size_t tb = (size_t)nt * NSP_TILE_ELEMS * 8;
-    NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_gXF, tb));
     NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_gGF, tb));
     NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_gXB, tb));
     NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_gGB, tb));
-    nspk::band_prep(c->d_gband, nt, wb, c->d_gXF, c->d_gGF, c->d_gXB, c->d_gGB, c->stream);
+    nspk::band_prep(c->d_gband, nt, wb, nullptr, c->d_gGF, c->d_gXB, c->d_gGB, c->stream);
     NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     NSP_CUDA_TRY(c, cudaGetLastError());
     c->g_P = P;

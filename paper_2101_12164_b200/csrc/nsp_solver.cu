@@ -644,17 +644,17 @@ nsp_status ag_tri(nsp_ctx* c, const double* X, int ldx, bool x_gamma, double* Y,
     const int cw = vec ? 1 : 32, P = c->g_P;
     static const bool rec_off = getenv("NSP_BAND_NOREC") != nullptr;
     // the reassociated one-product-per-row chunk sweeps (k_band_rec_vec / k_band_rec)
-    const bool rec = c->d_gXF && !rec_off && (vec || ldw % 32 == 0);
+    const bool rec = c->d_gGF && !rec_off && (vec || ldw % 32 == 0);
     if (fwd) {
-      if (rec && vec) nspk::band_rec_vec(c->d_gchunks, P, c->d_gXF, c->d_gGF, buf, true, c->stream);
-      else if (rec) nspk::band_rec(c->d_gchunks, P, c->d_gXF, c->d_gGF, buf, ldw, true, c->stream);
+      if (rec && vec) nspk::band_rec_vec(c->d_gchunks, P, c->d_gband, c->g_wb + 1, c->d_gGF, buf, true, c->stream);
+      else if (rec) nspk::band_rec(c->d_gchunks, P, c->d_gband, c->g_wb + 1, c->d_gGF, buf, ldw, true, c->stream);
       else nspk::tri_fb(c->d_gchunks, P, buf, ldw, cw, true, false, c->stream, c->g_wb);
       nspk::spike_tail(c->d_gspkF, c->d_gchunk_first, P, buf, ldw, s, true, c->stream);
       nspk::spike_update(c->d_gspkF, c->d_gchunk_first, c->d_gtile_chunk, P, c->g_nt, buf, ldw, s, true, c->stream);
     }
     if (bwd) {
-      if (rec && vec) nspk::band_rec_vec(c->d_gchunks, P, c->d_gXB, c->d_gGB, buf, false, c->stream);
-      else if (rec) nspk::band_rec(c->d_gchunks, P, c->d_gXB, c->d_gGB, buf, ldw, false, c->stream);
+      if (rec && vec) nspk::band_rec_vec(c->d_gchunks, P, c->d_gXB, 1, c->d_gGB, buf, false, c->stream);
+      else if (rec) nspk::band_rec(c->d_gchunks, P, c->d_gXB, 1, c->d_gGB, buf, ldw, false, c->stream);
       else nspk::tri_fb(c->d_gchunks, P, buf, ldw, cw, false, true, c->stream, c->g_wb);
       nspk::spike_tail(c->d_gspkB, c->d_gchunk_first, P, buf, ldw, s, false, c->stream);
       nspk::spike_update(c->d_gspkB, c->d_gchunk_first, c->d_gtile_chunk, P, c->g_nt, buf, ldw, s, false, c->stream);
