@@ -1279,6 +1279,7 @@ template <int NS>
 __global__ void __launch_bounds__(256) k_band_rec_vec(const TriSys* __restrict__ sys, const double* __restrict__ Xd,
                                                       int64_t xstride, const double* __restrict__ Gc, double* buf,
                                                       int fwd) {
+  pdl_wait();
   extern __shared__ __align__(128) double sm[];
   double* Tr = sm;                 // NS x (Xd tile, Gc tile)
   double* Wr = sm + NS * 8192;     // NS x 64 rhs
@@ -1491,6 +1492,7 @@ __global__ void __launch_bounds__(256) k_spike_tail(const double* __restrict__ s
 __global__ void __launch_bounds__(256) k_spike_tail_vec(const double* __restrict__ spk,
                                                         const int* __restrict__ chunk_first, int P,
                                                         double* buf, int fwd) {
+  pdl_wait();
   extern __shared__ __align__(128) double sm[];   // 3 x 4096 spike tiles (ring)
   __shared__ double xs[2][64];                     // ping-pong: the coupling vector of the previous step
   __shared__ __align__(8) uint64_t bar[3];
@@ -1544,6 +1546,7 @@ __global__ void __launch_bounds__(256) k_spike_update_vec(const double* __restri
                                                           const int* __restrict__ chunk_first,
                                                           const int* __restrict__ tile_chunk, int P, double* buf,
                                                           int fwd) {
+  pdl_wait();
   const int I = blockIdx.x;
   const int k = tile_chunk[I];
   int src;
@@ -1595,6 +1598,7 @@ __global__ void __launch_bounds__(256) k_spike_update(const double* __restrict__
 // scatter: dst[idx[r]][c] = src[r][c]   (c < s, idx[r] >= 0)
 __global__ void k_gather_rows(const double* __restrict__ src, int lds, const int32_t* __restrict__ idx, int64_t rows,
                               double* dst, int ldd, int s, double scale) {
+  pdl_wait();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t r = e / ldd;
   const int c = (int)(e - r * ldd);
@@ -1604,6 +1608,7 @@ __global__ void k_gather_rows(const double* __restrict__ src, int lds, const int
 }
 __global__ void k_scatter_rows(const double* __restrict__ src, int lds, const int32_t* __restrict__ idx, int64_t rows,
                                double* dst, int ldd, int s, int accumulate) {
+  pdl_wait();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t r = e / s;
   const int c = (int)(e - r * s);
@@ -1706,7 +1711,7 @@ void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, int64_t xstride
     attr = true;
   }
   nsp_count_launch();
-  k_band_rec_vec<NS><<<nsys, 256, smem, st>>>(sys, Xd, xstride, Gc, buf, fwd ? 1 : 0);
+  launch_k(k_band_rec_vec<NS>, dim3(nsys), dim3(256), smem, st, sys, Xd, xstride, Gc, buf, fwd ? 1 : 0);
 }
 
 void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd, bool bwd, cudaStream_t st,
@@ -1776,7 +1781,7 @@ void spike_tail(const double* spk, const int* chunk_first, int P, double* buf, i
       cudaFuncSetAttribute(k_spike_tail_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4096 * 8);
       attr1 = true;
     }
-    { nsp_count_launch(); k_spike_tail_vec<<<1, 256, 3 * 4096 * 8, st>>>(spk, chunk_first, P, buf, fwd); }
+    { nsp_count_launch(); launch_k(k_spike_tail_vec, dim3(1), dim3(256), 3 * 4096 * 8, st, spk, chunk_first, P, buf, fwd); }
     return;
   }
   if (ldw % 32 == 0 && !getenv("NSP_SPIKE_OLD")) {
@@ -1796,7 +1801,7 @@ void spike_update(const double* spk, const int* chunk_first, const int* tile_chu
                   int ldw, int s, bool fwd, cudaStream_t st) {
   if (P <= 1) return;
   if (s == 1 && ldw == 1) {
-    { nsp_count_launch(); k_spike_update_vec<<<nt, 256, 0, st>>>(spk, chunk_first, tile_chunk, P, buf, fwd); }
+    { nsp_count_launch(); launch_k(k_spike_update_vec, dim3(nt), dim3(256), 0, st, spk, chunk_first, tile_chunk, P, buf, fwd); }
     return;
   }
   if (ldw % 32 == 0 && !getenv("NSP_SPIKE_OLD")) {
@@ -1818,14 +1823,14 @@ void gather_rows(const double* src, int lds, const int32_t* idx, int64_t rows, d
                  double scale, cudaStream_t st) {
   const int64_t tot = rows * ldd;
   if (tot <= 0) return;
-  { nsp_count_launch(); k_gather_rows<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, lds, idx, rows, dst, ldd, s, scale); }
+  { nsp_count_launch(); launch_k(k_gather_rows, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, src, lds, idx, rows, dst, ldd, s, scale); }
 }
 
 void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,
                   bool accumulate, cudaStream_t st) {
   const int64_t tot = rows * s;
   if (tot <= 0) return;
-  { nsp_count_launch(); k_scatter_rows<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, lds, idx, rows, dst, ldd, s, accumulate); }
+  { nsp_count_launch(); launch_k(k_scatter_rows, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, src, lds, idx, rows, dst, ldd, s, accumulate); }
 }
 
 void l22_inverse(const FacSub* subs, int nsub, int max_ntb, const double* dense, double* minv, cudaStream_t st) {

@@ -18,7 +18,11 @@
 #include <cstring>
 
 #include "nsp_blas.h"
+#include "nsp_dmma.cuh"
 #include "nsp_solver.h"
+
+using nspd::launch_k;
+using nspd::pdl_wait;
 
 namespace {
 
@@ -31,6 +35,7 @@ constexpr int PCG_CHUNK = 8;        // PCG iterations per host status check (one
 __global__ void __launch_bounds__(RT) k_dot2_partial(const double* __restrict__ a1, const double* __restrict__ b1,
                                                      const double* __restrict__ a2, const double* __restrict__ b2,
                                                      int64_t n, double* __restrict__ part) {
+  pdl_wait();
   __shared__ double red[2][RT];
   const int64_t r0 = (int64_t)blockIdx.x * RPB;
   double s1 = 0.0, s2 = 0.0;
@@ -61,6 +66,7 @@ __global__ void __launch_bounds__(RT) k_dot2_partial(const double* __restrict__ 
 __global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ part, int nblk, double* sc, int slot,
                                                    int mode, double tol, BcgStatus* st, double* hist,
                                                    int hist_mod) {
+  pdl_wait();
   __shared__ double red[RT];
   if (mode == 1 && st->done) return;   // read by every thread before thread 0 can write it
   double s = 0.0;
@@ -116,6 +122,7 @@ __global__ void __launch_bounds__(RT) k_pcg_xr_f(double* __restrict__ x, double*
                                                  int64_t n, double* sc, int cur,
                                                  const double* __restrict__ pq_part, int nblk,
                                                  double* __restrict__ part, BcgStatus* st) {
+  pdl_wait();
   __shared__ double red[RT];
   __shared__ double bc;
   if (st->done) return;
@@ -147,6 +154,7 @@ __global__ void __launch_bounds__(RT) k_pcg_xr_f(double* __restrict__ x, double*
 __global__ void __launch_bounds__(RT) k_pcg_p_f(double* __restrict__ p, const double* __restrict__ z, int64_t n,
                                                 double* sc, int cur, const double* __restrict__ rz_part, int nblk,
                                                 const BcgStatus* st) {
+  pdl_wait();
   __shared__ double bc;
   if (st->done) return;
   const double rz = cta_sum_partials(rz_part, nblk, &bc);
@@ -159,6 +167,7 @@ __global__ void __launch_bounds__(RT) k_pcg_p_f(double* __restrict__ p, const do
 // y[i*ldy] = a[i*lda] + alpha * b[i*ldb]
 __global__ void k_axpy_strided(double* y, int ldy, const double* a, int lda, const double* b, int ldb, double alpha,
                                int64_t n) {
+  pdl_wait();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) y[i * ldy] = fma(alpha, b[i * ldb], a[i * lda]);
 }
@@ -167,6 +176,7 @@ __global__ void k_axpy_strided(double* y, int ldy, const double* a, int lda, con
 __global__ void __launch_bounds__(256) k_gemvt_partial(const double* __restrict__ Z, int ldz,
                                                        const double* __restrict__ r, int64_t n, int rk,
                                                        double* __restrict__ part) {
+  pdl_wait();
   // chunk of GT_ROWS rows; warp w takes rows w, w + 8, ...; lane covers columns lane + 32 j (j < 4),
   // so every row read is one coalesced 1 KB line; the 8 warp partials are summed in fixed order
   __shared__ double red[8][128];
@@ -199,6 +209,7 @@ __global__ void __launch_bounds__(256) k_gemvt_partial(const double* __restrict_
 __global__ void __launch_bounds__(1024) k_gemvt_reduce(const double* __restrict__ part, int nchunks,
                                                        const double* __restrict__ sigma, int rk,
                                                        double* __restrict__ g) {
+  pdl_wait();
   __shared__ double red[8][128];
   const int k = threadIdx.x & 127, grp = threadIdx.x >> 7;
   double s = 0.0;
@@ -217,6 +228,7 @@ __global__ void __launch_bounds__(1024) k_gemvt_reduce(const double* __restrict_
 // y[row] += sum_k Z[row][k] g[k]   (warp per row, butterfly sum)
 __global__ void k_gemv_add(const double* __restrict__ Z, int ldz, const double* __restrict__ g, int rk, int64_t n,
                            double* __restrict__ y) {
+  pdl_wait();
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -292,9 +304,9 @@ size_t pcg_ws_bytes(const nsp_ctx* c) { return pcg_layout(c, nullptr, nullptr); 
 static void dot(nsp_ctx* c, const double* a, const double* b, int64_t n, PcgWs& w, int slot) {
   const unsigned nb = nblk_of(n);
   nsp_count_launch();
-  k_dot2_partial<<<nb, RT, 0, c->stream>>>(a, b, nullptr, nullptr, n, w.part);
+  launch_k(k_dot2_partial, dim3(nb), dim3(RT), 0, c->stream, a, b, nullptr, nullptr, n, w.part);
   nsp_count_launch();
-  k_dot_reduce<<<1, RT, 0, c->stream>>>(w.part, (int)nb, w.sc, slot, 0, 0.0, w.st, w.hist, PCG_CHUNK);
+  launch_k(k_dot_reduce, dim3(1), dim3(RT), 0, c->stream, w.part, (int)nb, w.sc, slot, 0, 0.0, w.st, w.hist, PCG_CHUNK);
 }
 
 // z = M r for the PCG preconditioner (0: identity copy, 1: A_G^{-1}, 2: M_2)
@@ -313,9 +325,9 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
     NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
     const unsigned nch = grid1(n, GT_ROWS);
     nsp_count_launch();
-    k_gemvt_partial<<<nch, 256, 0, c->side_stream>>>(c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart);
+    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->side_stream, c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart);
     nsp_count_launch();
-    k_gemvt_reduce<<<1, 1024, 0, c->side_stream>>>(w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
+    launch_k(k_gemvt_reduce, dim3(1), dim3(1024), 0, c->side_stream, w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
     NSP_CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side_stream));
   }
   nsp_status e = ag_solve(c, r, 1, z, 1, 1, w.agbuf);
@@ -323,7 +335,7 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
   if (fork2) {
     NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     nsp_count_launch();
-    k_gemv_add<<<grid1(n * 32, 256), 256, 0, c->stream>>>(c->d_Z, c->nys_ld, w.g, c->nys_rank, n, z);
+    launch_k(k_gemv_add, dim3(grid1(n * 32, 256)), dim3(256), 0, c->stream, c->d_Z, c->nys_ld, w.g, c->nys_rank, n, z);
     NSP_CUDA_TRY(c, cudaGetLastError());
     return NSP_OK;
   }
@@ -332,29 +344,29 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
     const int kp = c->nys_ld, rk = c->nys_rank;
     if ((e = apply_into(c, z, 1, w.t2, 1, 1, 1, w.apply_wvu)) != NSP_OK) return e;     // S_G A_G^{-1} r
     nsp_count_launch();
-    k_axpy_strided<<<grid1(n, 256), 256, 0, c->stream>>>(w.t2, 1, r, 1, w.t2, 1, -1.0, n);   // d = r - S t
+    launch_k(k_axpy_strided, dim3(grid1(n, 256)), dim3(256), 0, c->stream, w.t2, 1, r, 1, w.t2, 1, -1.0, n);   // d = r - S t
     const unsigned nch = grid1(n, GT_ROWS);
     nsp_count_launch();
-    k_gemvt_partial<<<nch, 256, 0, c->stream>>>(c->d_Z, kp, w.t2, n, rk, w.gpart);
+    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->stream, c->d_Z, kp, w.t2, n, rk, w.gpart);
     double* G = w.eg;                 // kp x kp, column 0 = Z^T d
     double* H = w.eg + 128 * 128;     // kp x kp, column 0 = E^{-1} Z^T d
     NSP_CUDA_TRY(c, cudaMemsetAsync(G, 0, (size_t)kp * kp * 8, c->stream));
     nsp_count_launch();
-    k_gemvt_reduce<<<1, 1024, 0, c->stream>>>(w.gpart, (int)nch, nullptr, rk, w.g);
+    launch_k(k_gemvt_reduce, dim3(1), dim3(1024), 0, c->stream, w.gpart, (int)nch, nullptr, rk, w.g);
     NSP_CUDA_TRY(c, cudaMemcpy2DAsync(G, kp * 8, w.g, 8, 8, rk, cudaMemcpyDeviceToDevice, c->stream));
     nspb::chol_solve(c->d_ELp, kp, G, kp, H, kp, 1.0, true, true, nullptr, c->stream);
     NSP_CUDA_TRY(c, cudaMemcpy2DAsync(w.g, 8, H, kp * 8, 8, rk, cudaMemcpyDeviceToDevice, c->stream));
     nsp_count_launch();
-    k_gemv_add<<<grid1(n * 32, 256), 256, 0, c->stream>>>(c->d_Z, kp, w.g, rk, n, z);
+    launch_k(k_gemv_add, dim3(grid1(n * 32, 256)), dim3(256), 0, c->stream, c->d_Z, kp, w.g, rk, n, z);
   }
   if (which == 2 && c->nys_rank > 0) {
     const unsigned nch = grid1(n, GT_ROWS);
     nsp_count_launch();
-    k_gemvt_partial<<<nch, 256, 0, c->stream>>>(c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart);
+    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->stream, c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart);
     nsp_count_launch();
-    k_gemvt_reduce<<<1, 1024, 0, c->stream>>>(w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
+    launch_k(k_gemvt_reduce, dim3(1), dim3(1024), 0, c->stream, w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
     nsp_count_launch();
-    k_gemv_add<<<grid1(n * 32, 256), 256, 0, c->stream>>>(c->d_Z, c->nys_ld, w.g, c->nys_rank, n, z);
+    launch_k(k_gemv_add, dim3(grid1(n * 32, 256)), dim3(256), 0, c->stream, c->d_Z, c->nys_ld, w.g, c->nys_rank, n, z);
   }
   NSP_CUDA_TRY(c, cudaGetLastError());
   return NSP_OK;
@@ -399,7 +411,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
   nspk::gather_rows(b, 1, c->d_g_src, n, w.f, 1, 1, 1.0, st);
   if (n > 0) {
     nsp_count_launch();
-    k_axpy_strided<<<grid1(n, 256), 256, 0, st>>>(w.f, 1, w.f, 1, w.tmp, 1, -1.0, n);
+    launch_k(k_axpy_strided, dim3(grid1(n, 256)), dim3(256), 0, st, w.f, 1, w.f, 1, w.tmp, 1, -1.0, n);
   }
   // ---- PCG on S_G w = f
   BcgStatus init{};
@@ -411,9 +423,9 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
   {
     const unsigned nb = nblk_of(n);
     nsp_count_launch();
-    k_dot2_partial<<<nb, RT, 0, st>>>(w.f, w.f, nullptr, nullptr, n, w.part);
+    launch_k(k_dot2_partial, dim3(nb), dim3(RT), 0, st, w.f, w.f, nullptr, nullptr, n, w.part);
     nsp_count_launch();
-    k_dot_reduce<<<1, RT, 0, st>>>(w.part, (int)nb, w.sc, 4, 2, tol, w.st, w.hist, PCG_CHUNK);
+    launch_k(k_dot_reduce, dim3(1), dim3(RT), 0, st, w.part, (int)nb, w.sc, 4, 2, tol, w.st, w.hist, PCG_CHUNK);
   }
   if ((e = read_st(c, w.st, hs)) != NSP_OK) return e;
   if (rep && rep->hist && rep->hist_cap > 0) rep->hist[0] = hs->relres;
@@ -436,17 +448,17 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
       const unsigned nb = nblk_of(n);
       // p.q partials; their sum is taken inside k_pcg_xr_f (every CTA, same order)
       nsp_count_launch();
-      k_dot2_partial<<<nb, RT, 0, q>>>(w.p, w.q, nullptr, nullptr, n, w.part);
+      launch_k(k_dot2_partial, dim3(nb), dim3(RT), 0, q, w.p, w.q, nullptr, nullptr, n, w.part);
       nsp_count_launch();
-      k_pcg_xr_f<<<nb, RT, 0, q>>>(w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, (int)nb, w.part2, w.st);
+      launch_k(k_pcg_xr_f, dim3(nb), dim3(RT), 0, q, w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, (int)nb, w.part2, w.st);
       nsp_count_launch();
-      k_dot_reduce<<<1, RT, 0, q>>>(w.part2, (int)nb, w.sc, 3, 1, tol, w.st, hist_dev, hist_mod);
+      launch_k(k_dot_reduce, dim3(1), dim3(RT), 0, q, w.part2, (int)nb, w.sc, 3, 1, tol, w.st, hist_dev, hist_mod);
       if ((e2 = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e2;
       // r.z partials; the sum (and beta) inside k_pcg_p_f
       nsp_count_launch();
-      k_dot2_partial<<<nb, RT, 0, q>>>(w.r, w.z, nullptr, nullptr, n, w.part);
+      launch_k(k_dot2_partial, dim3(nb), dim3(RT), 0, q, w.r, w.z, nullptr, nullptr, n, w.part);
       nsp_count_launch();
-      k_pcg_p_f<<<grid1(n, RT), RT, 0, q>>>(w.p, w.z, n, w.sc, cur, w.part, (int)nb, w.st);
+      launch_k(k_pcg_p_f, dim3(grid1(n, RT)), dim3(RT), 0, q, w.p, w.z, n, w.sc, cur, w.part, (int)nb, w.st);
       cur ^= 1;
       return NSP_OK;
     };
@@ -619,7 +631,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
   nspk::spmm(c->A2G, w.w, 1, nullptr, 0, 0, w.tmpB, 32, 1, 0, true, st);            // A_IG w (B rows)
   if (c->wvu_rows > 0) {
     nsp_count_launch();
-    k_axpy_strided<<<grid1(c->wvu_rows, 256), 256, 0, st>>>(w.bB, 32, w.bB, 32, w.tmpB, 32, -1.0, c->wvu_rows);
+    launch_k(k_axpy_strided, dim3(grid1(c->wvu_rows, 256)), dim3(256), 0, st, w.bB, 32, w.bB, 32, w.tmpB, 32, -1.0, c->wvu_rows);
   }
   if ((e = interior_boundary_solve(c, w)) != NSP_OK) return e;                       // y_B in wvu
   nspk::spmm(c->C1, w.i1r, 32, w.wvu, 32, c->i1_rows, w.i1buf, 32, 1, 1, true, st); // r_1 - A_1B y_B
