@@ -461,6 +461,7 @@ __global__ void k_colsq_converge(const double* __restrict__ part, int ntiles, in
 }
 
 __global__ void k_sqrt_vec(const double* in, double* out, int n) {
+  pdl_wait();
   const int i = threadIdx.x + blockIdx.x * blockDim.x;
   if (i < n) out[i] = sqrt(in[i]);
 }
@@ -908,6 +909,7 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
 // C = alpha * op(A) op(B) + beta * C, all sp-ish small (m x n, inner k), row-major, FMA.
 __global__ void k_small_gemm(int m, int n, int k, double alpha, const double* A, int lda, int ta, const double* B,
                              int ldb, int tb, double beta, double* Cm, int ldc) {
+  pdl_wait();
   const int i = blockIdx.y * 16 + threadIdx.y;
   const int j = blockIdx.x * 16 + threadIdx.x;
   if (i >= m || j >= n) return;
@@ -931,6 +933,7 @@ __global__ void k_small_sym(double* A, int n, int ld, double shift) {
 // M[i][k] = V[i][k] * colscale[k] for k < r, 0 for k >= r (n rows, ld)
 __global__ void k_scale_cols(const double* V, int ldv, const double* colscale, int r, int n, int ncols, double* M,
                              int ldm, int mode) {
+  pdl_wait();
   const int i = blockIdx.y * 16 + threadIdx.y, k = blockIdx.x * 16 + threadIdx.x;
   if (i >= n || k >= ncols) return;
   double v = 0.0;
@@ -943,6 +946,7 @@ __global__ void k_scale_cols(const double* V, int ldv, const double* colscale, i
 
 // rows i < r scaled by d[i], rows r <= i < nrows zeroed
 __global__ void k_scale_rows(double* G, int ld, const double* d, int r, int nrows, int ncols) {
+  pdl_wait();
   const int i = blockIdx.y * 16 + threadIdx.y, j = blockIdx.x * 16 + threadIdx.x;
   if (i >= nrows || j >= ncols) return;
   G[i * ld + j] = i < r ? G[i * ld + j] * d[i] : 0.0;
@@ -953,6 +957,7 @@ __global__ void k_scale_rows(double* G, int ld, const double* d, int r, int nrow
 __global__ void k_cheb_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ d,
                               const double* __restrict__ t, double* __restrict__ dn, double c1, double c2, int64_t n,
                               int want_d) {
+  pdl_wait();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double di = d[i];
@@ -963,6 +968,7 @@ __global__ void k_cheb_update(double* __restrict__ x, double* __restrict__ r, co
 }
 
 __global__ void k_copy_pad(const double* src, int lds, double* dst, int ldd, int64_t n, int s, double scale) {
+  pdl_wait();
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t r = idx / ldd;
   const int c = (int)(idx - r * ldd);
@@ -1075,7 +1081,7 @@ void colsq_reduce(const double* part, int ntiles, int ldp, double* out, cudaStre
 }
 
 void sqrt_vec(const double* in, double* out, int n, cudaStream_t st) {
-  { nsp_count_launch(); k_sqrt_vec<<<(n + 255) / 256, 256, 0, st>>>(in, out, n); }
+  { nsp_count_launch(); launch_k(k_sqrt_vec, dim3((n + 255) / 256), dim3(256), 0, st, in, out, n); }
 }
 
 void colsq_converge(const double* part, int ntiles, int ldp, double* rsq, const double* bnorm, int s, double tol,
@@ -1109,24 +1115,24 @@ void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* 
 void small_gemm(int m, int n, int k, double alpha, const double* A, int lda, bool ta, const double* B, int ldb,
                 bool tb, double beta, double* C, int ldc, cudaStream_t st) {
   dim3 grid((n + 15) / 16, (m + 15) / 16);
-  { nsp_count_launch(); k_small_gemm<<<grid, dim3(16, 16), 0, st>>>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc); }
+  { nsp_count_launch(); launch_k(k_small_gemm, dim3(grid), dim3(dim3(16, 16)), 0, st, m, n, k, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc); }
 }
 
 void cheb_update(double* x, double* r, const double* d, const double* t, double* dn, double c1, double c2, int64_t n,
                  bool want_d, cudaStream_t st) {
   if (n <= 0) return;
-  { nsp_count_launch(); k_cheb_update<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, r, d, t, dn, c1, c2, n, want_d ? 1 : 0); }
+  { nsp_count_launch(); launch_k(k_cheb_update, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, x, r, d, t, dn, c1, c2, n, want_d ? 1 : 0); }
 }
 
 void copy_pad(const double* src, int lds, double* dst, int ldd, int64_t n, int s, double scale, cudaStream_t st) {
   const int64_t tot = n * ldd;
   if (tot <= 0) return;
-  { nsp_count_launch(); k_copy_pad<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, lds, dst, ldd, n, s, scale); }
+  { nsp_count_launch(); launch_k(k_copy_pad, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, src, lds, dst, ldd, n, s, scale); }
 }
 
 void scale_rows(double* G, int ld, const double* d, int r, int nrows, int ncols, cudaStream_t st) {
   dim3 grid((ncols + 15) / 16, (nrows + 15) / 16);
-  { nsp_count_launch(); k_scale_rows<<<grid, dim3(16, 16), 0, st>>>(G, ld, d, r, nrows, ncols); }
+  { nsp_count_launch(); launch_k(k_scale_rows, dim3(grid), dim3(dim3(16, 16)), 0, st, G, ld, d, r, nrows, ncols); }
 }
 
 void small_sym(double* A, int n, int ld, double shift, cudaStream_t st) {
@@ -1137,7 +1143,7 @@ void small_sym(double* A, int n, int ld, double shift, cudaStream_t st) {
 void scale_cols(const double* V, int ldv, const double* colscale, int r, int n, int ncols, double* M, int ldm,
                 int mode, cudaStream_t st) {
   dim3 grid((ncols + 15) / 16, (n + 15) / 16);
-  { nsp_count_launch(); k_scale_cols<<<grid, dim3(16, 16), 0, st>>>(V, ldv, colscale, r, n, ncols, M, ldm, mode); }
+  { nsp_count_launch(); launch_k(k_scale_cols, dim3(grid), dim3(dim3(16, 16)), 0, st, V, ldv, colscale, r, n, ncols, M, ldm, mode); }
 }
 
 }  // namespace nspb

@@ -22,6 +22,7 @@ __global__ void k_scatter(double* base, const int64_t* idx, const double* val, i
 }
 
 __global__ void k_pad_identity(double* base, const int64_t* tile_idx, const int* first_row, int cnt) {
+  pdl_wait();
   int t = blockIdx.x;
   if (t >= cnt) return;
   double* T = base + tile_idx[t] * NSP_TILE_ELEMS;
@@ -1348,6 +1349,7 @@ template <int CW>
 __global__ void __launch_bounds__(256) k_band_rec(const TriSys* __restrict__ sys, const double* __restrict__ Xd,
                                                   int64_t xstride, const double* __restrict__ Gc, double* buf, int ldw,
                                                   int fwd) {
+  pdl_wait();
   constexpr int NF = CW / 16;
   constexpr int LDV = CW + 4;
   extern __shared__ double sm[];
@@ -1630,7 +1632,7 @@ void scatter(double* base, const int64_t* idx, const double* val, int64_t cnt, c
 
 void set_pad_identity(double* base, const int64_t* tile_idx, const int* first_row, int cnt, cudaStream_t st) {
   if (cnt <= 0) return;
-  { nsp_count_launch(); k_pad_identity<<<cnt, 64, 0, st>>>(base, tile_idx, first_row, cnt); }
+  { nsp_count_launch(); launch_k(k_pad_identity, dim3(cnt), dim3(64), 0, st, base, tile_idx, first_row, cnt); }
 }
 
 void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, double* scratch,
@@ -1687,7 +1689,7 @@ void band_rec(const TriSys* sys, int nsys, const double* Xd, int64_t xstride, co
       attr16 = true;
     }
     nsp_count_launch();
-    k_band_rec<16><<<dim3(nsys, ldw / 16), 256, smem, st>>>(sys, Xd, xstride, Gc, buf, ldw, fwd ? 1 : 0);
+    launch_k(k_band_rec<16>, dim3(dim3(nsys, ldw / 16)), dim3(256), smem, st, sys, Xd, xstride, Gc, buf, ldw, fwd ? 1 : 0);
     return;
   }
   const size_t smem = (4 * 64 * LDT + 4 * 64 * 36) * sizeof(double);
@@ -1697,7 +1699,7 @@ void band_rec(const TriSys* sys, int nsys, const double* Xd, int64_t xstride, co
     attr = true;
   }
   nsp_count_launch();
-  k_band_rec<32><<<dim3(nsys, ldw / 32), 256, smem, st>>>(sys, Xd, xstride, Gc, buf, ldw, fwd ? 1 : 0);
+  launch_k(k_band_rec<32>, dim3(dim3(nsys, ldw / 32)), dim3(256), smem, st, sys, Xd, xstride, Gc, buf, ldw, fwd ? 1 : 0);
 }
 
 void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, int64_t xstride, const double* Gc, double* buf, bool fwd,
