@@ -581,12 +581,15 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
   constexpr int STAGE = NSP_MINV_TILE + 64 * LDV;   // one (M tile, W tile) pair
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar[2];
-  const int2 it = items[blockIdx.x];
+  // CM: grid (chunks, items) - the chunk CTAs of one item are adjacent in launch order, so they read
+  // each S_j^{-1} tile from L2 within the same wave
+  const int bx = CM ? blockIdx.y : blockIdx.x, by = CM ? blockIdx.x : blockIdx.y;
+  const int2 it = items[bx];
   const FacSub sb = subs[it.x];
   const int I = it.y, ntb = sb.ntb;
-  const int c0 = blockIdx.y * CW;
+  const int c0 = by * CW;
   const double* Mb = minv + sb.dense_off * NSP_MINV_TILE;
-  const double* Wb = CM ? W + blockIdx.y * cs + sb.wvu_row * (int64_t)LDV : W + sb.wvu_row * (int64_t)ldw + c0;
+  const double* Wb = CM ? W + by * cs + sb.wvu_row * (int64_t)LDV : W + sb.wvu_row * (int64_t)ldw + c0;
   auto mt = [&](int J) {   // stored tile holding block (I, J) (transposed when J > I)
     return J <= I ? Mb + ((int64_t)I * (I + 1) / 2 + J) * NSP_MINV_TILE
                   : Mb + ((int64_t)J * (J + 1) / 2 + I) * NSP_MINV_TILE;
@@ -628,7 +631,7 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
     if (J <= I) cta_mma<NF, false, false>(Ms, NSP_MINV_LD, Ms + NSP_MINV_TILE, LDV, acc);
     else cta_mma<NF, true, false>(Ms, NSP_MINV_LD, Ms + NSP_MINV_TILE, LDV, acc);
   }
-  double* out = CM ? U + blockIdx.y * cs + (sb.wvu_row + (int64_t)I * 64) * LDV
+  double* out = CM ? U + by * cs + (sb.wvu_row + (int64_t)I * 64) * LDV
                    : U + (sb.wvu_row + (int64_t)I * 64) * ldw + c0;
   const int ldo = CM ? LDV : ldw;
 #pragma unroll
@@ -1851,7 +1854,7 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
   // 112.6 us (TMA M + W, 29.2 TFLOP/s); 64-wide / 3-stage / half-tile variants are slower.
   const size_t smem = 2 * (NSP_MINV_TILE + 64 * (cw + 4)) * sizeof(double);
   if (cm_stride > 0) {   // ldw = the logical padded width (a multiple of 32), one CTA column per chunk
-    const dim3 grid(nitems, ldw / 32);
+    const dim3 grid(ldw / 32, nitems);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_symm<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
