@@ -280,12 +280,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t
     const int64_t rp = r0 + (int64_t)(q / PSPP) * 64;
     cp_block_zf(Ar + (q % PNS) * 64 * PLDA, PLDA, In + rp * pa.ldi + (q % PSPP) * PKC, pa.ldi, 64, PKC, r1 - rp);
   };
-  cp_block(Ms, PLDM, pa.M, pa.ldm, 128, 128);
-#pragma unroll
-  for (int q = 0; q < PNS - 1; ++q) {
-    if (q < nsteps) issue(q);
-    cp_commit();
-  }
+  // M rows [0, PKC) travel with the first chunk; the rest in a group of their own, waited for one step
+  // later (PNS == 2: the first product does not wait for the whole 128 KB multiplier)
+  static_assert(PNS == 2, "prologue assumes a 2-stage ring");
+  cp_block(Ms, PLDM, pa.M, pa.ldm, PKC, 128);
+  if (nsteps > 0) issue(0);
+  cp_commit();
+  cp_block(Ms + PKC * PLDM, PLDM, pa.M + (int64_t)PKC * pa.ldm, pa.ldm, 128 - PKC, 128);
+  cp_commit();
   double acc[2][NF][2];
   acc_zero(acc);
   double sq[NF][2];
@@ -306,7 +308,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t
                                          : make_double2(0.0, 0.0);
         }
     }
-    cp_wait<PNS - 2>();
+    if (q == 0) cp_wait<1>();   // chunk 0 and M's first rows (the rest of M may still be in flight)
+    else cp_wait<0>();
     __syncthreads();
     if (q + PNS - 1 < nsteps) issue(q + PNS - 1);
     cp_commit();
