@@ -326,7 +326,11 @@ __global__ void __launch_bounds__(256) k_chol16(const double* __restrict__ Ain, 
 // in smem; per 16-row block: x_kb <- X_kk x_kb (16 x 16 x 8 product, 2 DMMA m-fragments), then
 // the remaining rows x_i -= L_i,kb x_kb on the DMMA pipe (8-row fragments over the 4 warps).
 // gate (optional): skip when *gate != 0.
-__global__ void __launch_bounds__(128) k_chol_solve(const double* __restrict__ Lp, int sp,
+#ifndef NSP_CS_T
+#define NSP_CS_T 256
+#endif
+constexpr int CS_T = NSP_CS_T;   // threads per k_chol_solve CTA (8 warps: the rows-below updates in 2 rounds)
+__global__ void __launch_bounds__(CS_T) k_chol_solve(const double* __restrict__ Lp, int sp,
                                                     const double* __restrict__ B, int ldb, double* __restrict__ Out,
                                                     int ldo, double sgn, int fwd, int bwd, const int* gate) {
   pdl_wait();
@@ -347,12 +351,12 @@ __global__ void __launch_bounds__(128) k_chol_solve(const double* __restrict__ L
     fence_mbar_init();
   }
   __syncthreads();
-  for (int i = tid; i < sp; i += 128) {
+  for (int i = tid; i < sp; i += CS_T) {
     const int w = 16 * ((i >> 4) + 1);
     mbar_expect_copy(&lbar, Ls + i * LD, Lp + (int64_t)i * sp, 8u * w);
     for (int j = w; j < sp; ++j) Ls[i * LD + j] = 0.0;
   }
-  for (int e = tid; e < sp * 8; e += 128) {
+  for (int e = tid; e < sp * 8; e += CS_T) {
     const int i = e >> 3, c = e & 7;
     x[i * LX + c] = B ? B[(int64_t)i * ldb + c0 + c] : (i == c0 + c ? 1.0 : 0.0);
   }
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(128) k_chol_solve(const double* __restrict__ L
       }
       __syncthreads();
       // x_i -= L_i,kb x_kb for the rows below, 8-row groups
-      for (int grp = warp; grp < (sp - b0 - 16) / 8; grp += 4) {
+      for (int grp = warp; grp < (sp - b0 - 16) / 8; grp += CS_T / 32) {
         const int row0 = b0 + 16 + 8 * grp;
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll
@@ -404,7 +408,7 @@ __global__ void __launch_bounds__(128) k_chol_solve(const double* __restrict__ L
       }
       __syncthreads();
       // x_i -= L_kb,i^T x_kb for the rows above
-      for (int grp = warp; grp < b0 / 8; grp += 4) {
+      for (int grp = warp; grp < b0 / 8; grp += CS_T / 32) {
         const int row0 = 8 * grp;
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(128) k_chol_solve(const double* __restrict__ L
       }
       __syncthreads();
     }
-  for (int e = tid; e < sp * 8; e += 128) {
+  for (int e = tid; e < sp * 8; e += CS_T) {
     const int i = e >> 3, cc = e & 7;
     Out[(int64_t)i * ldo + c0 + cc] = sgn * x[i * LX + cc];
   }
@@ -447,7 +451,7 @@ void chol_solve(const double* Lp, int sp, const double* B, int ldb, double* Out,
     attr = true;
   }
   nsp_count_launch();
-  launch_k(k_chol_solve, dim3(sp / 8), dim3(128), smem, st, Lp, sp, B, ldb, Out, ldo, sgn, fwd, bwd, gate);
+  launch_k(k_chol_solve, dim3(sp / 8), dim3(CS_T), smem, st, Lp, sp, B, ldb, Out, ldo, sgn, fwd, bwd, gate);
 }
 
 }  // namespace nspb
