@@ -15,10 +15,10 @@ using namespace nspd;
 #define NSP_GR 32
 #endif
 #ifndef NSP_GNS
-#define NSP_GNS 4
+#define NSP_GNS 3
 #endif
 #ifndef NSP_GCTAS
-#define NSP_GCTAS 148
+#define NSP_GCTAS 296
 #endif
 namespace {
 
