@@ -18,9 +18,11 @@
  *    Gamma rows ordered as nsp_gamma_index() reports (single rank: ascending
  *    original node id, reading C10).
  *  - All work is enqueued on opts.stream (a cudaStream_t, may be NULL = legacy
- *    default stream).  nsp_schur_apply / nsp_kgamma_apply are asynchronous; the
- *    solvers synchronise the stream once per iteration (a small status read)
- *    and at exit.
+ *    default stream).  nsp_schur_apply / nsp_kgamma_apply are asynchronous.  The
+ *    single-rank solvers run their iterations as ONE device-driven CUDA graph
+ *    (a WHILE node with the stop test on the device) and synchronise the
+ *    stream once per solve; the multi-rank block CG reads a small status
+ *    block once per iteration.  All solvers synchronise at exit.
  *  - ws: optional caller-owned device workspace of nsp_workspace_bytes(s)
  *    bytes; NULL makes the context allocate (and keep) its own.
  *  - Errors: every call returns an nsp_status; on a negative status
@@ -218,6 +220,45 @@ nsp_status nsp_precond_apply(nsp_ctx* ctx, int which, const double* X, double* Y
  * Returns NSP_ERR_STATE for 2 / 3 before nsp_nystrom. */
 nsp_status nsp_pcg(nsp_ctx* ctx, const double* b, double* x, double tol, int maxit, int precond,
                    void* ws, nsp_report* rep);
+
+/* Switch the block-CG preconditioner of an existing context (opts.bcg_precond, reading C2):
+ * 0 = none (M = I), 1 = A_G^{-1} (needs the A_G factor / Chebyshev operator: opts.factor_gamma at
+ * setup, else NSP_ERR_STATE).  The workspace size (nsp_workspace_bytes) does not depend on it. */
+nsp_status nsp_set_bcg_precond(nsp_ctx* ctx, int precond);
+
+/* ---- evidence and kernel-level testing ----
+ * Dispatch-path counters: how many times each shape-specialised path was DISPATCHED in this process
+ * (an eager launch or a capture into a CUDA graph that is then replayed).  Tests read deltas to
+ * assert that the bench's code path (e.g. the one-wave s = 128 panel, the symmetric Gram) is the
+ * one their oracle comparison exercised.  out: host long long[n]; returns NSP_PATH_COUNT. */
+enum {
+  NSP_PATH_PANEL_ROWS = 0,   /* k_panel_rows: s = 128 one-wave row-range panel (n >= 64 x SMs) */
+  NSP_PATH_PANEL_TILES = 1,  /* k_panel: 64 x 64 tile panel (any s, any n) */
+  NSP_PATH_GRAM_SYM = 2,     /* Gram X^T X computing only the tiles on / above the diagonal */
+  NSP_PATH_GRAM_DE = 3,      /* [D | E] = P^T [Q | R] with D's upper tiles mirrored */
+  NSP_PATH_GRAM_FULL = 4,    /* Gram with every output tile computed */
+  NSP_PATH_SYMM = 5,         /* a2+a3 as the symmetric S_j^{-1} product (k_symm) */
+  NSP_PATH_SWEEPS = 6,       /* a2+a3 as two batched triangular sweeps (k_trsm_fb) */
+  NSP_PATH_SYMV = 7,         /* a2+a3 for one column (k_symv1) */
+  NSP_PATH_PANEL_GRAM = 8,   /* fused panel + Gram partial (R -= Q alpha with Q^T R; W = R + P beta with W^T W) */
+  NSP_PATH_CHOL_SOLVE = 9,   /* fused s x s Cholesky + triangular solve (one launch) */
+  NSP_PATH_COUNT = 16
+};
+int nsp_path_counters(long long* out, int n);
+
+/* Kernel-level test entry points for the block-CG building blocks (rows a6, a8, a10, a11) on caller
+ * device data, stream-ordered on `stream` (cudaStream_t), synchronous on return.  Blocks are n x s
+ * row-major with ld = s, s in {64, 128}.  path: 0 = the production dispatch, 1 = the generic
+ * kernels (64 x 64 tile panel, full-tile Gram).
+ *  nsp_dev_panel: Out = Cin + sgn * In M (M s x s; Cin may be NULL = 0, may alias Out);
+ *                 colsq (nullable, device double[s]) = column sums of squares of Out in the kernel's
+ *                 fixed reduction order.
+ *  nsp_dev_gram:  out = Xa^T Xb (s x s); with Xb2 != NULL also out2 = Xa^T Xb2; lower_first: out is
+ *                 only read through its lower triangle (D of [D | E]). */
+nsp_status nsp_dev_panel(double* Out, const double* Cin, const double* In, const double* M, int64_t n, int s,
+                         double sgn, double* colsq, int path, void* stream);
+nsp_status nsp_dev_gram(const double* Xa, const double* Xb, const double* Xb2, int64_t n, int s, double* out,
+                        double* out2, int lower_first, int path, void* stream);
 
 const char* nsp_last_error(const nsp_ctx* ctx);
 /* Number of device kernels this library has launched in the process (evidence counter). */

@@ -14,7 +14,7 @@ itself (closed forms, brute-force elimination, exact-arithmetic termination,
 exactness) except where a docstring says "parity unpinned".
 """
 from .dbbd import DBBD, dbbd  # noqa: F401
-from .schur import SchurOracle  # noqa: F401
+from .schur import LocalSchurOracle, SchurOracle  # noqa: F401
 from .bcg import bf_bcg, orth  # noqa: F401
 from .nystrom import nystrom_schur, nystrom_m1, NystromResult  # noqa: F401
 from .pcg import pcg, solve_full_system  # noqa: F401

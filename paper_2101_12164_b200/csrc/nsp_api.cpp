@@ -7,14 +7,26 @@
 #include "nsp_comm.h"
 #include "nsp_internal.h"
 #include "nsp_solver.h"
+#include "nsp_blas.h"
 
 namespace nspi {
+
+static int device_sms(int dev) {   // SM count per device (cached)
+  static int cache[64] = {0};
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
 
 int pick_cw(const nsp_ctx* c, int s) {
   const int tiles64 = (s + 63) / 64;
   if (const char* e = getenv("NSP_CW")) return atoi(e) == 64 && s > 32 ? 64 : 32;   // tuning override
   if (c->d_minv) return 32;   // k_symm: 32-wide chunks run 2 CTAs/SM (faster at every measured shape)
-  return (s > 32 && (int64_t)c->nsub * tiles64 >= 2 * 148) ? 64 : 32;
+  return (s > 32 && (int64_t)c->nsub * tiles64 >= 2 * device_sms(c->device)) ? 64 : 32;
 }
 
 int ld_pad(int s, int cw) { return ((s + cw - 1) / cw) * cw; }
@@ -69,12 +81,15 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
     if (s == 1) {   // one right-hand side (outer PCG): memory-bound matrix-vector form, tiles read once
       double* P = U + c->wvu_rows * (int64_t)ldw;
       P = (double*)(((uintptr_t)P + 255) & ~(uintptr_t)255);
+      nsp_count_path(NSP_PATH_SYMV);
       if (getenv("NSP_SYMV2")) nspk::symv(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, c->stream);
       else nspk::symv1(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, P, c->stream);
     } else {
+      nsp_count_path(NSP_PATH_SYMM);
       nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream, cs);
     }
   } else {
+    nsp_count_path(NSP_PATH_SWEEPS);
     nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, wvu, ldw, cw, c->stream);
   }
   if (gprof) {
@@ -220,6 +235,57 @@ nsp_status nsp_gamma_apply(nsp_ctx* c, const double* X, double* Y, int s) {
   return finish_shared_rows(c, X, s, Y, s, s, true);
 }
 
+nsp_status nsp_set_bcg_precond(nsp_ctx* c, int precond) {
+  if (!c || precond < 0 || precond > 1) return NSP_ERR_ARG;
+  if (precond == 1 && !c->has_ag) {
+    c->err = "nsp_set_bcg_precond: M = A_G^{-1} needs the A_G operator (opts.factor_gamma at setup)";
+    return NSP_ERR_STATE;
+  }
+  c->opts.bcg_precond = precond;   // the cached iteration graphs are keyed on it (rebuilt on change)
+  return NSP_OK;
+}
+
+nsp_status nsp_dev_panel(double* Out, const double* Cin, const double* In, const double* M, int64_t n, int s,
+                         double sgn, double* colsq, int path, void* stream) {
+  if (n < 0 || (s != 64 && s != 128) || path < 0 || path > 1) return NSP_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) {   // empty block: nothing to update, zero column sums
+    if (colsq && cudaMemsetAsync(colsq, 0, (size_t)s * 8, st) != cudaSuccess) return NSP_ERR_CUDA;
+    return cudaStreamSynchronize(st) == cudaSuccess ? NSP_OK : NSP_ERR_CUDA;
+  }
+  if (!Out || !In || !M) return NSP_ERR_ARG;
+  double* part = nullptr;
+  if (colsq && cudaMalloc(&part, (size_t)(std::max<int64_t>((n + 63) / 64, 1024) + 1) * s * 8) != cudaSuccess)
+    return NSP_ERR_CUDA;
+  nsp_force_generic = path;
+  const int npt = nspb::panel(Out, s, Cin, s, In, s, M, s, s, s, n, sgn, part, st);
+  nsp_force_generic = 0;
+  if (colsq) nspb::colsq_reduce(part, npt, s, colsq, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (part) cudaFree(part);
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NSP_OK : NSP_ERR_CUDA;
+}
+
+nsp_status nsp_dev_gram(const double* Xa, const double* Xb, const double* Xb2, int64_t n, int s, double* out,
+                        double* out2, int lower_first, int path, void* stream) {
+  if (!out || (Xb2 && !out2) || n < 0 || (s != 64 && s != 128) || path < 0 || path > 1) return NSP_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) {   // empty contraction: zero Gram
+    if (cudaMemsetAsync(out, 0, (size_t)s * s * 8, st) != cudaSuccess) return NSP_ERR_CUDA;
+    if (out2 && cudaMemsetAsync(out2, 0, (size_t)s * s * 8, st) != cudaSuccess) return NSP_ERR_CUDA;
+    return cudaStreamSynchronize(st) == cudaSuccess ? NSP_OK : NSP_ERR_CUDA;
+  }
+  if (!Xa || !Xb) return NSP_ERR_ARG;
+  double* ws = nullptr;
+  if (cudaMalloc(&ws, nspb::gram_ws_doubles(n, s, s) * 8) != cudaSuccess) return NSP_ERR_CUDA;
+  nsp_force_generic = path;
+  nspb::gram2(Xa, s, s, Xb, Xb2, s, s, n, out, out2, s, ws, st, lower_first != 0);
+  nsp_force_generic = 0;
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(ws);
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NSP_OK : NSP_ERR_CUDA;
+}
+
 const char* nsp_last_error(const nsp_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 void nsp_destroy(nsp_ctx* c) {
@@ -283,6 +349,16 @@ void nsp_destroy(nsp_ctx* c) {
 
 #include <atomic>
 static std::atomic<long long> g_launches{0};
+static std::atomic<long long> g_path[NSP_PATH_COUNT];
+thread_local int nsp_force_generic = 0;
+void nsp_count_path(int id) {
+  if (id >= 0 && id < NSP_PATH_COUNT) g_path[id].fetch_add(1, std::memory_order_relaxed);
+}
+extern "C" int nsp_path_counters(long long* out, int n) {
+  if (!out) return NSP_PATH_COUNT;
+  for (int i = 0; i < n && i < NSP_PATH_COUNT; ++i) out[i] = g_path[i].load();
+  return NSP_PATH_COUNT;
+}
 void nsp_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void nsp_count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 long long nsp_launch_count() { return g_launches.load(); }

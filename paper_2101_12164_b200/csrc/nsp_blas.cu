@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include "nsp_blas.h"
+#include "../../include/nsp.h"
 #include "nsp_dmma.cuh"
 
 using namespace nspd;
@@ -17,8 +18,8 @@ using namespace nspd;
 #ifndef NSP_GNS
 #define NSP_GNS 3
 #endif
-#ifndef NSP_GCTAS
-#define NSP_GCTAS 296
+#ifndef NSP_GCTAS_PER_SM
+#define NSP_GCTAS_PER_SM 2
 #endif
 namespace {
 
@@ -46,7 +47,7 @@ constexpr int LDS = 68;    // smem stride for 64-wide tiles
 
 // part[(chunk * ntm * ntn + tm * ntn + tn) * 4096 + i * 64 + j]
 //   = sum_{r in chunk} Xa[r][64 tm + i] * Xb[r][64 tn + j]
-// One wave of CTAs (tiles x chunks <= 148, one per SM), each streaming its contiguous row chunk
+// One wave of CTAs (tiles x chunks <= 2 x SMs, two per SM), each streaming its contiguous row chunk
 // through a GNS-stage cp.async ring of 32-row slabs (one barrier per slab), so the slab loads are
 // in flight GNS-1 slabs ahead of the DMMA work.
 constexpr int GNS = NSP_GNS;
@@ -983,23 +984,21 @@ __global__ void k_copy_pad(const double* src, int lds, double* dst, int ldd, int
 
 namespace nspb {
 
-static void set_smem(const void* f, size_t bytes) {
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-}
+static int gram_ctas() { return NSP_GCTAS_PER_SM * num_sms(); }   // Gram CTAs: two resident per SM
 
-int gram_chunks(int64_t n, int ntiles) {   // one wave: tiles x chunks <= 148 CTAs (1 per SM)
+int gram_chunks(int64_t n, int ntiles) {   // one wave: tiles x chunks <= NSP_GCTAS_PER_SM x SMs CTAs
   int64_t ch = (n + GR - 1) / GR;
-  const int64_t cap = NSP_GCTAS / ntiles;
+  const int64_t cap = gram_ctas() / ntiles;
   if (ch > cap) ch = cap;
   return (int)(ch < 1 ? 1 : ch);
 }
 
 size_t gram_ws_doubles(int64_t n, int sa, int sb) {
-  // every launch uses chunks x tiles <= max(NSP_GCTAS, tiles) partial tiles (the symmetric Gram has
+  // every launch uses chunks x tiles <= max(gram_ctas(), tiles) partial tiles (the symmetric Gram has
   // fewer tiles and so more chunks than the two-operand one)
   const int ntm = (sa + 63) / 64, ntn = 2 * ((sb + 63) / 64);
   (void)n;
-  return (size_t)std::max(NSP_GCTAS, ntm * ntn) * 4096;
+  return (size_t)std::max(gram_ctas(), ntm * ntn) * 4096;
 }
 
 void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb2, int ldb, int sb, int64_t n,
@@ -1007,20 +1006,18 @@ void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb
   const int ntm = (sa + 63) / 64, ntn1 = (sb + 63) / 64;
   const int ntn = Xb2 ? 2 * ntn1 : ntn1;
   // Xa == Xb (W^T W, Y^T Y): only the tiles on and above the diagonal (3 of 4 at s = 128)
-  static const bool sym_off = getenv("NSP_GRAM_NOSYM") != nullptr;
+  static const bool sym_env_off = getenv("NSP_GRAM_NOSYM") != nullptr;
+  const bool sym_off = sym_env_off || nsp_force_generic;
   int sym = (!sym_off && !Xb2 && Xa == Xb && lda == ldb && sa == sb && ntm > 1) ? 1 : 0;
   // [D | E] with D read only through its lower triangle: D's upper tiles are mirrored, not computed
   if (!sym_off && lower_first && Xb2 && ntn1 == ntm && ntm > 1) sym = 2;
+  nsp_count_path(sym == 1 ? NSP_PATH_GRAM_SYM : sym == 2 ? NSP_PATH_GRAM_DE : NSP_PATH_GRAM_FULL);
   const int ntiles = sym == 1 ? ntm * (ntm + 1) / 2 : sym == 2 ? ntm * (ntm + 1) / 2 + ntm * ntn1 : ntm * ntn;
   const int nch = gram_chunks(n, ntiles);
   int64_t rpc = (n + nch - 1) / nch;
   rpc = ((rpc + GR - 1) / GR) * GR;
   const size_t smem = GNS * 2 * GR * LDS * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    set_smem((const void*)k_gram_partial, smem);
-    attr = true;
-  }
+  smem_optin((const void*)k_gram_partial, smem);
   {
     nsp_count_launch();
     launch_k(k_gram_partial, dim3(dim3(ntiles, nch)), dim3(256), smem, st, Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn, sym);
@@ -1036,11 +1033,7 @@ void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, 
 void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   const size_t smem = (2 * 64 * 36 + 2 * 32 * LDS) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    set_smem((const void*)k_panel, smem);
-    attr = true;
-  }
+  smem_optin((const void*)k_panel, smem);
   dim3 grid((unsigned)((n + 63) / 64), (ncols + 63) / 64, a1 ? 2 : 1);
   { nsp_count_launch(); launch_k(k_panel, dim3(grid), dim3(256), smem, st, a0, a1 ? *a1 : a0, kdim, n); }
 }
@@ -1048,27 +1041,20 @@ void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64
 int panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
           int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st) {
   PanelArgs a{Out, ldo, Cin, ldc, In, ldi, M, ldm, sgn, normpart};
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm = num_sms();
   static const bool rows_off = [] {
     const char* e = getenv("NSP_PANEL_ROWS");
     return e && e[0] == '0';
   }();
   // one-wave row-range panel: s = 128 and at least one 64-row pass per SM (normpart rows = CTAs)
-  if (!rows_off && kdim == 128 && ncols == 128 && n >= (int64_t)64 * nsm && ldo >= 128) {
+  if (!rows_off && !nsp_force_generic && kdim == 128 && ncols == 128 && n >= (int64_t)64 * nsm && ldo >= 128) {
+    nsp_count_path(NSP_PATH_PANEL_ROWS);
     const size_t smem = (128 * PLDM + PNS * 64 * PLDA) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      set_smem((const void*)k_panel_rows<NSP_PANEL_NW>, smem);
-      attr = true;
-    }
+    smem_optin((const void*)k_panel_rows<NSP_PANEL_NW>, smem);
     { nsp_count_launch(); launch_k(k_panel_rows<NSP_PANEL_NW>, dim3(nsm), dim3(NSP_PANEL_NW * 32), smem, st, a, n, (n + 15) / 16); }
     return nsm;
   }
+  nsp_count_path(NSP_PATH_PANEL_TILES);
   panel2(a, nullptr, kdim, ncols, n, st);
   return (int)((n + 63) / 64);
 }
@@ -1100,7 +1086,7 @@ void converge(const double* rsq, const double* bnorm, int s, double tol, BcgStat
 void small_chol(const double* A, int sp, int mode, int nact, double tau, double* Out, BcgStatus* stt,
                 cudaStream_t st) {
   const size_t smem = (size_t)(128 * sc::LDA + 16 * 64 + 8 * 64) * sizeof(double);
-  set_smem((const void*)k_small_chol, smem);
+  smem_optin((const void*)k_small_chol, smem);
   { nsp_count_launch(); k_small_chol<<<1, 256, smem, st>>>(A, sp, mode, nact, tau, Out, stt); }
 }
 
@@ -1110,7 +1096,7 @@ void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* 
   const int g = ne >= 128 ? 8 : ne >= 64 ? 4 : 1;   // V row slices (rp = ne / g rows each)
   const int rp = (ne + g - 1) / g;
   const size_t smem = (size_t)(ne * (ne + 1) / 2 + ne * rp) * sizeof(double);
-  set_smem((const void*)k_small_eig, smem);
+  smem_optin((const void*)k_small_eig, smem);
   { nsp_count_launch(); launch_k(k_small_eig, dim3(g), dim3(1024), smem, st, A, lda, n, Vwork, ldv, lam, Vsorted, gate, tau, T, spT, stw); }
 }
 

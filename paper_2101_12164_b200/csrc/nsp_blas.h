@@ -20,6 +20,11 @@ struct BcgStatus {
 };
 
 void nsp_count_launch();
+// dispatch-path evidence counters (NSP_PATH_* in include/nsp.h): incremented at dispatch (eager or captured)
+void nsp_count_path(int id);
+// kernel-level tests (nsp_dev_*): force the generic kernels instead of the shape-specialised ones
+// (0 = production dispatch, 1 = generic k_panel / full-tile Gram); set only around a test call
+extern thread_local int nsp_force_generic;
 
 struct PanelArgs {
   double* Out;

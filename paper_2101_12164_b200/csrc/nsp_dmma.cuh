@@ -4,9 +4,39 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <utility>
 
 namespace nspd {
+
+// Dynamic shared memory above 48 KB is an opt-in per (kernel, DEVICE): cached per device so a
+// second device in the same process gets its own attribute (a process-wide flag would skip it).
+inline void smem_optin(const void* f, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[std::make_pair(f, dev)];
+  if (have >= bytes) return;
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  have = bytes;
+}
+
+// SM count of the current device (grid sizing: one wave = SMs x resident CTAs), cached per device.
+inline int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
 
 // D = A(8x4, row) * B(4x8, col) + C.  Fragment ownership (lane = 4*g + t):
 //   a = A[g][t], b = B[t][g], c = {C[g][2t], C[g][2t+1]}.

@@ -604,8 +604,11 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
     double* Ms = sm + (J & 1) * STAGE;
     if (threadIdx.x == 0) {
       fence_proxy_async();
-      mbar_expect_copy(&bar[J & 1], Ms, mt(J), NSP_MINV_TILE * 8);
-      if (CM) mbar_add_copy(&bar[J & 1], Ms + NSP_MINV_TILE, Wb + (int64_t)J * 64 * LDV, 64 * LDV * 8);
+      // the stage's full byte count is expected (arrive.expect_tx) BEFORE any of its copies is issued,
+      // so the phase cannot complete on a partial byte count
+      mbar_expect(&bar[J & 1], NSP_MINV_TILE * 8 + (CM ? 64 * LDV * 8 : 0));
+      bulk_copy(Ms, mt(J), NSP_MINV_TILE * 8, &bar[J & 1]);
+      if (CM) bulk_copy(Ms + NSP_MINV_TILE, Wb + (int64_t)J * 64 * LDV, 64 * LDV * 8, &bar[J & 1]);
     }
     if (!CM) cp_block(Ms + NSP_MINV_TILE, LDV, Wb + (int64_t)J * 64 * ldw, ldw, 64, CW);
   };
@@ -613,10 +616,14 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
   acc_zero(acc);
   // the S_j^{-1} tiles are constant: stage 0's M tile is requested BEFORE waiting for the producer of
   // W (programmatic dependent launch), so its latency hides behind the previous kernel's tail
-  if (threadIdx.x == 0) mbar_expect_copy(&bar[0], sm, mt(0), NSP_MINV_TILE * 8);
+  // (stage 0 expects M and W bytes up front: the W copy issued after pdl_wait() only completes it)
+  if (threadIdx.x == 0) {
+    mbar_expect(&bar[0], NSP_MINV_TILE * 8 + (CM ? 64 * LDV * 8 : 0));
+    bulk_copy(sm, mt(0), NSP_MINV_TILE * 8, &bar[0]);
+  }
   pdl_wait();
   if (CM) {
-    if (threadIdx.x == 0) mbar_add_copy(&bar[0], sm + NSP_MINV_TILE, Wb, 64 * LDV * 8);
+    if (threadIdx.x == 0) bulk_copy(sm + NSP_MINV_TILE, Wb, 64 * LDV * 8, &bar[0]);
   } else {
     cp_block(sm + NSP_MINV_TILE, LDV, Wb, ldw, 64, CW);
   }
@@ -1192,8 +1199,9 @@ __global__ void __launch_bounds__(256) k_band_fb_vec(const TriSys* __restrict__ 
         ++iJ;
       } else {
         if (tid == 0) {
-          mbar_expect_copy(&bar[sl], Lr + sl * 4096, tile(iI, iI), 32768);
-          mbar_add_copy(&bar[sl], Wr + sl * 64, Wb + (int64_t)iI * 64, 512);
+          mbar_expect(&bar[sl], 32768 + 512);   // full stage bytes before either copy is issued
+          bulk_copy(Lr + sl * 4096, tile(iI, iI), 32768, &bar[sl]);
+          bulk_copy(Wr + sl * 64, Wb + (int64_t)iI * 64, 512, &bar[sl]);
         }
         iI = next_row(iI);
         iJ = (fw ? iI < nt : iI >= 0) ? first_j(iI) : 0;
@@ -1304,9 +1312,10 @@ __global__ void __launch_bounds__(256) k_band_rec_vec(const TriSys* __restrict__
   auto issue = [&](int q) {
     if (q >= nt || tid != 0) return;
     const int sl = q % NS, I = row_of(q);
-    mbar_expect_copy(&bar[sl], Tr + sl * 8192, Xd + (t0 + I) * xstride * 4096, 32768);
-    if (q > 0) mbar_add_copy(&bar[sl], Tr + sl * 8192 + 4096, Gc + (t0 + I) * 4096, 32768);
-    mbar_add_copy(&bar[sl], Wr + sl * 64, Wb + (int64_t)I * 64, 512);
+    mbar_expect(&bar[sl], 32768 + (q > 0 ? 32768 : 0) + 512);   // full stage bytes first, then the copies
+    bulk_copy(Tr + sl * 8192, Xd + (t0 + I) * xstride * 4096, 32768, &bar[sl]);
+    if (q > 0) bulk_copy(Tr + sl * 8192 + 4096, Gc + (t0 + I) * 4096, 32768, &bar[sl]);
+    bulk_copy(Wr + sl * 64, Wb + (int64_t)I * 64, 512, &bar[sl]);
   };
   for (int q = 0; q < NS - 1; ++q) issue(q);
   for (int q = 0; q < nt; ++q) {
@@ -1642,11 +1651,7 @@ void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, do
                    const int* border_first, int* status, cudaStream_t st) {
   if (nsub <= 0) return;
   const size_t smem = 5 * 64 * LDT * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tile_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  smem_optin((const void*)k_tile_cholesky, (size_t)((int)smem));
   { nsp_count_launch(); k_tile_cholesky<<<nsub, 256, smem, st>>>(subs, band, dense, scratch, border_first, status); }
 }
 
@@ -1684,23 +1689,15 @@ void band_rec(const TriSys* sys, int nsys, const double* Xd, int64_t xstride, co
               bool fwd, cudaStream_t st) {
   if (nsys <= 0) return;
   // few independent sweeps: 16-wide column slices double the CTAs (as in tri_fb)
-  if (nsys * (ldw / 32) < 2 * 148) {
+  if (nsys * (ldw / 32) < 2 * num_sms()) {
     const size_t smem = (4 * 64 * LDT + 4 * 64 * 20) * sizeof(double);
-    static bool attr16 = false;
-    if (!attr16) {
-      cudaFuncSetAttribute(k_band_rec<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr16 = true;
-    }
+    smem_optin((const void*)k_band_rec<16>, (size_t)((int)smem));
     nsp_count_launch();
     launch_k(k_band_rec<16>, dim3(dim3(nsys, ldw / 16)), dim3(256), smem, st, sys, Xd, xstride, Gc, buf, ldw, fwd ? 1 : 0);
     return;
   }
   const size_t smem = (4 * 64 * LDT + 4 * 64 * 36) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_band_rec<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  smem_optin((const void*)k_band_rec<32>, (size_t)((int)smem));
   nsp_count_launch();
   launch_k(k_band_rec<32>, dim3(dim3(nsys, ldw / 32)), dim3(256), smem, st, sys, Xd, xstride, Gc, buf, ldw, fwd ? 1 : 0);
 }
@@ -1710,11 +1707,7 @@ void band_rec_vec(const TriSys* sys, int nsys, const double* Xd, int64_t xstride
   if (nsys <= 0) return;
   constexpr int NS = 3;
   const size_t smem = (NS * 8192 + NS * 64 + 2 * 64) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_band_rec_vec<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  smem_optin((const void*)k_band_rec_vec<NS>, (size_t)((int)smem));
   nsp_count_launch();
   launch_k(k_band_rec_vec<NS>, dim3(nsys), dim3(256), smem, st, sys, Xd, xstride, Gc, buf, fwd ? 1 : 0);
 }
@@ -1726,46 +1719,34 @@ void tri_fb(const TriSys* sys, int nsys, double* buf, int ldw, int cw, bool fwd,
   if (wbmax >= 0 && wbmax <= 2 && cw == 1 && ldw == 1 && !getenv("NSP_NO_BAND")) {   // one column: matvec chain
     constexpr int NS = 4;
     const size_t smem = (NS * 4096 + NS * 64 + 3 * 64 + 4 * 64 + 64) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_band_fb_vec<NS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    smem_optin((const void*)k_band_fb_vec<NS, 2>, (size_t)((int)smem));
     { nsp_count_launch(); k_band_fb_vec<NS, 2><<<nsys, 256, smem, st>>>(sys, buf, fwd, bwd); }
     return;
   }
   if (cw == 1) cw = 32;   // generic kernels: at least one 32-wide column chunk
   grid = dim3(nsys, ldw >= 32 ? ldw / cw : 1);
-  if (wbmax >= 0 && wbmax <= 2 && cw == 32 && nsys * (ldw / 32) < 2 * 148 && !getenv("NSP_NO_BAND")) {
+  if (wbmax >= 0 && wbmax <= 2 && cw == 32 && nsys * (ldw / 32) < 2 * num_sms() && !getenv("NSP_NO_BAND")) {
     // few independent sweeps (e.g. the single A_G system): 16-wide column chunks double the CTAs
     constexpr int NS = 3;
     const size_t smem = (NS * 64 * LDT + NS * 64 * 20 + 3 * 64 * 20) * sizeof(double);
-    static bool attr16 = false;
-    if (!attr16) {
-      cudaFuncSetAttribute(k_band_fb<16, NS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr16 = true;
-    }
+    smem_optin((const void*)k_band_fb<16, NS, 2>, (size_t)((int)smem));
     { nsp_count_launch(); k_band_fb<16, NS, 2><<<dim3(nsys, ldw / 16), 256, smem, st>>>(sys, buf, ldw, fwd, bwd); }
     return;
   }
   if (wbmax >= 0 && wbmax <= 2 && cw == 32 && !getenv("NSP_NO_BAND")) {   // narrow band: deep-prefetch kernel
     constexpr int NS = 3;
     const size_t smem = (NS * 64 * LDT + NS * 64 * 36 + 3 * 64 * 36) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_band_fb<32, NS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    smem_optin((const void*)k_band_fb<32, NS, 2>, (size_t)((int)smem));
     { nsp_count_launch(); k_band_fb<32, NS, 2><<<grid, 256, smem, st>>>(sys, buf, ldw, fwd, bwd); }
     return;
   }
   if (cw == 64) {
     const size_t smem = (2 * 64 * LDT + 2 * 64 * (64 + 4)) * sizeof(double);
-    cudaFuncSetAttribute(k_tri_fb<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_optin((const void*)k_tri_fb<64>, (size_t)((int)smem));
     { nsp_count_launch(); k_tri_fb<64><<<grid, 256, smem, st>>>(sys, buf, ldw, fwd, bwd); }
   } else {
     const size_t smem = (2 * 64 * LDT + 2 * 64 * (32 + 4)) * sizeof(double);
-    cudaFuncSetAttribute(k_tri_fb<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_optin((const void*)k_tri_fb<32>, (size_t)((int)smem));
     { nsp_count_launch(); k_tri_fb<32><<<grid, 256, smem, st>>>(sys, buf, ldw, fwd, bwd); }
   }
 }
@@ -1774,28 +1755,16 @@ void spike_tail(const double* spk, const int* chunk_first, int P, double* buf, i
                 cudaStream_t st) {
   if (P <= 1) return;
   const size_t smem = (64 * 65 + 64 * 33) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_spike_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_spike_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  smem_optin((const void*)k_spike_tail, (size_t)((int)smem));
+    smem_optin((const void*)k_spike_update, (size_t)((int)smem));
   if (s == 1 && ldw == 1) {
-    static bool attr1 = false;
-    if (!attr1) {
-      cudaFuncSetAttribute(k_spike_tail_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4096 * 8);
-      attr1 = true;
-    }
+    smem_optin((const void*)k_spike_tail_vec, (size_t)(3 * 4096 * 8));
     { nsp_count_launch(); launch_k(k_spike_tail_vec, dim3(1), dim3(256), 3 * 4096 * 8, st, spk, chunk_first, P, buf, fwd); }
     return;
   }
   if (ldw % 32 == 0 && !getenv("NSP_SPIKE_OLD")) {
     const size_t sm2 = (2 * 64 * LDT + 3 * 64 * 36) * sizeof(double);
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(k_spike_tail_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-      attr2 = true;
-    }
+    smem_optin((const void*)k_spike_tail_mma, (size_t)((int)sm2));
     { nsp_count_launch(); launch_k(k_spike_tail_mma, dim3(ldw / 32), dim3(256), sm2, st, spk, chunk_first, P, buf, ldw, fwd ? 1 : 0); }
     return;
   }
@@ -1811,11 +1780,7 @@ void spike_update(const double* spk, const int* chunk_first, const int* tile_chu
   }
   if (ldw % 32 == 0 && !getenv("NSP_SPIKE_OLD")) {
     const size_t sm2 = (64 * LDT + 64 * 36) * sizeof(double);
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(k_spike_update_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-      attr2 = true;
-    }
+    smem_optin((const void*)k_spike_update_mma, (size_t)((int)sm2));
     { nsp_count_launch(); launch_k(k_spike_update_mma, dim3(nt, ldw / 32), dim3(256), sm2, st, spk, chunk_first, tile_chunk, P, buf, ldw, fwd ? 1 : 0); }
     return;
   }
@@ -1841,7 +1806,7 @@ void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, 
 void l22_inverse(const FacSub* subs, int nsub, int max_ntb, const double* dense, double* minv, cudaStream_t st) {
   if (nsub <= 0 || max_ntb <= 0) return;
   const size_t smem = (2 * 64 * LDT + 2 * 64 * 68) * sizeof(double);
-  cudaFuncSetAttribute(k_l22_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  smem_optin((const void*)k_l22_inverse, (size_t)((int)smem));
   { nsp_count_launch(); k_l22_inverse<<<dim3(nsub, max_ntb), 256, smem, st>>>(subs, dense, minv); }
 }
 
@@ -1855,29 +1820,16 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
   const size_t smem = 2 * (NSP_MINV_TILE + 64 * (cw + 4)) * sizeof(double);
   if (cm_stride > 0) {   // ldw = the logical padded width (a multiple of 32), one CTA column per chunk
     const dim3 grid(ldw / 32, nitems);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_symm<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(2 * (NSP_MINV_TILE + 64 * 36) * sizeof(double)));
-      attr = true;
-    }
+    smem_optin((const void*)k_symm<32, true>, (size_t)((int)(2 * (NSP_MINV_TILE + 64 * 36) * sizeof(double))));
     { nsp_count_launch(); launch_k(k_symm<32, true>, grid, dim3(256), 2 * (NSP_MINV_TILE + 64 * 36) * sizeof(double), st, subs, items, minv, W, U, 36, cm_stride); }
     return;
   }
   dim3 grid(nitems, ldw / cw);
   if (cw == 64) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_symm<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    smem_optin((const void*)k_symm<64, false>, (size_t)((int)smem));
     { nsp_count_launch(); launch_k(k_symm<64, false>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw, (int64_t)0); }
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_symm<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    smem_optin((const void*)k_symm<32, false>, (size_t)((int)smem));
     { nsp_count_launch(); launch_k(k_symm<32, false>, dim3(grid), dim3(256), smem, st, subs, items, minv, W, U, ldw, (int64_t)0); }
   }
 }
@@ -1889,7 +1841,7 @@ void symv(const FacSub* subs, const int2* items, int nitems, int max_ntb, const 
   if (smem > 48 * 1024) {
     static size_t attr = 0;
     if (attr < smem) {
-      cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smem_optin((const void*)k_symv, (size_t)((int)smem));
       attr = smem;
     }
   }
@@ -1903,7 +1855,7 @@ void symv1(const FacSub* subs, const int2* items, int nitems, int max_ntb, const
   if (smem > 48 * 1024) {
     static size_t attr = 0;
     if (attr < smem) {
-      cudaFuncSetAttribute(k_symv1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smem_optin((const void*)k_symv1, (size_t)((int)smem));
       attr = smem;
     }
   }
@@ -1916,19 +1868,11 @@ void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int
   dim3 grid(nsub, ldw / cw);
   if (cw == 64) {
     const size_t smem = (2 * 64 * LDT + 2 * 64 * (64 + 4)) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_trsm_fb<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    smem_optin((const void*)k_trsm_fb<64>, (size_t)((int)smem));
     { nsp_count_launch(); k_trsm_fb<64><<<grid, 256, smem, st>>>(subs, dense, wvu, ldw); }
   } else {
     const size_t smem = (2 * 64 * LDT + 2 * 64 * (32 + 4)) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_trsm_fb<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    smem_optin((const void*)k_trsm_fb<32>, (size_t)((int)smem));
     { nsp_count_launch(); k_trsm_fb<32><<<grid, 256, smem, st>>>(subs, dense, wvu, ldw); }
   }
 }

@@ -436,11 +436,7 @@ namespace nspb {
 void chol_fac(const double* A, int sp, int mode, int nact, double tau, double* Lp, BcgStatus* stt, cudaStream_t st) {
   // sp = s rounded up to 64 (the block-CG padding): 64 or 128
   const size_t smem = (size_t)(128 * LDA + 8 * 256) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_chol16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  smem_optin((const void*)k_chol16, (size_t)((int)smem));
   nsp_count_launch();
   launch_k(k_chol16, dim3(1), dim3(CF_T), smem, st, A, sp, mode, nact, tau, Lp, stt);
 }
@@ -448,12 +444,7 @@ void chol_fac(const double* A, int sp, int mode, int nact, double tau, double* L
 void chol_solve(const double* Lp, int sp, const double* B, int ldb, double* Out, int ldo, double sgn, bool fwd,
                 bool bwd, const int* gate, cudaStream_t st) {
   const size_t smem = (size_t)(sp * (sp + 2) + sp * 10) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((128 * 130 + 128 * 10) * sizeof(double)));
-    attr = true;
-  }
+  smem_optin((const void*)k_chol_solve, (size_t)((int)((128 * 130 + 128 * 10) * sizeof(double))));
   nsp_count_launch();
   launch_k(k_chol_solve, dim3(sp / 8), dim3(CS_T), smem, st, Lp, sp, B, ldb, Out, ldo, sgn, fwd, bwd, gate);
 }

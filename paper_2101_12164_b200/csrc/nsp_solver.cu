@@ -106,7 +106,8 @@ static size_t bcg_layout(const nsp_ctx* c, int s, char* base, BcgWs* w, int kind
   t.P = cv.take(blk);
   t.Q = cv.take(blk);
   t.W = cv.take(blk);
-  t.Z = ((kind || c->opts.bcg_precond) ? cv.take(blk) : nullptr);
+  // Z exists whenever M = A_G^{-1} is possible (nsp_set_bcg_precond may switch M after setup)
+  t.Z = ((kind || c->opts.bcg_precond || c->has_ag) ? cv.take(blk) : nullptr);
   if (kind) {
     t.tG = cv.take((size_t)std::max<int64_t>(c->nG, 1) * sp);
     t.hB = cv.take((size_t)std::max<int64_t>(c->wvu_rows, 1) * sp);

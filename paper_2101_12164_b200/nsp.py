@@ -22,7 +22,12 @@ EXPORTED = ["nsp_default_opts", "nsp_setup", "nsp_dims", "nsp_gamma_index", "nsp
             "nsp_stats", "nsp_schur_apply", "nsp_kgamma_apply", "nsp_block_cg", "nsp_nystrom",
             "nsp_nystrom_sigma", "nsp_precond_apply", "nsp_pcg", "nsp_last_error", "nsp_destroy",
             "nsp_gamma_apply", "nsp_kernel_launches", "nsp_profile", "nsp_profile_read", "nsp_shard_plan",
-            "nsp_shard_info", "nsp_nccl_unique_id", "nsp_local_group_create", "nsp_local_group_destroy"]
+            "nsp_shard_info", "nsp_nccl_unique_id", "nsp_local_group_create", "nsp_local_group_destroy",
+            "nsp_set_bcg_precond", "nsp_path_counters", "nsp_dev_panel", "nsp_dev_gram"]
+
+# dispatch-path counter ids (include/nsp.h NSP_PATH_*)
+PATHS = ["panel_rows", "panel_tiles", "gram_sym", "gram_de", "gram_full", "symm", "sweeps", "symv",
+         "panel_gram", "chol_solve"]
 
 
 class nsp_csr(C.Structure):
@@ -93,6 +98,10 @@ def load_library(path: str = LIB_PATH):
     lib.nsp_kernel_launches.restype = C.c_longlong
     lib.nsp_destroy.argtypes = [P]
     lib.nsp_destroy.restype = None
+    lib.nsp_set_bcg_precond.argtypes = [P, I]
+    lib.nsp_path_counters.argtypes = [P, I]
+    lib.nsp_dev_panel.argtypes = [P, P, P, P, I64, I, D, P, I, P]
+    lib.nsp_dev_gram.argtypes = [P, P, P, I64, I, P, P, I, I, P]
     for f in EXPORTED:
         if f not in ("nsp_default_opts", "nsp_last_error", "nsp_destroy", "nsp_kernel_launches",
                      "nsp_local_group_create", "nsp_local_group_destroy"):
@@ -105,7 +114,7 @@ def _ptr(t) -> int:
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
         raise TypeError("expected a contiguous CUDA float64 tensor")
-    return t.data_ptr()
+    return t.data_ptr() or None
 
 
 class Report(dict):
@@ -126,6 +135,39 @@ def _report(rep: nsp_report, hist, widths) -> Report:
 
 def kernel_launches() -> int:
     return int(load_library().nsp_kernel_launches())
+
+
+def path_counters() -> dict:
+    """Dispatch-path counters (NSP_PATH_*): {name: dispatches so far in this process}."""
+    lib = load_library()
+    n = lib.nsp_path_counters(None, 0)
+    out = (C.c_longlong * n)()
+    lib.nsp_path_counters(out, n)
+    return {nm: int(out[i]) for i, nm in enumerate(PATHS)}
+
+
+def _stream_ptr(stream):
+    import torch
+    return (stream or torch.cuda.current_stream()).cuda_stream
+
+
+def dev_panel(Out, Cin, In, M, sgn, colsq=None, path=0, stream=None):
+    """nsp_dev_panel: Out = Cin + sgn * In M (n x s, s in {64, 128}); colsq = column sums of squares."""
+    lib = load_library()
+    st = lib.nsp_dev_panel(_ptr(Out), None if Cin is None else _ptr(Cin), _ptr(In), _ptr(M), In.shape[0],
+                           In.shape[1], sgn, None if colsq is None else _ptr(colsq), path, _stream_ptr(stream))
+    if st != 0:
+        raise NspError(st, "nsp_dev_panel failed")
+
+
+def dev_gram(Xa, Xb, out, Xb2=None, out2=None, lower_first=False, path=0, stream=None):
+    """nsp_dev_gram: out = Xa^T Xb (and out2 = Xa^T Xb2)."""
+    lib = load_library()
+    st = lib.nsp_dev_gram(_ptr(Xa), _ptr(Xb), None if Xb2 is None else _ptr(Xb2), Xa.shape[0], Xa.shape[1],
+                          _ptr(out), None if out2 is None else _ptr(out2), int(lower_first), path,
+                          _stream_ptr(stream))
+    if st != 0:
+        raise NspError(st, "nsp_dev_gram failed")
 
 
 def shard_plan(rowptr, colidx, val, part, K, nranks, rank):
@@ -258,6 +300,10 @@ class Context:
         ms, cnt = C.c_double(), C.c_longlong()
         self._check(self.lib.nsp_profile_read(self.ctx, C.byref(ms), C.byref(cnt)))
         return ms.value, cnt.value
+
+    def set_bcg_precond(self, precond: int):
+        """nsp_set_bcg_precond: 0 = M = I, 1 = M = A_G^{-1} (reading C2) for later block_cg calls."""
+        self._check(self.lib.nsp_set_bcg_precond(self.ctx, int(precond)))
 
     def gamma_apply(self, X, Y):
         self._check(self.lib.nsp_gamma_apply(self.ctx, _ptr(X), _ptr(Y), X.shape[1]))

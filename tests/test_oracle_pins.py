@@ -174,6 +174,46 @@ def test_schur_bruteforce_elimination(dims, K):
     assert np.max(np.abs(S.apply_rows(X, rows) - (S_bf @ X)[rows])) < 1e-13 * np.abs(S_bf @ X).max()
 
 
+@pytest.mark.parametrize("dims,axis,c", [((9, 7), 0, 4), ((16, 12), 1, 5), ((9, 6, 5), 0, 3)])
+def test_local_schur_single_separator_closed_form(dims, axis, c):
+    """LocalSchurOracle (S_G from dense local blocks, the full-size cfg2 oracle) against the closed-form
+    single-separator spectrum: S_G v_j = lambda_j v_j."""
+    A, part = _single_separator(dims, axis, c)
+    d = O.dbbd(A.to_scipy(), part, 2)
+    lam, V, _, _ = _closed_form_modes(dims, axis, c)
+    L = O.LocalSchurOracle(d)
+    assert np.max(np.abs(L.apply(V) - V * lam)) < 1e-12 * lam.max()
+
+
+@pytest.mark.parametrize("dims,K", [((7, 6), 4), ((5, 4, 4), 4)])
+def test_local_schur_bruteforce_elimination(dims, K):
+    """LocalSchurOracle against brute-force Gaussian elimination (pure Python loops) on tiny grids."""
+    A = P.laplacian(dims).to_scipy()
+    part = P.geometric_nd(dims, K)
+    d = O.dbbd(A, part, K)
+    Ad = A.toarray()[np.ix_(d.perm, d.perm)]
+    S_bf = _gauss_eliminate_schur(Ad.tolist(), d.n - d.n_gamma)
+    X = np.random.default_rng(0).standard_normal((d.n_gamma, 3))
+    L = O.LocalSchurOracle(d)
+    assert np.max(np.abs(L.apply(X) - S_bf @ X)) < 1e-13 * np.abs(S_bf @ X).max()
+
+
+def test_oracle_threads_bitwise_identical():
+    """The thread pool only distributes independent blocks; sums stay in ascending block order, so
+    the result is bitwise identical to the serial loop (any thread count)."""
+    pr = P.make("cfg2s")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    X = pr.omega()
+    Y1 = O.SchurOracle(d).apply(X)
+    Y4 = O.SchurOracle(d, threads=4).apply(X)
+    assert np.array_equal(Y1, Y4)
+    assert np.array_equal(O.LocalSchurOracle(d).apply(X), O.LocalSchurOracle(d, threads=4).apply(X))
+    # subset sums: K_G over a block subset = the sum of its blocks' terms
+    S = O.SchurOracle(d)
+    parts = S.k_gamma(X, blocks=range(0, d.K, 2)) + S.k_gamma(X, blocks=range(1, d.K, 2))
+    assert np.max(np.abs(parts - S.k_gamma(X))) <= 1e-13 * np.abs(parts).max()
+
+
 def test_schur_decoupled_and_arrow():
     """A_GI = 0 -> S_G = A_G; arrow matrix -> a_GG - sum a_i^2/d_i."""
     A = sp.csr_matrix(np.diag([2.0, 3.0, 4.0, 5.0]))
