@@ -3,12 +3,19 @@
 
 One step = one pass of the whole hot path over one
 batch of synthetic input:  B = K_G Omega (a0);  breakdown-free block CG on
-S_G X = B to tol (a1-a11);  Y = A_G X (a12).
+S_G X = B to tol (a1-a11, M = I: the north_star-literal mode, every iteration is
+exactly one S_G apply on n_G x s);  Y = A_G X (a12).
 value = s * (block-CG iterations) / (step time)  [S_G RHS-applies per second],
-whole job (summed over ranks).  Inputs resident in HBM when the timed region
-starts; L2 flushed (256 MiB write) before every timed step.
+whole job (one global problem sharded over the ranks).  Inputs resident in HBM
+when the timed region starts; L2 flushed (256 MiB write) before every timed step.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+Workload: BASELINE.json configs[4] (cfg5, 256^3 Laplacian, n = 16.8M, K = 1024,
+s = 128) - the largest configuration and the one the north_star's scaling target
+names; it fits one B200 (~130 GB).  The line also carries the paper-analog
+M = A_G^-1 time-to-tol (reading C2), the Nystrom (Alg. 2) and outer-PCG (M_2 to
+1e-8) times, the setup time, and a secondary object for cfg2 (configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl ours|reference]
 """
 from __future__ import annotations
 
@@ -165,92 +172,130 @@ def _cores():
         return os.cpu_count()
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _sample_blocks(K, nsample):
+    """Evenly spread block ids of the bounded CPU sample (the extrapolation is linear in K)."""
+    if nsample >= K:
+        return list(range(K))
+    return sorted(set(int(round(i * K / nsample)) for i in range(nsample)))
+
+
 # ------------------------------------------------------------------------------------------
-# reference arm: the CPU oracle, as it stands, on this box's host cores
+# the CPU oracle on a bounded sample (reference arm and cpu_baseline leg)
 # ------------------------------------------------------------------------------------------
+class OracleSample:
+    """The oracle's S_G apply (oracle.SchurOracle: A_G X minus the per-block K_G terms with scipy
+    SuperLU block solves), as it stands, on every core of this job's affinity mask (the block loop is
+    spread over threads; SuperLU releases the GIL).  For K > nsample blocks the K_G sum is timed on an
+    evenly spread sample of `nsample` blocks and extrapolated linearly:
+        t_apply = t(A_G X) + (K / nsample) * t(K_G terms of the sample blocks)."""
+
+    def __init__(self, pr, nsample):
+        import oracle as O
+        self.cores = _cores()
+        self.pr = pr
+        self.blocks = _sample_blocks(pr.K, nsample)
+        t0 = time.perf_counter()
+        self.d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K, blocks=None if len(self.blocks) == pr.K else self.blocks)
+        self.S = O.SchurOracle(self.d, threads=self.cores)
+        from oracle.schur import _map
+        _map(self.S.lu_block, self.blocks, self.cores)      # factorisation: setup, not timed
+        self.t_setup = time.perf_counter() - t0
+        self.X = pr.omega()
+
+    def apply_time(self):
+        t0 = time.perf_counter()
+        self.d.A_G @ self.X
+        t1 = time.perf_counter()
+        self.S.k_gamma(self.X, blocks=self.blocks)
+        t2 = time.perf_counter()
+        return (t1 - t0) + (t2 - t1) * self.pr.K / len(self.blocks)
+
+    def describe(self):
+        full = len(self.blocks) == self.pr.K
+        return (f"one oracle S_G apply (s={self.pr.s}) on {self.pr.name} (n_G={self.d.n_gamma}, K={self.pr.K}): "
+                f"A_G X plus the K_G terms of " + ("all blocks" if full else
+                f"{len(self.blocks)} evenly spread blocks, extrapolated x{self.pr.K / len(self.blocks):.0f} "
+                f"(linear in K)") + f"; scipy SuperLU block solves on {self.cores} threads ({_cpu_model()}); "
+                f"block factorisation ({self.t_setup:.1f} s incl. extraction) untimed")
+
+
 def run_reference(args, ws, rank):
+    """bench.py --impl reference: the oracle as it stands on this box's host cores, same config /
+    metric / unit; each step = one (bounded, extrapolated) oracle S_G apply.  Rank 0 only."""
     if rank != 0:
         return
-    from threadpoolctl import threadpool_limits
-    import oracle as O
     from nsp_inputs import problems as P
     pr = P.make(args.config)
-    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
-    S = O.SchurOracle(d)
-    s = pr.s
-    X = pr.omega()
-    with threadpool_limits(limits=1):
-        t0 = time.perf_counter()
-        for j in range(d.K):
-            S.lu_block(j)                      # factorisation (not timed in the metric)
-        t_fact = time.perf_counter() - t0
-        for _ in range(args.warmup):
-            S.apply(X)
-        times = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            S.apply(X)
-            times.append(time.perf_counter() - t0)
+    smp = OracleSample(pr, args.cpu_blocks)
+    for _ in range(args.warmup):
+        smp.apply_time()
+    times = [smp.apply_time() for _ in range(args.steps)]
     tmean = sum(times) / len(times)
-    value = s / tmean
-    sample = (f"one oracle S_G apply (scipy SuperLU per block, 1 thread) on {args.config} "
-              f"(n_G={d.n_gamma}, s={s}) per step; block factorisation {t_fact:.1f}s untimed")
+    value = pr.s / tmean
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmean * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": args.config, "s": s, "n_gamma": d.n_gamma,
-                                            "parallelism": "cpu-oracle"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "data": "synthetic", "config": {"workload": args.config, "s": pr.s, "n_gamma": smp.d.n_gamma,
+                                            "K": pr.K, "parallelism": f"cpu-oracle {smp.cores} threads"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": smp.cores, "kind": "oracle",
+                             "cpu_model": _cpu_model(), "sample": smp.describe()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(pr, seconds=20.0):
-    """The oracle timed on a bounded sample: S_G applies on the same workload (1 thread)."""
-    from threadpoolctl import threadpool_limits
-    import oracle as O
-    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
-    S = O.SchurOracle(d)
-    X = pr.omega()
-    with threadpool_limits(limits=1):
-        for j in range(d.K):
-            S.lu_block(j)
-        S.apply(X)
-        t0 = time.perf_counter()
-        reps = 0
-        while time.perf_counter() - t0 < seconds or reps == 0:
-            S.apply(X)
-            reps += 1
-        t = (time.perf_counter() - t0) / reps
-    return {"value": pr.s / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{reps} oracle S_G applies (s={pr.s}) on {pr.name}, scipy SuperLU block solves, "
-                      f"1 thread; block factorisation untimed"}
+def cpu_baseline(pr, seconds, nsample):
+    """The oracle timed on a bounded sample of the same workload, all affinity cores."""
+    smp = OracleSample(pr, nsample)
+    smp.apply_time()
+    t0 = time.perf_counter()
+    ts = []
+    while time.perf_counter() - t0 < seconds or not ts:
+        ts.append(smp.apply_time())
+    t = sum(ts) / len(ts)
+    return {"value": pr.s / t, "unit": UNIT, "cores": smp.cores, "kind": "oracle", "cpu_model": _cpu_model(),
+            "sample": f"{len(ts)} x " + smp.describe()}
 
 
 # ------------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------------
-def run_ours(args, ws, rank, local):
+def _timed(stream, fn, flush, reps):
     import torch
-    from nsp_inputs import problems as P
-    from paper_2101_12164_b200 import build as B
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    out = []
+    for _ in range(reps):
+        flush.zero_()
+        ev0.record(stream)
+        r = fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        out.append((ev0.elapsed_time(ev1), r))
+    return out
+
+
+def measure(pr, args, ws, rank, local, stream, nccl_id, headline):
+    """Time one configuration; returns the dict of measurements (headline: the full set)."""
+    import torch
     from paper_2101_12164_b200 import nsp
-    B.build()
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    stream = torch.cuda.current_stream(dev)
-    pr = P.make(args.config)
-    nccl_id = None
-    if ws > 1:   # the library's own NCCL communicator; its unique id travels through the process group
-        obj = [nsp.nccl_unique_id() if rank == 0 else None]
-        torch.distributed.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+    single = ws == 1
     t0 = time.perf_counter()
     ctx = nsp.Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, device=local,
-                      stream=stream.cuda_stream, nranks=ws, rank=rank, nccl_id=nccl_id)
+                      stream=stream.cuda_stream, nranks=ws, rank=rank, nccl_id=nccl_id,
+                      factor_gamma=single)
+    torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     st = ctx.stats()
     s, nG = pr.s, ctx.n_gamma_local
@@ -264,6 +309,11 @@ def run_ours(args, ws, rank, local):
     wsbuf = torch.empty(ctx.workspace_bytes(s), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     maxit = args.maxit
+    out = {"workload": pr.name, "n": pr.n, "n_gamma": ctx.n_gamma, "n_gamma_local": nG, "K": pr.K, "s": s,
+           "tol_bcg": pr.tol_bcg, "setup_ms": t_setup * 1e3,
+           "setup_split_ms": dict(zip(["host_analysis", "h2d", "gpu_factor", "ag_operator", "sj_inverse_tiles"],
+                                      ctx.setup_report["t_ms"][:5])),
+           "shared_rows": ctx.n_shared}
 
     def step():
         ctx.kgamma_apply(Om, Bm, wsbuf)
@@ -271,165 +321,192 @@ def run_ours(args, ws, rank, local):
         ctx.gamma_apply(X, Y)
         return rep
 
+    ctx.set_bcg_precond(0)
     for _ in range(args.warmup):
-        rep = step()
+        step()
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
     launches0 = nsp.kernel_launches()
-    times, iters = [], []
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    # the timed region runs the production path (the device-driven loop graph, no per-kernel events)
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush.zero_()
-            ev0.record(stream)
-            rep = step()
-            ev1.record(stream)
-            torch.cuda.synchronize()
-            times.append(ev0.elapsed_time(ev1))
-            iters.append(rep["iters"])
-    launches = (nsp.kernel_launches() - launches0) / args.steps
-    # live duration of the dominant kernel: the same K steps again with a CUDA event pair around every
-    # a2+a3 launch on the context stream (the loop then runs as one graph per iteration, which carries
-    # the event pair; the events bracket only that kernel)
+        if ws > 1:
+            torch.distributed.barrier()
+        res = _timed(stream, step, flush, args.steps)
+        if ws > 1:
+            torch.distributed.barrier()
+    out["clocks"] = clk.summary()
+    out["gpu_launches"] = (nsp.kernel_launches() - launches0) / args.steps
+    times = [t for t, _ in res]
+    iters = [r["iters"] for _, r in res]
+    tmean = sum(times) / len(times)
+    if ws > 1:
+        tt = torch.tensor([tmean], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        tmean = float(tt.item())
+    it_mean = sum(iters) / len(iters)
+    out.update(time_to_tol_ms=tmean, bcg_iters=it_mean, bcg_precond="none (M = I)",
+               rhs_applies_per_s=s * it_mean / (tmean * 1e-3), iteration_ms=tmean / max(it_mean, 1))
+    # live duration of the dominant kernel (a2+a3, k_symm): the same steps with a CUDA event pair around
+    # every a2+a3 launch on the context stream (per-iteration graphs carry the pair)
     ctx.profile(True)
     ctx.profile_read()
-    for _ in range(args.steps):
+    for _ in range(min(args.steps, 3)):
         flush.zero_()
         step()
     torch.cuda.synchronize()
     sweep_ms, sweeps = ctx.profile_read()
     ctx.profile(False)
-    # apply-only timing (K1/K2 pipeline), same stream, L2 flushed
+    out["k_symm"] = {"avg_launch_ms": sweep_ms / max(sweeps, 1), "launches": sweeps,
+                     "flops_per_launch": 2.0 * st["sum_b2"] * s,
+                     "alg_bytes_per_launch": 8 * (st["sum_b2"] + st["sum_b"]) / 2 + 2 * 8 * s * st["sum_b"]}
+    # apply-only timing (a1-a5), L2 flushed
     P_ = torch.randn(nG, s, dtype=torch.float64, device=dev)
     Q_ = torch.empty_like(P_)
-    at = []
-    for i in range(args.apply_reps + 3):
-        flush.zero_()
-        ev0.record(stream)
-        ctx.schur_apply(P_, Q_, wsbuf)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        if i >= 3:
-            at.append(ev0.elapsed_time(ev1))
+    at = [t for t, _ in _timed(stream, lambda: ctx.schur_apply(P_, Q_, wsbuf), flush, args.apply_reps + 3)[3:]]
     t_apply = statistics.median(at)
-    # the same apply with the two batched L22 triangular sweeps (north_star (b) literal kernel)
-    ctx_sw = nsp.Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, device=local,
-                         stream=stream.cuda_stream, nranks=ws, rank=rank, nccl_id=nccl_id, apply_kernel=1) \
-        if ws == 1 else None
-    t_apply_sweeps = None
-    if ctx_sw is not None:
-        ws_sw = torch.empty(ctx_sw.workspace_bytes(s), dtype=torch.uint8, device=dev)
-        at2 = []
-        for i in range(args.apply_reps + 3):
-            flush.zero_()
-            ev0.record(stream)
-            ctx_sw.schur_apply(P_, Q_, ws_sw)
-            ev1.record(stream)
-            torch.cuda.synchronize()
-            if i >= 3:
-                at2.append(ev0.elapsed_time(ev1))
-        t_apply_sweeps = statistics.median(at2)
-        ctx_sw.close()
-        del ws_sw
-    # the paper-analog block-CG preconditioner M = A_G^{-1} (reading C2): same step, its own context
-    analog = None
-    if ws == 1 and not args.no_analog:
-        ctx_a = nsp.Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, device=local,
-                            stream=stream.cuda_stream, bcg_precond=1)
-        ws_a = torch.empty(ctx_a.workspace_bytes(s), dtype=torch.uint8, device=dev)
-        Ba, Xa, Ya = torch.empty_like(Bm), torch.empty_like(Bm), torch.empty_like(Bm)
-
-        def step_a():
-            ctx_a.kgamma_apply(Om, Ba, ws_a)
-            r = ctx_a.block_cg(Ba, Xa, pr.tol_bcg, maxit, ws_a)
-            ctx_a.gamma_apply(Xa, Ya)
-            return r
-        for _ in range(args.warmup):
-            step_a()
-        ta, ia = [], []
-        for _ in range(args.steps):
-            flush.zero_()
-            ev0.record(stream)
-            r = step_a()
-            ev1.record(stream)
-            torch.cuda.synchronize()
-            ta.append(ev0.elapsed_time(ev1))
-            ia.append(r["iters"])
-        analog = {"bcg_precond": "A_G^-1 (paper-analog, reading C2)", "time_to_tol_ms": sum(ta) / len(ta),
-                  "bcg_iters": sum(ia) / len(ia),
-                  "rhs_applies_per_s": s * (sum(ia) / len(ia)) / (sum(ta) / len(ta) * 1e-3)}
-        ctx_a.close()
-        del ws_a
+    out["apply"] = {"ms": t_apply, "rhs_applies_per_s": s / (t_apply * 1e-3),
+                    "a2a3_tflops": 2.0 * st["sum_b2"] * s / (t_apply * 1e-3) / 1e12}
+    out["iteration_split_ms"] = {"iteration": out["iteration_ms"], "apply": t_apply,
+                                 "grams_panels_sxs": out["iteration_ms"] - t_apply}
     # e2e: Omega from pinned host memory, Y back to pinned host memory, inside the timed region
-    et = []
-    for _ in range(max(1, args.steps)):
-        flush.zero_()
-        ev0.record(stream)
+    def step_e2e():
         Om.copy_(Om_h, non_blocking=True)
-        rep_e = step()
+        r = step()
         Y_h.copy_(Y, non_blocking=True)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        et.append((ev0.elapsed_time(ev1), rep_e["iters"]))
-    tmax = sum(times) / len(times)
-    if ws > 1:
-        tt = torch.tensor([tmax], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        tmax = float(tt.item())
-    it_mean = sum(iters) / len(iters)
-    value = s * it_mean / (tmax * 1e-3)      # one global problem sharded over ws ranks (strong scaling)
+        return r
+    et = _timed(stream, step_e2e, flush, max(1, args.steps))
     e2e_t = sum(t for t, _ in et) / len(et)
-    e2e_it = sum(i for _, i in et) / len(et)
-    e2e_val = s * e2e_it / (e2e_t * 1e-3)
-    # roofline of the dominant kernel: the batched factor sweeps (a2+a3), fp64 DMMA-bound
-    sweep_avg_ms = sweep_ms / max(sweeps, 1)
-    flops_per_launch = 2.0 * st["sum_b2"] * s      # forward + backward: 2 * b_j^2 * s per block
-    achieved = flops_per_launch / (sweep_avg_ms * 1e-3) / 1e12
-    # algorithmic bytes: the unpadded lower triangle of every S_j^{-1} streamed once (k_symm: each
-    # stored tile serves two output rows) + W in + U out (s-wide boundary-layer rows)
-    hbm_alg = 8 * (st["sum_b2"] + st["sum_b"]) / 2 + 2 * 8 * s * st["sum_b"]
+    if ws > 1:
+        tt = torch.tensor([e2e_t], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+    e2e_it = sum(r["iters"] for _, r in et) / len(et)
+    out["e2e"] = {"value": s * e2e_it / (e2e_t * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nG * s * 8,
+                  "d2h_bytes_per_step": nG * s * 8}
+    if single and not args.no_analog:
+        # the paper-analog block-CG preconditioner M = A_G^-1 (reading C2), same context
+        ctx.set_bcg_precond(1)
+        for _ in range(max(1, args.warmup - 1)):
+            step()
+        ra = _timed(stream, step, flush, args.steps)
+        ta = sum(t for t, _ in ra) / len(ra)
+        ia = sum(r["iters"] for _, r in ra) / len(ra)
+        ctx.set_bcg_precond(0)
+        out["paper_analog"] = {"bcg_precond": "A_G^-1 (paper-analog, reading C2; " +
+                               ("Chebyshev A_G^-1" if st["ag_bw"] < 0 else "partitioned band factor") + ")",
+                               "time_to_tol_ms": ta, "bcg_iters": ia, "rhs_applies_per_s": s * ia / (ta * 1e-3)}
+    if single and not args.no_nystrom:
+        # Nystrom (Alg. 2: B = K_G Omega, block CG to tol, Y = A_G X, CholQR2, EVDs, Z = A_G^-1 U) and the
+        # outer PCG on the full system with M_2 to tol_pcg (eq:Sx=b)
+        del wsbuf
+        torch.cuda.empty_cache()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rn = ctx.nystrom(pr.rank, pr.oversample, Om, pr.tol_bcg, maxit)
+        torch.cuda.synchronize()
+        out["nystrom_ms"] = (time.perf_counter() - t0) * 1e3
+        out["nystrom_inner_iters"] = rn["iters"]
+        out["nystrom_rank"] = rn["rank"]
+        b = torch.from_numpy(pr.rhs()).to(dev)
+        xs = torch.zeros_like(b)
+        tol_pcg = pr.tol_pcg or 1e-8
+        ctx.pcg(b, xs, tol_pcg, 20000, precond=2)          # warm-up (graph capture)
+        torch.cuda.synchronize()
+        pt = []
+        for _ in range(2):
+            xs.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rp = ctx.pcg(b, xs, tol_pcg, 20000, precond=2)
+            torch.cuda.synchronize()
+            pt.append((time.perf_counter() - t0) * 1e3)
+        out["pcg_ms"] = min(pt)
+        out["pcg_iters"] = rp["iters"]
+        out["pcg_tol"] = tol_pcg
+        out["pcg_precond"] = "M_2 (Nystrom-Schur, Alg. 2)"
+    ctx.close()
+    return out
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    from nsp_inputs import problems as P
+    from paper_2101_12164_b200 import build as B
+    from paper_2101_12164_b200 import nsp
+    B.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+    nccl_id = None
+    if ws > 1:   # the library's own NCCL communicator; its unique id travels through the process group
+        obj = [nsp.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    pr = P.make(args.config)
+    m = measure(pr, args, ws, rank, local, stream, nccl_id, headline=True)
     peaks = _peaks()
+    ks = m["k_symm"]
+    achieved = ks["flops_per_launch"] / (ks["avg_launch_ms"] * 1e-3) / 1e12
     traffic, traffic_src = _traffic(args.config)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": tmax, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "n": pr.n, "n_gamma": nG, "K": pr.K, "s": s,
-                   "tol_bcg": pr.tol_bcg, "bcg_precond": "none",
-                   "parallelism": f"subdomains{ws} (blocks per rank, shared-separator NCCL allreduce)" if ws > 1
-                   else "1gpu", "n_gamma_global": ctx.n_gamma, "shared_rows": ctx.n_shared,
-                   "l2": "flushed (256 MiB write) before every timed step"},
-        "time_to_tol_ms": tmax, "bcg_iters": it_mean, "paper_analog": analog,
-        "apply": {"ms": t_apply, "rhs_applies_per_s": s / (t_apply * 1e-3), "a2a3": "k_symm (explicit S_j^-1 tiles)",
-                  "sweeps_ms": t_apply_sweeps,
-                  "sweeps_rhs_applies_per_s": s / (t_apply_sweeps * 1e-3) if t_apply_sweeps else None},
+        "metric": METRIC, "value": m["rhs_applies_per_s"] * 1.0, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["time_to_tol_ms"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "n": pr.n, "n_gamma": m["n_gamma"], "K": pr.K, "s": pr.s,
+                   "tol_bcg": pr.tol_bcg, "bcg_precond": "none (M = I, north_star-literal)",
+                   "parallelism": f"subdomains over {ws} ranks (contiguous ND subtrees, shared-separator NCCL "
+                                  f"allreduce)" if ws > 1 else "1gpu",
+                   "shared_rows": m["shared_rows"], "l2": "flushed (256 MiB write) before every timed step"},
+        "time_to_tol_ms": m["time_to_tol_ms"], "bcg_iters": m["bcg_iters"],
+        "paper_analog": m.get("paper_analog"),
+        "nystrom_ms": m.get("nystrom_ms"), "nystrom_inner_iters": m.get("nystrom_inner_iters"),
+        "pcg_ms": m.get("pcg_ms"), "pcg_iters": m.get("pcg_iters"), "pcg_tol": m.get("pcg_tol"),
+        "setup_ms": m["setup_ms"], "setup_split_ms": m["setup_split_ms"],
+        "apply": m["apply"], "iteration_split_ms": m["iteration_split_ms"],
         "roofline": {"kernel": "k_symm (a2+a3: U_j = S_j^-1 W_j, all blocks one launch)", "bound": "tensor",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
-                     "algorithmic_bytes_per_launch": hbm_alg,
-                     "peak_source": "fp64 DMMA microbenchmark tools/fp64_peak.cu (profiles/r01_fp64_peak.txt)",
-                     "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": sweep_avg_ms,
+                     "peak_source": "fp64 DMMA microbenchmark tools/fp64_peak.cu (profiles/r01_fp64_peak.txt); "
+                                    "MEASURED_PEAKS.json has no fp64 figure",
+                     "algorithmic_flops_per_launch": ks["flops_per_launch"],
+                     "algorithmic_bytes_per_launch": ks["alg_bytes_per_launch"],
+                     "avg_launch_ms": ks["avg_launch_ms"], "launches": ks["launches"],
                      "timing": "CUDA events around each a2+a3 launch on the context stream, in a pass of the "
-                               "same K steps right after the timed region (the timed region itself runs "
-                               "the event-free device-driven loop graph)",
-                     "launches": sweeps,
-                     "hbm_gbs_at_alg_bytes": hbm_alg / (sweep_avg_ms * 1e-3) / 1e9,
-                     "hbm_peak_gbs": peaks.get("hbm_gbs")},
-        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": nG * s * 8, "d2h_bytes_per_step": nG * s * 8},
-        "gpu_launches": launches,
-        "setup_s": t_setup, "setup_ms": ctx.setup_report["t_ms"][:3],
-        "clocks": clk.summary(),
+                               "same steps right after the timed region (the timed region runs the event-free "
+                               "device-driven loop graph)",
+                     "hbm_gbs_at_alg_bytes": ks["alg_bytes_per_launch"] / (ks["avg_launch_ms"] * 1e-3) / 1e9,
+                     "hbm_peak_gbs": peaks.get("hbm_gbs"),
+                     "iteration_split_ms": m["iteration_split_ms"]},
+        "e2e": m["e2e"], "gpu_launches": m["gpu_launches"], "clocks": m["clocks"],
     }
+    if ws == 1 and not args.no_secondary and args.secondary and args.secondary != args.config:
+        torch.cuda.empty_cache()
+        pr2 = P.make(args.secondary)
+        m2 = measure(pr2, args, ws, rank, local, stream, nccl_id, headline=False)
+        line["secondary"] = {k: m2.get(k) for k in ("workload", "n", "n_gamma", "K", "s", "time_to_tol_ms",
+                                                     "bcg_iters", "rhs_applies_per_s", "iteration_ms", "apply",
+                                                     "paper_analog", "nystrom_ms", "nystrom_inner_iters",
+                                                     "pcg_ms", "pcg_iters", "setup_ms", "e2e", "k_symm")}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(pr, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(pr, args.cpu_seconds, args.cpu_blocks)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def _relaunch(args):
+    """bench.py --gpus N without torchrun: launch N ranks (one per GPU) through torch.distributed.run."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -437,15 +514,24 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--secondary", default="cfg2", help="second workload reported in the same line (N = 1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--maxit", type=int, default=1000)
-    ap.add_argument("--apply-reps", type=int, default=20)
+    ap.add_argument("--apply-reps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--cpu-blocks", type=int, default=16, help="blocks in the oracle's bounded timing sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-analog", action="store_true", help="skip the M = A_G^-1 block-CG timing")
+    ap.add_argument("--no-analog", action="store_true", help="skip the M = A_G^{-1} block-CG timing")
+    ap.add_argument("--no-nystrom", action="store_true", help="skip the Nystrom + outer PCG timing")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        _relaunch(args)
     ws, rank, local = _dist()
+    if ws != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={ws}"}), flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return

@@ -36,9 +36,11 @@ class DBBD:
         return [m.T.tocsr() for m in self.A_IG]
 
 
-def dbbd(A: sp.csr_matrix, part: np.ndarray, K: int) -> DBBD:
+def dbbd(A: sp.csr_matrix, part: np.ndarray, K: int, blocks=None) -> DBBD:
     """Doubly bordered block diagonal form of A (eq:perm_A PAPER.md:371-380): the K interior blocks
-    A_I_j (part == j), the border Gamma (part == -1, ascending id; reading C10) and the couplings."""
+    A_I_j (part == j), the border Gamma (part == -1, ascending id; reading C10) and the couplings.
+    blocks (optional): extract A_I_j / A_I_jG only for these block ids (the others are None) - a bounded
+    timing sample of a config too large to extract whole; the separator check still covers all of A."""
     A = sp.csr_matrix(A)
     n = A.shape[0]
     if A.shape != (n, n):
@@ -58,9 +60,15 @@ def dbbd(A: sp.csr_matrix, part: np.ndarray, K: int) -> DBBD:
         raise ValueError(f"separator property violated at entry ({coo.row[k]}, {coo.col[k]}) "
                          f"between blocks {bi[k]} and {bj[k]}")
     gamma = np.flatnonzero(part < 0)
-    blocks = [np.flatnonzero(part == j) for j in range(K)]
-    A_I = [A[b][:, b].tocsr() for b in blocks]
-    A_IG = [A[b][:, gamma].tocsr() for b in blocks]
+    want = set(range(K)) if blocks is None else set(int(j) for j in blocks)
+    if blocks is None:
+        blks = [np.flatnonzero(part == j) for j in range(K)]
+    else:   # one stable sort instead of K scans: block j's ids are ascending within its run
+        order = np.argsort(part, kind="stable")
+        starts = np.searchsorted(part[order], np.arange(K + 1))
+        blks = [order[starts[j]:starts[j + 1]] for j in range(K)]
+    A_I = [A[b][:, b].tocsr() if j in want else None for j, b in enumerate(blks)]
+    A_IG = [A[b][:, gamma].tocsr() if j in want else None for j, b in enumerate(blks)]
     A_G = A[gamma][:, gamma].tocsr()
-    perm = np.concatenate(blocks + [gamma])
-    return DBBD(n, K, gamma, blocks, A_I, A_IG, A_G, perm)
+    perm = np.concatenate(blks + [gamma])
+    return DBBD(n, K, gamma, blks, A_I, A_IG, A_G, perm)
