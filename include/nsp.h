@@ -259,6 +259,11 @@ nsp_status nsp_dev_panel(double* Out, const double* Cin, const double* In, const
                          double sgn, double* colsq, int path, void* stream);
 nsp_status nsp_dev_gram(const double* Xa, const double* Xb, const double* Xb2, int64_t n, int s, double* out,
                         double* out2, int lower_first, int path, void* stream);
+/*  nsp_dev_panel_gram: the fused s = 128 pass (n >= 64 x SMs, else NSP_ERR_ARG): Out = Cin + sgn In M and
+ *                 gram = In^T Out (gmode 0: the R -= Q alpha, F = Q^T R pass) or Out^T Out (gmode 1: the
+ *                 W = R + P beta, W^T W pass; exactly symmetric); colsq as nsp_dev_panel. */
+nsp_status nsp_dev_panel_gram(double* Out, const double* Cin, const double* In, const double* M, int64_t n,
+                              double sgn, int gmode, double* gram, double* colsq, void* stream);
 
 const char* nsp_last_error(const nsp_ctx* ctx);
 /* Number of device kernels this library has launched in the process (evidence counter). */

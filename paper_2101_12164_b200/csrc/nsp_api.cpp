@@ -286,6 +286,24 @@ nsp_status nsp_dev_gram(const double* Xa, const double* Xb, const double* Xb2, i
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NSP_OK : NSP_ERR_CUDA;
 }
 
+nsp_status nsp_dev_panel_gram(double* Out, const double* Cin, const double* In, const double* M, int64_t n,
+                              double sgn, int gmode, double* gram, double* colsq, void* stream) {
+  if (!Out || !In || !M || !gram || (gmode != 0 && gmode != 1) || !nspb::panel_gram_ok(128, n)) return NSP_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  double *ws = nullptr, *part = nullptr;
+  if (cudaMalloc(&ws, nspb::gram_ws_doubles(n, 128, 128) * 8) != cudaSuccess) return NSP_ERR_CUDA;
+  if (colsq && cudaMalloc(&part, (size_t)((n + 63) / 64 + 1) * 128 * 8) != cudaSuccess) {
+    cudaFree(ws);
+    return NSP_ERR_CUDA;
+  }
+  const int npt = nspb::panel_gram(Out, Cin, In, M, n, sgn, part, gmode, gram, ws, st);
+  if (colsq) nspb::colsq_reduce(part, npt, 128, colsq, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(ws);
+  if (part) cudaFree(part);
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NSP_OK : NSP_ERR_CUDA;
+}
+
 const char* nsp_last_error(const nsp_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 void nsp_destroy(nsp_ctx* c) {

@@ -365,6 +365,168 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t
         ((red[threadIdx.x] + red[128 + threadIdx.x]) + red[256 + threadIdx.x]) + red[384 + threadIdx.x];
 }
 
+// Fused s = 128 panel + Gram partial (rows a8+a10 / a10+a11 of the block-CG iteration, one pass over
+// the tall blocks instead of two):
+//   Out = Cin + sgn In M   (the panel of k_panel_rows)   and   G_cta = Aop^T Out over the CTA's rows,
+// Aop = In (GMODE 0: R -= Q alpha with F = Q^T R_new, M = I) or Out (GMODE 1: W = R + P beta with W^T W,
+// only the tiles on / above the diagonal).  One CTA per SM (16 warps) owning a contiguous range of 16-row
+// groups, M resident in shared memory, 32-row passes: the pass's In tile is staged in shared memory
+// from registers that were loaded during the previous pass (the global loads of pass p+1 are in flight
+// while pass p computes), the panel product runs as 2 x 8 warps of 16 x 16 outputs, the Out tile goes
+// to global memory AND to shared memory, and the Gram accumulates 32 x 32 blocks per warp in registers
+// across all passes.  Each CTA writes its Gram partial in k_gram_reduce's tile layout (full 2 x 2 tiles,
+// or the 3 upper tiles) and, optionally, the column sums of squares of Out (the convergence norms) in
+// k_panel_rows' normpart layout: fixed-order sums throughout (reading C17).
+constexpr int FG_LD = 132;
+template <int GMODE>
+__global__ void __launch_bounds__(512, 1) k_panel_gram(PanelArgs pa, int64_t n, int64_t ngroups,
+                                                      double* __restrict__ gpart) {
+  pdl_wait();
+  extern __shared__ __align__(16) double sm[];
+  double* Ms = sm;                       // 128 x FG_LD
+  double* Is = Ms + 128 * FG_LD;         // 32 x FG_LD: In rows of the pass
+  double* Os = Is + 32 * FG_LD;          // 32 x FG_LD: Out rows of the pass
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t g0 = (int64_t)blockIdx.x * ngroups / gridDim.x;
+  const int64_t g1 = (int64_t)(blockIdx.x + 1) * ngroups / gridDim.x;
+  const int64_t r0 = g0 * 16, r1 = min(n, g1 * 16);
+  const int npass = r1 > r0 ? (int)((r1 - r0 + 31) / 32) : 0;
+  const double* __restrict__ In = pa.In;
+  // M by cp.async (waited for before the first product)
+  cp_block(Ms, FG_LD, pa.M, pa.ldm, 128, 128);
+  cp_commit();
+  // In prefetch: 32 x 128 doubles per pass = 4 double2 per thread (coalesced rows)
+  double2 pre[4];
+  auto load_in = [&](int p) {
+    const int64_t rb = r0 + (int64_t)p * 32;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = 2 * tid + 1024 * k, rr = e >> 7, cc = e & 127;
+      const int64_t r = rb + rr;
+      pre[k] = (p < npass && r < r1) ? *reinterpret_cast<const double2*>(In + r * pa.ldi + cc) : make_double2(0.0, 0.0);
+    }
+  };
+  load_in(0);
+  // panel warp layout: rows 16 * rg .. +16, cols 16 * cg .. +16
+  const int rg = warp >> 3, cg = warp & 7;
+  // Gram warp layout: 32 x 32 block (bi, bj) of the 128 x 128 output
+  const int bi = warp >> 2, bj = warp & 3;
+  const bool gact = GMODE == 0 || bi <= bj;   // symmetric: the blocks on / above the diagonal
+  double gacc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) gacc[i][j][0] = gacc[i][j][1] = 0.0;
+  double sq[2][2];
+  sq[0][0] = sq[0][1] = sq[1][0] = sq[1][1] = 0.0;
+  cp_wait<0>();
+  for (int p = 0; p < npass; ++p) {
+    const int64_t rb = r0 + (int64_t)p * 32;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = 2 * tid + 1024 * k, rr = e >> 7, cc = e & 127;
+      *reinterpret_cast<double2*>(Is + rr * FG_LD + cc) = pre[k];
+    }
+    // this pass's Cin rows into Os by cp.async (Os is free until the epilogue), in flight behind the product
+    if (pa.Cin) cp_block_zf(Os, FG_LD, pa.Cin + rb * pa.ldc, pa.ldc, 32, 128, r1 - rb);
+    cp_commit();
+    load_in(p + 1);   // next pass's In (zeros past the range)
+    __syncthreads();  // Is complete (and M on the first pass)
+    double acc[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < 128; k += 4) {
+      double a[2], b[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) a[i] = Is[(rg * 16 + i * 8 + g) * FG_LD + k + t];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Ms[(k + t) * FG_LD + cg * 16 + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    cp_wait<0>();
+    __syncthreads();  // Cin rows in Os visible to every thread
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int rr = rg * 16 + i * 8 + g;
+        const int64_t r = rb + rr;
+        const int c = cg * 16 + j * 8 + 2 * t;
+        double v0 = 0.0, v1 = 0.0;
+        if (r < r1) {
+          const double2 cv = pa.Cin ? *reinterpret_cast<const double2*>(Os + rr * FG_LD + c) : make_double2(0.0, 0.0);
+          v0 = pa.sgn * acc[i][j][0] + cv.x;
+          v1 = pa.sgn * acc[i][j][1] + cv.y;
+          *reinterpret_cast<double2*>(pa.Out + r * pa.ldo + c) = make_double2(v0, v1);
+          sq[j][0] += v0 * v0;
+          sq[j][1] += v1 * v1;
+        }
+        *reinterpret_cast<double2*>(Os + rr * FG_LD + c) = make_double2(v0, v1);
+      }
+    __syncthreads();  // Os complete
+    if (gact) {
+      const double* Aop = GMODE == 0 ? Is : Os;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = Aop[(k + t) * FG_LD + bi * 32 + i * 8 + g];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Os[(k + t) * FG_LD + bj * 32 + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(gacc[i][j][0], gacc[i][j][1], a[i], b[j]);
+      }
+    }
+    __syncthreads();  // Is / Os free for the next pass
+  }
+  // Gram partial: tile (tm, tn) of 64 x 64 -> k_gram_reduce's layout (GMODE 1: upper tiles 0,1,2 = (0,0),(0,1),(1,1))
+  if (gact) {
+    const int tm = bi >> 1, tn = bj >> 1;
+    const int ntiles = GMODE == 0 ? 4 : 3;
+    const int tile = GMODE == 0 ? tm * 2 + tn : (tm == 0 ? tn : 2);
+    double* out = gpart + ((int64_t)blockIdx.x * ntiles + tile) * 4096;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int rr = (bi & 1) * 32 + i * 8 + g, cc = (bj & 1) * 32 + j * 8 + 2 * t;
+        *reinterpret_cast<double2*>(out + rr * 64 + cc) = make_double2(gacc[i][j][0], gacc[i][j][1]);
+      }
+  }
+  if (!pa.normpart) return;
+  // column sums of squares: the 8 row lanes by butterfly, then the two row-group warps in order
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double v = sq[j][e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      sq[j][e] = v;
+    }
+  double* red = Is;   // 2 x 128
+  if (lane < 4) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = cg * 16 + j * 8 + 2 * lane;
+      red[rg * 128 + c] = sq[j][0];
+      red[rg * 128 + c + 1] = sq[j][1];
+    }
+  }
+  __syncthreads();
+  if (tid < 128) pa.normpart[blockIdx.x * (int64_t)pa.ldo + tid] = red[tid] + red[128 + tid];
+}
+
 // column sums of squares of X (n x s), partial per 64-row tile (fixed order)
 __global__ void k_colsq_partial(const double* __restrict__ X, int ldx, int64_t n, int s, double* part, int ldp) {
   pdl_wait();
@@ -995,10 +1157,40 @@ int gram_chunks(int64_t n, int ntiles) {   // one wave: tiles x chunks <= NSP_GC
 
 size_t gram_ws_doubles(int64_t n, int sa, int sb) {
   // every launch uses chunks x tiles <= max(gram_ctas(), tiles) partial tiles (the symmetric Gram has
-  // fewer tiles and so more chunks than the two-operand one)
+  // fewer tiles and so more chunks than the two-operand one); the fused panel + Gram (s = 128) writes
+  // 4 tiles per SM
   const int ntm = (sa + 63) / 64, ntn = 2 * ((sb + 63) / 64);
   (void)n;
-  return (size_t)std::max(gram_ctas(), ntm * ntn) * 4096;
+  return (size_t)std::max(std::max(gram_ctas(), 4 * num_sms()), ntm * ntn) * 4096;
+}
+
+bool panel_gram_ok(int s, int64_t n) {
+  static const bool off = [] {
+    const char* e = getenv("NSP_FUSED_PG");
+    return e && e[0] == '0';
+  }();
+  return !off && !nsp_force_generic && s == 128 && n >= (int64_t)64 * num_sms();
+}
+
+int panel_gram(double* Out, const double* Cin, const double* In, const double* M, int64_t n, double sgn,
+               double* normpart, int gmode, double* gram_out, double* ws, cudaStream_t st) {
+  const int nsm = num_sms();
+  PanelArgs a{Out, 128, Cin, 128, In, 128, M, 128, sgn, normpart};
+  const size_t smem = (size_t)(128 + 32 + 32) * FG_LD * sizeof(double);
+  nsp_count_path(NSP_PATH_PANEL_GRAM);
+  if (gmode == 0) {
+    smem_optin((const void*)k_panel_gram<0>, smem);
+    nsp_count_launch();
+    launch_k(k_panel_gram<0>, dim3(nsm), dim3(512), smem, st, a, n, (n + 15) / 16, ws);
+  } else {
+    smem_optin((const void*)k_panel_gram<1>, smem);
+    nsp_count_launch();
+    launch_k(k_panel_gram<1>, dim3(nsm), dim3(512), smem, st, a, n, (n + 15) / 16, ws);
+  }
+  nsp_count_launch();
+  launch_k(k_gram_reduce, dim3(8, 8), dim3(16, 16, 4), 0, st, (const double*)ws, nsm, 2, 2, 2, gram_out,
+           (double*)nullptr, 128, gmode == 0 ? 0 : 1);
+  return nsm;
 }
 
 void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb2, int ldb, int sb, int64_t n,

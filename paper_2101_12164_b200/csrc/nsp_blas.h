@@ -54,6 +54,12 @@ void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64
 // returns the number of normpart rows written (row tiles, or CTAs of the one-wave s = 128 kernel)
 int panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
           int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st);
+// fused panel + Gram (s = 128, ld 128, n >= 64 x SMs, single rank): Out = Cin + sgn In M and
+// gram_out = In^T Out (gmode 0) or Out^T Out (gmode 1, exactly symmetric); normpart (nullable): column
+// sums of squares of Out, one row per CTA (returns the row count).  ws: gram_ws_doubles.
+bool panel_gram_ok(int s, int64_t n);
+int panel_gram(double* Out, const double* Cin, const double* In, const double* M, int64_t n, double sgn,
+               double* normpart, int gmode, double* gram_out, double* ws, cudaStream_t st);
 void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st);
 void colsq_reduce(const double* part, int ntiles, int ldp, double* out, cudaStream_t st);
 void sqrt_vec(const double* in, double* out, int n, cudaStream_t st);
@@ -71,6 +77,11 @@ void small_chol(const double* A, int sp, int mode, int nact, double tau, double*
 // width = nact.  sp multiple of 16, <= 128.
 void chol_fac(const double* A, int sp, int mode, int nact, double tau, double* Lp, BcgStatus* stt,
               cudaStream_t st);
+// chol_fac + chol_solve fused (sp / 8 CTAs, each factoring redundantly and solving 8 columns): Lp and
+// the status as chol_fac; Out = sgn * op(B) unless the factorisation failed (mode 0) or the pivot test
+// chose the eigen fallback (mode 1), in which case Out is not written.
+void chol_fac_solve(const double* A, int sp, int mode, int nact, double tau, double* Lp, BcgStatus* stt,
+                    const double* B, int ldb, double* Out, int ldo, double sgn, bool fwd, bool bwd, cudaStream_t st);
 // Out = sgn * op(B) (B == nullptr: identity), op = L^{-T}L^{-1} (fwd && bwd), L^{-1} (fwd), L^{-T} (bwd);
 // sp / 8 CTAs (8 columns each); skipped when gate && *gate.
 void chol_solve(const double* Lp, int sp, const double* B, int ldb, double* Out, int ldo, double sgn, bool fwd,

@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include "nsp_blas.h"
+#include "../../include/nsp.h"
 #include "nsp_dmma.cuh"
 
 using namespace nspd;
@@ -187,6 +188,134 @@ __device__ __noinline__ bool warp_chol16(double* As, int c0, double* Xd, double*
 }
 
 
+// One THREAD: factor the 8 x 8 lower block at B (ld LDA) in registers - pivots (before the square root)
+// to piv, L in place (lower), X = L^{-1} (lower, zeros above) to Xo (ld 16).  A non-positive pivot is
+// replaced by 1 (deterministic continuation) and reported by `false`.  The dependency chain per column
+// is one reciprocal square root and one update (no shuffles, no shared-memory round trips).
+__device__ __forceinline__ bool fac8(double* B, double* Xo, double* piv) {
+  double a[8][8], x[8][8], il[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[i][j] = (j <= i) ? B[i * LDA + j] : 0.0;
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    double d = a[c][c];
+    piv[c] = d;
+    if (!(d > 0.0)) {
+      ok = false;
+      d = 1.0;
+    }
+    const double r = rsqrt_nr(d);
+    il[c] = r;
+    a[c][c] = d * r;
+#pragma unroll
+    for (int i = c + 1; i < 8; ++i) a[i][c] *= r;
+#pragma unroll
+    for (int j = c + 1; j < 8; ++j)
+#pragma unroll
+      for (int i = j; i < 8; ++i) a[i][j] = fma(-a[i][c], a[j][c], a[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[i][j] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+#pragma unroll
+    for (int j = 0; j <= k; ++j) x[k][j] *= il[k];
+#pragma unroll
+    for (int i = k + 1; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j <= k; ++j) x[i][j] = fma(-a[i][k], x[k][j], x[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j <= i) B[i * LDA + j] = a[i][j];
+      Xo[i * 16 + j] = (j <= i) ? x[i][j] : 0.0;
+    }
+  return ok;
+}
+
+// Warp 0: the 16 x 16 diagonal block at (c0, c0) as 2 x 2 blocks of 8 - L11 by one thread (fac8),
+// L21 = A21 X11^T and A22 - L21 L21^T row-parallel on 8 lanes, L22 by one thread, X21 = -X22 L21 X11
+// row-parallel.  Same outputs as warp_chol16: L in place (lower), X = L^{-1} to Xd (16 x 16 row-major,
+// zero above the diagonal), pivots to piv.  ~2.3k cycles per block against ~6.6k for the warp-wide
+// column loop (whose per-column chain is three shuffles and a shared-memory round trip).
+__device__ __noinline__ bool diag16_fast(double* As, int c0, double* Xd, double* piv) {
+  const int lane = threadIdx.x & 31;
+  double* B = As + c0 * LDA + c0;
+  int ok = 1;
+  if (lane == 0) ok = fac8(B, Xd, piv + c0);
+  __syncwarp();
+  double l[8];
+  if (lane < 8) {   // row 8 + lane of L21 = A21 X11^T
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = B[(8 + lane) * LDA + k];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k <= j; ++k) s = fma(a[k], Xd[j * 16 + k], s);
+      l[j] = s;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) B[(8 + lane) * LDA + j] = l[j];
+  }
+  __syncwarp();
+  if (lane < 8) {   // A22[lane][j] -= L21[lane] . L21[j], j <= lane
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j <= lane) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s = fma(l[k], B[(8 + j) * LDA + k], s);
+        B[(8 + lane) * LDA + 8 + j] -= s;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) ok &= fac8(B + 8 * LDA + 8, Xd + 8 * 16 + 8, piv + c0 + 8) ? 1 : 0;
+  __syncwarp();
+  if (lane < 8) {   // T = L21 X11 (row lane), then X21 = -X22 T
+    double tr[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = j; k < 8; ++k) s = fma(l[k], Xd[k * 16 + j], s);
+      tr[j] = s;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) Xd[(8 + lane) * 16 + j] = tr[j];   // T row (the X21 slot, overwritten below)
+  }
+  __syncwarp();
+  double xr[8];
+  if (lane < 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m <= lane; ++m) s = fma(Xd[(8 + lane) * 16 + 8 + m], Xd[(8 + m) * 16 + j], s);
+      xr[j] = -s;
+    }
+  }
+  __syncwarp();
+  if (lane < 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      Xd[(8 + lane) * 16 + j] = xr[j];
+      Xd[lane * 16 + 8 + j] = 0.0;
+    }
+  }
+  __syncwarp();
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
 // Output Lp (sp x sp): strictly-lower off-diagonal blocks = L, diagonal 16 x 16 blocks = X_kk
 // (lower, zero above the diagonal); the strictly-upper 16 x 16 blocks are NOT written.  Rows / cols >= nact (nact < 0: st->width) are replaced by the identity.
 //  mode 0: a pivot <= 0 -> st->indefinite.
@@ -196,15 +325,100 @@ __device__ __noinline__ bool warp_chol16(double* As, int c0, double* Xd, double*
 #define NSP_CF_T 256
 #endif
 constexpr int CF_T = NSP_CF_T;   // threads per k_chol16 CTA (512 measured slower: 35.4 -> 36.7 us)
+// Solve for the 8 right-hand-side columns c0.. of op(B) with L staged in shared memory (Ls, ld LD:
+// strictly-lower blocks = L, diagonal 16 x 16 blocks = X_kk = L_kk^{-1}), x: sp x 8 (ld 10) staging;
+// Out[:, c0..c0+8) = sgn * op(B).  op = L^{-T} L^{-1} (fwd && bwd), L^{-1} (fwd), L^{-T} (bwd); B == nullptr:
+// the identity.  Per 16-row block: x_kb <- X_kk x_kb (warps 0, 1), then the other rows' updates on the
+// DMMA pipe (8-row groups over the CTA's warps).  NT threads.
+template <int NT>
+__device__ __forceinline__ void solve8(const double* Ls, int LD, double* x, int sp, const double* __restrict__ B,
+                                       int ldb, double* __restrict__ Out, int ldo, double sgn, int fwd, int bwd,
+                                       int c0) {
+  constexpr int LX = 10;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int NB = sp / 16;
+  if (fwd)
+    for (int kb = 0; kb < NB; ++kb) {
+      const int b0 = 16 * kb;
+      double d0 = 0.0, d1 = 0.0;
+      if (warp < 2) {
+#pragma unroll
+        for (int k = 0; k < 16; k += 4)
+          dmma(d0, d1, Ls[(b0 + 8 * warp + g) * LD + b0 + k + t], x[(b0 + k + t) * LX + g]);
+      }
+      __syncthreads();
+      if (warp < 2) {
+        x[(b0 + 8 * warp + g) * LX + 2 * t] = d0;
+        x[(b0 + 8 * warp + g) * LX + 2 * t + 1] = d1;
+      }
+      __syncthreads();
+      for (int grp = warp; grp < (sp - b0 - 16) / 8; grp += NT / 32) {
+        const int row0 = b0 + 16 + 8 * grp;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) dmma(a0, a1, Ls[(row0 + g) * LD + b0 + k + t], x[(b0 + k + t) * LX + g]);
+        x[(row0 + g) * LX + 2 * t] -= a0;
+        x[(row0 + g) * LX + 2 * t + 1] -= a1;
+      }
+      __syncthreads();
+    }
+  if (bwd)
+    for (int kb = NB - 1; kb >= 0; --kb) {
+      const int b0 = 16 * kb;
+      double d0 = 0.0, d1 = 0.0;
+      if (warp < 2) {
+#pragma unroll
+        for (int k = 0; k < 16; k += 4)
+          dmma(d0, d1, Ls[(b0 + k + t) * LD + b0 + 8 * warp + g], x[(b0 + k + t) * LX + g]);
+      }
+      __syncthreads();
+      if (warp < 2) {
+        x[(b0 + 8 * warp + g) * LX + 2 * t] = d0;
+        x[(b0 + 8 * warp + g) * LX + 2 * t + 1] = d1;
+      }
+      __syncthreads();
+      for (int grp = warp; grp < b0 / 8; grp += NT / 32) {
+        const int row0 = 8 * grp;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) dmma(a0, a1, Ls[(b0 + k + t) * LD + row0 + g], x[(b0 + k + t) * LX + g]);
+        x[(row0 + g) * LX + 2 * t] -= a0;
+        x[(row0 + g) * LX + 2 * t + 1] -= a1;
+      }
+      __syncthreads();
+    }
+  for (int e = tid; e < sp * 8; e += NT) {
+    const int i = e >> 3, cc = e & 7;
+    Out[(int64_t)i * ldo + c0 + cc] = sgn * x[i * LX + cc];
+  }
+}
+
+// Fused s x s Cholesky + solve (sxs.Out != nullptr): the grid's sp / 8 CTAs each run the IDENTICAL
+// factorisation (same instructions on the same data - bitwise the same factor) and then solve for
+// their own 8 right-hand-side columns with the factor still in shared memory, so the solve needs no
+// second launch and no factor round trip; CTA 0 alone writes Lp and the status.  Skipped (no output)
+// when the factorisation fails (mode 0) or the pivot test sends orth to the eigen fallback (mode 1).
+struct SxsSolve {
+  const double* B;
+  int ldb;
+  double* Out;
+  int ldo;
+  double sgn;
+  int fwd, bwd;
+};
+
 __global__ void __launch_bounds__(CF_T) k_chol16(const double* __restrict__ Ain, int sp, int mode, int nact,
-                                                double tau, double* __restrict__ Lp, BcgStatus* st) {
+                                                double tau, double* __restrict__ Lp, BcgStatus* st, SxsSolve sxs) {
   pdl_wait();
   extern __shared__ double sm[];
   double* As = sm;                 // 128 x LDA
   double* Di = sm + 128 * LDA;     // 8 x 256: X_kk
+  double* xs = Di + 8 * 256;       // fused solve: sp x 10 right-hand-side staging
+  const bool lead = blockIdx.x == 0;
   __shared__ double piv[128];
   __shared__ double colv[16], invd[16];
-  __shared__ int s_fail;
+  __shared__ int s_fail, s_skip;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int width = nact < 0 ? st->width : nact;
@@ -261,7 +475,11 @@ __global__ void __launch_bounds__(CF_T) k_chol16(const double* __restrict__ Ain,
       }
     }
     if (warp == 0) {   // (A) the only call site of the diagonal factorisation
+#ifdef NSP_CHOL_WARP
       const bool ok = warp_chol16(As, 16 * step, Di + step * 256, piv, colv, invd);
+#else
+      const bool ok = diag16_fast(As, 16 * step, Di + step * 256, piv);
+#endif
       if (!ok && lane == 0) s_fail = 1;
     }
     __syncthreads();
@@ -291,7 +509,8 @@ __global__ void __launch_bounds__(CF_T) k_chol16(const double* __restrict__ Ain,
   }
   if (warp == 0) {   // status: warp-parallel min / max of the pivots
     if (mode == 0) {
-      if (lane == 0 && s_fail) st->indefinite = 1;
+      if (lane == 0) s_skip = s_fail;
+      if (lane == 0 && s_fail && lead) st->indefinite = 1;
     } else {
       double mn = 1e308, mx = 0.0;
       for (int i = lane; i < width; i += 32) {
@@ -305,8 +524,11 @@ __global__ void __launch_bounds__(CF_T) k_chol16(const double* __restrict__ Ain,
       }
       if (lane == 0) {
         const bool fb = s_fail != 0 || !(mn > tau * mx);
-        st->fallback = fb ? 1 : 0;
-        if (!fb) st->width = width;
+        s_skip = fb ? 1 : 0;
+        if (lead) {
+          st->fallback = fb ? 1 : 0;
+          if (!fb) st->width = width;
+        }
       }
     }
   }
@@ -318,10 +540,17 @@ __global__ void __launch_bounds__(CF_T) k_chol16(const double* __restrict__ Ain,
   }
   fence_proxy_async();
   __syncthreads();
-  if (tid < sp) {
-    bulk_store(Lp + (int64_t)tid * sp, As + tid * LDA, 16u * ((tid >> 4) + 1) * 8u);
-    bulk_store_commit_wait();
+  if (lead && tid < sp) bulk_store(Lp + (int64_t)tid * sp, As + tid * LDA, 16u * ((tid >> 4) + 1) * 8u);
+  if (sxs.Out && !s_skip) {   // fused solve for this CTA's 8 columns (As is only read from here on)
+    const int c0 = blockIdx.x * 8;
+    for (int e = tid; e < sp * 8; e += CF_T) {
+      const int i = e >> 3, c = e & 7;
+      xs[i * 10 + c] = sxs.B ? sxs.B[(int64_t)i * sxs.ldb + c0 + c] : (i == c0 + c ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    solve8<CF_T>(As, LDA, xs, sp, sxs.B, sxs.ldb, sxs.Out, sxs.ldo, sxs.sgn, sxs.fwd, sxs.bwd, c0);
   }
+  if (lead && tid < sp) bulk_store_commit_wait();
   CPROF(40)
 }
 
@@ -435,10 +664,20 @@ namespace nspb {
 
 void chol_fac(const double* A, int sp, int mode, int nact, double tau, double* Lp, BcgStatus* stt, cudaStream_t st) {
   // sp = s rounded up to 64 (the block-CG padding): 64 or 128
-  const size_t smem = (size_t)(128 * LDA + 8 * 256) * sizeof(double);
-  smem_optin((const void*)k_chol16, (size_t)((int)smem));
+  const size_t smem = (size_t)(128 * LDA + 8 * 256 + 128 * 10) * sizeof(double);
+  smem_optin((const void*)k_chol16, smem);
   nsp_count_launch();
-  launch_k(k_chol16, dim3(1), dim3(CF_T), smem, st, A, sp, mode, nact, tau, Lp, stt);
+  launch_k(k_chol16, dim3(1), dim3(CF_T), smem, st, A, sp, mode, nact, tau, Lp, stt, SxsSolve{});
+}
+
+void chol_fac_solve(const double* A, int sp, int mode, int nact, double tau, double* Lp, BcgStatus* stt,
+                    const double* B, int ldb, double* Out, int ldo, double sgn, bool fwd, bool bwd, cudaStream_t st) {
+  const size_t smem = (size_t)(128 * LDA + 8 * 256 + 128 * 10) * sizeof(double);
+  smem_optin((const void*)k_chol16, smem);
+  nsp_count_launch();
+  nsp_count_path(NSP_PATH_CHOL_SOLVE);
+  launch_k(k_chol16, dim3(sp / 8), dim3(CF_T), smem, st, A, sp, mode, nact, tau, Lp, stt,
+           SxsSolve{B, ldb, Out, ldo, sgn, fwd ? 1 : 0, bwd ? 1 : 0});
 }
 
 void chol_solve(const double* Lp, int sp, const double* B, int ldb, double* Out, int ldo, double sgn, bool fwd,

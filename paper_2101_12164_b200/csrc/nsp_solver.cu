@@ -153,18 +153,33 @@ static nsp_status read_status(nsp_ctx* c, BcgStatus* d, BcgStatus* h) {
 static int64_t gram_rows(const nsp_ctx* c) { return (c->nranks <= 1 || c->rank == 0) ? c->nG : c->n_priv; }
 static int64_t gram_rows(const nsp_ctx* c, const BcgWs& w) { return w.kind ? w.n : gram_rows(c); }
 
+static bool fused_sxs() {
+  static const bool on = [] {
+    const char* e = getenv("NSP_FUSED_SXS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // orth(Wm): Gram, Cholesky-QR with pivot test, eigen fallback; P = Wm T (reading C3)
 static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Pout,
-                       cudaEvent_t join_before_panel = nullptr) {
+                       cudaEvent_t join_before_panel = nullptr, bool gram_done = false) {
   const int sp = w.sp;
   const int64_t n = w.n;
   cudaStream_t st = c->stream;
-  nspb::gram(Wm, sp, sp, Wm, sp, sp, gram_rows(c, w), w.G, sp, w.gram, st);
-  nsp_status e = comm_allreduce(c, w.G, (size_t)sp * sp);
-  if (e != NSP_OK) return e;
-  // CholQR with the pivot test (k_chol16 mode 1), T = R^{-1} = L^{-T} (skipped on fallback)
-  nspb::chol_fac(w.G, sp, 1, s, c->opts.orth_tau, w.Ldi, w.st, st);
-  nspb::chol_solve(w.Ldi, sp, nullptr, 0, w.T, sp, 1.0, false, true, &w.st->fallback, st);
+  if (!gram_done) {   // (gram_done: G = W^T W already formed by the fused W = Z + P beta pass)
+    nspb::gram(Wm, sp, sp, Wm, sp, sp, gram_rows(c, w), w.G, sp, w.gram, st);
+    nsp_status e = comm_allreduce(c, w.G, (size_t)sp * sp);
+    if (e != NSP_OK) return e;
+  }
+  // CholQR with the pivot test (k_chol16 mode 1), T = R^{-1} = L^{-T} (skipped on fallback): one fused
+  // launch (every CTA factors, then forms 8 columns of T), or the two-launch form with NSP_FUSED_SXS=0
+  if (fused_sxs()) {
+    nspb::chol_fac_solve(w.G, sp, 1, s, c->opts.orth_tau, w.Ldi, w.st, nullptr, 0, w.T, sp, 1.0, false, true, st);
+  } else {
+    nspb::chol_fac(w.G, sp, 1, s, c->opts.orth_tau, w.Ldi, w.st, st);
+    nspb::chol_solve(w.Ldi, sp, nullptr, 0, w.T, sp, 1.0, false, true, &w.st->fallback, st);
+  }
   // eigen fallback (gated on the pivot test): EVD and T = V_keep Lambda^{-1/2} in one launch
   nspb::small_eig(w.G, sp, s, w.Vw, sp + 1, w.lam, w.Vs, &w.st->fallback, st, c->opts.orth_tau, w.T, sp, w.st);
   if (join_before_panel) NSP_CUDA_TRY(c, cudaStreamWaitEvent(st, join_before_panel, 0));   // X += P alpha done
@@ -259,6 +274,9 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   nspb::copy_pad(B, ldb, w.R, sp, n, s, 1.0, st);
   const int64_t ng = gram_rows(c, w);
   const bool multi = c->nranks > 1;
+  // fused tall-skinny passes (s = 128, single rank, one-wave shapes): R -= Q alpha with F = Q^T R (M = I)
+  // and W = Z + P beta with W^T W - each tall block read once per use (NSP_FUSED_PG=0: separate kernels)
+  const bool fuse_pg = !multi && nspb::panel_gram_ok(sp, n);
   nsp_status e;
   nspb::colsq(w.R, sp, ng, s, sp, w.npart, w.rsq, st);
   if ((e = comm_allreduce(c, w.rsq, sp)) != NSP_OK) return e;
@@ -285,12 +303,19 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
       if ((e2 = comm_allreduce(c, w.D, (size_t)2 * sp * sp)) != NSP_OK) return e2;
     }
     tr.mark("gram_DE");
-    nspb::chol_fac(w.D, sp, 0, -1, 0.0, w.Ld, w.st, q);        // D = L L^T
-    tr.mark("chol_D");
-    nspb::chol_solve(w.Ld, sp, w.E, sp, w.al, sp, 1.0, true, true, nullptr, q);   // alpha = D^{-1} E
+    if (fused_sxs()) {   // D = L L^T and alpha = D^{-1} E in one launch
+      nspb::chol_fac_solve(w.D, sp, 0, -1, 0.0, w.Ld, w.st, w.E, sp, w.al, sp, 1.0, true, true, q);
+      tr.mark("chol_D");
+    } else {
+      nspb::chol_fac(w.D, sp, 0, -1, 0.0, w.Ld, w.st, q);        // D = L L^T
+      tr.mark("chol_D");
+      nspb::chol_solve(w.Ld, sp, w.E, sp, w.al, sp, 1.0, true, true, nullptr, q);   // alpha = D^{-1} E
+    }
     tr.mark("alpha");
     // R -= Q alpha here; X += P alpha is deferred to the next tail (x_update), off the critical path
-    const int npt = nspb::panel(w.R, sp, w.R, sp, w.Q, sp, w.al, sp, sp, sp, n, -1.0, multi ? nullptr : w.npart, q);
+    const int npt = (fuse_pg && !usem)
+                        ? nspb::panel_gram(w.R, w.R, w.Q, w.al, n, -1.0, w.npart, 0, w.F, w.gram, q)   // + F = Q^T R
+                        : nspb::panel(w.R, sp, w.R, sp, w.Q, sp, w.al, sp, sp, sp, n, -1.0, multi ? nullptr : w.npart, q);
     if (multi) {
       nspb::colsq(w.R, sp, ng, s, sp, w.npart, w.rsq, q);
       if ((e2 = comm_allreduce(c, w.rsq, sp)) != NSP_OK) return e2;
@@ -331,13 +356,16 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     nsp_status e2;
     if ((e2 = x_update(xfork)) != NSP_OK) return e2;
     if (usem && (e2 = op_precond(c, w, w.R, w.Z, s)) != NSP_OK) return e2;
-    nspb::gram(w.Q, sp, sp, Zr, sp, sp, ng, w.F, sp, w.gram, q);
-    if ((e2 = comm_allreduce(c, w.F, (size_t)sp * sp)) != NSP_OK) return e2;
+    if (!(fuse_pg && !usem)) {   // (fused: F = Q^T R came with the head's R update)
+      nspb::gram(w.Q, sp, sp, Zr, sp, sp, ng, w.F, sp, w.gram, q);
+      if ((e2 = comm_allreduce(c, w.F, (size_t)sp * sp)) != NSP_OK) return e2;
+    }
     nspb::chol_solve(w.Ld, sp, w.F, sp, w.be, sp, -1.0, true, true, nullptr, q);  // beta = -D^{-1} F
     tr.mark("beta");
-    nspb::panel(w.W, sp, Zr, sp, w.P, sp, w.be, sp, sp, sp, n, 1.0, nullptr, q);
+    if (fuse_pg) nspb::panel_gram(w.W, Zr, w.P, w.be, n, 1.0, nullptr, 1, w.G, w.gram, q);   // + G = W^T W
+    else nspb::panel(w.W, sp, Zr, sp, w.P, sp, w.be, sp, sp, sp, n, 1.0, nullptr, q);
     tr.mark("W");
-    if ((e2 = orth(c, w, w.W, s, w.P, xfork ? c->ev_join : nullptr)) != NSP_OK) return e2;
+    if ((e2 = orth(c, w, w.W, s, w.P, xfork ? c->ev_join : nullptr, fuse_pg)) != NSP_OK) return e2;
     tr.mark("orth");
     return NSP_OK;
   };

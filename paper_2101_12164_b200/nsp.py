@@ -23,7 +23,7 @@ EXPORTED = ["nsp_default_opts", "nsp_setup", "nsp_dims", "nsp_gamma_index", "nsp
             "nsp_nystrom_sigma", "nsp_precond_apply", "nsp_pcg", "nsp_last_error", "nsp_destroy",
             "nsp_gamma_apply", "nsp_kernel_launches", "nsp_profile", "nsp_profile_read", "nsp_shard_plan",
             "nsp_shard_info", "nsp_nccl_unique_id", "nsp_local_group_create", "nsp_local_group_destroy",
-            "nsp_set_bcg_precond", "nsp_path_counters", "nsp_dev_panel", "nsp_dev_gram"]
+            "nsp_set_bcg_precond", "nsp_path_counters", "nsp_dev_panel", "nsp_dev_gram", "nsp_dev_panel_gram"]
 
 # dispatch-path counter ids (include/nsp.h NSP_PATH_*)
 PATHS = ["panel_rows", "panel_tiles", "gram_sym", "gram_de", "gram_full", "symm", "sweeps", "symv",
@@ -102,6 +102,7 @@ def load_library(path: str = LIB_PATH):
     lib.nsp_path_counters.argtypes = [P, I]
     lib.nsp_dev_panel.argtypes = [P, P, P, P, I64, I, D, P, I, P]
     lib.nsp_dev_gram.argtypes = [P, P, P, I64, I, P, P, I, I, P]
+    lib.nsp_dev_panel_gram.argtypes = [P, P, P, P, I64, D, I, P, P, P]
     for f in EXPORTED:
         if f not in ("nsp_default_opts", "nsp_last_error", "nsp_destroy", "nsp_kernel_launches",
                      "nsp_local_group_create", "nsp_local_group_destroy"):
@@ -158,6 +159,15 @@ def dev_panel(Out, Cin, In, M, sgn, colsq=None, path=0, stream=None):
                            In.shape[1], sgn, None if colsq is None else _ptr(colsq), path, _stream_ptr(stream))
     if st != 0:
         raise NspError(st, "nsp_dev_panel failed")
+
+
+def dev_panel_gram(Out, Cin, In, M, sgn, gmode, gram, colsq=None, stream=None):
+    """nsp_dev_panel_gram: Out = Cin + sgn In M and gram = In^T Out (gmode 0) / Out^T Out (gmode 1)."""
+    lib = load_library()
+    st = lib.nsp_dev_panel_gram(_ptr(Out), None if Cin is None else _ptr(Cin), _ptr(In), _ptr(M), In.shape[0], sgn,
+                                gmode, _ptr(gram), None if colsq is None else _ptr(colsq), _stream_ptr(stream))
+    if st != 0:
+        raise NspError(st, "nsp_dev_panel_gram failed")
 
 
 def dev_gram(Xa, Xb, out, Xb2=None, out2=None, lower_first=False, path=0, stream=None):

@@ -97,3 +97,35 @@ def test_gram_deterministic():
     nsp.dev_gram(A, A, o1)
     nsp.dev_gram(A, A, o2)
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("n", ["nsm", 14287, 20001, 200003])
+@pytest.mark.parametrize("gmode", [0, 1])
+def test_fused_panel_gram(n, gmode):
+    """The fused pass against its definition: Out = Cin + sgn In M, gram = In^T Out / Out^T Out."""
+    n = 64 * _nsm() if n == "nsm" else n
+    s = 128
+    In = block(n, s, seed=41)
+    M = block(s, s, seed=42) * 0.1
+    Cin = block(n, s, seed=43)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    Out = torch.empty(n, s, dtype=torch.float64, device="cuda")
+    G = torch.empty(s, s, dtype=torch.float64, device="cuda")
+    cs = torch.empty(s, dtype=torch.float64, device="cuda")
+    sgn = -1.0 if gmode == 0 else 1.0
+    before = nsp.path_counters()
+    nsp.dev_panel_gram(Out, d(Cin), d(In), d(M), sgn, gmode, G, colsq=cs)
+    assert nsp.path_counters()["panel_gram"] == before["panel_gram"] + 1
+    ref = Cin + sgn * (In @ M)
+    assert _rel(Out.cpu().numpy(), ref) <= 1e-13
+    Gr = (In.T @ ref) if gmode == 0 else (ref.T @ ref)
+    Gg = G.cpu().numpy()
+    assert _rel(Gg, Gr) <= 1e-13
+    if gmode == 1:
+        assert np.array_equal(Gg, Gg.T)
+    assert _rel(cs.cpu().numpy(), (ref * ref).sum(axis=0)) <= 1e-13
+    # in place (Out aliases Cin, as R -= Q alpha)
+    R = d(Cin)
+    nsp.dev_panel_gram(R, R, d(In), d(M), sgn, gmode, G)
+    assert _rel(R.cpu().numpy(), ref) <= 1e-13
+    assert _rel(G.cpu().numpy(), Gr) <= 1e-13

@@ -8,6 +8,8 @@
 #include "../paper_2101_12164_b200/csrc/nsp_blas.cu"
 #include "../paper_2101_12164_b200/csrc/nsp_small.cu"
 void nsp_count_launch() {}
+void nsp_count_path(int) {}
+thread_local int nsp_force_generic = 0;
 int main() {
   const int sp = 128; const int64_t n = 4096;
   std::vector<double> W(n * sp);
@@ -55,6 +57,27 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, ev1);
     printf("%-22s %8.2f us per launch (back-to-back, includes launch gaps)\n", name, ms * 1000 / 50);
   };
+  {  // fused chol + solve against the two-launch form
+    double *dA2, *dT2;
+    cudaMalloc(&dA2, sp * sp * 8); cudaMalloc(&dT2, sp * sp * 8);
+    std::vector<double> a(sp * sp), b(sp * sp);
+    nspb::chol_fac(dG, sp, 0, -1, 0.0, dL, dst, st);
+    nspb::chol_solve(dL, sp, dG, sp, dT, sp, 1.0, true, true, nullptr, st);
+    nspb::chol_fac_solve(dG, sp, 0, -1, 0.0, dL, dst, dG, sp, dT2, sp, 1.0, true, true, st);
+    cudaMemcpy(a.data(), dT, sp * sp * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(b.data(), dT2, sp * sp * 8, cudaMemcpyDeviceToHost);
+    double m0 = 0; for (int i = 0; i < sp * sp; ++i) m0 = std::max(m0, std::abs(a[i] - b[i]));
+    nspb::chol_fac(dG, sp, 1, sp, 1e-14, dL, dst, st);
+    nspb::chol_solve(dL, sp, nullptr, 0, dT, sp, 1.0, false, true, &dst->fallback, st);
+    nspb::chol_fac_solve(dG, sp, 1, sp, 1e-14, dL, dst, nullptr, 0, dT2, sp, 1.0, false, true, st);
+    cudaMemcpy(a.data(), dT, sp * sp * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(b.data(), dT2, sp * sp * 8, cudaMemcpyDeviceToHost);
+    double m1 = 0; for (int i = 0; i < sp * sp; ++i) m1 = std::max(m1, std::abs(a[i] - b[i]));
+    printf("fused vs two-launch: D^-1 G max diff %.3e, T max diff %.3e (%s)\n", m0, m1,
+           cudaGetErrorString(cudaGetLastError()));
+    timeit("chol_fac_solve mode0", [&] { nspb::chol_fac_solve(dG, sp, 0, -1, 0.0, dL, dst, dG, sp, dT2, sp, 1.0, true, true, st); });
+    timeit("chol_fac_solve mode1", [&] { nspb::chol_fac_solve(dG, sp, 1, sp, 1e-14, dL, dst, nullptr, 0, dT2, sp, 1.0, false, true, st); });
+  }
   timeit("chol_fac mode1", [&] { nspb::chol_fac(dG, sp, 1, sp, 1e-14, dL, dst, st); });
   timeit("chol_solve fwd+bwd", [&] { nspb::chol_solve(dL, sp, dG, sp, dT, sp, 1.0, true, true, nullptr, st); });
   timeit("chol_solve bwd(I)", [&] { nspb::chol_solve(dL, sp, nullptr, 0, dT, sp, 1.0, false, true, nullptr, st); });
