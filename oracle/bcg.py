@@ -42,10 +42,21 @@ def cholesky_pivots(G: np.ndarray):
     return R, piv, True
 
 
-def orth(W: np.ndarray, tau: float = 1e-14):
+def inner_fp64(A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """Block inner product A^T B in fp64 (BLAS)."""
+    return A.T @ B
+
+
+def inner_extended(A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """Block inner product A^T B accumulated in the host's extended precision (x87 80-bit long double),
+    rounded once to fp64 (reading R8: the Gram accuracy the GPU's chunked fixed-order sums reach)."""
+    return (A.astype(np.longdouble).T @ B.astype(np.longdouble)).astype(np.float64)
+
+
+def orth(W: np.ndarray, tau: float = 1e-14, inner=inner_fp64):
     """Rank-revealing orthonormalisation of the direction block (reading C3).
     Returns (P, width, used_fallback)."""
-    G = W.T @ W
+    G = inner(W, W)
     R, piv, ok = cholesky_pivots(G)
     if ok and piv.min() > tau * piv.max():
         # P = W R^{-1}: solve P R = W row by row (R upper triangular)
@@ -60,9 +71,11 @@ def orth(W: np.ndarray, tau: float = 1e-14):
 
 
 def bf_bcg(apply_S, B: np.ndarray, tol: float, maxit: int, apply_M=None, tau: float = 1e-14,
-           X0=None):
+           X0=None, inner=inner_fp64):
     """Breakdown-free block (P)CG of the module docstring (reading C3 step by step,
-    stopping rule reading C4): returns (X, info) with info = iters, status, relres history, widths."""
+    stopping rule reading C4): returns (X, info) with info = iters, status, relres history, widths.
+    inner: the block inner product used for every Gram (P^T Q, P^T R, Q^T Z, W^T W); inner_extended
+    accumulates them in extended precision (reading R8)."""
     B = np.asarray(B, dtype=np.float64)
     n, s = B.shape
     X = np.zeros_like(B) if X0 is None else np.array(X0, dtype=np.float64)
@@ -81,7 +94,7 @@ def bf_bcg(apply_S, B: np.ndarray, tol: float, maxit: int, apply_M=None, tau: fl
         info["status"] = NSP_OK
         return X, info
     Z = apply_M(R) if apply_M is not None else R
-    P, w, fb = orth(Z, tau)
+    P, w, fb = orth(Z, tau, inner)
     info["fallbacks"] += int(fb)
     for _ in range(maxit):
         if w == 0:
@@ -89,12 +102,12 @@ def bf_bcg(apply_S, B: np.ndarray, tol: float, maxit: int, apply_M=None, tau: fl
             return X, info
         info["widths"].append(w)
         Q = apply_S(P)
-        D = P.T @ Q
+        D = inner(P, Q)
         _, _, ok = cholesky_pivots(D)
         if not ok:
             info["status"] = NSP_ERR_INDEFINITE
             return X, info
-        alpha = np.linalg.solve(D, P.T @ R)
+        alpha = np.linalg.solve(D, inner(P, R))
         X = X + P @ alpha
         R = R - Q @ alpha
         info["iters"] += 1
@@ -104,7 +117,7 @@ def bf_bcg(apply_S, B: np.ndarray, tol: float, maxit: int, apply_M=None, tau: fl
             info["status"] = NSP_OK
             return X, info
         Z = apply_M(R) if apply_M is not None else R
-        beta = -np.linalg.solve(D, Q.T @ Z)
-        P, w, fb = orth(Z + P @ beta, tau)
+        beta = -np.linalg.solve(D, inner(Q, Z))
+        P, w, fb = orth(Z + P @ beta, tau, inner)
         info["fallbacks"] += int(fb)
     return X, info

@@ -268,6 +268,110 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __res
     for (int cc = 32 * NQ + lane; cc < ypad; cc += 32) y[(cc >> 5) * ycs + (cc & 31)] = 0.0;
 }
 
+// The same SpMM with 16-byte (double2) loads: lane l owns the column pairs (2l, 2l+1) + 64q, so one
+// warp instruction moves a 512-byte row segment and an s = 128 row takes two loads per nonzero instead
+// of four; the row's nonzeros are consumed two at a time (both gathers in flight before the FMAs).
+// Requires even s and even leading dimensions / chunk strides (16-byte aligned rows).
+template <int NQ2>
+__global__ void __launch_bounds__(256) k_spmm2(int64_t rows, const int32_t* __restrict__ rp,
+                                               const int32_t* __restrict__ ci, const double* __restrict__ va,
+                                               const double* __restrict__ X, int ldx,
+                                               const double* __restrict__ U, int ldu, int64_t ucs, int64_t split,
+                                               double* __restrict__ Y, int ldy, int64_t ycs, int ypad, int s, int mode,
+                                               int zero_pad) {
+  pdl_wait();
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int beg = rp[row], end = rp[row + 1];
+  double2 acc[NQ2];
+#pragma unroll
+  for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
+  // element offset of column pair (2 lane + 64 q) in a layout with 32-column chunks of stride cs
+  auto off = [&](int q, int64_t cs) -> int64_t {
+    const int c = 2 * lane + 64 * q;
+    return (int64_t)(c >> 5) * cs + (c & 31);
+  };
+  auto src_of = [&](int64_t col, double& a, int64_t& cs) -> const double* {
+    if (mode == 0 || mode == 4 || col < split) {
+      if (mode == 2) return nullptr;
+      cs = 32;
+      return X + col * ldx;
+    }
+    if (mode == 3) return nullptr;
+    if (mode == 2) a = -a;
+    cs = ucs;
+    return U + (col - split) * ldu;
+  };
+  for (int base = beg; base < end; base += 32) {
+    const int k = base + lane;
+    const int c = k < end ? ci[k] : 0;
+    const double v = k < end ? va[k] : 0.0;
+    const int cnt = min(32, end - base);
+    int q = 0;
+    for (; q + 1 < cnt; q += 2) {
+      const int64_t c0 = __shfl_sync(0xffffffffu, c, q), c1 = __shfl_sync(0xffffffffu, c, q + 1);
+      double a0 = __shfl_sync(0xffffffffu, v, q), a1 = __shfl_sync(0xffffffffu, v, q + 1);
+      int64_t cs0 = 32, cs1 = 32;
+      const double* s0 = src_of(c0, a0, cs0);
+      const double* s1 = src_of(c1, a1, cs1);
+      double2 x0[NQ2], x1[NQ2];
+#pragma unroll
+      for (int qq = 0; qq < NQ2; ++qq) {
+        const bool in = 2 * lane + 64 * qq < s;
+        x0[qq] = (s0 && in) ? __ldg(reinterpret_cast<const double2*>(s0 + off(qq, cs0))) : make_double2(0.0, 0.0);
+        x1[qq] = (s1 && in) ? __ldg(reinterpret_cast<const double2*>(s1 + off(qq, cs1))) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int qq = 0; qq < NQ2; ++qq) {
+        if (s0) {
+          acc[qq].x = fma(a0, x0[qq].x, acc[qq].x);
+          acc[qq].y = fma(a0, x0[qq].y, acc[qq].y);
+        }
+        if (s1) {
+          acc[qq].x = fma(a1, x1[qq].x, acc[qq].x);
+          acc[qq].y = fma(a1, x1[qq].y, acc[qq].y);
+        }
+      }
+    }
+    if (q < cnt) {
+      const int64_t c0 = __shfl_sync(0xffffffffu, c, q);
+      double a0 = __shfl_sync(0xffffffffu, v, q);
+      int64_t cs0 = 32;
+      const double* s0 = src_of(c0, a0, cs0);
+      if (s0) {
+#pragma unroll
+        for (int qq = 0; qq < NQ2; ++qq) {
+          if (2 * lane + 64 * qq < s) {
+            const double2 x0 = __ldg(reinterpret_cast<const double2*>(s0 + off(qq, cs0)));
+            acc[qq].x = fma(a0, x0.x, acc[qq].x);
+            acc[qq].y = fma(a0, x0.y, acc[qq].y);
+          }
+        }
+      }
+    }
+  }
+  double* y = Y + row * ldy;
+#pragma unroll
+  for (int qq = 0; qq < NQ2; ++qq) {
+    const int cc = 2 * lane + 64 * qq;
+    double2* yc = reinterpret_cast<double2*>(y + off(qq, ycs));
+    if (cc < s) {
+      if (mode == 4) {
+        const double2 o = *yc;
+        *yc = make_double2(o.x + acc[qq].x, o.y + acc[qq].y);
+      } else {
+        *yc = acc[qq];
+      }
+    } else if (zero_pad && cc < ypad) {
+      *yc = make_double2(0.0, 0.0);
+    }
+  }
+  if (zero_pad)
+    for (int cc = 64 * NQ2 + 2 * lane; cc < ypad; cc += 64)
+      *reinterpret_cast<double2*>(y + (int64_t)(cc >> 5) * ycs + (cc & 31)) = make_double2(0.0, 0.0);
+}
+
 // One right-hand side (s = 1): the same modes as k_spmm, G lanes per row (several rows per warp),
 // the lanes take the row's nonzeros in parallel (independent gathers of x) and combine them with a
 // G-lane butterfly (fixed order).  k_spmm's lane-over-columns layout would leave 31 of 32 lanes idle
@@ -1662,6 +1766,22 @@ void spmm_cs(const DevCSR& A, const double* X, int ldx, const double* U, int ldu
   if (s == 1 && ycs == 32 && ucs == 32) {
     const unsigned b8 = (unsigned)((A.rows * 8 + 255) / 256);
     { nsp_count_launch(); launch_k(k_spmv<8>, dim3(b8), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, mode, zero_pad); }
+    return;
+  }
+  static const int vmode = [] {
+    const char* e = getenv("NSP_SPMM_V");
+    return e ? atoi(e) : 2;
+  }();
+  // 16-byte loads when every row segment is 16-byte aligned (even s, even strides)
+  if (vmode == 2 && s % 2 == 0 && ldx % 2 == 0 && ldu % 2 == 0 && ucs % 2 == 0 && ldy % 2 == 0 && ycs % 2 == 0 &&
+      ypad % 2 == 0 && s <= 256) {
+    const int nq2 = (s + 63) / 64;
+    if (nq2 == 1)
+      { nsp_count_launch(); launch_k(k_spmm2<1>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad); }
+    else if (nq2 == 2)
+      { nsp_count_launch(); launch_k(k_spmm2<2>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad); }
+    else
+      { nsp_count_launch(); launch_k(k_spmm2<4>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad); }
     return;
   }
   if (s <= 32)

@@ -22,10 +22,10 @@ def _rhs(pr, d, S):
 @pytest.mark.parametrize("name", NAMES)
 def test_bcg_parity(name):
     """Free-running: iteration count within +-1 and the GPU X meets tol on the oracle's S_G.
-    Equal counts k (reading C16): ||X_gpu - X_oracle|| / ||X_oracle|| <= max(1e-8, 100 * spread_k),
+    Equal counts k (reading C16): ||X_gpu - X_oracle|| / ||X_oracle|| <= max(1e-8, 10 * spread_k),
     spread_k = the oracle's own sensitivity (implicit-solve vs dense S_G evaluation order, same
     algorithm) - block CG on the ill-conditioned configs amplifies 1-ulp perturbations
-    exponentially with k (DESIGN.md "parity tolerances"), so the bound is 1e-8 wherever the
+    exponentially with k (DESIGN.md "Parity tolerances"), so the bound is 1e-8 wherever the
     arithmetic allows it."""
     pr, d, S = problem(name)
     B = _rhs(pr, d, S)
@@ -49,7 +49,7 @@ def test_bcg_parity(name):
         assert rep2["iters"] == k
         diff = relfro(X2.cpu().numpy(), Xk)
         print(f"{name} k={k} gpu-vs-oracle {diff:.2e} oracle spread {spread:.2e}")
-        assert diff <= max(1e-8, 100 * spread), (k, diff, spread)
+        assert diff <= max(1e-8, 10 * spread), (k, diff, spread)
         if spread < 1e-10:   # the rank decisions are determined by the arithmetic here
             assert rep2["widths"] == ik["widths"]
     ctx.close()
@@ -69,27 +69,64 @@ def test_bcg_exact_termination_cfg1():
     ctx.close()
 
 
-def test_bcg_duplicate_and_zero_columns():
-    """a duplicated column drops the active width by one, a zero column stays zero.
-    cfg1 (well-conditioned): with an exactly singular Gram every iteration takes the eigen fallback,
-    and on an ill-conditioned S_G (cfg2s: 132 iterations to 1e-6) the count is rounding-sensitive."""
-    pr, d, S = problem("cfg1")
+@pytest.mark.parametrize("name,tol", [("cfg1", 1e-6), ("cfg2s", 1e-6)])
+def test_bcg_duplicate_and_zero_columns(name, tol):
+    """a duplicated column drops the active width by one (the eigen fallback fires every
+    iteration), a zero column stays zero.  cfg2s at tol 1e-6 runs ~130 iterations past the
+    loss-of-orthogonality point, where the count depends on the accuracy of the Gram inner products
+    (reading R8: the oracle with fp64 BLAS Grams takes 132, with extended-precision Grams 130): the
+    count is checked within +-1 of the extended-precision oracle, and X at equal counts."""
+    from oracle.bcg import inner_extended
+    pr, d, S = problem(name)
     B = block(d.n_gamma, 8)
     B[:, 5] = B[:, 2]
     B[:, 7] = 0.0
-    Xo, io = O.bf_bcg(S.apply, B, 1e-6, 500)
+    Xo, io = O.bf_bcg(S.apply, B, tol, 500)
+    Xe, ie = O.bf_bcg(S.apply, B, tol, 500, inner=inner_extended)
     ctx = context(pr)
     X = torch.zeros(d.n_gamma, 8, dtype=torch.float64, device="cuda")
-    rep = ctx.block_cg(dev(B), X, 1e-6, 500)
-    assert rep["converged"] and abs(rep["iters"] - io["iters"]) <= 1
-    assert rep["widths"][0] == 6
+    rep = ctx.block_cg(dev(B), X, tol, 500)
+    print(f"{name} dup+zero: gpu {rep['iters']}, oracle fp64 Grams {io['iters']}, extended Grams {ie['iters']}")
+    assert rep["converged"] and abs(rep["iters"] - ie["iters"]) <= 1
+    assert rep["widths"][0] == 6 and set(rep["widths"]) == {6}
     Xc = X.cpu().numpy()
     assert np.array_equal(Xc[:, 7], np.zeros(d.n_gamma))
     assert np.allclose(Xc[:, 5], Xc[:, 2], rtol=0, atol=1e-12 * np.abs(Xc).max())
+    true_res = np.linalg.norm(B - S.apply(Xc), axis=0)[:7] / np.linalg.norm(B, axis=0)[:7]
+    assert true_res.max() <= tol * 1.01
+    ctx.close()
+
+
+def test_bcg_long_run_gram_accuracy_cfg2s():
+    """Reading R8 on a long ill-conditioned run (cfg2s, s = 8, tol 1e-6, ~116 iterations): free-running
+    count within +-1 of the oracle with extended-precision Grams (the fp64-BLAS-Gram oracle takes 2
+    more), X at equal counts within max(1e-8, 10 x the oracle's
+    local-vs-dense spread) at k = 20 and k = 100."""
+    from oracle.bcg import inner_extended
+    pr, d, S = problem("cfg2s")
+    B = block(d.n_gamma, 8)
+    _, ie = O.bf_bcg(S.apply, B, 1e-6, 500, inner=inner_extended)
+    _, io = O.bf_bcg(S.apply, B, 1e-6, 500)
+    ctx = context(pr)
+    X = torch.zeros(d.n_gamma, 8, dtype=torch.float64, device="cuda")
+    rep = ctx.block_cg(dev(B), X, 1e-6, 500)
+    print(f"cfg2s s=8 tol 1e-6: gpu {rep['iters']}, oracle fp64 Grams {io['iters']}, extended Grams {ie['iters']}")
+    assert rep["converged"] and abs(rep["iters"] - ie["iters"]) <= 1
+    Sd = S.dense()
+    for k in (20, 100):
+        Xk, _ = O.bf_bcg(S.apply, B, 0.0, k, inner=inner_extended)
+        Xd, _ = O.bf_bcg(lambda V: Sd @ V, B, 0.0, k, inner=inner_extended)
+        X2 = torch.zeros_like(X)
+        ctx.block_cg(dev(B), X2, 0.0, k)
+        diff, spread = relfro(X2.cpu().numpy(), Xk), relfro(Xd, Xk)
+        print(f"  k={k}: gpu-vs-oracle(extended) {diff:.2e}, oracle spread {spread:.2e}")
+        assert diff <= max(1e-8, 10 * spread), (k, diff, spread)
     ctx.close()
 
 
 def test_bcg_s1_matches_cg():
+    """block CG with s = 1 is CG - free-running count within +-1 of the oracle's textbook CG,
+    X at the oracle's count within max(1e-8, 10 x the oracle's own implicit-vs-dense spread)."""
     pr, d, S = problem("cfg2s")
     b = block(d.n_gamma, 1)
     xo, io = O.pcg(lambda v: S.apply(v[:, None])[:, 0], b[:, 0], 1e-8, 1000)
@@ -97,5 +134,13 @@ def test_bcg_s1_matches_cg():
     X = torch.zeros(d.n_gamma, 1, dtype=torch.float64, device="cuda")
     rep = ctx.block_cg(dev(b), X, 1e-8, 1000)
     assert abs(rep["iters"] - io["iters"]) <= 1
-    assert relfro(X.cpu().numpy()[:, 0], xo) <= 1e-7
+    k = io["iters"]
+    Sd = S.dense()
+    xd, _ = O.pcg(lambda v: Sd @ v, b[:, 0], 0.0, k)
+    xk, _ = O.pcg(lambda v: S.apply(v[:, None])[:, 0], b[:, 0], 0.0, k)
+    X2 = torch.zeros_like(X)
+    ctx.block_cg(dev(b), X2, 0.0, k)
+    diff, spread = relfro(X2.cpu().numpy()[:, 0], xk), relfro(xd, xk)
+    print(f"cfg2s s=1: gpu {rep['iters']} its, oracle CG {k}; at k: gpu-vs-oracle {diff:.2e}, spread {spread:.2e}")
+    assert diff <= max(1e-8, 10 * spread), (diff, spread)
     ctx.close()

@@ -44,8 +44,9 @@ def test_panel_matches_definition(idx, path):
         assert _rel(Out.cpu().numpy(), ref) <= 1e-13
     assert _rel(cs.cpu().numpy(), (ref * ref).sum(axis=0)) <= 1e-13 if n else float(cs.abs().max()) == 0.0
     rows = path == 0 and s == 128 and n >= 64 * _nsm()
-    assert after["panel_rows"] - before["panel_rows"] == (1 if rows else 0)
-    assert after["panel_tiles"] - before["panel_tiles"] == (0 if rows else 1)
+    if n:   # (an empty block returns before any dispatch)
+        assert after["panel_rows"] - before["panel_rows"] == (1 if rows else 0)
+        assert after["panel_tiles"] - before["panel_tiles"] == (0 if rows else 1)
     # in place (Out aliases Cin: R -= Q alpha) and without Cin (P = W T)
     R = d(Cin)
     nsp.dev_panel(R, R, d(In), d(M), -1.0, path=path)

@@ -317,6 +317,48 @@ def test_bcg_zero_rhs_and_stagnation():
     assert info["status"] != NSP_OK
 
 
+def test_inner_extended_error_bound():
+    """oracle.bcg.inner_extended (reading R8) against the exact inner product (rational arithmetic): the
+    error obeys the dot-product bound with the EXTENDED unit roundoff, |err| <= n u_ext sum |a_i b_i|
+    + u_64 |exact| (one final rounding), and on a cancellation-heavy case it is far below the fp64 error."""
+    from fractions import Fraction
+    from oracle.bcg import inner_extended
+    u_ext = float(np.finfo(np.longdouble).eps)
+    assert u_ext < 1e-18, "inner_extended needs an extended long double"
+    rng = np.random.default_rng(5)
+    n = 4000
+    a = rng.standard_normal(n) * np.exp(rng.uniform(-5, 5, n))
+    b = rng.standard_normal(n)
+    b[-1] = -(a[:-1] @ b[:-1]) / a[-1]          # heavy cancellation in column 0
+    A, Bm = a[:, None], np.stack([b, np.abs(rng.standard_normal(n))], axis=1)
+    got = inner_extended(A, Bm)[0]
+    f64 = (A.T @ Bm)[0]
+    for j in range(2):
+        exact = float(sum(Fraction(x) * Fraction(y) for x, y in zip(a, Bm[:, j])))
+        mag = float(np.sum(np.abs(a * Bm[:, j])))
+        err = abs(got[j] - exact)
+        assert err <= n * u_ext * mag + np.spacing(abs(exact)), (j, err, n * u_ext * mag)
+        if j == 0:
+            assert err < abs(f64[j] - exact) / 100, (err, abs(f64[j] - exact))
+
+
+def test_bcg_extended_inner_structural_pins():
+    """bf_bcg with extended-precision Grams keeps the exact-arithmetic pins: cfg1 terminates in
+    ceil(n_G/s) iterations with widths 30+30+30+30+7 = n_G; s = 1 is textbook CG."""
+    from oracle.bcg import inner_extended
+    pr = P.make("cfg1")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    S = O.SchurOracle(d)
+    B = S.k_gamma(pr.omega())
+    X, info = O.bf_bcg(S.apply, B, 1e-12, 50, inner=inner_extended)
+    assert info["iters"] <= math.ceil(d.n_gamma / pr.s) and sum(info["widths"]) == d.n_gamma
+    assert np.max(np.abs(X - np.linalg.solve(S.dense(), B))) < 1e-10 * np.abs(X).max()
+    b = B[:, :1]
+    Xb, _ = O.bf_bcg(S.apply, b, 0.0, 10, inner=inner_extended)
+    xc, _ = O.pcg(lambda v: S.apply(v[:, None])[:, 0], b[:, 0], 0.0, 10)
+    assert np.max(np.abs(Xb[:, 0] - xc)) < 1e-10 * np.abs(xc).max()
+
+
 def test_orth_fallback_rank():
     rng = np.random.default_rng(3)
     W = rng.standard_normal((50, 6))
