@@ -195,13 +195,16 @@ nsp_status nsp_gamma_apply(nsp_ctx* ctx, const double* X, double* Y, int s);
 nsp_status nsp_block_cg(nsp_ctx* ctx, const double* B, double* X, int s, double tol, int maxit,
                         void* ws, nsp_report* rep);
 
-/* Alg. 2 steps 1-12 (opts.nys_power = q > 0: first q power steps G <- orth(B_H G), each one block
- * solve; rep->iters = total inner iterations): B = K_G Omega; block CG to tol_inner; Y = A_G X; thin
- * Cholesky-QR2 of Y; C = sym(Omega^T Y); EVD split at eps; T; EVD of T;
+/* Alg. 2 steps 1-12 (opts.nys_power = q > 0: first q power steps G <- orth(B_H G),
+ * each one block solve; rep->iters = total inner iterations): B = K_G Omega; block CG to tol_inner;
+ * Y = A_G X; thin Cholesky-QR2 of Y; C = sym(Omega^T Y); EVD split at eps; T; EVD of T;
  * U~ = Q W(:,1:k); Z = A_G^{-1} U~; keeps (Z, Sigma) in ctx for nsp_pcg.
- * Omega: device n_gamma_local x (rank+oversample). */
-nsp_status nsp_nystrom(nsp_ctx* ctx, int rank, int oversample, const double* Omega, double tol_inner,
-                       int maxit_inner, void* ws, nsp_report* rep);
+ * Omega: device n_gamma_local x (rank+oversample) row-major, or NULL: generated on the device from
+ * `seed` (Philox4x32-10 stream 0, Box-Muller; the row index is the global Gamma index, so it equals
+ * nsp_inputs.philox.gaussian_block(seed, 0, n_gamma, s) up to the last-ulp rounding of log / cos;
+ * reading C7).  NULL is accepted for nys_form 0 / 1 (NSP_ERR_ARG for the M_3 / M_1 forms). */
+nsp_status nsp_nystrom(nsp_ctx* ctx, int rank, int oversample, uint64_t seed, const double* Omega,
+                       double tol_inner, int maxit_inner, void* ws, nsp_report* rep);
 /* sigma: host double[>= rank]; rank_out: approximation rank. */
 nsp_status nsp_nystrom_sigma(const nsp_ctx* ctx, double* sigma, int* rank_out);
 /* Y = M X for M in {0: identity, 1: A_G^{-1}, 2: M_2 (M_1 / M_3 after nys_form 3 / 2),
@@ -262,6 +265,10 @@ nsp_status nsp_dev_gram(const double* Xa, const double* Xb, const double* Xb2, i
 /*  nsp_dev_panel_gram: the fused s = 128 pass (n >= 64 x SMs, else NSP_ERR_ARG): Out = Cin + sgn In M and
  *                 gram = In^T Out (gmode 0: the R -= Q alpha, F = Q^T R pass) or Out^T Out (gmode 1: the
  *                 W = R + P beta, W^T W pass; exactly symmetric); colsq as nsp_dev_panel. */
+/*  nsp_dev_philox_gaussian: out (device rows x s, row-major) = the device Omega generator of nsp_nystrom
+ *                 (Omega == NULL) for the global rows row0 .. row0+rows-1 and Philox stream `stream_id`. */
+nsp_status nsp_dev_philox_gaussian(double* out, int64_t rows, int s, uint64_t seed, unsigned stream_id, int64_t row0,
+                                   void* stream);
 nsp_status nsp_dev_panel_gram(double* Out, const double* Cin, const double* In, const double* M, int64_t n,
                               double sgn, int gmode, double* gram, double* colsq, void* stream);
 

@@ -3,6 +3,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "nsp_comm.h"
 #include "nsp_internal.h"
@@ -301,6 +302,22 @@ nsp_status nsp_dev_panel_gram(double* Out, const double* Cin, const double* In, 
   const cudaError_t e = cudaStreamSynchronize(st);
   cudaFree(ws);
   if (part) cudaFree(part);
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NSP_OK : NSP_ERR_CUDA;
+}
+
+nsp_status nsp_dev_philox_gaussian(double* out, int64_t rows, int s, uint64_t seed, unsigned stream_id, int64_t row0,
+                                   void* stream) {
+  if (!out || rows < 0 || s <= 0 || row0 < 0) return NSP_ERR_ARG;
+  if (rows == 0) return NSP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int64_t> g((size_t)rows);
+  for (int64_t r = 0; r < rows; ++r) g[(size_t)r] = row0 + r;
+  int64_t* dg = nullptr;
+  if (cudaMalloc((void**)&dg, (size_t)rows * 8) != cudaSuccess) return NSP_ERR_CUDA;
+  cudaMemcpy(dg, g.data(), (size_t)rows * 8, cudaMemcpyHostToDevice);
+  nspk::philox_gaussian(out, rows, s, s, dg, seed, stream_id, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(dg);
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NSP_OK : NSP_ERR_CUDA;
 }
 

@@ -92,6 +92,7 @@ struct nsp_ctx {
   std::string err;
 
   std::vector<int64_t> gamma;     // local Gamma row -> original id
+  std::vector<int64_t> gamma_gidx;  // local Gamma row -> global Gamma index (ascending original id)
   std::vector<FacSub> subs;       // host copy
   std::vector<int64_t> sub_n;     // |block j|
 
@@ -262,6 +263,11 @@ void gather_rows(const double* src, int lds, const int32_t* idx, int64_t rows, d
                  double scale, cudaStream_t st);
 void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,
                   bool accumulate, cudaStream_t st);
+// Gaussian block on the device, bit-compatible with nsp_inputs.philox.gaussian_block (reading C7):
+// out[r * ld + j] (j < s; columns s..ld-1 zeroed) = N(0,1) from Philox4x32-10 counter (gidx[r] * s + j,
+// stream, 0), key = seed, Box-Muller cosine branch.  gidx: device int64 row indices.
+void philox_gaussian(double* out, int64_t rows, int s, int ld, const int64_t* gidx, uint64_t seed, uint32_t stream,
+                     cudaStream_t st);
 }  // namespace nspk
 
 #define NSP_CUDA_TRY(ctx, call)                                                   \

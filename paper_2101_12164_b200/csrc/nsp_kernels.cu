@@ -1711,6 +1711,38 @@ __global__ void __launch_bounds__(256) k_spike_update(const double* __restrict__
   }
 }
 
+// Philox4x32-10 (Salmon et al., SC'11; Random123 constants) + the Box-Muller cosine branch, the same
+// stream layout as nsp_inputs/philox.py (reading C7): counter = (e lo, e hi, stream, 0), key = seed.
+__global__ void k_philox_gaussian(double* __restrict__ out, int64_t rows, int s, int ld,
+                                  const int64_t* __restrict__ gidx, uint64_t seed, uint32_t stream) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * ld) return;
+  const int64_t r = i / ld;
+  const int j = (int)(i - r * ld);
+  if (j >= s) {
+    out[i] = 0.0;
+    return;
+  }
+  const uint64_t e = (uint64_t)gidx[r] * (uint64_t)s + (uint64_t)j;
+  uint32_t c0 = (uint32_t)e, c1 = (uint32_t)(e >> 32), c2 = stream, c3 = 0u;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int q = 0; q < 10; ++q) {
+    const uint64_t p0 = 0xD2511F53ull * c0, p1 = 0xCD9E8D57ull * c2;
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0, hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    c0 = hi1 ^ c1 ^ k0;
+    c1 = lo1;
+    c2 = hi0 ^ c3 ^ k1;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const double scale = 1.0 / 9007199254740992.0;   // 2^-53
+  const double u1 = ((double)(((uint64_t)(c0 >> 5)) * 67108864ull + (c1 >> 6)) + 0.5) * scale;
+  const double u2 = ((double)(((uint64_t)(c2 >> 5)) * 67108864ull + (c3 >> 6)) + 0.5) * scale;
+  out[i] = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
+}
+
 // row gather / scatter between an n x s block (ld lds) and a padded buffer (ld ldd):
 // gather: dst[r][c] = idx[r] >= 0 && c < s ? scale * src[idx[r]][c] : 0  for r < rows, c < ldd
 // scatter: dst[idx[r]][c] = src[r][c]   (c < s, idx[r] >= 0)
@@ -1797,6 +1829,14 @@ void spmm_cs(const DevCSR& A, const double* X, int ldx, const double* U, int ldu
 void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split, double* Y,
           int ldy, int s, int mode, bool zero_pad, cudaStream_t st) {
   spmm_cs(A, X, ldx, U, ldu, 32, split, Y, ldy, 32, ldy, s, mode, zero_pad, st);
+}
+
+void philox_gaussian(double* out, int64_t rows, int s, int ld, const int64_t* gidx, uint64_t seed, uint32_t stream,
+                     cudaStream_t st) {
+  const int64_t tot = rows * ld;
+  if (tot <= 0) return;
+  nsp_count_launch();
+  k_philox_gaussian<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(out, rows, s, ld, gidx, seed, stream);
 }
 
 void band_prep(const double* T, int nt, int wb, double* XF, double* GF, double* XB, double* GB, cudaStream_t st) {

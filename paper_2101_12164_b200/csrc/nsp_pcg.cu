@@ -20,6 +20,7 @@
 #include "nsp_blas.h"
 #include "nsp_dmma.cuh"
 #include "nsp_solver.h"
+#include "nsp_comm.h"
 
 using nspd::launch_k;
 using nspd::pdl_wait;
@@ -78,7 +79,8 @@ __global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ pa
     __syncthreads();
   }
   if (threadIdx.x != 0) return;
-  const double v = red[0];
+  // nblk < 0: the sum was formed beforehand (several ranks: summed over ranks) in sc[-nblk - 1]
+  const double v = nblk < 0 ? sc[-nblk - 1] : red[0];
   if (mode == 0) {
     sc[slot] = v;
   } else if (mode == 1) {
@@ -104,6 +106,7 @@ __global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ pa
 // Fixed-order sum of nblk chunk partials (stride 2), evaluated identically by every CTA that needs
 // it: warp 0 loads lane-strided, then a fixed xor tree; the result is broadcast through smem.
 __device__ __forceinline__ double cta_sum_partials(const double* __restrict__ part, int nblk, double* bcast) {
+  if (nblk < 0) return part[0];   // already reduced (several ranks: summed over ranks)
   if (threadIdx.x < 32) {
     double v = 0.0;
     for (int b = threadIdx.x; b < nblk; b += 32) v += part[b * 2];
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(RT) k_pcg_xr_f(double* __restrict__ x, double*
                                                  const double* __restrict__ p, const double* __restrict__ q,
                                                  int64_t n, double* sc, int cur,
                                                  const double* __restrict__ pq_part, int nblk,
-                                                 double* __restrict__ part, BcgStatus* st) {
+                                                 double* __restrict__ part, BcgStatus* st, int64_t ngram) {
   pdl_wait();
   __shared__ double red[RT];
   __shared__ double bc;
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(RT) k_pcg_xr_f(double* __restrict__ x, double*
     x[i] = fma(alpha, p[i], x[i]);
     const double v = fma(-alpha, q[i], r[i]);
     r[i] = v;
-    s = fma(v, v, s);
+    if (i < ngram) s = fma(v, v, s);   // several ranks: the shared rows count on rank 0 only
   }
   red[threadIdx.x] = s;
   __syncthreads();
@@ -300,13 +303,18 @@ static size_t pcg_layout(const nsp_ctx* c, char* base, PcgWs* out) {
 
 size_t pcg_ws_bytes(const nsp_ctx* c) { return pcg_layout(c, nullptr, nullptr); }
 
-// out slot = a . b
-static void dot(nsp_ctx* c, const double* a, const double* b, int64_t n, PcgWs& w, int slot) {
+// Rows that enter inner products: all local rows on one rank; with several ranks the private rows of every
+// rank plus the shared rows once (rank 0), SURVEY.md §8(e) - the shared rows are the trailing local rows.
+static int64_t dot_rows(const nsp_ctx* c) { return (c->nranks <= 1 || c->rank == 0) ? c->nG : c->n_priv; }
+
+// out slot = a . b over the first n rows (several ranks: summed over ranks by one allreduce of the scalar)
+static nsp_status dot(nsp_ctx* c, const double* a, const double* b, int64_t n, PcgWs& w, int slot) {
   const unsigned nb = nblk_of(n);
   nsp_count_launch();
   launch_k(k_dot2_partial, dim3(nb), dim3(RT), 0, c->stream, a, b, nullptr, nullptr, n, w.part);
   nsp_count_launch();
   launch_k(k_dot_reduce, dim3(1), dim3(RT), 0, c->stream, w.part, (int)nb, w.sc, slot, 0, 0.0, w.st, w.hist, PCG_CHUNK);
+  return c->nranks > 1 ? comm_allreduce(c, w.sc + slot, 1) : NSP_OK;
 }
 
 // z = M r for the PCG preconditioner (0: identity copy, 1: A_G^{-1}, 2: M_2)
@@ -318,8 +326,9 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
   }
   // M_2: the low-rank coefficient g = Sigma Z^T r does not depend on A_G^{-1} r, so it runs on a forked
   // side stream (a graph branch when captured) while the A_G solve - a latency-bound chain on a few
-  // SMs - runs on the context stream; z += Z g after the join
-  const bool fork2 = which == 2 && c->nys_rank > 0 && c->side_stream && c->ev_fork && c->ev_join;
+  // SMs - runs on the context stream; z += Z g after the join (one rank: the allreduce of g of several
+  // ranks stays on the context stream)
+  const bool fork2 = which == 2 && c->nys_rank > 0 && c->side_stream && c->ev_fork && c->ev_join && c->nranks == 1;
   if (fork2) {
     NSP_CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
     NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
@@ -360,11 +369,13 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
     launch_k(k_gemv_add, dim3(grid1(n * 32, 256)), dim3(256), 0, c->stream, c->d_Z, kp, w.g, rk, n, z);
   }
   if (which == 2 && c->nys_rank > 0) {
-    const unsigned nch = grid1(n, GT_ROWS);
+    const int64_t ng = dot_rows(c);
+    const unsigned nch = grid1(ng, GT_ROWS);
     nsp_count_launch();
-    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->stream, c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart);
+    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->stream, c->d_Z, c->nys_ld, r, ng, c->nys_rank, w.gpart);
     nsp_count_launch();
     launch_k(k_gemvt_reduce, dim3(1), dim3(1024), 0, c->stream, w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
+    if (c->nranks > 1 && (e = comm_allreduce(c, w.g, c->nys_rank)) != NSP_OK) return e;
     nsp_count_launch();
     launch_k(k_gemv_add, dim3(grid1(n * 32, 256)), dim3(256), 0, c->stream, c->d_Z, c->nys_ld, w.g, c->nys_rank, n, z);
   }
@@ -403,11 +414,17 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
   const int64_t n = c->nG;
   BcgStatus* hs = (BcgStatus*)c->h_status;
   nsp_status e;
+  // several ranks: each rank reduces its own blocks, the S_G applies and A_G^{-1}
+  // (Chebyshev) are sharded with their shared-row allreduce, inner products run over dot_rows and are
+  // summed over ranks; the loop runs eagerly with one status read per iteration
+  const bool multi = c->nranks > 1;
+  const int64_t ng = dot_rows(c);
   // ---- reduction to the border: f = b_G - A_GI A_I^{-1} b_I
   nspk::gather_rows(b, 1, c->d_i1_src, c->i1_rows, w.i1r, 32, 1, 1.0, st);
   nspk::gather_rows(b, 1, c->d_b_src, c->wvu_rows, w.bB, 32, 1, 1.0, st);
   if ((e = interior_boundary_solve(c, w)) != NSP_OK) return e;
   nspk::spmm(c->AGG2, nullptr, 0, w.wvu, 32, n, w.tmp, 1, 1, 2, false, st);      // K-part: A_GI y_B
+  if (multi && (e = finish_shared_rows(c, nullptr, 1, w.tmp, 1, 1, false)) != NSP_OK) return e;
   nspk::gather_rows(b, 1, c->d_g_src, n, w.f, 1, 1, 1.0, st);
   if (n > 0) {
     nsp_count_launch();
@@ -420,7 +437,11 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
   NSP_CUDA_TRY(c, cudaMemcpyAsync(w.st, hs, sizeof(BcgStatus), cudaMemcpyHostToDevice, st));
   NSP_CUDA_TRY(c, cudaMemsetAsync(w.w, 0, (size_t)std::max<int64_t>(n, 1) * 8, st));
   NSP_CUDA_TRY(c, cudaMemcpyAsync(w.r, w.f, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
-  {
+  if (multi) {   // ||f||^2 summed over ranks (slot 5), then the status from it
+    if ((e = dot(c, w.f, w.f, ng, w, 5)) != NSP_OK) return e;
+    nsp_count_launch();
+    launch_k(k_dot_reduce, dim3(1), dim3(RT), 0, st, w.part, -6, w.sc, 4, 2, tol, w.st, w.hist, PCG_CHUNK);
+  } else {
     const unsigned nb = nblk_of(n);
     nsp_count_launch();
     launch_k(k_dot2_partial, dim3(nb), dim3(RT), 0, st, w.f, w.f, nullptr, nullptr, n, w.part);
@@ -435,7 +456,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
   if (!hs->converged) {
     if ((e = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e;
     NSP_CUDA_TRY(c, cudaMemcpyAsync(w.p, w.z, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
-    dot(c, w.r, w.z, n, w, 0);
+    if ((e = dot(c, w.r, w.z, ng, w, 0)) != NSP_OK) return e;
     int cur = 0;
     // one iteration, enqueued; stops itself on the device once st->done is set (converged, p^T S p
     // <= 0, non-finite, or maxit), so PCG_CHUNK iterations run between host status checks and the
@@ -446,11 +467,30 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
       nsp_status e2;
       if ((e2 = apply_into(c, w.p, 1, w.q, 1, 1, 1, w.apply_wvu)) != NSP_OK) return e2;   // q = S_G p
       const unsigned nb = nblk_of(n);
+      if (multi) {   // the same steps with every scalar summed over ranks before use (slots 6, 7, 8)
+        if ((e2 = dot(c, w.p, w.q, ng, w, 6)) != NSP_OK) return e2;                           // p.q
+        nsp_count_launch();
+        launch_k(k_pcg_xr_f, dim3(nb), dim3(RT), 0, q, w.w, w.r, w.p, w.q, n, w.sc, cur, (const double*)(w.sc + 6), -1,
+                 w.part2, w.st, ng);
+        nsp_count_launch();
+        launch_k(k_dot_reduce, dim3(1), dim3(RT), 0, q, w.part2, (int)nb, w.sc, 7, 0, 0.0, w.st, hist_dev, hist_mod);
+        if ((e2 = comm_allreduce(c, w.sc + 7, 1)) != NSP_OK) return e2;                       // r.r
+        nsp_count_launch();
+        launch_k(k_dot_reduce, dim3(1), dim3(RT), 0, q, w.part2, -8, w.sc, 3, 1, tol, w.st, hist_dev, hist_mod);
+        if ((e2 = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e2;
+        if ((e2 = dot(c, w.r, w.z, ng, w, 8)) != NSP_OK) return e2;                           // r.z
+        nsp_count_launch();
+        launch_k(k_pcg_p_f, dim3(grid1(n, RT)), dim3(RT), 0, q, w.p, w.z, n, w.sc, cur, (const double*)(w.sc + 8), -1,
+                 w.st);
+        cur ^= 1;
+        return NSP_OK;
+      }
       // p.q partials; their sum is taken inside k_pcg_xr_f (every CTA, same order)
       nsp_count_launch();
       launch_k(k_dot2_partial, dim3(nb), dim3(RT), 0, q, w.p, w.q, nullptr, nullptr, n, w.part);
       nsp_count_launch();
-      launch_k(k_pcg_xr_f, dim3(nb), dim3(RT), 0, q, w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, (int)nb, w.part2, w.st);
+      launch_k(k_pcg_xr_f, dim3(nb), dim3(RT), 0, q, w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, (int)nb, w.part2, w.st,
+               n);
       nsp_count_launch();
       launch_k(k_dot_reduce, dim3(1), dim3(RT), 0, q, w.part2, (int)nb, w.sc, 3, 1, tol, w.st, hist_dev, hist_mod);
       if ((e2 = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e2;
@@ -463,7 +503,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
       return NSP_OK;
     };
     const char* genv = getenv("NSP_GRAPH");
-    const bool use_graph = !c->prof_on && !(genv && genv[0] == '0');
+    const bool use_graph = !multi && !c->prof_on && !(genv && genv[0] == '0');
     const PcgKey key{w.w, n, precond, tol, maxit, c->nys_rank, c->d_Z, c->d_ELp, c->nys_gen};
     double hbuf[PCG_CHUNK];
     // device-driven loop (default): ONE launch of a graph whose WHILE node repeats the iteration
@@ -599,7 +639,9 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
         NSP_CUDA_TRY(c, cudaGraphLaunch(c->pcg_graph, st));
         nsp_count_launches(c->pcg_graph_kernels);
       } else {
-        for (int j = 0; j < PCG_CHUNK; ++j)
+        // several ranks: one iteration per status read (every rank runs the same collective sequence and
+        // stops on the same, bit-identical, replicated decision)
+        for (int j = 0; j < (multi ? 1 : PCG_CHUNK); ++j)
           if ((e = iteration(st)) != NSP_OK) return e;
       }
       NSP_CUDA_TRY(c, cudaMemcpyAsync(hbuf, w.hist, sizeof(hbuf), cudaMemcpyDeviceToHost, st));
@@ -636,9 +678,12 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
   if ((e = interior_boundary_solve(c, w)) != NSP_OK) return e;                       // y_B in wvu
   nspk::spmm(c->C1, w.i1r, 32, w.wvu, 32, c->i1_rows, w.i1buf, 32, 1, 1, true, st); // r_1 - A_1B y_B
   nspk::tri_fb(c->d_i1sys, c->nsub, w.i1buf, 32, 32, true, true, st, c->i1_wbmax);               // y_1
+  if (multi) NSP_CUDA_TRY(c, cudaMemsetAsync(x, 0, (size_t)c->n * 8, st));
   nspk::scatter_rows(w.i1buf, 32, c->d_i1_src, c->i1_rows, x, 1, 1, false, st);
   nspk::scatter_rows(w.wvu, 32, c->d_b_src, c->wvu_rows, x, 1, 1, false, st);
-  nspk::scatter_rows(w.w, 1, c->d_g_src, n, x, 1, 1, false, st);
+  nspk::scatter_rows(w.w, 1, c->d_g_src, ng, x, 1, 1, false, st);   // shared Gamma rows once (rank 0)
+  // several ranks: every rank wrote its own rows (zero elsewhere); one allreduce assembles x on all ranks
+  if (multi && (e = comm_allreduce(c, x, (size_t)c->n)) != NSP_OK) return e;
   NSP_CUDA_TRY(c, cudaStreamSynchronize(st));
   NSP_CUDA_TRY(c, cudaGetLastError());
   if (rep) {
@@ -660,8 +705,8 @@ extern "C" nsp_status nsp_pcg(nsp_ctx* c, const double* b, double* x, double tol
     if (c) c->err = "nsp_pcg: bad arguments (precond in {0, 1, 2, 3})";
     return NSP_ERR_ARG;
   }
-  if (c->nranks != 1) {
-    c->err = "nsp_pcg: multi-rank full solve not built";
+  if (c->nranks != 1 && precond == 3) {
+    c->err = "nsp_pcg: M_A-DEF2 (precond 3) is single-rank";
     return NSP_ERR_STATE;
   }
   if (precond >= 1 && !c->has_ag) {

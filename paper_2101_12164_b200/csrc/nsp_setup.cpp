@@ -189,15 +189,25 @@ static double tridiag_count_below(const std::vector<double>& al, const std::vect
   return cnt;
 }
 
+// glist: the Gamma rows the spectrum bounds are taken over, gpos: original id -> position in glist.  One
+// rank: the local rows.  Several ranks: the GLOBAL Gamma set (every rank derives the same bounds and
+// coefficients - the polynomial is one operator on the whole border; its applications are sharded).
 static nsp_status setup_gamma_cheb(nsp_ctx* c, const nsp_csr* A, const int32_t* part,
-                                   const std::vector<int32_t>& gpos) {
-  const int64_t nG = c->nG;
+                                   const std::vector<int32_t>& gpos_local, const std::vector<int64_t>* glist_in = nullptr) {
+  std::vector<int32_t> gpos_glob;
+  const std::vector<int64_t>& glist = glist_in ? *glist_in : c->gamma;
+  if (glist_in) {
+    gpos_glob.assign(A->n, -1);
+    for (size_t g = 0; g < glist.size(); ++g) gpos_glob[glist[g]] = (int32_t)g;
+  }
+  const std::vector<int32_t>& gpos = glist_in ? gpos_glob : gpos_local;
+  const int64_t nG = (int64_t)glist.size();
   const int64_t* rp = A->rowptr;
   const int32_t* ci = A->colidx;
   const double* va = A->val;
   std::vector<int64_t> grp(nG + 1, 0);
   for (int64_t g = 0; g < nG; ++g) {
-    const int64_t v = c->gamma[g];
+    const int64_t v = glist[g];
     int64_t k = 0;
     for (int64_t q = rp[v]; q < rp[v + 1]; ++q)
       if (part[ci[q]] < 0) ++k;
@@ -208,7 +218,7 @@ static nsp_status setup_gamma_cheb(nsp_ctx* c, const nsp_csr* A, const int32_t* 
   double gersh = 0.0;
 #pragma omp parallel for schedule(static) reduction(max : gersh)
   for (int64_t g = 0; g < nG; ++g) {
-    const int64_t v = c->gamma[g];
+    const int64_t v = glist[g];
     int64_t k = grp[g];
     double rs = 0.0;
     for (int64_t q = rp[v]; q < rp[v + 1]; ++q)
@@ -582,9 +592,10 @@ extern "C" nsp_status nsp_setup(const nsp_csr* A, const int32_t* part, int K, co
   c->stream = (cudaStream_t)c->opts.stream;
   c->nranks = c->opts.nranks > 0 ? c->opts.nranks : 1;
   c->rank = c->opts.rank;
-  if (c->nranks > 1 && (c->opts.factor_gamma || c->opts.bcg_precond))
-    return fail(c, NSP_ERR_ARG, "nsp_setup: the A_G factor (M = A_G^{-1}, M_2, PCG) is single-rank in this "
-                                "version; multi-rank runs use bcg_precond = 0 (reading C2)");
+  if (c->nranks > 1 && (c->opts.factor_gamma || c->opts.bcg_precond) &&
+      (c->opts.ag_solver == 1 || c->opts.nys_form != 0))
+    return fail(c, NSP_ERR_ARG, "nsp_setup: with several ranks A_G^{-1} is the sharded Chebyshev operator "
+                                "(ag_solver 0 / 2) and nys_form must be 0");
   nsp_status vs = validate_inputs(c, A, part, K);   // host-only: errors reported without a device
   if (vs != NSP_OK) return vs;
   NSP_CUDA_TRY(c, cudaSetDevice(c->device));
@@ -694,6 +705,16 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   }
   c->nG = (int64_t)c->gamma.size();
   c->nG_global = nG_global;
+  {   // global Gamma index (position in ascending original id) of every local row: the row index of a
+      // device-generated Omega (nsp_nystrom with Omega == NULL; reading C7)
+    std::vector<int64_t> gall;
+    gall.reserve((size_t)nG_global);
+    for (int64_t i = 0; i < n; ++i)
+      if (part[i] < 0) gall.push_back(i);
+    c->gamma_gidx.resize(c->gamma.size());
+    for (size_t g = 0; g < c->gamma.size(); ++g)
+      c->gamma_gidx[g] = std::lower_bound(gall.begin(), gall.end(), c->gamma[g]) - gall.begin();
+  }
   c->n_priv = (int64_t)plan.priv.size();
   c->blk0 = B0;
   c->nsub = KL;
@@ -1230,11 +1251,20 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   double t_ag = 0.0;
   if (c->opts.factor_gamma) {
     auto t3 = Clock::now();
-    nsp_status sg = c->opts.ag_solver == 2 ? NSP_ERR_OOM : setup_gamma_factor(c, A, part, gpos, rep);
-    if (sg == NSP_ERR_OOM && c->opts.ag_solver != 1 && c->nranks == 1) {
-      (void)cudaGetLastError();
-      sg = setup_gamma_cheb(c, A, part, gpos);
-      if (sg == NSP_OK) c->err.clear();
+    nsp_status sg;
+    if (c->nranks > 1) {   // sharded: the Chebyshev polynomial of the global A_G, applied on local rows
+      std::vector<int64_t> gall;
+      gall.reserve((size_t)c->nG_global);
+      for (int64_t i = 0; i < A->n; ++i)
+        if (part[i] < 0) gall.push_back(i);
+      sg = setup_gamma_cheb(c, A, part, gpos, &gall);
+    } else {
+      sg = c->opts.ag_solver == 2 ? NSP_ERR_OOM : setup_gamma_factor(c, A, part, gpos, rep);
+      if (sg == NSP_ERR_OOM && c->opts.ag_solver != 1) {
+        (void)cudaGetLastError();
+        sg = setup_gamma_cheb(c, A, part, gpos);
+        if (sg == NSP_OK) c->err.clear();
+      }
     }
     if (sg != NSP_OK) return sg;
     t_ag = ms_since(t3);

@@ -635,6 +635,10 @@ static nsp_status ag_cheb(nsp_ctx* c, const double* X, int ldx, double* Y, int l
   NSP_CUDA_TRY(c, cudaMemsetAsync(xw, 0, blk * 8, st));
   for (int k = 0; k < c->cheb_K; ++k) {
     nspk::spmm(c->AGG2, d0, ld, nullptr, 0, n, t, ld, s, 3, true, st);   // t = A_G d
+    if (c->nranks > 1) {   // shared rows: sum the per-rank partials, add the shared x shared term
+      nsp_status e = finish_shared_rows(c, d0, ld, t, ld, s, true);
+      if (e != NSP_OK) return e;
+    }
     nspb::cheb_update(xw, r, d0, t, d1, c->cheb_c1[k], c->cheb_c2[k], (int64_t)n * ld, k + 1 < c->cheb_K, st);
     std::swap(d0, d1);
   }
@@ -710,7 +714,11 @@ nsp_status m2_apply(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, in
   if (c->nys_rank > 0) {
     // G = Z^T X (nys_ld x sp), G <- diag(sigma) G, Y += Z G
     const int sp = ((s + 63) / 64) * 64;
-    nspb::gram(c->d_Z, c->nys_ld, c->nys_ld, X, ldx, sp, c->nG, gsm, sp, gws, c->stream);
+    nspb::gram(c->d_Z, c->nys_ld, c->nys_ld, X, ldx, sp, gram_rows(c), gsm, sp, gws, c->stream);
+    if (c->nranks > 1) {
+      e = comm_allreduce(c, gsm, (size_t)c->nys_ld * sp);
+      if (e != NSP_OK) return e;
+    }
     nspb::scale_rows(gsm, sp, c->d_sigma, c->nys_rank, c->nys_ld, sp, c->stream);
     PanelArgs pa{Y, ldy, Y, ldy, c->d_Z, c->nys_ld, gsm, sp, 1.0, nullptr};
     nspb::panel2(pa, nullptr, c->nys_ld, sp, c->nG, c->stream);
@@ -745,11 +753,15 @@ nsp_status nsp_block_cg(nsp_ctx* c, const double* B, double* X, int s, double to
 
 // Alg. 2 with readings C1 (border system), C5 (U~ = Q W), C6 (symmetrised C,
 // eps split, descending T eigenpairs, rank = min(r, k)).
-nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega, double tol_inner, int maxit_inner,
-                       void* ws, nsp_report* rep) {
+nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, const double* Omega, double tol_inner,
+                       int maxit_inner, void* ws, nsp_report* rep) {
   const int s = rank + oversample;
-  if (!c || !Omega || rank <= 0 || oversample < 0 || s > 128 || maxit_inner < 0) {
+  if (!c || rank <= 0 || oversample < 0 || s > 128 || maxit_inner < 0) {
     if (c) c->err = "nsp_nystrom: bad arguments (rank > 0, rank + oversample <= 128)";
+    return NSP_ERR_ARG;
+  }
+  if (!Omega && (c->opts.nys_form == 2 || c->opts.nys_form == 3)) {
+    c->err = "nsp_nystrom: the M_3 / M_1 forms take an explicit Omega (device generation covers the Gamma-indexed forms)";
     return NSP_ERR_ARG;
   }
   if (!c->has_ag) {
@@ -767,6 +779,10 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
     c->err = "nsp_nystrom: the M_1 form (nys_form 3) is single-rank";
     return NSP_ERR_STATE;
   }
+  // several ranks (form 0): every Gram is summed over the private rows of every rank plus the shared rows
+  // once (gram_rows) and allreduced; the s x s steps are then replicated bit-identically; A_G X completes
+  // its shared rows with one allreduce; A_G^{-1} is the sharded Chebyshev operator
+  const bool multi = c->nranks > 1;
   if ((form == 1 || form == 2) && (c->nranks != 1 || c->AII.rows == 0)) {
     c->err = "nsp_nystrom: the S_I forms need opts.nys_form set at nsp_setup (single rank)";
     return NSP_ERR_STATE;
@@ -822,8 +838,13 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
     const double* Qin = Yin;
     double* Qout = QA;
     int passes = 2;
+    const int64_t ngr = (multi && nr == n) ? gram_rows(c) : nr;
     for (int pass = 0; pass < passes; ++pass) {
-      nspb::gram(Qin, sp, sp, Qin, sp, sp, nr, G, sp, w.gram, st);
+      nspb::gram(Qin, sp, sp, Qin, sp, sp, ngr, G, sp, w.gram, st);
+      if (multi) {
+        nsp_status ea = comm_allreduce(c, G, sm);
+        if (ea != NSP_OK) return ea;
+      }
       nspb::small_chol(G, sp, 2, s, 0.0, Rk, w.st, st);
       if (pass == 0) {
         nsp_status e2 = read_status(c, w.st, hs);
@@ -861,7 +882,15 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
     return NSP_OK;
   };
   // G = Omega; q power steps G <- orth(B_H G) (eq:power PAPER.md:204-212), then Alg. 2 steps 1-4 on G
-  nspb::copy_pad(Omega, s, Om, sp, n, s, 1.0, st);
+  if (Omega) {
+    nspb::copy_pad(Omega, s, Om, sp, n, s, 1.0, st);
+  } else {   // Omega generated on the device: Philox stream 0 at the rows' global Gamma indices (reading C7)
+    int64_t* dg = nullptr;
+    NSP_CUDA_TRY(c, cudaMallocAsync((void**)&dg, (size_t)std::max<int64_t>(n, 1) * 8, st));
+    NSP_CUDA_TRY(c, cudaMemcpyAsync(dg, c->gamma_gidx.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    nspk::philox_gaussian(Om, n, s, sp, dg, seed, 0u, st);
+    NSP_CUDA_TRY(c, cudaFreeAsync(dg, st));
+  }
   const int q = c->opts.nys_power > 0 ? c->opts.nys_power : 0;
   nsp_report brep{};
   int total_iters = 0;
@@ -926,6 +955,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
     total_iters += brep.iters;
     // step 4: Y = A_G X  (M_1: Y = R_G^{-T} A_G X, in R_G's row space)
     nspk::spmm(c->AGG2, Xn, sp, nullptr, 0, n, Y, sp, s, 3, true, st);
+    if (multi && (e = finish_shared_rows(c, Xn, sp, Y, sp, s, true)) != NSP_OK) return e;
     if (form == 3 && (e = ag_tri(c, Y, sp, true, Y, sp, false, s, true, false, w.wvu)) != NSP_OK) return e;
     if (pw < q) {   // power step: G <- orthonormal basis of Y
       const double* Qp = nullptr;
@@ -942,7 +972,8 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
   const double* Q = nullptr;
   if ((e = (form == 2 ? cholqr(Ys, &Q, nY, Qa2, Qb2) : cholqr(Ys, &Q))) != NSP_OK) return e;
   // step 6: C = Omega^T Y, symmetrised (reading C6)
-  nspb::gram(Gs, sp, sp, Ys, sp, sp, nY, C, sp, w.gram, st);
+  nspb::gram(Gs, sp, sp, Ys, sp, sp, multi ? gram_rows(c) : nY, C, sp, w.gram, st);
+  if (multi && (e = comm_allreduce(c, C, sm)) != NSP_OK) return e;
   nspb::small_sym(C, s, sp, 0.0, st);
   // step 7: EVD of C, split at eps = nys_eps_rel * lambda_max
   nspb::small_eig(C, sp, s, Vw, sp + 1, lamC, VC, nullptr, st);
@@ -1003,7 +1034,8 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, const double* Omega
     {
       double* SZ = Qa;    // n x kp scratch (reuse)
       if ((e = apply_into(c, c->d_Z, kp, SZ, kp, rk, 1, w.wvu)) != NSP_OK) return e;
-      nspb::gram(c->d_Z, kp, kp, SZ, kp, kp, n, G, kp, w.gram, st);
+      nspb::gram(c->d_Z, kp, kp, SZ, kp, kp, multi ? gram_rows(c) : n, G, kp, w.gram, st);
+      if (multi && (e = comm_allreduce(c, G, (size_t)kp * kp)) != NSP_OK) return e;
       nspb::small_sym(G, rk, kp, 0.0, st);
       if (c->d_ELp) cudaFree(c->d_ELp);
       c->d_ELp = nullptr;

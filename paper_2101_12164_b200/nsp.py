@@ -23,7 +23,8 @@ EXPORTED = ["nsp_default_opts", "nsp_setup", "nsp_dims", "nsp_gamma_index", "nsp
             "nsp_nystrom_sigma", "nsp_precond_apply", "nsp_pcg", "nsp_last_error", "nsp_destroy",
             "nsp_gamma_apply", "nsp_kernel_launches", "nsp_profile", "nsp_profile_read", "nsp_shard_plan",
             "nsp_shard_info", "nsp_nccl_unique_id", "nsp_local_group_create", "nsp_local_group_destroy",
-            "nsp_set_bcg_precond", "nsp_path_counters", "nsp_dev_panel", "nsp_dev_gram", "nsp_dev_panel_gram"]
+            "nsp_set_bcg_precond", "nsp_path_counters", "nsp_dev_panel", "nsp_dev_gram", "nsp_dev_panel_gram",
+            "nsp_dev_philox_gaussian"]
 
 # dispatch-path counter ids (include/nsp.h NSP_PATH_*)
 PATHS = ["panel_rows", "panel_tiles", "gram_sym", "gram_de", "gram_full", "symm", "sweeps", "symv",
@@ -78,7 +79,7 @@ def load_library(path: str = LIB_PATH):
     lib.nsp_schur_apply.argtypes = [P, P, P, I, P]
     lib.nsp_kgamma_apply.argtypes = [P, P, P, I, P]
     lib.nsp_block_cg.argtypes = [P, P, P, I, D, I, P, P]
-    lib.nsp_nystrom.argtypes = [P, I, I, P, D, I, P, P]
+    lib.nsp_nystrom.argtypes = [P, I, I, C.c_uint64, P, D, I, P, P]
     lib.nsp_nystrom_sigma.argtypes = [P, P, P]
     lib.nsp_precond_apply.argtypes = [P, I, P, P, I, P]
     lib.nsp_pcg.argtypes = [P, P, P, D, I, I, P, P]
@@ -103,6 +104,7 @@ def load_library(path: str = LIB_PATH):
     lib.nsp_dev_panel.argtypes = [P, P, P, P, I64, I, D, P, I, P]
     lib.nsp_dev_gram.argtypes = [P, P, P, I64, I, P, P, I, I, P]
     lib.nsp_dev_panel_gram.argtypes = [P, P, P, P, I64, D, I, P, P, P]
+    lib.nsp_dev_philox_gaussian.argtypes = [P, I64, I, C.c_uint64, C.c_uint, I64, P]
     for f in EXPORTED:
         if f not in ("nsp_default_opts", "nsp_last_error", "nsp_destroy", "nsp_kernel_launches",
                      "nsp_local_group_create", "nsp_local_group_destroy"):
@@ -168,6 +170,14 @@ def dev_panel_gram(Out, Cin, In, M, sgn, gmode, gram, colsq=None, stream=None):
                                 gmode, _ptr(gram), None if colsq is None else _ptr(colsq), _stream_ptr(stream))
     if st != 0:
         raise NspError(st, "nsp_dev_panel_gram failed")
+
+
+def dev_philox_gaussian(out, seed, stream_id=0, row0=0, stream=None):
+    """nsp_dev_philox_gaussian: the device Omega generator into out (rows x s)."""
+    st = load_library().nsp_dev_philox_gaussian(_ptr(out), out.shape[0], out.shape[1], seed, stream_id, row0,
+                                                _stream_ptr(stream))
+    if st != 0:
+        raise NspError(st, "nsp_dev_philox_gaussian failed")
 
 
 def dev_gram(Xa, Xb, out, Xb2=None, out2=None, lower_first=False, path=0, stream=None):
@@ -331,14 +341,16 @@ class Context:
         self._check(st)
         return _report(rep, hist, widths)
 
-    def nystrom(self, rank, oversample, Omega, tol_inner, maxit_inner, ws=None):
+    def nystrom(self, rank, oversample, Omega, tol_inner, maxit_inner, ws=None, seed=0):
+        """nsp_nystrom; Omega None -> generated on the device from `seed` (reading C7)."""
         cap = maxit_inner + 1
         hist = (C.c_double * cap)()
         widths = (C.c_int * cap)()
         rep = nsp_report()
         rep.hist, rep.hist_cap = C.addressof(hist), cap
         rep.widths, rep.widths_cap = C.addressof(widths), cap
-        st = self.lib.nsp_nystrom(self.ctx, rank, oversample, _ptr(Omega), tol_inner, maxit_inner,
+        st = self.lib.nsp_nystrom(self.ctx, rank, oversample, seed, None if Omega is None else _ptr(Omega),
+                                  tol_inner, maxit_inner,
                                   None if ws is None else ws.data_ptr(), C.byref(rep))
         self._check(st)
         r = _report(rep, hist, widths)

@@ -130,3 +130,20 @@ def test_fused_panel_gram(n, gmode):
     nsp.dev_panel_gram(R, R, d(In), d(M), sgn, gmode, G)
     assert _rel(R.cpu().numpy(), ref) <= 1e-13
     assert _rel(G.cpu().numpy(), Gr) <= 1e-13
+
+
+@pytest.mark.parametrize("seed,stream_id,row0,rows,s", [(0, 0, 0, 4096, 30), (7, 9, 123457, 1000, 128),
+                                                        (2**40 + 3, 1, 10**9, 64, 1)])
+def test_device_philox_matches_host_generator(seed, stream_id, row0, rows, s):
+    """Reading C7: the device Omega generator equals nsp_inputs.philox (counter (e, stream, 0), key seed,
+    Box-Muller cosine branch) up to the last-ulp rounding of log / cos (<= 4 ulp); row0 = 0 is exactly
+    philox.gaussian_block."""
+    from nsp_inputs import philox
+    out = torch.empty(rows, s, dtype=torch.float64, device="cuda")
+    nsp.dev_philox_gaussian(out, seed, stream_id, row0)
+    u1, u2 = philox._uniform_pair(philox._raw(seed, stream_id, row0 * s, rows * s))
+    ref = (np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)).reshape(rows, s)
+    if row0 == 0:
+        assert np.array_equal(ref, philox.gaussian_block(seed, stream_id, rows, s))
+    got = out.cpu().numpy()
+    assert np.all(np.abs(got - ref) <= 4 * np.spacing(np.abs(ref)) + 1e-300)

@@ -97,3 +97,87 @@ def test_multirank_block_cg_matches_single_rank(name, G):
         assert true_res.max() <= pr.tol_bcg * 1.001
     print(f"{name} G={G}: {rep1['iters']} its, shared rows {res[0]['B'].shape[0] - res[0]['npv']}, "
           f"X vs 1 rank {relfro(Xg, X1):.1e}")
+
+
+def _run_ranks_method(pr, d, G, Om, b, tol_pcg):
+    """Every rank: block CG with M = A_G^{-1} (sharded Chebyshev), the Nystrom step (Alg. 2) and the outer
+    PCG with M_2 on the full system (precond 2), all through the sharded code path."""
+    grp = nsp.LocalGroup(G)
+    res = [None] * G
+    errs = []
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                ctx = Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, device=0,
+                              stream=stream.cuda_stream, nranks=G, rank=r, local_group=grp, factor_gamma=True,
+                              ag_solver=2)
+                pos = np.searchsorted(d.gamma, ctx.gamma_index())
+                Bl = torch.empty(pos.size, Om.shape[1], dtype=torch.float64, device="cuda")
+                ctx.kgamma_apply(dev(Om[pos]), Bl)
+                ctx.set_bcg_precond(1)
+                Xl = torch.zeros_like(Bl)
+                repm = ctx.block_cg(Bl, Xl, pr.tol_bcg, 500)
+                ctx.set_bcg_precond(0)
+                rn = ctx.nystrom(pr.rank, pr.oversample, dev(Om[pos]), pr.tol_bcg, 500)
+                sig = ctx.nystrom_sigma()
+                x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
+                rp = ctx.pcg(dev(b), x, tol_pcg, 3000, precond=2)
+                stream.synchronize()
+                res[r] = dict(pos=pos, npv=ctx.n_private, Xm=Xl.cpu().numpy(), repm=repm, rn=rn, sig=sig,
+                              x=x.cpu().numpy(), rp=rp)
+                ctx.close()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append((r, repr(e)))
+
+    th = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in th), "rank threads hung"
+    assert not errs, errs
+    grp.close()
+    return res
+
+
+@pytest.mark.parametrize("name,G", [("cfg2s", 2), ("cfg5s", 4), ("cfg2s", 8)])
+def test_multirank_nystrom_pcg_matches_single_rank(name, G):
+    """SURVEY.md §8(e) "What stays replicated": the s x s steps and the Nystrom EVDs replicated, A_G^{-1}
+    (here the Chebyshev operator of the global A_G, reading R7) and the outer PCG's S_G apply sharded.
+    Against the single-rank run of the same operators: block-CG (M = A_G^{-1}) and Nystrom inner counts
+    equal, Sigma within 1e-8, PCG count within +-1, x within 1e-8 and bitwise identical on every rank."""
+    pr, d, S = problem(name)
+    Om = pr.omega()
+    b = pr.rhs()
+    tol_pcg = pr.tol_pcg or 1e-8
+    ctx1 = context(pr, factor_gamma=True, ag_solver=2)
+    B = S.k_gamma(Om)
+    ctx1.set_bcg_precond(1)
+    X1 = torch.zeros(d.n_gamma, pr.s, dtype=torch.float64, device="cuda")
+    repm1 = ctx1.block_cg(dev(B), X1, pr.tol_bcg, 500)
+    ctx1.set_bcg_precond(0)
+    rn1 = ctx1.nystrom(pr.rank, pr.oversample, dev(Om), pr.tol_bcg, 500)
+    sig1 = ctx1.nystrom_sigma()
+    x1 = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
+    rp1 = ctx1.pcg(dev(b), x1, tol_pcg, 3000, precond=2)
+    x1 = x1.cpu().numpy()
+    ctx1.close()
+    res = _run_ranks_method(pr, d, G, Om, b, tol_pcg)
+    Xg = np.zeros((d.n_gamma, pr.s))
+    for r in range(G):
+        q = res[r]
+        assert q["repm"]["iters"] == repm1["iters"], (r, q["repm"]["iters"], repm1["iters"])
+        Xg[q["pos"]] = q["Xm"]
+        assert q["rn"]["iters"] == rn1["iters"] and q["rn"]["rank"] == rn1["rank"]
+        assert np.max(np.abs(q["sig"] - sig1) / np.abs(sig1)) <= 1e-8
+        assert abs(q["rp"]["iters"] - rp1["iters"]) <= 1, (r, q["rp"]["iters"], rp1["iters"])
+        assert np.array_equal(q["x"], res[0]["x"])          # assembled x bitwise identical on every rank
+    assert relfro(Xg, X1.cpu().numpy()) <= 1e-8
+    assert relfro(res[0]["x"], x1) <= 1e-8
+    A = pr.A.to_scipy()
+    assert np.linalg.norm(b - A @ res[0]["x"]) / np.linalg.norm(b) <= 1e-7
+    print(f"{name} G={G}: bcg(M=A_G^-1) {repm1['iters']} its, Nystrom {rn1['iters']} inner its, "
+          f"PCG {rp1['iters']} / {res[0]['rp']['iters']} its, x vs 1 rank {relfro(res[0]['x'], x1):.1e}")

@@ -351,3 +351,17 @@ def test_m1_rcm_factor_pcg_cfg5s():
         its[order] = rp["iters"]
         ctx.close()
     assert abs(its[0] - its[1]) <= max(2, 0.2 * its[1]), its
+
+
+def test_nystrom_device_omega_cfg2s():
+    """nsp_nystrom with Omega == NULL (generated on the device from the seed, reading C7) reproduces the
+    run with the host-generated Omega: same inner count, Sigma within 1e-8."""
+    pr, d, S = problem("cfg2s")
+    ctx = context(pr, factor_gamma=True)
+    r1 = ctx.nystrom(pr.rank, pr.oversample, dev(pr.omega()), pr.tol_bcg, 500)
+    sig1 = ctx.nystrom_sigma()
+    r2 = ctx.nystrom(pr.rank, pr.oversample, None, pr.tol_bcg, 500, seed=0)
+    sig2 = ctx.nystrom_sigma()
+    assert abs(r1["iters"] - r2["iters"]) <= 1 and r1["rank"] == r2["rank"]
+    assert np.max(np.abs(sig1 - sig2) / np.abs(sig1)) <= 1e-8
+    ctx.close()
