@@ -289,7 +289,7 @@ nsp_status nsp_dev_gram(const double* Xa, const double* Xb, const double* Xb2, i
 
 nsp_status nsp_dev_panel_gram(double* Out, const double* Cin, const double* In, const double* M, int64_t n,
                               double sgn, int gmode, double* gram, double* colsq, void* stream) {
-  if (!Out || !In || !M || !gram || (gmode != 0 && gmode != 1) || !nspb::panel_gram_ok(128, n)) return NSP_ERR_ARG;
+  if (!Out || !In || !M || !gram || (gmode != 0 && gmode != 1) || !nspb::panel_gram_shape_ok(128, n)) return NSP_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   double *ws = nullptr, *part = nullptr;
   if (cudaMalloc(&ws, nspb::gram_ws_doubles(n, 128, 128) * 8) != cudaSuccess) return NSP_ERR_CUDA;
@@ -319,6 +319,12 @@ nsp_status nsp_dev_philox_gaussian(double* out, int64_t rows, int s, uint64_t se
   const cudaError_t e = cudaStreamSynchronize(st);
   cudaFree(dg);
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NSP_OK : NSP_ERR_CUDA;
+}
+
+nsp_status nsp_dev_set_fused_pg(int mode) {
+  if (mode < 0 || mode > 2) return NSP_ERR_ARG;
+  nspb::nsp_fused_pg_mode = mode;
+  return NSP_OK;
 }
 
 const char* nsp_last_error(const nsp_ctx* c) { return c ? c->err.c_str() : "null context"; }

@@ -1164,13 +1164,22 @@ size_t gram_ws_doubles(int64_t n, int sa, int sb) {
   return (size_t)std::max(std::max(gram_ctas(), 4 * num_sms()), ntm * ntn) * 4096;
 }
 
+bool panel_gram_shape_ok(int s, int64_t n) { return s == 128 && n >= (int64_t)64 * num_sms(); }
+
+int nsp_fused_pg_mode = 0;   // nsp_dev_set_fused_pg: 0 production threshold, 1 force (shape ok), 2 never
 bool panel_gram_ok(int s, int64_t n) {
   static const bool off = [] {
     const char* e = getenv("NSP_FUSED_PG");
     return e && e[0] == '0';
   }();
-  return !off && !nsp_force_generic && s == 128 && n >= (int64_t)64 * num_sms();
+  if (nsp_fused_pg_mode == 1) return panel_gram_shape_ok(s, n);
+  if (nsp_fused_pg_mode == 2) return false;
+  // the fused pass wins only with many 32-row passes per SM: cfg5 (12.4k rows / SM) 4.26 + 4.50 ms
+  // against 2.19 + 3.56 ms (panel + Gram) per pair; cfg2 (97 rows / SM) 51 + 53 us against 25 + 26 +
+  // 9 us - there both are latency-bound at ~50 % of the DMMA peak and fusing adds a reduce of 148 partials
+  return !off && s == 128 && n >= (int64_t)512 * num_sms();
 }
+
 
 int panel_gram(double* Out, const double* Cin, const double* In, const double* M, int64_t n, double sgn,
                double* normpart, int gmode, double* gram_out, double* ws, cudaStream_t st) {

@@ -57,7 +57,9 @@ int panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, in
 // fused panel + Gram (s = 128, ld 128, n >= 64 x SMs, single rank): Out = Cin + sgn In M and
 // gram_out = In^T Out (gmode 0) or Out^T Out (gmode 1, exactly symmetric); normpart (nullable): column
 // sums of squares of Out, one row per CTA (returns the row count).  ws: gram_ws_doubles.
-bool panel_gram_ok(int s, int64_t n);
+bool panel_gram_ok(int s, int64_t n);          // the production choice (large n)
+bool panel_gram_shape_ok(int s, int64_t n);    // the kernel's shape requirement (kernel-level tests)
+extern int nsp_fused_pg_mode;                  // 0 production, 1 force whenever the shape allows, 2 never
 int panel_gram(double* Out, const double* Cin, const double* In, const double* M, int64_t n, double sgn,
                double* normpart, int gmode, double* gram_out, double* ws, cudaStream_t st);
 void colsq(const double* X, int ldx, int64_t n, int s, int ldp, double* part, double* out, cudaStream_t st);

@@ -270,10 +270,11 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __res
 
 // The same SpMM with 16-byte (double2) loads: lane l owns the column pairs (2l, 2l+1) + 64q, so one
 // warp instruction moves a 512-byte row segment and an s = 128 row takes two loads per nonzero instead
-// of four; the row's nonzeros are consumed two at a time (both gathers in flight before the FMAs).
-// Requires even s and even leading dimensions / chunk strides (16-byte aligned rows).
+// of four.  At most 32 registers (8 CTAs of 256 threads per SM: full occupancy hides the dependent
+// row-pointer -> index -> row-load chain).  Requires even s and even leading dimensions / chunk strides
+// (16-byte aligned rows).
 template <int NQ2>
-__global__ void __launch_bounds__(256) k_spmm2(int64_t rows, const int32_t* __restrict__ rp,
+__global__ void __launch_bounds__(256, NQ2 <= 2 ? 8 : 4) k_spmm2(int64_t rows, const int32_t* __restrict__ rp,
                                                const int32_t* __restrict__ ci, const double* __restrict__ va,
                                                const double* __restrict__ X, int ldx,
                                                const double* __restrict__ U, int ldu, int64_t ucs, int64_t split,
@@ -308,33 +309,7 @@ __global__ void __launch_bounds__(256) k_spmm2(int64_t rows, const int32_t* __re
     const int c = k < end ? ci[k] : 0;
     const double v = k < end ? va[k] : 0.0;
     const int cnt = min(32, end - base);
-    int q = 0;
-    for (; q + 1 < cnt; q += 2) {
-      const int64_t c0 = __shfl_sync(0xffffffffu, c, q), c1 = __shfl_sync(0xffffffffu, c, q + 1);
-      double a0 = __shfl_sync(0xffffffffu, v, q), a1 = __shfl_sync(0xffffffffu, v, q + 1);
-      int64_t cs0 = 32, cs1 = 32;
-      const double* s0 = src_of(c0, a0, cs0);
-      const double* s1 = src_of(c1, a1, cs1);
-      double2 x0[NQ2], x1[NQ2];
-#pragma unroll
-      for (int qq = 0; qq < NQ2; ++qq) {
-        const bool in = 2 * lane + 64 * qq < s;
-        x0[qq] = (s0 && in) ? __ldg(reinterpret_cast<const double2*>(s0 + off(qq, cs0))) : make_double2(0.0, 0.0);
-        x1[qq] = (s1 && in) ? __ldg(reinterpret_cast<const double2*>(s1 + off(qq, cs1))) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int qq = 0; qq < NQ2; ++qq) {
-        if (s0) {
-          acc[qq].x = fma(a0, x0[qq].x, acc[qq].x);
-          acc[qq].y = fma(a0, x0[qq].y, acc[qq].y);
-        }
-        if (s1) {
-          acc[qq].x = fma(a1, x1[qq].x, acc[qq].x);
-          acc[qq].y = fma(a1, x1[qq].y, acc[qq].y);
-        }
-      }
-    }
-    if (q < cnt) {
+    for (int q = 0; q < cnt; ++q) {
       const int64_t c0 = __shfl_sync(0xffffffffu, c, q);
       double a0 = __shfl_sync(0xffffffffu, v, q);
       int64_t cs0 = 32;

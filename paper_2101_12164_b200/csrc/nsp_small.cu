@@ -243,8 +243,10 @@ __device__ __forceinline__ bool fac8(double* B, double* Xo, double* piv) {
 // Warp 0: the 16 x 16 diagonal block at (c0, c0) as 2 x 2 blocks of 8 - L11 by one thread (fac8),
 // L21 = A21 X11^T and A22 - L21 L21^T row-parallel on 8 lanes, L22 by one thread, X21 = -X22 L21 X11
 // row-parallel.  Same outputs as warp_chol16: L in place (lower), X = L^{-1} to Xd (16 x 16 row-major,
-// zero above the diagonal), pivots to piv.  ~2.3k cycles per block against ~6.6k for the warp-wide
-// column loop (whose per-column chain is three shuffles and a shared-memory round trip).
+// zero above the diagonal), pivots to piv.  Kept behind NSP_CHOL_FAST8: measured SLOWER than the
+// warp-wide column loop (a 128 x 128 factorisation 94.2k vs 67.9k cycles, gpurun_out r02b) - one
+// thread's dependent fp64 chain (rsqrt + Newton, the 8 x 8 inverse) costs more than the warp's
+// shuffles.
 __device__ __noinline__ bool diag16_fast(double* As, int c0, double* Xd, double* piv) {
   const int lane = threadIdx.x & 31;
   double* B = As + c0 * LDA + c0;
@@ -475,10 +477,10 @@ __global__ void __launch_bounds__(CF_T) k_chol16(const double* __restrict__ Ain,
       }
     }
     if (warp == 0) {   // (A) the only call site of the diagonal factorisation
-#ifdef NSP_CHOL_WARP
-      const bool ok = warp_chol16(As, 16 * step, Di + step * 256, piv, colv, invd);
-#else
+#ifdef NSP_CHOL_FAST8   // measured slower (tools/bench_chol16.cu: 94.2k vs 67.9k cycles per 128 x 128)
       const bool ok = diag16_fast(As, 16 * step, Di + step * 256, piv);
+#else
+      const bool ok = warp_chol16(As, 16 * step, Di + step * 256, piv, colv, invd);
 #endif
       if (!ok && lane == 0) s_fail = 1;
     }

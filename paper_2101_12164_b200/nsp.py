@@ -24,7 +24,7 @@ EXPORTED = ["nsp_default_opts", "nsp_setup", "nsp_dims", "nsp_gamma_index", "nsp
             "nsp_gamma_apply", "nsp_kernel_launches", "nsp_profile", "nsp_profile_read", "nsp_shard_plan",
             "nsp_shard_info", "nsp_nccl_unique_id", "nsp_local_group_create", "nsp_local_group_destroy",
             "nsp_set_bcg_precond", "nsp_path_counters", "nsp_dev_panel", "nsp_dev_gram", "nsp_dev_panel_gram",
-            "nsp_dev_philox_gaussian"]
+            "nsp_dev_philox_gaussian", "nsp_dev_set_fused_pg"]
 
 # dispatch-path counter ids (include/nsp.h NSP_PATH_*)
 PATHS = ["panel_rows", "panel_tiles", "gram_sym", "gram_de", "gram_full", "symm", "sweeps", "symv",
@@ -105,6 +105,7 @@ def load_library(path: str = LIB_PATH):
     lib.nsp_dev_gram.argtypes = [P, P, P, I64, I, P, P, I, I, P]
     lib.nsp_dev_panel_gram.argtypes = [P, P, P, P, I64, D, I, P, P, P]
     lib.nsp_dev_philox_gaussian.argtypes = [P, I64, I, C.c_uint64, C.c_uint, I64, P]
+    lib.nsp_dev_set_fused_pg.argtypes = [I]
     for f in EXPORTED:
         if f not in ("nsp_default_opts", "nsp_last_error", "nsp_destroy", "nsp_kernel_launches",
                      "nsp_local_group_create", "nsp_local_group_destroy"):
@@ -178,6 +179,12 @@ def dev_philox_gaussian(out, seed, stream_id=0, row0=0, stream=None):
                                                 _stream_ptr(stream))
     if st != 0:
         raise NspError(st, "nsp_dev_philox_gaussian failed")
+
+
+def dev_set_fused_pg(mode: int):
+    """nsp_dev_set_fused_pg: 0 production threshold, 1 force the fused panel + Gram pass, 2 never."""
+    if load_library().nsp_dev_set_fused_pg(mode) != 0:
+        raise NspError(-1, "nsp_dev_set_fused_pg: mode in {0, 1, 2}")
 
 
 def dev_gram(Xa, Xb, out, Xb2=None, out2=None, lower_first=False, path=0, stream=None):

@@ -93,3 +93,36 @@ def test_bench_path_bcg_parity_cfg2(mode):
     spread = gold["spread_local_vs_dense"][str(kk)]
     print(f"  k={kk}: gpu-vs-oracle {diff:.2e}, oracle spread {spread:.2e}")
     assert diff <= max(1e-8, 10 * spread), (kk, diff, spread)
+
+
+def test_fused_panel_gram_path_parity_cfg2():
+    """The fused s = 128 panel + Gram passes (k_panel_gram: R -= Q alpha with F = Q^T R, W = R + P beta with
+    W^T W) that the bench dispatches at cfg5 (n_G >= 512 x SMs), forced on at cfg2 so the ORACLE can check
+    them: free-running count = the oracle's (+-1), X at equal counts k in {1, 2, 3, 60} within
+    max(1e-8, 10 x spread)."""
+    st = _setup()
+    pr, L, B, gold = st["pr"], st["L"], st["B"], st["gold"]["modes"]["I"]
+    ctx = context(pr)                      # fresh context: its graphs are captured with the fused passes
+    nsp.dev_set_fused_pg(1)
+    try:
+        Bd = dev(B)
+        X = torch.zeros_like(Bd)
+        ws = torch.empty(ctx.workspace_bytes(pr.s), dtype=torch.uint8, device="cuda")
+        c0 = nsp.path_counters()
+        rep = ctx.block_cg(Bd, X, pr.tol_bcg, 500, ws)
+        c1 = nsp.path_counters()
+        assert c1["panel_gram"] > c0["panel_gram"], (c0, c1)
+        print(f"cfg2 fused panel+Gram: gpu {rep['iters']} its, golden {gold['iters']}")
+        assert rep["converged"] and abs(rep["iters"] - gold["iters"]) <= 1
+        for k in (1, 2, 3, gold["iters"]):
+            Xk, ik = O.bf_bcg(L.apply, B, 0.0, k)
+            X2 = torch.zeros_like(Bd)
+            rep2 = ctx.block_cg(Bd, X2, 0.0, k, ws)
+            diff = relfro(X2.cpu().numpy(), Xk)
+            spread = gold["spread_local_vs_dense"][str(k)]
+            print(f"  k={k}: gpu-vs-oracle {diff:.2e}, oracle spread {spread:.2e}")
+            assert diff <= max(1e-8, 10 * spread), (k, diff, spread)
+            assert rep2["widths"] == ik["widths"]
+    finally:
+        nsp.dev_set_fused_pg(0)
+        ctx.close()
