@@ -270,8 +270,8 @@ nsp_status nsp_dev_gram(const double* Xa, const double* Xb, const double* Xb2, i
 nsp_status nsp_dev_philox_gaussian(double* out, int64_t rows, int s, uint64_t seed, unsigned stream_id, int64_t row0,
                                    void* stream);
 /*  nsp_dev_set_fused_pg: process-wide choice of the fused s = 128 panel + Gram pass in block CG for the
- *                 contexts' NEXT graph captures: 0 = production (n >= 512 x SMs), 1 = whenever the shape
- *                 allows (n >= 64 x SMs; lets the oracle parity tests reach it at cfg2), 2 = never. */
+ *                 contexts' NEXT graph captures: 0 = production (off: measured not faster),
+ *                 1 = whenever the shape allows (n >= 64 x SMs; the oracle parity test), 2 = never. */
 nsp_status nsp_dev_set_fused_pg(int mode);
 nsp_status nsp_dev_panel_gram(double* Out, const double* Cin, const double* In, const double* M, int64_t n,
                               double sgn, int gmode, double* gram, double* colsq, void* stream);

@@ -1174,10 +1174,14 @@ bool panel_gram_ok(int s, int64_t n) {
   }();
   if (nsp_fused_pg_mode == 1) return panel_gram_shape_ok(s, n);
   if (nsp_fused_pg_mode == 2) return false;
-  // the fused pass wins only with many 32-row passes per SM: cfg5 (12.4k rows / SM) 4.26 + 4.50 ms
-  // against 2.19 + 3.56 ms (panel + Gram) per pair; cfg2 (97 rows / SM) 51 + 53 us against 25 + 26 +
-  // 9 us - there both are latency-bound at ~50 % of the DMMA peak and fusing adds a reduce of 148 partials
-  return !off && s == 128 && n >= (int64_t)512 * num_sms();
+  // Not used by default: measured NOT faster.  The tall-skinny passes are DMMA-bound (s / 8 = 16 flop/B
+  // at s = 128), so reading each block once saves HBM bytes that are not the binding resource, while
+  // the fused pass does the panel and the Gram flops back to back in one CTA per SM.  cfg2 (97 rows / SM):
+  // 51 + 53 us against 25 + 26 + 9 us (block CG 464 vs 438 us per iteration); cfg5 (12.4k rows / SM):
+  // 4.26 + 4.50 ms against 2.19 + 2.0 and 2.19 + 1.5 ms (block CG 97.3 vs 96.8 ms per iteration)
+  // (profiles/r02_ab_*.jsonl, r02_launches_*).  nsp_dev_set_fused_pg(1) forces it (parity tests).
+  (void)n;
+  return !off && false;
 }
 
 
