@@ -400,6 +400,7 @@ def measure(pr, args, ws, rank, local, stream, nccl_id, headline):
         # outer PCG on the full system with M_2 to tol_pcg (eq:Sx=b)
         del wsbuf
         torch.cuda.empty_cache()
+        ctx.nystrom(pr.rank, pr.oversample, Om, pr.tol_bcg, maxit)   # warm-up: workspaces, graph capture
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         rn = ctx.nystrom(pr.rank, pr.oversample, Om, pr.tol_bcg, maxit)

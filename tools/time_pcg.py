@@ -11,9 +11,9 @@ pr = P.make(name)
 ctx = nsp.Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, factor_gamma=True)
 ctx.nystrom(pr.rank, pr.oversample, torch.from_numpy(pr.omega()).cuda(), pr.tol_bcg, 1000)
 b = torch.from_numpy(pr.rhs()).cuda()
-for prec in (2, 1):
+for prec in [int(x) for x in os.environ.get('NSP_PRECS', '2,1').split(',')]:
     ts, its = [], None
-    for r in range(reps + 2):
+    for r in range(reps + int(os.environ.get('NSP_PCG_WARM', '2'))):
         x = torch.zeros_like(b)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
