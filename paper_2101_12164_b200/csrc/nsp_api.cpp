@@ -370,6 +370,9 @@ void nsp_destroy(nsp_ctx* c) {
   if (c->d_bwidth) cudaFree(c->d_bwidth);
   if (c->gstream) cudaStreamDestroy(c->gstream);
   if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  if (c->apply_stream) cudaStreamDestroy(c->apply_stream);
+  if (c->ev_afork) cudaEventDestroy(c->ev_afork);
+  if (c->ev_ajoin) cudaEventDestroy(c->ev_ajoin);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   for (DevCSR* m : {&c->A2G, &c->AGG2, &c->AGSH, &c->CB, &c->C1, &c->AII}) {

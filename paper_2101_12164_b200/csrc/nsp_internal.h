@@ -198,6 +198,8 @@ struct nsp_ctx {
   cudaStream_t gstream = nullptr;
   cudaStream_t side_stream = nullptr;   // block CG: the deferred X update (forked, joined before orth)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t apply_stream = nullptr;  // block CG: S_G W on a forked branch while W^T W / chol run (R9)
+  cudaEvent_t ev_afork = nullptr, ev_ajoin = nullptr;
   bool capturing = false;          // block CG is capturing its iteration graph
   bool gprof_in_graph = false;     // the cached graph records gprof_ev around a2+a3
   cudaEvent_t gprof_ev[2] = {nullptr, nullptr};

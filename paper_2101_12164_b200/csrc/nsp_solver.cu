@@ -83,7 +83,7 @@ struct Carver {
 struct BcgWs {
   int sp, kind;
   int64_t n;
-  double *X, *R, *P, *Q, *W, *Z;
+  double *X, *R, *P, *Q, *W, *Z, *QW;
   double *tG, *hB, *wB, *agb;   // kind 1 scratch
   double *D, *E, *F, *G, *Ld, *Ldi, *T, *al, *be, *tmp, *Vw, *Vs, *lam, *bnorm, *rsq, *gram, *npart, *wvu;
   BcgStatus* st;
@@ -108,6 +108,7 @@ static size_t bcg_layout(const nsp_ctx* c, int s, char* base, BcgWs* w, int kind
   t.W = cv.take(blk);
   // Z exists whenever M = A_G^{-1} is possible (nsp_set_bcg_precond may switch M after setup)
   t.Z = ((kind || c->opts.bcg_precond || c->has_ag) ? cv.take(blk) : nullptr);
+  t.QW = cv.take(blk);   // S_G W of the apply-first iteration (reading R9)
   if (kind) {
     t.tG = cv.take((size_t)std::max<int64_t>(c->nG, 1) * sp);
     t.hB = cv.take((size_t)std::max<int64_t>(c->wvu_rows, 1) * sp);
@@ -163,7 +164,7 @@ static bool fused_sxs() {
 
 // orth(Wm): Gram, Cholesky-QR with pivot test, eigen fallback; P = Wm T (reading C3)
 static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Pout,
-                       cudaEvent_t join_before_panel = nullptr, bool gram_done = false) {
+                       cudaEvent_t join_before_panel = nullptr, bool gram_done = false, bool no_panel = false) {
   const int sp = w.sp;
   const int64_t n = w.n;
   cudaStream_t st = c->stream;
@@ -182,6 +183,7 @@ static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Po
   }
   // eigen fallback (gated on the pivot test): EVD and T = V_keep Lambda^{-1/2} in one launch
   nspb::small_eig(w.G, sp, s, w.Vw, sp + 1, w.lam, w.Vs, &w.st->fallback, st, c->opts.orth_tau, w.T, sp, w.st);
+  if (no_panel) return NSP_OK;   // (apply-first: the caller forms P = W T and Q = (S W) T together)
   if (join_before_panel) NSP_CUDA_TRY(c, cudaStreamWaitEvent(st, join_before_panel, 0));   // X += P alpha done
   nspb::panel(Pout, sp, nullptr, 0, Wm, sp, w.T, sp, sp, sp, n, 1.0, nullptr, st);
   return NSP_OK;
@@ -292,11 +294,18 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   double relres = hs->relres;
   double* Zr = usem ? w.Z : w.R;
   // head: a1-a8 (Q = S P, D|E, chol(D), alpha, X/R update, norms, convergence) + the status copy
+  // apply-first (reading R9; one rank, small n_G where the iteration is latency-bound): the tail applies
+  // S_G to W = Z + P beta on a forked branch while W^T W, its Cholesky and T = L^{-T} run, then forms
+  // P = W T and Q = (S_G W) T in one panel launch - Q = S_G P by linearity - and the head skips its apply
+  const char* afe = getenv("NSP_APPLY_FIRST");
+  const bool apply_first = !multi && !tr.on && w.kind == 0 &&
+                           (afe ? afe[0] == '1' : n <= 65536);
+  bool skip_apply = false;   // the head's Q was formed by the preceding tail
   auto head = [&](bool copy_status) -> nsp_status {
     cudaStream_t q = c->stream;
     nsp_status e2;
     tr.mark("loop");
-    if ((e2 = op_apply(c, w, w.P, w.Q, s)) != NSP_OK) return e2;
+    if (!skip_apply && (e2 = op_apply(c, w, w.P, w.Q, s)) != NSP_OK) return e2;
     tr.mark("apply");
     nspb::gram2(w.P, sp, sp, w.Q, w.R, sp, sp, ng, w.D, w.E, sp, w.gram, q, true);   // D: lower tiles (chol)
     if (multi) {   // D and E are adjacent in the workspace: one allreduce
@@ -365,7 +374,28 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
     if (fuse_pg) nspb::panel_gram(w.W, Zr, w.P, w.be, n, 1.0, nullptr, 1, w.G, w.gram, q);   // + G = W^T W
     else nspb::panel(w.W, sp, Zr, sp, w.P, sp, w.be, sp, sp, sp, n, 1.0, nullptr, q);
     tr.mark("W");
-    if ((e2 = orth(c, w, w.W, s, w.P, xfork ? c->ev_join : nullptr, fuse_pg)) != NSP_OK) return e2;
+    if (apply_first) {
+      if (!c->apply_stream) NSP_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->apply_stream, cudaStreamNonBlocking));
+      if (!c->ev_afork) NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_afork, cudaEventDisableTiming));
+      if (!c->ev_ajoin) NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_ajoin, cudaEventDisableTiming));
+      NSP_CUDA_TRY(c, cudaEventRecord(c->ev_afork, q));
+      NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->apply_stream, c->ev_afork, 0));
+      c->stream = c->apply_stream;   // the apply's kernels go to the forked branch (a graph branch when captured)
+      e2 = op_apply(c, w, w.W, w.QW, s);
+      c->stream = q;
+      if (e2 != NSP_OK) return e2;
+      NSP_CUDA_TRY(c, cudaEventRecord(c->ev_ajoin, c->apply_stream));
+      if ((e2 = orth(c, w, w.W, s, w.P, nullptr, fuse_pg, true)) != NSP_OK) return e2;   // G, chol, T (or eig)
+      if (xfork) NSP_CUDA_TRY(c, cudaStreamWaitEvent(q, c->ev_join, 0));                // X += P alpha done
+      NSP_CUDA_TRY(c, cudaStreamWaitEvent(q, c->ev_ajoin, 0));                           // S_G W done
+      PanelArgs pp{w.P, sp, nullptr, 0, w.W, sp, w.T, sp, 1.0, nullptr};
+      PanelArgs pq{w.Q, sp, nullptr, 0, w.QW, sp, w.T, sp, 1.0, nullptr};
+      nspb::panel2(pp, &pq, sp, sp, n, q);   // P = W T and Q = (S_G W) T, one launch
+      skip_apply = true;
+    } else {
+      if ((e2 = orth(c, w, w.W, s, w.P, xfork ? c->ev_join : nullptr, fuse_pg)) != NSP_OK) return e2;
+      skip_apply = false;
+    }
     tr.mark("orth");
     return NSP_OK;
   };
