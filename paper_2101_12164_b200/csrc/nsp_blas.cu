@@ -3,6 +3,7 @@
 // Cholesky / triangular inverse / Jacobi eigensolver, small GEMMs.  All reductions are
 // fixed-order two-stage (no fp64 atomics): results are bitwise reproducible (reading C17).
 #include <algorithm>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -51,6 +52,11 @@ constexpr int LDS = 68;    // smem stride for 64-wide tiles
 // through a GNS-stage cp.async ring of 32-row slabs (one barrier per slab), so the slab loads are
 // in flight GNS-1 slabs ahead of the DMMA work.
 constexpr int GNS = NSP_GNS;
+// CL > 1: the grid's chunk dimension is split into clusters of CL CTAs (one thread-block cluster each);
+// after its slab loop every CTA parks its 64 x 64 partial in shared memory and the cluster sums the CL
+// partials through distributed shared memory (each CTA a 64/CL-row slice, ranks in order), so the
+// partial buffer - and the k_gram_reduce that follows - holds CL x fewer chunks.
+template <int CL>
 __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__ Xa, int lda,
                                                       const double* __restrict__ Xb, const double* __restrict__ Xb2,
                                                       int ldb, int ntn1, int64_t n,
@@ -107,14 +113,40 @@ __global__ void __launch_bounds__(256) k_gram_partial(const double* __restrict__
     const double* st = sm + (q % GNS) * STG;
     cta_mma<4, true, false>(st, LDS, st + GR * LDS, LDS, acc, GR);
   }
-  double* out = part + ((int64_t)blockIdx.y * gridDim.x + tile) * 4096;
+  if constexpr (CL == 1) {
+    double* out = part + ((int64_t)blockIdx.y * gridDim.x + tile) * 4096;
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int rr = acc_row<4>(i), cc = acc_col<4>(j);
-      *reinterpret_cast<double2*>(out + rr * 64 + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
+      for (int j = 0; j < 4; ++j) {
+        const int rr = acc_row<4>(i), cc = acc_col<4>(j);
+        *reinterpret_cast<double2*>(out + rr * 64 + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+  } else {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    cp_wait<0>();
+    __syncthreads();   // the slab ring is free
+    double* mine = sm;   // 64 x 64 partial of this CTA
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int rr = acc_row<4>(i), cc = acc_col<4>(j);
+        *reinterpret_cast<double2*>(mine + rr * 64 + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    cluster.sync();
+    const int rank = (int)cluster.block_rank();
+    constexpr int SL = 4096 / CL;   // this CTA's slice of the tile (64 / CL rows)
+    double* out = part + ((int64_t)(blockIdx.y / CL) * gridDim.x + tile) * 4096 + rank * SL;
+    for (int e = threadIdx.x; e < SL; e += blockDim.x) {
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < CL; ++q) v += cluster.map_shared_rank(mine, q)[rank * SL + e];
+      out[e] = v;
     }
+    cluster.sync();   // no CTA leaves while another may still read its shared memory
+  }
 }
 
 // out (or out2 for column tiles >= ntn1) = sum over chunks, 4 chunk groups per element combined
@@ -1218,16 +1250,41 @@ void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb
   if (!sym_off && lower_first && Xb2 && ntn1 == ntm && ntm > 1) sym = 2;
   nsp_count_path(sym == 1 ? NSP_PATH_GRAM_SYM : sym == 2 ? NSP_PATH_GRAM_DE : NSP_PATH_GRAM_FULL);
   const int ntiles = sym == 1 ? ntm * (ntm + 1) / 2 : sym == 2 ? ntm * (ntm + 1) / 2 + ntm * ntn1 : ntm * ntn;
-  const int nch = gram_chunks(n, ntiles);
+  int nch = gram_chunks(n, ntiles);
+  // clusters of GCL chunk-CTAs pre-sum their partials in distributed shared memory (NSP_GRAM_CL=1: off)
+  static const int gcl_env = [] {
+    const char* e = getenv("NSP_GRAM_CL");
+    return e ? atoi(e) : 8;
+  }();
+  const int gcl = (gcl_env == 8 && nch >= 16 && !nsp_force_generic) ? 8 : 1;
+  if (gcl > 1) nch = (nch / gcl) * gcl;
   int64_t rpc = (n + nch - 1) / nch;
   rpc = ((rpc + GR - 1) / GR) * GR;
   const size_t smem = GNS * 2 * GR * LDS * sizeof(double);
-  smem_optin((const void*)k_gram_partial, smem);
-  {
+  if (gcl > 1) {
+    smem_optin((const void*)k_gram_partial<8>, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles, nch);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 1;
+    at[1].val.clusterDim.y = 8;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
     nsp_count_launch();
-    launch_k(k_gram_partial, dim3(dim3(ntiles, nch)), dim3(256), smem, st, Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn, sym);
+    cudaLaunchKernelEx(&cfg, k_gram_partial<8>, Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn, sym);
+  } else {
+    smem_optin((const void*)k_gram_partial<1>, smem);
+    nsp_count_launch();
+    launch_k(k_gram_partial<1>, dim3(dim3(ntiles, nch)), dim3(256), smem, st, Xa, lda, Xb, Xb2, ldb, ntn1, n, rpc, ws, ntm, ntn, sym);
   }
-  { nsp_count_launch(); launch_k(k_gram_reduce, dim3(dim3(ntn * 4, ntm * 4)), dim3(dim3(16, 16, 4)), 0, st, ws, nch, ntm, ntn, ntn1, out, out2, ldo, sym); }
+  { nsp_count_launch(); launch_k(k_gram_reduce, dim3(dim3(ntn * 4, ntm * 4)), dim3(dim3(16, 16, 4)), 0, st, ws, nch / gcl, ntm, ntn, ntn1, out, out2, ldo, sym); }
 }
 
 void gram(const double* Xa, int lda, int sa, const double* Xb, int ldb, int sb, int64_t n, double* out, int ldo,
