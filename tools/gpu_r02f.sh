@@ -15,3 +15,5 @@ for v in "NSP_GRAM_CL=1" "NSP_GRAM_CL=8"; do
 done
 env NSP_GRAM_CL=1 timeout 600 python tools/ab_bcg.py cfg5 3 >> "$OUT/ab_cl.jsonl" 2>> "$OUT/ab.err"
 env NSP_GRAM_CL=8 timeout 600 python tools/ab_bcg.py cfg5 3 >> "$OUT/ab_cl.jsonl" 2>> "$OUT/ab.err"
+NSP_PRECS=2 NSP_PCG_WARM=0 NSP_GRAPH=1 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 30000 --csv \
+      --log-file "$OUT/launches_pcg_cfg5.csv" python tools/time_pcg.py cfg5 1 > "$OUT/ncu_pcg_cfg5.log" 2>&1

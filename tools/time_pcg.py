@@ -19,7 +19,7 @@ for prec in [int(x) for x in os.environ.get('NSP_PRECS', '2,1').split(',')]:
         t0 = time.perf_counter()
         rep = ctx.pcg(b, x, pr.tol_pcg or 1e-8, 20000, precond=prec)
         torch.cuda.synchronize()
-        if r >= 2:
+        if r >= int(os.environ.get('NSP_PCG_WARM', '2')):
             ts.append(time.perf_counter() - t0)
         its = rep["iters"]
     med = statistics.median(ts)
