@@ -265,6 +265,10 @@ void gather_rows(const double* src, int lds, const int32_t* idx, int64_t rows, d
                  double scale, cudaStream_t st);
 void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, double* dst, int ldd, int s,
                   bool accumulate, cudaStream_t st);
+// one fused Chebyshev step (one rank): t = A_G d (the cols < split prefix of A's rows), x += d, r -= t,
+// dn = c1 d + c2 r; blocks n x ld row-major (ld = 1 with s = 1)
+void cheb_step(const DevCSR& A, int64_t split, const double* d, int ld, int s, double* x, double* r, double* dn,
+               double c1, double c2, bool want_d, cudaStream_t st);
 // Gaussian block on the device, bit-compatible with nsp_inputs.philox.gaussian_block (reading C7):
 // out[r * ld + j] (j < s; columns s..ld-1 zeroed) = N(0,1) from Philox4x32-10 counter (gidx[r] * s + j,
 // stream, 0), key = seed, Box-Muller cosine branch.  gidx: device int64 row indices.

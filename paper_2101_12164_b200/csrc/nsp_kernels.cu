@@ -347,6 +347,91 @@ __global__ void __launch_bounds__(256, NQ2 <= 2 ? 8 : 4) k_spmm2(int64_t rows, c
       *reinterpret_cast<double2*>(y + (int64_t)(cc >> 5) * ycs + (cc & 31)) = make_double2(0.0, 0.0);
 }
 
+// One step of the fixed Chebyshev iteration for A_G^{-1} (reading R7; one rank) fused with its sparse
+// product: per row, t = (A_G d)[row] over the A_G prefix of the AGG2 row (cols < split), then the
+// elementwise update x += d, r -= t, d' = c1 d + c2 r of the same row - one pass instead of an SpMM that
+// writes t and an update that reads it back.  Same summation order as k_spmv / k_spmm2 + k_cheb_update
+// (bitwise the same iterate).  s = 1: G lanes per row; s > 1: a warp per row, column pairs per lane.
+template <int G>
+__global__ void __launch_bounds__(256) k_cheb_step_vec(int64_t rows, const int32_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ ci, const double* __restrict__ va,
+                                                       int64_t split, const double* __restrict__ d,
+                                                       double* __restrict__ x, double* __restrict__ r,
+                                                       double* __restrict__ dn, double c1, double c2, int want_d) {
+  pdl_wait();
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int sub = threadIdx.x & (G - 1);
+  double acc = 0.0;
+  if (row < rows) {
+    const int beg = rp[row], end = rp[row + 1];
+    for (int k = beg + sub; k < end; k += G) {
+      const int64_t col = ci[k];
+      if (col < split) acc = fma(va[k], __ldg(d + col), acc);
+    }
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (row >= rows || sub != 0) return;
+  const double di = d[row];
+  x[row] += di;
+  const double ri = r[row] - acc;
+  r[row] = ri;
+  if (want_d) dn[row] = fma(c1, di, c2 * ri);
+}
+
+template <int NQ2>
+__global__ void __launch_bounds__(256, NQ2 <= 2 ? 8 : 4) k_cheb_step_blk(int64_t rows, const int32_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ ci, const double* __restrict__ va,
+                                                       int64_t split, const double* __restrict__ d, int ld,
+                                                       double* __restrict__ x, double* __restrict__ r,
+                                                       double* __restrict__ dn, double c1, double c2, int want_d) {
+  pdl_wait();
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int beg = rp[row], end = rp[row + 1];
+  double2 acc[NQ2];
+#pragma unroll
+  for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
+  for (int base = beg; base < end; base += 32) {
+    const int k = base + lane;
+    const int c = k < end ? ci[k] : 0;
+    const double v = k < end ? va[k] : 0.0;
+    const int cnt = min(32, end - base);
+    for (int q = 0; q < cnt; ++q) {
+      const int64_t col = __shfl_sync(0xffffffffu, c, q);
+      const double a = __shfl_sync(0xffffffffu, v, q);
+      if (col >= split) continue;
+      const double* src = d + col * ld;
+#pragma unroll
+      for (int qq = 0; qq < NQ2; ++qq) {
+        const int cc = 2 * lane + 64 * qq;
+        if (cc < ld) {
+          const double2 dv = __ldg(reinterpret_cast<const double2*>(src + cc));
+          acc[qq].x = fma(a, dv.x, acc[qq].x);
+          acc[qq].y = fma(a, dv.y, acc[qq].y);
+        }
+      }
+    }
+  }
+  const int64_t o = row * ld;
+#pragma unroll
+  for (int qq = 0; qq < NQ2; ++qq) {
+    const int cc = 2 * lane + 64 * qq;
+    if (cc >= ld) continue;
+    const double2 di = *reinterpret_cast<const double2*>(d + o + cc);
+    double2 xi = *reinterpret_cast<const double2*>(x + o + cc);
+    double2 ri = *reinterpret_cast<const double2*>(r + o + cc);
+    xi.x += di.x;
+    xi.y += di.y;
+    ri.x = ri.x - acc[qq].x;
+    ri.y = ri.y - acc[qq].y;
+    *reinterpret_cast<double2*>(x + o + cc) = xi;
+    *reinterpret_cast<double2*>(r + o + cc) = ri;
+    if (want_d) *reinterpret_cast<double2*>(dn + o + cc) = make_double2(fma(c1, di.x, c2 * ri.x), fma(c1, di.y, c2 * ri.y));
+  }
+}
+
 // One right-hand side (s = 1): the same modes as k_spmm, G lanes per row (several rows per warp),
 // the lanes take the row's nonzeros in parallel (independent gathers of x) and combine them with a
 // G-lane butterfly (fixed order).  k_spmm's lane-over-columns layout would leave 31 of 32 lanes idle
@@ -1804,6 +1889,29 @@ void spmm_cs(const DevCSR& A, const double* X, int ldx, const double* U, int ldu
 void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split, double* Y,
           int ldy, int s, int mode, bool zero_pad, cudaStream_t st) {
   spmm_cs(A, X, ldx, U, ldu, 32, split, Y, ldy, 32, ldy, s, mode, zero_pad, st);
+}
+
+void cheb_step(const DevCSR& A, int64_t split, const double* d, int ld, int s, double* x, double* r, double* dn,
+               double c1, double c2, bool want_d, cudaStream_t st) {
+  if (A.rows <= 0) return;
+  if (s == 1 && ld == 1) {
+    nsp_count_launch();
+    launch_k(k_cheb_step_vec<8>, dim3((unsigned)((A.rows * 8 + 255) / 256)), dim3(256), 0, st, A.rows, A.rowptr,
+             A.col, A.val, split, d, x, r, dn, c1, c2, want_d ? 1 : 0);
+    return;
+  }
+  const unsigned blocks = (unsigned)((A.rows * 32 + 255) / 256);
+  const int nq2 = (ld + 63) / 64;
+  nsp_count_launch();
+  if (nq2 <= 1)
+    launch_k(k_cheb_step_blk<1>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, split, d, ld, x, r, dn, c1,
+             c2, want_d ? 1 : 0);
+  else if (nq2 == 2)
+    launch_k(k_cheb_step_blk<2>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, split, d, ld, x, r, dn, c1,
+             c2, want_d ? 1 : 0);
+  else
+    launch_k(k_cheb_step_blk<4>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, split, d, ld, x, r, dn, c1,
+             c2, want_d ? 1 : 0);
 }
 
 void philox_gaussian(double* out, int64_t rows, int s, int ld, const int64_t* gidx, uint64_t seed, uint32_t stream,

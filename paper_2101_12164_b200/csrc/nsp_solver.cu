@@ -663,7 +663,13 @@ static nsp_status ag_cheb(nsp_ctx* c, const double* X, int ldx, double* Y, int l
   const double theta = 0.5 * (c->cheb_b + c->cheb_a);
   nspb::copy_pad(X, ldx, d0, ld, n, s, 1.0 / theta, st);
   NSP_CUDA_TRY(c, cudaMemsetAsync(xw, 0, blk * 8, st));
+  static const bool fused_off = getenv("NSP_CHEB_FUSED") && getenv("NSP_CHEB_FUSED")[0] == '0';
   for (int k = 0; k < c->cheb_K; ++k) {
+    if (c->nranks == 1 && !fused_off && (ld == 1 || ld % 2 == 0)) {   // product and update in one pass
+      nspk::cheb_step(c->AGG2, n, d0, ld, s, xw, r, d1, c->cheb_c1[k], c->cheb_c2[k], k + 1 < c->cheb_K, st);
+      std::swap(d0, d1);
+      continue;
+    }
     nspk::spmm(c->AGG2, d0, ld, nullptr, 0, n, t, ld, s, 3, true, st);   // t = A_G d
     if (c->nranks > 1) {   // shared rows: sum the per-rank partials, add the shared x shared term
       nsp_status e = finish_shared_rows(c, d0, ld, t, ld, s, true);
