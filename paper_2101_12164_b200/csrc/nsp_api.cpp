@@ -77,6 +77,42 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   if (gprof) cudaEventRecordWithFlags(c->gprof_ev[0], c->stream, cudaEventRecordExternal);   // a graph node
   if (prof) cudaEventRecord(c->prof_ev[c->prof_used], c->stream);
   double* U = wvu;
+  // several ranks, s > 1 (SURVEY.md §8(e) budget: "process the subdomains adjacent to shared separators
+  // first and launch the allreduce on a second stream"): the blocks coupled to shared rows are multiplied
+  // first, their shared-row partials formed and allreduced on the comm stream while the other blocks'
+  // products and the private rows' a4+a5 run on the context stream
+  static const bool ovl_off = getenv("NSP_COMM_OVERLAP") && getenv("NSP_COMM_OVERLAP")[0] == '0';
+  if (c->nranks > 1 && c->d_minv && s > 1 && !gprof && !prof && !ovl_off) {
+    U = cm ? wvu + (int64_t)(ldw / 32) * cs : wvu + c->wvu_rows * (int64_t)ldw;
+    const int nsh_it = c->n_items_sh, nrest = c->n_items - c->n_items_sh;
+    const int64_t nsh = c->nG - c->n_priv;
+    cudaStream_t main = c->stream;
+    nsp_count_path(NSP_PATH_SYMM);
+    nspk::symm(c->d_subs, c->d_items, nsh_it, c->d_minv, wvu, U, ldw, cw, main, cs);
+    DevCSR shr = c->AGG2;   // the shared rows' slice of the a4+a5 operator
+    shr.rows = nsh;
+    shr.rowptr = c->AGG2.rowptr + c->n_priv;
+    if (cm) nspk::spmm_cs(shr, X, ldx, U, 36, cs, c->nG, Y + c->n_priv * (int64_t)ldy, ldy, 32, ldy, s, mode, true, main);
+    else nspk::spmm(shr, X, ldx, U, ldw, c->nG, Y + c->n_priv * (int64_t)ldy, ldy, s, mode, true, main);
+    if (!c->comm_stream) NSP_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    if (!c->ev_cfork) NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_cfork, cudaEventDisableTiming));
+    if (!c->ev_cjoin) NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_cjoin, cudaEventDisableTiming));
+    NSP_CUDA_TRY(c, cudaEventRecord(c->ev_cfork, main));
+    NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_cfork, 0));
+    c->stream = c->comm_stream;
+    nsp_status e = finish_shared_rows(c, X, ldx, Y, ldy, s, mode != 2);   // allreduce + shared x shared A_G
+    c->stream = main;
+    if (e != NSP_OK) return e;
+    NSP_CUDA_TRY(c, cudaEventRecord(c->ev_cjoin, c->comm_stream));
+    if (nrest > 0) nspk::symm(c->d_subs, c->d_items + nsh_it, nrest, c->d_minv, wvu, U, ldw, cw, main, cs);
+    DevCSR prv = c->AGG2;   // the private rows
+    prv.rows = c->n_priv;
+    if (cm) nspk::spmm_cs(prv, X, ldx, U, 36, cs, c->nG, Y, ldy, 32, ldy, s, mode, true, main);
+    else nspk::spmm(prv, X, ldx, U, ldw, c->nG, Y, ldy, s, mode, true, main);
+    NSP_CUDA_TRY(c, cudaStreamWaitEvent(main, c->ev_cjoin, 0));
+    NSP_CUDA_TRY(c, cudaGetLastError());
+    return NSP_OK;
+  }
   if (c->d_minv) {
     U = cm ? wvu + (int64_t)(ldw / 32) * cs : wvu + c->wvu_rows * (int64_t)ldw;
     if (s == 1) {   // one right-hand side (outer PCG): memory-bound matrix-vector form, tiles read once
@@ -371,6 +407,9 @@ void nsp_destroy(nsp_ctx* c) {
   if (c->gstream) cudaStreamDestroy(c->gstream);
   if (c->side_stream) cudaStreamDestroy(c->side_stream);
   if (c->apply_stream) cudaStreamDestroy(c->apply_stream);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_cfork) cudaEventDestroy(c->ev_cfork);
+  if (c->ev_cjoin) cudaEventDestroy(c->ev_cjoin);
   if (c->ev_afork) cudaEventDestroy(c->ev_afork);
   if (c->ev_ajoin) cudaEventDestroy(c->ev_ajoin);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);

@@ -109,6 +109,7 @@ struct nsp_ctx {
   double* d_minv = nullptr;
   int2* d_items = nullptr;
   int n_items = 0;
+  int n_items_sh = 0;         // several ranks: items [0, n_items_sh) belong to blocks coupled to shared rows
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
   DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)
@@ -198,6 +199,8 @@ struct nsp_ctx {
   cudaStream_t gstream = nullptr;
   cudaStream_t side_stream = nullptr;   // block CG: the deferred X update (forked, joined before orth)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t comm_stream = nullptr;   // several ranks: the shared-row allreduce, overlapped with the apply
+  cudaEvent_t ev_cfork = nullptr, ev_cjoin = nullptr;
   cudaStream_t apply_stream = nullptr;  // block CG: S_G W on a forked branch while W^T W / chol run (R9)
   cudaEvent_t ev_afork = nullptr, ev_ajoin = nullptr;
   bool capturing = false;          // block CG is capturing its iteration graph

@@ -1239,10 +1239,26 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_minv, bytes));
       nspk::l22_inverse(c->d_subs, c->nsub, c->max_ntb, c->d_dense, c->d_minv, c->stream);
       NSP_CUDA_TRY(c, cudaGetLastError());
+      // several ranks: the blocks coupled to a SHARED Gamma row first (their U feeds the shared-row
+      // partials, so the shared-row allreduce can start while the other blocks' products run)
+      std::vector<char> blk_sh(KL, 0);
+      if (c->nranks > 1)
+        for (int j = 0; j < KL; ++j)
+          for (int64_t r = c->subs[j].wvu_row; r < c->subs[j].wvu_row + sh[j].b && !blk_sh[j]; ++r)
+            for (int32_t q = A2G.rowptr[r]; q < A2G.rowptr[r + 1]; ++q)
+              if (A2G.col[q] >= c->n_priv) {
+                blk_sh[j] = 1;
+                break;
+              }
       std::vector<int2> items;
-      for (int j = 0; j < KL; ++j)
-        for (int I = 0; I < sh[j].ntb; ++I) items.push_back(make_int2(j, I));
+      for (int pass = 0; pass < 2; ++pass)
+        for (int j = 0; j < KL; ++j)
+          if (blk_sh[j] == (pass == 0 ? 1 : 0))
+            for (int I = 0; I < sh[j].ntb; ++I) items.push_back(make_int2(j, I));
       c->n_items = (int)items.size();
+      c->n_items_sh = 0;
+      for (int j = 0; j < KL; ++j)
+        if (blk_sh[j]) c->n_items_sh += sh[j].ntb;
       if ((st = upload(c, &c->d_items, items)) != NSP_OK) return st;
       NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     }
