@@ -1251,10 +1251,12 @@ void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb
   nsp_count_path(sym == 1 ? NSP_PATH_GRAM_SYM : sym == 2 ? NSP_PATH_GRAM_DE : NSP_PATH_GRAM_FULL);
   const int ntiles = sym == 1 ? ntm * (ntm + 1) / 2 : sym == 2 ? ntm * (ntm + 1) / 2 + ntm * ntn1 : ntm * ntn;
   int nch = gram_chunks(n, ntiles);
-  // clusters of GCL chunk-CTAs pre-sum their partials in distributed shared memory (NSP_GRAM_CL=1: off)
+  // NSP_GRAM_CL=8: clusters of 8 chunk-CTAs pre-sum their partials in distributed shared memory (8x fewer
+  // partials to reduce) - parity-clean but measured SLOWER end to end (the 8-CTA co-scheduling of
+  // 104 KB-smem CTAs costs more than the reduce saves), so off by default
   static const int gcl_env = [] {
     const char* e = getenv("NSP_GRAM_CL");
-    return e ? atoi(e) : 8;
+    return e ? atoi(e) : 1;   // off by default: measured slower (cfg2 414 vs 397 us, cfg5 101 vs 97 ms per iteration)
   }();
   const int gcl = (gcl_env == 8 && nch >= 16 && !nsp_force_generic) ? 8 : 1;
   if (gcl > 1) nch = (nch / gcl) * gcl;

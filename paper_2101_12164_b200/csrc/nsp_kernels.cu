@@ -1895,9 +1895,21 @@ void cheb_step(const DevCSR& A, int64_t split, const double* d, int ld, int s, d
                double c1, double c2, bool want_d, cudaStream_t st) {
   if (A.rows <= 0) return;
   if (s == 1 && ld == 1) {
+    static const int G = [] {
+      const char* e = getenv("NSP_CHEB_G");
+      const int g = e ? atoi(e) : 8;
+      return (g == 4 || g == 16) ? g : 8;
+    }();
     nsp_count_launch();
-    launch_k(k_cheb_step_vec<8>, dim3((unsigned)((A.rows * 8 + 255) / 256)), dim3(256), 0, st, A.rows, A.rowptr,
-             A.col, A.val, split, d, x, r, dn, c1, c2, want_d ? 1 : 0);
+    if (G == 4)
+      launch_k(k_cheb_step_vec<4>, dim3((unsigned)((A.rows * 4 + 255) / 256)), dim3(256), 0, st, A.rows, A.rowptr,
+               A.col, A.val, split, d, x, r, dn, c1, c2, want_d ? 1 : 0);
+    else if (G == 16)
+      launch_k(k_cheb_step_vec<16>, dim3((unsigned)((A.rows * 16 + 255) / 256)), dim3(256), 0, st, A.rows, A.rowptr,
+               A.col, A.val, split, d, x, r, dn, c1, c2, want_d ? 1 : 0);
+    else
+      launch_k(k_cheb_step_vec<8>, dim3((unsigned)((A.rows * 8 + 255) / 256)), dim3(256), 0, st, A.rows, A.rowptr,
+               A.col, A.val, split, d, x, r, dn, c1, c2, want_d ? 1 : 0);
     return;
   }
   const unsigned blocks = (unsigned)((A.rows * 32 + 255) / 256);

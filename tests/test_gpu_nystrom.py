@@ -207,7 +207,8 @@ def test_nystrom_m1_full_rank_closed_form_gpu(order):
     below eq:Rt_S-1_R, independent of R_G's ordering: RCM (0) and natural (1) factors), and M_1 ~ S_G^{-1}:
     the outer PCG needs at most a few iterations.  Tolerance: with s = rank the sketch Omega^T A Omega is
     square and its condition number (1e6 natural, 9e8 RCM for this Omega, computed in fp64 on the host)
-    multiplies the 1e-13 inner residual into Sigma: the top 20 are compared at 1e-8 (natural) / 1e-4
+    multiplies the 1e-13 inner residual into Sigma (1e6 x 1e-13 = 1e-7; measured 3.5e-8 once the block CG's
+    rounding association changed, reading R9): the top 20 are compared at 1e-7 (natural) / 1e-4
     (RCM; the oracle with exact solves and an RCM-ordered R_G already loses 1e-11 there)."""
     import scipy.linalg as sl
     from nsp_inputs import philox
@@ -222,7 +223,7 @@ def test_nystrom_m1_full_rank_closed_form_gpu(order):
     ctx.nystrom(rk, 0, dev(Om), 1e-13, 200)
     sig = ctx.nystrom_sigma()
     assert len(sig) == rk
-    assert np.allclose(sig[:20], ref[:20], rtol=1e-8 if order == 1 else 1e-4), (sig[:4], ref[:4])
+    assert np.allclose(sig[:20], ref[:20], rtol=1e-7 if order == 1 else 1e-4), (sig[:4], ref[:4])
     b = pr.rhs()
     x = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
     rp = ctx.pcg(dev(b), x, 1e-8, 50, precond=2)
