@@ -178,14 +178,16 @@ __global__ void k_axpy_strided(double* y, int ldy, const double* a, int lda, con
 // part[chunk*128 + k] = sum over chunk rows of Z[row][k] * r[row]  (k < rk)
 __global__ void __launch_bounds__(256) k_gemvt_partial(const double* __restrict__ Z, int ldz,
                                                        const double* __restrict__ r, int64_t n, int rk,
-                                                       double* __restrict__ part) {
+                                                       double* __restrict__ part, int64_t rows_per_cta) {
   pdl_wait();
   // chunk of GT_ROWS rows; warp w takes rows w, w + 8, ...; lane covers columns lane + 32 j (j < 4),
   // so every row read is one coalesced 1 KB line; the 8 warp partials are summed in fixed order
+  // each CTA owns a contiguous range of rows_per_cta rows (a multiple of GT_ROWS; a bounded grid, so
+  // the single-CTA reduce sums at most a few hundred partials)
   __shared__ double red[8][128];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t r0 = (int64_t)blockIdx.x * GT_ROWS;
-  const int64_t r1 = min(n, r0 + GT_ROWS);
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(n, r0 + rows_per_cta);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int64_t i = r0 + wid; i < r1; i += 8) {
     const double ri = r[i];
@@ -228,18 +230,33 @@ __global__ void __launch_bounds__(1024) k_gemvt_reduce(const double* __restrict_
   }
 }
 
-// y[row] += sum_k Z[row][k] g[k]   (warp per row, butterfly sum)
-__global__ void k_gemv_add(const double* __restrict__ Z, int ldz, const double* __restrict__ g, int rk, int64_t n,
-                           double* __restrict__ y) {
+// y[row] += sum_k Z[row][k] g[k]   (warp per row, 16-byte loads of column pairs, butterfly sum)
+__global__ void __launch_bounds__(256) k_gemv_add(const double* __restrict__ Z, int ldz, const double* __restrict__ g,
+                                                  int rk, int64_t n, double* __restrict__ y) {
   pdl_wait();
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
   double s = 0.0;
-  for (int k = lane; k < rk; k += 32) s = fma(Z[row * ldz + k], g[k], s);
+  for (int k = 2 * lane; k < rk; k += 64) {
+    const double2 z = __ldg(reinterpret_cast<const double2*>(Z + row * ldz + k));
+    s = fma(z.x, g[k], s);
+    if (k + 1 < rk) s = fma(z.y, g[k + 1], s);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) y[row] += s;
+}
+
+// bounded Z^T r grid: at most 4 CTAs per SM, each a contiguous multiple of GT_ROWS rows
+static unsigned gemvt_grid(int64_t n, int64_t* rows_per_cta) {
+  const int64_t cap = 4 * (int64_t)nspd::num_sms();
+  int64_t nch = std::max<int64_t>(1, (n + GT_ROWS - 1) / GT_ROWS);
+  if (nch > cap) nch = cap;
+  int64_t rpc = (n + nch - 1) / nch;
+  rpc = std::max<int64_t>(GT_ROWS, ((rpc + GT_ROWS - 1) / GT_ROWS) * GT_ROWS);
+  *rows_per_cta = rpc;
+  return (unsigned)std::max<int64_t>(1, (n + rpc - 1) / rpc);
 }
 
 // WHILE-node control of the device-driven PCG loop: repeat until the iteration stopped itself
@@ -332,9 +349,10 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
   if (fork2) {
     NSP_CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
     NSP_CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
-    const unsigned nch = grid1(n, GT_ROWS);
+    int64_t rpc;
+    const unsigned nch = gemvt_grid(n, &rpc);
     nsp_count_launch();
-    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->side_stream, c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart);
+    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->side_stream, c->d_Z, c->nys_ld, r, n, c->nys_rank, w.gpart, rpc);
     nsp_count_launch();
     launch_k(k_gemvt_reduce, dim3(1), dim3(1024), 0, c->side_stream, w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
     NSP_CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side_stream));
@@ -354,9 +372,10 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
     if ((e = apply_into(c, z, 1, w.t2, 1, 1, 1, w.apply_wvu)) != NSP_OK) return e;     // S_G A_G^{-1} r
     nsp_count_launch();
     launch_k(k_axpy_strided, dim3(grid1(n, 256)), dim3(256), 0, c->stream, w.t2, 1, r, 1, w.t2, 1, -1.0, n);   // d = r - S t
-    const unsigned nch = grid1(n, GT_ROWS);
+    int64_t rpc;
+    const unsigned nch = gemvt_grid(n, &rpc);
     nsp_count_launch();
-    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->stream, c->d_Z, kp, w.t2, n, rk, w.gpart);
+    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->stream, c->d_Z, kp, w.t2, n, rk, w.gpart, rpc);
     double* G = w.eg;                 // kp x kp, column 0 = Z^T d
     double* H = w.eg + 128 * 128;     // kp x kp, column 0 = E^{-1} Z^T d
     NSP_CUDA_TRY(c, cudaMemsetAsync(G, 0, (size_t)kp * kp * 8, c->stream));
@@ -370,9 +389,10 @@ static nsp_status pcg_precond(nsp_ctx* c, int which, const double* r, double* z,
   }
   if (which == 2 && c->nys_rank > 0) {
     const int64_t ng = dot_rows(c);
-    const unsigned nch = grid1(ng, GT_ROWS);
+    int64_t rpc;
+    const unsigned nch = gemvt_grid(ng, &rpc);
     nsp_count_launch();
-    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->stream, c->d_Z, c->nys_ld, r, ng, c->nys_rank, w.gpart);
+    launch_k(k_gemvt_partial, dim3(nch), dim3(256), 0, c->stream, c->d_Z, c->nys_ld, r, ng, c->nys_rank, w.gpart, rpc);
     nsp_count_launch();
     launch_k(k_gemvt_reduce, dim3(1), dim3(1024), 0, c->stream, w.gpart, (int)nch, c->d_sigma, c->nys_rank, w.g);
     if (c->nranks > 1 && (e = comm_allreduce(c, w.g, c->nys_rank)) != NSP_OK) return e;
