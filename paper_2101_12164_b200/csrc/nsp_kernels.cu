@@ -1895,13 +1895,18 @@ void cheb_step(const DevCSR& A, int64_t split, const double* d, int ld, int s, d
                double c1, double c2, bool want_d, cudaStream_t st) {
   if (A.rows <= 0) return;
   if (s == 1 && ld == 1) {
+    // lanes per row: cfg5 outer PCG (M_2, 91 its) 15.04 / 17.56 / 23.34 ms per iteration with 4 / 8 / 16
+    // lanes (the unfused SpMV + update: 16.54 ms)
     static const int G = [] {
       const char* e = getenv("NSP_CHEB_G");
-      const int g = e ? atoi(e) : 8;
-      return (g == 4 || g == 16) ? g : 8;
+      const int g = e ? atoi(e) : 4;
+      return (g == 2 || g == 8 || g == 16) ? g : 4;
     }();
     nsp_count_launch();
-    if (G == 4)
+    if (G == 2)
+      launch_k(k_cheb_step_vec<2>, dim3((unsigned)((A.rows * 2 + 255) / 256)), dim3(256), 0, st, A.rows, A.rowptr,
+               A.col, A.val, split, d, x, r, dn, c1, c2, want_d ? 1 : 0);
+    else if (G == 4)
       launch_k(k_cheb_step_vec<4>, dim3((unsigned)((A.rows * 4 + 255) / 256)), dim3(256), 0, st, A.rows, A.rowptr,
                A.col, A.val, split, d, x, r, dn, c1, c2, want_d ? 1 : 0);
     else if (G == 16)
