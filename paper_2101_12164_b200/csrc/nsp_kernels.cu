@@ -1856,8 +1856,18 @@ void spmm_cs(const DevCSR& A, const double* X, int ldx, const double* U, int ldu
   if (A.rows <= 0) return;
   const unsigned blocks = (unsigned)((A.rows * 32 + 255) / 256);
   if (s == 1 && ycs == 32 && ucs == 32) {
-    const unsigned b8 = (unsigned)((A.rows * 8 + 255) / 256);
-    { nsp_count_launch(); launch_k(k_spmv<8>, dim3(b8), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, mode, zero_pad); }
+    static const int G = [] {
+      const char* e = getenv("NSP_SPMV_G");
+      const int g = e ? atoi(e) : 8;
+      return (g == 2 || g == 4) ? g : 8;
+    }();
+    nsp_count_launch();
+    if (G == 2)
+      launch_k(k_spmv<2>, dim3((unsigned)((A.rows * 2 + 255) / 256)), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, mode, zero_pad);
+    else if (G == 4)
+      launch_k(k_spmv<4>, dim3((unsigned)((A.rows * 4 + 255) / 256)), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, mode, zero_pad);
+    else
+      launch_k(k_spmv<8>, dim3((unsigned)((A.rows * 8 + 255) / 256)), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, split, Y, ldy, mode, zero_pad);
     return;
   }
   static const int vmode = [] {
