@@ -84,3 +84,56 @@ def test_degenerate_block_cg_and_pcg(deg):
         assert r["converged"], (prec, r)
         assert _rel(x.cpu().numpy(), xd) <= 1e-9, prec
     ctx.close()
+
+
+def test_round2_abi_error_paths():
+    """Round-2 entry points fail loudly on bad use: M = A_G^{-1} without the A_G operator (NSP_ERR_STATE),
+    an out-of-range M, an explicit-Omega-only Nystrom form called with Omega = NULL (NSP_ERR_ARG), kernel
+    entries with unsupported widths / too-small fused shapes (NSP_ERR_ARG), a bad fused-pass mode."""
+    from paper_2101_12164_b200 import nsp
+    from paper_2101_12164_b200.nsp import NspError
+    from nsp_inputs import problems as P
+    pr = P.make("cfg1")
+    ctx = Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K)
+    with pytest.raises(NspError, match="NSP_ERR_STATE"):
+        ctx.set_bcg_precond(1)
+    with pytest.raises(NspError, match="NSP_ERR_ARG"):
+        ctx.set_bcg_precond(2)
+    ctx.close()
+    ctx = Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, factor_gamma=True, nys_form=3, ag_order=1)
+    with pytest.raises(NspError, match="NSP_ERR_ARG"):
+        ctx.nystrom(pr.rank, pr.oversample, None, 0.1, 50)
+    ctx.close()
+    X = torch.zeros(100, 32, dtype=torch.float64, device="cuda")
+    M = torch.zeros(32, 32, dtype=torch.float64, device="cuda")
+    with pytest.raises(NspError):
+        nsp.dev_panel(X, None, X, M, 1.0)                     # s = 32: not a supported width
+    Y = torch.zeros(100, 128, dtype=torch.float64, device="cuda")
+    G = torch.zeros(128, 128, dtype=torch.float64, device="cuda")
+    with pytest.raises(NspError):
+        nsp.dev_panel_gram(Y, None, Y, G, 1.0, 0, G)          # n < 64 x SMs: no fused shape
+    with pytest.raises(NspError):
+        nsp.dev_set_fused_pg(3)
+
+
+def test_block_cg_precond_switch_reuses_context():
+    """nsp_set_bcg_precond switches M on one context (the bench times both modes on one cfg5 context):
+    each mode gives the same iterations and X as a context built for that mode (bitwise: same kernels)."""
+    from nsp_inputs import problems as P
+    pr = P.make("cfg2s")
+    d = O.dbbd(pr.A.to_scipy(), pr.part, pr.K)
+    B = _dev(O.SchurOracle(d).k_gamma(pr.omega()))
+    ctx = Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, factor_gamma=True)
+    out = {}
+    for m in (0, 1, 0):
+        ctx.set_bcg_precond(m)
+        X = torch.zeros_like(B)
+        rep = ctx.block_cg(B, X, pr.tol_bcg, 500)
+        out.setdefault(m, []).append((rep["iters"], X.cpu().numpy()))
+    ctx.close()
+    assert out[0][0][0] == out[0][1][0] and np.array_equal(out[0][0][1], out[0][1][1])
+    ref = Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, bcg_precond=1)
+    X = torch.zeros_like(B)
+    rep = ref.block_cg(B, X, pr.tol_bcg, 500)
+    ref.close()
+    assert rep["iters"] == out[1][0][0] and np.array_equal(X.cpu().numpy(), out[1][0][1])
