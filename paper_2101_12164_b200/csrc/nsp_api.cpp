@@ -250,6 +250,7 @@ nsp_status nsp_workspace_bytes(const nsp_ctx* c, int s, size_t* bytes) {
 }
 
 nsp_status nsp_schur_apply(nsp_ctx* c, const double* X, double* Y, int s, void* ws) {
+  NspNvtx nvtx_range_("nsp_schur_apply");
   if (!c || !X || !Y || s <= 0 || s > 256) return NSP_ERR_ARG;
   char* w;
   nsp_status st = get_ws(c, ws, apply_ws_bytes(c, s), &w);
@@ -258,6 +259,7 @@ nsp_status nsp_schur_apply(nsp_ctx* c, const double* X, double* Y, int s, void* 
 }
 
 nsp_status nsp_kgamma_apply(nsp_ctx* c, const double* X, double* Y, int s, void* ws) {
+  NspNvtx nvtx_range_("nsp_kgamma_apply");
   if (!c || !X || !Y || s <= 0 || s > 256) return NSP_ERR_ARG;
   char* w;
   nsp_status st = get_ws(c, ws, apply_ws_bytes(c, s), &w);
@@ -266,6 +268,7 @@ nsp_status nsp_kgamma_apply(nsp_ctx* c, const double* X, double* Y, int s, void*
 }
 
 nsp_status nsp_gamma_apply(nsp_ctx* c, const double* X, double* Y, int s) {
+  NspNvtx nvtx_range_("nsp_gamma_apply");
   if (!c || !X || !Y || s <= 0 || s > 256) return NSP_ERR_ARG;
   nspk::spmm(c->AGG2, X, s, nullptr, 0, c->nG, Y, s, s, 3, false, c->stream);
   NSP_CUDA_TRY(c, cudaGetLastError());

@@ -7,6 +7,14 @@
 #include <vector>
 
 #include "../../include/nsp.h"
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX range around an ABI call (tracing: visible in nsys / ncu --nvtx timelines; header-only NVTX3,
+// a no-op unless a tool is attached)
+struct NspNvtx {
+  explicit NspNvtx(const char* name) { nvtxRangePushA(name); }
+  ~NspNvtx() { nvtxRangePop(); }
+};
 
 #define NSP_TILE 64          // factor tile edge (rows = cols)
 #define NSP_TILE_ELEMS (NSP_TILE * NSP_TILE)

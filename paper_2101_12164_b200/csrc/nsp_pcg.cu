@@ -721,6 +721,7 @@ using namespace nspi;
 
 extern "C" nsp_status nsp_pcg(nsp_ctx* c, const double* b, double* x, double tol, int maxit, int precond, void* ws,
                               nsp_report* rep) {
+  NspNvtx nvtx_range_("nsp_pcg");
   if (!c || !b || !x || maxit < 0 || precond < 0 || precond > 3) {
     if (c) c->err = "nsp_pcg: bad arguments (precond in {0, 1, 2, 3})";
     return NSP_ERR_ARG;

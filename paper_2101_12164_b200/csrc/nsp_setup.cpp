@@ -581,6 +581,7 @@ extern "C" nsp_status nsp_shard_plan(const nsp_csr* A, const int32_t* part, int 
 
 extern "C" nsp_status nsp_setup(const nsp_csr* A, const int32_t* part, int K, const nsp_opts* opts,
                                 nsp_ctx** out, nsp_report* rep) {
+  NspNvtx nvtx_range_("nsp_setup");
   if (!out) return NSP_ERR_ARG;
   *out = nullptr;
   nsp_ctx* c = new nsp_ctx();

@@ -775,6 +775,7 @@ extern "C" {
 
 nsp_status nsp_block_cg(nsp_ctx* c, const double* B, double* X, int s, double tol, int maxit, void* ws,
                         nsp_report* rep) {
+  NspNvtx nvtx_range_("nsp_block_cg");
   if (!c || !B || !X || s <= 0 || s > 128 || maxit < 0) {
     if (c) c->err = "nsp_block_cg: bad arguments (1 <= s <= 128)";
     return NSP_ERR_ARG;
@@ -791,6 +792,7 @@ nsp_status nsp_block_cg(nsp_ctx* c, const double* B, double* X, int s, double to
 // eps split, descending T eigenpairs, rank = min(r, k)).
 nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, const double* Omega, double tol_inner,
                        int maxit_inner, void* ws, nsp_report* rep) {
+  NspNvtx nvtx_range_("nsp_nystrom");
   const int s = rank + oversample;
   if (!c || rank <= 0 || oversample < 0 || s > 128 || maxit_inner < 0) {
     if (c) c->err = "nsp_nystrom: bad arguments (rank > 0, rank + oversample <= 128)";
@@ -1108,6 +1110,7 @@ nsp_status nsp_nystrom_sigma(const nsp_ctx* c, double* sigma, int* rank_out) {
 }
 
 nsp_status nsp_precond_apply(nsp_ctx* c, int which, const double* X, double* Y, int s, void* ws) {
+  NspNvtx nvtx_range_("nsp_precond_apply");
   if (!c || !X || !Y || s <= 0 || s > 128 || which < 0 || which > 4) return NSP_ERR_ARG;
   if (which == 0) {
     NSP_CUDA_TRY(c, cudaMemcpyAsync(Y, X, (size_t)c->nG * s * 8, cudaMemcpyDeviceToDevice, c->stream));
