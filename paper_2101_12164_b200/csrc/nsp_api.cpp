@@ -417,7 +417,7 @@ void nsp_destroy(nsp_ctx* c) {
   if (c->ev_ajoin) cudaEventDestroy(c->ev_ajoin);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
-  for (DevCSR* m : {&c->A2G, &c->AGG2, &c->AGSH, &c->CB, &c->C1, &c->AII}) {
+  for (DevCSR* m : {&c->A2G, &c->AGG2, &c->AGSH, &c->AGO, &c->CB, &c->C1, &c->AII}) {
     fr(m->rowptr);
     fr(m->col);
     fr(m->val);

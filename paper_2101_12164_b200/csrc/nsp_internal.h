@@ -121,6 +121,8 @@ struct nsp_ctx {
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
   DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)
+  DevCSR AGO;                 // one rank: A_G alone (the cols < nG prefix of every AGG2 row) - the
+                              // Chebyshev A_G^{-1} steps read only these entries
   int64_t n_priv = 0;         // local Gamma rows [0, n_priv) private, [n_priv, nG) shared (replicated)
   struct NspComm* comm = nullptr;
 

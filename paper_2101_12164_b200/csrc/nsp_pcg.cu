@@ -64,6 +64,8 @@ __global__ void __launch_bounds__(RT) k_dot2_partial(const double* __restrict__ 
 //   sc[0], sc[1]: r.z (ping-pong by iteration parity)   sc[2]: p.q   sc[3]: r.r   sc[4]: ||f||
 // mode 0: out slot = sum (q = 0);   mode 1: out slot = sum (q = 0), status relres / converged from
 // sum = r.r;  mode 2: ||f|| (sqrt of sum) and the initial status.
+__device__ __forceinline__ void dot_status(double v, int mode, double* sc, int slot, double tol, BcgStatus* st,
+                                           double* hist, int hist_mod);
 __global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ part, int nblk, double* sc, int slot,
                                                    int mode, double tol, BcgStatus* st, double* hist,
                                                    int hist_mod) {
@@ -81,6 +83,12 @@ __global__ void __launch_bounds__(RT) k_dot_reduce(const double* __restrict__ pa
   if (threadIdx.x != 0) return;
   // nblk < 0: the sum was formed beforehand (several ranks: summed over ranks) in sc[-nblk - 1]
   const double v = nblk < 0 ? sc[-nblk - 1] : red[0];
+  dot_status(v, mode, sc, slot, tol, st, hist, hist_mod);
+}
+
+// the scalar / status update of k_dot_reduce for the reduced value v (one thread)
+__device__ __forceinline__ void dot_status(double v, int mode, double* sc, int slot, double tol, BcgStatus* st,
+                                           double* hist, int hist_mod) {
   if (mode == 0) {
     sc[slot] = v;
   } else if (mode == 1) {
@@ -124,10 +132,12 @@ __global__ void __launch_bounds__(RT) k_pcg_xr_f(double* __restrict__ x, double*
                                                  const double* __restrict__ p, const double* __restrict__ q,
                                                  int64_t n, double* sc, int cur,
                                                  const double* __restrict__ pq_part, int nblk,
-                                                 double* __restrict__ part, BcgStatus* st, int64_t ngram) {
+                                                 double* __restrict__ part, BcgStatus* st, int64_t ngram,
+                                                 unsigned* done_ctr, double tol, double* hist, int hist_mod) {
   pdl_wait();
   __shared__ double red[RT];
   __shared__ double bc;
+  __shared__ bool last;
   if (st->done) return;
   const double pq = cta_sum_partials(pq_part, nblk, &bc);
   const double alpha = pq > 0.0 ? sc[cur] / pq : 0.0;
@@ -150,6 +160,28 @@ __global__ void __launch_bounds__(RT) k_pcg_xr_f(double* __restrict__ x, double*
     __syncthreads();
   }
   if (threadIdx.x == 0) part[blockIdx.x * 2] = red[0];
+  if (!done_ctr) return;
+  // one rank: the LAST CTA to finish sums the r.r partials in k_dot_reduce's fixed order (bitwise the same
+  // value) and updates the status - no separate reduce launch
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nblk_out = (int)gridDim.x;
+  double t = 0.0;
+  for (int b = threadIdx.x; b < nblk_out; b += RT) t += ((volatile double*)part)[b * 2];
+  red[threadIdx.x] = t;
+  __syncthreads();
+  for (int w = RT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *done_ctr = 0u;
+    dot_status(red[0], 1, sc, 3, tol, st, hist, hist_mod);
+  }
 }
 
 // p = z + beta p with the r.z reduction folded in: rz_new = sum(partials), beta = rz_new / sc[cur];
@@ -277,6 +309,7 @@ struct PcgWs {
   double *i1r, *i1buf;                     // band rows x 32
   double *agbuf, *apply_wvu, *part, *part2, *gpart, *g, *sc, *hist;
   BcgStatus* st;
+  unsigned* ctr;   // last-CTA counter of k_pcg_xr_f (zero between uses)
 };
 
 static size_t pcg_layout(const nsp_ctx* c, char* base, PcgWs* out) {
@@ -314,6 +347,7 @@ static size_t pcg_layout(const nsp_ctx* c, char* base, PcgWs* out) {
   w.sc = take(16);
   w.hist = take(PCG_CHUNK);
   w.st = (BcgStatus*)take(sizeof(BcgStatus) / 8 + 1);
+  w.ctr = (unsigned*)take(1);
   if (out) *out = w;
   return ((off + 255) & ~size_t(255)) + 256;
 }
@@ -456,6 +490,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
   std::memcpy(hs, &init, sizeof(init));
   NSP_CUDA_TRY(c, cudaMemcpyAsync(w.st, hs, sizeof(BcgStatus), cudaMemcpyHostToDevice, st));
   NSP_CUDA_TRY(c, cudaMemsetAsync(w.w, 0, (size_t)std::max<int64_t>(n, 1) * 8, st));
+  NSP_CUDA_TRY(c, cudaMemsetAsync(w.ctr, 0, sizeof(unsigned), st));
   NSP_CUDA_TRY(c, cudaMemcpyAsync(w.r, w.f, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
   if (multi) {   // ||f||^2 summed over ranks (slot 5), then the status from it
     if ((e = dot(c, w.f, w.f, ng, w, 5)) != NSP_OK) return e;
@@ -491,7 +526,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
         if ((e2 = dot(c, w.p, w.q, ng, w, 6)) != NSP_OK) return e2;                           // p.q
         nsp_count_launch();
         launch_k(k_pcg_xr_f, dim3(nb), dim3(RT), 0, q, w.w, w.r, w.p, w.q, n, w.sc, cur, (const double*)(w.sc + 6), -1,
-                 w.part2, w.st, ng);
+                 w.part2, w.st, ng, (unsigned*)nullptr, tol, hist_dev, hist_mod);
         nsp_count_launch();
         launch_k(k_dot_reduce, dim3(1), dim3(RT), 0, q, w.part2, (int)nb, w.sc, 7, 0, 0.0, w.st, hist_dev, hist_mod);
         if ((e2 = comm_allreduce(c, w.sc + 7, 1)) != NSP_OK) return e2;                       // r.r
@@ -510,9 +545,7 @@ nsp_status pcg_impl(nsp_ctx* c, const double* b, double* x, double tol, int maxi
       launch_k(k_dot2_partial, dim3(nb), dim3(RT), 0, q, w.p, w.q, nullptr, nullptr, n, w.part);
       nsp_count_launch();
       launch_k(k_pcg_xr_f, dim3(nb), dim3(RT), 0, q, w.w, w.r, w.p, w.q, n, w.sc, cur, w.part, (int)nb, w.part2, w.st,
-               n);
-      nsp_count_launch();
-      launch_k(k_dot_reduce, dim3(1), dim3(RT), 0, q, w.part2, (int)nb, w.sc, 3, 1, tol, w.st, hist_dev, hist_mod);
+               n, w.ctr, tol, hist_dev, hist_mod);   // + the r.r reduce and status (last CTA)
       if ((e2 = pcg_precond(c, precond, w.r, w.z, w)) != NSP_OK) return e2;
       // r.z partials; the sum (and beta) inside k_pcg_p_f
       nsp_count_launch();

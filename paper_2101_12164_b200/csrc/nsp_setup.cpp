@@ -1084,6 +1084,18 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
   if ((st = upload_csr(c, c->A2G, A2G)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->AGG2, AGG2)) != NSP_OK) return st;
   if ((st = upload_csr(c, c->AGSH, AGSH)) != NSP_OK) return st;
+  if (c->nranks == 1 && c->opts.factor_gamma) {   // A_G alone for the Chebyshev steps (rows are col-sorted)
+    HostCSR32 AGO;
+    AGO.rowptr.assign(c->nG + 1, 0);
+    for (int64_t g = 0; g < c->nG; ++g) {
+      for (int32_t q = AGG2.rowptr[g]; q < AGG2.rowptr[g + 1] && AGG2.col[q] < c->nG; ++q) {
+        AGO.col.push_back(AGG2.col[q]);
+        AGO.val.push_back(AGG2.val[q]);
+      }
+      AGO.rowptr[g + 1] = (int32_t)AGO.col.size();
+    }
+    if ((st = upload_csr(c, c->AGO, AGO)) != NSP_OK) return st;
+  }
   if ((st = upload_csr(c, c->CB, CB)) != NSP_OK) return st;
   if (!AII.rowptr.empty()) {
     if ((st = upload_csr(c, c->AII, AII)) != NSP_OK) return st;

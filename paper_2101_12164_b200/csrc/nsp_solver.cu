@@ -666,7 +666,8 @@ static nsp_status ag_cheb(nsp_ctx* c, const double* X, int ldx, double* Y, int l
   static const bool fused_off = getenv("NSP_CHEB_FUSED") && getenv("NSP_CHEB_FUSED")[0] == '0';
   for (int k = 0; k < c->cheb_K; ++k) {
     if (c->nranks == 1 && !fused_off && (ld == 1 || ld % 2 == 0)) {   // product and update in one pass
-      nspk::cheb_step(c->AGG2, n, d0, ld, s, xw, r, d1, c->cheb_c1[k], c->cheb_c2[k], k + 1 < c->cheb_K, st);
+      nspk::cheb_step(c->AGO.rows ? c->AGO : c->AGG2, n, d0, ld, s, xw, r, d1, c->cheb_c1[k], c->cheb_c2[k],
+                      k + 1 < c->cheb_K, st);
       std::swap(d0, d1);
       continue;
     }
