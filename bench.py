@@ -364,10 +364,15 @@ def measure(pr, args, ws, rank, local, stream, nccl_id, headline):
     Q_ = torch.empty_like(P_)
     at = [t for t, _ in _timed(stream, lambda: ctx.schur_apply(P_, Q_, wsbuf), flush, args.apply_reps + 3)[3:]]
     t_apply = statistics.median(at)
+    tg = [t for t, _ in _timed(stream, lambda: ctx.gamma_apply(P_, Q_), flush, args.apply_reps + 3)[3:]]
+    t_gamma = statistics.median(tg)
     out["apply"] = {"ms": t_apply, "rhs_applies_per_s": s / (t_apply * 1e-3),
-                    "a2a3_tflops": 2.0 * st["sum_b2"] * s / (t_apply * 1e-3) / 1e12}
-    out["iteration_split_ms"] = {"iteration": out["iteration_ms"], "apply": t_apply,
-                                 "grams_panels_sxs": out["iteration_ms"] - t_apply}
+                    "a2a3_tflops": 2.0 * st["sum_b2"] * s / (t_apply * 1e-3) / 1e12, "gamma_apply_ms": t_gamma}
+    # one block-CG iteration: the step minus its a0 (K_G Omega, one apply) and a12 (A_G X), per iteration
+    it_ms = (out["time_to_tol_ms"] - t_apply - t_gamma) / max(out["bcg_iters"], 1)
+    out["iteration_ms"] = it_ms
+    out["iteration_split_ms"] = {"iteration": it_ms, "apply": t_apply, "grams_panels_sxs": it_ms - t_apply,
+                                 "step_outside_loop": t_apply + t_gamma}
     # e2e: Omega from pinned host memory, Y back to pinned host memory, inside the timed region
     def step_e2e():
         Om.copy_(Om_h, non_blocking=True)
