@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnsp.so")
+LIB_PATH = os.environ.get("NSP_LIB") or os.path.join(_HERE, "libnsp.so")   # NSP_LIB: tuning variants only
 
 NSP_STATUS = {0: "NSP_OK", 1: "NSP_NOT_CONVERGED", -1: "NSP_ERR_ARG", -2: "NSP_ERR_NOT_SPD",
               -3: "NSP_ERR_INDEFINITE", -4: "NSP_ERR_STAGNATION", -5: "NSP_ERR_RANK_COLLAPSE",
