@@ -397,6 +397,109 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t
         ((red[threadIdx.x] + red[128 + threadIdx.x]) + red[256 + threadIdx.x]) + red[384 + threadIdx.x];
 }
 
+// The s = 128 panel with TWO CTAs per SM: CTA 2g + h owns the rows of group g (one contiguous range of
+// 16-row groups per pair, as k_panel_rows) and the output columns 64h .. 64h + 63, so its share of the
+// multiplier M[:, 64h:64h+64] (68 KB) and a 2-stage ring of 64 x 32 In chunks fit twice per SM.  8 warps
+// = 4 row groups x 2 column quarters (16 x 32 per warp); 4 k-chunks per 64-row pass.  While one CTA of an
+// SM waits at a barrier or in its epilogue the other's products keep the DMMA pipe busy (k_panel_rows:
+// one 16-warp CTA per SM, every warp in lockstep).  normpart as k_panel_rows (row g, 128 columns).
+constexpr int HKC = 32, HLDM = 68, HLDA = 36, HSPP = 128 / HKC;
+__global__ void __launch_bounds__(256, 2) k_panel_half(PanelArgs pa, int64_t n, int64_t ngroups) {
+  constexpr int NF = 4;
+  pdl_wait();
+  extern __shared__ __align__(16) double sm[];
+  double* Ms = sm;                  // 128 x HLDM: M[:, c0 .. c0 + 64)
+  double* Ar = sm + 128 * HLDM;     // 2 x 64 x HLDA
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rg = warp >> 1, cb = (warp & 1) * 32;
+  const int grp = blockIdx.x >> 1, c0 = (blockIdx.x & 1) * 64;
+  const int ngrp = gridDim.x >> 1;
+  const int64_t g0 = (int64_t)grp * ngroups / ngrp;
+  const int64_t g1 = (int64_t)(grp + 1) * ngroups / ngrp;
+  const int64_t r0 = g0 * 16, r1 = min(n, g1 * 16);
+  const int npass = r1 > r0 ? (int)((r1 - r0 + 63) / 64) : 0;
+  const int nsteps = npass * HSPP;
+  const double* __restrict__ In = pa.In;
+  auto issue = [&](int q) {
+    const int64_t rp = r0 + (int64_t)(q / HSPP) * 64;
+    cp_block_zf(Ar + (q & 1) * 64 * HLDA, HLDA, In + rp * pa.ldi + (q % HSPP) * HKC, pa.ldi, 64, HKC, r1 - rp);
+  };
+  cp_block(Ms, HLDM, pa.M + c0, pa.ldm, 128, 64);
+  if (nsteps > 0) issue(0);
+  cp_commit();
+  double acc[2][NF][2];
+  acc_zero(acc);
+  double sq[NF][2];
+#pragma unroll
+  for (int j = 0; j < NF; ++j) sq[j][0] = sq[j][1] = 0.0;
+  double2 cin[2][NF];
+  for (int q = 0; q < nsteps; ++q) {
+    const int kc = q % HSPP;
+    const int64_t rp = r0 + (int64_t)(q / HSPP) * 64;
+    if (kc == 0) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int64_t r = rp + rg * 16 + acc_row<NF>(i, 0);
+          const int c = c0 + cb + acc_col<NF>(j, 0);
+          cin[i][j] = (pa.Cin && r < r1) ? *reinterpret_cast<const double2*>(pa.Cin + r * pa.ldc + c)
+                                         : make_double2(0.0, 0.0);
+        }
+    }
+    cp_wait<0>();
+    __syncthreads();
+    if (q + 1 < nsteps) issue(q + 1);
+    cp_commit();
+    const double* As = Ar + (q & 1) * 64 * HLDA;
+    if (rp + rg * 16 < r1)
+      cta_mma<NF, false, false>(As + rg * 16 * HLDA, HLDA, Ms + kc * HKC * HLDM + cb, HLDM, acc, HKC, 0);
+    if (kc == HSPP - 1) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int64_t r = rp + rg * 16 + acc_row<NF>(i, 0);
+          const int c = c0 + cb + acc_col<NF>(j, 0);
+          if (r < r1) {
+            const double v0 = pa.sgn * acc[i][j][0] + cin[i][j].x;
+            const double v1 = pa.sgn * acc[i][j][1] + cin[i][j].y;
+            *reinterpret_cast<double2*>(pa.Out + r * pa.ldo + c) = make_double2(v0, v1);
+            sq[j][0] += v0 * v0;
+            sq[j][1] += v1 * v1;
+          }
+        }
+      acc_zero(acc);
+    }
+  }
+  if (!pa.normpart) return;
+#pragma unroll
+  for (int j = 0; j < NF; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double v = sq[j][e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      sq[j][e] = v;
+    }
+  cp_wait<0>();
+  __syncthreads();
+  double* red = Ar;   // 4 x 64
+  if (lane < 4) {
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+      const int c = cb + acc_col<NF>(j, 0);
+      red[rg * 64 + c] = sq[j][0];
+      red[rg * 64 + c + 1] = sq[j][1];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 64)
+    pa.normpart[grp * (int64_t)pa.ldo + c0 + threadIdx.x] =
+        ((red[threadIdx.x] + red[64 + threadIdx.x]) + red[128 + threadIdx.x]) + red[192 + threadIdx.x];
+}
+
 // Fused s = 128 panel + Gram partial (rows a8+a10 / a10+a11 of the block-CG iteration, one pass over
 // the tall blocks instead of two):
 //   Out = Cin + sgn In M   (the panel of k_panel_rows)   and   G_cta = Aop^T Out over the CTA's rows,
@@ -1311,6 +1414,18 @@ int panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, in
     return e && e[0] == '0';
   }();
   // one-wave row-range panel: s = 128 and at least one 64-row pass per SM (normpart rows = CTAs)
+  static const bool half_on = [] {
+    const char* e = getenv("NSP_PANEL_HALF");
+    return e && e[0] == '1';
+  }();
+  if (half_on && !rows_off && !nsp_force_generic && kdim == 128 && ncols == 128 && n >= (int64_t)64 * nsm &&
+      ldo >= 128) {
+    nsp_count_path(NSP_PATH_PANEL_ROWS);
+    const size_t smem = (128 * HLDM + 2 * 64 * HLDA) * sizeof(double);
+    smem_optin((const void*)k_panel_half, smem);
+    { nsp_count_launch(); launch_k(k_panel_half, dim3(2 * nsm), dim3(256), smem, st, a, n, (n + 15) / 16); }
+    return nsm;
+  }
   if (!rows_off && !nsp_force_generic && kdim == 128 && ncols == 128 && n >= (int64_t)64 * nsm && ldo >= 128) {
     nsp_count_path(NSP_PATH_PANEL_ROWS);
     const size_t smem = (128 * PLDM + PNS * 64 * PLDA) * sizeof(double);
