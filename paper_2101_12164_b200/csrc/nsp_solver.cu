@@ -342,7 +342,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   // orth overwrites P: it overlaps the tail's small s x s kernels.  Inside a captured graph the
   // fork / join become graph edges.
   const char* xfe = getenv("NSP_XFORK");
-  const bool xfork = !multi && !tr.on && !(xfe && xfe[0] == '0');
+  const bool xfork = !tr.on && !(xfe && xfe[0] == '0');   // (several ranks too: no collective in it)
   if (xfork) {
     if (!c->side_stream) NSP_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
     if (!c->ev_fork) NSP_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
