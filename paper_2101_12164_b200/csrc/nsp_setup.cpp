@@ -587,6 +587,7 @@ extern "C" nsp_status nsp_setup(const nsp_csr* A, const int32_t* part, int K, co
   nsp_ctx* c = new nsp_ctx();
   if (opts) c->opts = *opts;
   else nsp_default_opts(&c->opts);
+  if (const char* ev = getenv("NSP_VERBOSE")) c->opts.verbose = ev[0] == '1';   // diagnostics
   *out = c;
   if (!A || !part || K <= 0) return fail(c, NSP_ERR_ARG, "nsp_setup: null A/part or K <= 0");
   c->device = c->opts.device;
