@@ -399,6 +399,9 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_ELp);
   fr(c->d_int_src);
   fr(c->d_sigma);
+  fr(c->d_sell_ptr);
+  fr(c->d_sell_col);
+  fr(c->d_sell_val);
   comm_free(c);
   if (c->bcg_graph) cudaGraphExecDestroy(c->bcg_graph);
   if (c->pcg_graph) cudaGraphExecDestroy(c->pcg_graph);

@@ -123,6 +123,11 @@ struct nsp_ctx {
   DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)
   DevCSR AGO;                 // one rank: A_G alone (the cols < nG prefix of every AGG2 row) - the
                               // Chebyshev A_G^{-1} steps read only these entries
+  // the same A_G as sliced ELL (32-row slices, column-major within a slice, width = the slice's longest
+  // row, col -1 = padding): the s = 1 Chebyshev step, one thread per row with no row-pointer hop
+  int64_t* d_sell_ptr = nullptr;   // nslices + 1 element offsets
+  int32_t* d_sell_col = nullptr;
+  double* d_sell_val = nullptr;
   int64_t n_priv = 0;         // local Gamma rows [0, n_priv) private, [n_priv, nG) shared (replicated)
   struct NspComm* comm = nullptr;
 
@@ -282,6 +287,9 @@ void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, 
 // dn = c1 d + c2 r; blocks n x ld row-major (ld = 1 with s = 1)
 void cheb_step(const DevCSR& A, int64_t split, const double* d, int ld, int s, double* x, double* r, double* dn,
                double c1, double c2, bool want_d, cudaStream_t st);
+// the s = 1 step on the sliced-ELL A_G (rows = n_G)
+void cheb_step_sell(int64_t rows, const int64_t* sptr, const int32_t* col, const double* val, const double* d,
+                    double* x, double* r, double* dn, double c1, double c2, bool want_d, cudaStream_t st);
 // Gaussian block on the device, bit-compatible with nsp_inputs.philox.gaussian_block (reading C7):
 // out[r * ld + j] (j < s; columns s..ld-1 zeroed) = N(0,1) from Philox4x32-10 counter (gidx[r] * s + j,
 // stream, 0), key = seed, Box-Muller cosine branch.  gidx: device int64 row indices.

@@ -379,6 +379,33 @@ __global__ void __launch_bounds__(256) k_cheb_step_vec(int64_t rows, const int32
   if (want_d) dn[row] = fma(c1, di, c2 * ri);
 }
 
+// s = 1 on the sliced-ELL copy of A_G: one thread per row, the slice's entries column-major (coalesced
+// 32-row segments), no row-pointer hop before the index loads: the dependent chain is index -> d gather.
+__global__ void __launch_bounds__(256) k_cheb_step_sell(int64_t rows, const int64_t* __restrict__ sptr,
+                                                        const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                        const double* __restrict__ d, double* __restrict__ x,
+                                                        double* __restrict__ r, double* __restrict__ dn, double c1,
+                                                        double c2, int want_d) {
+  pdl_wait();
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const int64_t sl = row >> 5;
+  const int lane = (int)(row & 31);
+  const int64_t b = sptr[sl];
+  const int w = (int)((sptr[sl + 1] - b) >> 5);
+  double acc = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < w; ++j) {
+    const int c = col[b + j * 32 + lane];
+    if (c >= 0) acc = fma(val[b + j * 32 + lane], __ldg(d + c), acc);
+  }
+  const double di = d[row];
+  x[row] += di;
+  const double ri = r[row] - acc;
+  r[row] = ri;
+  if (want_d) dn[row] = fma(c1, di, c2 * ri);
+}
+
 template <int NQ2>
 __global__ void __launch_bounds__(256, NQ2 <= 2 ? 8 : 4) k_cheb_step_blk(int64_t rows, const int32_t* __restrict__ rp,
                                                        const int32_t* __restrict__ ci, const double* __restrict__ va,
@@ -1939,6 +1966,14 @@ void cheb_step(const DevCSR& A, int64_t split, const double* d, int ld, int s, d
   else
     launch_k(k_cheb_step_blk<4>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, split, d, ld, x, r, dn, c1,
              c2, want_d ? 1 : 0);
+}
+
+void cheb_step_sell(int64_t rows, const int64_t* sptr, const int32_t* col, const double* val, const double* d,
+                    double* x, double* r, double* dn, double c1, double c2, bool want_d, cudaStream_t st) {
+  if (rows <= 0) return;
+  nsp_count_launch();
+  launch_k(k_cheb_step_sell, dim3((unsigned)((rows + 255) / 256)), dim3(256), 0, st, rows, sptr, col, val, d, x, r, dn,
+           c1, c2, want_d ? 1 : 0);
 }
 
 void philox_gaussian(double* out, int64_t rows, int s, int ld, const int64_t* gidx, uint64_t seed, uint32_t stream,

@@ -1096,6 +1096,28 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
       AGO.rowptr[g + 1] = (int32_t)AGO.col.size();
     }
     if ((st = upload_csr(c, c->AGO, AGO)) != NSP_OK) return st;
+    // sliced ELL copy (32-row slices, column-major inside a slice)
+    const int64_t nsl = (c->nG + 31) / 32;
+    std::vector<int64_t> sptr(nsl + 1, 0);
+    for (int64_t q = 0; q < nsl; ++q) {
+      int w = 0;
+      for (int64_t g = q * 32; g < std::min<int64_t>(c->nG, q * 32 + 32); ++g)
+        w = std::max(w, AGO.rowptr[g + 1] - AGO.rowptr[g]);
+      sptr[q + 1] = sptr[q] + (int64_t)w * 32;
+    }
+    std::vector<int32_t> scol(sptr[nsl], -1);
+    std::vector<double> sval(sptr[nsl], 0.0);
+    for (int64_t g = 0; g < c->nG; ++g) {
+      const int64_t q = g / 32, lane = g % 32;
+      for (int32_t k = AGO.rowptr[g]; k < AGO.rowptr[g + 1]; ++k) {
+        const int64_t e = sptr[q] + (int64_t)(k - AGO.rowptr[g]) * 32 + lane;
+        scol[e] = AGO.col[k];
+        sval[e] = AGO.val[k];
+      }
+    }
+    if ((st = upload(c, &c->d_sell_ptr, sptr)) != NSP_OK) return st;
+    if ((st = upload(c, &c->d_sell_col, scol)) != NSP_OK) return st;
+    if ((st = upload(c, &c->d_sell_val, sval)) != NSP_OK) return st;
   }
   if ((st = upload_csr(c, c->CB, CB)) != NSP_OK) return st;
   if (!AII.rowptr.empty()) {

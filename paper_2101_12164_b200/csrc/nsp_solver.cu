@@ -665,6 +665,13 @@ static nsp_status ag_cheb(nsp_ctx* c, const double* X, int ldx, double* Y, int l
   NSP_CUDA_TRY(c, cudaMemsetAsync(xw, 0, blk * 8, st));
   static const bool fused_off = getenv("NSP_CHEB_FUSED") && getenv("NSP_CHEB_FUSED")[0] == '0';
   for (int k = 0; k < c->cheb_K; ++k) {
+    static const bool sell_off = getenv("NSP_CHEB_SELL") && getenv("NSP_CHEB_SELL")[0] == '0';
+    if (c->nranks == 1 && !fused_off && ld == 1 && c->d_sell_ptr && !sell_off) {   // s = 1: sliced ELL
+      nspk::cheb_step_sell(n, c->d_sell_ptr, c->d_sell_col, c->d_sell_val, d0, xw, r, d1, c->cheb_c1[k],
+                           c->cheb_c2[k], k + 1 < c->cheb_K, st);
+      std::swap(d0, d1);
+      continue;
+    }
     if (c->nranks == 1 && !fused_off && (ld == 1 || ld % 2 == 0)) {   // product and update in one pass
       nspk::cheb_step(c->AGO.rows ? c->AGO : c->AGG2, n, d0, ld, s, xw, r, d1, c->cheb_c1[k], c->cheb_c2[k],
                       k + 1 < c->cheb_K, st);
