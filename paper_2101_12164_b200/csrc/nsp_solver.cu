@@ -825,6 +825,16 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
     c->err = "nsp_nystrom: the M_1 form (nys_form 3) is single-rank";
     return NSP_ERR_STATE;
   }
+  // NSP_NYS_TRACE=1: host wall time per phase (stream synchronised; diagnostics only)
+  static const bool ntr = getenv("NSP_NYS_TRACE") && getenv("NSP_NYS_TRACE")[0] == '1';
+  auto nyt0 = std::chrono::steady_clock::now();
+  auto nymark = [&](const char* lab) {
+    if (!ntr) return;
+    cudaStreamSynchronize(c->stream);
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[nsp nys] %-10s %8.3f ms\n", lab, std::chrono::duration<double, std::milli>(t1 - nyt0).count());
+    nyt0 = t1;
+  };
   // several ranks (form 0): every Gram is summed over the private rows of every rank plus the shared rows
   // once (gram_rows) and allreduced; the s x s steps are then replicated bit-identically; A_G X completes
   // its shared rows with one allreduce; A_G^{-1} is the sharded Chebyshev operator
@@ -978,6 +988,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
       }
       continue;
     }
+    nymark("start");
     // steps 1-2: B = K_G G  (reading C1); M_1 (form 3): the operator is R_G^{-T} B_H R_G^{-1}, so the
     // sketch enters as R_G^{-1} G (eq:lr_approximation_S-1_A-I)
     const double* Gin = Om;
@@ -987,6 +998,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
       Gin = Qa;
     }
     if ((e = apply_into(c, Gin, sp, Bn, sp, s, 2, w.wvu)) != NSP_OK) return e;
+    nymark("K_G Omega");
     // step 3: S_G X = B by breakdown-free block CG to tol_inner
     brep = nsp_report{};
     if (rep && pw == q) {
@@ -999,6 +1011,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
     if (sbi < 0) return sbi;
     if (sbi == NSP_NOT_CONVERGED) sb = NSP_NOT_CONVERGED;
     total_iters += brep.iters;
+    nymark("block CG");
     // step 4: Y = A_G X  (M_1: Y = R_G^{-T} A_G X, in R_G's row space)
     nspk::spmm(c->AGG2, Xn, sp, nullptr, 0, n, Y, sp, s, 3, true, st);
     if (multi && (e = finish_shared_rows(c, Xn, sp, Y, sp, s, true)) != NSP_OK) return e;
@@ -1014,9 +1027,11 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
   const int64_t nY = form == 2 ? n_int : n;
   const double* Gs = form == 2 ? Fi : Om;
   const double* Ys = form == 2 ? Xi : Y;
+  nymark("A_G X");
   // step 5: Y = Q R
   const double* Q = nullptr;
   if ((e = (form == 2 ? cholqr(Ys, &Q, nY, Qa2, Qb2) : cholqr(Ys, &Q))) != NSP_OK) return e;
+  nymark("CholQR2");
   // step 6: C = Omega^T Y, symmetrised (reading C6)
   nspb::gram(Gs, sp, sp, Ys, sp, sp, multi ? gram_rows(c) : nY, C, sp, w.gram, st);
   if (multi && (e = comm_allreduce(c, C, sm)) != NSP_OK) return e;
@@ -1041,6 +1056,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
   c->h_sigma.clear();
   nsp_status ret = sb == NSP_NOT_CONVERGED ? NSP_NOT_CONVERGED : NSP_OK;
   if (rk > 0) {
+    nymark("C + EVD");
     // step 8: T = R V1 D1^{-1} V1^T R^T = M1 M1^T with M1 = R V1 D1^{-1/2}
     NSP_CUDA_TRY(c, cudaMemsetAsync(Vsc, 0, sm * 8, st));
     nspb::scale_cols(VC, s, lamC, r, s, sp, Vsc, sp, 1, st);
@@ -1057,6 +1073,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
     nspb::scale_cols(VT, s, lamT, rk, s, kp, Wc, kp, 3, st);
     PanelArgs pu{U, kp, nullptr, 0, Q, sp, Wc, kp, 1.0, nullptr};
     nspb::panel2(pu, nullptr, sp, kp, nY, st);
+    nymark("T, EVD, U");
     // step 11: Z = A_G^{-1} U~  (M_3: Z^ = A_G^{-1} A_GI V^, eq:left_prec_mat2)
     NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_Z, (size_t)std::max<int64_t>(n, 1) * kp * 8));
     NSP_CUDA_TRY(c, cudaMemsetAsync(c->d_Z, 0, (size_t)std::max<int64_t>(n, 1) * kp * 8, st));
@@ -1076,6 +1093,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
     NSP_CUDA_TRY(c, cudaStreamSynchronize(st));
     c->nys_rank = rk;
     c->nys_ld = kp;
+    nymark("Z = A_G^-1 U");
     // M_A-DEF2 (reading R5): E = Z^T S_G Z (one S_G block apply on Z) and its Cholesky factor
     {
       double* SZ = Qa;    // n x kp scratch (reuse)
@@ -1096,6 +1114,7 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
     ret = NSP_ERR_RANK_COLLAPSE;
     c->err = "nsp_nystrom: no eigenvalue of C >= eps (M_2 degenerates to A_G^{-1})";
   }
+  nymark("E = Z^T S Z");
   NSP_CUDA_TRY(c, cudaGetLastError());
   if (rep) {
     rep->iters = brep.iters;
