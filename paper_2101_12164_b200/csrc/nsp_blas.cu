@@ -404,25 +404,30 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t
 // SM waits at a barrier or in its epilogue the other's products keep the DMMA pipe busy (k_panel_rows:
 // one 16-warp CTA per SM, every warp in lockstep).  normpart as k_panel_rows (row g, 128 columns).
 constexpr int HKC = 32, HLDM = 68, HLDA = 36, HSPP = 128 / HKC;
+// PR = rows per pass (64: 8 warps = 4 row groups x 2 column quarters of 32; 32: 2 row groups x 4 column
+// groups of 16 - finer passes for small n, where a 64-row pass over a 96-row range wastes half a pass)
+template <int PR>
 __global__ void __launch_bounds__(256, 2) k_panel_half(PanelArgs pa, int64_t n, int64_t ngroups) {
-  constexpr int NF = 4;
+  constexpr int NF = PR == 64 ? 4 : 2;
+  constexpr int NRG = PR / 16;              // row groups per pass
+  constexpr int CW = 64 / (8 / NRG);        // columns per warp: 32 (PR 64) or 16 (PR 32)
   pdl_wait();
   extern __shared__ __align__(16) double sm[];
   double* Ms = sm;                  // 128 x HLDM: M[:, c0 .. c0 + 64)
-  double* Ar = sm + 128 * HLDM;     // 2 x 64 x HLDA
+  double* Ar = sm + 128 * HLDM;     // 2 x PR x HLDA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rg = warp >> 1, cb = (warp & 1) * 32;
+  const int rg = warp / (8 / NRG), cb = (warp % (8 / NRG)) * CW;
   const int grp = blockIdx.x >> 1, c0 = (blockIdx.x & 1) * 64;
   const int ngrp = gridDim.x >> 1;
   const int64_t g0 = (int64_t)grp * ngroups / ngrp;
   const int64_t g1 = (int64_t)(grp + 1) * ngroups / ngrp;
   const int64_t r0 = g0 * 16, r1 = min(n, g1 * 16);
-  const int npass = r1 > r0 ? (int)((r1 - r0 + 63) / 64) : 0;
+  const int npass = r1 > r0 ? (int)((r1 - r0 + PR - 1) / PR) : 0;
   const int nsteps = npass * HSPP;
   const double* __restrict__ In = pa.In;
   auto issue = [&](int q) {
-    const int64_t rp = r0 + (int64_t)(q / HSPP) * 64;
-    cp_block_zf(Ar + (q & 1) * 64 * HLDA, HLDA, In + rp * pa.ldi + (q % HSPP) * HKC, pa.ldi, 64, HKC, r1 - rp);
+    const int64_t rp = r0 + (int64_t)(q / HSPP) * PR;
+    cp_block_zf(Ar + (q & 1) * PR * HLDA, HLDA, In + rp * pa.ldi + (q % HSPP) * HKC, pa.ldi, PR, HKC, r1 - rp);
   };
   cp_block(Ms, HLDM, pa.M + c0, pa.ldm, 128, 64);
   if (nsteps > 0) issue(0);
@@ -435,7 +440,7 @@ __global__ void __launch_bounds__(256, 2) k_panel_half(PanelArgs pa, int64_t n, 
   double2 cin[2][NF];
   for (int q = 0; q < nsteps; ++q) {
     const int kc = q % HSPP;
-    const int64_t rp = r0 + (int64_t)(q / HSPP) * 64;
+    const int64_t rp = r0 + (int64_t)(q / HSPP) * PR;
     if (kc == 0) {
 #pragma unroll
       for (int i = 0; i < 2; ++i)
@@ -451,7 +456,7 @@ __global__ void __launch_bounds__(256, 2) k_panel_half(PanelArgs pa, int64_t n, 
     __syncthreads();
     if (q + 1 < nsteps) issue(q + 1);
     cp_commit();
-    const double* As = Ar + (q & 1) * 64 * HLDA;
+    const double* As = Ar + (q & 1) * PR * HLDA;
     if (rp + rg * 16 < r1)
       cta_mma<NF, false, false>(As + rg * 16 * HLDA, HLDA, Ms + kc * HKC * HLDM + cb, HLDM, acc, HKC, 0);
     if (kc == HSPP - 1) {
@@ -485,7 +490,7 @@ __global__ void __launch_bounds__(256, 2) k_panel_half(PanelArgs pa, int64_t n, 
     }
   cp_wait<0>();
   __syncthreads();
-  double* red = Ar;   // 4 x 64
+  double* red = Ar;   // NRG x 64
   if (lane < 4) {
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
@@ -495,9 +500,12 @@ __global__ void __launch_bounds__(256, 2) k_panel_half(PanelArgs pa, int64_t n, 
     }
   }
   __syncthreads();
-  if (threadIdx.x < 64)
-    pa.normpart[grp * (int64_t)pa.ldo + c0 + threadIdx.x] =
-        ((red[threadIdx.x] + red[64 + threadIdx.x]) + red[128 + threadIdx.x]) + red[192 + threadIdx.x];
+  if (threadIdx.x < 64) {
+    double v = red[threadIdx.x];
+#pragma unroll
+    for (int q = 1; q < NRG; ++q) v += red[q * 64 + threadIdx.x];
+    pa.normpart[grp * (int64_t)pa.ldo + c0 + threadIdx.x] = v;
+  }
 }
 
 // Fused s = 128 panel + Gram partial (rows a8+a10 / a10+a11 of the block-CG iteration, one pass over
@@ -1420,16 +1428,24 @@ int panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, in
     return e && e[0] == '0';
   }();
   // one-wave row-range panel: s = 128 and at least one 64-row pass per SM (normpart rows = CTAs)
-  static const bool half_on = [] {
+  static const int half_mode = [] {   // NSP_PANEL_HALF: 0 off, 1 two CTAs / SM with 64-row passes, 2 with 32-row
     const char* e = getenv("NSP_PANEL_HALF");
-    return e && e[0] == '1';
+    return e ? atoi(e) : 0;
   }();
-  if (half_on && !rows_off && !nsp_force_generic && kdim == 128 && ncols == 128 && n >= (int64_t)64 * nsm &&
+  if (half_mode && !rows_off && !nsp_force_generic && kdim == 128 && ncols == 128 && n >= (int64_t)64 * nsm &&
       ldo >= 128) {
     nsp_count_path(NSP_PATH_PANEL_ROWS);
-    const size_t smem = (128 * HLDM + 2 * 64 * HLDA) * sizeof(double);
-    smem_optin((const void*)k_panel_half, smem);
-    { nsp_count_launch(); launch_k(k_panel_half, dim3(2 * nsm), dim3(256), smem, st, a, n, (n + 15) / 16); }
+    if (half_mode == 2) {
+      const size_t smem = (128 * HLDM + 2 * 32 * HLDA) * sizeof(double);
+      smem_optin((const void*)k_panel_half<32>, smem);
+      nsp_count_launch();
+      launch_k(k_panel_half<32>, dim3(2 * nsm), dim3(256), smem, st, a, n, (n + 15) / 16);
+    } else {
+      const size_t smem = (128 * HLDM + 2 * 64 * HLDA) * sizeof(double);
+      smem_optin((const void*)k_panel_half<64>, smem);
+      nsp_count_launch();
+      launch_k(k_panel_half<64>, dim3(2 * nsm), dim3(256), smem, st, a, n, (n + 15) / 16);
+    }
     return nsm;
   }
   if (!rows_off && !nsp_force_generic && kdim == 128 && ncols == 128 && n >= (int64_t)64 * nsm && ldo >= 128) {
