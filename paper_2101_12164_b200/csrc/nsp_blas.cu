@@ -1103,6 +1103,7 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
     tots = tots + offs;
     offs = 2.0 * offs;
     if (!(offs > 1e-28 * tots) || tots == 0.0) break;
+    const double tot_sweep = tots;
     // rounding floor: the off-diagonal norm has stopped falling (a sweep no longer halves it) at a level
     // already below 1e-12 ||A||_F - the 1e-14 target is under the attainable floor for this matrix and
     // further sweeps only cost time (round 2: C and T of Nystrom took the full 60 sweeps, 15 ms each)
@@ -1128,7 +1129,10 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
         double& apq = Ap[tri(p, q)];
         double c = 1.0, s = 0.0;
         const double a_pq = apq, a_pp = app, a_qq = aqq;
-        if (fabs(a_pq) > 1e-300 && a_pq * a_pq > 1e-36 * fabs(a_pp * a_qq)) {
+        // rotate unless a_pq is negligible relative to its diagonal pair OR to the whole matrix (|a_pq| <=
+        // 1e-17 ||A||_F: rounding noise that rotations between tiny diagonal entries would otherwise keep
+        // regenerating elsewhere, so the sweeps never reached the off-norm target)
+        if (fabs(a_pq) > 1e-300 && a_pq * a_pq > 1e-36 * fabs(a_pp * a_qq) && a_pq * a_pq > 1e-34 * tot_sweep) {
           // t = sign(th) / (|th| + sqrt(th^2 + 1)), th = d / (2 a_pq), d = a_qq - a_pp, written
           // as t = 2 a_pq sign(d) / (|d| + sqrt(d^2 + 4 a_pq^2)): one sqrt, one divide
           const double d = a_qq - a_pp;
