@@ -161,6 +161,7 @@ struct nsp_ctx {
   long long nys_gen = 0;   // bumped by every nsp_nystrom
   double* d_ELp = nullptr;        // Cholesky (k_chol16 packed) of E = Z^T S_G Z for M_A-DEF2
   bool adef_ok = false;
+  bool adef_ready = false;        // E of the current Z formed (lazily, on the first M_A-DEF2 use)
   std::vector<double> h_sigma;
 
   // full-system solve (nsp_pcg; eq:A_LDLT PAPER.md:381-385): every block's interior rows I1 in

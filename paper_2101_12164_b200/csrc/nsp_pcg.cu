@@ -767,6 +767,10 @@ extern "C" nsp_status nsp_pcg(nsp_ctx* c, const double* b, double* x, double tol
     c->err = "nsp_pcg: the A_G^{-1} / M_2 preconditioner needs the A_G factor (opts.factor_gamma = 1)";
     return NSP_ERR_STATE;
   }
+  if (precond == 3 && c->nys_rank > 0) {
+    nsp_status ea = adef_prepare(c);
+    if (ea != NSP_OK) return ea;
+  }
   if (precond == 3 && c->nys_rank > 0 && !c->adef_ok) {
     c->err = "nsp_pcg: E = Z^T S_G Z not positive definite (M_A-DEF2 unavailable)";
     return NSP_ERR_STATE;

@@ -775,6 +775,56 @@ static nsp_status precond(nsp_ctx* c, const double* R, double* Z, int ld, int s,
   return ag_solve(c, R, ld, Z, ld, s, buf);
 }
 
+nsp_status adef_prepare(nsp_ctx* c) {
+  if (c->adef_ready || c->nys_rank <= 0) return NSP_OK;
+  const int kp = c->nys_ld, rk = c->nys_rank;
+  const int64_t n = c->nG;
+  cudaStream_t st = c->stream;
+  const size_t nb = (size_t)std::max<int64_t>(n, 1) * kp;
+  double *SZ = nullptr, *wvu = nullptr, *G = nullptr, *gw = nullptr;
+  BcgStatus* dst = nullptr;
+  auto release = [&]() {
+    cudaFree(SZ);
+    cudaFree(wvu);
+    cudaFree(G);
+    cudaFree(gw);
+    cudaFree(dst);
+  };
+  if (cudaMalloc((void**)&SZ, nb * 8) != cudaSuccess || cudaMalloc((void**)&wvu, apply_ws_bytes(c, kp)) != cudaSuccess ||
+      cudaMalloc((void**)&G, (size_t)kp * kp * 8) != cudaSuccess ||
+      cudaMalloc((void**)&gw, nspb::gram_ws_doubles(n, kp, kp) * 8) != cudaSuccess ||
+      cudaMalloc((void**)&dst, sizeof(BcgStatus)) != cudaSuccess) {
+    release();
+    c->err = "adef_prepare: out of device memory";
+    return NSP_ERR_OOM;
+  }
+  BcgStatus* hs = (BcgStatus*)c->h_status;
+  *hs = BcgStatus{};
+  nsp_status e = NSP_OK;
+  if (cudaMemcpyAsync(dst, hs, sizeof(BcgStatus), cudaMemcpyHostToDevice, st) != cudaSuccess) e = NSP_ERR_CUDA;
+  if (e == NSP_OK) e = apply_into(c, c->d_Z, kp, SZ, kp, rk, 1, wvu);   // S_G Z
+  if (e == NSP_OK) {
+    nspb::gram(c->d_Z, kp, kp, SZ, kp, kp, gram_rows(c), G, kp, gw, st);
+    if (c->nranks > 1) e = comm_allreduce(c, G, (size_t)kp * kp);
+  }
+  if (e == NSP_OK) {
+    nspb::small_sym(G, rk, kp, 0.0, st);
+    if (cudaMalloc((void**)&c->d_ELp, (size_t)kp * kp * 8) != cudaSuccess) e = NSP_ERR_OOM;
+  }
+  if (e == NSP_OK) {
+    nspb::chol_fac(G, kp, 0, rk, 0.0, c->d_ELp, dst, st);
+    if (cudaMemcpyAsync(hs, dst, sizeof(BcgStatus), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      e = NSP_ERR_CUDA;
+  }
+  release();
+  if (e != NSP_OK) return e;
+  c->adef_ok = !hs->indefinite;
+  c->adef_ready = true;
+  c->nys_gen += 1;   // the cached PCG graphs bake in d_ELp
+  return NSP_OK;
+}
+
 }  // namespace nspi
 
 using namespace nspi;
@@ -1094,22 +1144,12 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
     c->nys_rank = rk;
     c->nys_ld = kp;
     nymark("Z = A_G^-1 U");
-    // M_A-DEF2 (reading R5): E = Z^T S_G Z (one S_G block apply on Z) and its Cholesky factor
-    {
-      double* SZ = Qa;    // n x kp scratch (reuse)
-      if ((e = apply_into(c, c->d_Z, kp, SZ, kp, rk, 1, w.wvu)) != NSP_OK) return e;
-      nspb::gram(c->d_Z, kp, kp, SZ, kp, kp, multi ? gram_rows(c) : n, G, kp, w.gram, st);
-      if (multi && (e = comm_allreduce(c, G, (size_t)kp * kp)) != NSP_OK) return e;
-      nspb::small_sym(G, rk, kp, 0.0, st);
-      if (c->d_ELp) cudaFree(c->d_ELp);
-      c->d_ELp = nullptr;
-      NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_ELp, (size_t)kp * kp * 8));
-      nspb::chol_fac(G, kp, 0, rk, 0.0, c->d_ELp, w.st, st);
-      if ((e = read_status(c, w.st, hs)) != NSP_OK) return e;
-      c->adef_ok = !hs->indefinite;
-      hs->indefinite = 0;
-      NSP_CUDA_TRY(c, cudaMemcpyAsync(w.st, hs, sizeof(BcgStatus), cudaMemcpyHostToDevice, st));
-    }
+    // M_A-DEF2 (reading R5): E = Z^T S_G Z is formed lazily, on the first nsp_pcg(precond = 3) (adef_prepare):
+    // one S_G block apply on Z that the M_2 / M_1 / M_3 paths never need
+    if (c->d_ELp) cudaFree(c->d_ELp);
+    c->d_ELp = nullptr;
+    c->adef_ok = false;
+    c->adef_ready = false;
   } else {
     ret = NSP_ERR_RANK_COLLAPSE;
     c->err = "nsp_nystrom: no eigenvalue of C >= eps (M_2 degenerates to A_G^{-1})";

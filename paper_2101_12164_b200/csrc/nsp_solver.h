@@ -19,4 +19,7 @@ size_t ag_ws_doubles(const nsp_ctx* c, int s);
 nsp_status ag_solve(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, double* buf);
 nsp_status ag_tri(nsp_ctx* c, const double* X, int ldx, bool x_gamma, double* Y, int ldy, bool y_gamma, int s,
                   bool fwd, bool bwd, double* buf);
+// M_A-DEF2 (reading R5): E = Z^T S_G Z and its Cholesky factor for the current Nystrom basis, formed once
+// on first use (one S_G block apply on Z); sets adef_ok
+nsp_status adef_prepare(nsp_ctx* c);
 }  // namespace nspi
