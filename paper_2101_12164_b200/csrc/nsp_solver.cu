@@ -1086,6 +1086,14 @@ nsp_status nsp_nystrom(nsp_ctx* c, int rank, int oversample, uint64_t seed, cons
   nspb::gram(Gs, sp, sp, Ys, sp, sp, multi ? gram_rows(c) : nY, C, sp, w.gram, st);
   if (multi && (e = comm_allreduce(c, C, sm)) != NSP_OK) return e;
   nspb::small_sym(C, s, sp, 0.0, st);
+  if (const char* dump = getenv("NSP_DUMP_C")) {   // diagnostics: C (s x s, ld sp) as raw fp64
+    std::vector<double> hc((size_t)sp * sp);
+    cudaMemcpy(hc.data(), C, hc.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(dump, "wb")) {
+      fwrite(hc.data(), 8, hc.size(), f);
+      fclose(f);
+    }
+  }
   // step 7: EVD of C, split at eps = nys_eps_rel * lambda_max
   nspb::small_eig(C, sp, s, Vw, sp + 1, lamC, VC, nullptr, st);
   std::vector<double> hl(s);
