@@ -3,6 +3,7 @@
 // Cholesky / triangular inverse / Jacobi eigensolver, small GEMMs.  All reductions are
 // fixed-order two-stage (no fp64 atomics): results are bitwise reproducible (reading C17).
 #include <algorithm>
+#include <cstdio>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -1503,6 +1504,14 @@ void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* 
   const size_t smem = (size_t)(ne * (ne + 1) / 2 + ne * rp) * sizeof(double);
   smem_optin((const void*)k_small_eig, smem);
   { nsp_count_launch(); launch_k(k_small_eig, dim3(g), dim3(1024), smem, st, A, lda, n, Vwork, ldv, lam, Vsorted, gate, tau, T, spT, stw); }
+#ifdef NSP_EIG_PROF
+  {   // diagnostics build: sweeps of this call
+    cudaStreamSynchronize(st);
+    int sw = 0;
+    cudaMemcpyFromSymbol(&sw, g_eig_sweeps, sizeof(int));
+    fprintf(stderr, "[nsp eig] n = %d: %d sweeps\n", n, sw);
+  }
+#endif
 }
 
 
