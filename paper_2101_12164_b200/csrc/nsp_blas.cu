@@ -1505,7 +1505,9 @@ void small_eig(const double* A, int lda, int n, double* Vwork, int ldv, double* 
   smem_optin((const void*)k_small_eig, smem);
   { nsp_count_launch(); launch_k(k_small_eig, dim3(g), dim3(1024), smem, st, A, lda, n, Vwork, ldv, lam, Vsorted, gate, tau, T, spT, stw); }
 #ifdef NSP_EIG_PROF
-  {   // diagnostics build: sweeps of this call
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cst);
+  if (cst == cudaStreamCaptureStatusNone) {   // diagnostics build: sweeps of this (eager) call
     cudaStreamSynchronize(st);
     int sw = 0;
     cudaMemcpyFromSymbol(&sw, g_eig_sweeps, sizeof(int));
