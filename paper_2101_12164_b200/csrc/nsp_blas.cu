@@ -1112,6 +1112,9 @@ __global__ void __launch_bounds__(1024) k_small_eig(const double* __restrict__ A
     prev_offs = offs;
 #ifdef NSP_EIG_PROF
     if (tid == 0) g_eig_sweeps = sweep + 1;
+#ifdef NSP_EIG_TRACE
+    if (tid == 0 && blockIdx.x == 0) printf("sweep %d off/tot %.3e\n", sweep, offs / tots);
+#endif
 #endif
     for (int round = 0; round < ne - 1; ++round) {
       // phase 1: tournament pairing (position 0 fixed, the others rotate), rotation parameters,

@@ -15,7 +15,11 @@ int main() {
   std::vector<double> X(4096 * n), A(sp * sp);
   for (auto& x : X) x = nd(g);
   const bool graded = getenv("EIG_GRADED") != nullptr;   // eigenvalues 30 * 10^(-14 t), t in [0, 1] (Nystrom's C)
-  if (!graded) {
+  if (const char* fn = getenv("EIG_FILE")) {   // a dumped 128 x 128 fp64 matrix (NSP_DUMP_C)
+    FILE* f = fopen(fn, "rb");
+    if (!f || fread(A.data(), 8, sp * sp, f) != (size_t)(sp * sp)) { printf("cannot read %s\n", fn); return 1; }
+    fclose(f);
+  } else if (!graded) {
     for (int i = 0; i < n; ++i) for (int j = 0; j < n; ++j) { double s = 0; for (int k = 0; k < 4096; ++k) s += X[k * n + i] * X[k * n + j] * (1.0 + (k % 97)); A[i * sp + j] = s; }
   } else {
     // V = Q of a Gram-Schmidt on random columns; A = V diag(l) V^T
