@@ -5,6 +5,7 @@ another rank's kernel).  Everything else - the shard plan, the private/shared ro
 shared-row allreduce per S_G apply, the Gram ownership rule - is the code path the NCCL ranks run.
 Checks: K_G / S_G applies against the oracle (<= 1e-12), block-CG iteration counts and widths equal
 to the single-rank run, X within 1e-10 of it, shared rows bitwise identical on every rank."""
+import os
 import threading
 
 import numpy as np
@@ -16,6 +17,21 @@ from paper_2101_12164_b200 import Context, nsp
 from tests.gpu_util import block, context, dev, problem, relfro
 
 pytestmark = pytest.mark.gpu
+
+
+class _same_iteration_structure:
+    """The one-rank reference runs the iteration exactly as the sharded ranks do: without the apply-first
+    reassociation (reading R9, one rank only), so the comparison isolates the sharding."""
+
+    def __enter__(self):
+        self.prev = os.environ.get("NSP_APPLY_FIRST")
+        os.environ["NSP_APPLY_FIRST"] = "0"
+
+    def __exit__(self, *a):
+        if self.prev is None:
+            os.environ.pop("NSP_APPLY_FIRST", None)
+        else:
+            os.environ["NSP_APPLY_FIRST"] = self.prev
 
 
 def _run_ranks(pr, d, G, Om, Xprobe, tol, maxit):
@@ -64,7 +80,8 @@ def test_multirank_block_cg_matches_single_rank(name, G):
     B = S.k_gamma(Om)
     ctx1 = context(pr)
     X1 = torch.zeros(d.n_gamma, pr.s, dtype=torch.float64, device="cuda")
-    rep1 = ctx1.block_cg(dev(B), X1, pr.tol_bcg, 500)
+    with _same_iteration_structure():
+        rep1 = ctx1.block_cg(dev(B), X1, pr.tol_bcg, 500)
     X1 = X1.cpu().numpy()
     ctx1.close()
     res = _run_ranks(pr, d, G, Om, Xprobe, pr.tol_bcg, 500)
@@ -157,9 +174,10 @@ def test_multirank_nystrom_pcg_matches_single_rank(name, G):
     B = S.k_gamma(Om)
     ctx1.set_bcg_precond(1)
     X1 = torch.zeros(d.n_gamma, pr.s, dtype=torch.float64, device="cuda")
-    repm1 = ctx1.block_cg(dev(B), X1, pr.tol_bcg, 500)
-    ctx1.set_bcg_precond(0)
-    rn1 = ctx1.nystrom(pr.rank, pr.oversample, dev(Om), pr.tol_bcg, 500)
+    with _same_iteration_structure():
+        repm1 = ctx1.block_cg(dev(B), X1, pr.tol_bcg, 500)
+        ctx1.set_bcg_precond(0)
+        rn1 = ctx1.nystrom(pr.rank, pr.oversample, dev(Om), pr.tol_bcg, 500)
     sig1 = ctx1.nystrom_sigma()
     x1 = torch.zeros(pr.n, dtype=torch.float64, device="cuda")
     rp1 = ctx1.pcg(dev(b), x1, tol_pcg, 3000, precond=2)
