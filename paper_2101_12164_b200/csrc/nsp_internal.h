@@ -84,8 +84,10 @@ struct GraphKey {
   double tol = 0.0;
   int kind = 0, usem = 0;
   double tau = 0.0;
+  int af = 0;   // apply-first structure (reading R9)
   bool operator==(const GraphKey& o) const {
-    return X == o.X && n == o.n && s == o.s && tol == o.tol && kind == o.kind && usem == o.usem && tau == o.tau;
+    return X == o.X && n == o.n && s == o.s && tol == o.tol && kind == o.kind && usem == o.usem && tau == o.tau &&
+           af == o.af;
   }
 };
 

@@ -406,7 +406,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
   const bool use_graph = !multi && !tr.on && !(genv && genv[0] == '0');
   cudaGraphExec_t gexec = nullptr;
   if (use_graph) {
-    const GraphKey key{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau};
+    const GraphKey key{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau, apply_first ? 1 : 0};
     if (c->bcg_graph && c->bcg_key == key) gexec = c->bcg_graph;
   }
   const bool heads_run = !hs->converged && maxit > 0;
@@ -454,7 +454,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
             NSP_CUDA_TRY(c, cudaGraphInstantiate(&gexec, g, 0));
             cudaGraphDestroy(g);
             c->bcg_graph = gexec;
-            c->bcg_key = GraphKey{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau};
+            c->bcg_key = GraphKey{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau, apply_first ? 1 : 0};
           }
           NSP_CUDA_TRY(c, cudaGraphLaunch(gexec, st));
           nsp_count_launches(c->bcg_graph_kernels);
@@ -516,7 +516,7 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
           c->bcg_wgraph = nullptr;
         }
       }
-      const GraphKey key{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau};
+      const GraphKey key{w.X, n, s, tol, w.kind, usem ? 1 : 0, c->opts.orth_tau, apply_first ? 1 : 0};
       // build (or reuse) the WHILE graph; any CUDA error while building it (a node type the
       // conditional body does not support) falls back to the per-iteration graph for good
       auto build_while = [&]() -> cudaError_t {
