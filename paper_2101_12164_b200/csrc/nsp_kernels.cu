@@ -1,6 +1,7 @@
 // Device kernels of the S_G apply and the setup factorisation (north_star (a), (b); §8(a) rows
 // a1-a5, s0).  fp64 throughout; dense tile products on the DMMA pipe (mma.sync f64).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdlib>
 #include <stdint.h>
 
@@ -839,6 +840,103 @@ __global__ void __launch_bounds__(256) k_symm(const FacSub* __restrict__ subs, c
       const int r = acc_row<NF>(i), c = acc_col<NF>(j);
       *reinterpret_cast<double2*>(out + (int64_t)r * ldo + c) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
+}
+
+// Persistent form of k_symm (chunk-major W/U): 2 CTAs per SM walk the work units u = item * nch + chunk
+// (chunk fastest, so the chunk CTAs of one item still share each S_j^{-1} tile through L2) with ONE
+// 2-stage TMA ring that runs across unit boundaries - the first stage of the next unit is in flight while
+// the current one finishes its last product and writes its U tile, instead of every CTA paying its own
+// prologue and epilogue.
+template <int CW>
+__global__ void __launch_bounds__(256, 2) k_symm_p(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                                   int nitems, int nch, const double* __restrict__ minv,
+                                                   const double* __restrict__ W, double* __restrict__ U, int64_t cs) {
+  constexpr int NF = CW / 16;
+  constexpr int LDV = CW + 4;
+  constexpr int STAGE = NSP_MINV_TILE + 64 * LDV;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int64_t total = (int64_t)nitems * nch;
+  struct Unit {
+    const double* Mb;
+    const double* Wb;
+    double* out;
+    int I, ntb;
+  };
+  auto unit = [&](int64_t u) {
+    const int2 it = items[u / nch];
+    const int by = (int)(u % nch);
+    const FacSub sb = subs[it.x];
+    Unit r;
+    r.Mb = minv + sb.dense_off * NSP_MINV_TILE;
+    r.Wb = W + by * cs + sb.wvu_row * (int64_t)LDV;
+    r.out = U + by * cs + (sb.wvu_row + (int64_t)it.y * 64) * LDV;
+    r.I = it.y;
+    r.ntb = sb.ntb;
+    return r;
+  };
+  auto mt = [](const Unit& q, int J) {
+    return J <= q.I ? q.Mb + ((int64_t)q.I * (q.I + 1) / 2 + J) * NSP_MINV_TILE
+                    : q.Mb + ((int64_t)J * (J + 1) / 2 + q.I) * NSP_MINV_TILE;
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int64_t u = blockIdx.x;
+  if (u >= total) {
+    pdl_wait();
+    return;
+  }
+  Unit cur = unit(u);
+  // stage 0: the constant M tile before the programmatic-launch wait, W after it
+  if (threadIdx.x == 0) {
+    mbar_expect(&bar[0], NSP_MINV_TILE * 8 + 64 * LDV * 8);
+    bulk_copy(sm, mt(cur, 0), NSP_MINV_TILE * 8, &bar[0]);
+  }
+  pdl_wait();
+  if (threadIdx.x == 0) bulk_copy(sm + NSP_MINV_TILE, cur.Wb, 64 * LDV * 8, &bar[0]);
+  double acc[2][NF][2];
+  acc_zero(acc);
+  unsigned g = 0;   // global step: stage g & 1, phase (g >> 1) & 1
+  while (true) {
+    const int64_t un = u + gridDim.x;
+    const bool has_next = un < total;
+    Unit nxt;
+    if (has_next) nxt = unit(un);
+    for (int J = 0; J < cur.ntb; ++J, ++g) {
+      mbar_wait(&bar[g & 1], (g >> 1) & 1);
+      __syncthreads();   // stage g complete for every thread; stage g + 1 free (its last reader was g - 1)
+      if (threadIdx.x == 0) {
+        const bool more = J + 1 < cur.ntb;
+        if (more || has_next) {
+          const Unit& q = more ? cur : nxt;
+          const int Jn = more ? J + 1 : 0;
+          double* Ms = sm + ((g + 1) & 1) * STAGE;
+          fence_proxy_async();
+          mbar_expect(&bar[(g + 1) & 1], NSP_MINV_TILE * 8 + 64 * LDV * 8);
+          bulk_copy(Ms, mt(q, Jn), NSP_MINV_TILE * 8, &bar[(g + 1) & 1]);
+          bulk_copy(Ms + NSP_MINV_TILE, q.Wb + (int64_t)Jn * 64 * LDV, 64 * LDV * 8, &bar[(g + 1) & 1]);
+        }
+      }
+      const double* Ms = sm + (g & 1) * STAGE;
+      if (J <= cur.I) cta_mma<NF, false, false>(Ms, NSP_MINV_LD, Ms + NSP_MINV_TILE, LDV, acc);
+      else cta_mma<NF, true, false>(Ms, NSP_MINV_LD, Ms + NSP_MINV_TILE, LDV, acc);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int r = acc_row<NF>(i), c = acc_col<NF>(j);
+        *reinterpret_cast<double2*>(cur.out + (int64_t)r * LDV + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    acc_zero(acc);
+    if (!has_next) break;
+    u = un;
+    cur = nxt;
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -2123,6 +2221,20 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
   // Measured on cfg2 shapes (tools/bench_symm_tma.cu): 135.1 us (both cp.async) -> 122.9 (TMA M) ->
   // 112.6 us (TMA M + W, 29.2 TFLOP/s); 64-wide / 3-stage / half-tile variants are slower.
   const size_t smem = 2 * (NSP_MINV_TILE + 64 * (cw + 4)) * sizeof(double);
+  static const bool persist = [] {
+    const char* e = getenv("NSP_SYMM_PERSIST");
+    return e && e[0] == '1';
+  }();
+  if (cm_stride > 0 && persist) {   // persistent: 2 CTAs per SM over (item, chunk) units
+    const size_t sm2 = 2 * (NSP_MINV_TILE + 64 * 36) * sizeof(double);
+    smem_optin((const void*)k_symm_p<32>, sm2);
+    const int nch = ldw / 32;
+    const int64_t total = (int64_t)nitems * nch;
+    const int grid = (int)std::min<int64_t>(total, 2 * (int64_t)num_sms());
+    nsp_count_launch();
+    launch_k(k_symm_p<32>, dim3(grid), dim3(256), sm2, st, subs, items, nitems, nch, minv, W, U, cm_stride);
+    return;
+  }
   if (cm_stride > 0) {   // ldw = the logical padded width (a multiple of 32), one CTA column per chunk
     const dim3 grid(ldw / 32, nitems);
     smem_optin((const void*)k_symm<32, true>, (size_t)((int)(2 * (NSP_MINV_TILE + 64 * 36) * sizeof(double))));
