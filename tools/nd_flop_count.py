@@ -6,13 +6,13 @@ import sys, time
 sys.path.insert(0, '/root/repo')
 import numpy as np, scipy.sparse as sp, scipy.sparse.linalg as spla
 from nsp_inputs import problems as P
-import oracle as O
 pr = P.make("cfg5")
 A = pr.A.to_scipy()
 blocks = [0, 300, 511]
-d = O.dbbd(A, pr.part, pr.K, blocks=blocks)
+gamma = np.flatnonzero(pr.part < 0)
 for j in blocks:
-    AI = d.A_I[j]; AIG = d.A_IG[j]
+    blk = np.flatnonzero(pr.part == j)
+    AI = A[blk][:, blk].tocsr(); AIG = A[blk][:, gamma].tocsr()
     n = AI.shape[0]
     B = np.flatnonzero(np.diff(AIG.tocsr().indptr))          # boundary-layer rows
     for spec in ["MMD_AT_PLUS_A", "COLAMD"]:
