@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(256) k_panel(PanelArgs pa0, PanelArgs pa1, int
   const int64_t r0 = blockIdx.x * 64ll;
   const int c0 = blockIdx.y * 64;
   const int64_t nv = n - r0;
+  const bool upper = pa.upper_unless && *pa.upper_unless == 0;
   double acc[2][4][2];
   acc_zero(acc);
   const int nk = (kdim + 31) / 32;
@@ -238,7 +239,9 @@ __global__ void __launch_bounds__(256) k_panel(PanelArgs pa0, PanelArgs pa1, int
       cp_block(Bs[b ^ 1], LDS, M + (int64_t)(kb + 1) * 32 * ldm + c0, ldm, 32, 64);
       cp_commit();
     }
-    cta_mma<4, false, false>(As[b], LDA, Bs[b], LDS, acc, 32);
+    // upper-triangular M: a warp's columns c0 + 32 (warp & 1) .. + 31 see zeros for k > their last column
+    if (!(upper && kb * 32 > c0 + (int)(threadIdx.x >> 5 & 1) * 32 + 31))
+      cta_mma<4, false, false>(As[b], LDA, Bs[b], LDS, acc, 32);
   }
   __syncthreads();   // smem reused below
   double* sq = sm;  // reuse: 64 x 65 squares
@@ -310,6 +313,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t
   const int npass = r1 > r0 ? (int)((r1 - r0 + 63) / 64) : 0;
   const int nsteps = npass * PSPP;
   const double* __restrict__ In = pa.In;
+  const bool upper = pa.upper_unless && *pa.upper_unless == 0;
   auto issue = [&](int q) {
     const int64_t rp = r0 + (int64_t)(q / PSPP) * 64;
     cp_block_zf(Ar + (q % PNS) * 64 * PLDA, PLDA, In + rp * pa.ldi + (q % PSPP) * PKC, pa.ldi, 64, PKC, r1 - rp);
@@ -348,8 +352,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel_rows(PanelArgs pa, int64_t
     if (q + PNS - 1 < nsteps) issue(q + PNS - 1);
     cp_commit();
     const double* As = Ar + (q % PNS) * 64 * PLDA;
-    // a warp whose 16-row group lies past the range skips its products (the DMMA pipe is the limit)
-    if (rp + rg * 16 < r1)
+    // a warp whose 16-row group lies past the range skips its products (the DMMA pipe is the limit), and so
+    // does a warp whose columns see an all-zero chunk of an upper-triangular M
+    if (rp + rg * 16 < r1 && !(upper && kc * PKC > cb + NF * 8 - 1))
       cta_mma<NF, false, false>(As + rg * 16 * PLDA, PLDA, Ms + kc * PKC * PLDM + cb, PLDM, acc, PKC, 0);
     if (kc == PSPP - 1) {
 #pragma unroll
@@ -1428,8 +1433,8 @@ void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64
 }
 
 int panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
-          int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st) {
-  PanelArgs a{Out, ldo, Cin, ldc, In, ldi, M, ldm, sgn, normpart};
+          int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st, const int* upper_unless) {
+  PanelArgs a{Out, ldo, Cin, ldc, In, ldi, M, ldm, sgn, normpart, upper_unless};
   const int nsm = num_sms();
   static const bool rows_off = [] {
     const char* e = getenv("NSP_PANEL_ROWS");

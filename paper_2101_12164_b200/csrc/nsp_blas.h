@@ -37,6 +37,9 @@ struct PanelArgs {
   int ldm;
   double sgn;
   double* normpart;
+  // optional: when non-null and *upper_unless == 0, M is upper triangular (M[k][c] = 0 for k > c: orth's
+  // T = R^{-1} after a successful Cholesky-QR) and the all-zero k-chunks of M are skipped per warp
+  const int* upper_unless;
 };
 
 namespace nspb {
@@ -53,7 +56,8 @@ void gram2(const double* Xa, int lda, int sa, const double* Xb, const double* Xb
 void panel2(const PanelArgs& a0, const PanelArgs* a1, int kdim, int ncols, int64_t n, cudaStream_t st);
 // returns the number of normpart rows written (row tiles, or CTAs of the one-wave s = 128 kernel)
 int panel(double* Out, int ldo, const double* Cin, int ldc, const double* In, int ldi, const double* M, int ldm,
-          int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st);
+          int kdim, int ncols, int64_t n, double sgn, double* normpart, cudaStream_t st,
+          const int* upper_unless = nullptr);
 // fused panel + Gram (s = 128, ld 128, n >= 64 x SMs, single rank): Out = Cin + sgn In M and
 // gram_out = In^T Out (gmode 0) or Out^T Out (gmode 1, exactly symmetric); normpart (nullable): column
 // sums of squares of Out, one row per CTA (returns the row count).  ws: gram_ws_doubles.

@@ -185,7 +185,8 @@ static nsp_status orth(nsp_ctx* c, BcgWs& w, const double* Wm, int s, double* Po
   nspb::small_eig(w.G, sp, s, w.Vw, sp + 1, w.lam, w.Vs, &w.st->fallback, st, c->opts.orth_tau, w.T, sp, w.st);
   if (no_panel) return NSP_OK;   // (apply-first: the caller forms P = W T and Q = (S W) T together)
   if (join_before_panel) NSP_CUDA_TRY(c, cudaStreamWaitEvent(st, join_before_panel, 0));   // X += P alpha done
-  nspb::panel(Pout, sp, nullptr, 0, Wm, sp, w.T, sp, sp, sp, n, 1.0, nullptr, st);
+  // P = W T; T upper triangular unless the eigen fallback fired (its zero chunks skipped, bitwise the same)
+  nspb::panel(Pout, sp, nullptr, 0, Wm, sp, w.T, sp, sp, sp, n, 1.0, nullptr, st, &w.st->fallback);
   return NSP_OK;
 }
 
@@ -388,8 +389,8 @@ nsp_status block_cg_impl(nsp_ctx* c, const double* B, int ldb, double* Xout, int
       if ((e2 = orth(c, w, w.W, s, w.P, nullptr, fuse_pg, true)) != NSP_OK) return e2;   // G, chol, T (or eig)
       if (xfork) NSP_CUDA_TRY(c, cudaStreamWaitEvent(q, c->ev_join, 0));                // X += P alpha done
       NSP_CUDA_TRY(c, cudaStreamWaitEvent(q, c->ev_ajoin, 0));                           // S_G W done
-      PanelArgs pp{w.P, sp, nullptr, 0, w.W, sp, w.T, sp, 1.0, nullptr};
-      PanelArgs pq{w.Q, sp, nullptr, 0, w.QW, sp, w.T, sp, 1.0, nullptr};
+      PanelArgs pp{w.P, sp, nullptr, 0, w.W, sp, w.T, sp, 1.0, nullptr, &w.st->fallback};
+      PanelArgs pq{w.Q, sp, nullptr, 0, w.QW, sp, w.T, sp, 1.0, nullptr, &w.st->fallback};
       nspb::panel2(pp, &pq, sp, sp, n, q);   // P = W T and Q = (S_G W) T, one launch
       skip_apply = true;
     } else {
