@@ -79,8 +79,12 @@ typedef struct {
   void* local_group;     /* testing only: nsp_local_group_create(nranks) handle shared by nranks host
                             threads driving ranks on ONE device (replaces NCCL); NULL otherwise */
   int apply_kernel;      /* a2+a3 of the S_G apply: 0 = one symmetric product with the explicit
-                            S_j^{-1} = L22^{-T} L22^{-1} tiles formed in setup (default); 1 = the
-                            two batched triangular sweeps with L22 (no extra memory) */
+                            S_j^{-1} = L22^{-T} L22^{-1} tiles formed in setup (default): for s >= 48
+                            on the INT8 tensor cores with fp64 accuracy (tcgen05 kind::i8, Ozaki
+                            splitting of the D-scaled tiles into 7 int8 slices, reading R10; built in
+                            setup when the device budget allows, env NSP_OZAKI=0 disables), else the
+                            fp64 DMMA product; 1 = the two batched triangular sweeps with L22 (no extra
+                            memory); 2 = the fp64 DMMA product only; 3 = the INT8 path for every s > 1 */
   int nys_power;         /* q >= 0: q-power iteration Nystrom (eq:power PAPER.md:204-212), G = B_H^q Omega
                             with the columns orthonormalised between applications; 0 = Alg. 2 as written */
   int nys_form;          /* inner system of nsp_nystrom: 0 = the border system S_G X = K_G G, Y = A_G X
@@ -123,7 +127,8 @@ typedef struct {
   int rank;                        /* Nystrom: rank of the approximation (min(r, k)) */
   int fallbacks;                   /* block CG: eigen-fallback orthonormalisations */
   double t_ms[8];                  /* setup: [0] host analysis, [1] H2D, [2] GPU factor, [3] A_G factor,
-                                      [4] S_j^{-1} tiles (apply_kernel 0) */
+                                      [4] S_j^{-1} tiles (apply_kernel 0), [5] their INT8
+                                      slices (reading R10) */
 } nsp_report;
 
 void nsp_default_opts(nsp_opts* o);
@@ -245,6 +250,7 @@ enum {
   NSP_PATH_SYMV = 7,         /* a2+a3 for one column (k_symv1) */
   NSP_PATH_PANEL_GRAM = 8,   /* fused panel + Gram partial (R -= Q alpha with Q^T R; W = R + P beta with W^T W) */
   NSP_PATH_CHOL_SOLVE = 9,   /* fused s x s Cholesky + triangular solve (one launch) */
+  NSP_PATH_OZAKI = 10,       /* a2+a3 on the INT8 tensor cores (k_oz_slice_w + k_oz_symm, reading R10) */
   NSP_PATH_COUNT = 16
 };
 int nsp_path_counters(long long* out, int n);

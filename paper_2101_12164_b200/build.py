@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp", "-I", INCLUDE,
          "--expt-relaxed-constexpr"]
-SOURCES = ["nsp_kernels.cu", "nsp_blas.cu", "nsp_small.cu", "nsp_solver.cu", "nsp_pcg.cu", "nsp_comm.cu", "nsp_setup.cpp", "nsp_api.cpp"]
+SOURCES = ["nsp_kernels.cu", "nsp_blas.cu", "nsp_small.cu", "nsp_solver.cu", "nsp_pcg.cu", "nsp_comm.cu", "nsp_ozaki.cu", "nsp_setup.cpp", "nsp_api.cpp"]
 HEADERS = ["nsp_comm.h", "nsp_internal.h", "nsp_dmma.cuh", "nsp_solver.h", "nsp_blas.h"]
 
 

@@ -32,7 +32,35 @@ int pick_cw(const nsp_ctx* c, int s) {
 
 int ld_pad(int s, int cw) { return ((s + cw - 1) / cw) * cw; }
 
+size_t apply_ws_bytes_base(const nsp_ctx* c, int s);
+
+// a2+a3 on the INT8 tensor cores for this width (reading R10): apply_kernel 0 from s >= 48 (NSP_OZ_MIN_S),
+// apply_kernel 3 for every s > 1
+bool use_ozaki(const nsp_ctx* c, int s) {
+  if (!c->d_oz_msl || s <= 1) return false;
+  if (c->opts.apply_kernel == 3) return true;
+  static const int min_s = getenv("NSP_OZ_MIN_S") ? atoi(getenv("NSP_OZ_MIN_S")) : 48;
+  return c->opts.apply_kernel == 0 && s >= min_s;
+}
+
+// byte offset of the INT8 W^T slices / column exponents inside the apply workspace
+static size_t oz_ws_offset(const nsp_ctx* c, int s) {
+  const int cw = pick_cw(c, s);
+  size_t b = c->d_minv ? (size_t)c->wvu_rows * (ld_pad(s, cw) / 32) * 36 * 8 * 2 + 512
+                       : (size_t)c->wvu_rows * ld_pad(s, cw) * 8 + 512;
+  if (c->d_minv) b += (size_t)c->wvu_rows * c->max_ntb * 8 + 256;
+  return (b + 1023) & ~(size_t)1023;
+}
+
 size_t apply_ws_bytes(const nsp_ctx* c, int s) {
+  if (use_ozaki(c, s)) {
+    const int nct = (s + 127) / 128;
+    return oz_ws_offset(c, s) + nspk::oz_wslice_bytes(c->wvu_rows, s) + (size_t)c->nsub * nct * 128 * 4 + 1024;
+  }
+  return apply_ws_bytes_base(c, s);
+}
+
+size_t apply_ws_bytes_base(const nsp_ctx* c, int s) {
   const int cw = pick_cw(c, s);
   // W and U; with the S_j^{-1} tiles the chunk-major padded layout (36 doubles per row per 32-col chunk)
   size_t b = c->d_minv ? (size_t)c->wvu_rows * (ld_pad(s, cw) / 32) * 36 * 8 * 2 + 512
@@ -87,8 +115,19 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
     const int nsh_it = c->n_items_sh, nrest = c->n_items - c->n_items_sh;
     const int64_t nsh = c->nG - c->n_priv;
     cudaStream_t main = c->stream;
-    nsp_count_path(NSP_PATH_SYMM);
-    nspk::symm(c->d_subs, c->d_items, nsh_it, c->d_minv, wvu, U, ldw, cw, main, cs);
+    const bool oz = use_ozaki(c, s);
+    int8_t* wsl = oz ? (int8_t*)((char*)wvu + oz_ws_offset(c, s)) : nullptr;
+    int* sexp = oz ? (int*)(wsl + nspk::oz_wslice_bytes(c->wvu_rows, s)) : nullptr;
+    auto prod = [&](const int2* its, int nit) {
+      if (oz) nspk::oz_product(c->d_subs, its, nit, s, ldw / 32, U, cs, c->d_oz_dexp, c->d_oz_mexp, c->d_oz_msl,
+                               wsl, sexp, main);
+      else nspk::symm(c->d_subs, its, nit, c->d_minv, wvu, U, ldw, cw, main, cs);
+    };
+    nsp_count_path(oz ? NSP_PATH_OZAKI : NSP_PATH_SYMM);
+    if (oz)
+      nspk::oz_slice_w(c->d_subs, c->d_items, c->n_items, c->nsub, s, ldw / 32, wvu, cs, c->d_oz_dexp, wsl, sexp,
+                       main);
+    prod(c->d_items, nsh_it);
     DevCSR shr = c->AGG2;   // the shared rows' slice of the a4+a5 operator
     shr.rows = nsh;
     shr.rowptr = c->AGG2.rowptr + c->n_priv;
@@ -104,7 +143,7 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
     c->stream = main;
     if (e != NSP_OK) return e;
     NSP_CUDA_TRY(c, cudaEventRecord(c->ev_cjoin, c->comm_stream));
-    if (nrest > 0) nspk::symm(c->d_subs, c->d_items + nsh_it, nrest, c->d_minv, wvu, U, ldw, cw, main, cs);
+    if (nrest > 0) prod(c->d_items + nsh_it, nrest);
     DevCSR prv = c->AGG2;   // the private rows
     prv.rows = c->n_priv;
     if (cm) nspk::spmm_cs(prv, X, ldx, U, 36, cs, c->nG, Y, ldy, 32, ldy, s, mode, true, main);
@@ -121,6 +160,14 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
       nsp_count_path(NSP_PATH_SYMV);
       if (getenv("NSP_SYMV2")) nspk::symv(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, c->stream);
       else nspk::symv1(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, P, c->stream);
+    } else if (use_ozaki(c, s)) {
+      nsp_count_path(NSP_PATH_OZAKI);
+      int8_t* wsl = (int8_t*)((char*)wvu + oz_ws_offset(c, s));
+      int* sexp = (int*)(wsl + nspk::oz_wslice_bytes(c->wvu_rows, s));
+      nspk::oz_slice_w(c->d_subs, c->d_items, c->n_items, c->nsub, s, ldw / 32, wvu, cs, c->d_oz_dexp, wsl, sexp,
+                       c->stream);
+      nspk::oz_product(c->d_subs, c->d_items, c->n_items, s, ldw / 32, U, cs, c->d_oz_dexp, c->d_oz_mexp,
+                       c->d_oz_msl, wsl, sexp, c->stream);
     } else {
       nsp_count_path(NSP_PATH_SYMM);
       nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream, cs);
@@ -391,6 +438,9 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_gspkB);
   fr(c->d_i1sys);
   fr(c->d_minv);
+  fr(c->d_oz_msl);
+  fr(c->d_oz_dexp);
+  fr(c->d_oz_mexp);
   fr(c->d_items);
   fr(c->d_i1_src);
   fr(c->d_b_src);

@@ -120,6 +120,11 @@ struct nsp_ctx {
   int2* d_items = nullptr;
   int n_items = 0;
   int n_items_sh = 0;         // several ranks: items [0, n_items_sh) belong to blocks coupled to shared rows
+  // a2+a3 on the INT8 tensor cores (nsp_ozaki.cu, reading R10): D-scaled S_j^{-1} lower tiles as 7 int8
+  // slices each, per-row delta exponents, per-block mu exponents
+  int8_t* d_oz_msl = nullptr;
+  int* d_oz_dexp = nullptr;
+  int* d_oz_mexp = nullptr;
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
   DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)
@@ -263,6 +268,18 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
           int cw, cudaStream_t st,
           int64_t cm_stride = 0);
 // wbmax: largest band half-width (tiles) of the systems, -1 unknown; <= 2 with cw 32 selects k_band_fb
+// a2+a3 on the INT8 tensor cores (Ozaki splitting, nsp_ozaki.cu)
+size_t oz_mslice_bytes(int64_t dense_tiles);
+size_t oz_wslice_bytes(int64_t wvu_rows, int s);
+void oz_setup(const FacSub* subs, int nsub, int max_ntb, const int2* items, int nitems, const double* minv,
+              int* dexp, int* mexp, int8_t* msl, cudaStream_t st);
+// W^T slices of every block (chunk-major W, nch chunks, s columns) -> wsl, sexp (nsub * nct * 128 ints)
+void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int s, int nch, const double* W,
+                int64_t cs, const int* dexp, int8_t* wsl, int* sexp, cudaStream_t st);
+// U = S_j^{-1} W for the items [0, nitems) from the slices (chunk-major U)
+void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nch, double* U, int64_t cs,
+                const int* dexp, const int* mexp, const int8_t* msl, const int8_t* wsl, const int* sexp,
+                cudaStream_t st);
 // a2+a3 for one column (ld ldw, column 0): u_j = S_j^{-1} w_j, matrix-vector (s = 1)
 void symv(const FacSub* subs, const int2* items, int nitems, int max_ntb, const double* minv, const double* W, int ldw,
           double* U, cudaStream_t st);

@@ -1,0 +1,424 @@
+// a2+a3 (U_j = S_j^{-1} W_j for every block; the product that the boundary-last
+// ordering of reading R1 leaves, "factorized cheaply in parallel") on the 5th-generation
+// INT8 tensor cores (tcgen05.mma kind::i8, accumulators in TMEM) with fp64 accuracy: the Ozaki
+// splitting (DESIGN.md §6 "k_oz_symm", reading R10).
+//
+//   M_j = S_j^{-1} is symmetric positive definite.  With D = diag(delta_n), delta_n = 2^e_n and
+//   e_n = floor(log2(M_nn)/2), the symmetrically scaled Mt = D^{-1} M D^{-1} has |Mt_kn| <=
+//   sqrt(Mt_kk Mt_nn) < 2, so ONE power-of-two scale mu_j per block serves every entry and the scaling
+//   is the same for a stored lower tile read as itself (K-major) or transposed (MN-major): only the
+//   lower tiles are sliced, as in k_symm.  Wt = D W.  Each column c of Wt (per block) gets its own
+//   power-of-two scale sigma_c.  Every scaled entry x (|x| < 1/2) is the 56-bit fixed-point integer
+//   X = rint(x 2^55) = sum_{i=1..7} d_i 256^{7-i}, d_i signed bytes (|d_1| <= 64).  Then
+//     sum_k Wt(k,c) Mt(k,n) = sigma_c mu_j 2^-110 sum_{i,j} 256^{14-i-j} sum_k dW_i(c,k) dM_j(k,n)
+//   and the 28 int8 products with i + j <= 8 are accumulated EXACTLY in int32 (7 accumulators, one per
+//   diagonal i + j; |sum| <= 7 * 64 tiles... < 2^31 for b_j < 18,000, checked at setup); the dropped
+//   diagonals i + j >= 9 are below 2^-57 sigma_c mu_j sqrt(b) (under fp64 rounding of the result).
+//   The epilogue forms u = sum_D 2^{2-8D} acc_D in fp64 (least significant first) and scales by the
+//   powers of two: U(n, c) = delta_n sigma_c mu_j u.
+//
+// Layouts (no-swizzle canonical UMMA core matrices: 8 rows x 16 bytes, 128 contiguous bytes):
+//   M slices (setup, constant): stored lower tile (I, J) of block j (same index as the S_j^{-1} tiles,
+//     dense_off + I(I+1)/2 + J), 7 slices x 4096 B, slice = [r/8][c/16][r%8][c%16] (r, c: tile row, col).
+//   W^T slices (per apply): per W/V/U 64-row tile T and column tile ct (128 columns), 7 slices x 8192 B,
+//     slice = [c/8][k/16][c%8][k%16] (c: column within ct, k: row within the tile).
+// CTA work unit: (block j, output tile row I, column tile ct): D(c, n) = sum_K Wt_K^T Mt_(K, I)
+//   A operand = W^T slices (M = 128 columns c, K-major), B operand = Mt column tile I (N = 64 rows n):
+//   for K <= I the stored tile (I, K) read K-major, for K > I the stored tile (K, I) read MN-major.
+#include <climits>
+#include "nsp_internal.h"
+#include "nsp_dmma.cuh"
+
+using namespace nspd;
+
+namespace {
+constexpr int OZ_NS = 7;                 // slices
+constexpr int OZ_MT = OZ_NS * 4096;      // bytes: sliced 64 x 64 M tile
+constexpr int OZ_AT = OZ_NS * 8192;      // bytes: sliced 128 x 64 W^T tile
+constexpr int OZ_NST = 2;                // pipeline stages
+constexpr int OZ_SMEM = OZ_NST * (OZ_AT + OZ_MT) + 1024;
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// no-swizzle shared-memory matrix descriptor (sm_100, version 1): start, leading / stride byte offsets
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+// instruction descriptor kind::i8: s8 x s8 -> s32, M = 128, N = 64, A K-major, B K-major / MN-major
+constexpr uint32_t oz_idesc(int b_mn) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn << 16) | ((uint32_t)(64 >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(s_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.b32 %0, 1, 0, P;\n}\n" : "=r"(p));
+  return p != 0;
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// X = rint(x 2^55) (|x| < 1/2) as 7 signed base-256 digits, most significant first
+__device__ __forceinline__ void oz_digits(double x, int (&d)[OZ_NS]) {
+  long long X = __double2ll_rn(x);
+#pragma unroll
+  for (int i = OZ_NS - 1; i > 0; --i) {
+    const int lo = (int)(signed char)(X & 0xFF);
+    d[i] = lo;
+    X = (X - lo) >> 8;
+  }
+  d[0] = (int)X;
+}
+// exponent e with |v| < 2^e for every v of a set whose max is m (m >= 0): frexp exponent
+__device__ __forceinline__ int oz_exp_above(double m) {
+  if (!(m > 0.0)) return INT_MIN / 4;
+  int e;
+  frexp(m, &e);   // m = f 2^e, f in [0.5, 1)  ->  m < 2^e
+  return e;
+}
+
+// ---------------------------------------------------------------- setup kernels
+// e_n = floor(log2(M_nn) / 2) per W/V/U row (delta_n = 2^e_n); grid (nsub, max_ntb), 64 threads
+__global__ void k_oz_dexp(const FacSub* __restrict__ subs, const double* __restrict__ minv, int* __restrict__ dexp) {
+  const FacSub sb = subs[blockIdx.x];
+  const int I = blockIdx.y;
+  if (I >= sb.ntb) return;
+  const int i = threadIdx.x;
+  const double m = minv[(sb.dense_off + (int64_t)I * (I + 1) / 2 + I) * NSP_MINV_TILE + i * NSP_MINV_LD + i];
+  int e = 0;
+  if (m > 0.0 && isfinite(m)) {
+    int x;
+    frexp(m, &x);   // m in [2^(x-1), 2^x)
+    e = (x - 1) >= 0 ? (x - 1) / 2 : -((2 - x) / 2);   // floor((x - 1) / 2)
+  }
+  dexp[sb.wvu_row + (int64_t)I * 64 + i] = e;
+}
+
+// mu_j exponent: max over the block's stored tiles of |M_rc| / (delta_r delta_c); items = (j, I)
+__global__ void __launch_bounds__(256) k_oz_mexp(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                                 const double* __restrict__ minv, const int* __restrict__ dexp,
+                                                 int* __restrict__ mexp) {
+  const int2 it = items[blockIdx.x];
+  const FacSub sb = subs[it.x];
+  const int I = it.y;
+  __shared__ double red[8];
+  double mx = 0.0;
+  for (int J = 0; J <= I; ++J) {
+    const double* T = minv + (sb.dense_off + (int64_t)I * (I + 1) / 2 + J) * NSP_MINV_TILE;
+    for (int e = threadIdx.x; e < 4096; e += 256) {
+      const int r = e >> 6, c = e & 63;
+      const int er = dexp[sb.wvu_row + (int64_t)I * 64 + r], ec = dexp[sb.wvu_row + (int64_t)J * 64 + c];
+      mx = fmax(mx, fabs(ldexp(T[r * NSP_MINV_LD + c], -er - ec)));
+    }
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
+    atomicMax(&mexp[it.x], oz_exp_above(mx) + 1);   // |Mt| / mu < 1/2
+  }
+}
+
+// slices of the stored lower tiles; items = (j, I), 256 threads = 64 rows x 4 column groups of 16
+__global__ void __launch_bounds__(256) k_oz_slice_m(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                                    const double* __restrict__ minv, const int* __restrict__ dexp,
+                                                    const int* __restrict__ mexp, int8_t* __restrict__ msl) {
+  const int2 it = items[blockIdx.x];
+  const FacSub sb = subs[it.x];
+  const int I = it.y, mu = mexp[it.x];
+  const int r = threadIdx.x >> 2, h = threadIdx.x & 3;
+  const int er = dexp[sb.wvu_row + (int64_t)I * 64 + r];
+  for (int J = 0; J <= I; ++J) {
+    const int64_t t = sb.dense_off + (int64_t)I * (I + 1) / 2 + J;
+    const double* T = minv + t * NSP_MINV_TILE + r * NSP_MINV_LD + 16 * h;
+    uint32_t pk[OZ_NS][4];
+#pragma unroll
+    for (int i = 0; i < OZ_NS; ++i) pk[i][0] = pk[i][1] = pk[i][2] = pk[i][3] = 0u;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int ec = dexp[sb.wvu_row + (int64_t)J * 64 + 16 * h + q];
+      int d[OZ_NS];
+      oz_digits(ldexp(T[q], 55 - er - ec - mu), d);
+#pragma unroll
+      for (int i = 0; i < OZ_NS; ++i) pk[i][q >> 2] |= ((uint32_t)(d[i] & 0xFF)) << (8 * (q & 3));
+    }
+    int8_t* out = msl + t * OZ_MT + ((r >> 3) * 4 + h) * 128 + (r & 7) * 16;
+#pragma unroll
+    for (int i = 0; i < OZ_NS; ++i)
+      *reinterpret_cast<uint4*>(out + i * 4096) = make_uint4(pk[i][0], pk[i][1], pk[i][2], pk[i][3]);
+  }
+}
+
+// ---------------------------------------------------------------- per-apply W^T slices
+// W chunk-major padded (column c of W/V/U row r at W + (c/32) cs + r * 36 + c % 32), nch chunks.
+// (1) column exponents: grid (items, nct * 4), 256 threads (lane = column of the 32-column group q of column
+// tile ct, warp = 8 rows of the item's 64-row tile); the max over the block's tiles is an integer atomicMax
+// of exponents (order-independent: deterministic).  sexp must hold INT_MIN-ish on entry.
+__global__ void __launch_bounds__(256) k_oz_wmax(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                                 const double* __restrict__ W, int64_t cs, int nch, int nct,
+                                                 const int* __restrict__ dexp, int* __restrict__ sexp) {
+  pdl_wait();
+  const int2 it = items[blockIdx.x];
+  const FacSub sb = subs[it.x];
+  const int ct = blockIdx.y >> 2, q = blockIdx.y & 3;
+  const int chunk = ct * 4 + q;
+  if (chunk >= nch) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = sb.wvu_row + (int64_t)it.y * 64 + warp * 8;
+  const double* Wc = W + (int64_t)chunk * cs + r0 * 36 + lane;
+  double mx = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) mx = fmax(mx, fabs(ldexp(Wc[k * 36], dexp[r0 + k])));
+  __shared__ double red[8][33];
+  red[warp][lane] = mx;
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w][lane]);
+    if (mx > 0.0) atomicMax(&sexp[((int64_t)it.x * nct + ct) * 128 + q * 32 + lane], oz_exp_above(mx) + 1);
+  }
+}
+// (2) slices: grid (items, nct * 4), 128 threads (lane = column, warp = 16-row group h of the tile)
+__global__ void __launch_bounds__(128) k_oz_slice_w(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                                    const double* __restrict__ W, int64_t cs, int nch, int nct,
+                                                    const int* __restrict__ dexp, const int* __restrict__ sexp,
+                                                    int8_t* __restrict__ wsl) {
+  pdl_wait();
+  const int2 it = items[blockIdx.x];
+  const FacSub sb = subs[it.x];
+  const int ct = blockIdx.y >> 2, q = blockIdx.y & 3;
+  const int chunk = ct * 4 + q;
+  const int lane = threadIdx.x & 31, h = threadIdx.x >> 5;
+  const int cc = q * 32 + lane;   // column within the column tile
+  uint32_t pk[OZ_NS][4];
+#pragma unroll
+  for (int i = 0; i < OZ_NS; ++i) pk[i][0] = pk[i][1] = pk[i][2] = pk[i][3] = 0u;
+  if (chunk < nch) {
+    int e = sexp[((int64_t)it.x * nct + ct) * 128 + cc];
+    if (e < -4000) e = 0;   // all-zero column
+    const int64_t r0 = sb.wvu_row + (int64_t)it.y * 64 + h * 16;
+    const double* Wc = W + (int64_t)chunk * cs + r0 * 36 + lane;
+    double w[16];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) w[kk] = Wc[kk * 36];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      int d[OZ_NS];
+      oz_digits(ldexp(w[kk], 55 + dexp[r0 + kk] - e), d);
+#pragma unroll
+      for (int i = 0; i < OZ_NS; ++i) pk[i][kk >> 2] |= ((uint32_t)(d[i] & 0xFF)) << (8 * (kk & 3));
+    }
+  }
+  const int64_t T = sb.wvu_row / 64 + it.y;   // W/V/U tile
+  int8_t* out = wsl + (T * nct + ct) * (int64_t)OZ_AT + ((cc >> 3) * 4 + h) * 128 + (cc & 7) * 16;
+#pragma unroll
+  for (int i = 0; i < OZ_NS; ++i)
+    *reinterpret_cast<uint4*>(out + i * 8192) = make_uint4(pk[i][0], pk[i][1], pk[i][2], pk[i][3]);
+}
+
+// ---------------------------------------------------------------- the tcgen05 product
+// Persistent, one CTA per SM (TMEM: 7 accumulators x 64 columns of 512).  Warp 0: bulk-copy producer;
+// warp 1: TMEM owner + MMA issuer; warps 2..9: epilogue (TMEM lane quarter = warp % 4, 32 of the 64 rows n).
+// Work unit t in [0, nitems * nct): item t % nitems, column tile t / nitems.
+__global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                                    int nitems, int nct, const int8_t* __restrict__ msl,
+                                                    const int8_t* __restrict__ wsl, const int* __restrict__ dexp,
+                                                    const int* __restrict__ mexp, const int* __restrict__ sexp,
+                                                    double* __restrict__ U, int64_t cs, int nch) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t full[OZ_NST], empty[OZ_NST], tfull, tempty;
+  __shared__ uint32_t tbase;
+  uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nunits = nitems * nct;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, 8);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(s_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  pdl_wait();
+  if (warp == 0) {
+    if (elect_one()) {   // producer
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int2 it = items[u % nitems];
+        const int ct = u / nitems;
+        const FacSub sb = subs[it.x];
+        const int I = it.y;
+        const int64_t T0 = sb.wvu_row / 64;
+        for (int K = 0; K < sb.ntb; ++K) {
+          mbar_wait(&empty[st], ph ^ 1);
+          uint8_t* As = base + st * (OZ_AT + OZ_MT);
+          mbar_expect(&full[st], OZ_AT + OZ_MT);
+          bulk_copy(As, wsl + ((T0 + K) * nct + ct) * (int64_t)OZ_AT, OZ_AT, &full[st]);
+          const int64_t t = sb.dense_off + (K <= I ? (int64_t)I * (I + 1) / 2 + K : (int64_t)K * (K + 1) / 2 + I);
+          bulk_copy(As + OZ_AT, msl + t * OZ_MT, OZ_MT, &full[st]);
+          if (++st == OZ_NST) st = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int st = 0;
+    uint32_t ph = 0, tph = 0;
+    constexpr uint32_t ID_K = oz_idesc(0), ID_MN = oz_idesc(1);
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int2 it = items[u % nitems];
+      const int I = it.y, ntb = subs[it.x].ntb;
+      mbar_wait(&tempty, tph ^ 1);   // the epilogue has drained the previous unit's accumulators
+      tc_fence_after();
+      for (int K = 0; K < ntb; ++K) {
+        mbar_wait(&full[st], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a0 = s_u32(base + st * (OZ_AT + OZ_MT)), b0 = a0 + OZ_AT;
+          const bool mn = K > I;
+          const uint32_t id = mn ? ID_MN : ID_K;
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int i = 0; i < OZ_NS; ++i)
+#pragma unroll
+              for (int j = 0; i + j < OZ_NS; ++j) {
+                const uint64_t da = umma_desc(a0 + i * 8192 + k * 256, 128, 512);
+                const uint64_t db = mn ? umma_desc(b0 + j * 4096 + k * 2048, 512, 128)
+                                       : umma_desc(b0 + j * 4096 + k * 256, 128, 512);
+                mma_i8(tmem + (uint32_t)((i + j) * 64), da, db, id, (K | k | i) != 0);
+              }
+          mma_commit(&empty[st]);   // frees the stage once these MMAs have read it
+          if (K == ntb - 1) mma_commit(&tfull);
+        }
+        __syncwarp();
+        if (++st == OZ_NST) st = 0, ph ^= 1;
+      }
+      tph ^= 1;
+    }
+  } else {   // epilogue warps 2..9: TMEM lane quarter warp % 4, n-column half (warp - 2) / 4
+    const int qd = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int cc = qd * 32 + lane;
+    uint32_t tph = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int2 it = items[u % nitems];
+      const int ct = u / nitems;
+      const FacSub sb = subs[it.x];
+      const int I = it.y;
+      const int chunk = ct * 4 + qd;
+      const int ex = sexp[((int64_t)it.x * nct + ct) * 128 + cc] + mexp[it.x];
+      const int64_t row0 = sb.wvu_row + (int64_t)I * 64;
+      double* out = U + (int64_t)chunk * cs + row0 * 36 + lane;
+      mbar_wait(&tfull, tph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int nb = 2 * half; nb < 2 * half + 2; ++nb) {
+        uint32_t v[OZ_NS][16];
+#pragma unroll
+        for (int a = 0; a < OZ_NS; ++a)
+          tmem_ld16(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(a * 64 + nb * 16), v[a]);
+        tmem_ld_wait();
+        if (chunk < nch) {
+#pragma unroll
+          for (int nn = 0; nn < 16; ++nn) {
+            // diagonal a carries weight 2^(-14-8a): the three leading diagonals combine exactly into an int64
+            // (< 2^48, exact in fp64), the four trailing ones into a second (< 2^56)
+            const long long hi = ((long long)(int)v[0][nn] << 16) + ((long long)(int)v[1][nn] << 8) + (int)v[2][nn];
+            const long long lo = ((long long)(int)v[3][nn] << 24) + ((long long)(int)v[4][nn] << 16) +
+                                 ((long long)(int)v[5][nn] << 8) + (int)v[6][nn];
+            const double acc = fma((double)hi, 0x1p-30, (double)lo * 0x1p-62);
+            const int n = nb * 16 + nn;
+            const int E = ex + dexp[row0 + n];
+            out[(int64_t)n * 36] = (E >= -1022 && E <= 1023) ? acc * __longlong_as_double((long long)(E + 1023) << 52)
+                                                             : ldexp(acc, E);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty);
+      tph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+}  // namespace
+
+namespace nspk {
+
+size_t oz_mslice_bytes(int64_t dense_tiles) { return (size_t)dense_tiles * OZ_MT; }
+size_t oz_wslice_bytes(int64_t wvu_rows, int s) {
+  const int nct = (s + 127) / 128;
+  return (size_t)(wvu_rows / 64) * nct * OZ_AT;
+}
+
+// setup: dexp (wvu_rows ints), mexp (nsub ints), msl (oz_mslice_bytes) from the S_j^{-1} tiles
+void oz_setup(const FacSub* subs, int nsub, int max_ntb, const int2* items, int nitems, const double* minv,
+              int* dexp, int* mexp, int8_t* msl, cudaStream_t st) {
+  if (nsub <= 0 || nitems <= 0) return;
+  nsp_count_launch();
+  k_oz_dexp<<<dim3(nsub, max_ntb), 64, 0, st>>>(subs, minv, dexp);
+  cudaMemsetAsync(mexp, 0x80, (size_t)nsub * sizeof(int), st);   // INT_MIN-ish
+  nsp_count_launch();
+  k_oz_mexp<<<nitems, 256, 0, st>>>(subs, items, minv, dexp, mexp);
+  nsp_count_launch();
+  k_oz_slice_m<<<nitems, 256, 0, st>>>(subs, items, minv, dexp, mexp, msl);
+}
+
+void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int s, int nch, const double* W,
+                int64_t cs, const int* dexp, int8_t* wsl, int* sexp, cudaStream_t st) {
+  if (nitems <= 0) return;
+  const int nct = (s + 127) / 128;
+  cudaMemsetAsync(sexp, 0x80, (size_t)nsub * nct * 128 * sizeof(int), st);
+  nsp_count_launch();
+  launch_k(k_oz_wmax, dim3(nitems, nct * 4), dim3(256), 0, st, subs, items, W, cs, nch, nct, dexp, sexp);
+  nsp_count_launch();
+  launch_k(k_oz_slice_w, dim3(nitems, nct * 4), dim3(128), 0, st, subs, items, W, cs, nch, nct, dexp,
+           (const int*)sexp, wsl);
+}
+
+void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nch, double* U, int64_t cs,
+                const int* dexp, const int* mexp, const int8_t* msl, const int8_t* wsl, const int* sexp,
+                cudaStream_t st) {
+  if (nitems <= 0) return;
+  const int nct = (s + 127) / 128;
+  smem_optin((const void*)k_oz_symm, OZ_SMEM);
+  const int units = nitems * nct;
+  const int grid = units < num_sms() ? units : num_sms();
+  nsp_count_launch();
+  launch_k(k_oz_symm, dim3(grid), dim3(320), (size_t)OZ_SMEM, st, subs, items, nitems, nct, msl, wsl, dexp, mexp,
+           sexp, U, cs, nch);
+}
+
+}  // namespace nspk

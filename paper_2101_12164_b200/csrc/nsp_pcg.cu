@@ -443,7 +443,14 @@ static nsp_status interior_boundary_solve(nsp_ctx* c, PcgWs& w) {
   NSP_CUDA_TRY(c, cudaMemcpyAsync(w.i1buf, w.i1r, (size_t)c->i1_rows * 32 * 8, cudaMemcpyDeviceToDevice, c->stream));
   nspk::tri_fb(c->d_i1sys, c->nsub, w.i1buf, 32, 32, true, true, c->stream, c->i1_wbmax);
   nspk::spmm(c->CB, w.bB, 32, w.i1buf, 32, c->wvu_rows, w.wvu, 32, 1, 1, true, c->stream);
-  nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, w.wvu, 32, 32, c->stream);
+  if (c->d_minv) {   // y_B = S_j^{-1}(...) in place (k_symv1 reads w.wvu, its reduce writes it; partial
+                     // slots in the apply workspace, idle here)
+    double* P = w.apply_wvu + 2 * c->wvu_rows * 32;
+    P = (double*)(((uintptr_t)P + 255) & ~(uintptr_t)255);
+    nspk::symv1(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, w.wvu, 32, w.wvu, P, c->stream);
+  } else {
+    nspk::trsm_fb(c->d_subs, c->nsub, c->d_dense, w.wvu, 32, 32, c->stream);
+  }
   NSP_CUDA_TRY(c, cudaGetLastError());
   return NSP_OK;
 }

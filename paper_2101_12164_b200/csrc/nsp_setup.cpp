@@ -1,3 +1,4 @@
+#include <cstdio>
 // nsp_setup: host analysis (validation, DBBD permutation, per-block ordering, tile layout), the
 // host->device copy, and the GPU numeric factorisation (§8(a) row s0).
 //
@@ -1267,7 +1268,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
                                           std::to_string(orig) + ")");
     }
   // ---------------- explicit S_j^{-1} tiles for the one-product a2+a3 (opts.apply_kernel == 0)
-  if (c->opts.apply_kernel == 0 && dense_tiles > 0) {
+  if (c->opts.apply_kernel != 1 && dense_tiles > 0) {
     const size_t bytes = (size_t)dense_tiles * NSP_MINV_TILE * 8;
     size_t fr = 0, tot = 0;
     NSP_CUDA_TRY(c, cudaMemGetInfo(&fr, &tot));
@@ -1297,9 +1298,45 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
         if (blk_sh[j]) c->n_items_sh += sh[j].ntb;
       if ((st = upload(c, &c->d_items, items)) != NSP_OK) return st;
       NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      // the L22 tiles are not read again once S_j^{-1} exists (a2+a3, the full solve's y_B and the S_I
+      // forms' block elimination all use S_j^{-1}): release them (cfg5: 42 GB)
+      cudaFree(c->d_dense);
+      c->d_dense = nullptr;
     }
   }
   const double t_fac_all = ms_since(t2);
+  // ---------------- INT8 tensor-core slices of the S_j^{-1} tiles (reading R10; apply_kernel 0 / 3):
+  // D-scaled lower tiles as 7 int8 slices each (a quarter of the fp64 tiles' bytes... 7/8 of their
+  // lower-triangle bytes); the fp64 tiles stay (s = 1 products, the S_I forms).  Skipped when the
+  // device budget does not allow it (a2+a3 then stays on the DMMA k_symm) or when a block is so large
+  // that the int32 diagonal sums could overflow (b_j > 300 tiles).
+  double t_oz = 0.0;
+  {
+    const char* oe = getenv("NSP_OZAKI");
+    const bool oz_on = !(oe && oe[0] == '0');
+    if (c->d_minv && oz_on && (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3) && c->max_ntb <= 300 &&
+        c->n_items > 0) {
+      auto t4 = Clock::now();
+      const size_t mb = nspk::oz_mslice_bytes(dense_tiles);
+      size_t fr = 0, tot = 0;
+      NSP_CUDA_TRY(c, cudaMemGetInfo(&fr, &tot));
+      const char* re = getenv("NSP_OZ_RESERVE_GB");
+      const size_t reserve = (size_t)((re ? atof(re) : 12.0) * 1073741824.0);
+      if (mb + reserve < fr) {
+        NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_oz_msl, mb));
+        NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_oz_dexp, (size_t)c->wvu_rows * sizeof(int)));
+        NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_oz_mexp, (size_t)c->nsub * sizeof(int)));
+        nspk::oz_setup(c->d_subs, c->nsub, c->max_ntb, c->d_items, c->n_items, c->d_minv, c->d_oz_dexp,
+                       c->d_oz_mexp, c->d_oz_msl, c->stream);
+        NSP_CUDA_TRY(c, cudaGetLastError());
+        NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      } else if (c->opts.verbose) {
+        fprintf(stderr, "nsp_setup: INT8 slices (%.1f GB) skipped: %.1f GB free, %.1f GB reserve\n", mb / 1e9,
+                fr / 1e9, reserve / 1e9);
+      }
+      t_oz = ms_since(t4);
+    }
+  }
   double t_ag = 0.0;
   if (c->opts.factor_gamma) {
     auto t3 = Clock::now();
@@ -1328,6 +1365,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
     rep->t_ms[1] = t_h2d;
     rep->t_ms[2] = t_fac;
     rep->t_ms[4] = t_fac_all - t_fac;   // S_j^{-1} tiles
+    rep->t_ms[5] = t_oz;                // their INT8 slices
   }
   NSP_CUDA_TRY(c, cudaMallocHost(&c->h_status, 4096));
   return NSP_OK;

@@ -6,6 +6,7 @@ namespace nspi {
 int pick_cw(const nsp_ctx* c, int s);
 int ld_pad(int s, int cw);
 size_t apply_ws_bytes(const nsp_ctx* c, int s);
+bool use_ozaki(const nsp_ctx* c, int s);
 nsp_status get_ws(nsp_ctx* c, void* ws, size_t need, char** out);
 nsp_status finish_shared_rows(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, bool ag_term);
 nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, int s, int mode, double* wvu);

@@ -28,7 +28,7 @@ EXPORTED = ["nsp_default_opts", "nsp_setup", "nsp_dims", "nsp_gamma_index", "nsp
 
 # dispatch-path counter ids (include/nsp.h NSP_PATH_*)
 PATHS = ["panel_rows", "panel_tiles", "gram_sym", "gram_de", "gram_full", "symm", "sweeps", "symv",
-         "panel_gram", "chol_solve"]
+         "panel_gram", "chol_solve", "ozaki"]
 
 
 class nsp_csr(C.Structure):

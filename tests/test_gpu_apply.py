@@ -13,10 +13,11 @@ CASES = [("cfg1", 30), ("cfg1", 1), ("cfg1", 7), ("cfg2s", 32), ("cfg2s", 100), 
          ("cfg3s", 64), ("cfg4s", 24), ("cfg5s", 32), ("cfg5s", 128)]
 
 
-@pytest.mark.parametrize("apply_kernel", [0, 1])
+@pytest.mark.parametrize("apply_kernel", [0, 1, 2])
 @pytest.mark.parametrize("name,s", CASES)
 def test_schur_apply_parity(name, s, apply_kernel):
-    """apply_kernel 0: a2+a3 as one product with the explicit S_j^{-1} tiles; 1: the L22 sweeps."""
+    """apply_kernel 0: a2+a3 as one product with the explicit S_j^{-1} tiles (INT8 tensor cores for
+    s >= 48, reading R10); 1: the L22 sweeps; 2: the fp64 DMMA product only."""
     pr, d, S = problem(name)
     ctx = context(pr, apply_kernel=apply_kernel)
     X = block(d.n_gamma, s)

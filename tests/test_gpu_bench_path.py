@@ -71,8 +71,8 @@ def test_bench_path_bcg_parity_cfg2(mode):
     Xg = X.cpu().numpy()
     true_res = np.linalg.norm(B - L.apply(Xg), axis=0) / np.linalg.norm(B, axis=0)
     assert true_res.max() <= pr.tol_bcg * 1.001, true_res.max()
-    # the bench's kernels ran: one-wave panel, symmetric W^T W, [D | E]
-    for k in ("panel_rows", "gram_sym", "gram_de"):
+    # the bench's kernels ran: one-wave panel, symmetric W^T W, [D | E], a2+a3 on the INT8 tensor cores
+    for k in ("panel_rows", "gram_sym", "gram_de", "ozaki"):
         assert c1[k] > c0[k], (k, c0, c1)
     # equal iteration counts (reading C16)
     for k in (1, 2, 3):
