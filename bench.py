@@ -350,14 +350,24 @@ def measure(pr, args, ws, rank, local, stream, nccl_id, headline):
     # every a2+a3 launch on the context stream (per-iteration graphs carry the pair)
     ctx.profile(True)
     ctx.profile_read()
+    pc0 = nsp.path_counters()
     for _ in range(min(args.steps, 3)):
         flush.zero_()
         step()
     torch.cuda.synchronize()
     sweep_ms, sweeps = ctx.profile_read()
     ctx.profile(False)
+    int8 = nsp.path_counters()["ozaki"] > pc0["ozaki"]
+    # tile bookkeeping: stored lower S_j^-1 tiles T_l = sum ntb(ntb+1)/2, W/V/U tiles T_w = sum ntb,
+    # (output tile, K tile) pairs sum ntb^2 = 2 T_l - T_w
+    t_l, t_w = st["l22_entries"] // 4096, st["wvu_rows"] // 64
+    nct = (s + 127) // 128
     out["k_symm"] = {"avg_launch_ms": sweep_ms / max(sweeps, 1), "launches": sweeps,
-                     "flops_per_launch": 2.0 * st["sum_b2"] * s,
+                     "flops_per_launch": 2.0 * st["sum_b2"] * s, "int8": int8,
+                     # INT8 path: 28 slice products of 128 x 64 x 64 per (output tile, K tile) pair and column tile
+                     "int8_ops_per_launch": 2.0 * 28 * 128 * 64 * 64 * (2 * t_l - t_w) * nct,
+                     # unique bytes: the 7 slices of every stored tile, the W^T slices, U out (fp64)
+                     "int8_alg_bytes_per_launch": 7 * 4096 * t_l + 7 * 8192 * nct * t_w + 8 * s * st["wvu_rows"],
                      "alg_bytes_per_launch": 8 * (st["sum_b2"] + st["sum_b"]) / 2 + 2 * 8 * s * st["sum_b"]}
     # apply-only timing (a1-a5), L2 flushed
     P_ = torch.randn(nG, s, dtype=torch.float64, device=dev)
@@ -456,11 +466,45 @@ def run_ours(args, ws, rank, local):
     peaks = _peaks()
     ks = m["k_symm"]
     achieved = ks["flops_per_launch"] / (ks["avg_launch_ms"] * 1e-3) / 1e12
-    traffic, traffic_src = _traffic(args.config)
+    if ks["int8"]:
+        traffic, traffic_src = _traffic(args.config, "k_oz_symm")
+        i8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0)
+        i8_ach = ks["int8_ops_per_launch"] / (ks["avg_launch_ms"] * 1e-3) / 1e12
+        roof = {"kernel": "k_oz_symm (a2+a3: U_j = S_j^-1 W_j on the INT8 tensor cores, tcgen05 kind::i8 with TMEM "
+                          "accumulators; Ozaki splitting into 7 int8 slices, 28 exact int32 slice products, fp64 "
+                          "result; reading R10)",
+                "bound": "tensor", "achieved": i8_ach, "peak": i8_peak, "unit": "TOP/s", "frac": i8_ach / i8_peak,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst, cuBLAS) x 2, the nominal INT8:BF16 dense "
+                               "ratio of the B200 tensor core" + ("" if "bf16_tflops" in peaks else
+                                                                  " (fallback: nominal 2.25 PF bf16)"),
+                "algorithmic_int8_ops_per_launch": ks["int8_ops_per_launch"],
+                "algorithmic_bytes_per_launch": ks["int8_alg_bytes_per_launch"],
+                "fp64_equivalent_tflops": achieved,
+                "fp64_equivalent_vs_dmma_peak": achieved / FP64_PEAK_TFLOPS,
+                "hbm_gbs_at_alg_bytes": ks["int8_alg_bytes_per_launch"] / (ks["avg_launch_ms"] * 1e-3) / 1e9}
+    else:
+        traffic, traffic_src = _traffic(args.config)
+        roof = {"kernel": "k_symm (a2+a3: U_j = S_j^-1 W_j, all blocks one launch)", "bound": "tensor",
+                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": "fp64 DMMA microbenchmark tools/fp64_peak.cu (profiles/r01_fp64_peak.txt); "
+                               "MEASURED_PEAKS.json has no fp64 figure",
+                "algorithmic_flops_per_launch": ks["flops_per_launch"],
+                "algorithmic_bytes_per_launch": ks["alg_bytes_per_launch"],
+                "hbm_gbs_at_alg_bytes": ks["alg_bytes_per_launch"] / (ks["avg_launch_ms"] * 1e-3) / 1e9}
+    roof.update({"avg_launch_ms": ks["avg_launch_ms"], "launches": ks["launches"],
+                 "timing": "CUDA events around each launch of the kernel on the context stream, in a pass of the "
+                           "same steps right after the timed region (the timed region runs the event-free "
+                           "device-driven loop graph)",
+                 "hbm_peak_gbs": peaks.get("hbm_gbs"), "iteration_split_ms": m["iteration_split_ms"]})
+    traffic, traffic_src = roof["traffic"], roof["traffic_source"]
     line = {
         "metric": METRIC, "value": m["rhs_applies_per_s"] * 1.0, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["time_to_tol_ms"],
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "dtype_note": "fp64 results; a2+a3 as exact int32 sums of int8 slice products on the tensor cores (reading R10)",
+        "data": "synthetic",
         "config": {"workload": args.config, "n": pr.n, "n_gamma": m["n_gamma"], "K": pr.K, "s": pr.s,
                    "tol_bcg": pr.tol_bcg, "bcg_precond": "none (M = I, north_star-literal)",
                    "parallelism": f"subdomains over {ws} ranks (contiguous ND subtrees, shared-separator NCCL "
@@ -472,20 +516,7 @@ def run_ours(args, ws, rank, local):
         "pcg_ms": m.get("pcg_ms"), "pcg_iters": m.get("pcg_iters"), "pcg_tol": m.get("pcg_tol"),
         "setup_ms": m["setup_ms"], "setup_split_ms": m["setup_split_ms"],
         "apply": m["apply"], "iteration_split_ms": m["iteration_split_ms"],
-        "roofline": {"kernel": "k_symm (a2+a3: U_j = S_j^-1 W_j, all blocks one launch)", "bound": "tensor",
-                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
-                     "peak_source": "fp64 DMMA microbenchmark tools/fp64_peak.cu (profiles/r01_fp64_peak.txt); "
-                                    "MEASURED_PEAKS.json has no fp64 figure",
-                     "algorithmic_flops_per_launch": ks["flops_per_launch"],
-                     "algorithmic_bytes_per_launch": ks["alg_bytes_per_launch"],
-                     "avg_launch_ms": ks["avg_launch_ms"], "launches": ks["launches"],
-                     "timing": "CUDA events around each a2+a3 launch on the context stream, in a pass of the "
-                               "same steps right after the timed region (the timed region runs the event-free "
-                               "device-driven loop graph)",
-                     "hbm_gbs_at_alg_bytes": ks["alg_bytes_per_launch"] / (ks["avg_launch_ms"] * 1e-3) / 1e9,
-                     "hbm_peak_gbs": peaks.get("hbm_gbs"),
-                     "iteration_split_ms": m["iteration_split_ms"]},
+        "roofline": roof,
         "e2e": m["e2e"], "gpu_launches": m["gpu_launches"], "clocks": m["clocks"],
     }
     if ws == 1 and not args.no_secondary and args.secondary and args.secondary != args.config:

@@ -102,8 +102,14 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   // graph) the context's dedicated pair, read after every graph launch (nsp_solver.cu)
   const bool gprof = c->prof_on && c->capturing;
   const bool prof = !gprof && c->prof_on && (size_t)(c->prof_used + 2) <= c->prof_ev.size();
-  if (gprof) cudaEventRecordWithFlags(c->gprof_ev[0], c->stream, cudaEventRecordExternal);   // a graph node
-  if (prof) cudaEventRecord(c->prof_ev[c->prof_used], c->stream);
+  // the pair brackets the dominant kernel: the whole a2+a3 (DMMA product, sweeps, s = 1 product) or, on the
+  // INT8 path, the tensor-core product k_oz_symm after the W^T slicing
+  const bool oz1 = c->d_minv && s > 1 && use_ozaki(c, s);
+  auto mark_start = [&]() {
+    if (gprof) cudaEventRecordWithFlags(c->gprof_ev[0], c->stream, cudaEventRecordExternal);   // a graph node
+    if (prof) cudaEventRecord(c->prof_ev[c->prof_used], c->stream);
+  };
+  if (!oz1) mark_start();
   double* U = wvu;
   // several ranks, s > 1 (SURVEY.md §8(e) budget: "process the subdomains adjacent to shared separators
   // first and launch the allreduce on a second stream"): the blocks coupled to shared rows are multiplied
@@ -166,6 +172,7 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
       int* sexp = (int*)(wsl + nspk::oz_wslice_bytes(c->wvu_rows, s));
       nspk::oz_slice_w(c->d_subs, c->d_items, c->n_items, c->nsub, s, ldw / 32, wvu, cs, c->d_oz_dexp, wsl, sexp,
                        c->stream);
+      mark_start();
       nspk::oz_product(c->d_subs, c->d_items, c->n_items, s, ldw / 32, U, cs, c->d_oz_dexp, c->d_oz_mexp,
                        c->d_oz_msl, wsl, sexp, c->stream);
     } else {
