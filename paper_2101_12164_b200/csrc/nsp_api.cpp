@@ -93,8 +93,18 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
   // chunk-major padded W/U (s > 1 with the S_j^{-1} tiles): a 64 x 32 tile of W is one contiguous bulk copy
   const bool cm = c->d_minv && s > 1;
   const int64_t cs = (int64_t)c->wvu_rows * 36;
-  // a1: W = A_IG X on the boundary-layer rows (zero padding rows / columns)
-  if (cm) nspk::spmm_cs(c->A2G, X, ldx, nullptr, 0, 32, 0, wvu, 36, cs, ldw, s, 0, true, c->stream);
+  // a1: W = A_IG X on the boundary-layer rows (zero padding rows / columns); on the INT8 a2+a3 path it also
+  // reduces the W^T slices' per-(block, column) scale exponents (no separate pass over W)
+  const bool ozp = cm && use_ozaki(c, s);
+  int8_t* oz_wsl = ozp ? (int8_t*)((char*)wvu + oz_ws_offset(c, s)) : nullptr;
+  int* oz_sexp = ozp ? (int*)(oz_wsl + nspk::oz_wslice_bytes(c->wvu_rows, s)) : nullptr;
+  bool oz_have_exp = false;
+  if (ozp) {
+    NSP_CUDA_TRY(c, cudaMemsetAsync(oz_sexp, 0x80, (size_t)c->nsub * ((s + 127) / 128) * 128 * sizeof(int), c->stream));
+    oz_have_exp = nspk::spmm_cs_oz(c->A2G, X, ldx, wvu, cs, ldw, s, c->d_oz_dexp, c->d_oz_tblk, oz_sexp, c->stream);
+  }
+  if (oz_have_exp) {
+  } else if (cm) nspk::spmm_cs(c->A2G, X, ldx, nullptr, 0, 32, 0, wvu, 36, cs, ldw, s, 0, true, c->stream);
   else nspk::spmm(c->A2G, X, ldx, nullptr, 0, 0, wvu, ldw, s, 0, true, c->stream);
   // a2 + a3: U = L22^{-T} L22^{-1} W for every block, one launch: either as one symmetric product
   // with the setup's S_j^{-1} tiles (k_symm, no dependency chain) or as the two batched sweeps
@@ -122,8 +132,8 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
     const int64_t nsh = c->nG - c->n_priv;
     cudaStream_t main = c->stream;
     const bool oz = use_ozaki(c, s);
-    int8_t* wsl = oz ? (int8_t*)((char*)wvu + oz_ws_offset(c, s)) : nullptr;
-    int* sexp = oz ? (int*)(wsl + nspk::oz_wslice_bytes(c->wvu_rows, s)) : nullptr;
+    int8_t* wsl = oz_wsl;
+    int* sexp = oz_sexp;
     auto prod = [&](const int2* its, int nit) {
       if (oz) nspk::oz_product(c->d_subs, its, nit, s, ldw / 32, U, cs, c->d_oz_dexp, c->d_oz_mexp, c->d_oz_msl,
                                wsl, sexp, main);
@@ -132,7 +142,7 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
     nsp_count_path(oz ? NSP_PATH_OZAKI : NSP_PATH_SYMM);
     if (oz)
       nspk::oz_slice_w(c->d_subs, c->d_items, c->n_items, c->nsub, s, ldw / 32, wvu, cs, c->d_oz_dexp, wsl, sexp,
-                       main);
+                       main, oz_have_exp);
     prod(c->d_items, nsh_it);
     DevCSR shr = c->AGG2;   // the shared rows' slice of the a4+a5 operator
     shr.rows = nsh;
@@ -168,10 +178,10 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
       else nspk::symv1(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, P, c->stream);
     } else if (use_ozaki(c, s)) {
       nsp_count_path(NSP_PATH_OZAKI);
-      int8_t* wsl = (int8_t*)((char*)wvu + oz_ws_offset(c, s));
-      int* sexp = (int*)(wsl + nspk::oz_wslice_bytes(c->wvu_rows, s));
+      int8_t* wsl = oz_wsl;
+      int* sexp = oz_sexp;
       nspk::oz_slice_w(c->d_subs, c->d_items, c->n_items, c->nsub, s, ldw / 32, wvu, cs, c->d_oz_dexp, wsl, sexp,
-                       c->stream);
+                       c->stream, oz_have_exp);
       mark_start();
       nspk::oz_product(c->d_subs, c->d_items, c->n_items, s, ldw / 32, U, cs, c->d_oz_dexp, c->d_oz_mexp,
                        c->d_oz_msl, wsl, sexp, c->stream);
@@ -448,6 +458,7 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_oz_msl);
   fr(c->d_oz_dexp);
   fr(c->d_oz_mexp);
+  fr(c->d_oz_tblk);
   fr(c->d_items);
   fr(c->d_i1_src);
   fr(c->d_b_src);

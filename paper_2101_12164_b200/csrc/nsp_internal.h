@@ -125,6 +125,7 @@ struct nsp_ctx {
   int8_t* d_oz_msl = nullptr;
   int* d_oz_dexp = nullptr;
   int* d_oz_mexp = nullptr;
+  int* d_oz_tblk = nullptr;   // W/V/U tile -> local block
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
   DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)
@@ -257,6 +258,10 @@ void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, do
 // chunk strides: column c at row * ld + (c / 32) * cs + c % 32 (cs = 32: row-major)
 void spmm_cs(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t ucs, int64_t split,
              double* Y, int ldy, int64_t ycs, int ypad, int s, int mode, bool zero_pad, cudaStream_t st);
+// a1 for the INT8 a2+a3 (mode 0, chunk-major W, ld 36): also folds the per-(block, column) W^T scale exponents
+// into ozse (atomicMax; ozse pre-filled with INT_MIN-ish); false (nothing launched) when the shape is not eligible
+bool spmm_cs_oz(const DevCSR& A, const double* X, int ldx, double* Y, int64_t ycs, int ypad, int s,
+                const int* ozdx, const int* oztb, int* ozse, cudaStream_t st);
 void spmm(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t split,
           double* Y, int ldy, int s, int mode, bool zero_pad, cudaStream_t st);
 void trsm_fb(const FacSub* subs, int nsub, const double* dense, double* wvu, int ldw, int cw,
@@ -275,7 +280,7 @@ void oz_setup(const FacSub* subs, int nsub, int max_ntb, const int2* items, int 
               int* dexp, int* mexp, int8_t* msl, cudaStream_t st);
 // W^T slices of every block (chunk-major W, nch chunks, s columns) -> wsl, sexp (nsub * nct * 128 ints)
 void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int s, int nch, const double* W,
-                int64_t cs, const int* dexp, int8_t* wsl, int* sexp, cudaStream_t st);
+                int64_t cs, const int* dexp, int8_t* wsl, int* sexp, cudaStream_t st, bool have_exp = false);
 // U = S_j^{-1} W for the items [0, nitems) from the slices (chunk-major U)
 void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nch, double* U, int64_t cs,
                 const int* dexp, const int* mexp, const int8_t* msl, const int8_t* wsl, const int* sexp,

@@ -1,3 +1,4 @@
+#include <climits>
 // Device kernels of the S_G apply and the setup factorisation (north_star (a), (b); §8(a) rows
 // a1-a5, s0).  fp64 throughout; dense tile products on the DMMA pipe (mma.sync f64).
 #include <cuda_runtime.h>
@@ -274,17 +275,23 @@ __global__ void __launch_bounds__(256) k_spmm(int64_t rows, const int32_t* __res
 // of four.  At most 32 registers (8 CTAs of 256 threads per SM: full occupancy hides the dependent
 // row-pointer -> index -> row-load chain).  Requires even s and even leading dimensions / chunk strides
 // (16-byte aligned rows).
-template <int NQ2>
+// OZ (a1 feeding the INT8 a2+a3, reading R10): the CTA's 8 rows lie in one 64-row W/V/U tile (rows is a
+// multiple of 64), so the per-(block, column) scale exponents of the W^T slices are reduced over the 8 rows in
+// shared memory and folded into ozse[block * 128 * nct + c] by integer atomicMax (order-independent); ozdx:
+// delta exponent per row, oztb: block of each tile.
+template <int NQ2, bool OZ = false>
 __global__ void __launch_bounds__(256, NQ2 <= 2 ? 8 : 4) k_spmm2(int64_t rows, const int32_t* __restrict__ rp,
                                                const int32_t* __restrict__ ci, const double* __restrict__ va,
                                                const double* __restrict__ X, int ldx,
                                                const double* __restrict__ U, int ldu, int64_t ucs, int64_t split,
                                                double* __restrict__ Y, int ldy, int64_t ycs, int ypad, int s, int mode,
-                                               int zero_pad) {
+                                               int zero_pad, const int* __restrict__ ozdx = nullptr,
+                                               const int* __restrict__ oztb = nullptr, int* __restrict__ ozse = nullptr,
+                                               int ozn = 0) {
   pdl_wait();
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
+  if (!OZ && row >= rows) return;
   const int beg = rp[row], end = rp[row + 1];
   double2 acc[NQ2];
 #pragma unroll
@@ -346,6 +353,30 @@ __global__ void __launch_bounds__(256, NQ2 <= 2 ? 8 : 4) k_spmm2(int64_t rows, c
   if (zero_pad)
     for (int cc = 64 * NQ2 + 2 * lane; cc < ypad; cc += 64)
       *reinterpret_cast<double2*>(y + (int64_t)(cc >> 5) * ycs + (cc & 31)) = make_double2(0.0, 0.0);
+  if constexpr (OZ) {
+    __shared__ int ex[8][64 * NQ2];
+    const int w = threadIdx.x >> 5, d = ozdx[row];
+    auto ex_of = [&](double v) {
+      const double a = fabs(ldexp(v, d));
+      int e;
+      frexp(a, &e);
+      return a > 0.0 ? e + 1 : INT_MIN / 2;   // |v delta| / 2^e < 1/2
+    };
+#pragma unroll
+    for (int qq = 0; qq < NQ2; ++qq) {
+      const int cc = 2 * lane + 64 * qq;
+      ex[w][cc] = cc < s ? ex_of(acc[qq].x) : INT_MIN / 2;
+      ex[w][cc + 1] = cc + 1 < s ? ex_of(acc[qq].y) : INT_MIN / 2;
+    }
+    __syncthreads();
+    const int64_t blk = oztb[(row - w) / 64];
+    for (int c = threadIdx.x; c < s; c += 256) {
+      int m = ex[0][c];
+#pragma unroll
+      for (int r = 1; r < 8; ++r) m = max(m, ex[r][c]);
+      if (m > INT_MIN / 2) atomicMax(&ozse[blk * ozn + c], m);
+    }
+  }
 }
 
 // One step of the fixed Chebyshev iteration for A_G^{-1} (reading R7; one rank) fused with its sparse
@@ -1976,6 +2007,25 @@ void tile_cholesky(const FacSub* subs, int nsub, double* band, double* dense, do
   { nsp_count_launch(); k_tile_cholesky<<<nsub, 256, smem, st>>>(subs, band, dense, scratch, border_first, status); }
 }
 
+bool spmm_cs_oz(const DevCSR& A, const double* X, int ldx, double* Y, int64_t ycs, int ypad, int s,
+                const int* ozdx, const int* oztb, int* ozse, cudaStream_t st) {
+  if (A.rows <= 0 || A.rows % 64 || s % 2 || ldx % 2 || ycs % 2 || ypad % 2 || s > 256) return false;
+  const unsigned blocks = (unsigned)(A.rows / 8);
+  const int ozn = 128 * ((s + 127) / 128);
+  const int nq2 = (s + 63) / 64;
+  nsp_count_launch();
+  if (nq2 == 1)
+    launch_k(k_spmm2<1, true>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, nullptr, 0,
+             (int64_t)32, (int64_t)0, Y, 36, ycs, ypad, s, 0, 1, ozdx, oztb, ozse, ozn);
+  else if (nq2 == 2)
+    launch_k(k_spmm2<2, true>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, nullptr, 0,
+             (int64_t)32, (int64_t)0, Y, 36, ycs, ypad, s, 0, 1, ozdx, oztb, ozse, ozn);
+  else
+    launch_k(k_spmm2<4, true>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, nullptr, 0,
+             (int64_t)32, (int64_t)0, Y, 36, ycs, ypad, s, 0, 1, ozdx, oztb, ozse, ozn);
+  return true;
+}
+
 void spmm_cs(const DevCSR& A, const double* X, int ldx, const double* U, int ldu, int64_t ucs, int64_t split,
              double* Y, int ldy, int64_t ycs, int ypad, int s, int mode, bool zero_pad, cudaStream_t st) {
   if (A.rows <= 0) return;
@@ -2004,11 +2054,11 @@ void spmm_cs(const DevCSR& A, const double* X, int ldx, const double* U, int ldu
       ypad % 2 == 0 && s <= 256) {
     const int nq2 = (s + 63) / 64;
     if (nq2 == 1)
-      { nsp_count_launch(); launch_k(k_spmm2<1>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad); }
+      { nsp_count_launch(); launch_k(k_spmm2<1>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad, (const int*)nullptr, (const int*)nullptr, (int*)nullptr, 0); }
     else if (nq2 == 2)
-      { nsp_count_launch(); launch_k(k_spmm2<2>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad); }
+      { nsp_count_launch(); launch_k(k_spmm2<2>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad, (const int*)nullptr, (const int*)nullptr, (int*)nullptr, 0); }
     else
-      { nsp_count_launch(); launch_k(k_spmm2<4>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad); }
+      { nsp_count_launch(); launch_k(k_spmm2<4>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, X, ldx, U, ldu, ucs, split, Y, ldy, ycs, ypad, s, mode, zero_pad, (const int*)nullptr, (const int*)nullptr, (int*)nullptr, 0); }
     return;
   }
   if (s <= 32)

@@ -36,6 +36,7 @@ constexpr int OZ_NS = 7;                 // slices
 constexpr int OZ_MT = OZ_NS * 4096;      // bytes: sliced 64 x 64 M tile
 constexpr int OZ_AT = OZ_NS * 8192;      // bytes: sliced 128 x 64 W^T tile
 constexpr int OZ_NST = 2;                // pipeline stages
+constexpr int OZ_TS = 4;                 // A slices staged in TMEM (7 x 64 accumulator + 2 x 4 x 8 = 512 columns)
 constexpr int OZ_SMEM = OZ_NST * (OZ_AT + OZ_MT) + 1024;
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -55,6 +56,17 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+// A operand in TMEM (columns [ta, ta + 8)), B from shared memory
+__device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t ta, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(ta), "l"(b), "r"(id), "r"(acc));
+}
+// shared memory (canonical K-major, 128 rows x 32 bytes) -> TMEM (128 lanes x 8 columns)
+__device__ __forceinline__ void tc_cp(uint32_t ta, uint64_t sd) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n" ::"r"(ta), "l"(sd));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(s_u32(bar))
@@ -243,7 +255,7 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
                                                     int nitems, int nct, const int8_t* __restrict__ msl,
                                                     const int8_t* __restrict__ wsl, const int* __restrict__ dexp,
                                                     const int* __restrict__ mexp, const int* __restrict__ sexp,
-                                                    double* __restrict__ U, int64_t cs, int nch) {
+                                                    double* __restrict__ U, int64_t cs, int nch, int dbg) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ __align__(8) uint64_t full[OZ_NST], empty[OZ_NST], tfull, tempty;
   __shared__ uint32_t tbase;
@@ -281,10 +293,11 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
         for (int K = 0; K < sb.ntb; ++K) {
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* As = base + st * (OZ_AT + OZ_MT);
-          mbar_expect(&full[st], OZ_AT + OZ_MT);
-          bulk_copy(As, wsl + ((T0 + K) * nct + ct) * (int64_t)OZ_AT, OZ_AT, &full[st]);
+          mbar_expect(&full[st], ((dbg & 1) ? 0 : OZ_AT) + ((dbg & 2) ? 0 : OZ_MT) + ((dbg & 3) == 3 ? 16 : 0));
+          if (!(dbg & 1)) bulk_copy(As, wsl + ((T0 + K) * nct + ct) * (int64_t)OZ_AT, OZ_AT, &full[st]);
           const int64_t t = sb.dense_off + (K <= I ? (int64_t)I * (I + 1) / 2 + K : (int64_t)K * (K + 1) / 2 + I);
-          bulk_copy(As + OZ_AT, msl + t * OZ_MT, OZ_MT, &full[st]);
+          if (!(dbg & 2)) bulk_copy(As + OZ_AT, msl + t * OZ_MT, OZ_MT, &full[st]);
+          if ((dbg & 3) == 3) bulk_copy(As, wsl, 16, &full[st]);
           if (++st == OZ_NST) st = 0, ph ^= 1;
         }
       }
@@ -306,16 +319,25 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
           const bool mn = K > I;
           const uint32_t id = mn ? ID_MN : ID_K;
 #pragma unroll
-          for (int k = 0; k < 2; ++k)
+          for (int k = 0; k < 2; ++k) {
+            // the OZ_TS most-used A slices (slice i feeds 7 - i products) are staged in TMEM (tcgen05.cp,
+            // 8 columns each, double-buffered per K-step in columns 448..511): a TMEM-sourced MMA skips the
+            // 4 KB shared-memory A read that holds the SS form at 48 instead of 32 cycles (measured,
+            // tools/bench_i8mma.cu: 1344 -> 1120 cycles per K-step of 28 products)
+            const uint32_t ta = tmem + 448u + (uint32_t)(k * 8 * OZ_TS);
+#pragma unroll
+            for (int i = 0; i < OZ_TS; ++i) tc_cp(ta + 8 * i, umma_desc(a0 + i * 8192 + k * 256, 128, 512));
 #pragma unroll
             for (int i = 0; i < OZ_NS; ++i)
 #pragma unroll
               for (int j = 0; i + j < OZ_NS; ++j) {
-                const uint64_t da = umma_desc(a0 + i * 8192 + k * 256, 128, 512);
                 const uint64_t db = mn ? umma_desc(b0 + j * 4096 + k * 2048, 512, 128)
                                        : umma_desc(b0 + j * 4096 + k * 256, 128, 512);
-                mma_i8(tmem + (uint32_t)((i + j) * 64), da, db, id, (K | k | i) != 0);
+                const uint32_t dd = tmem + (uint32_t)((i + j) * 64);
+                if (i < OZ_TS) mma_i8_ts(dd, ta + 8 * i, db, id, (K | k | i) != 0);
+                else mma_i8(dd, umma_desc(a0 + i * 8192 + k * 256, 128, 512), db, id, (K | k | i) != 0);
               }
+          }
           mma_commit(&empty[st]);   // frees the stage once these MMAs have read it
           if (K == ntb - 1) mma_commit(&tfull);
         }
@@ -397,12 +419,14 @@ void oz_setup(const FacSub* subs, int nsub, int max_ntb, const int2* items, int 
 }
 
 void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int s, int nch, const double* W,
-                int64_t cs, const int* dexp, int8_t* wsl, int* sexp, cudaStream_t st) {
+                int64_t cs, const int* dexp, int8_t* wsl, int* sexp, cudaStream_t st, bool have_exp) {
   if (nitems <= 0) return;
   const int nct = (s + 127) / 128;
-  cudaMemsetAsync(sexp, 0x80, (size_t)nsub * nct * 128 * sizeof(int), st);
-  nsp_count_launch();
-  launch_k(k_oz_wmax, dim3(nitems, nct * 4), dim3(256), 0, st, subs, items, W, cs, nch, nct, dexp, sexp);
+  if (!have_exp) {   // the column exponents were not folded into a1 (spmm_cs_oz): a pass of their own
+    cudaMemsetAsync(sexp, 0x80, (size_t)nsub * nct * 128 * sizeof(int), st);
+    nsp_count_launch();
+    launch_k(k_oz_wmax, dim3(nitems, nct * 4), dim3(256), 0, st, subs, items, W, cs, nch, nct, dexp, sexp);
+  }
   nsp_count_launch();
   launch_k(k_oz_slice_w, dim3(nitems, nct * 4), dim3(128), 0, st, subs, items, W, cs, nch, nct, dexp,
            (const int*)sexp, wsl);
@@ -416,9 +440,10 @@ void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nc
   smem_optin((const void*)k_oz_symm, OZ_SMEM);
   const int units = nitems * nct;
   const int grid = units < num_sms() ? units : num_sms();
+  static const int dbg = getenv("NSP_OZ_DBG") ? atoi(getenv("NSP_OZ_DBG")) : 0;   // diagnostics: 1 / 2 skip A / B loads
   nsp_count_launch();
   launch_k(k_oz_symm, dim3(grid), dim3(320), (size_t)OZ_SMEM, st, subs, items, nitems, nct, msl, wsl, dexp, mexp,
-           sexp, U, cs, nch);
+           sexp, U, cs, nch, dbg);
 }
 
 }  // namespace nspk

@@ -1326,6 +1326,12 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
         NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_oz_msl, mb));
         NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_oz_dexp, (size_t)c->wvu_rows * sizeof(int)));
         NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_oz_mexp, (size_t)c->nsub * sizeof(int)));
+        {
+          std::vector<int> tb((size_t)(c->wvu_rows / 64), 0);
+          for (int j = 0; j < c->nsub; ++j)
+            for (int I = 0; I < c->subs[j].ntb; ++I) tb[(size_t)(c->subs[j].wvu_row / 64 + I)] = j;
+          if ((st = upload(c, &c->d_oz_tblk, tb)) != NSP_OK) return st;
+        }
         nspk::oz_setup(c->d_subs, c->nsub, c->max_ntb, c->d_items, c->n_items, c->d_minv, c->d_oz_dexp,
                        c->d_oz_mexp, c->d_oz_msl, c->stream);
         NSP_CUDA_TRY(c, cudaGetLastError());

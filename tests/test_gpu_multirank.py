@@ -34,7 +34,7 @@ class _same_iteration_structure:
             os.environ["NSP_APPLY_FIRST"] = self.prev
 
 
-def _run_ranks(pr, d, G, Om, Xprobe, tol, maxit):
+def _run_ranks(pr, d, G, Om, Xprobe, tol, maxit, apply_kernel=0):
     grp = nsp.LocalGroup(G)
     res = [None] * G
     errs = []
@@ -45,7 +45,8 @@ def _run_ranks(pr, d, G, Om, Xprobe, tol, maxit):
             stream = torch.cuda.Stream()
             with torch.cuda.stream(stream):
                 ctx = Context(pr.A.rowptr, pr.A.colidx, pr.A.val, pr.part, pr.K, device=0,
-                              stream=stream.cuda_stream, nranks=G, rank=r, local_group=grp)
+                              stream=stream.cuda_stream, nranks=G, rank=r, local_group=grp,
+                              apply_kernel=apply_kernel)
                 pos = np.searchsorted(d.gamma, ctx.gamma_index())
                 Bl = torch.empty(pos.size, Om.shape[1], dtype=torch.float64, device="cuda")
                 ctx.kgamma_apply(dev(Om[pos]), Bl)
@@ -71,20 +72,21 @@ def _run_ranks(pr, d, G, Om, Xprobe, tol, maxit):
     return res
 
 
-@pytest.mark.parametrize("name,G", [("cfg2s", 2), ("cfg5s", 2), ("cfg5s", 4), ("cfg4s", 4), ("cfg3s", 8),
-                                    ("cfg2s", 16)])
-def test_multirank_block_cg_matches_single_rank(name, G):
+@pytest.mark.parametrize("name,G,ak", [("cfg2s", 2, 0), ("cfg5s", 2, 0), ("cfg5s", 4, 0), ("cfg4s", 4, 0),
+                                       ("cfg3s", 8, 0), ("cfg2s", 16, 0), ("cfg2s", 2, 3), ("cfg5s", 4, 3)])
+def test_multirank_block_cg_matches_single_rank(name, G, ak):
+    """ak = 3: a2+a3 on the INT8 tensor cores for every width (reading R10), shared-first item split."""
     pr, d, S = problem(name)
     Om = pr.omega()
-    Xprobe = block(d.n_gamma, 24, seed=5)
+    Xprobe = block(d.n_gamma, 24 if ak == 0 else 100, seed=5)
     B = S.k_gamma(Om)
-    ctx1 = context(pr)
+    ctx1 = context(pr, apply_kernel=ak)
     X1 = torch.zeros(d.n_gamma, pr.s, dtype=torch.float64, device="cuda")
     with _same_iteration_structure():
         rep1 = ctx1.block_cg(dev(B), X1, pr.tol_bcg, 500)
     X1 = X1.cpu().numpy()
     ctx1.close()
-    res = _run_ranks(pr, d, G, Om, Xprobe, pr.tol_bcg, 500)
+    res = _run_ranks(pr, d, G, Om, Xprobe, pr.tol_bcg, 500, apply_kernel=ak)
     Sref = S.apply(Xprobe)
     Xg = np.zeros_like(X1)
     for r in range(G):
