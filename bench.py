@@ -467,7 +467,7 @@ def run_ours(args, ws, rank, local):
     ks = m["k_symm"]
     achieved = ks["flops_per_launch"] / (ks["avg_launch_ms"] * 1e-3) / 1e12
     if ks["int8"]:
-        traffic, traffic_src = _traffic(args.config, "k_oz_symm")
+        traffic, traffic_src = _traffic(args.config + "_int8", "k_oz_symm")
         i8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0)
         i8_ach = ks["int8_ops_per_launch"] / (ks["avg_launch_ms"] * 1e-3) / 1e12
         roof = {"kernel": "k_oz_symm (a2+a3: U_j = S_j^-1 W_j on the INT8 tensor cores, tcgen05 kind::i8 with TMEM "
