@@ -184,7 +184,7 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
                        c->stream, oz_have_exp);
       mark_start();
       nspk::oz_product(c->d_subs, c->d_items, c->n_items, s, ldw / 32, U, cs, c->d_oz_dexp, c->d_oz_mexp,
-                       c->d_oz_msl, wsl, sexp, c->stream);
+                       c->d_oz_msl, wsl, sexp, c->stream, c->d_oz_pairs, c->n_oz_pairs);
     } else {
       nsp_count_path(NSP_PATH_SYMM);
       nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream, cs);
@@ -459,6 +459,7 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_oz_dexp);
   fr(c->d_oz_mexp);
   fr(c->d_oz_tblk);
+  fr(c->d_oz_pairs);
   fr(c->d_items);
   fr(c->d_i1_src);
   fr(c->d_b_src);

@@ -126,6 +126,8 @@ struct nsp_ctx {
   int* d_oz_dexp = nullptr;
   int* d_oz_mexp = nullptr;
   int* d_oz_tblk = nullptr;   // W/V/U tile -> local block
+  int2* d_oz_pairs = nullptr; // (block, even tile row I0): the two-CTA cluster work units
+  int n_oz_pairs = 0;
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
   DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)
@@ -282,9 +284,10 @@ void oz_setup(const FacSub* subs, int nsub, int max_ntb, const int2* items, int 
 void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int s, int nch, const double* W,
                 int64_t cs, const int* dexp, int8_t* wsl, int* sexp, cudaStream_t st, bool have_exp = false);
 // U = S_j^{-1} W for the items [0, nitems) from the slices (chunk-major U)
+// pairs (j, I0), I0 even, covering the same items: clusters of two CTAs share the W^T slices (multicast)
 void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nch, double* U, int64_t cs,
                 const int* dexp, const int* mexp, const int8_t* msl, const int8_t* wsl, const int* sexp,
-                cudaStream_t st);
+                cudaStream_t st, const int2* pairs = nullptr, int npairs = 0);
 // a2+a3 for one column (ld ldw, column 0): u_j = S_j^{-1} w_j, matrix-vector (s = 1)
 void symv(const FacSub* subs, const int2* items, int nitems, int max_ntb, const double* minv, const double* W, int ldw,
           double* U, cudaStream_t st);

@@ -68,6 +68,29 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t ta, uint64_t b, u
 __device__ __forceinline__ void tc_cp(uint32_t ta, uint64_t sd) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n" ::"r"(ta), "l"(sd));
 }
+// cluster of CL CTAs: the W^T slices of a K tile are multicast (each CTA fetches 1/CL of them for all), the
+// stage is freed when every CTA's MMAs have read it (commit multicast to every CTA's empty barrier)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_copy_mc(void* dst, const void* src, unsigned bytes, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          s_u32(dst)),
+      "l"(src), "r"(bytes), "r"(s_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                   s_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(s_u32(bar))
                : "memory");
@@ -251,6 +274,10 @@ __global__ void __launch_bounds__(128) k_oz_slice_w(const FacSub* __restrict__ s
 // Persistent, one CTA per SM (TMEM: 7 accumulators x 64 columns of 512).  Warp 0: bulk-copy producer;
 // warp 1: TMEM owner + MMA issuer; warps 2..9: epilogue (TMEM lane quarter = warp % 4, 32 of the 64 rows n).
 // Work unit t in [0, nitems * nct): item t % nitems, column tile t / nitems.
+// CL = 2: clusters of two CTAs take pair units (block j, tile rows I0, I0 + 1) from items = (j, I0) (I0 even);
+// the second CTA of a pair whose I0 + 1 = ntb_j recomputes tile I0 and discards it (the multicast protocol
+// needs both CTAs to walk the same K loop)
+template <int CL>
 __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ subs, const int2* __restrict__ items,
                                                     int nitems, int nct, const int8_t* __restrict__ msl,
                                                     const int8_t* __restrict__ wsl, const int* __restrict__ dexp,
@@ -262,10 +289,12 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nunits = nitems * nct;
+  const int crank = CL == 2 ? (int)cluster_rank() : 0;
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   if (threadIdx.x == 0) {
     for (int s = 0; s < OZ_NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);
     }
     mbar_init(&tfull, 1);
     mbar_init(&tempty, 8);
@@ -276,7 +305,8 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL == 2) cluster_sync_all();   // the peer's barriers exist before any multicast targets them
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tbase;
   pdl_wait();
@@ -284,17 +314,23 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
     if (elect_one()) {   // producer
       int st = 0;
       uint32_t ph = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      for (int u = cid; u < nunits; u += ncl) {
         const int2 it = items[u % nitems];
         const int ct = u / nitems;
         const FacSub sb = subs[it.x];
-        const int I = it.y;
+        const int I = min(it.y + crank, sb.ntb - 1);
         const int64_t T0 = sb.wvu_row / 64;
         for (int K = 0; K < sb.ntb; ++K) {
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* As = base + st * (OZ_AT + OZ_MT);
           mbar_expect(&full[st], ((dbg & 1) ? 0 : OZ_AT) + ((dbg & 2) ? 0 : OZ_MT) + ((dbg & 3) == 3 ? 16 : 0));
-          if (!(dbg & 1)) bulk_copy(As, wsl + ((T0 + K) * nct + ct) * (int64_t)OZ_AT, OZ_AT, &full[st]);
+          const int8_t* Ag = wsl + ((T0 + K) * nct + ct) * (int64_t)OZ_AT;
+          if (CL == 2) {
+            if (!(dbg & 1))
+              bulk_copy_mc(As + crank * (OZ_AT / 2), Ag + crank * (OZ_AT / 2), OZ_AT / 2, &full[st], (uint16_t)3);
+          } else if (!(dbg & 1)) {
+            bulk_copy(As, Ag, OZ_AT, &full[st]);
+          }
           const int64_t t = sb.dense_off + (K <= I ? (int64_t)I * (I + 1) / 2 + K : (int64_t)K * (K + 1) / 2 + I);
           if (!(dbg & 2)) bulk_copy(As + OZ_AT, msl + t * OZ_MT, OZ_MT, &full[st]);
           if ((dbg & 3) == 3) bulk_copy(As, wsl, 16, &full[st]);
@@ -306,9 +342,10 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
     int st = 0;
     uint32_t ph = 0, tph = 0;
     constexpr uint32_t ID_K = oz_idesc(0), ID_MN = oz_idesc(1);
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    for (int u = cid; u < nunits; u += ncl) {
       const int2 it = items[u % nitems];
-      const int I = it.y, ntb = subs[it.x].ntb;
+      const int ntb = subs[it.x].ntb;
+      const int I = min(it.y + crank, ntb - 1);
       mbar_wait(&tempty, tph ^ 1);   // the epilogue has drained the previous unit's accumulators
       tc_fence_after();
       for (int K = 0; K < ntb; ++K) {
@@ -338,7 +375,8 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
                 else mma_i8(dd, umma_desc(a0 + i * 8192 + k * 256, 128, 512), db, id, (K | k | i) != 0);
               }
           }
-          mma_commit(&empty[st]);   // frees the stage once these MMAs have read it
+          if (CL == 2) mma_commit_mc(&empty[st], (uint16_t)3);   // frees the stage in both CTAs' accounting
+          else mma_commit(&empty[st]);   // frees the stage once these MMAs have read it
           if (K == ntb - 1) mma_commit(&tfull);
         }
         __syncwarp();
@@ -351,12 +389,12 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
     const int half = (warp - 2) >> 2;
     const int cc = qd * 32 + lane;
     uint32_t tph = 0;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    for (int u = cid; u < nunits; u += ncl) {
       const int2 it = items[u % nitems];
       const int ct = u / nitems;
       const FacSub sb = subs[it.x];
-      const int I = it.y;
-      const int chunk = ct * 4 + qd;
+      const int I = it.y + crank;
+      const int chunk = (I < sb.ntb) ? ct * 4 + qd : nch;   // a discarded duplicate tile: no stores
       const int ex = sexp[((int64_t)it.x * nct + ct) * 128 + cc] + mexp[it.x];
       const int64_t row0 = sb.wvu_row + (int64_t)I * 64;
       double* out = U + (int64_t)chunk * cs + row0 * 36 + lane;
@@ -392,7 +430,8 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL == 2) cluster_sync_all();   // no CTA leaves while its peer may still multicast / commit into it
+  else __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 }  // namespace
@@ -434,15 +473,38 @@ void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int
 
 void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nch, double* U, int64_t cs,
                 const int* dexp, const int* mexp, const int8_t* msl, const int8_t* wsl, const int* sexp,
-                cudaStream_t st) {
+                cudaStream_t st, const int2* pairs, int npairs) {
   if (nitems <= 0) return;
   const int nct = (s + 127) / 128;
-  smem_optin((const void*)k_oz_symm, OZ_SMEM);
+  static const int dbg = getenv("NSP_OZ_DBG") ? atoi(getenv("NSP_OZ_DBG")) : 0;   // diagnostics: 1 / 2 skip A / B loads
+  static const bool cl_off = getenv("NSP_OZ_CLUSTER") && getenv("NSP_OZ_CLUSTER")[0] == '0';
+  if (pairs && npairs > 0 && !cl_off) {   // clusters of two CTAs sharing the W^T slices by multicast
+    smem_optin((const void*)k_oz_symm<2>, OZ_SMEM);
+    const int units = npairs * nct;
+    int grid = 2 * (units < num_sms() / 2 ? units : num_sms() / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(320);
+    cfg.dynamicSmemBytes = OZ_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    nsp_count_launch();
+    cudaLaunchKernelEx(&cfg, k_oz_symm<2>, subs, pairs, npairs, nct, msl, wsl, dexp, mexp, sexp, U, cs, nch, dbg);
+    return;
+  }
+  smem_optin((const void*)k_oz_symm<1>, OZ_SMEM);
   const int units = nitems * nct;
   const int grid = units < num_sms() ? units : num_sms();
-  static const int dbg = getenv("NSP_OZ_DBG") ? atoi(getenv("NSP_OZ_DBG")) : 0;   // diagnostics: 1 / 2 skip A / B loads
   nsp_count_launch();
-  launch_k(k_oz_symm, dim3(grid), dim3(320), (size_t)OZ_SMEM, st, subs, items, nitems, nct, msl, wsl, dexp, mexp,
+  launch_k(k_oz_symm<1>, dim3(grid), dim3(320), (size_t)OZ_SMEM, st, subs, items, nitems, nct, msl, wsl, dexp, mexp,
            sexp, U, cs, nch, dbg);
 }
 

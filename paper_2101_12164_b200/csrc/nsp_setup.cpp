@@ -1331,6 +1331,11 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
           for (int j = 0; j < c->nsub; ++j)
             for (int I = 0; I < c->subs[j].ntb; ++I) tb[(size_t)(c->subs[j].wvu_row / 64 + I)] = j;
           if ((st = upload(c, &c->d_oz_tblk, tb)) != NSP_OK) return st;
+          std::vector<int2> pr;
+          for (int j = 0; j < c->nsub; ++j)
+            for (int I = 0; I < c->subs[j].ntb; I += 2) pr.push_back(make_int2(j, I));
+          c->n_oz_pairs = (int)pr.size();
+          if (!pr.empty() && (st = upload(c, &c->d_oz_pairs, pr)) != NSP_OK) return st;
         }
         nspk::oz_setup(c->d_subs, c->nsub, c->max_ntb, c->d_items, c->n_items, c->d_minv, c->d_oz_dexp,
                        c->d_oz_mexp, c->d_oz_msl, c->stream);
