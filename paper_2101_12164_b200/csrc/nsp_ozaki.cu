@@ -477,8 +477,10 @@ void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nc
   if (nitems <= 0) return;
   const int nct = (s + 127) / 128;
   static const int dbg = getenv("NSP_OZ_DBG") ? atoi(getenv("NSP_OZ_DBG")) : 0;   // diagnostics: 1 / 2 skip A / B loads
-  static const bool cl_off = getenv("NSP_OZ_CLUSTER") && getenv("NSP_OZ_CLUSTER")[0] == '0';
-  if (pairs && npairs > 0 && !cl_off) {   // clusters of two CTAs sharing the W^T slices by multicast
+  // clusters of two CTAs sharing the W^T slices by multicast: parity-clean but measured no faster (cfg5 apply
+  // 33.9 vs 33.4 ms: the L2 -> SM traffic does not bind; the shared-memory port does), opt-in NSP_OZ_CLUSTER=1
+  static const bool cl_on = getenv("NSP_OZ_CLUSTER") && getenv("NSP_OZ_CLUSTER")[0] == '1';
+  if (pairs && npairs > 0 && cl_on) {
     smem_optin((const void*)k_oz_symm<2>, OZ_SMEM);
     const int units = npairs * nct;
     int grid = 2 * (units < num_sms() / 2 ? units : num_sms() / 2);

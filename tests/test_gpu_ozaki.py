@@ -90,3 +90,31 @@ def test_ozaki_scale_extremes():
         else:
             assert np.linalg.norm(Yh[:, c] - ref[:, c]) / nr <= 1e-12, c
     ctx.close()
+
+
+def test_ozaki_cluster_multicast_variant():
+    """The two-CTA cluster variant (W^T slices multicast, NSP_OZ_CLUSTER=1, opt-in) gives the bitwise same
+    result as the one-CTA kernel (same products, same epilogue; only the data movement differs), including
+    blocks with an odd tile count (the pair's second CTA recomputes and discards)."""
+    import subprocess, sys, os
+    code = (
+        "import numpy as np, torch, sys\n"
+        "sys.path.insert(0, %r)\n"
+        "from tests.gpu_util import block, context, dev, problem\n"
+        "pr, d, S = problem('cfg2s')\n"
+        "ctx = context(pr, apply_kernel=3)\n"
+        "X = dev(block(d.n_gamma, 128))\n"
+        "Y = torch.empty_like(X)\n"
+        "ctx.schur_apply(X, Y)\n"
+        "torch.cuda.synchronize()\n"
+        "np.save(sys.argv[1], Y.cpu().numpy())\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import tempfile
+    outs = []
+    with tempfile.TemporaryDirectory() as td:
+        for cl in ("0", "1"):
+            f = os.path.join(td, f"y{cl}.npy")
+            env = dict(os.environ, NSP_OZ_CLUSTER=cl)
+            r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
