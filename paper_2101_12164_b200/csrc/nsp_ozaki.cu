@@ -434,6 +434,240 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
   else __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
+
+// ---------------------------------------------------------------- register-staged variant (opt-in, slower)
+// The four most-used W^T slices reach TMEM from REGISTERS (tcgen05.st by the epilogue warps, which are idle
+// while the tensor core runs), not through shared memory: the shared-memory port - the binding resource of
+// k_oz_symm (per K-step 96 KB of MMA / copy reads + 42 KB of TMA writes at 128 B/clk) - then carries only
+// slices 4..6 and the M tile (per K-step 80 KB reads + 26 KB writes), and the tensor pipe runs no tcgen05.cp:
+// 6 x 48 + 22 x 32 = 992 cycles per K-step instead of 1,120.  TMEM: 7 x 64 accumulator columns + 2 buffers
+// x 4 slices x 8 columns.  Per K-step g the stagers fill buffer g & 1 (afull, 8 warp arrivals) once the MMAs
+// of step g - 2 have released it (afree, one commit); the W^T rows are prefetched into registers one K-step
+// ahead.  The first K-step of unit u + 1 is staged before unit u's epilogue, so the tensor core restarts as
+// soon as the accumulators are drained.
+constexpr int RS_NST = 3;
+constexpr int RS_AT = 3 * 8192;                  // slices 4..6 of the W^T tile
+constexpr int RS_STAGE = RS_AT + OZ_MT;
+constexpr int RS_SMEM = RS_NST * RS_STAGE + 1024;
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, uint4 a, uint4 b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(a.x),
+               "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+struct OzStep {   // position in a CTA's (unit, K tile, K-step) sequence
+  int u, K, k, ntb;
+  int2 it;
+  bool valid;
+};
+
+__global__ void __launch_bounds__(320, 1) k_oz_symm_rs(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                                       int nitems, int nct, const int8_t* __restrict__ msl,
+                                                       const int8_t* __restrict__ wsl, const int* __restrict__ dexp,
+                                                       const int* __restrict__ mexp, const int* __restrict__ sexp,
+                                                       double* __restrict__ U, int64_t cs, int nch) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t full[RS_NST], empty[RS_NST], afull[2], afree[2], tfull, tempty;
+  __shared__ uint32_t tbase;
+  uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nunits = nitems * nct;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RS_NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&afull[b], 8);
+      mbar_init(&afree[b], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, 8);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(s_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  pdl_wait();
+  if (warp == 0) {
+    if (elect_one()) {   // producer: slices 4..6 of the W^T tile + the stored M tile per K tile
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int2 it = items[u % nitems];
+        const int ct = u / nitems;
+        const FacSub sb = subs[it.x];
+        const int I = it.y;
+        const int64_t T0 = sb.wvu_row / 64;
+        for (int K = 0; K < sb.ntb; ++K) {
+          mbar_wait(&empty[st], ph ^ 1);
+          uint8_t* As = base + st * RS_STAGE;
+          mbar_expect(&full[st], RS_AT + OZ_MT);
+          bulk_copy(As, wsl + ((T0 + K) * nct + ct) * (int64_t)OZ_AT + 4 * 8192, RS_AT, &full[st]);
+          const int64_t t = sb.dense_off + (K <= I ? (int64_t)I * (I + 1) / 2 + K : (int64_t)K * (K + 1) / 2 + I);
+          bulk_copy(As + RS_AT, msl + t * OZ_MT, OZ_MT, &full[st]);
+          if (++st == RS_NST) st = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {   // MMA issuer
+    int st = 0;
+    uint32_t ph = 0, tph = 0, g = 0;
+    constexpr uint32_t ID_K = oz_idesc(0), ID_MN = oz_idesc(1);
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int2 it = items[u % nitems];
+      const int I = it.y, ntb = subs[it.x].ntb;
+      mbar_wait(&tempty, tph ^ 1);   // the epilogue has drained the previous unit's accumulators
+      tc_fence_after();
+      for (int K = 0; K < ntb; ++K) {
+        mbar_wait(&full[st], ph);
+        const uint32_t a0 = s_u32(base + st * RS_STAGE), b0 = a0 + RS_AT;
+        const bool mn = K > I;
+        const uint32_t id = mn ? ID_MN : ID_K;
+#pragma unroll
+        for (int k = 0; k < 2; ++k, ++g) {
+          const uint32_t b = g & 1;
+          mbar_wait(&afull[b], (g >> 1) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t ta = tmem + 448u + 32u * b;
+#pragma unroll
+            for (int i = 0; i < OZ_NS; ++i)
+#pragma unroll
+              for (int j = 0; i + j < OZ_NS; ++j) {
+                const uint64_t db = mn ? umma_desc(b0 + j * 4096 + k * 2048, 512, 128)
+                                       : umma_desc(b0 + j * 4096 + k * 256, 128, 512);
+                const uint32_t dd = tmem + (uint32_t)((i + j) * 64);
+                if (i < 4) mma_i8_ts(dd, ta + 8 * i, db, id, (K | k | i) != 0);
+                else mma_i8(dd, umma_desc(a0 + (i - 4) * 8192 + k * 256, 128, 512), db, id, (K | k | i) != 0);
+              }
+            mma_commit(&afree[b]);                 // the staging buffer is free once these MMAs have read it
+            if (k == 1) mma_commit(&empty[st]);    // and the shared-memory stage after the second K-step
+            if (k == 1 && K == ntb - 1) mma_commit(&tfull);
+          }
+          __syncwarp();
+        }
+        if (++st == RS_NST) st = 0, ph ^= 1;
+      }
+      tph ^= 1;
+    }
+  } else {   // warps 2..9: stage W^T slices {2 grp, 2 grp + 1} into TMEM; epilogue half grp
+    const int qd = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    const int cc = qd * 32 + lane;
+    auto first_of = [&](int u) {
+      OzStep p;
+      p.u = u;
+      p.K = 0;
+      p.k = 0;
+      p.valid = u < nunits;
+      if (p.valid) {
+        p.it = items[u % nitems];
+        p.ntb = subs[p.it.x].ntb;
+      }
+      return p;
+    };
+    auto advance = [&](OzStep p) {
+      if (++p.k == 2) {
+        p.k = 0;
+        if (++p.K == p.ntb) return first_of(p.u + gridDim.x);
+      }
+      return p;
+    };
+    auto load = [&](const OzStep& p, uint4 (&r)[4]) {
+      const FacSub sb = subs[p.it.x];
+      const int ct = p.u / nitems;
+      const int8_t* Ag = wsl + ((sb.wvu_row / 64 + p.K) * nct + ct) * (int64_t)OZ_AT +
+                         ((cc >> 3) * 4 + 2 * p.k) * 128 + (cc & 7) * 16;
+#pragma unroll
+      for (int sl = 0; sl < 2; ++sl) {
+        const int8_t* q = Ag + (2 * grp + sl) * 8192;
+        r[2 * sl] = __ldg(reinterpret_cast<const uint4*>(q));
+        r[2 * sl + 1] = __ldg(reinterpret_cast<const uint4*>(q + 128));
+      }
+    };
+    auto epilogue = [&](int u, uint32_t tph) {
+      const int2 it = items[u % nitems];
+      const int ct = u / nitems;
+      const FacSub sb = subs[it.x];
+      const int I = it.y;
+      const int chunk = ct * 4 + qd;
+      const int ex = sexp[((int64_t)it.x * nct + ct) * 128 + cc] + mexp[it.x];
+      const int64_t row0 = sb.wvu_row + (int64_t)I * 64;
+      double* out = U + (int64_t)chunk * cs + row0 * 36 + lane;
+      mbar_wait(&tfull, tph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int nb = 2 * grp; nb < 2 * grp + 2; ++nb) {
+        uint32_t v[OZ_NS][16];
+#pragma unroll
+        for (int a = 0; a < OZ_NS; ++a)
+          tmem_ld16(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(a * 64 + nb * 16), v[a]);
+        tmem_ld_wait();
+        if (chunk < nch) {
+#pragma unroll
+          for (int nn = 0; nn < 16; ++nn) {
+            const long long hi = ((long long)(int)v[0][nn] << 16) + ((long long)(int)v[1][nn] << 8) + (int)v[2][nn];
+            const long long lo = ((long long)(int)v[3][nn] << 24) + ((long long)(int)v[4][nn] << 16) +
+                                 ((long long)(int)v[5][nn] << 8) + (int)v[6][nn];
+            const double acc = fma((double)hi, 0x1p-30, (double)lo * 0x1p-62);
+            const int n = nb * 16 + nn;
+            const int E = ex + dexp[row0 + n];
+            out[(int64_t)n * 36] = (E >= -1022 && E <= 1023) ? acc * __longlong_as_double((long long)(E + 1023) << 52)
+                                                             : ldexp(acc, E);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty);
+    };
+    OzStep cur = first_of(blockIdx.x);
+    OzStep nx1 = cur.valid ? advance(cur) : cur;
+    uint4 rn[4], rn2[4];
+    if (cur.valid) load(cur, rn);
+    if (nx1.valid) load(nx1, rn2);
+    uint32_t g = 0, tph = 0;
+    int pend = -1;   // unit whose epilogue is due
+    while (cur.valid) {
+      uint4 rc[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) rc[q] = rn[q], rn[q] = rn2[q];
+      const OzStep nxt = nx1;
+      const OzStep nx2 = nx1.valid ? advance(nx1) : nx1;
+      if (nx2.valid) load(nx2, rn2);   // two K-steps ahead
+      const uint32_t b = g & 1;
+      mbar_wait(&afree[b], ((g >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + 448u + 32u * b + 16u * grp;
+      tmem_st8(ta, rc[0], rc[1]);
+      tmem_st8(ta + 8, rc[2], rc[3]);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&afull[b]);
+      ++g;
+      if (cur.K == 0 && cur.k == 0 && pend >= 0) {   // the next unit's first step is staged: drain the last
+        epilogue(pend, tph);
+        tph ^= 1;
+      }
+      if (cur.K == 0 && cur.k == 0) pend = cur.u;
+      cur = nxt;
+      nx1 = nx2;
+    }
+    if (pend >= 0) epilogue(pend, tph);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
 }  // namespace
 
 namespace nspk {
@@ -502,8 +736,19 @@ void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nc
     cudaLaunchKernelEx(&cfg, k_oz_symm<2>, subs, pairs, npairs, nct, msl, wsl, dexp, mexp, sexp, U, cs, nch, dbg);
     return;
   }
-  smem_optin((const void*)k_oz_symm<1>, OZ_SMEM);
+  // NSP_OZ_KERNEL=2: the register-staged variant k_oz_symm_rs - parity-clean, measured SLOWER (cfg5 apply
+  // 39.0 vs 33.5 ms: the stagers' W^T loads sit on the critical path of every K-step), opt-in only
+  static const int kv = getenv("NSP_OZ_KERNEL") ? atoi(getenv("NSP_OZ_KERNEL")) : 1;
   const int units = nitems * nct;
+  if (kv == 2 && !dbg) {
+    smem_optin((const void*)k_oz_symm_rs, RS_SMEM);
+    const int grid = units < num_sms() ? units : num_sms();
+    nsp_count_launch();
+    launch_k(k_oz_symm_rs, dim3(grid), dim3(320), (size_t)RS_SMEM, st, subs, items, nitems, nct, msl, wsl, dexp,
+             mexp, sexp, U, cs, nch);
+    return;
+  }
+  smem_optin((const void*)k_oz_symm<1>, OZ_SMEM);
   const int grid = units < num_sms() ? units : num_sms();
   nsp_count_launch();
   launch_k(k_oz_symm<1>, dim3(grid), dim3(320), (size_t)OZ_SMEM, st, subs, items, nitems, nct, msl, wsl, dexp, mexp,

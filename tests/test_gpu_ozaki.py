@@ -118,3 +118,29 @@ def test_ozaki_cluster_multicast_variant():
             assert r.returncode == 0, r.stderr[-2000:]
             outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_ozaki_register_staged_variant():
+    """The register-staged kernel (NSP_OZ_KERNEL=2, opt-in) computes the identical digit products: bitwise the
+    same S_G X as the default kernel."""
+    import subprocess, sys, os, tempfile
+    code = (
+        "import numpy as np, torch, sys\n"
+        "sys.path.insert(0, %r)\n"
+        "from tests.gpu_util import block, context, dev, problem\n"
+        "pr, d, S = problem('cfg5s')\n"
+        "ctx = context(pr, apply_kernel=3)\n"
+        "X = dev(block(d.n_gamma, 128))\n"
+        "Y = torch.empty_like(X)\n"
+        "ctx.schur_apply(X, Y)\n"
+        "torch.cuda.synchronize()\n"
+        "np.save(sys.argv[1], Y.cpu().numpy())\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    outs = []
+    with tempfile.TemporaryDirectory() as td:
+        for kv in ("1", "2"):
+            f = os.path.join(td, f"y{kv}.npy")
+            env = dict(os.environ, NSP_OZ_KERNEL=kv)
+            r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
