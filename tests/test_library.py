@@ -33,6 +33,10 @@ def test_sass_has_dmma():
     B.build()
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", B.LIB], capture_output=True, text=True).stdout
     assert "DMMA" in out, "fp64 tensor-pipe (DMMA) instructions missing from libnsp.so"
+    # a2+a3 on the 5th-generation tensor cores (reading R10): tcgen05 kind::i8 MMAs (SS and TMEM-A forms),
+    # smem -> TMEM copies, TMEM loads, and the bulk copies that feed them
+    for m in ("UTCIMMA", "UTCCP", "LDTM", "UBLKCP"):
+        assert m in out, f"{m} missing from libnsp.so"
     assert "sm_100a" in subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", B.LIB],
                                        capture_output=True, text=True).stdout
 
