@@ -311,8 +311,8 @@ def measure(pr, args, ws, rank, local, stream, nccl_id, headline):
     maxit = args.maxit
     out = {"workload": pr.name, "n": pr.n, "n_gamma": ctx.n_gamma, "n_gamma_local": nG, "K": pr.K, "s": s,
            "tol_bcg": pr.tol_bcg, "setup_ms": t_setup * 1e3,
-           "setup_split_ms": dict(zip(["host_analysis", "h2d", "gpu_factor", "ag_operator", "sj_inverse_tiles"],
-                                      ctx.setup_report["t_ms"][:5])),
+           "setup_split_ms": dict(zip(["host_analysis", "h2d", "gpu_factor", "ag_operator", "sj_inverse_tiles",
+                                       "sj_inverse_int8_slices"], ctx.setup_report["t_ms"][:6])),
            "shared_rows": ctx.n_shared}
 
     def step():
@@ -336,6 +336,8 @@ def measure(pr, args, ws, rank, local, stream, nccl_id, headline):
             torch.distributed.barrier()
     out["clocks"] = clk.summary()
     out["gpu_launches"] = (nsp.kernel_launches() - launches0) / args.steps
+    fr_, tot_ = torch.cuda.mem_get_info(dev)
+    out["device_memory_gb"] = {"in_use": (tot_ - fr_) / 1e9, "total": tot_ / 1e9}
     times = [t for t, _ in res]
     iters = [r["iters"] for _, r in res]
     tmean = sum(times) / len(times)
@@ -518,6 +520,7 @@ def run_ours(args, ws, rank, local):
         "apply": m["apply"], "iteration_split_ms": m["iteration_split_ms"],
         "roofline": roof,
         "e2e": m["e2e"], "gpu_launches": m["gpu_launches"], "clocks": m["clocks"],
+        "device_memory_gb": m.get("device_memory_gb"),
     }
     if ws == 1 and not args.no_secondary and args.secondary and args.secondary != args.config:
         torch.cuda.empty_cache()

@@ -128,6 +128,7 @@ struct nsp_ctx {
   int* d_oz_tblk = nullptr;   // W/V/U tile -> local block
   int2* d_oz_pairs = nullptr; // (block, even tile row I0): the two-CTA cluster work units
   int n_oz_pairs = 0;
+  int* d_oz_ctr = nullptr;    // k_oz_symm's dynamic work counter (reset before every launch)
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
   DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)
@@ -287,7 +288,7 @@ void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int
 // pairs (j, I0), I0 even, covering the same items: clusters of two CTAs share the W^T slices (multicast)
 void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nch, double* U, int64_t cs,
                 const int* dexp, const int* mexp, const int8_t* msl, const int8_t* wsl, const int* sexp,
-                cudaStream_t st, const int2* pairs = nullptr, int npairs = 0);
+                cudaStream_t st, const int2* pairs = nullptr, int npairs = 0, int* uctr = nullptr);
 // a2+a3 for one column (ld ldw, column 0): u_j = S_j^{-1} w_j, matrix-vector (s = 1)
 void symv(const FacSub* subs, const int2* items, int nitems, int max_ntb, const double* minv, const double* W, int ldw,
           double* U, cudaStream_t st);

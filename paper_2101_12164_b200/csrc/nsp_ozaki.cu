@@ -68,6 +68,20 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t ta, uint64_t b, u
 __device__ __forceinline__ void tc_cp(uint32_t ta, uint64_t sd) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n" ::"r"(ta), "l"(sd));
 }
+// bulk copy with an L2 cache policy (createpolicy: evict_last keeps the W^T slices of the running blocks -
+// re-read by every unit of the block - resident against the stream of M tiles)
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_copy_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          s_u32(dst)),
+      "l"(src), "r"(bytes), "r"(s_u32(bar)), "l"(pol)
+      : "memory");
+}
 // cluster of CL CTAs: the W^T slices of a K tile are multicast (each CTA fetches 1/CL of them for all), the
 // stage is freed when every CTA's MMAs have read it (commit multicast to every CTA's empty barrier)
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -274,6 +288,32 @@ __global__ void __launch_bounds__(128) k_oz_slice_w(const FacSub* __restrict__ s
 // Persistent, one CTA per SM (TMEM: 7 accumulators x 64 columns of 512).  Warp 0: bulk-copy producer;
 // warp 1: TMEM owner + MMA issuer; warps 2..9: epilogue (TMEM lane quarter = warp % 4, 32 of the 64 rows n).
 // Work unit t in [0, nitems * nct): item t % nitems, column tile t / nitems.
+// K-tile order of a unit (block j, output tile row I): natural 0, 1, ..., or (diagnostic NSP_OZ_DBG bit 8)
+// I, I + 1, I - 1, I + 2, I - 2, ... in which the two readers of a stored tile (a, b) reach it at the same
+// step.  With the dynamic unit counter the units of one block run side by side and either order re-reads
+// the stored tiles from L2 (cfg5 DRAM per launch 69 GB -> 49.2 GB natural / 46.9 GB symmetric against
+// 45.2 GB unique; time 26.2 vs 26.5 ms: the natural order is kept).
+struct OzKOrder {
+  int I, ntb, lo, hi, side, K;
+  __device__ OzKOrder(int I_, int ntb_, bool natural) : I(I_), ntb(ntb_), lo(I_ - 1), hi(I_ + 1), side(0) {
+    K = natural ? 0 : I_;
+    if (natural) lo = -2;   // marks the natural order
+  }
+  __device__ void next() {
+    if (lo == -2) {
+      ++K;
+      return;
+    }
+    if ((side == 0 && hi < ntb) || lo < 0) {
+      K = hi++;
+      side = 1;
+    } else {
+      K = lo--;
+      side = 0;
+    }
+  }
+};
+
 // CL = 2: clusters of two CTAs take pair units (block j, tile rows I0, I0 + 1) from items = (j, I0) (I0 even);
 // the second CTA of a pair whose I0 + 1 = ntb_j recomputes tile I0 and discards it (the multicast protocol
 // needs both CTAs to walk the same K loop)
@@ -282,10 +322,12 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
                                                     int nitems, int nct, const int8_t* __restrict__ msl,
                                                     const int8_t* __restrict__ wsl, const int* __restrict__ dexp,
                                                     const int* __restrict__ mexp, const int* __restrict__ sexp,
-                                                    double* __restrict__ U, int64_t cs, int nch, int dbg) {
+                                                    double* __restrict__ U, int64_t cs, int nch, int dbg,
+                                                    int* __restrict__ uctr) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ __align__(8) uint64_t full[OZ_NST], empty[OZ_NST], tfull, tempty;
+  __shared__ __align__(8) uint64_t full[OZ_NST], empty[OZ_NST], tfull, tempty, ufull[4], uempty[4];
   __shared__ uint32_t tbase;
+  __shared__ int uring[4];
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nunits = nitems * nct;
@@ -298,8 +340,35 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
     }
     mbar_init(&tfull, 1);
     mbar_init(&tempty, 8);
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(&ufull[q], 1);
+      mbar_init(&uempty[q], 9);
+    }
     fence_mbar_init();
   }
+  // work units: dynamic (uctr: one atomic grab per unit, in order, so the units of one block run side by side
+  // and share their W^T and M tiles through L2; also no tail imbalance) or the static cid, cid + ncl, ...;
+  // the producer publishes every unit index to the MMA and epilogue warps through a 4-deep ring
+  const bool dyn = CL == 1 && uctr != nullptr;
+  int ustat = cid, uslot = 0;
+  uint32_t uph = 0;
+  auto publish = [&]() -> int {   // producer thread
+    const int u = dyn ? atomicAdd(uctr, 1) : ustat;
+    ustat += ncl;
+    mbar_wait(&uempty[uslot], uph ^ 1);
+    *(volatile int*)&uring[uslot] = u;
+    mbar_arrive(&ufull[uslot]);
+    if (++uslot == 4) uslot = 0, uph ^= 1;
+    return u;
+  };
+  auto receive = [&]() -> int {   // every lane of a consumer warp
+    mbar_wait(&ufull[uslot], uph);
+    const int u = *(volatile int*)&uring[uslot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&uempty[uslot]);
+    if (++uslot == 4) uslot = 0, uph ^= 1;
+    return u;
+  };
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(s_u32(&tbase)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -314,13 +383,17 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
     if (elect_one()) {   // producer
       int st = 0;
       uint32_t ph = 0;
-      for (int u = cid; u < nunits; u += ncl) {
+      const bool hint = (dbg & 4) == 0;
+      const uint64_t pol = l2_evict_last();
+      for (int u = publish(); u < nunits; u = publish()) {
         const int2 it = items[u % nitems];
         const int ct = u / nitems;
         const FacSub sb = subs[it.x];
         const int I = min(it.y + crank, sb.ntb - 1);
         const int64_t T0 = sb.wvu_row / 64;
-        for (int K = 0; K < sb.ntb; ++K) {
+        OzKOrder ko(I, sb.ntb, CL == 2 || !(dbg & 8));
+        for (int step = 0; step < sb.ntb; ++step, ko.next()) {
+          const int K = ko.K;
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* As = base + st * (OZ_AT + OZ_MT);
           mbar_expect(&full[st], ((dbg & 1) ? 0 : OZ_AT) + ((dbg & 2) ? 0 : OZ_MT) + ((dbg & 3) == 3 ? 16 : 0));
@@ -329,7 +402,8 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
             if (!(dbg & 1))
               bulk_copy_mc(As + crank * (OZ_AT / 2), Ag + crank * (OZ_AT / 2), OZ_AT / 2, &full[st], (uint16_t)3);
           } else if (!(dbg & 1)) {
-            bulk_copy(As, Ag, OZ_AT, &full[st]);
+            if (hint) bulk_copy_hint(As, Ag, OZ_AT, &full[st], pol);
+            else bulk_copy(As, Ag, OZ_AT, &full[st]);
           }
           const int64_t t = sb.dense_off + (K <= I ? (int64_t)I * (I + 1) / 2 + K : (int64_t)K * (K + 1) / 2 + I);
           if (!(dbg & 2)) bulk_copy(As + OZ_AT, msl + t * OZ_MT, OZ_MT, &full[st]);
@@ -342,13 +416,15 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
     int st = 0;
     uint32_t ph = 0, tph = 0;
     constexpr uint32_t ID_K = oz_idesc(0), ID_MN = oz_idesc(1);
-    for (int u = cid; u < nunits; u += ncl) {
+    for (int u = receive(); u < nunits; u = receive()) {
       const int2 it = items[u % nitems];
       const int ntb = subs[it.x].ntb;
       const int I = min(it.y + crank, ntb - 1);
       mbar_wait(&tempty, tph ^ 1);   // the epilogue has drained the previous unit's accumulators
       tc_fence_after();
-      for (int K = 0; K < ntb; ++K) {
+      OzKOrder ko(I, ntb, CL == 2 || !(dbg & 8));
+      for (int step = 0; step < ntb; ++step, ko.next()) {
+        const int K = ko.K;
         mbar_wait(&full[st], ph);
         tc_fence_after();
         if (elect_one()) {
@@ -371,13 +447,13 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
                 const uint64_t db = mn ? umma_desc(b0 + j * 4096 + k * 2048, 512, 128)
                                        : umma_desc(b0 + j * 4096 + k * 256, 128, 512);
                 const uint32_t dd = tmem + (uint32_t)((i + j) * 64);
-                if (i < OZ_TS) mma_i8_ts(dd, ta + 8 * i, db, id, (K | k | i) != 0);
-                else mma_i8(dd, umma_desc(a0 + i * 8192 + k * 256, 128, 512), db, id, (K | k | i) != 0);
+                if (i < OZ_TS) mma_i8_ts(dd, ta + 8 * i, db, id, (step | k | i) != 0);
+                else mma_i8(dd, umma_desc(a0 + i * 8192 + k * 256, 128, 512), db, id, (step | k | i) != 0);
               }
           }
           if (CL == 2) mma_commit_mc(&empty[st], (uint16_t)3);   // frees the stage in both CTAs' accounting
           else mma_commit(&empty[st]);   // frees the stage once these MMAs have read it
-          if (K == ntb - 1) mma_commit(&tfull);
+          if (step == ntb - 1) mma_commit(&tfull);
         }
         __syncwarp();
         if (++st == OZ_NST) st = 0, ph ^= 1;
@@ -389,7 +465,7 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
     const int half = (warp - 2) >> 2;
     const int cc = qd * 32 + lane;
     uint32_t tph = 0;
-    for (int u = cid; u < nunits; u += ncl) {
+    for (int u = receive(); u < nunits; u = receive()) {
       const int2 it = items[u % nitems];
       const int ct = u / nitems;
       const FacSub sb = subs[it.x];
@@ -707,10 +783,11 @@ void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int
 
 void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nch, double* U, int64_t cs,
                 const int* dexp, const int* mexp, const int8_t* msl, const int8_t* wsl, const int* sexp,
-                cudaStream_t st, const int2* pairs, int npairs) {
+                cudaStream_t st, const int2* pairs, int npairs, int* uctr) {
   if (nitems <= 0) return;
   const int nct = (s + 127) / 128;
-  static const int dbg = getenv("NSP_OZ_DBG") ? atoi(getenv("NSP_OZ_DBG")) : 0;   // diagnostics: 1 / 2 skip A / B loads
+  // diagnostics: bits 1 / 2 skip the A / B loads, 4 drops the L2 evict-last hint, 8 the symmetric K order
+  static const int dbg = getenv("NSP_OZ_DBG") ? atoi(getenv("NSP_OZ_DBG")) : 0;
   // clusters of two CTAs sharing the W^T slices by multicast: parity-clean but measured no faster (cfg5 apply
   // 33.9 vs 33.4 ms: the L2 -> SM traffic does not bind; the shared-memory port does), opt-in NSP_OZ_CLUSTER=1
   static const bool cl_on = getenv("NSP_OZ_CLUSTER") && getenv("NSP_OZ_CLUSTER")[0] == '1';
@@ -733,14 +810,15 @@ void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nc
     cfg.attrs = at;
     cfg.numAttrs = 2;
     nsp_count_launch();
-    cudaLaunchKernelEx(&cfg, k_oz_symm<2>, subs, pairs, npairs, nct, msl, wsl, dexp, mexp, sexp, U, cs, nch, dbg);
+    cudaLaunchKernelEx(&cfg, k_oz_symm<2>, subs, pairs, npairs, nct, msl, wsl, dexp, mexp, sexp, U, cs, nch, dbg,
+                       (int*)nullptr);
     return;
   }
   // NSP_OZ_KERNEL=2: the register-staged variant k_oz_symm_rs - parity-clean, measured SLOWER (cfg5 apply
   // 39.0 vs 33.5 ms: the stagers' W^T loads sit on the critical path of every K-step), opt-in only
   static const int kv = getenv("NSP_OZ_KERNEL") ? atoi(getenv("NSP_OZ_KERNEL")) : 1;
   const int units = nitems * nct;
-  if (kv == 2 && !dbg) {
+  if (kv == 2 && !(dbg & 3)) {
     smem_optin((const void*)k_oz_symm_rs, RS_SMEM);
     const int grid = units < num_sms() ? units : num_sms();
     nsp_count_launch();
@@ -751,8 +829,10 @@ void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nc
   smem_optin((const void*)k_oz_symm<1>, OZ_SMEM);
   const int grid = units < num_sms() ? units : num_sms();
   nsp_count_launch();
+  static const bool stat = getenv("NSP_OZ_STATIC") && getenv("NSP_OZ_STATIC")[0] == '1';
+  if (uctr && !stat) cudaMemsetAsync(uctr, 0, sizeof(int), st);
   launch_k(k_oz_symm<1>, dim3(grid), dim3(320), (size_t)OZ_SMEM, st, subs, items, nitems, nct, msl, wsl, dexp, mexp,
-           sexp, U, cs, nch, dbg);
+           sexp, U, cs, nch, dbg, stat ? (int*)nullptr : uctr);
 }
 
 }  // namespace nspk
