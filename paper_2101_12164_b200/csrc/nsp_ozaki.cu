@@ -744,6 +744,251 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm_rs(const FacSub* __restrict_
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
+
+// ---------------------------------------------------------------- register-staged variant 2 (opt-in, slower)
+// NSP_OZ_KERNEL=3; parity-clean, measured 28.6 vs 26.2 ms per cfg5 launch (profiles/r02_ab_oz_register_staged2.txt).
+// As k_oz_symm_rs, but the four most-used W^T slices are staged by four DEDICATED warps (one per TMEM lane
+// quarter) that keep three K-steps of them in registers (loads issued two K-steps ahead of their st), so the
+// staging never waits on a load; the epilogue warps only drain the accumulators; units come from the dynamic
+// counter through the shared-memory ring (13 consumer warps).  Tensor pipe per K-step: 22 TMEM-A + 6
+// shared-memory-A MMAs, no copies (992 instead of 1,120 cycles).
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+__global__ void __launch_bounds__(448, 1) k_oz_symm_rs2(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                                        int nitems, int nct, const int8_t* __restrict__ msl,
+                                                        const int8_t* __restrict__ wsl, const int* __restrict__ dexp,
+                                                        const int* __restrict__ mexp, const int* __restrict__ sexp,
+                                                        double* __restrict__ U, int64_t cs, int nch,
+                                                        int* __restrict__ uctr) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t full[RS_NST], empty[RS_NST], afull[2], afree[2], tfull, tempty, ufull[4], uempty[4];
+  __shared__ uint32_t tbase;
+  __shared__ int uring[4];
+  uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nunits = nitems * nct;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RS_NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&afull[b], 4);
+      mbar_init(&afree[b], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, 8);
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(&ufull[q], 1);
+      mbar_init(&uempty[q], 13);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(s_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  pdl_wait();
+  int uslot = 0;
+  uint32_t uph = 0;
+  int ustat = blockIdx.x;
+  auto publish = [&]() -> int {
+    const int u = uctr ? atomicAdd(uctr, 1) : ustat;
+    ustat += gridDim.x;
+    mbar_wait(&uempty[uslot], uph ^ 1);
+    *(volatile int*)&uring[uslot] = u;
+    mbar_arrive(&ufull[uslot]);
+    if (++uslot == 4) uslot = 0, uph ^= 1;
+    return u;
+  };
+  auto receive = [&]() -> int {
+    mbar_wait(&ufull[uslot], uph);
+    const int u = *(volatile int*)&uring[uslot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&uempty[uslot]);
+    if (++uslot == 4) uslot = 0, uph ^= 1;
+    return u;
+  };
+  if (warp == 0) {
+    if (elect_one()) {   // producer: slices 4..6 of the W^T tile + the stored M tile per K tile
+      int st = 0;
+      uint32_t ph = 0;
+      const uint64_t pol = l2_evict_last();
+      for (int u = publish(); u < nunits; u = publish()) {
+        const int2 it = items[u % nitems];
+        const int ct = u / nitems;
+        const FacSub sb = subs[it.x];
+        const int I = it.y;
+        const int64_t T0 = sb.wvu_row / 64;
+        for (int K = 0; K < sb.ntb; ++K) {
+          mbar_wait(&empty[st], ph ^ 1);
+          uint8_t* As = base + st * RS_STAGE;
+          mbar_expect(&full[st], RS_AT + OZ_MT);
+          bulk_copy_hint(As, wsl + ((T0 + K) * nct + ct) * (int64_t)OZ_AT + 4 * 8192, RS_AT, &full[st], pol);
+          const int64_t t = sb.dense_off + (K <= I ? (int64_t)I * (I + 1) / 2 + K : (int64_t)K * (K + 1) / 2 + I);
+          bulk_copy(As + RS_AT, msl + t * OZ_MT, OZ_MT, &full[st]);
+          if (++st == RS_NST) st = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {   // MMA issuer
+    int st = 0;
+    uint32_t ph = 0, tph = 0, g = 0;
+    constexpr uint32_t ID_K = oz_idesc(0), ID_MN = oz_idesc(1);
+    for (int u = receive(); u < nunits; u = receive()) {
+      const int2 it = items[u % nitems];
+      const int I = it.y, ntb = subs[it.x].ntb;
+      mbar_wait(&tempty, tph ^ 1);
+      tc_fence_after();
+      for (int K = 0; K < ntb; ++K) {
+        mbar_wait(&full[st], ph);
+        const uint32_t a0 = s_u32(base + st * RS_STAGE), b0 = a0 + RS_AT;
+        const bool mn = K > I;
+        const uint32_t id = mn ? ID_MN : ID_K;
+#pragma unroll
+        for (int k = 0; k < 2; ++k, ++g) {
+          const uint32_t b = g & 1;
+          mbar_wait(&afull[b], (g >> 1) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t ta = tmem + 448u + 32u * b;
+#pragma unroll
+            for (int i = 0; i < OZ_NS; ++i)
+#pragma unroll
+              for (int j = 0; i + j < OZ_NS; ++j) {
+                const uint64_t db = mn ? umma_desc(b0 + j * 4096 + k * 2048, 512, 128)
+                                       : umma_desc(b0 + j * 4096 + k * 256, 128, 512);
+                const uint32_t dd = tmem + (uint32_t)((i + j) * 64);
+                if (i < 4) mma_i8_ts(dd, ta + 8 * i, db, id, (K | k | i) != 0);
+                else mma_i8(dd, umma_desc(a0 + (i - 4) * 8192 + k * 256, 128, 512), db, id, (K | k | i) != 0);
+              }
+            mma_commit(&afree[b]);
+            if (k == 1) mma_commit(&empty[st]);
+            if (k == 1 && K == ntb - 1) mma_commit(&tfull);
+          }
+          __syncwarp();
+        }
+        if (++st == RS_NST) st = 0, ph ^= 1;
+      }
+      tph ^= 1;
+    }
+  } else if (warp < 10) {   // epilogue warps 2..9
+    const int qd = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int cc = qd * 32 + lane;
+    uint32_t tph = 0;
+    for (int u = receive(); u < nunits; u = receive()) {
+      const int2 it = items[u % nitems];
+      const int ct = u / nitems;
+      const FacSub sb = subs[it.x];
+      const int I = it.y;
+      const int chunk = ct * 4 + qd;
+      const int ex = sexp[((int64_t)it.x * nct + ct) * 128 + cc] + mexp[it.x];
+      const int64_t row0 = sb.wvu_row + (int64_t)I * 64;
+      double* out = U + (int64_t)chunk * cs + row0 * 36 + lane;
+      mbar_wait(&tfull, tph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int nb = 4 * half; nb < 4 * half + 4; ++nb) {
+        uint32_t v[OZ_NS][8];
+#pragma unroll
+        for (int a = 0; a < OZ_NS; ++a) tmem_ld8(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(a * 64 + nb * 8), v[a]);
+        tmem_ld_wait();
+        if (chunk < nch) {
+#pragma unroll
+          for (int nn = 0; nn < 8; ++nn) {
+            const long long hi = ((long long)(int)v[0][nn] << 16) + ((long long)(int)v[1][nn] << 8) + (int)v[2][nn];
+            const long long lo = ((long long)(int)v[3][nn] << 24) + ((long long)(int)v[4][nn] << 16) +
+                                 ((long long)(int)v[5][nn] << 8) + (int)v[6][nn];
+            const double acc = fma((double)hi, 0x1p-30, (double)lo * 0x1p-62);
+            const int n = nb * 8 + nn;
+            const int E = ex + dexp[row0 + n];
+            out[(int64_t)n * 36] = (E >= -1022 && E <= 1023) ? acc * __longlong_as_double((long long)(E + 1023) << 52)
+                                                             : ldexp(acc, E);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty);
+      tph ^= 1;
+    }
+  } else {   // stager warps 10..13: TMEM lane quarter warp % 4, the four most-used W^T slices of every K-step
+    const int qd = warp & 3;
+    const int cc = qd * 32 + lane;
+    const int64_t roff = ((cc >> 3) * 4) * 128 + (cc & 7) * 16;   // row cc's bytes inside a slice (K-step 0)
+    // step iterator (unit u, K tile, K-step k); the next unit is received when a unit's steps are exhausted
+    int u = receive();
+    int ntb = 0, K = 0, k = 0;
+    const int8_t* ub = nullptr;   // W^T slices of the unit's first K tile, row cc
+    auto set_unit = [&]() {
+      if (u < nunits) {
+        const int2 it = items[u % nitems];
+        const FacSub sb = subs[it.x];
+        ntb = sb.ntb;
+        ub = wsl + ((sb.wvu_row / 64) * nct + u / nitems) * (int64_t)OZ_AT + roff;
+      }
+      K = 0;
+      k = 0;
+    };
+    set_unit();
+    // the iterator position of the NEXT load
+    auto load = [&](uint4 (&r)[8]) -> bool {
+      if (u >= nunits) return false;
+      const int8_t* q = ub + (int64_t)K * nct * OZ_AT + k * 256;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        r[2 * i] = __ldg(reinterpret_cast<const uint4*>(q + i * 8192));
+        r[2 * i + 1] = __ldg(reinterpret_cast<const uint4*>(q + i * 8192 + 128));
+      }
+      if (++k == 2) {
+        k = 0;
+        if (++K == ntb) {
+          u = receive();
+          set_unit();
+        }
+      }
+      return true;
+    };
+    uint32_t g = 0;
+    auto stage = [&](const uint4 (&r)[8]) {
+      const uint32_t b = g & 1;
+      mbar_wait(&afree[b], ((g >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + 448u + 32u * b;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tmem_st8(ta + 8 * i, r[2 * i], r[2 * i + 1]);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&afull[b]);
+      ++g;
+    };
+    uint4 r0[8], r1[8], r2[8];
+    bool v0 = load(r0), v1 = load(r1), v2;
+    while (v0) {
+      v2 = load(r2);
+      stage(r0);
+      if (!v1) break;
+      v0 = load(r0);
+      stage(r1);
+      if (!v2) break;
+      v1 = load(r1);
+      stage(r2);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
 }  // namespace
 
 namespace nspk {
@@ -818,6 +1063,16 @@ void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nc
   // 39.0 vs 33.5 ms: the stagers' W^T loads sit on the critical path of every K-step), opt-in only
   static const int kv = getenv("NSP_OZ_KERNEL") ? atoi(getenv("NSP_OZ_KERNEL")) : 1;
   const int units = nitems * nct;
+  if (kv == 3) {
+    static const bool stat3 = getenv("NSP_OZ_STATIC") && getenv("NSP_OZ_STATIC")[0] == '1';
+    if (uctr && !stat3) cudaMemsetAsync(uctr, 0, sizeof(int), st);
+    smem_optin((const void*)k_oz_symm_rs2, RS_SMEM);
+    const int grid = units < num_sms() ? units : num_sms();
+    nsp_count_launch();
+    launch_k(k_oz_symm_rs2, dim3(grid), dim3(448), (size_t)RS_SMEM, st, subs, items, nitems, nct, msl, wsl, dexp,
+             mexp, sexp, U, cs, nch, stat3 ? (int*)nullptr : uctr);
+    return;
+  }
   if (kv == 2 && !(dbg & 3)) {
     smem_optin((const void*)k_oz_symm_rs, RS_SMEM);
     const int grid = units < num_sms() ? units : num_sms();
