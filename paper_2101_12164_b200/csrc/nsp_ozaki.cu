@@ -4,8 +4,8 @@
 // splitting (DESIGN.md §6 "k_oz_symm", reading R10).
 //
 //   M_j = S_j^{-1} is symmetric positive definite.  With D = diag(delta_n), delta_n = 2^e_n and
-//   e_n = floor(log2(M_nn)/2), the symmetrically scaled Mt = D^{-1} M D^{-1} has |Mt_kn| <=
-//   sqrt(Mt_kk Mt_nn) < 2, so ONE power-of-two scale mu_j per block serves every entry and the scaling
+//   e_n = floor(log2(M_nn)/2), the symmetrically scaled Mt = D^{-1} M D^{-1} has Mt_nn in [1, 4) and
+//   |Mt_kn| <= sqrt(Mt_kk Mt_nn) < 4, so ONE power-of-two scale mu_j per block serves every entry and the scaling
 //   is the same for a stored lower tile read as itself (K-major) or transposed (MN-major): only the
 //   lower tiles are sliced, as in k_symm.  Wt = D W.  Each column c of Wt (per block) gets its own
 //   power-of-two scale sigma_c.  Every scaled entry x (|x| < 1/2) is the 56-bit fixed-point integer
