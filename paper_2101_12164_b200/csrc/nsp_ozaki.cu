@@ -12,7 +12,7 @@
 //   X = rint(x 2^55) = sum_{i=1..7} d_i 256^{7-i}, d_i signed bytes (|d_1| <= 64).  Then
 //     sum_k Wt(k,c) Mt(k,n) = sigma_c mu_j 2^-110 sum_{i,j} 256^{14-i-j} sum_k dW_i(c,k) dM_j(k,n)
 //   and the 28 int8 products with i + j <= 8 are accumulated EXACTLY in int32 (7 accumulators, one per
-//   diagonal i + j; |sum| <= 7 * 64 tiles... < 2^31 for b_j < 18,000, checked at setup); the dropped
+//   diagonal i + j; |sum| <= (64 * 128 + 6 * 128^2) b_j < 2^31 for b_j < 20,000: ntb <= 300 checked at setup); the dropped
 //   diagonals i + j >= 9 are below 2^-57 sigma_c mu_j sqrt(b) (under fp64 rounding of the result).
 //   The epilogue forms u = sum_D 2^{2-8D} acc_D in fp64 (least significant first) and scales by the
 //   powers of two: U(n, c) = delta_n sigma_c mu_j u.
