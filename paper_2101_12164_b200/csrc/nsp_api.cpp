@@ -461,6 +461,8 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_oz_tblk);
   fr(c->d_oz_pairs);
   fr(c->d_oz_ctr);
+  fr(c->d_sell_code);
+  fr(c->d_sell_tab);
   fr(c->d_items);
   fr(c->d_i1_src);
   fr(c->d_b_src);

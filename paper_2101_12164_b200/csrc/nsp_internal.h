@@ -139,6 +139,8 @@ struct nsp_ctx {
   int64_t* d_sell_ptr = nullptr;   // nslices + 1 element offsets
   int32_t* d_sell_col = nullptr;
   double* d_sell_val = nullptr;
+  uint8_t* d_sell_code = nullptr;   // dictionary-coded values (<= 255 distinct) and their table, or null
+  double* d_sell_tab = nullptr;
   int64_t n_priv = 0;         // local Gamma rows [0, n_priv) private, [n_priv, nG) shared (replicated)
   struct NspComm* comm = nullptr;
 
@@ -318,7 +320,8 @@ void cheb_step(const DevCSR& A, int64_t split, const double* d, int ld, int s, d
                double c1, double c2, bool want_d, cudaStream_t st);
 // the s = 1 step on the sliced-ELL A_G (rows = n_G)
 void cheb_step_sell(int64_t rows, const int64_t* sptr, const int32_t* col, const double* val, const double* d,
-                    double* x, double* r, double* dn, double c1, double c2, bool want_d, cudaStream_t st);
+                    double* x, double* r, double* dn, double c1, double c2, bool want_d, cudaStream_t st,
+                    const uint8_t* code = nullptr, const double* tab = nullptr);
 // Gaussian block on the device, bit-compatible with nsp_inputs.philox.gaussian_block (reading C7):
 // out[r * ld + j] (j < s; columns s..ld-1 zeroed) = N(0,1) from Philox4x32-10 counter (gidx[r] * s + j,
 // stream, 0), key = seed, Box-Muller cosine branch.  gidx: device int64 row indices.

@@ -438,6 +438,39 @@ __global__ void __launch_bounds__(256) k_cheb_step_sell(int64_t rows, const int6
   if (want_d) dn[row] = fma(c1, di, c2 * ri);
 }
 
+// The same step with A_G's values dictionary-coded (one byte per entry into a table of the <= 255 distinct
+// values, built in setup when A_G has that few - every constant-coefficient stencil): 5 instead of 12 bytes
+// per stored entry, the values bitwise the same.
+__global__ void __launch_bounds__(256) k_cheb_step_sell_dict(int64_t rows, const int64_t* __restrict__ sptr,
+                                                             const int32_t* __restrict__ col,
+                                                             const uint8_t* __restrict__ code,
+                                                             const double* __restrict__ tab,
+                                                             const double* __restrict__ d, double* __restrict__ x,
+                                                             double* __restrict__ r, double* __restrict__ dn,
+                                                             double c1, double c2, int want_d) {
+  __shared__ double st[256];
+  st[threadIdx.x] = tab[threadIdx.x];
+  pdl_wait();
+  __syncthreads();
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const int64_t sl = row >> 5;
+  const int lane = (int)(row & 31);
+  const int64_t b = sptr[sl];
+  const int w = (int)((sptr[sl + 1] - b) >> 5);
+  double acc = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < w; ++j) {
+    const int c = col[b + j * 32 + lane];
+    if (c >= 0) acc = fma(st[code[b + j * 32 + lane]], __ldg(d + c), acc);
+  }
+  const double di = d[row];
+  x[row] += di;
+  const double ri = r[row] - acc;
+  r[row] = ri;
+  if (want_d) dn[row] = fma(c1, di, c2 * ri);
+}
+
 template <int NQ2>
 __global__ void __launch_bounds__(256, NQ2 <= 2 ? 8 : 4) k_cheb_step_blk(int64_t rows, const int32_t* __restrict__ rp,
                                                        const int32_t* __restrict__ ci, const double* __restrict__ va,
@@ -2117,8 +2150,15 @@ void cheb_step(const DevCSR& A, int64_t split, const double* d, int ld, int s, d
 }
 
 void cheb_step_sell(int64_t rows, const int64_t* sptr, const int32_t* col, const double* val, const double* d,
-                    double* x, double* r, double* dn, double c1, double c2, bool want_d, cudaStream_t st) {
+                    double* x, double* r, double* dn, double c1, double c2, bool want_d, cudaStream_t st,
+                    const uint8_t* code, const double* tab) {
   if (rows <= 0) return;
+  if (code && tab) {
+    nsp_count_launch();
+    launch_k(k_cheb_step_sell_dict, dim3((unsigned)((rows + 255) / 256)), dim3(256), 0, st, rows, sptr, col, code, tab,
+             d, x, r, dn, c1, c2, want_d ? 1 : 0);
+    return;
+  }
   nsp_count_launch();
   launch_k(k_cheb_step_sell, dim3((unsigned)((rows + 255) / 256)), dim3(256), 0, st, rows, sptr, col, val, d, x, r, dn,
            c1, c2, want_d ? 1 : 0);

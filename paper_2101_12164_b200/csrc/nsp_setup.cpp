@@ -1119,6 +1119,27 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
     if ((st = upload(c, &c->d_sell_ptr, sptr)) != NSP_OK) return st;
     if ((st = upload(c, &c->d_sell_col, scol)) != NSP_OK) return st;
     if ((st = upload(c, &c->d_sell_val, sval)) != NSP_OK) return st;
+    {   // dictionary coding of the values when A_G has at most 255 distinct ones (code 255: padding)
+      std::vector<double> tab;
+      std::vector<uint8_t> code(sval.size(), 255);
+      bool ok = true;
+      for (size_t e = 0; e < sval.size() && ok; ++e) {
+        if (scol[e] < 0) continue;
+        size_t t = 0;
+        while (t < tab.size() && std::memcmp(&tab[t], &sval[e], sizeof(double)) != 0) ++t;   // bitwise
+        if (t == tab.size()) {
+          if (tab.size() == 255) ok = false;
+          else tab.push_back(sval[e]);
+        }
+        code[e] = (uint8_t)t;
+      }
+      const char* de = getenv("NSP_SELL_DICT");
+      if (ok && !(de && de[0] == '0')) {
+        tab.resize(256, 0.0);
+        if ((st = upload(c, &c->d_sell_code, code)) != NSP_OK) return st;
+        if ((st = upload(c, &c->d_sell_tab, tab)) != NSP_OK) return st;
+      }
+    }
   }
   if ((st = upload_csr(c, c->CB, CB)) != NSP_OK) return st;
   if (!AII.rowptr.empty()) {

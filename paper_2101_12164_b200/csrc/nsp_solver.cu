@@ -669,7 +669,7 @@ static nsp_status ag_cheb(nsp_ctx* c, const double* X, int ldx, double* Y, int l
     static const bool sell_off = getenv("NSP_CHEB_SELL") && getenv("NSP_CHEB_SELL")[0] == '0';
     if (c->nranks == 1 && !fused_off && ld == 1 && c->d_sell_ptr && !sell_off) {   // s = 1: sliced ELL
       nspk::cheb_step_sell(n, c->d_sell_ptr, c->d_sell_col, c->d_sell_val, d0, xw, r, d1, c->cheb_c1[k],
-                           c->cheb_c2[k], k + 1 < c->cheb_K, st);
+                           c->cheb_c2[k], k + 1 < c->cheb_K, st, c->d_sell_code, c->d_sell_tab);
       std::swap(d0, d1);
       continue;
     }
