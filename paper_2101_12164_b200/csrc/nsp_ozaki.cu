@@ -26,6 +26,7 @@
 //   A operand = W^T slices (M = 128 columns c, K-major), B operand = Mt column tile I (N = 64 rows n):
 //   for K <= I the stored tile (I, K) read K-major, for K > I the stored tile (K, I) read MN-major.
 #include <climits>
+#include <cstdio>
 #include "nsp_internal.h"
 #include "nsp_dmma.cuh"
 
@@ -63,6 +64,31 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t ta, uint64_t b, u
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
       "r"(ta), "l"(b), "r"(id), "r"(acc));
+}
+// weight-stationary form: the B operand can be held in collector buffer b0 across consecutive MMAs (fill /
+// use / lastuse), so the 7 - j products that share B slice j read it from shared memory once
+#define OZ_WS_SS(QUAL, d, a, b, id, acc)                                                                 \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                                     \
+               "tcgen05.mma.ws.cta_group::1.kind::i8" QUAL " [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d), "l"(a), \
+               "l"(b), "r"(id), "r"((uint32_t)(acc)))
+#define OZ_WS_TS(QUAL, d, a, b, id, acc)                                                                   \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                                       \
+               "tcgen05.mma.ws.cta_group::1.kind::i8" QUAL " [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d), "r"(a), \
+               "l"(b), "r"(id), "r"((uint32_t)(acc)))
+__device__ __forceinline__ void mma_ws(int coll, bool ts, uint32_t d, uint32_t ta, uint64_t a, uint64_t b,
+                                       uint32_t id, uint32_t acc) {
+  // coll: 0 none, 1 fill, 2 use, 3 lastuse
+  if (ts) {
+    if (coll == 1) OZ_WS_TS(".collector::b0::fill", d, ta, b, id, acc);
+    else if (coll == 2) OZ_WS_TS(".collector::b0::use", d, ta, b, id, acc);
+    else if (coll == 3) OZ_WS_TS(".collector::b0::lastuse", d, ta, b, id, acc);
+    else OZ_WS_TS("", d, ta, b, id, acc);
+  } else {
+    if (coll == 1) OZ_WS_SS(".collector::b0::fill", d, a, b, id, acc);
+    else if (coll == 2) OZ_WS_SS(".collector::b0::use", d, a, b, id, acc);
+    else if (coll == 3) OZ_WS_SS(".collector::b0::lastuse", d, a, b, id, acc);
+    else OZ_WS_SS("", d, a, b, id, acc);
+  }
 }
 // shared memory (canonical K-major, 128 rows x 32 bytes) -> TMEM (128 lanes x 8 columns)
 __device__ __forceinline__ void tc_cp(uint32_t ta, uint64_t sd) {
@@ -415,17 +441,36 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
   } else if (warp == 1) {
     int st = 0;
     uint32_t ph = 0, tph = 0;
+#ifdef NSP_OZ_PROF
+    long long t_tmem = 0, t_full = 0, t_all = clock64();
+#endif
     constexpr uint32_t ID_K = oz_idesc(0), ID_MN = oz_idesc(1);
+    // diagnostic bit 16: the B-stationary order with collector reuse (tcgen05.mma.ws) - parity-clean and faster
+    // in isolation (tools/bench_i8mma.cu: 1,344 -> 1,177 cycles per K-step for the all-SS form) but slower here
+    // combined with the TMEM-sourced A slices (cfg5 27.25 vs 25.93 ms per launch): off
+    const bool ws = (dbg & 16) != 0;
     for (int u = receive(); u < nunits; u = receive()) {
       const int2 it = items[u % nitems];
       const int ntb = subs[it.x].ntb;
       const int I = min(it.y + crank, ntb - 1);
+#ifdef NSP_OZ_PROF
+      long long t0 = clock64();
+#endif
       mbar_wait(&tempty, tph ^ 1);   // the epilogue has drained the previous unit's accumulators
+#ifdef NSP_OZ_PROF
+      t_tmem += clock64() - t0;
+#endif
       tc_fence_after();
       OzKOrder ko(I, ntb, CL == 2 || !(dbg & 8));
       for (int step = 0; step < ntb; ++step, ko.next()) {
         const int K = ko.K;
+#ifdef NSP_OZ_PROF
+        long long t1 = clock64();
+#endif
         mbar_wait(&full[st], ph);
+#ifdef NSP_OZ_PROF
+        t_full += clock64() - t1;
+#endif
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a0 = s_u32(base + st * (OZ_AT + OZ_MT)), b0 = a0 + OZ_AT;
@@ -440,16 +485,31 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
             const uint32_t ta = tmem + 448u + (uint32_t)(k * 8 * OZ_TS);
 #pragma unroll
             for (int i = 0; i < OZ_TS; ++i) tc_cp(ta + 8 * i, umma_desc(a0 + i * 8192 + k * 256, 128, 512));
+            if (ws) {   // B-stationary order: j outer, the products sharing B slice j read it once (collector b0)
 #pragma unroll
-            for (int i = 0; i < OZ_NS; ++i)
-#pragma unroll
-              for (int j = 0; i + j < OZ_NS; ++j) {
+              for (int j = 0; j < OZ_NS; ++j) {
                 const uint64_t db = mn ? umma_desc(b0 + j * 4096 + k * 2048, 512, 128)
                                        : umma_desc(b0 + j * 4096 + k * 256, 128, 512);
-                const uint32_t dd = tmem + (uint32_t)((i + j) * 64);
-                if (i < OZ_TS) mma_i8_ts(dd, ta + 8 * i, db, id, (step | k | i) != 0);
-                else mma_i8(dd, umma_desc(a0 + i * 8192 + k * 256, 128, 512), db, id, (step | k | i) != 0);
+#pragma unroll
+                for (int i = 0; i + j < OZ_NS; ++i) {
+                  const uint32_t dd = tmem + (uint32_t)((i + j) * 64);
+                  const int coll = (j == OZ_NS - 1) ? 0 : (i == 0 ? 1 : (i + j == OZ_NS - 1 ? 3 : 2));
+                  mma_ws(coll, i < OZ_TS, dd, ta + 8 * i, umma_desc(a0 + i * 8192 + k * 256, 128, 512), db, id,
+                         (step | k | j) != 0);   // the first product into diagonal i + j is the one with j = 0
+                }
               }
+            } else {
+#pragma unroll
+              for (int i = 0; i < OZ_NS; ++i)
+#pragma unroll
+                for (int j = 0; i + j < OZ_NS; ++j) {
+                  const uint64_t db = mn ? umma_desc(b0 + j * 4096 + k * 2048, 512, 128)
+                                         : umma_desc(b0 + j * 4096 + k * 256, 128, 512);
+                  const uint32_t dd = tmem + (uint32_t)((i + j) * 64);
+                  if (i < OZ_TS) mma_i8_ts(dd, ta + 8 * i, db, id, (step | k | i) != 0);
+                  else mma_i8(dd, umma_desc(a0 + i * 8192 + k * 256, 128, 512), db, id, (step | k | i) != 0);
+                }
+            }
           }
           if (CL == 2) mma_commit_mc(&empty[st], (uint16_t)3);   // frees the stage in both CTAs' accounting
           else mma_commit(&empty[st]);   // frees the stage once these MMAs have read it
@@ -460,6 +520,13 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
       }
       tph ^= 1;
     }
+#ifdef NSP_OZ_PROF
+    if (lane == 0 && uctr) {
+      atomicAdd((unsigned long long*)(uctr + 64), (unsigned long long)t_tmem);
+      atomicAdd((unsigned long long*)(uctr + 66), (unsigned long long)t_full);
+      atomicAdd((unsigned long long*)(uctr + 68), (unsigned long long)(clock64() - t_all));
+    }
+#endif
   } else {   // epilogue warps 2..9: TMEM lane quarter warp % 4, n-column half (warp - 2) / 4
     const int qd = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -1086,8 +1153,20 @@ void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nc
   nsp_count_launch();
   static const bool stat = getenv("NSP_OZ_STATIC") && getenv("NSP_OZ_STATIC")[0] == '1';
   if (uctr && !stat) cudaMemsetAsync(uctr, 0, sizeof(int), st);
+#ifdef NSP_OZ_PROF
+  if (uctr) cudaMemsetAsync(uctr + 64, 0, 64, st);
+#endif
   launch_k(k_oz_symm<1>, dim3(grid), dim3(320), (size_t)OZ_SMEM, st, subs, items, nitems, nct, msl, wsl, dexp, mexp,
            sexp, U, cs, nch, dbg, stat ? (int*)nullptr : uctr);
+#ifdef NSP_OZ_PROF
+  if (uctr) {
+    unsigned long long h[3];
+    cudaMemcpyAsync(h, uctr + 64, 24, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[oz prof] MMA warp per CTA: tempty wait %.3f, full wait %.3f, total %.3f Mcycles (grid %d)\n",
+            h[0] / 1e6 / grid, h[1] / 1e6 / grid, h[2] / 1e6 / grid, grid);
+  }
+#endif
 }
 
 }  // namespace nspk

@@ -1356,7 +1356,7 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
           for (int j = 0; j < c->nsub; ++j)
             for (int I = 0; I < c->subs[j].ntb; I += 2) pr.push_back(make_int2(j, I));
           c->n_oz_pairs = (int)pr.size();
-          NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_oz_ctr, 256));
+          NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_oz_ctr, 1024));   // [0]: the counter; [64..69]: NSP_OZ_PROF diagnostics
           if (!pr.empty() && (st = upload(c, &c->d_oz_pairs, pr)) != NSP_OK) return st;
         }
         nspk::oz_setup(c->d_subs, c->nsub, c->max_ntb, c->d_items, c->n_items, c->d_minv, c->d_oz_dexp,

@@ -410,6 +410,110 @@ __global__ void k_rate_ts(int reps, long long* cyc, int32_t* sink) {
   if (threadIdx.x < 32) tmem_dealloc(t0, 512);
 }
 
+// ---------------------------------------------------------------- weight-stationary form with the B collector
+#define WS_MMA(QUAL, d, a, b, id, acc)                                                                  \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                                       \
+               "tcgen05.mma.ws.cta_group::1.kind::i8" QUAL " [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d), "l"(a), \
+               "l"(b), "r"(id), "r"((uint32_t)(acc)))
+// D_t (t = 0, 1) = A_t B: the first MMA fills the B collector, the second reuses it
+__global__ void k_check_ws(const int8_t* A, const int8_t* B, int32_t* D, int K) {
+  constexpr int N = 64;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  int8_t* As = (int8_t*)sm;            // two A operands of 128 x K
+  int8_t* Bs = As + 2 * 128 * K;
+  for (int i = threadIdx.x; i < 2 * 128 * K; i += blockDim.x) As[i] = A[i];
+  for (int i = threadIdx.x; i < N * K; i += blockDim.x) Bs[i] = B[i];
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (threadIdx.x < 32) tmem_alloc(&tbase, 256);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t t0 = tbase;
+  if (threadIdx.x < 32 && elect_one()) {
+    const uint32_t id = idesc_i8(128, N, 0, 0);
+    for (int k = 0; k < K / 32; ++k) {
+      const uint64_t db = sdesc(smem_u32(Bs) + k * 256, 128, (K / 16) * 128);
+      const uint64_t da0 = sdesc(smem_u32(As) + k * 256, 128, (K / 16) * 128);
+      const uint64_t da1 = sdesc(smem_u32(As + 128 * K) + k * 256, 128, (K / 16) * 128);
+      WS_MMA(".collector::b0::fill", t0, da0, db, id, k > 0);
+      WS_MMA(".collector::b0::lastuse", t0 + N, da1, db, id, k > 0);
+    }
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = 0; c < 2 * N; c += 16) {
+    uint32_t v[16];
+    ld16(t0 + ((uint32_t)(32 * w) << 16) + c, v);
+    for (int q = 0; q < 16; ++q) D[(32 * w + lane) * 2 * N + c + q] = (int32_t)v[q];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(t0, 256);
+}
+// Ozaki pattern in weight-stationary order: for each B slice j, the 7 - j products with A slices i share it
+template <int KC, bool COLL>
+__global__ void k_rate_ws(int reps, long long* cyc, int32_t* sink) {
+  constexpr int N = 64;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  int8_t* As = (int8_t*)sm;
+  int8_t* Bs = As + 7 * 128 * KC;
+  for (int i = threadIdx.x; i < 7 * (128 + N) * KC; i += blockDim.x) As[i] = (int8_t)((i * 37) & 7) - 3;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (threadIdx.x < 32) tmem_alloc(&tbase, 512);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t t0 = tbase;
+  if (threadIdx.x < 32 && elect_one()) {
+    constexpr uint32_t id = idesc_i8(128, N, 0, 0);
+    const uint64_t a0 = sdesc(smem_u32(As), 128, (KC / 16) * 128);
+    const uint64_t b0 = sdesc(smem_u32(Bs), 128, (KC / 16) * 128);
+    const long long c0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int k = 0; k < KC / 32; ++k)
+#pragma unroll
+        for (int j = 0; j < 7; ++j)
+#pragma unroll
+          for (int i = 0; i + j < 7; ++i) {
+            const uint64_t da = a0 + (uint64_t)((i * 128 * KC + k * 256) >> 4);
+            const uint64_t db = b0 + (uint64_t)((j * N * KC + k * 256) >> 4);
+            const uint32_t dd = t0 + (uint32_t)((i + j) * N);
+            const uint32_t acc = (r | k) > 0;
+            if (!COLL || j == 6) WS_MMA("", dd, da, db, id, acc);
+            else if (i == 0) WS_MMA(".collector::b0::fill", dd, da, db, id, acc);
+            else if (i + j == 6) WS_MMA(".collector::b0::lastuse", dd, da, db, id, acc);
+            else WS_MMA(".collector::b0::use", dd, da, db, id, acc);
+          }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    cyc[blockIdx.x] = clock64() - c0;
+  }
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  uint32_t v[16];
+  ld16(t0 + ((uint32_t)(32 * (threadIdx.x >> 5)) << 16), v);
+  if (v[0] == 0x7fffffff) sink[0] = v[1];
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(t0, 512);
+}
+
 int main() {
   std::mt19937 rng(7);
   std::uniform_int_distribution<int> dist(-128, 127);
@@ -494,6 +598,42 @@ int main() {
     printf("check TS (A in TMEM via tcgen05.cp) N=64: %s (%d bad)\n", bad ? "FAIL" : "ok", bad);
     fails += bad != 0;
   }
+  {   // weight-stationary MMA with the B collector
+    const int N = 64, K = 64;
+    std::vector<int8_t> a(2 * 128 * K), b(N * K), ab(2 * 128 * K), bb(N * K);
+    for (auto& x : a) x = (int8_t)dist(rng);
+    for (auto& x : b) x = (int8_t)dist(rng);
+    for (int t = 0; t < 2; ++t)
+      for (int m = 0; m < 128; ++m)
+        for (int k = 0; k < K; ++k)
+          ab[t * 128 * K + ((m / 8) * (K / 16) + k / 16) * 128 + (m % 8) * 16 + k % 16] = a[(t * 128 + m) * K + k];
+    for (int n = 0; n < N; ++n)
+      for (int k = 0; k < K; ++k) bb[((n / 8) * (K / 16) + k / 16) * 128 + (n % 8) * 16 + k % 16] = b[n * K + k];
+    int8_t *dA, *dB;
+    int32_t* dD;
+    CK(cudaMalloc(&dA, ab.size()));
+    CK(cudaMalloc(&dB, bb.size()));
+    CK(cudaMalloc(&dD, 128 * 2 * N * 4));
+    CK(cudaMemcpy(dA, ab.data(), ab.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, bb.data(), bb.size(), cudaMemcpyHostToDevice));
+    k_check_ws<<<1, 128, 2 * 128 * K + N * K>>>(dA, dB, dD, K);
+    CK(cudaDeviceSynchronize());
+    std::vector<int32_t> d(128 * 2 * N);
+    CK(cudaMemcpy(d.data(), dD, d.size() * 4, cudaMemcpyDeviceToHost));
+    int bad = 0;
+    for (int t = 0; t < 2; ++t)
+      for (int m = 0; m < 128; ++m)
+        for (int n = 0; n < N; ++n) {
+          int32_t ref = 0;
+          for (int k = 0; k < K; ++k) ref += (int32_t)a[(t * 128 + m) * K + k] * b[n * K + k];
+          if (ref != d[m * 2 * N + t * N + n]) {
+            if (bad < 4) printf("  WS mismatch t=%d (%d,%d): got %d ref %d\n", t, m, n, d[m * 2 * N + t * N + n], ref);
+            ++bad;
+          }
+        }
+    printf("check WS (B collector fill / lastuse) N=64: %s (%d bad)\n", bad ? "FAIL" : "ok", bad);
+    fails += bad != 0;
+  }
   long long* dc;
   int32_t* sink;
   CK(cudaMalloc(&dc, 1024 * 8));
@@ -548,6 +688,8 @@ int main() {
   run2(k_rate2<64, 128>, 64, 128, 28, 128, 7 * (128 + 64) * 128, "ozaki-tight");
   run2(k_rate2<32, 128>, 32, 128, 28, 128, 7 * (128 + 32) * 128, "ozaki-tight");
   run2(k_rate_mn<64, 64>, 64, 64, 28, 256, 7 * (128 + 64) * 64, "ozaki-MN-B");
+  run2(k_rate_ws<64, false>, 64, 64, 28, 256, 7 * (128 + 64) * 64, "ozaki-WS");
+  run2(k_rate_ws<64, true>, 64, 64, 28, 256, 7 * (128 + 64) * 64, "ozaki-WS-collector");
   run2(k_rate_ts<1, 64>, 64, 64, 28, 256, 7 * (128 + 64) * 64, "ozaki-TS1");
   run2(k_rate_ts<2, 64>, 64, 64, 28, 256, 7 * (128 + 64) * 64, "ozaki-TS2");
   run2(k_rate_ts<3, 64>, 64, 64, 28, 256, 7 * (128 + 64) * 64, "ozaki-TS3");
