@@ -319,6 +319,12 @@ void scatter_rows(const double* src, int lds, const int32_t* idx, int64_t rows, 
 void cheb_step(const DevCSR& A, int64_t split, const double* d, int ld, int s, double* x, double* r, double* dn,
                double c1, double c2, bool want_d, cudaStream_t st);
 // the s = 1 step on the sliced-ELL A_G (rows = n_G)
+// three-term Chebyshev step x_{k+1} = x_k + c1 (x_k - x_{k-1}) + c2 (b - A x_k) (rows of A with cols < split; s = 1:
+// the sliced ELL copy of A_G over `split` rows); xn may alias xp
+void cheb3_step(const DevCSR& A, int64_t split, const double* xk, int ld, int s, const double* xp, const double* b,
+                double* xn, double c1, double c2, cudaStream_t st, const int64_t* sptr = nullptr,
+                const int32_t* scol = nullptr, const double* sval = nullptr, const uint8_t* code = nullptr,
+                const double* tab = nullptr);
 void cheb_step_sell(int64_t rows, const int64_t* sptr, const int32_t* col, const double* val, const double* d,
                     double* x, double* r, double* dn, double c1, double c2, bool want_d, cudaStream_t st,
                     const uint8_t* code = nullptr, const double* tab = nullptr);

@@ -471,6 +471,98 @@ __global__ void __launch_bounds__(256) k_cheb_step_sell_dict(int64_t rows, const
   if (want_d) dn[row] = fma(c1, di, c2 * ri);
 }
 
+// Three-term form of the same Chebyshev iteration (x only): with d_{k-1} = x_k - x_{k-1} and
+// r_k = b - A x_k the step x_{k+1} = x_k + d_k, d_k = c1 d_{k-1} + c2 r_k becomes
+//   x_{k+1} = x_k + c1 (x_k - x_{k-1}) + c2 (b - A x_k),
+// the same polynomial in A with 4 instead of 6 block passes per step (reads x_k, x_{k-1}, b; writes x_{k+1}
+// over x_{k-1}, which no other row reads).  xn may alias xp.
+template <int NQ2>
+__global__ void __launch_bounds__(256, NQ2 <= 2 ? 8 : 4) k_cheb3_step_blk(int64_t rows, const int32_t* __restrict__ rp,
+                                                        const int32_t* __restrict__ ci, const double* __restrict__ va,
+                                                        int64_t split, const double* __restrict__ xk, int ld,
+                                                        const double* xp, const double* __restrict__ b,
+                                                        double* xn, double c1, double c2) {
+  pdl_wait();
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int beg = rp[row], end = rp[row + 1];
+  double2 acc[NQ2];
+#pragma unroll
+  for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
+  for (int base = beg; base < end; base += 32) {
+    const int k = base + lane;
+    const int c = k < end ? ci[k] : 0;
+    const double v = k < end ? va[k] : 0.0;
+    const int cnt = min(32, end - base);
+    for (int q = 0; q < cnt; ++q) {
+      const int64_t col = __shfl_sync(0xffffffffu, c, q);
+      const double a = __shfl_sync(0xffffffffu, v, q);
+      if (col >= split) continue;
+      const double* src = xk + col * ld;
+#pragma unroll
+      for (int qq = 0; qq < NQ2; ++qq) {
+        const int cc = 2 * lane + 64 * qq;
+        if (cc < ld) {
+          const double2 dv = __ldg(reinterpret_cast<const double2*>(src + cc));
+          acc[qq].x = fma(a, dv.x, acc[qq].x);
+          acc[qq].y = fma(a, dv.y, acc[qq].y);
+        }
+      }
+    }
+  }
+  const int64_t o = row * ld;
+#pragma unroll
+  for (int qq = 0; qq < NQ2; ++qq) {
+    const int cc = 2 * lane + 64 * qq;
+    if (cc >= ld) continue;
+    const double2 xi = *reinterpret_cast<const double2*>(xk + o + cc);
+    const double2 xo = *reinterpret_cast<const double2*>(xp + o + cc);
+    const double2 bi = __ldg(reinterpret_cast<const double2*>(b + o + cc));
+    double2 y;
+    y.x = xi.x + fma(c1, xi.x - xo.x, c2 * (bi.x - acc[qq].x));
+    y.y = xi.y + fma(c1, xi.y - xo.y, c2 * (bi.y - acc[qq].y));
+    *reinterpret_cast<double2*>(xn + o + cc) = y;
+  }
+}
+
+// s = 1, sliced ELL (values direct or dictionary-coded): one thread per row
+__global__ void __launch_bounds__(256) k_cheb3_step_sell(int64_t rows, const int64_t* __restrict__ sptr,
+                                                         const int32_t* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const uint8_t* __restrict__ code,
+                                                         const double* __restrict__ tab,
+                                                         const double* __restrict__ xk, const double* xp,
+                                                         const double* __restrict__ b, double* xn, double c1,
+                                                         double c2) {
+  __shared__ double stab[256];
+  if (code) stab[threadIdx.x] = tab[threadIdx.x];
+  pdl_wait();
+  __syncthreads();
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const int64_t sl = row >> 5;
+  const int lane = (int)(row & 31);
+  const int64_t b0 = sptr[sl];
+  const int w = (int)((sptr[sl + 1] - b0) >> 5);
+  double acc = 0.0;
+  if (code) {
+#pragma unroll 4
+    for (int j = 0; j < w; ++j) {
+      const int c = col[b0 + j * 32 + lane];
+      if (c >= 0) acc = fma(stab[code[b0 + j * 32 + lane]], __ldg(xk + c), acc);
+    }
+  } else {
+#pragma unroll 4
+    for (int j = 0; j < w; ++j) {
+      const int c = col[b0 + j * 32 + lane];
+      if (c >= 0) acc = fma(val[b0 + j * 32 + lane], __ldg(xk + c), acc);
+    }
+  }
+  const double xi = xk[row];
+  xn[row] = xi + fma(c1, xi - xp[row], c2 * (b[row] - acc));
+}
+
 template <int NQ2>
 __global__ void __launch_bounds__(256, NQ2 <= 2 ? 8 : 4) k_cheb_step_blk(int64_t rows, const int32_t* __restrict__ rp,
                                                        const int32_t* __restrict__ ci, const double* __restrict__ va,
@@ -2147,6 +2239,31 @@ void cheb_step(const DevCSR& A, int64_t split, const double* d, int ld, int s, d
   else
     launch_k(k_cheb_step_blk<4>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, split, d, ld, x, r, dn, c1,
              c2, want_d ? 1 : 0);
+}
+
+void cheb3_step(const DevCSR& A, int64_t split, const double* xk, int ld, int s, const double* xp, const double* b,
+                double* xn, double c1, double c2, cudaStream_t st, const int64_t* sptr, const int32_t* scol,
+                const double* sval, const uint8_t* code, const double* tab) {
+  if (A.rows <= 0 && !(s == 1 && sptr)) return;
+  if (s == 1 && ld == 1) {
+    const int64_t rows = split;
+    nsp_count_launch();
+    launch_k(k_cheb3_step_sell, dim3((unsigned)((rows + 255) / 256)), dim3(256), 0, st, rows, sptr, scol, sval, code,
+             tab, xk, xp, b, xn, c1, c2);
+    return;
+  }
+  const unsigned blocks = (unsigned)((A.rows * 32 + 255) / 256);
+  const int nq2 = (ld + 63) / 64;
+  nsp_count_launch();
+  if (nq2 == 1)
+    launch_k(k_cheb3_step_blk<1>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, split, xk, ld, xp, b,
+             xn, c1, c2);
+  else if (nq2 == 2)
+    launch_k(k_cheb3_step_blk<2>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, split, xk, ld, xp, b,
+             xn, c1, c2);
+  else
+    launch_k(k_cheb3_step_blk<4>, dim3(blocks), dim3(256), 0, st, A.rows, A.rowptr, A.col, A.val, split, xk, ld, xp, b,
+             xn, c1, c2);
 }
 
 void cheb_step_sell(int64_t rows, const int64_t* sptr, const int32_t* col, const double* val, const double* d,

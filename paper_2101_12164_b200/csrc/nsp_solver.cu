@@ -662,6 +662,24 @@ static nsp_status ag_cheb(nsp_ctx* c, const double* X, int ldx, double* Y, int l
   if (n == 0) return NSP_OK;
   nspb::copy_pad(X, ldx, r, ld, n, s, 1.0, st);
   const double theta = 0.5 * (c->cheb_b + c->cheb_a);
+  // one rank: the three-term (x-only) form of the same polynomial, 4 instead of 6 block passes per step
+  static const bool three_off = getenv("NSP_CHEB3") && getenv("NSP_CHEB3")[0] == '0';
+  const bool s1_sell = ld == 1 && c->d_sell_ptr;
+  if (c->nranks == 1 && !three_off && c->cheb_K >= 1 && (s1_sell || (ld > 1 && ld % 2 == 0 && c->AGO.rows))) {
+    // x_0 = 0, x_1 = d_0 = b / theta, then K - 1 steps x_{k+1} = x_k + c1_{k-1} (x_k - x_{k-1}) + c2_{k-1} (b - A x_k)
+    double* xk = d0;   // x_1
+    double* xo = xw;   // x_0 = 0 (overwritten by x_2)
+    nspb::copy_pad(X, ldx, xk, ld, n, s, 1.0 / theta, st);
+    NSP_CUDA_TRY(c, cudaMemsetAsync(xo, 0, blk * 8, st));
+    for (int k = 1; k < c->cheb_K; ++k) {
+      nspk::cheb3_step(c->AGO, n, xk, ld, s, xo, r, xo, c->cheb_c1[k - 1], c->cheb_c2[k - 1], st, c->d_sell_ptr,
+                       c->d_sell_col, c->d_sell_val, c->d_sell_code, c->d_sell_tab);
+      std::swap(xk, xo);
+    }
+    nspb::copy_pad(xk, ld, Y, ldy, n, s, 1.0, st);
+    NSP_CUDA_TRY(c, cudaGetLastError());
+    return NSP_OK;
+  }
   nspb::copy_pad(X, ldx, d0, ld, n, s, 1.0 / theta, st);
   NSP_CUDA_TRY(c, cudaMemsetAsync(xw, 0, blk * 8, st));
   static const bool fused_off = getenv("NSP_CHEB_FUSED") && getenv("NSP_CHEB_FUSED")[0] == '0';
