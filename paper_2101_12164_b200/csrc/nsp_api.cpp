@@ -174,7 +174,13 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
       double* P = U + c->wvu_rows * (int64_t)ldw;
       P = (double*)(((uintptr_t)P + 255) & ~(uintptr_t)255);
       nsp_count_path(NSP_PATH_SYMV);
+      // NSP_OZ_SYMV=1: the product from the INT8 slices, decoded per entry - parity-clean but measured slower
+      // (cfg5 outer PCG 20.1 vs 12.2 ms per iteration: the decode, not the bytes, binds); opt-in only
+      static const bool oz_symv = getenv("NSP_OZ_SYMV") && getenv("NSP_OZ_SYMV")[0] == '1';
       if (getenv("NSP_SYMV2")) nspk::symv(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, c->stream);
+      else if (c->d_oz_msl && oz_symv && c->opts.apply_kernel != 2)   // the INT8 slices, decoded (7 B per entry)
+        nspk::oz_symv1(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_oz_msl, c->d_oz_dexp, c->d_oz_mexp, wvu, ldw,
+                       U, P, c->stream);
       else nspk::symv1(c->d_subs, c->d_items, c->n_items, c->max_ntb, c->d_minv, wvu, ldw, U, P, c->stream);
     } else if (use_ozaki(c, s)) {
       nsp_count_path(NSP_PATH_OZAKI);

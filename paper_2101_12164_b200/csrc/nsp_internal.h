@@ -287,6 +287,9 @@ void oz_setup(const FacSub* subs, int nsub, int max_ntb, const int2* items, int 
 void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int s, int nch, const double* W,
                 int64_t cs, const int* dexp, int8_t* wsl, int* sexp, cudaStream_t st, bool have_exp = false);
 // U = S_j^{-1} W for the items [0, nitems) from the slices (chunk-major U)
+// s = 1: u_j = S_j^{-1} w_j from the slices (one column, ld ldw; P: partial slots as k_symv1)
+void oz_symv1(const FacSub* subs, const int2* items, int nitems, int max_ntb, const int8_t* msl, const int* dexp,
+              const int* mexp, const double* W, int ldw, double* U, double* P, cudaStream_t st);
 // pairs (j, I0), I0 even, covering the same items: clusters of two CTAs share the W^T slices (multicast)
 void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nch, double* U, int64_t cs,
                 const int* dexp, const int* mexp, const int8_t* msl, const int8_t* wsl, const int* sexp,

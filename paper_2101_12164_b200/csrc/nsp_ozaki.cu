@@ -1056,6 +1056,94 @@ __global__ void __launch_bounds__(448, 1) k_oz_symm_rs2(const FacSub* __restrict
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
+
+// ---------------------------------------------------------------- s = 1: the matrix-vector product on the slices
+// u_j = S_j^{-1} w_j for one column (the outer PCG's apply) from the same int8 slices, read once per stored tile
+// (k_symv1's symmetric single read: the CTA of stored row I forms M_IJ w_J for row I and M_IJ^T w_I for row J).
+// Each entry is decoded exactly: X = rint(2^55 Mt) = hi 2^32 + lo from its 7 digits, (double)hi 2^32 + (double)lo
+// (exact parts, one rounding); u_n = delta_n mu_j 2^-55 sum_k X_nk (delta_k w_k).  7 instead of 8.5 bytes per stored
+// entry (no fp64 tile padding).  Partials are scaled in the fixed-order reduce.
+__global__ void __launch_bounds__(256, 2) k_oz_symv1(const FacSub* __restrict__ subs, const int2* __restrict__ items,
+                                                  const int8_t* __restrict__ msl, const int* __restrict__ dexp,
+                                                  const double* __restrict__ W, int ldw, int max_ntb,
+                                                  double* __restrict__ P) {
+  pdl_wait();
+  extern __shared__ double wv[];            // ntb x 64: delta_k w_k of the block
+  __shared__ double cpart[8][64];
+  const int2 it = items[blockIdx.x];
+  const FacSub sb = subs[it.x];
+  const int I = it.y, ntb = sb.ntb;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rr = lane >> 2, h = lane & 3;   // row 8 warp + rr, columns 16 h .. 16 h + 15
+  const double* Wb = W + sb.wvu_row * (int64_t)ldw;
+  const int* dx = dexp + sb.wvu_row;
+  const int64_t gt0 = sb.wvu_row / 64;
+  for (int e = tid; e < ntb * 64; e += 256) wv[e] = ldexp(Wb[(int64_t)e * ldw], dx[e]);
+  __syncthreads();
+  const double wr = wv[I * 64 + warp * 8 + rr];   // this lane's row of w_I (column part)
+  double racc = 0.0;
+  for (int J = 0; J <= I; ++J) {
+    const int8_t* T = msl + (sb.dense_off + (int64_t)I * (I + 1) / 2 + J) * OZ_MT + (warp * 4 + h) * 128 + rr * 16;
+    uint4 q[OZ_NS];
+#pragma unroll
+    for (int i = 0; i < OZ_NS; ++i) q[i] = __ldg(reinterpret_cast<const uint4*>(T + i * 4096));
+    const double* v = wv + J * 64 + 16 * h;
+    double cval[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+      const int w32 = b >> 2, sh = 8 * (b & 3);
+      auto dig = [&](int i) {
+        const uint32_t word = w32 == 0 ? q[i].x : w32 == 1 ? q[i].y : w32 == 2 ? q[i].z : q[i].w;
+        return (int)(int8_t)(word >> sh);
+      };
+      const int hi = (dig(0) << 16) + (dig(1) << 8) + dig(2);
+      const long long lo = ((long long)dig(3) << 24) + (dig(4) << 16) + (dig(5) << 8) + dig(6);
+      const double x = fma((double)hi, 0x1p32, (double)lo);
+      racc = fma(x, v[b], racc);
+      cval[b] = x * wr;
+    }
+    if (J < I) {   // column part: sum over the tile's 64 rows (8 in this warp, then the 8 warps), fixed order
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        double t = cval[b];
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        t += __shfl_xor_sync(0xffffffffu, t, 8);
+        t += __shfl_xor_sync(0xffffffffu, t, 16);
+        cval[b] = t;
+      }
+      if (rr == 0) {
+#pragma unroll
+        for (int b = 0; b < 16; ++b) cpart[warp][16 * h + b] = cval[b];
+      }
+      __syncthreads();
+      if (tid < 64) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sum += cpart[w][tid];
+        P[((gt0 + J) * max_ntb + I) * 64 + tid] = sum;
+      }
+      __syncthreads();
+    }
+  }
+  racc += __shfl_xor_sync(0xffffffffu, racc, 1);
+  racc += __shfl_xor_sync(0xffffffffu, racc, 2);
+  if (h == 0) P[((gt0 + I) * max_ntb + I) * 64 + warp * 8 + rr] = racc;
+}
+
+__global__ void k_oz_symv_reduce(const FacSub* __restrict__ subs, const int2* __restrict__ items, int max_ntb,
+                                 const double* __restrict__ P, const int* __restrict__ dexp,
+                                 const int* __restrict__ mexp, double* __restrict__ U, int ldw) {
+  pdl_wait();
+  const int2 it = items[blockIdx.x];
+  const FacSub sb = subs[it.x];
+  const int J = it.y, ntb = sb.ntb;
+  const int64_t gt = sb.wvu_row / 64 + J;
+  const double* p = P + gt * max_ntb * 64 + threadIdx.x;
+  double sum = 0.0;
+  for (int I = J; I < ntb; ++I) sum += p[I * 64];
+  const int64_t row = sb.wvu_row + (int64_t)J * 64 + threadIdx.x;
+  U[row * ldw] = ldexp(sum, dexp[row] + mexp[it.x] - 55);
+}
 }  // namespace
 
 namespace nspk {
@@ -1077,6 +1165,17 @@ void oz_setup(const FacSub* subs, int nsub, int max_ntb, const int2* items, int 
   k_oz_mexp<<<nitems, 256, 0, st>>>(subs, items, minv, dexp, mexp);
   nsp_count_launch();
   k_oz_slice_m<<<nitems, 256, 0, st>>>(subs, items, minv, dexp, mexp, msl);
+}
+
+void oz_symv1(const FacSub* subs, const int2* items, int nitems, int max_ntb, const int8_t* msl, const int* dexp,
+              const int* mexp, const double* W, int ldw, double* U, double* P, cudaStream_t st) {
+  if (nitems <= 0) return;
+  const size_t smem = (size_t)max_ntb * 64 * sizeof(double);
+  if (smem > 48 * 1024) smem_optin((const void*)k_oz_symv1, smem);
+  nsp_count_launch();
+  launch_k(k_oz_symv1, dim3(nitems), dim3(256), smem, st, subs, items, msl, dexp, W, ldw, max_ntb, P);
+  nsp_count_launch();
+  launch_k(k_oz_symv_reduce, dim3(nitems), dim3(64), 0, st, subs, items, max_ntb, (const double*)P, dexp, mexp, U, ldw);
 }
 
 void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int s, int nch, const double* W,
