@@ -136,7 +136,7 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
     int* sexp = oz_sexp;
     auto prod = [&](const int2* its, int nit) {
       if (oz) nspk::oz_product(c->d_subs, its, nit, s, ldw / 32, U, cs, c->d_oz_dexp, c->d_oz_mexp, c->d_oz_msl,
-                               wsl, sexp, main, nullptr, 0, c->d_oz_ctr);
+                               wsl, sexp, main, nullptr, 0, c->d_oz_ctr, c->d_oz_mz);
       else nspk::symm(c->d_subs, its, nit, c->d_minv, wvu, U, ldw, cw, main, cs);
     };
     nsp_count_path(oz ? NSP_PATH_OZAKI : NSP_PATH_SYMM);
@@ -190,7 +190,7 @@ nsp_status apply_into(nsp_ctx* c, const double* X, int ldx, double* Y, int ldy, 
                        c->stream, oz_have_exp);
       mark_start();
       nspk::oz_product(c->d_subs, c->d_items, c->n_items, s, ldw / 32, U, cs, c->d_oz_dexp, c->d_oz_mexp,
-                       c->d_oz_msl, wsl, sexp, c->stream, c->d_oz_pairs, c->n_oz_pairs, c->d_oz_ctr);
+                       c->d_oz_msl, wsl, sexp, c->stream, c->d_oz_pairs, c->n_oz_pairs, c->d_oz_ctr, c->d_oz_mz);
     } else {
       nsp_count_path(NSP_PATH_SYMM);
       nspk::symm(c->d_subs, c->d_items, c->n_items, c->d_minv, wvu, U, ldw, cw, c->stream, cs);
@@ -467,6 +467,7 @@ void nsp_destroy(nsp_ctx* c) {
   fr(c->d_oz_tblk);
   fr(c->d_oz_pairs);
   fr(c->d_oz_ctr);
+  fr(c->d_oz_mz);
   fr(c->d_sell_code);
   fr(c->d_sell_tab);
   fr(c->d_items);

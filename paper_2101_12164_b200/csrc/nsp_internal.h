@@ -129,6 +129,7 @@ struct nsp_ctx {
   int2* d_oz_pairs = nullptr; // (block, even tile row I0): the two-CTA cluster work units
   int n_oz_pairs = 0;
   int* d_oz_ctr = nullptr;    // k_oz_symm's dynamic work counter (reset before every launch)
+  int8_t* d_oz_mz = nullptr;  // per stored tile: leading all-zero slices (skipped by the product)
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
   DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)
@@ -282,7 +283,7 @@ void symm(const FacSub* subs, const int2* items, int nitems, const double* minv,
 size_t oz_mslice_bytes(int64_t dense_tiles);
 size_t oz_wslice_bytes(int64_t wvu_rows, int s);
 void oz_setup(const FacSub* subs, int nsub, int max_ntb, const int2* items, int nitems, const double* minv,
-              int* dexp, int* mexp, int8_t* msl, cudaStream_t st);
+              int* dexp, int* mexp, int8_t* msl, int8_t* mz, cudaStream_t st);
 // W^T slices of every block (chunk-major W, nch chunks, s columns) -> wsl, sexp (nsub * nct * 128 ints)
 void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int s, int nch, const double* W,
                 int64_t cs, const int* dexp, int8_t* wsl, int* sexp, cudaStream_t st, bool have_exp = false);
@@ -293,7 +294,8 @@ void oz_symv1(const FacSub* subs, const int2* items, int nitems, int max_ntb, co
 // pairs (j, I0), I0 even, covering the same items: clusters of two CTAs share the W^T slices (multicast)
 void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nch, double* U, int64_t cs,
                 const int* dexp, const int* mexp, const int8_t* msl, const int8_t* wsl, const int* sexp,
-                cudaStream_t st, const int2* pairs = nullptr, int npairs = 0, int* uctr = nullptr);
+                cudaStream_t st, const int2* pairs = nullptr, int npairs = 0, int* uctr = nullptr,
+                const int8_t* mz = nullptr);
 // a2+a3 for one column (ld ldw, column 0): u_j = S_j^{-1} w_j, matrix-vector (s = 1)
 void symv(const FacSub* subs, const int2* items, int nitems, int max_ntb, const double* minv, const double* W, int ldw,
           double* U, cudaStream_t st);

@@ -214,9 +214,14 @@ __global__ void __launch_bounds__(256) k_oz_mexp(const FacSub* __restrict__ subs
 }
 
 // slices of the stored lower tiles; items = (j, I), 256 threads = 64 rows x 4 column groups of 16
+// mz[t]: the number of leading slices of stored tile t that are zero in every entry (the tile's entries are
+// small against the block scale mu_j: the far-apart boundary points of S_j^{-1}); the product skips their MMAs
+// and their bytes (bitwise the same result: the skipped digit products are exact zeros)
 __global__ void __launch_bounds__(256) k_oz_slice_m(const FacSub* __restrict__ subs, const int2* __restrict__ items,
                                                     const double* __restrict__ minv, const int* __restrict__ dexp,
-                                                    const int* __restrict__ mexp, int8_t* __restrict__ msl) {
+                                                    const int* __restrict__ mexp, int8_t* __restrict__ msl,
+                                                    int8_t* __restrict__ mz) {
+  __shared__ int zmin;
   const int2 it = items[blockIdx.x];
   const FacSub sb = subs[it.x];
   const int I = it.y, mu = mexp[it.x];
@@ -240,6 +245,14 @@ __global__ void __launch_bounds__(256) k_oz_slice_m(const FacSub* __restrict__ s
 #pragma unroll
     for (int i = 0; i < OZ_NS; ++i)
       *reinterpret_cast<uint4*>(out + i * 4096) = make_uint4(pk[i][0], pk[i][1], pk[i][2], pk[i][3]);
+    int z = 0;   // leading all-zero slices of this thread's 16 entries
+    while (z < OZ_NS - 1 && (pk[z][0] | pk[z][1] | pk[z][2] | pk[z][3]) == 0u) ++z;
+    if (threadIdx.x == 0) zmin = OZ_NS;
+    __syncthreads();
+    atomicMin(&zmin, z);
+    __syncthreads();
+    if (threadIdx.x == 0) mz[t] = (int8_t)zmin;
+    __syncthreads();
   }
 }
 
@@ -349,7 +362,7 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
                                                     const int8_t* __restrict__ wsl, const int* __restrict__ dexp,
                                                     const int* __restrict__ mexp, const int* __restrict__ sexp,
                                                     double* __restrict__ U, int64_t cs, int nch, int dbg,
-                                                    int* __restrict__ uctr) {
+                                                    int* __restrict__ uctr, const int8_t* __restrict__ mz) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ __align__(8) uint64_t full[OZ_NST], empty[OZ_NST], tfull, tempty, ufull[4], uempty[4];
   __shared__ uint32_t tbase;
@@ -420,9 +433,13 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
         OzKOrder ko(I, sb.ntb, CL == 2 || !(dbg & 8));
         for (int step = 0; step < sb.ntb; ++step, ko.next()) {
           const int K = ko.K;
+          const int64_t t = sb.dense_off + (K <= I ? (int64_t)I * (I + 1) / 2 + K : (int64_t)K * (K + 1) / 2 + I);
+          // leading zero slices are neither loaded nor multiplied (all of them on a unit's first K tile, whose
+          // products initialise the accumulators)
+          const int zt = (mz && step > 0) ? mz[t] : 0;
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* As = base + st * (OZ_AT + OZ_MT);
-          mbar_expect(&full[st], ((dbg & 1) ? 0 : OZ_AT) + ((dbg & 2) ? 0 : OZ_MT) + ((dbg & 3) == 3 ? 16 : 0));
+          mbar_expect(&full[st], ((dbg & 1) ? 0 : OZ_AT) + ((dbg & 2) ? 0 : OZ_MT - zt * 4096) + ((dbg & 3) == 3 ? 16 : 0));
           const int8_t* Ag = wsl + ((T0 + K) * nct + ct) * (int64_t)OZ_AT;
           if (CL == 2) {
             if (!(dbg & 1))
@@ -431,8 +448,8 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
             if (hint) bulk_copy_hint(As, Ag, OZ_AT, &full[st], pol);
             else bulk_copy(As, Ag, OZ_AT, &full[st]);
           }
-          const int64_t t = sb.dense_off + (K <= I ? (int64_t)I * (I + 1) / 2 + K : (int64_t)K * (K + 1) / 2 + I);
-          if (!(dbg & 2)) bulk_copy(As + OZ_AT, msl + t * OZ_MT, OZ_MT, &full[st]);
+          if (!(dbg & 2))
+            bulk_copy(As + OZ_AT + zt * 4096, msl + t * OZ_MT + zt * 4096, OZ_MT - zt * 4096, &full[st]);
           if ((dbg & 3) == 3) bulk_copy(As, wsl, 16, &full[st]);
           if (++st == OZ_NST) st = 0, ph ^= 1;
         }
@@ -464,6 +481,9 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
       OzKOrder ko(I, ntb, CL == 2 || !(dbg & 8));
       for (int step = 0; step < ntb; ++step, ko.next()) {
         const int K = ko.K;
+        const int zt = (mz && step > 0)
+                           ? mz[subs[it.x].dense_off + (K <= I ? (int64_t)I * (I + 1) / 2 + K : (int64_t)K * (K + 1) / 2 + I)]
+                           : 0;
 #ifdef NSP_OZ_PROF
         long long t1 = clock64();
 #endif
@@ -506,6 +526,7 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
                   const uint64_t db = mn ? umma_desc(b0 + j * 4096 + k * 2048, 512, 128)
                                          : umma_desc(b0 + j * 4096 + k * 256, 128, 512);
                   const uint32_t dd = tmem + (uint32_t)((i + j) * 64);
+                  if (j < zt) continue;   // a zero B slice (never on step 0)
                   if (i < OZ_TS) mma_i8_ts(dd, ta + 8 * i, db, id, (step | k | i) != 0);
                   else mma_i8(dd, umma_desc(a0 + i * 8192 + k * 256, 128, 512), db, id, (step | k | i) != 0);
                 }
@@ -1156,7 +1177,7 @@ size_t oz_wslice_bytes(int64_t wvu_rows, int s) {
 
 // setup: dexp (wvu_rows ints), mexp (nsub ints), msl (oz_mslice_bytes) from the S_j^{-1} tiles
 void oz_setup(const FacSub* subs, int nsub, int max_ntb, const int2* items, int nitems, const double* minv,
-              int* dexp, int* mexp, int8_t* msl, cudaStream_t st) {
+              int* dexp, int* mexp, int8_t* msl, int8_t* mz, cudaStream_t st) {
   if (nsub <= 0 || nitems <= 0) return;
   nsp_count_launch();
   k_oz_dexp<<<dim3(nsub, max_ntb), 64, 0, st>>>(subs, minv, dexp);
@@ -1164,7 +1185,7 @@ void oz_setup(const FacSub* subs, int nsub, int max_ntb, const int2* items, int 
   nsp_count_launch();
   k_oz_mexp<<<nitems, 256, 0, st>>>(subs, items, minv, dexp, mexp);
   nsp_count_launch();
-  k_oz_slice_m<<<nitems, 256, 0, st>>>(subs, items, minv, dexp, mexp, msl);
+  k_oz_slice_m<<<nitems, 256, 0, st>>>(subs, items, minv, dexp, mexp, msl, mz);
 }
 
 void oz_symv1(const FacSub* subs, const int2* items, int nitems, int max_ntb, const int8_t* msl, const int* dexp,
@@ -1194,7 +1215,7 @@ void oz_slice_w(const FacSub* subs, const int2* items, int nitems, int nsub, int
 
 void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nch, double* U, int64_t cs,
                 const int* dexp, const int* mexp, const int8_t* msl, const int8_t* wsl, const int* sexp,
-                cudaStream_t st, const int2* pairs, int npairs, int* uctr) {
+                cudaStream_t st, const int2* pairs, int npairs, int* uctr, const int8_t* mz) {
   if (nitems <= 0) return;
   const int nct = (s + 127) / 128;
   // diagnostics: bits 1 / 2 skip the A / B loads, 4 drops the L2 evict-last hint, 8 the symmetric K order
@@ -1222,7 +1243,7 @@ void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nc
     cfg.numAttrs = 2;
     nsp_count_launch();
     cudaLaunchKernelEx(&cfg, k_oz_symm<2>, subs, pairs, npairs, nct, msl, wsl, dexp, mexp, sexp, U, cs, nch, dbg,
-                       (int*)nullptr);
+                       (int*)nullptr, (const int8_t*)nullptr);
     return;
   }
   // NSP_OZ_KERNEL=2: the register-staged variant k_oz_symm_rs - parity-clean, measured SLOWER (cfg5 apply
@@ -1256,7 +1277,7 @@ void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nc
   if (uctr) cudaMemsetAsync(uctr + 64, 0, 64, st);
 #endif
   launch_k(k_oz_symm<1>, dim3(grid), dim3(320), (size_t)OZ_SMEM, st, subs, items, nitems, nct, msl, wsl, dexp, mexp,
-           sexp, U, cs, nch, dbg, stat ? (int*)nullptr : uctr);
+           sexp, U, cs, nch, dbg, stat ? (int*)nullptr : uctr, (dbg & 48) ? (const int8_t*)nullptr : mz);
 #ifdef NSP_OZ_PROF
   if (uctr) {
     unsigned long long h[3];

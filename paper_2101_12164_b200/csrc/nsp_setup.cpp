@@ -1359,10 +1359,20 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
           NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_oz_ctr, 1024));   // [0]: the counter; [64..69]: NSP_OZ_PROF diagnostics
           if (!pr.empty() && (st = upload(c, &c->d_oz_pairs, pr)) != NSP_OK) return st;
         }
+        NSP_CUDA_TRY(c, cudaMalloc((void**)&c->d_oz_mz, (size_t)dense_tiles));
         nspk::oz_setup(c->d_subs, c->nsub, c->max_ntb, c->d_items, c->n_items, c->d_minv, c->d_oz_dexp,
-                       c->d_oz_mexp, c->d_oz_msl, c->stream);
+                       c->d_oz_mexp, c->d_oz_msl, c->d_oz_mz, c->stream);
         NSP_CUDA_TRY(c, cudaGetLastError());
         NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        if (c->opts.verbose || getenv("NSP_VERBOSE")) {   // how many slices the product skips
+          std::vector<int8_t> hz((size_t)dense_tiles);
+          NSP_CUDA_TRY(c, cudaMemcpy(hz.data(), c->d_oz_mz, hz.size(), cudaMemcpyDeviceToHost));
+          long long cnt[8] = {0};
+          for (int8_t z : hz) cnt[z < 0 ? 0 : (z > 7 ? 7 : z)]++;
+          fprintf(stderr, "[nsp] INT8 slices: stored tiles by leading zero slices 0..6:");
+          for (int q = 0; q < 7; ++q) fprintf(stderr, " %lld", cnt[q]);
+          fprintf(stderr, "\n");
+        }
       } else if (c->opts.verbose) {
         fprintf(stderr, "nsp_setup: INT8 slices (%.1f GB) skipped: %.1f GB free, %.1f GB reserve\n", mb / 1e9,
                 fr / 1e9, reserve / 1e9);
