@@ -364,14 +364,22 @@ def measure(pr, args, ws, rank, local, stream, nccl_id, headline):
     # (output tile, K tile) pairs sum ntb^2 = 2 T_l - T_w
     t_l, t_w = st["l22_entries"] // 4096, st["wvu_rows"] // 64
     nct = (s + 127) // 128
+    oz = ctx.ozaki_stats()
+    # share of the 28 slice products per (unit, K tile) that k_oz_symm executes: the products with an all-zero
+    # leading S_j^-1 slice are skipped (exact zeros), so they are not counted as work either
+    keep = oz["slice_products_executed"] / oz["slice_products_full"] if oz["slice_products_full"] else 1.0
     out["k_symm"] = {"avg_launch_ms": sweep_ms / max(sweeps, 1), "launches": sweeps,
                      "flops_per_launch": 2.0 * st["sum_b2"] * s, "int8": int8,
-                     # INT8 path, algorithmic: 28 exact int8 slice products per fp64 multiply-add of U_j = S_j^-1 W_j
-                     # (2 s sum b_j^2 of them; the tiles' zero padding, +2.3 % at cfg5, is not counted)
-                     "int8_ops_per_launch": 28 * 2.0 * st["sum_b2"] * s,
-                     "int8_ops_executed_per_launch": 2.0 * 28 * 128 * 64 * 64 * (2 * t_l - t_w) * nct,
-                     # unique bytes: the 7 slices of every stored tile, the W^T slices, U out (fp64)
-                     "int8_alg_bytes_per_launch": 7 * 4096 * t_l + 7 * 8192 * nct * t_w + 8 * s * st["wvu_rows"],
+                     # INT8 path, algorithmic: the exact int8 slice products per fp64 multiply-add of
+                     # U_j = S_j^-1 W_j (2 s sum b_j^2 of them) - 28, times the executed share `keep` (the
+                     # leading-zero-slice skip); the tiles' zero padding, +2.3 % at cfg5, is not counted
+                     "int8_ops_per_launch": 28 * keep * 2.0 * st["sum_b2"] * s,
+                     "int8_ops_28_products_per_launch": 28 * 2.0 * st["sum_b2"] * s,
+                     "int8_products_kept": keep,
+                     "int8_ops_executed_per_launch": 2.0 * 128 * 64 * 64 * oz["slice_products_executed"] * nct,
+                     # unique bytes: the stored tiles' slices (skip applied), the W^T slices, U out (fp64)
+                     "int8_alg_bytes_per_launch": (oz["m_slice_bytes"] or 7 * 4096 * t_l) + 7 * 8192 * nct * t_w
+                     + 8 * s * st["wvu_rows"],
                      "alg_bytes_per_launch": 8 * (st["sum_b2"] + st["sum_b"]) / 2 + 2 * 8 * s * st["sum_b"]}
     # apply-only timing (a1-a5), L2 flushed
     P_ = torch.randn(nG, s, dtype=torch.float64, device=dev)
@@ -483,6 +491,8 @@ def run_ours(args, ws, rank, local):
                                "ratio of the B200 tensor core" + ("" if "bf16_tflops" in peaks else
                                                                   " (fallback: nominal 2.25 PF bf16)"),
                 "algorithmic_int8_ops_per_launch": ks["int8_ops_per_launch"],
+                "int8_products_kept": ks["int8_products_kept"],
+                "int8_ops_28_products_per_launch": ks["int8_ops_28_products_per_launch"],
                 "executed_int8_ops_per_launch": ks["int8_ops_executed_per_launch"],
                 "algorithmic_bytes_per_launch": ks["int8_alg_bytes_per_launch"],
                 "fp64_equivalent_tflops": achieved,

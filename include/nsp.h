@@ -178,6 +178,11 @@ nsp_status nsp_workspace_bytes(const nsp_ctx* ctx, int s, size_t* bytes);
  * apply (padded tiles), factor tiles, nnz(A_G), nnz(A_GI), max b_j, A_G bandwidth, sum b_j^2,
  * sum b_j, local blocks, W/V/U rows} */
 nsp_status nsp_stats(const nsp_ctx* ctx, int64_t* stats12);
+/* INT8 a2+a3 work per apply and 128-column tile (reading R10): host int64[3] = {int8 slice products
+ * (128 x 64 x 64 each) k_oz_symm executes with the leading-zero-slice skip, the same count with all 28
+ * products per (unit, K tile), unique bytes of the stored S_j^-1 tile slices it reads (skip applied)};
+ * all 0 when the INT8 slices were not built.  Host-only; NSP_ERR_ARG on NULL. */
+nsp_status nsp_ozaki_stats(const nsp_ctx* ctx, int64_t* out3);
 /* Live timing of the batched factor-sweep kernel (a2+a3): enable = 1 records a CUDA event pair
  * around every launch on the context stream; nsp_profile_read synchronises the stream and
  * returns the summed duration and launch count since the last read. */

@@ -313,6 +313,14 @@ nsp_status nsp_stats(const nsp_ctx* c, int64_t* st) {
   return NSP_OK;
 }
 
+nsp_status nsp_ozaki_stats(const nsp_ctx* c, int64_t* out) {
+  if (!c || !out) return NSP_ERR_ARG;
+  out[0] = c->d_oz_msl ? c->oz_prod_exec : 0;
+  out[1] = c->d_oz_msl ? c->oz_prod_full : 0;
+  out[2] = c->d_oz_msl ? c->oz_slice_bytes : 0;
+  return NSP_OK;
+}
+
 nsp_status nsp_workspace_bytes(const nsp_ctx* c, int s, size_t* bytes) {
   if (!c || !bytes || s <= 0) return NSP_ERR_ARG;
   *bytes = solver_ws_bytes(c, s);

@@ -130,6 +130,10 @@ struct nsp_ctx {
   int n_oz_pairs = 0;
   int* d_oz_ctr = nullptr;    // k_oz_symm's dynamic work counter (reset before every launch)
   int8_t* d_oz_mz = nullptr;  // per stored tile: leading all-zero slices (skipped by the product)
+  // int8 slice products (128 x 64 x 64 each) one column tile of an apply executes: with the leading-zero
+  // skip (natural K order, the unit's first K tile unskipped) and the full 28 per (unit, K tile)
+  int64_t oz_prod_exec = 0, oz_prod_full = 0;
+  int64_t oz_slice_bytes = 0;   // unique bytes of the stored-tile slices one column tile reads (skip applied)
   DevCSR A2G;                 // rows: W/V/U rows; cols: local Gamma
   DevCSR AGG2;                // rows: local Gamma; cols < nG: A_G, cols >= nG: -A_GI (W/V/U row + nG)
   DevCSR AGSH;                // multi-rank: shared x shared part of A_G (rows/cols relative to n_priv)

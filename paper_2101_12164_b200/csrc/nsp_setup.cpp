@@ -1364,14 +1364,31 @@ nsp_status nsp_setup_impl(nsp_ctx* c, const nsp_csr* A, const int32_t* part, int
                        c->d_oz_mexp, c->d_oz_msl, c->d_oz_mz, c->stream);
         NSP_CUDA_TRY(c, cudaGetLastError());
         NSP_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-        if (c->opts.verbose || getenv("NSP_VERBOSE")) {   // how many slices the product skips
+        {   // executed slice products per column tile (k_oz_symm's K loop: natural order, tile K = 0 unskipped,
+            // product (i, j) with i + j < 7 dropped when B slice j < mz[t]) - the bench's roofline counts these
           std::vector<int8_t> hz((size_t)dense_tiles);
           NSP_CUDA_TRY(c, cudaMemcpy(hz.data(), c->d_oz_mz, hz.size(), cudaMemcpyDeviceToHost));
+          int64_t ex = 0, full = 0, sl = 0;
+          for (const FacSub& f : c->subs)
+            for (int I = 0; I < f.ntb; ++I)
+              for (int K = 0; K < f.ntb; ++K) {
+                if (K <= I)   // unique slice bytes: a tile with J = 0 is also read whole (as a unit's first K tile)
+                  sl += 4096 * (7 - (K == 0 ? 0 : std::max(0, std::min(7, (int)hz[(size_t)(f.dense_off + (int64_t)I * (I + 1) / 2 + K)]))));
+                const int64_t t = f.dense_off + (K <= I ? (int64_t)I * (I + 1) / 2 + K : (int64_t)K * (K + 1) / 2 + I);
+                const int z = K == 0 ? 0 : std::max(0, std::min(7, (int)hz[(size_t)t]));
+                full += 28;
+                ex += 28 - (7 * z - z * (z - 1) / 2);
+              }
+          c->oz_prod_exec = ex;
+          c->oz_prod_full = full;
+          c->oz_slice_bytes = sl;
+        if (c->opts.verbose || getenv("NSP_VERBOSE")) {   // how many slices the product skips
           long long cnt[8] = {0};
           for (int8_t z : hz) cnt[z < 0 ? 0 : (z > 7 ? 7 : z)]++;
           fprintf(stderr, "[nsp] INT8 slices: stored tiles by leading zero slices 0..6:");
           for (int q = 0; q < 7; ++q) fprintf(stderr, " %lld", cnt[q]);
           fprintf(stderr, "\n");
+        }
         }
       } else if (c->opts.verbose) {
         fprintf(stderr, "nsp_setup: INT8 slices (%.1f GB) skipped: %.1f GB free, %.1f GB reserve\n", mb / 1e9,

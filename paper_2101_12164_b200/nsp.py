@@ -19,7 +19,7 @@ NSP_STATUS = {0: "NSP_OK", 1: "NSP_NOT_CONVERGED", -1: "NSP_ERR_ARG", -2: "NSP_E
               -10: "NSP_ERR_OOM"}
 
 EXPORTED = ["nsp_default_opts", "nsp_setup", "nsp_dims", "nsp_gamma_index", "nsp_workspace_bytes",
-            "nsp_stats", "nsp_schur_apply", "nsp_kgamma_apply", "nsp_block_cg", "nsp_nystrom",
+            "nsp_stats", "nsp_ozaki_stats", "nsp_schur_apply", "nsp_kgamma_apply", "nsp_block_cg", "nsp_nystrom",
             "nsp_nystrom_sigma", "nsp_precond_apply", "nsp_pcg", "nsp_last_error", "nsp_destroy",
             "nsp_gamma_apply", "nsp_kernel_launches", "nsp_profile", "nsp_profile_read", "nsp_shard_plan",
             "nsp_shard_info", "nsp_nccl_unique_id", "nsp_local_group_create", "nsp_local_group_destroy",
@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH):
     lib.nsp_gamma_index.argtypes = [P, P]
     lib.nsp_workspace_bytes.argtypes = [P, I, P]
     lib.nsp_stats.argtypes = [P, P]
+    lib.nsp_ozaki_stats.argtypes = [P, P]
     lib.nsp_schur_apply.argtypes = [P, P, P, I, P]
     lib.nsp_kgamma_apply.argtypes = [P, P, P, I, P]
     lib.nsp_block_cg.argtypes = [P, P, P, I, D, I, P, P]
@@ -306,6 +307,12 @@ class Context:
         keys = ["n_I", "n_boundary_layer", "l22_entries", "factor_tiles", "nnz_AG", "nnz_AGI", "max_b", "ag_bw",
                 "sum_b2", "sum_b", "n_sub", "wvu_rows"]
         return dict(zip(keys, [int(x) for x in out]))
+
+    def ozaki_stats(self) -> dict:
+        out = np.zeros(3, dtype=np.int64)
+        self._check(self.lib.nsp_ozaki_stats(self.ctx, out.ctypes.data))
+        return {"slice_products_executed": int(out[0]), "slice_products_full": int(out[1]),
+                "m_slice_bytes": int(out[2])}
 
     def workspace_bytes(self, s: int) -> int:
         b = C.c_size_t()

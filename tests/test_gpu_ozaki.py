@@ -144,3 +144,21 @@ def test_ozaki_register_staged_variant():
             assert r.returncode == 0, r.stderr[-2000:]
             outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("name", ["cfg2s", "cfg5s"])
+def test_ozaki_work_counts(name):
+    """nsp_ozaki_stats (the bench's INT8 roofline numerator): 28 slice products per (unit, K tile), i.e.
+    28 sum ntb_j^2 in all; the executed count (leading-zero-slice skip) is no larger and no smaller than the
+    count of units' first K tiles (never skipped); the unique slice bytes lie between those two bounds too."""
+    pr, d, S = problem(name)
+    ctx = context(pr, apply_kernel=3)
+    st = ctx.stats()
+    oz = ctx.ozaki_stats()
+    t_l, t_w = st["l22_entries"] // 4096, st["wvu_rows"] // 64
+    assert oz["slice_products_full"] == 28 * (2 * t_l - t_w)
+    assert 28 * t_w <= oz["slice_products_executed"] <= oz["slice_products_full"]
+    assert 7 * 4096 * t_w <= oz["m_slice_bytes"] <= 7 * 4096 * t_l
+    print(f"{name}: executed {oz['slice_products_executed']} of {oz['slice_products_full']} slice products, "
+          f"slice bytes {oz['m_slice_bytes']} of {7 * 4096 * t_l}")
+    ctx.close()
