@@ -437,16 +437,19 @@ __global__ void __launch_bounds__(320, 1) k_oz_symm(const FacSub* __restrict__ s
           // leading zero slices are neither loaded nor multiplied (all of them on a unit's first K tile, whose
           // products initialise the accumulators)
           const int zt = (mz && step > 0) ? mz[t] : 0;
+          // with zt zero B slices only the W^T slices i <= 6 - zt meet a product (i + j < 7, j >= zt): the
+          // rest are not loaded either (diagnostic bit 64 loads all 7)
+          const int abytes = (CL == 1 && !(dbg & 64)) ? (OZ_NS - zt) * 8192 : OZ_AT;
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* As = base + st * (OZ_AT + OZ_MT);
-          mbar_expect(&full[st], ((dbg & 1) ? 0 : OZ_AT) + ((dbg & 2) ? 0 : OZ_MT - zt * 4096) + ((dbg & 3) == 3 ? 16 : 0));
+          mbar_expect(&full[st], ((dbg & 1) ? 0 : abytes) + ((dbg & 2) ? 0 : OZ_MT - zt * 4096) + ((dbg & 3) == 3 ? 16 : 0));
           const int8_t* Ag = wsl + ((T0 + K) * nct + ct) * (int64_t)OZ_AT;
           if (CL == 2) {
             if (!(dbg & 1))
               bulk_copy_mc(As + crank * (OZ_AT / 2), Ag + crank * (OZ_AT / 2), OZ_AT / 2, &full[st], (uint16_t)3);
           } else if (!(dbg & 1)) {
-            if (hint) bulk_copy_hint(As, Ag, OZ_AT, &full[st], pol);
-            else bulk_copy(As, Ag, OZ_AT, &full[st]);
+            if (hint) bulk_copy_hint(As, Ag, abytes, &full[st], pol);
+            else bulk_copy(As, Ag, abytes, &full[st]);
           }
           if (!(dbg & 2))
             bulk_copy(As + OZ_AT + zt * 4096, msl + t * OZ_MT + zt * 4096, OZ_MT - zt * 4096, &full[st]);
@@ -1243,7 +1246,7 @@ void oz_product(const FacSub* subs, const int2* items, int nitems, int s, int nc
     cfg.numAttrs = 2;
     nsp_count_launch();
     cudaLaunchKernelEx(&cfg, k_oz_symm<2>, subs, pairs, npairs, nct, msl, wsl, dexp, mexp, sexp, U, cs, nch, dbg,
-                       (int*)nullptr, (const int8_t*)nullptr);
+                       (int*)nullptr, (dbg & 48) ? (const int8_t*)nullptr : mz);
     return;
   }
   // NSP_OZ_KERNEL=2: the register-staged variant k_oz_symm_rs - parity-clean, measured SLOWER (cfg5 apply
