@@ -408,8 +408,67 @@ def measure(pr, args, ws, rank, local, stream, nccl_id, headline):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_t = float(tt.item())
     e2e_it = sum(r["iters"] for _, r in et) / len(et)
-    out["e2e"] = {"value": s * e2e_it / (e2e_t * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nG * s * 8,
-                  "d2h_bytes_per_step": nG * s * 8}
+    e2e_serial = s * e2e_it / (e2e_t * 1e-3)
+
+    # e2e as a serving loop runs it: the same K steps back to back, double-buffered - step k + 1's Omega upload
+    # (copy stream) overlaps step k's block CG, step k's Y download (second copy stream) overlaps step k + 1;
+    # timed from the first upload's start to the last download's end (every step's copies inside the region)
+    def e2e_pipelined(nsteps):
+        Omb, Yb = [Om, torch.empty_like(Om)], [Y, torch.empty_like(Y)]
+        Yhb = [Y_h, torch.empty_like(Y_h).pin_memory()]
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        e_in = [torch.cuda.Event(), torch.cuda.Event()]
+        e_used = [torch.cuda.Event(), torch.cuda.Event()]
+        e_y = [torch.cuda.Event(), torch.cuda.Event()]
+        e_out = [torch.cuda.Event(), torch.cuda.Event()]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        t0.record(s_in)
+        with torch.cuda.stream(s_in):
+            Omb[0].copy_(Om_h, non_blocking=True)
+        e_in[0].record(s_in)
+        its = []
+        for k in range(nsteps):
+            b = k % 2
+            stream.wait_event(e_in[b])
+            if k >= 2:
+                stream.wait_event(e_out[b])          # Y[b] downloaded before step k overwrites it
+            ctx.kgamma_apply(Omb[b], Bm, wsbuf)
+            e_used[b].record(stream)
+            if k + 1 < nsteps:
+                nb = 1 - b
+                if k >= 1:
+                    s_in.wait_event(e_used[nb])      # Omega[nb] consumed by step k - 1
+                with torch.cuda.stream(s_in):
+                    Omb[nb].copy_(Om_h, non_blocking=True)
+                e_in[nb].record(s_in)
+            r = ctx.block_cg(Bm, X, pr.tol_bcg, maxit, wsbuf)
+            ctx.gamma_apply(X, Yb[b])
+            e_y[b].record(stream)
+            s_out.wait_event(e_y[b])
+            with torch.cuda.stream(s_out):
+                Yhb[b].copy_(Yb[b], non_blocking=True)
+            e_out[b].record(s_out)
+            its.append(r["iters"])
+        t1.record(s_out)
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1), sum(its)
+    e2e_pipelined(2)                                  # warm-up (second Y / Omega buffers, streams)
+    tp, itp = e2e_pipelined(max(2, args.steps))
+    if ws > 1:
+        tt = torch.tensor([tp], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        tp = float(tt.item())
+    out["e2e"] = {"value": s * itp / (tp * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nG * s * 8,
+                  "d2h_bytes_per_step": nG * s * 8,
+                  "mode": "K steps back to back through the public API, double-buffered: step k+1's Omega upload "
+                          "and step k's Y download (pinned host memory, two copy streams) overlap the compute; "
+                          "timed from the first upload's start to the last download's end",
+                  "serial_value": e2e_serial,
+                  "serial_mode": "each step alone: upload, step, download, synchronize (L2 flushed between steps)"}
     if single and not args.no_analog:
         # the paper-analog block-CG preconditioner M = A_G^-1 (reading C2), same context
         ctx.set_bcg_precond(1)
