@@ -165,6 +165,12 @@ nsp_status nsp_shard_info(const nsp_ctx* ctx, int64_t* n_private, int64_t* n_sha
 /* 128-byte ncclUniqueId for opts.nccl_id (call on one rank, broadcast to all); NSP_ERR_NCCL if
  * libnccl.so.2 cannot be loaded. */
 nsp_status nsp_nccl_unique_id(void* out128);
+/* The NCCL branch's call sequence (dlopen of libnccl.so.2, ncclGetUniqueId, ncclCommInitRank, in-place
+ * ncclAllReduce(ncclDouble, ncclSum) on a stream, ncclCommDestroy) on a ONE-rank communicator on `device`:
+ * count (> 0) fp64 values go through the allreduce and must come back unchanged; *max_abs_err (HOST pointer)
+ * receives the largest deviation (0 expected).  SURVEY.md 8(e): a one-GPU box cannot run two ranks, this is
+ * the hardware check of the production collective.  NSP_ERR_NCCL if NCCL cannot be loaded or a call fails. */
+nsp_status nsp_nccl_selftest(int device, size_t count, double* max_abs_err);
 /* Testing the sharded path on one device: a group for nranks (<= 16) host threads; each thread sets
  * opts.local_group, opts.nranks, opts.rank and calls nsp_setup / the solvers concurrently.  The
  * allreduce is then two host barriers around a rank-ordered device sum (no kernel waits on another

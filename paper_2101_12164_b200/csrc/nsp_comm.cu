@@ -15,7 +15,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -121,6 +123,44 @@ extern "C" nsp_status nsp_nccl_unique_id(void* out128) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
   std::memcpy(out128, &id, 128);
   return NSP_OK;
+}
+
+// The production collective's exact call sequence (dlopen, ncclGetUniqueId, ncclCommInitRank, in-place
+// ncclAllReduce(ncclDouble, ncclSum) on a stream, ncclCommDestroy) on a ONE-rank communicator: the sum over
+// one rank is the identity, so the buffer must come back bitwise unchanged.  The pool has a single GPU, so
+// this is how the NCCL branch of comm_init / comm_allreduce is exercised on hardware.
+extern "C" nsp_status nsp_nccl_selftest(int device, size_t count, double* max_abs_err) {
+  if (count == 0 || !max_abs_err) return NSP_ERR_ARG;
+  *max_abs_err = -1.0;
+  NcclApi& a = nccl();
+  if (!a.loaded) return NSP_ERR_NCCL;
+  if (cudaSetDevice(device) != cudaSuccess) return NSP_ERR_CUDA;
+  std::vector<double> h(count), g(count);
+  for (size_t i = 0; i < count; ++i) h[i] = 1.0 / (double)(i + 3) - 0.25 * (double)(i % 7);
+  double* d = nullptr;
+  cudaStream_t st = nullptr;
+  ncclComm_t nc = nullptr;
+  nsp_status ret = NSP_OK;
+  ncclUniqueId id;
+  if (cudaMalloc(&d, count * 8) != cudaSuccess || cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    ret = NSP_ERR_CUDA;
+  } else if (a.GetUniqueId(&id) != ncclSuccess || a.CommInitRank(&nc, 1, id, 0) != ncclSuccess) {
+    ret = NSP_ERR_NCCL;
+  } else {
+    cudaMemcpyAsync(d, h.data(), count * 8, cudaMemcpyHostToDevice, st);
+    if (a.AllReduce(d, d, count, ncclDouble, ncclSum, nc, st) != ncclSuccess) ret = NSP_ERR_NCCL;
+    cudaMemcpyAsync(g.data(), d, count * 8, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) ret = NSP_ERR_CUDA;
+    if (ret == NSP_OK) {
+      double m = 0.0;
+      for (size_t i = 0; i < count; ++i) m = std::max(m, std::fabs(g[i] - h[i]));
+      *max_abs_err = m;
+    }
+  }
+  if (nc) a.CommDestroy(nc);
+  if (st) cudaStreamDestroy(st);
+  if (d) cudaFree(d);
+  return ret;
 }
 
 extern "C" void* nsp_local_group_create(int nranks) {

@@ -22,7 +22,7 @@ EXPORTED = ["nsp_default_opts", "nsp_setup", "nsp_dims", "nsp_gamma_index", "nsp
             "nsp_stats", "nsp_ozaki_stats", "nsp_schur_apply", "nsp_kgamma_apply", "nsp_block_cg", "nsp_nystrom",
             "nsp_nystrom_sigma", "nsp_precond_apply", "nsp_pcg", "nsp_last_error", "nsp_destroy",
             "nsp_gamma_apply", "nsp_kernel_launches", "nsp_profile", "nsp_profile_read", "nsp_shard_plan",
-            "nsp_shard_info", "nsp_nccl_unique_id", "nsp_local_group_create", "nsp_local_group_destroy",
+            "nsp_shard_info", "nsp_nccl_unique_id", "nsp_nccl_selftest", "nsp_local_group_create", "nsp_local_group_destroy",
             "nsp_set_bcg_precond", "nsp_path_counters", "nsp_dev_panel", "nsp_dev_gram", "nsp_dev_panel_gram",
             "nsp_dev_philox_gaussian", "nsp_dev_set_fused_pg"]
 
@@ -92,6 +92,7 @@ def load_library(path: str = LIB_PATH):
     lib.nsp_shard_plan.argtypes = [P, P, I, I, I, P, P, P, P, P]
     lib.nsp_shard_info.argtypes = [P, P, P, P, P]
     lib.nsp_nccl_unique_id.argtypes = [P]
+    lib.nsp_nccl_selftest.argtypes = [I, C.c_size_t, P]
     lib.nsp_local_group_create.argtypes = [I]
     lib.nsp_local_group_create.restype = C.c_void_p
     lib.nsp_local_group_destroy.argtypes = [P]
@@ -222,6 +223,15 @@ def nccl_unique_id() -> bytes:
     if st != 0:
         raise NspError(st, "nsp_nccl_unique_id: libnccl.so.2 not loadable")
     return buf.raw
+
+
+def nccl_selftest(device: int = 0, count: int = 1 << 20) -> float:
+    """One-rank NCCL communicator: allreduce `count` fp64 values in place; returns the largest deviation."""
+    err = C.c_double(-1.0)
+    st = load_library().nsp_nccl_selftest(int(device), int(count), C.byref(err))
+    if st != 0:
+        raise NspError(st, "nsp_nccl_selftest")
+    return err.value
 
 
 class LocalGroup:

@@ -201,3 +201,13 @@ def test_multirank_nystrom_pcg_matches_single_rank(name, G):
     assert np.linalg.norm(b - A @ res[0]["x"]) / np.linalg.norm(b) <= 1e-7
     print(f"{name} G={G}: bcg(M=A_G^-1) {repm1['iters']} its, Nystrom {rn1['iters']} inner its, "
           f"PCG {rp1['iters']} / {res[0]['rp']['iters']} its, x vs 1 rank {relfro(res[0]['x'], x1):.1e}")
+
+
+@pytest.mark.parametrize("count", [1, 2 * 128 * 128, (1 << 20) + 3])
+def test_nccl_branch_one_rank_communicator(count):
+    """The production collective's call sequence (dlopen libnccl.so.2, ncclGetUniqueId, ncclCommInitRank,
+    in-place ncclAllReduce(ncclDouble, ncclSum) on a stream, ncclCommDestroy) on the B200 with a ONE-rank
+    communicator - what a one-GPU pool can run of the NCCL branch of nsp_comm.cu.  The sum over one rank is
+    the identity: bit-exact.  Sizes: a scalar (the PCG dots), the [D|E] Gram pair at s = 128, a ragged block."""
+    assert nsp.nccl_selftest(0, count) == 0.0
+    assert len(nsp.nccl_unique_id()) == 128
